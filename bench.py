@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark of the SAGIPS hot path on B200 (events/s per GPU and train_step
+time at 1/2/4/8 GPUs, BASELINE.json `metric`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1)
+
+A step is one full `sagips_train_step` (a1-a13 of SURVEY 8(a)): noise ->
+generator -> constrain -> sampler -> bootstrap -> D step + Adam(D) -> G loss
+through the updated D -> sampler backward -> generator backward -> ring
+exchange -> Adam(G).  Workload at N = 1: C2 (BASELINE.json configs[1]):
+paper-size MLPs, k = m = 1024 (2^20 synthetic events per rank), fp32.  For
+N > 1: C3, the same per rank (weak scaling) with the one-sided ring over all
+ranks.  Inputs are synthetic and generated on the device from the counter-
+based RNG.  Rank 0 prints one JSON line.
+"""
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "events/sec/GPU and train_step time at 1/2/4/8 B200 (weak-scaling efficiency)"
+SM_COUNT = 148
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=["c2", "c1", "c5"], default="c2")
+    p.add_argument("--mode", choices=["rma", "arar", "arar-arar", "sync", "none"], default="rma")
+    p.add_argument("--group-size", type=int, default=0)
+    p.add_argument("--staleness", type=int, default=1)
+    p.add_argument("--outer-every", type=int, default=1000)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- configs
+def lib_config(args, L, rank, world):
+    if args.config == "c1":
+        cfg = L.config_init(L.PRESET_DESK)
+        workload = "C1: 1 rank desk MLPs G[8,64,64,6] D[2,64,64,1], k=64 m=16 (1024 events/step), fp32"
+    else:
+        cfg = L.config_init(L.PRESET_PAPER)
+        workload = ("C2: paper MLPs G[6,128x4,6] D[2,128x4,1] (51,206/50,049 params), k=1024 m=1024 "
+                    "(2^20 events/rank/step), fp32")
+        if args.config == "c5":
+            cfg.events_per_sample = 16384
+            cfg.reference_rows = 2 * 1024 * 16384
+            cfg.shard_rows = 1024 * 16384
+            cfg.precision = L.PREC_BF16
+            workload = "C5: paper MLPs, k=1024 m=16384 (2^24 events/rank/step), bf16 D GEMMs"
+    cfg.world, cfg.rank = world, rank
+    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
+             "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
+    cfg.mode = modes[args.mode] if world > 1 else L.MODE_NONE
+    cfg.group_size = args.group_size if (args.group_size and world > 1) else world
+    cfg.outer_every = args.outer_every
+    cfg.staleness = args.staleness if world > 1 else 0
+    cfg.phase_timing = 1
+    if world > 1:
+        workload = workload.replace("C2:", "C3:") + f", {args.mode} ring g={cfg.group_size} s={cfg.staleness}"
+    return cfg, workload
+
+
+def disc_flops_per_event(cfg):
+    """8 F per synthetic event: D step = 6F per event pair
+    (fwd + bwd on 2N rows), G step = 2F; F = 2 * sum(in*out) of D."""
+    sizes = [2] + [cfg.disc_hidden] * cfg.disc_depth + [1]
+    F = 2 * sum(sizes[i] * sizes[i + 1] for i in range(len(sizes) - 1))
+    return 8 * F
+
+
+# ---------------------------------------------------------------- oracle (CPU)
+def run_oracle_sample(steps, seconds_cap=30.0):
+    """The oracle, as it stands, on a bounded sample of the C2 workload:
+    paper-size MLPs with k = 16 parameter samples x m = 1024 events
+    (2^14 events) per step, BLAS limited to one thread."""
+    from threadpoolctl import threadpool_limits
+    from oracle import gan
+    cfg = gan.paper_config(param_samples=16, events_per_sample=1024, reference_rows=2 * 16384, shard_rows=16384)
+    with threadpool_limits(limits=1):
+        st = gan.RankState(cfg, 0)
+        t0 = time.perf_counter()
+        done = 0
+        for t in range(steps):
+            o = gan.local_step(cfg, st, t)
+            gan.apply_generator(cfg, st, o["packet"], o["db_g"])
+            done += 1
+            if time.perf_counter() - t0 > seconds_cap:
+                break
+        dt = time.perf_counter() - t0
+    ev = cfg.n_events * done
+    return {"value": ev / dt, "unit": "events/s", "cores": 1, "kind": "oracle",
+            "sample": f"{done} oracle steps of C2 at k=16 m=1024 (2^14 events/step, paper-size MLPs), 1 BLAS thread, "
+                      f"{dt:.1f} s"}, dt / done
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    steps = max(1, args.steps)
+    for _ in range(min(args.warmup, 1)):
+        run_oracle_sample(1, seconds_cap=5.0)
+    cb, sec_per_step = run_oracle_sample(steps, seconds_cap=120.0)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "events/s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (counter-based Philox, DESIGN.md input recipe)",
+            "config": {"workload": "C2 sample: paper MLPs, k=16 m=1024 per step (oracle, CPU)"},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- ours
+def ours_arm(args):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2407_00051_b200 import _lib as L
+    from paper_2407_00051_b200 import runtime
+    cfg, workload = lib_config(args, L, rank, world)
+    ctx = runtime.make_context(cfg)
+    if world > 1:
+        runtime.connect(ctx)
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    N = cfg.param_samples * cfg.events_per_sample
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    step = 0
+    for _ in range(args.warmup):
+        ctx.train_step(step, 0, sp)
+        step += 1
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ctx.train_step(step, 0, sp)
+        step += 1
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - n0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    phases, nph = ctx.phase_times()
+    stats = ctx.get(L.T_STATS)
+    value = world * N / (ms * 1e-3)
+
+    # e2e: the user-level loop through the public API with a per-step
+    # device->host read of the step's result (the stats record)
+    e2e = None
+    if not args.no_e2e:
+        steps_e2e = max(3, args.steps // 2)
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            ctx.train_step(step, 0, sp)
+            step += 1
+            ctx.get(L.T_STATS)  # synchronising D2H copy of the 64-byte record
+        t1 = time.perf_counter()
+        e2e_ms = (t1 - t0) * 1e3 / steps_e2e
+        if dist is not None:
+            t = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": world * N / (e2e_ms * 1e-3), "unit": "events/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": 64, "ms_per_step": e2e_ms,
+               "note": "inputs are drawn on the device by the counter-based RNG and the reference shard is "
+                       "resident (P:144); per step the host issues the call and reads back the stats record"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+
+    peaks, peak_src = load_peaks()
+    disc_ms = phases["disc_step"] + phases["gen_loss_through_disc"]
+    disc_flops = disc_flops_per_event(cfg) * N
+    if cfg.precision == L.PREC_BF16:
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak_src": f"{peak_src} bf16 sustained"}
+    else:
+        # FP32 FFMA on CUDA cores: 148 SMs x 128 lanes x 2 flop x max SM clock
+        peak = SM_COUNT * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        roof = {"bound": "alu", "unit": "TFLOP/s",
+                "peak_src": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md unit counts)"}
+    achieved = disc_flops / (disc_ms * 1e-3) / 1e12
+    roof.update({"kernel": "discriminator MLP (a7+a8: D step fwd/bwd on 2N rows + G-step fwd/bwd on N rows)",
+                 "achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
+                 "algorithmic": f"8F = {disc_flops_per_event(cfg)} FLOP/event x {N} events"})
+    samp_ms = phases["sampler"]
+    samp_bytes = 16 * N + 4 * N  # fake + real rows written (8 B + 8 B) + 4 B real index
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    roof_sampler = {"bound": "hbm", "kernel": "k_sample (a4-a6)", "achieved": samp_bytes / (samp_ms * 1e-3) / 1e9,
+                    "peak": hbm, "unit": "GB/s", "frac": samp_bytes / (samp_ms * 1e-3) / 1e9 / hbm,
+                    "algorithmic": "20 B/event written (fake 8 + real 8 + index 4)"}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu, _ = run_oracle_sample(50, seconds_cap=20.0)
+        except Exception as e:  # the oracle is optional on the box
+            cpu = {"error": str(e)}
+    line = {"metric": METRIC, "value": value, "unit": "events/s (all GPUs)", "per_gpu": value / world,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if cfg.precision == L.PREC_BF16 else "f32",
+            "data": "synthetic: loop-closure reference from p* and counter-based Philox draws (DESIGN.md)",
+            "config": {"workload": workload, "events_per_rank_per_step": N, "global_events_per_step": N * world,
+                       "l2": "step working set (D activations ~4 GB at C2) exceeds the 126 MB L2",
+                       "mode": args.mode if world > 1 else "none"},
+            "clocks": clk, "gpu_launches": launches, "phases_ms": phases, "phase_steps_averaged": nph,
+            "roofline": roof, "roofline_sampler": roof_sampler, "cpu_baseline": cpu, "e2e": e2e,
+            "loss_d": stats.loss_d, "loss_g": stats.loss_g}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

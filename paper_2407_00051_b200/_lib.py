@@ -1,0 +1,227 @@
+"""ctypes binding of libsagips.so (include/sagips.h).  Argument marshalling
+only: every step of the hot path runs in the library's CUDA kernels.  There
+is no fallback -- importing this module fails loudly if the shared library
+is missing or was built for another ABI."""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsagips.so")
+
+OK = 0
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "CUDA", 4: "NONFINITE", 5: "PROTOCOL",
+          6: "STATE", 7: "TIMEOUT", 8: "UNSUPPORTED"}
+
+MODE_NONE, MODE_ARAR, MODE_ARAR_ARAR, MODE_RMA_ARAR_ARAR, MODE_SYNC_ALLREDUCE = range(5)
+PREC_FP32, PREC_BF16 = 0, 1
+PRESET_DESK, PRESET_PAPER = 0, 1
+STEP_LOCAL_ONLY, STEP_NO_ADAM_G = 1, 2
+IPC_HANDLE_BYTES = 64
+NCCL_ID_BYTES = 128
+
+(T_GEN_W, T_GEN_B, T_DISC_W, T_DISC_B, T_GEN_ADAM, T_DISC_ADAM, T_NOISE, T_RAW, T_C, T_EVENTS,
+ T_REAL_IDX, T_HIST, T_LOGITS_D, T_LOGITS_G, T_DY, T_DRAW, T_GEN_DW, T_GEN_DB, T_DISC_DW,
+ T_DISC_DB, T_REDUCED, T_STATS, T_REFERENCE, T_SHARD) = range(24)
+
+_UINT32_TENSORS = {T_REAL_IDX, T_HIST}
+
+
+class SagipsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"sagips: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("group_size", ctypes.c_int32),
+        ("outer_every", ctypes.c_int32), ("mode", ctypes.c_int32), ("staleness", ctypes.c_int32),
+        ("reduce_mean", ctypes.c_int32), ("precision", ctypes.c_int32),
+        ("noise_dim", ctypes.c_int32), ("gen_hidden", ctypes.c_int32), ("gen_depth", ctypes.c_int32),
+        ("disc_hidden", ctypes.c_int32), ("disc_depth", ctypes.c_int32),
+        ("param_samples", ctypes.c_int32), ("events_per_sample", ctypes.c_int32),
+        ("reference_rows", ctypes.c_int64), ("shard_rows", ctypes.c_int64),
+        ("gen_lr", ctypes.c_float), ("disc_lr", ctypes.c_float), ("leaky_slope", ctypes.c_float),
+        ("adam_beta1", ctypes.c_float), ("adam_beta2", ctypes.c_float), ("adam_eps", ctypes.c_float),
+        ("true_params", ctypes.c_float * 6),
+        ("hist_bins", ctypes.c_int32), ("hist_lo", ctypes.c_float * 2), ("hist_hi", ctypes.c_float * 2),
+        ("seed", ctypes.c_uint64),
+        ("exchange_timeout_ms", ctypes.c_int32), ("phase_timing", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 6),
+    ]
+
+
+class StepStats(ctypes.Structure):
+    _fields_ = [("loss_d", ctypes.c_float), ("loss_g", ctypes.c_float), ("step", ctypes.c_uint64),
+                ("outer_fired", ctypes.c_uint32), ("nonfinite", ctypes.c_uint32),
+                ("wait_ns", ctypes.c_uint64), ("reserved", ctypes.c_uint64 * 4)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libsagips.so not built ({LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, sz, st = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    P = ctypes.POINTER
+    sig = {
+        "sagips_abi_version": ([], ctypes.c_int32),
+        "sagips_config_init": ([P(Config), ctypes.c_int32], st),
+        "sagips_workspace_size": ([P(Config), P(ctypes.c_size_t)], st),
+        "sagips_create": ([P(Config), vp, sz, vp, P(vp)], st),
+        "sagips_destroy": ([vp], st),
+        "sagips_last_error": ([vp], ctypes.c_char_p),
+        "sagips_sample_events": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
+                                  ctypes.c_uint32, ctypes.c_uint32, vp, vp, ctypes.c_int32, vp, vp, vp], st),
+        "sagips_train_step": ([vp, ctypes.c_uint64, ctypes.c_uint32, vp], st),
+        "sagips_push_generator_grad": ([vp, ctypes.c_uint64, vp], st),
+        "sagips_pull_generator_grad": ([vp, ctypes.c_uint64, vp], st),
+        "sagips_tensor_bytes": ([vp, ctypes.c_int32, P(ctypes.c_size_t)], st),
+        "sagips_get": ([vp, ctypes.c_int32, vp, sz], st),
+        "sagips_set": ([vp, ctypes.c_int32, vp, sz], st),
+        "sagips_ipc_handle": ([vp, vp, sz], st),
+        "sagips_connect_peers": ([vp, vp, sz], st),
+        "sagips_nccl_unique_id": ([vp, sz], st),
+        "sagips_connect_nccl": ([vp, vp, sz], st),
+        "sagips_launch_count": ([vp, P(ctypes.c_uint64)], st),
+        "sagips_phase_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    if lib.sagips_abi_version() != 1:
+        raise ImportError("libsagips.so ABI mismatch")
+    return lib
+
+
+lib = _load()
+EXPORTED = [
+    "sagips_abi_version", "sagips_config_init", "sagips_workspace_size", "sagips_create", "sagips_destroy",
+    "sagips_last_error", "sagips_sample_events", "sagips_train_step", "sagips_push_generator_grad",
+    "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
+    "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
+    "sagips_phase_times"]
+NUM_PHASES = 7
+PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
+
+
+def _check(status, ctx=None):
+    if status != OK:
+        msg = lib.sagips_last_error(ctx).decode() if ctx else ""
+        raise SagipsError(status, msg)
+
+
+def config_init(preset=PRESET_DESK, **overrides):
+    cfg = Config()
+    _check(lib.sagips_config_init(ctypes.byref(cfg), preset))
+    for k, v in overrides.items():
+        if k in ("true_params", "hist_lo", "hist_hi"):
+            arr = getattr(cfg, k)
+            for i, x in enumerate(v):
+                arr[i] = x
+        else:
+            setattr(cfg, k, v)
+    return cfg
+
+
+def workspace_size(cfg):
+    n = ctypes.c_size_t()
+    _check(lib.sagips_workspace_size(ctypes.byref(cfg), ctypes.byref(n)))
+    return n.value
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(lib.sagips_nccl_unique_id(buf, NCCL_ID_BYTES))
+    return buf.raw
+
+
+def sample_events(c_ptr, k, m, seed, step, rank, stream_id, events_ptr, hist_ptr=None, bins=0,
+                  lo=(0.0, 0.0), hi=(4.0, 4.0), stream=None):
+    """Device pointers in, device pointers out (see sagips.h)."""
+    lo_a = (ctypes.c_float * 2)(*lo)
+    hi_a = (ctypes.c_float * 2)(*hi)
+    _check(lib.sagips_sample_events(c_ptr, k, m, seed, step, rank, stream_id, events_ptr, hist_ptr, bins,
+                                    ctypes.cast(lo_a, ctypes.c_void_p), ctypes.cast(hi_a, ctypes.c_void_p), stream))
+
+
+class Context:
+    """One rank.  `workspace_ptr` is a device allocation of at least
+    workspace_size(cfg) bytes owned by the caller (e.g. a torch uint8 tensor
+    kept alive in `self.keepalive`)."""
+
+    def __init__(self, cfg, workspace_ptr, workspace_bytes, stream=None, keepalive=None):
+        self.cfg = cfg
+        self.keepalive = keepalive
+        h = ctypes.c_void_p()
+        st = lib.sagips_create(ctypes.byref(cfg), workspace_ptr, workspace_bytes, stream, ctypes.byref(h))
+        if st != OK:
+            raise SagipsError(st, "sagips_create failed")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib.sagips_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def train_step(self, step, flags=0, stream=None):
+        _check(lib.sagips_train_step(self.h, step, flags, stream), self.h)
+
+    def push_generator_grad(self, step, stream=None):
+        _check(lib.sagips_push_generator_grad(self.h, step, stream), self.h)
+
+    def pull_generator_grad(self, step, stream=None):
+        _check(lib.sagips_pull_generator_grad(self.h, step, stream), self.h)
+
+    def tensor_bytes(self, which):
+        n = ctypes.c_size_t()
+        _check(lib.sagips_tensor_bytes(self.h, which, ctypes.byref(n)), self.h)
+        return n.value
+
+    def get(self, which):
+        n = self.tensor_bytes(which)
+        if which == T_STATS:
+            s = StepStats()
+            _check(lib.sagips_get(self.h, which, ctypes.byref(s), n), self.h)
+            return s
+        dt = np.uint32 if which in _UINT32_TENSORS else np.float32
+        out = np.empty(n // 4, dtype=dt)
+        _check(lib.sagips_get(self.h, which, out.ctypes.data, n), self.h)
+        return out
+
+    def set(self, which, arr):
+        dt = np.uint32 if which in _UINT32_TENSORS else np.float32
+        a = np.ascontiguousarray(arr, dtype=dt).reshape(-1)
+        _check(lib.sagips_set(self.h, which, a.ctypes.data, a.nbytes), self.h)
+
+    def ipc_handle(self):
+        buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(lib.sagips_ipc_handle(self.h, buf, IPC_HANDLE_BYTES), self.h)
+        return buf.raw
+
+    def connect_peers(self, handles):
+        blob = b"".join(handles)
+        _check(lib.sagips_connect_peers(self.h, blob, len(blob)), self.h)
+
+    def connect_nccl(self, uid):
+        _check(lib.sagips_connect_nccl(self.h, uid, len(uid)), self.h)
+
+    def phase_times(self):
+        """Mean per-phase device milliseconds over the recent timed steps."""
+        arr = (ctypes.c_float * NUM_PHASES)()
+        n = ctypes.c_int32()
+        _check(lib.sagips_phase_times(self.h, arr, NUM_PHASES, ctypes.byref(n)), self.h)
+        return dict(zip(PHASES, list(arr))), n.value
+
+    def launch_count(self):
+        n = ctypes.c_uint64()
+        _check(lib.sagips_launch_count(self.h, ctypes.byref(n)), self.h)
+        return n.value

@@ -1,0 +1,95 @@
+// ctx.h -- the rank context (host struct) behind the opaque sagips_ctx.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/sagips.h"
+#include "internal.h"
+
+namespace sagips {
+
+struct MlpLayout {
+  int L = 0;                    // linear layers
+  int sizes[kMaxLayers + 1] = {};
+  int64_t w_off[kMaxLayers] = {}, b_off[kMaxLayers] = {};
+  int64_t nw = 0, nb = 0;       // weights / biases
+  int maxw = 0;                 // widest layer
+  void build(int in, int hidden, int depth, int out);
+};
+
+struct ExchangeState;  // exchange.cu
+struct TcState;        // k_disc_tc.cu
+
+}  // namespace sagips
+
+struct sagips_ctx {
+  sagips_config cfg{};
+  int dev = 0;
+  std::string err;
+  sagips::MlpLayout G, D;
+  int64_t N = 0;
+  size_t ws_bytes = 0;
+  uint64_t launch_base = 0;
+  // parameters and Adam state (fp32 masters)
+  float *gW = nullptr, *gB = nullptr, *gmW = nullptr, *gvW = nullptr, *gmB = nullptr, *gvB = nullptr;
+  float *dW = nullptr, *dB = nullptr, *dmW = nullptr, *dvW = nullptr, *dmB = nullptr, *dvB = nullptr;
+  // gradients; g_dW is the weights-only packet
+  float *g_dW = nullptr, *g_dB = nullptr, *d_dW = nullptr, *d_dB = nullptr, *reduced = nullptr;
+  // data
+  float *ref = nullptr, *shard = nullptr;
+  // generator activations
+  float* noise = nullptr;
+  float* gAct[sagips::kMaxLayers] = {};
+  float* gdZ[2] = {};
+  float *cbuf = nullptr, *draw = nullptr;
+  // discriminator input/activations (fp32 path)
+  float* X = nullptr;
+  uint32_t* real_idx = nullptr;
+  float* dAct[sagips::kMaxLayers] = {};
+  float* dZb[2] = {};
+  float *logits_d = nullptr, *logits_g = nullptr, *dy = nullptr;
+  uint32_t* hist = nullptr;
+  float* part = nullptr;
+  int64_t part_floats = 0;
+  float* colpart = nullptr;
+  float* head_tmp = nullptr;
+  double* loss_part = nullptr;
+  sagips_step_stats* stats = nullptr;
+  // step bookkeeping
+  int64_t g_tau = 0, d_tau = 0;
+  bool have_step = false;
+  uint64_t last_step = 0;
+  uint64_t local_done_step = ~0ull;
+  bool pushed = false;
+  bool skip_adam_once = false;
+  sagips::ExchangeState* xs = nullptr;
+  sagips::TcState* tc = nullptr;
+  // phase timing: events at the SAGIPS_NUM_PHASES+1 boundaries of the
+  // last 64 steps (cfg.phase_timing)
+  static constexpr int kTimingRing = 64;
+  cudaEvent_t pev[kTimingRing][SAGIPS_NUM_PHASES + 1] = {};
+  int64_t timed_steps = 0;
+  int pslot = 0;
+};
+
+namespace sagips {
+inline void mark(sagips_ctx* c, int boundary, cudaStream_t st) {
+  if (c->cfg.phase_timing) cudaEventRecord(c->pev[c->pslot][boundary], st);
+}
+}  // namespace sagips
+
+namespace sagips {
+void adam_gen(sagips_ctx* c, cudaStream_t st);
+// exchange.cu
+sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st);
+sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st);
+sagips_status exchange_check(sagips_ctx* c);
+void exchange_destroy(sagips_ctx* c);
+// k_disc_tc.cu (bf16 tcgen05 discriminator)
+bool tc_disc_supported(const sagips_config* cfg);
+sagips_status tc_disc_init(sagips_ctx* c);
+void tc_disc_destroy(sagips_ctx* c);
+void tc_disc_step(sagips_ctx* c, cudaStream_t st);
+void tc_gen_loss(sagips_ctx* c, cudaStream_t st);
+}  // namespace sagips

@@ -1,0 +1,487 @@
+// exchange.cu -- the asynchronous ring exchange of generator weight
+// gradients between GPUs, B200-native:
+//
+//  * one-sided ring (RMA-ARAR): every rank owns a window of
+//    version-indexed packet slots in its HBM, cudaMalloc'ed here and mapped
+//    into every peer over NVLink/NVSwitch by CUDA IPC.  push(t) stores the
+//    packet straight into the successor's slot and publishes it with a
+//    release store of the tag t+1 (the writer never waits); a
+//    forwarding agent on a high-priority side stream passes the packets of
+//    the other origins along the ring as they land (Alg. 1, R10);
+//    pull(t) waits (bounded, acquire loads) for the packets it needs and
+//    folds them in ascending origin order.
+//  * two-sided ring (ARAR): the same pass-along schedule with
+//    ncclSend/ncclRecv on the side stream.
+//  * outer leaders' ring every h steps (R13): NCCL send/recv
+//    among the first rank of each inner group.
+//  * SYNC_ALLREDUCE: ncclAllReduce (the synchronous baseline).
+//  * staleness s (R12): pull(t) folds the own packet of step t with the
+//    others' packets of step t-s, so with s = 1 the ring of step t runs on
+//    the side stream while step t+1 computes.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <nccl.h>
+
+#include "ctx.h"
+
+namespace sagips {
+
+constexpr int kVersions = 4;  // slot depth: >= 2 + 2s (exchange)
+enum { RING_INNER = 0 };
+
+struct DevFlags {
+  unsigned long long tag[kMaxWorld][kVersions];
+};
+
+struct ExchangeState {
+  int pos = 0, g = 1;            // position in the inner group, group size
+  int first = 0;                 // first rank of the inner group
+  int succ = 0, pred = 0;        // ring neighbours (global ranks)
+  // one-sided window: slots[origin][version][Pw] fp32 + flags
+  float* win = nullptr;          // own window (cudaMalloc, IPC-exported)
+  DevFlags* flags = nullptr;     // own flags (inside the same allocation)
+  size_t win_bytes = 0;
+  cudaIpcMemHandle_t handle{};
+  bool have_handle = false;
+  char* peer_base[kMaxWorld] = {};
+  bool peers_ok = false;
+  // two-sided / outer / sync
+  ncclComm_t comm_ring = nullptr;   // side-stream ring
+  ncclComm_t comm_main = nullptr;   // outer ring and all-reduce (main stream)
+  float* gather[2] = {nullptr, nullptr};  // [g][Pw] per version parity
+  float* outer_buf = nullptr;              // [n_leaders][Pw]
+  // streams/events
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  bool ring_issued[2] = {false, false};
+  uint64_t ring_step[2] = {0, 0};
+  // device error word and wait accounting
+  unsigned int* err = nullptr;      // device: 1 timeout, 2 protocol
+};
+
+static size_t slot_floats(const sagips_ctx* c) { return (size_t)c->G.nw; }
+
+static float* slot_ptr(char* base, const sagips_ctx* c, int origin, uint64_t version) {
+  const size_t per_origin = kVersions * slot_floats(c);
+  return reinterpret_cast<float*>(base) + origin * per_origin + (version % kVersions) * slot_floats(c);
+}
+static DevFlags* flags_ptr(char* base, const sagips_ctx* c) {
+  return reinterpret_cast<DevFlags*>(base + sizeof(float) * (size_t)c->cfg.world * kVersions * slot_floats(c));
+}
+
+// ---------------------------------------------------------------- device side
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait until *flag >= want; returns false on timeout (sets *err = 1).
+__device__ bool wait_tag(const unsigned long long* flag, unsigned long long want, unsigned long long timeout_ns,
+                         unsigned int* err) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(flag) < want) {
+    if (globaltimer() - t0 > timeout_ns) {
+      atomicExch(err, 1u);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+// Block-wide copy of n floats (16-byte aligned).
+__device__ void block_copy(float* __restrict__ dst, const float* __restrict__ src, int64_t n) {
+  const int64_t n4 = n / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int64_t i = threadIdx.x; i < n4; i += blockDim.x) d4[i] = s4[i];
+  for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// push: own packet -> successor's slot (origin = me), then release the tag.
+// A single CTA: the copy is ~200 KB, latency-bound over NVLink.
+__global__ void __launch_bounds__(1024) k_push(const float* __restrict__ packet, int64_t n, float* dst_slot,
+                                               unsigned long long* dst_flag, unsigned long long tag) {
+  block_copy(dst_slot, packet, n);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(dst_flag, tag);
+  }
+}
+
+struct FwdArgs {
+  float* src[kMaxWorld];               // own window slots, in hop order
+  float* dst[kMaxWorld];               // successor's slots
+  unsigned long long* src_flag[kMaxWorld];
+  unsigned long long* dst_flag[kMaxWorld];
+  int hops;
+};
+
+// forwarding agent: for hop j, wait for the packet of origin pos-j in the own
+// window, then pass it to the successor (Alg. 1's "send to rank i+1").
+__global__ void __launch_bounds__(1024) k_forward(FwdArgs a, int64_t n, unsigned long long tag,
+                                                  unsigned long long timeout_ns, unsigned int* err) {
+  __shared__ int ok;
+  for (int j = 0; j < a.hops; ++j) {
+    if (threadIdx.x == 0) ok = wait_tag(a.src_flag[j], tag, timeout_ns, err);
+    __syncthreads();
+    if (!ok) return;
+    block_copy(a.dst[j], a.src[j], n);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(a.dst_flag[j], tag);
+    }
+  }
+}
+
+struct WaitArgs {
+  unsigned long long* flag[kMaxWorld];
+  unsigned long long want[kMaxWorld];
+  int count;
+};
+
+__global__ void k_wait(WaitArgs a, unsigned long long timeout_ns, unsigned int* err, unsigned long long* wait_ns) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer();
+  for (int i = 0; i < a.count; ++i) {
+    if (!wait_tag(a.flag[i], a.want[i], timeout_ns, err)) break;
+    if (ld_acquire_sys(a.flag[i]) != a.want[i]) atomicExch(err, 2u);  // a newer packet overwrote the slot
+  }
+  *wait_ns = globaltimer() - t0;
+}
+
+// ---------------------------------------------------------------- host side
+#define XCK(call)                                                                          \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(e_);                         \
+      return SAGIPS_ERR_CUDA;                                                              \
+    }                                                                                      \
+  } while (0)
+#define NCK(call)                                                                          \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess) {                                                               \
+      c->err = std::string(#call) + ": " + ncclGetErrorString(r_);                         \
+      return SAGIPS_ERR_CUDA;                                                              \
+    }                                                                                      \
+  } while (0)
+
+static bool one_sided(const sagips_ctx* c) { return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR; }
+static bool needs_nccl(const sagips_ctx* c) {
+  const auto& g = c->cfg;
+  if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) return false;
+  if (g.mode == SAGIPS_MODE_RMA_ARAR_ARAR) return g.outer_every > 0 && g.group_size < g.world;
+  return true;
+}
+
+static sagips_status ensure_state(sagips_ctx* c) {
+  if (c->xs) return SAGIPS_OK;
+  auto* x = new ExchangeState();
+  c->xs = x;
+  const auto& g = c->cfg;
+  int gs = g.group_size;
+  if (g.mode == SAGIPS_MODE_ARAR) gs = g.world;  // ungrouped
+  x->g = gs;
+  x->first = (g.rank / gs) * gs;
+  x->pos = g.rank - x->first;
+  x->succ = x->first + (x->pos + 1) % gs;
+  x->pred = x->first + (x->pos + gs - 1) % gs;
+  int lo, hi;
+  XCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  XCK(cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, hi));
+  for (int i = 0; i < 2; ++i) {
+    XCK(cudaEventCreateWithFlags(&x->ev_ready[i], cudaEventDisableTiming));
+    XCK(cudaEventCreateWithFlags(&x->ev_done[i], cudaEventDisableTiming));
+  }
+  XCK(cudaMalloc(&x->err, sizeof(unsigned int)));
+  XCK(cudaMemset(x->err, 0, sizeof(unsigned int)));
+  if (g.world > 1 && g.mode != SAGIPS_MODE_NONE) {
+    const size_t pw = slot_floats(c);
+    XCK(cudaMalloc(&x->gather[0], sizeof(float) * pw * gs));
+    XCK(cudaMalloc(&x->gather[1], sizeof(float) * pw * gs));
+    const int nlead = g.world / g.group_size;
+    XCK(cudaMalloc(&x->outer_buf, sizeof(float) * pw * std::max(nlead, 1)));
+    if (one_sided(c)) {
+      x->win_bytes = sizeof(float) * (size_t)g.world * kVersions * pw + sizeof(DevFlags);
+      XCK(cudaMalloc(&x->win, x->win_bytes));
+      XCK(cudaMemset(x->win, 0, x->win_bytes));
+      x->flags = flags_ptr(reinterpret_cast<char*>(x->win), c);
+      XCK(cudaIpcGetMemHandle(&x->handle, x->win));
+      x->have_handle = true;
+    }
+  }
+  return SAGIPS_OK;
+}
+
+sagips_status exchange_check(sagips_ctx* c) {
+  if (!c->xs || !c->xs->err) return SAGIPS_OK;
+  unsigned int e = 0;
+  if (cudaMemcpy(&e, c->xs->err, sizeof e, cudaMemcpyDeviceToHost) != cudaSuccess) return SAGIPS_ERR_CUDA;
+  if (e == 1) { c->err = "exchange wait timed out"; return SAGIPS_ERR_TIMEOUT; }
+  if (e == 2) { c->err = "exchange slot overrun (protocol)"; return SAGIPS_ERR_PROTOCOL; }
+  return SAGIPS_OK;
+}
+
+void exchange_destroy(sagips_ctx* c) {
+  ExchangeState* x = c->xs;
+  if (!x) return;
+  cudaDeviceSynchronize();
+  for (int q = 0; q < c->cfg.world; ++q)
+    if (x->peer_base[q] && q != c->cfg.rank) cudaIpcCloseMemHandle(x->peer_base[q]);
+  if (x->comm_ring) ncclCommDestroy(x->comm_ring);
+  if (x->comm_main) ncclCommDestroy(x->comm_main);
+  cudaFree(x->win);
+  cudaFree(x->gather[0]);
+  cudaFree(x->gather[1]);
+  cudaFree(x->outer_buf);
+  cudaFree(x->err);
+  for (int i = 0; i < 2; ++i) {
+    if (x->ev_ready[i]) cudaEventDestroy(x->ev_ready[i]);
+    if (x->ev_done[i]) cudaEventDestroy(x->ev_done[i]);
+  }
+  if (x->side) cudaStreamDestroy(x->side);
+  delete x;
+  c->xs = nullptr;
+}
+
+static unsigned long long timeout_ns(const sagips_ctx* c) {
+  return (unsigned long long)c->cfg.exchange_timeout_ms * 1000000ull;
+}
+
+// the two-sided pass-along ring of one version over the inner group (side stream)
+static sagips_status nccl_ring(sagips_ctx* c, uint64_t step) {
+  ExchangeState* x = c->xs;
+  const size_t pw = slot_floats(c);
+  float* gbuf = x->gather[step & 1];
+  for (int j = 1; j < x->g; ++j) {
+    const int send_pos = (x->pos - j + 1 + x->g) % x->g;
+    const int recv_pos = (x->pos - j + x->g) % x->g;
+    NCK(ncclGroupStart());
+    NCK(ncclSend(gbuf + send_pos * pw, pw, ncclFloat32, x->succ, x->comm_ring, x->side));
+    NCK(ncclRecv(gbuf + recv_pos * pw, pw, ncclFloat32, x->pred, x->comm_ring, x->side));
+    NCK(ncclGroupEnd());
+  }
+  return SAGIPS_OK;
+}
+
+sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
+  const auto& g = c->cfg;
+  if (g.world == 1 || g.mode == SAGIPS_MODE_NONE || g.mode == SAGIPS_MODE_SYNC_ALLREDUCE) return SAGIPS_OK;
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  ExchangeState* x = c->xs;
+  const size_t pw = slot_floats(c);
+  if (x->g == 1) return SAGIPS_OK;
+  if (one_sided(c)) {
+    if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
+    char* sb = x->peer_base[x->succ];
+    k_push<<<1, 1024, 0, st>>>(c->g_dW, (int64_t)pw, slot_ptr(sb, c, g.rank, step),
+                               &flags_ptr(sb, c)->tag[g.rank][step % kVersions], step + 1);
+    count_launch();
+    if (x->g > 2) {
+      // the agent forwards origins pos-1 .. pos-(g-2) of this version
+      XCK(cudaEventRecord(x->ev_ready[step & 1], st));
+      XCK(cudaStreamWaitEvent(x->side, x->ev_ready[step & 1], 0));
+      FwdArgs a{};
+      a.hops = x->g - 2;
+      char* own = x->peer_base[g.rank];
+      for (int j = 1; j <= x->g - 2; ++j) {
+        const int o = x->first + (x->pos - j + x->g) % x->g;
+        a.src[j - 1] = slot_ptr(own, c, o, step);
+        a.src_flag[j - 1] = &flags_ptr(own, c)->tag[o][step % kVersions];
+        a.dst[j - 1] = slot_ptr(sb, c, o, step);
+        a.dst_flag[j - 1] = &flags_ptr(sb, c)->tag[o][step % kVersions];
+      }
+      k_forward<<<1, 1024, 0, x->side>>>(a, (int64_t)pw, step + 1, timeout_ns(c), x->err);
+      count_launch();
+    }
+  } else {
+    if (!x->comm_ring) { c->err = "sagips_connect_nccl not called"; return SAGIPS_ERR_STATE; }
+    float* gbuf = x->gather[step & 1];
+    XCK(cudaMemcpyAsync(gbuf + x->pos * pw, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
+    XCK(cudaEventRecord(x->ev_ready[step & 1], st));
+    XCK(cudaStreamWaitEvent(x->side, x->ev_ready[step & 1], 0));
+    s = nccl_ring(c, step);
+    if (s != SAGIPS_OK) return s;
+    XCK(cudaEventRecord(x->ev_done[step & 1], x->side));
+    x->ring_issued[step & 1] = true;
+    x->ring_step[step & 1] = step;
+  }
+  return SAGIPS_OK;
+}
+
+static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
+  ExchangeState* x = c->xs;
+  const auto& g = c->cfg;
+  const int nlead = g.world / g.group_size;
+  if (g.mode == SAGIPS_MODE_ARAR || nlead < 2 || g.outer_every <= 0) return SAGIPS_OK;
+  if ((step + 1) % (uint64_t)g.outer_every != 0) return SAGIPS_OK;
+  if (g.rank % g.group_size != 0) return SAGIPS_OK;  // leaders only
+  if (!x->comm_main) { c->err = "sagips_connect_nccl not called (outer ring)"; return SAGIPS_ERR_STATE; }
+  const size_t pw = slot_floats(c);
+  const int lp = g.rank / g.group_size;
+  const int lsucc = ((lp + 1) % nlead) * g.group_size, lpred = ((lp + nlead - 1) % nlead) * g.group_size;
+  XCK(cudaMemcpyAsync(x->outer_buf + lp * pw, c->reduced, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
+  for (int j = 1; j < nlead; ++j) {
+    const int sp = (lp - j + 1 + nlead) % nlead, rp = (lp - j + nlead) % nlead;
+    NCK(ncclGroupStart());
+    NCK(ncclSend(x->outer_buf + sp * pw, pw, ncclFloat32, lsucc, x->comm_main, st));
+    NCK(ncclRecv(x->outer_buf + rp * pw, pw, ncclFloat32, lpred, x->comm_main, st));
+    NCK(ncclGroupEnd());
+  }
+  PacketList pl{};
+  pl.count = nlead;
+  for (int i = 0; i < nlead; ++i) pl.p[i] = x->outer_buf + i * pw;
+  launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)nlead : 1.0f, st);
+  uint32_t one = 1;
+  XCK(cudaMemcpyAsync(&c->stats->outer_fired, &one, sizeof one, cudaMemcpyHostToDevice, st));
+  XCK(cudaStreamSynchronize(st));  // `one` is on the host stack
+  return SAGIPS_OK;
+}
+
+sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st) {
+  const auto& g = c->cfg;
+  const size_t pw = slot_floats(c);
+  XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
+  if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) {
+    XCK(cudaMemcpyAsync(c->reduced, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
+    return SAGIPS_OK;
+  }
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  ExchangeState* x = c->xs;
+  if (g.mode == SAGIPS_MODE_SYNC_ALLREDUCE) {
+    if (!x->comm_main) { c->err = "sagips_connect_nccl not called"; return SAGIPS_ERR_STATE; }
+    NCK(ncclAllReduce(c->g_dW, c->reduced, pw, ncclFloat32, ncclSum, x->comm_main, st));
+    if (g.reduce_mean) {
+      PacketList pl{};
+      pl.count = 1;
+      pl.p[0] = c->reduced;
+      launch_fold(pl, (int64_t)pw, c->reduced, (float)g.world, st);
+    }
+    return SAGIPS_OK;
+  }
+  const int64_t stale = (int64_t)step - g.staleness;  // version of the others' packets
+  PacketList pl{};
+  pl.count = x->g;
+  if (x->g == 1) {
+    pl.p[0] = c->g_dW;
+  } else if (one_sided(c)) {
+    char* own = x->peer_base[g.rank];
+    if (stale >= 0) {
+      WaitArgs w{};
+      w.count = x->g - 1;
+      for (int j = 1; j < x->g; ++j) {
+        const int o = x->first + (x->pos - j + x->g) % x->g;
+        w.flag[j - 1] = &flags_ptr(own, c)->tag[o][stale % kVersions];
+        w.want[j - 1] = (unsigned long long)stale + 1;
+      }
+      k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), x->err, reinterpret_cast<unsigned long long*>(&c->stats->wait_ns));
+      count_launch();
+    }
+    for (int i = 0; i < x->g; ++i) {
+      const int o = x->first + i;
+      pl.p[i] = (o == g.rank) ? c->g_dW : (stale >= 0 ? slot_ptr(own, c, o, stale) : nullptr);
+    }
+  } else {
+    if (stale >= 0) {
+      const int v = (int)(stale & 1);
+      if (!x->ring_issued[v] || x->ring_step[v] != (uint64_t)stale) {
+        c->err = "pull: ring of the needed version was not issued";
+        return SAGIPS_ERR_STATE;
+      }
+      XCK(cudaStreamWaitEvent(st, x->ev_done[v], 0));
+    }
+    for (int i = 0; i < x->g; ++i)
+      pl.p[i] = (i == x->pos) ? c->g_dW : (stale >= 0 ? x->gather[stale & 1] + i * pw : nullptr);
+  }
+  if (stale < 0 && x->g > 1) {
+    // before step s the other members' packets are zero (R12): own packet only
+    PacketList own{};
+    own.count = 1;
+    own.p[0] = c->g_dW;
+    launch_fold(own, (int64_t)pw, c->reduced, g.reduce_mean ? (float)x->g : 1.0f, st);
+  } else {
+    launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)x->g : 1.0f, st);
+  }
+  return outer_ring(c, step, st);
+}
+
+}  // namespace sagips
+
+using namespace sagips;
+
+extern "C" {
+
+sagips_status sagips_ipc_handle(sagips_ctx* c, void* host_handle, size_t bytes) {
+  if (!c || !host_handle || bytes != SAGIPS_IPC_HANDLE_BYTES) return SAGIPS_ERR_INVALID_ARG;
+  std::memset(host_handle, 0, bytes);
+  if (!one_sided(c) || c->cfg.world == 1) return SAGIPS_OK;  // nothing to share
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  static_assert(sizeof(cudaIpcMemHandle_t) == SAGIPS_IPC_HANDLE_BYTES, "handle size");
+  std::memcpy(host_handle, &c->xs->handle, bytes);
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_connect_peers(sagips_ctx* c, const void* host_handles, size_t bytes) {
+  if (!c || !host_handles || bytes != (size_t)SAGIPS_IPC_HANDLE_BYTES * c->cfg.world) return SAGIPS_ERR_INVALID_ARG;
+  if (!one_sided(c) || c->cfg.world == 1) return SAGIPS_OK;
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  ExchangeState* x = c->xs;
+  const char* h = (const char*)host_handles;
+  for (int q = x->first; q < x->first + x->g; ++q) {  // only the inner group is touched
+    if (q == c->cfg.rank) {
+      x->peer_base[q] = reinterpret_cast<char*>(x->win);
+      continue;
+    }
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, h + (size_t)q * SAGIPS_IPC_HANDLE_BYTES, sizeof hd);
+    void* p = nullptr;
+    XCK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+    x->peer_base[q] = reinterpret_cast<char*>(p);
+  }
+  x->peers_ok = true;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_nccl_unique_id(void* host_id, size_t bytes) {
+  if (!host_id || bytes != SAGIPS_NCCL_ID_BYTES) return SAGIPS_ERR_INVALID_ARG;
+  static_assert(sizeof(ncclUniqueId) == SAGIPS_NCCL_ID_BYTES, "nccl id size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return SAGIPS_ERR_CUDA;
+  std::memcpy(host_id, &id, bytes);
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_connect_nccl(sagips_ctx* c, const void* host_id, size_t bytes) {
+  if (!c || !host_id || bytes != SAGIPS_NCCL_ID_BYTES) return SAGIPS_ERR_INVALID_ARG;
+  if (!needs_nccl(c)) return SAGIPS_OK;
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  ExchangeState* x = c->xs;
+  ncclUniqueId id;
+  std::memcpy(&id, host_id, sizeof id);
+  NCK(ncclCommInitRank(&x->comm_main, c->cfg.world, id, c->cfg.rank));
+  NCK(ncclCommSplit(x->comm_main, 0, c->cfg.rank, &x->comm_ring, nullptr));
+  return SAGIPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// internal.h -- kernel launchers shared by the translation units of
+// libsagips.so.  Not part of the public ABI (include/sagips.h is).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace sagips {
+
+constexpr int kMaxLayers = 16;
+constexpr int kMaxWorld = 64;
+
+void count_launch();
+uint64_t launches_total();
+
+struct Coef6 { float v[6]; };
+
+enum EpiKind { EPI_STORE = 0, EPI_BIAS_ACT = 1, EPI_ACT_GRAD = 2 };
+struct Epi {
+  int kind;
+  const float* bias;  // EPI_BIAS_ACT
+  int lrelu;          // EPI_BIAS_ACT: apply LeakyReLU
+  float alpha;        // LeakyReLU slope
+  const float* H;     // EPI_ACT_GRAD: post-activation whose sign selects 1 or alpha
+  int ldh;
+};
+
+struct PacketList {
+  const float* p[kMaxWorld];
+  int count;
+};
+
+// k_data.cu
+void launch_normals(float* out, int64_t count, float scale, uint64_t seed, uint32_t step, uint32_t rank,
+                    uint32_t stream_id, cudaStream_t st);
+void launch_reference(float* ref, int64_t n, const float c_true[6], uint64_t seed, cudaStream_t st);
+void launch_shard(const float* ref, int64_t n_ref, float* shard, int64_t n_s, uint64_t seed, uint32_t rank,
+                  cudaStream_t st);
+void launch_constrain(const float* raw, float* c, int k, cudaStream_t st);
+void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard, uint64_t seed,
+                        uint32_t step, uint32_t rank, float* x_events, uint32_t* real_idx, uint32_t* hist,
+                        int bins, const float lo[2], const float hi[2], cudaStream_t st);
+void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t step, uint32_t rank,
+                          uint32_t stream_id, float* events, uint32_t* hist, int bins, const float lo[2],
+                          const float hi[2], cudaStream_t st);
+void launch_sample_bwd(const float* dy, const float* raw, int k, int m, uint64_t seed, uint32_t step,
+                       uint32_t rank, float* draw, cudaStream_t st);
+
+// k_mlp_simt.cu
+void launch_gemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                 float* C, int ldc, const Epi& ep, int splits, int64_t c_split, cudaStream_t st);
+void launch_colsum(const float* X, int rows, int cols, int ldx, int splits, float* part, cudaStream_t st);
+void launch_reduce_parts(const float* part, int nparts, int64_t n, float* out, float scale, cudaStream_t st);
+int head_blocks();
+void launch_head(const float* H, int M, int hd, const float* w, const float* b, int n_real, float label_rest,
+                 float scale, float alpha, float* logits, float* dZprev, float* part, double* loss_part,
+                 bool want_wgrad, cudaStream_t st);
+void launch_finish_loss(const double* loss_part, int nparts, double scale, float* out, uint32_t* nonfinite,
+                        cudaStream_t st);
+
+// k_adam.cu
+void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,
+                 double b2, double eps, cudaStream_t st);
+void launch_fold(const PacketList& pl, int64_t n, float* out, float divisor, cudaStream_t st);
+
+}  // namespace sagips

@@ -1,0 +1,52 @@
+// k_adam.cu -- Adam (PyTorch form, R7) and the ascending fold of packets.
+//
+//   m <- b1 m + (1-b1) g ; v <- b2 v + (1-b2) g^2
+//   p <- p - (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps),  bc_i = 1 - b_i^tau
+// bc1 / sqrt(bc2) are computed on the host in double, as torch.optim.Adam.
+#include "internal.h"
+
+namespace sagips {
+
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                       float* __restrict__ v, int64_t n, float step_size, float bc2_sqrt, float b1, float b2,
+                       float eps) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float denom = sqrtf(vi) / bc2_sqrt + eps;
+    p[i] -= step_size * (mi / denom);
+  }
+}
+
+void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,
+                 double b2, double eps, cudaStream_t st) {
+  if (n <= 0) return;
+  const double bc1 = 1.0 - std::pow(b1, (double)tau);
+  const double bc2 = 1.0 - std::pow(b2, (double)tau);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_adam<<<blocks, 256, 0, st>>>(p, g, m, v, n, (float)(lr / bc1), (float)std::sqrt(bc2), (float)b1, (float)b2,
+                                 (float)eps);
+  count_launch();
+}
+
+// out[i] = (((P_0[i] + P_1[i]) + P_2[i]) + ...)  / divisor over the given
+// packets in the given (ascending origin) order (R10).  Pointers may be
+// local or peer-mapped (NVLink) addresses.
+__global__ void k_fold(PacketList pl, int64_t n, float* __restrict__ out, float divisor) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = pl.p[0][i];
+    for (int j = 1; j < pl.count; ++j) acc += pl.p[j][i];
+    out[i] = acc / divisor;
+  }
+}
+
+void launch_fold(const PacketList& pl, int64_t n, float* out, float divisor, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);
+  k_fold<<<blocks, 256, 0, st>>>(pl, n, out, divisor);
+  count_launch();
+}
+
+}  // namespace sagips

@@ -1,0 +1,273 @@
+// k_data.cu -- random-number-driven kernels of the step: Kaiming init,
+// reference data, bootstrap shard, generator noise, the fused event sampler
+// (constrain -> Philox -> inverse CDF -> feature rows -> histograms, plus the
+// bootstrap gather of the real rows), and the sampler backward.
+//
+// Paper: P:272 (reference data from known parameters), P:144-146 + P:387
+// (50% shard, bootstrap batches), P:295 (inverse-CDF sampler), P:297 (Kaiming
+// normal init).  Readings R1, R-RNG, R-UNIF, R-BOOT, R22 in DESIGN.md.
+#include "internal.h"
+
+namespace sagips {
+
+// ---------------------------------------------------------------- normals
+// Call c of the stream gives normals 4c..4c+3: (w0,w1) -> (r cos, r sin),
+// (w2,w3) -> (r cos, r sin), r = sqrt(-2 ln u_a), angle 2 pi u_b.
+__global__ void k_normals(float* __restrict__ out, int64_t count, float scale, PhiloxKey key,
+                          uint32_t step, uint32_t rank, uint32_t stream) {
+  const int64_t ncalls = (count + 3) / 4;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncalls;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox_call(key, (uint32_t)c, step, rank, stream);
+    float z[4];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const float ua = uniform_open01(p ? w.z : w.x);
+      const float ub = uniform_open01(p ? w.w : w.y);
+      const float r = sqrtf(-2.0f * logf(ua));
+      float s, co;
+      sincospif(2.0f * ub, &s, &co);
+      z[2 * p] = r * co;
+      z[2 * p + 1] = r * s;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t f = 4 * c + q;
+      if (f < count) out[f] = scale * z[q];
+    }
+  }
+}
+
+void launch_normals(float* out, int64_t count, float scale, uint64_t seed, uint32_t step,
+                    uint32_t rank, uint32_t stream_id, cudaStream_t st) {
+  if (count <= 0) return;
+  const int64_t ncalls = (count + 3) / 4;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((ncalls + threads - 1) / threads, 148 * 16);
+  k_normals<<<blocks, threads, 0, st>>>(out, count, scale, make_key(seed), step, rank, stream_id);
+  count_launch();
+}
+
+// ---------------------------------------------------------------- reference
+// ref[i][o] = Q(u(word 2i+o of stream REF, step 0, rank 0); c_true[o]).
+__global__ void k_reference(float* __restrict__ ref, int64_t n, Coef6 c, PhiloxKey key) {
+  const int64_t ncalls = (n + 1) / 2;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ncalls;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox_call(key, (uint32_t)q, 0, 0, kStreamRef);
+    const int64_t e0 = 2 * q;
+    ref[2 * e0 + 0] = quantile_f32(uniform_open01(w.x), c.v[0], c.v[1], c.v[2]);
+    ref[2 * e0 + 1] = quantile_f32(uniform_open01(w.y), c.v[3], c.v[4], c.v[5]);
+    if (e0 + 1 < n) {
+      ref[2 * e0 + 2] = quantile_f32(uniform_open01(w.z), c.v[0], c.v[1], c.v[2]);
+      ref[2 * e0 + 3] = quantile_f32(uniform_open01(w.w), c.v[3], c.v[4], c.v[5]);
+    }
+  }
+}
+
+void launch_reference(float* ref, int64_t n, const float c_true[6], uint64_t seed, cudaStream_t st) {
+  Coef6 c;
+  for (int i = 0; i < 6; ++i) c.v[i] = c_true[i];
+  const int64_t ncalls = (n + 1) / 2;
+  const int blocks = (int)std::min<int64_t>((ncalls + 255) / 256, 148 * 16);
+  k_reference<<<blocks, 256, 0, st>>>(ref, n, c, make_key(seed));
+  count_launch();
+}
+
+// ---------------------------------------------------------------- shard
+// shard[i] = ref[(w_i * n_ref) >> 32], w_i = word i of stream SHARD (step 0).
+__global__ void k_shard(const float2* __restrict__ ref, uint32_t n_ref, float2* __restrict__ shard,
+                        int64_t n_s, PhiloxKey key, uint32_t rank) {
+  const int64_t ncalls = (n_s + 3) / 4;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncalls;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 w = philox_call(key, (uint32_t)c, 0, rank, kStreamShard);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = 4 * c + q;
+      if (i < n_s) shard[i] = ref[lemire(word_of(w, q), n_ref)];
+    }
+  }
+}
+
+void launch_shard(const float* ref, int64_t n_ref, float* shard, int64_t n_s, uint64_t seed,
+                  uint32_t rank, cudaStream_t st) {
+  const int64_t ncalls = (n_s + 3) / 4;
+  const int blocks = (int)std::min<int64_t>((ncalls + 255) / 256, 148 * 16);
+  k_shard<<<blocks, 256, 0, st>>>(reinterpret_cast<const float2*>(ref), (uint32_t)n_ref,
+                                  reinterpret_cast<float2*>(shard), n_s, make_key(seed), rank);
+  count_launch();
+}
+
+// ---------------------------------------------------------------- constrain
+// c[s] = (raw0, softplus(raw1), softplus(raw2), raw3, softplus(raw4), softplus(raw5)) (R1)
+__global__ void k_constrain(const float* __restrict__ raw, float* __restrict__ c, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 6 * k) return;
+  const int j = i % 3;
+  const float x = raw[i];
+  c[i] = (j == 0) ? x : softplus_f(x);
+}
+
+void launch_constrain(const float* raw, float* c, int k, cudaStream_t st) {
+  k_constrain<<<(6 * k + 255) / 256, 256, 0, st>>>(raw, c, k);
+  count_launch();
+}
+
+// ---------------------------------------------------------------- sampler
+// One thread = one group of 4 consecutive events e = 4g..4g+3:
+//   fake: Philox calls 2g and 2g+1 of stream FAKE give the 8 words 2e+o;
+//   real: call g of stream REAL gives the 4 bootstrap words (word e).
+// Rows of X: [0, N) real, [N, 2N) fake (R9).  Histograms are privatised in
+// shared memory (uint32, exact) and merged with integer atomics.
+template <bool kReal>
+__global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int m, int64_t n_events,
+                                                const float2* __restrict__ shard, uint32_t n_shard,
+                                                PhiloxKey key, uint32_t step, uint32_t rank,
+                                                uint32_t fake_stream, float2* __restrict__ x_real,
+                                                float2* __restrict__ y_fake, uint32_t* __restrict__ real_idx,
+                                                uint32_t* __restrict__ hist, int bins, float lo0, float sc0,
+                                                float lo1, float sc1) {
+  extern __shared__ uint32_t sh_hist[];  // [2 sets][2 obs][bins+2]
+  const int hsz = 4 * (bins + 2);
+  if (hist) {
+    for (int i = threadIdx.x; i < hsz; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
+  }
+  const int64_t ngroups = (n_events + 3) / 4;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 wa = philox_call(key, (uint32_t)(2 * g), step, rank, fake_stream);
+    const uint4 wb = philox_call(key, (uint32_t)(2 * g + 1), step, rank, fake_stream);
+    const uint32_t wf[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+    uint4 wr = make_uint4(0, 0, 0, 0);
+    if (kReal) wr = philox_call(key, (uint32_t)g, step, rank, kStreamReal);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t e = 4 * g + q;
+      if (e >= n_events) break;
+      const int64_t s = e / m;
+      const float* cs = c + 6 * s;
+      const float y0 = quantile_f32(uniform_open01(wf[2 * q]), __ldg(cs + 0), __ldg(cs + 1), __ldg(cs + 2));
+      const float y1 = quantile_f32(uniform_open01(wf[2 * q + 1]), __ldg(cs + 3), __ldg(cs + 4), __ldg(cs + 5));
+      y_fake[e] = make_float2(y0, y1);
+      if (hist) {
+        atomicAdd(&sh_hist[2 * (bins + 2) + hist_bin(y0, lo0, sc0, bins)], 1u);
+        atomicAdd(&sh_hist[3 * (bins + 2) + hist_bin(y1, lo1, sc1, bins)], 1u);
+      }
+      if (kReal) {
+        const uint32_t idx = lemire(word_of(wr, q), n_shard);
+        const float2 xv = __ldg(shard + idx);
+        x_real[e] = xv;
+        real_idx[e] = idx;
+        if (hist) {
+          atomicAdd(&sh_hist[0 * (bins + 2) + hist_bin(xv.x, lo0, sc0, bins)], 1u);
+          atomicAdd(&sh_hist[1 * (bins + 2) + hist_bin(xv.y, lo1, sc1, bins)], 1u);
+        }
+      }
+    }
+  }
+  if (hist) {
+    __syncthreads();
+    const int off = kReal ? 0 : 2 * (bins + 2);
+    for (int i = off + threadIdx.x; i < hsz; i += blockDim.x)
+      if (sh_hist[i]) atomicAdd(&hist[i - off], sh_hist[i]);
+  }
+}
+
+static void hist_params(const float lo[2], const float hi[2], int bins, float* sc) {
+  for (int o = 0; o < 2; ++o) sc[o] = (float)bins / (hi[o] - lo[o]);  // fp32, as the oracle
+}
+
+void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard,
+                        uint64_t seed, uint32_t step, uint32_t rank, float* x_events,
+                        uint32_t* real_idx, uint32_t* hist, int bins, const float lo[2],
+                        const float hi[2], cudaStream_t st) {
+  const int64_t n = (int64_t)k * m;
+  float sc[2];
+  hist_params(lo, hi, bins, sc);
+  if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * (bins + 2), st);
+  const int64_t ngroups = (n + 3) / 4;
+  const int blocks = (int)std::min<int64_t>((ngroups + 255) / 256, 148 * 8);
+  const size_t smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) : 0;
+  float2* x = reinterpret_cast<float2*>(x_events);
+  k_sample<true><<<blocks, 256, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard),
+                                            (uint32_t)n_shard, make_key(seed), step, rank, kStreamFake,
+                                            x, x + n, real_idx, hist, bins, lo[0], sc[0], lo[1], sc[1]);
+  count_launch();
+}
+
+void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t step, uint32_t rank,
+                          uint32_t stream_id, float* events, uint32_t* hist, int bins,
+                          const float lo[2], const float hi[2], cudaStream_t st) {
+  const int64_t n = (int64_t)k * m;
+  float sc[2] = {0.f, 0.f};
+  float l[2] = {0.f, 0.f};
+  if (hist) {
+    hist_params(lo, hi, bins, sc);
+    l[0] = lo[0];
+    l[1] = lo[1];
+    cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * (bins + 2), st);
+  }
+  const int64_t ngroups = (n + 3) / 4;
+  const int blocks = (int)std::min<int64_t>((ngroups + 255) / 256, 148 * 8);
+  const size_t smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) : 0;
+  k_sample<false><<<blocks, 256, smem, st>>>(c, m, n, nullptr, 1, make_key(seed), step, rank, stream_id,
+                                             nullptr, reinterpret_cast<float2*>(events), nullptr, hist,
+                                             bins, l[0], sc[0], l[1], sc[1]);
+  count_launch();
+}
+
+// ---------------------------------------------------------------- sampler backward
+// One block per parameter sample s:
+//   dc[o][j] = sum_{e in s} dy[e][o] * u[e][o]^j   (dQ/dc = (1, u, u^2))
+//   draw[s][3o] = dc[o][0], draw[s][3o+1] = dc[o][1] softplus'(raw), ...
+// u is recomputed from the FAKE stream (not stored).  The block reduction has
+// a fixed order, so the result is deterministic.
+__global__ void __launch_bounds__(256) k_sample_bwd(const float2* __restrict__ dy, const float* __restrict__ raw,
+                                                    int m, PhiloxKey key, uint32_t step, uint32_t rank,
+                                                    float* __restrict__ draw) {
+  const int s = blockIdx.x;
+  float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t e = (int64_t)s * m + i;
+    const uint4 w = philox_call(key, (uint32_t)(e >> 1), step, rank, kStreamFake);
+    const bool odd = e & 1;
+    const float u0 = uniform_open01(odd ? w.z : w.x);
+    const float u1 = uniform_open01(odd ? w.w : w.y);
+    const float2 g = dy[e];
+    acc[0] += g.x;
+    acc[1] += g.x * u0;
+    acc[2] += g.x * u0 * u0;
+    acc[3] += g.y;
+    acc[4] += g.y * u1;
+    acc[5] += g.y * u1 * u1;
+  }
+  __shared__ float red[6][32];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) {
+    float v = acc[j];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int j = threadIdx.x;
+    float v = 0.f;
+    for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi) v += red[j][wi];
+    const int jj = j % 3;
+    const float r = raw[6 * s + j];
+    draw[6 * s + j] = jj == 0 ? v : v * softplus_grad_f(r);
+  }
+}
+
+void launch_sample_bwd(const float* dy, const float* raw, int k, int m, uint64_t seed, uint32_t step,
+                       uint32_t rank, float* draw, cudaStream_t st) {
+  int threads = 32 * ((std::min(m, 256) + 31) / 32);
+  k_sample_bwd<<<k, threads, 0, st>>>(reinterpret_cast<const float2*>(dy), raw, m, make_key(seed),
+                                      step, rank, draw);
+  count_launch();
+}
+
+}  // namespace sagips

@@ -1,0 +1,622 @@
+// sagips.cu -- the C ABI of libsagips.so (include/sagips.h): rank context,
+// workspace layout in HBM, and the stream-ordered orchestration of one
+// SAGIPS training step (order R8).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sagips.h"
+#include "ctx.h"
+#include "internal.h"
+
+namespace sagips {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launches_total() { return g_launches.load(std::memory_order_relaxed); }
+
+void MlpLayout::build(int in, int hidden, int depth, int out) {
+  L = depth + 1;
+  sizes[0] = in;
+  for (int i = 1; i <= depth; ++i) sizes[i] = hidden;
+  sizes[L] = out;
+  nw = nb = 0;
+  maxw = 0;
+  for (int l = 0; l < L; ++l) {
+    w_off[l] = nw;
+    b_off[l] = nb;
+    nw += (int64_t)sizes[l + 1] * sizes[l];
+    nb += sizes[l + 1];
+    maxw = std::max(maxw, std::max(sizes[l], sizes[l + 1]));
+  }
+}
+
+// ---------------------------------------------------------------- layout
+// All device buffers are carved out of the caller's workspace (256-B
+// aligned).  The same function sizes (base == nullptr) and carves.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(int64_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += sizeof(T) * (size_t)std::max<int64_t>(count, 1);
+    return p;
+  }
+};
+
+static int wgrad_splits(int M, int N, int64_t K) {
+  const int tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  int s = std::max(1, 296 / tiles);
+  const int64_t kmax = std::max<int64_t>(1, K / 256);
+  return (int)std::min<int64_t>(s, kmax);
+}
+
+static void carve(sagips_ctx* c, char* base) {
+  Carver cv{base};
+  const sagips_config& g = c->cfg;
+  const int64_t k = g.param_samples, N = c->N;
+  auto& G = c->G;
+  auto& D = c->D;
+  c->gW = cv.take<float>(G.nw);  c->gB = cv.take<float>(G.nb);
+  c->gmW = cv.take<float>(G.nw); c->gvW = cv.take<float>(G.nw);
+  c->gmB = cv.take<float>(G.nb); c->gvB = cv.take<float>(G.nb);
+  c->dW = cv.take<float>(D.nw);  c->dB = cv.take<float>(D.nb);
+  c->dmW = cv.take<float>(D.nw); c->dvW = cv.take<float>(D.nw);
+  c->dmB = cv.take<float>(D.nb); c->dvB = cv.take<float>(D.nb);
+  c->g_dW = cv.take<float>(G.nw); c->g_dB = cv.take<float>(G.nb);
+  c->d_dW = cv.take<float>(D.nw); c->d_dB = cv.take<float>(D.nb);
+  c->reduced = cv.take<float>(G.nw);
+  c->ref = cv.take<float>(2 * g.reference_rows);
+  c->shard = cv.take<float>(2 * g.shard_rows);
+  c->noise = cv.take<float>(k * g.noise_dim);
+  for (int l = 0; l < G.L; ++l) c->gAct[l] = cv.take<float>(k * G.sizes[l + 1]);
+  c->gdZ[0] = cv.take<float>(k * G.maxw);
+  c->gdZ[1] = cv.take<float>(k * G.maxw);
+  c->cbuf = cv.take<float>(6 * k);
+  c->draw = cv.take<float>(6 * k);
+  c->X = cv.take<float>(4 * N);
+  c->real_idx = cv.take<uint32_t>(N);
+  for (int l = 0; l < D.L - 1; ++l) c->dAct[l] = cv.take<float>(2 * N * D.sizes[l + 1]);
+  c->dZb[0] = cv.take<float>(2 * N * D.maxw);
+  c->dZb[1] = cv.take<float>(2 * N * D.maxw);
+  c->logits_d = cv.take<float>(2 * N);
+  c->logits_g = cv.take<float>(N);
+  c->dy = cv.take<float>(2 * N);
+  c->hist = cv.take<uint32_t>(4 * (g.hist_bins + 2));
+  // split-K partials: the largest wgrad of either network, or the head
+  int64_t pf = (int64_t)head_blocks() * (D.maxw + 1);
+  for (int l = 0; l < D.L - 1; ++l)
+    pf = std::max<int64_t>(pf, (int64_t)wgrad_splits(D.sizes[l + 1], D.sizes[l], 2 * N) * D.sizes[l + 1] * D.sizes[l]);
+  for (int l = 0; l < G.L; ++l)
+    pf = std::max<int64_t>(pf, (int64_t)wgrad_splits(G.sizes[l + 1], G.sizes[l], k) * G.sizes[l + 1] * G.sizes[l]);
+  c->part = cv.take<float>(pf);
+  c->part_floats = pf;
+  c->colpart = cv.take<float>(296 * std::max(D.maxw, G.maxw));
+  c->head_tmp = cv.take<float>(D.maxw + 1);
+  c->loss_part = cv.take<double>(head_blocks());
+  c->stats = cv.take<sagips_step_stats>(1);
+  c->ws_bytes = cv.off;
+}
+
+}  // namespace sagips
+
+using namespace sagips;
+
+// ---------------------------------------------------------------- helpers
+static sagips_status fail(sagips_ctx* c, sagips_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(ctx, SAGIPS_ERR_CUDA, "%s: %s (%s:%d)", #call,         \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__);           \
+  } while (0)
+
+static sagips_status validate(const sagips_config* g, std::string* why) {
+  auto bad = [&](const char* m) { *why = m; return SAGIPS_ERR_CONFIG; };
+  if (g->world < 1 || g->world > kMaxWorld) return bad("world must be in [1, 64]");
+  if (g->rank < 0 || g->rank >= g->world) return bad("rank out of range");
+  if (g->group_size < 1 || g->world % g->group_size != 0) return bad("world % group_size != 0");
+  if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_SYNC_ALLREDUCE) return bad("unknown mode");
+  if (g->staleness < 0 || g->staleness > 1) return bad("staleness must be 0 or 1");
+  if (g->precision != SAGIPS_PREC_FP32 && g->precision != SAGIPS_PREC_BF16) return bad("unknown precision");
+  if (g->noise_dim < 1 || g->gen_hidden < 1 || g->gen_depth < 1 || g->disc_depth < 1) return bad("model dims");
+  if (g->gen_depth + 1 > kMaxLayers || g->disc_depth + 1 > kMaxLayers) return bad("too many layers");
+  const int hd = g->disc_hidden;
+  if (hd != 32 && hd != 64 && hd != 128 && hd != 256) return bad("disc_hidden must be 32, 64, 128 or 256");
+  if (g->param_samples < 1 || g->events_per_sample < 1) return bad("k, m >= 1");
+  const int64_t N = (int64_t)g->param_samples * g->events_per_sample;
+  if (2 * N >= (1LL << 31)) return bad("2N must be < 2^31");
+  if (g->reference_rows < 1 || g->reference_rows >= (1LL << 32)) return bad("reference_rows in [1, 2^32)");
+  if (g->shard_rows < 1 || g->shard_rows >= (1LL << 32)) return bad("shard_rows in [1, 2^32)");
+  for (int o = 0; o < 2; ++o)
+    if (!(g->true_params[3 * o + 1] > 0.f) || !(g->true_params[3 * o + 2] > 0.f))
+      return bad("true c1, c2 must be > 0 (softplus range)");
+  if (g->hist_bins < 1 || g->hist_bins > 4096) return bad("hist_bins in [1, 4096]");
+  for (int o = 0; o < 2; ++o)
+    if (!(g->hist_hi[o] > g->hist_lo[o])) return bad("hist_hi must exceed hist_lo");
+  return SAGIPS_OK;
+}
+
+static void setup_dims(sagips_ctx* c) {
+  const sagips_config& g = c->cfg;
+  c->G.build(g.noise_dim, g.gen_hidden, g.gen_depth, 6);   // Eq. 4: six parameters
+  c->D.build(2, g.disc_hidden, g.disc_depth, 1);           // two observables -> one logit
+  c->N = (int64_t)g.param_samples * g.events_per_sample;
+}
+
+extern "C" {
+
+int32_t sagips_abi_version(void) { return SAGIPS_ABI_VERSION; }
+
+sagips_status sagips_config_init(sagips_config* cfg, int32_t preset) {
+  if (!cfg) return SAGIPS_ERR_INVALID_ARG;
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->world = 1; cfg->rank = 0; cfg->group_size = 1; cfg->outer_every = 0;
+  cfg->mode = SAGIPS_MODE_NONE; cfg->staleness = 0; cfg->reduce_mean = 1;
+  cfg->precision = SAGIPS_PREC_FP32;
+  cfg->gen_lr = 1e-5f; cfg->disc_lr = 1e-4f; cfg->leaky_slope = 0.01f;
+  cfg->adam_beta1 = 0.9f; cfg->adam_beta2 = 0.999f; cfg->adam_eps = 1e-8f;
+  const float p[6] = {1.0f, 1.0f, 0.5f, 2.0f, 0.5f, 1.0f};
+  std::memcpy(cfg->true_params, p, sizeof p);
+  cfg->hist_bins = 64;
+  cfg->hist_lo[0] = cfg->hist_lo[1] = 0.0f;
+  cfg->hist_hi[0] = cfg->hist_hi[1] = 4.0f;
+  cfg->seed = 1;
+  cfg->exchange_timeout_ms = 10000;
+  if (preset == SAGIPS_PRESET_DESK) {
+    cfg->noise_dim = 8; cfg->gen_hidden = 64; cfg->gen_depth = 2; cfg->disc_hidden = 64; cfg->disc_depth = 2;
+    cfg->param_samples = 64; cfg->events_per_sample = 16;
+  } else if (preset == SAGIPS_PRESET_PAPER) {
+    cfg->noise_dim = 6; cfg->gen_hidden = 128; cfg->gen_depth = 4; cfg->disc_hidden = 128; cfg->disc_depth = 4;
+    cfg->param_samples = 1024; cfg->events_per_sample = 1024;
+  } else {
+    return SAGIPS_ERR_INVALID_ARG;
+  }
+  const int64_t N = (int64_t)cfg->param_samples * cfg->events_per_sample;
+  cfg->reference_rows = 2 * N;  // R18: n_s = 50% of N_ref = N
+  cfg->shard_rows = N;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_workspace_size(const sagips_config* cfg, size_t* bytes) {
+  if (!cfg || !bytes) return SAGIPS_ERR_INVALID_ARG;
+  std::string why;
+  sagips_status s = validate(cfg, &why);
+  if (s != SAGIPS_OK) return s;
+  sagips_ctx tmp;
+  tmp.cfg = *cfg;
+  setup_dims(&tmp);
+  carve(&tmp, nullptr);
+  *bytes = tmp.ws_bytes + 256;
+  return SAGIPS_OK;
+}
+
+const char* sagips_last_error(const sagips_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t workspace_bytes, void* stream,
+                            sagips_ctx** out) {
+  if (!cfg || !workspace || !out) return SAGIPS_ERR_INVALID_ARG;
+  *out = nullptr;
+  std::string why;
+  sagips_status s = validate(cfg, &why);
+  if (s != SAGIPS_OK) {
+    fprintf(stderr, "sagips_create: %s\n", why.c_str());
+    return s;
+  }
+  if (cfg->precision == SAGIPS_PREC_BF16 && !tc_disc_supported(cfg)) return SAGIPS_ERR_UNSUPPORTED;
+  sagips_ctx* ctx = new sagips_ctx();
+  ctx->cfg = *cfg;
+  if (ctx->cfg.exchange_timeout_ms <= 0) ctx->cfg.exchange_timeout_ms = 10000;
+  setup_dims(ctx);
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  carve(ctx, base);
+  if ((size_t)(base - (char*)workspace) + ctx->ws_bytes > workspace_bytes) {
+    delete ctx;
+    return SAGIPS_ERR_INVALID_ARG;
+  }
+  ctx->launch_base = launches_total();
+  cudaGetDevice(&ctx->dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const sagips_config& g = ctx->cfg;
+  auto bail = [&](sagips_status r) { *out = nullptr; return r; };
+  // Kaiming-normal weights: G identical on every rank, D per rank
+  const float a = g.leaky_slope;
+  for (int l = 0; l < ctx->G.L; ++l) {
+    const float std_ = std::sqrt(2.0f / ((1.0f + a * a) * ctx->G.sizes[l]));
+    launch_normals(ctx->gW + ctx->G.w_off[l], (int64_t)ctx->G.sizes[l + 1] * ctx->G.sizes[l], std_, g.seed, l, 0,
+                   kStreamInitG, st);
+  }
+  for (int l = 0; l < ctx->D.L; ++l) {
+    const float std_ = std::sqrt(2.0f / ((1.0f + a * a) * ctx->D.sizes[l]));
+    launch_normals(ctx->dW + ctx->D.w_off[l], (int64_t)ctx->D.sizes[l + 1] * ctx->D.sizes[l], std_, g.seed, l,
+                   g.rank, kStreamInitD, st);
+  }
+  cudaError_t e = cudaSuccess;
+  e = cudaMemsetAsync(ctx->gB, 0, sizeof(float) * ctx->G.nb, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->dB, 0, sizeof(float) * ctx->D.nb, st);
+  for (float* p : {ctx->gmW, ctx->gvW, ctx->dmW, ctx->dvW})
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(float) * (p == ctx->gmW || p == ctx->gvW ? ctx->G.nw : ctx->D.nw), st);
+  for (float* p : {ctx->gmB, ctx->gvB, ctx->dmB, ctx->dvB})
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(float) * (p == ctx->gmB || p == ctx->gvB ? ctx->G.nb : ctx->D.nb), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->stats, 0, sizeof(sagips_step_stats), st);
+  // loop-closure reference and the rank's shard
+  launch_reference(ctx->ref, g.reference_rows, g.true_params, g.seed, st);
+  launch_shard(ctx->ref, g.reference_rows, ctx->shard, g.shard_rows, g.seed, g.rank, st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "sagips_create: %s\n", cudaGetErrorString(e));
+    delete ctx;
+    return bail(SAGIPS_ERR_CUDA);
+  }
+  if (g.precision == SAGIPS_PREC_BF16) {
+    sagips_status r = tc_disc_init(ctx);
+    if (r != SAGIPS_OK) { delete ctx; return bail(r); }
+  }
+  *out = ctx;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_destroy(sagips_ctx* ctx) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  exchange_destroy(ctx);
+  tc_disc_destroy(ctx);
+  for (auto& row : ctx->pev)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
+  delete ctx;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_sample_events(const float* c, int32_t k, int32_t m, uint64_t seed, uint64_t step, uint32_t rank,
+                                   uint32_t stream_id, float* events, uint32_t* hist, int32_t bins, const float* lo,
+                                   const float* hi, void* stream) {
+  if (!c || !events || k < 1 || m < 1) return SAGIPS_ERR_INVALID_ARG;
+  if (hist && (bins < 1 || !lo || !hi || !(hi[0] > lo[0]) || !(hi[1] > lo[1]))) return SAGIPS_ERR_INVALID_ARG;
+  if ((int64_t)k * m >= (1LL << 31)) return SAGIPS_ERR_INVALID_ARG;
+  launch_sample_events(c, k, m, seed, (uint32_t)step, rank, stream_id, events, hist, bins, lo, hi,
+                       (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- the step
+namespace sagips {
+
+// Hidden layers of the discriminator on `rows` rows of X -> dAct[0..L-2].
+static void disc_hidden_forward_simt(sagips_ctx* c, const float* X, int rows, cudaStream_t st) {
+  const auto& D = c->D;
+  const float* in = X;
+  for (int l = 0; l < D.L - 1; ++l) {
+    Epi ep{EPI_BIAS_ACT, c->dB + D.b_off[l], 1, c->cfg.leaky_slope, nullptr, 0};
+    launch_gemm(false, true, rows, D.sizes[l + 1], D.sizes[l], in, D.sizes[l], c->dW + D.w_off[l], D.sizes[l],
+                c->dAct[l], D.sizes[l + 1], ep, 1, 0, st);
+    in = c->dAct[l];
+  }
+}
+
+// wgrad + bias grad of one layer: dW = dZ^T Hin (K = rows), db = colsum(dZ).
+static void layer_wgrad(sagips_ctx* c, const float* dZ, const float* Hin, int rows, int out, int in, float* dW,
+                        float* db, cudaStream_t st) {
+  const int S = wgrad_splits(out, in, rows);
+  Epi ep{EPI_STORE, nullptr, 0, 0.f, nullptr, 0};
+  launch_gemm(true, false, out, in, rows, dZ, out, Hin, in, c->part, in, ep, S, (int64_t)out * in, st);
+  launch_reduce_parts(c->part, S, (int64_t)out * in, dW, 1.0f, st);
+  const int S2 = (int)std::min<int64_t>(296, std::max(1, rows / 256));
+  launch_colsum(dZ, rows, out, out, S2, c->colpart, st);
+  launch_reduce_parts(c->colpart, S2, out, db, 1.0f, st);
+}
+
+static void disc_step_simt(sagips_ctx* c, cudaStream_t st) {
+  const auto& D = c->D;
+  const int N = (int)c->N;
+  const int rows = 2 * N;
+  const float a = c->cfg.leaky_slope;
+  const int Lh = D.L - 1;  // index of the head layer
+  const int hd = D.sizes[Lh];
+  disc_hidden_forward_simt(c, c->X, rows, st);
+  // head: logits, BCE (labels: real rows 1, fake rows 0; mean over 2N), dz
+  launch_head(c->dAct[Lh - 1], rows, hd, c->dW + D.w_off[Lh], c->dB + D.b_off[Lh], N, 0.0f, 1.0f / (float)rows, a,
+              c->logits_d, c->dZb[0], c->part, c->loss_part, true, st);
+  launch_reduce_parts(c->part, head_blocks(), hd + 1, c->head_tmp, 1.0f, st);
+  cudaMemcpyAsync(c->d_dW + D.w_off[Lh], c->head_tmp, sizeof(float) * hd, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(c->d_dB + D.b_off[Lh], c->head_tmp + hd, sizeof(float), cudaMemcpyDeviceToDevice, st);
+  launch_finish_loss(c->loss_part, head_blocks(), 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
+  int cur = 0;
+  for (int l = Lh - 1; l >= 0; --l) {
+    const float* Hin = (l == 0) ? c->X : c->dAct[l - 1];
+    const int out = D.sizes[l + 1], in = D.sizes[l];
+    layer_wgrad(c, c->dZb[cur], Hin, rows, out, in, c->d_dW + D.w_off[l], c->d_dB + D.b_off[l], st);
+    if (l > 0) {
+      Epi ep{EPI_ACT_GRAD, nullptr, 0, a, c->dAct[l - 1], in};
+      launch_gemm(false, false, rows, in, out, c->dZb[cur], out, c->dW + D.w_off[l], in, c->dZb[cur ^ 1], in, ep, 1,
+                  0, st);
+      cur ^= 1;
+    }
+  }
+}
+
+static void gen_loss_through_disc_simt(sagips_ctx* c, cudaStream_t st) {
+  const auto& D = c->D;
+  const int N = (int)c->N;
+  const float a = c->cfg.leaky_slope;
+  const int Lh = D.L - 1;
+  const int hd = D.sizes[Lh];
+  const float* Y = c->X + 2 * (int64_t)N;  // fake rows
+  disc_hidden_forward_simt(c, Y, N, st);
+  // non-saturating generator loss: label 1 on fake rows, mean over N
+  launch_head(c->dAct[Lh - 1], N, hd, c->dW + D.w_off[Lh], c->dB + D.b_off[Lh], 0, 1.0f, 1.0f / (float)N, a,
+              c->logits_g, c->dZb[0], c->part, c->loss_part, false, st);
+  launch_finish_loss(c->loss_part, head_blocks(), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
+  int cur = 0;
+  for (int l = Lh - 1; l >= 0; --l) {
+    const int out = D.sizes[l + 1], in = D.sizes[l];
+    if (l > 0) {
+      Epi ep{EPI_ACT_GRAD, nullptr, 0, a, c->dAct[l - 1], in};
+      launch_gemm(false, false, N, in, out, c->dZb[cur], out, c->dW + D.w_off[l], in, c->dZb[cur ^ 1], in, ep, 1, 0,
+                  st);
+      cur ^= 1;
+    } else {
+      Epi ep{EPI_STORE, nullptr, 0, 0.f, nullptr, 0};
+      launch_gemm(false, false, N, in, out, c->dZb[cur], out, c->dW + D.w_off[0], in, c->dy, in, ep, 1, 0, st);
+    }
+  }
+}
+
+static void adam_disc(sagips_ctx* c, cudaStream_t st) {
+  const auto& g = c->cfg;
+  c->d_tau += 1;
+  launch_adam(c->dW, c->d_dW, c->dmW, c->dvW, c->D.nw, g.disc_lr, c->d_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+  launch_adam(c->dB, c->d_dB, c->dmB, c->dvB, c->D.nb, g.disc_lr, c->d_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+}
+
+void adam_gen(sagips_ctx* c, cudaStream_t st) {
+  const auto& g = c->cfg;
+  c->g_tau += 1;
+  launch_adam(c->gW, c->reduced, c->gmW, c->gvW, c->G.nw, g.gen_lr, c->g_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+  launch_adam(c->gB, c->g_dB, c->gmB, c->gvB, c->G.nb, g.gen_lr, c->g_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+}
+
+// Steps a1..a11: everything up to and including the packet.
+static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
+  const sagips_config& g = c->cfg;
+  const auto& G = c->G;
+  const int k = g.param_samples, m = g.events_per_sample;
+  const float a = g.leaky_slope;
+  const uint32_t step = (uint32_t)t;
+  mark(c, 0, st);
+  // a1 noise ~ N(0,1)
+  launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
+  // a2 generator forward (hidden LeakyReLU, linear output)
+  const float* in = c->noise;
+  for (int l = 0; l < G.L; ++l) {
+    Epi ep{EPI_BIAS_ACT, c->gB + G.b_off[l], l < G.L - 1, a, nullptr, 0};
+    launch_gemm(false, true, k, G.sizes[l + 1], G.sizes[l], in, G.sizes[l], c->gW + G.w_off[l], G.sizes[l],
+                c->gAct[l], G.sizes[l + 1], ep, 1, 0, st);
+    in = c->gAct[l];
+  }
+  const float* raw = c->gAct[G.L - 1];
+  // a3 constrain ; a4-a6 fused sampler + bootstrap + histograms
+  launch_constrain(raw, c->cbuf, k, st);
+  mark(c, 1, st);
+  launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
+                     g.hist_bins, g.hist_lo, g.hist_hi, st);
+  mark(c, 2, st);
+  // a7 discriminator step + Adam(D) ; a8 generator loss through the updated D
+  if (g.precision == SAGIPS_PREC_BF16) {
+    tc_disc_step(c, st);
+    adam_disc(c, st);
+    mark(c, 3, st);
+    tc_gen_loss(c, st);
+  } else {
+    disc_step_simt(c, st);
+    adam_disc(c, st);
+    mark(c, 3, st);
+    gen_loss_through_disc_simt(c, st);
+  }
+  mark(c, 4, st);
+  // a9 sampler backward
+  launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st);
+  mark(c, 5, st);
+  // a10 generator backward (the output layer is linear: dZ_L = draw);
+  // a11 the weight gradients land in g_dW, which *is* the packet layout
+  const float* cur = c->draw;
+  int buf = 0;
+  for (int l = G.L - 1; l >= 0; --l) {
+    const float* Hin = (l == 0) ? c->noise : c->gAct[l - 1];
+    const int out = G.sizes[l + 1], inn = G.sizes[l];
+    layer_wgrad(c, cur, Hin, k, out, inn, c->g_dW + G.w_off[l], c->g_dB + G.b_off[l], st);
+    if (l > 0) {
+      Epi ep{EPI_ACT_GRAD, nullptr, 0, a, c->gAct[l - 1], inn};
+      launch_gemm(false, false, k, inn, out, cur, out, c->gW + G.w_off[l], inn, c->gdZ[buf], inn, ep, 1, 0, st);
+      cur = c->gdZ[buf];
+      buf ^= 1;
+    }
+  }
+  mark(c, 6, st);
+}
+
+}  // namespace sagips
+
+extern "C" {
+
+sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  if (ctx->have_step && step <= ctx->last_step) return fail(ctx, SAGIPS_ERR_STATE, "steps must increase");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ctx->cfg.phase_timing) {
+    if (!ctx->pev[0][0])
+      for (auto& row : ctx->pev)
+        for (auto& e : row) CK(cudaEventCreate(&e));
+    ctx->pslot = (int)(ctx->timed_steps % sagips_ctx::kTimingRing);
+  }
+  local_step(ctx, step, st);
+  CK(cudaGetLastError());
+  ctx->have_step = true;
+  ctx->last_step = step;
+  ctx->pushed = false;
+  ctx->local_done_step = step;
+  if (flags & SAGIPS_STEP_LOCAL_ONLY) {
+    mark(ctx, 7, st);
+    if (ctx->cfg.phase_timing) ctx->timed_steps++;
+    return SAGIPS_OK;
+  }
+  sagips_status s = sagips_push_generator_grad(ctx, step, stream);
+  if (s != SAGIPS_OK) return s;
+  if (flags & SAGIPS_STEP_NO_ADAM_G) {
+    ctx->skip_adam_once = true;
+  }
+  return sagips_pull_generator_grad(ctx, step, stream);
+}
+
+sagips_status sagips_push_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  if (!ctx->have_step || ctx->local_done_step != step) return fail(ctx, SAGIPS_ERR_STATE, "push before train_step");
+  sagips_status s = exchange_push(ctx, step, (cudaStream_t)stream);
+  if (s != SAGIPS_OK) return s;
+  ctx->pushed = true;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_pull_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  if (!ctx->pushed || ctx->local_done_step != step) return fail(ctx, SAGIPS_ERR_STATE, "pull before push");
+  cudaStream_t st = (cudaStream_t)stream;
+  sagips_status s = exchange_pull(ctx, step, st);
+  if (s != SAGIPS_OK) return s;
+  if (ctx->skip_adam_once) {
+    ctx->skip_adam_once = false;
+  } else {
+    adam_gen(ctx, st);
+  }
+  mark(ctx, 7, st);
+  if (ctx->cfg.phase_timing) ctx->timed_steps++;
+  ctx->pushed = false;
+  CK(cudaGetLastError());
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_phase_times(sagips_ctx* ctx, float* host_ms, int32_t n, int32_t* steps_averaged) {
+  if (!ctx || !host_ms || n < SAGIPS_NUM_PHASES) return SAGIPS_ERR_INVALID_ARG;
+  if (!ctx->cfg.phase_timing || ctx->timed_steps == 0) return fail(ctx, SAGIPS_ERR_STATE, "no timed steps");
+  CK(cudaDeviceSynchronize());
+  const int cnt = (int)std::min<int64_t>(ctx->timed_steps, sagips_ctx::kTimingRing);
+  double acc[SAGIPS_NUM_PHASES] = {};
+  for (int s = 0; s < cnt; ++s)
+    for (int p = 0; p < SAGIPS_NUM_PHASES; ++p) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->pev[s][p], ctx->pev[s][p + 1]));
+      acc[p] += ms;
+    }
+  for (int p = 0; p < SAGIPS_NUM_PHASES; ++p) host_ms[p] = (float)(acc[p] / cnt);
+  if (steps_averaged) *steps_averaged = cnt;
+  return SAGIPS_OK;
+}
+
+static bool tensor_ref(sagips_ctx* c, int32_t which, void** p, size_t* bytes) {
+  const auto& g = c->cfg;
+  const int64_t k = g.param_samples, N = c->N;
+  const int64_t hb = 4 * (g.hist_bins + 2);
+  switch (which) {
+    case SAGIPS_T_GEN_W: *p = c->gW; *bytes = 4 * c->G.nw; return true;
+    case SAGIPS_T_GEN_B: *p = c->gB; *bytes = 4 * c->G.nb; return true;
+    case SAGIPS_T_DISC_W: *p = c->dW; *bytes = 4 * c->D.nw; return true;
+    case SAGIPS_T_DISC_B: *p = c->dB; *bytes = 4 * c->D.nb; return true;
+    case SAGIPS_T_GEN_ADAM: *p = nullptr; *bytes = 4 * 2 * (c->G.nw + c->G.nb); return true;
+    case SAGIPS_T_DISC_ADAM: *p = nullptr; *bytes = 4 * 2 * (c->D.nw + c->D.nb); return true;
+    case SAGIPS_T_NOISE: *p = c->noise; *bytes = 4 * k * g.noise_dim; return true;
+    case SAGIPS_T_RAW: *p = c->gAct[c->G.L - 1]; *bytes = 4 * 6 * k; return true;
+    case SAGIPS_T_C: *p = c->cbuf; *bytes = 4 * 6 * k; return true;
+    case SAGIPS_T_EVENTS: *p = c->X; *bytes = 4 * 4 * N; return true;
+    case SAGIPS_T_REAL_IDX: *p = c->real_idx; *bytes = 4 * N; return true;
+    case SAGIPS_T_HIST: *p = c->hist; *bytes = 4 * hb; return true;
+    case SAGIPS_T_LOGITS_D: *p = c->logits_d; *bytes = 4 * 2 * N; return true;
+    case SAGIPS_T_LOGITS_G: *p = c->logits_g; *bytes = 4 * N; return true;
+    case SAGIPS_T_DY: *p = c->dy; *bytes = 4 * 2 * N; return true;
+    case SAGIPS_T_DRAW: *p = c->draw; *bytes = 4 * 6 * k; return true;
+    case SAGIPS_T_GEN_DW: *p = c->g_dW; *bytes = 4 * c->G.nw; return true;
+    case SAGIPS_T_GEN_DB: *p = c->g_dB; *bytes = 4 * c->G.nb; return true;
+    case SAGIPS_T_DISC_DW: *p = c->d_dW; *bytes = 4 * c->D.nw; return true;
+    case SAGIPS_T_DISC_DB: *p = c->d_dB; *bytes = 4 * c->D.nb; return true;
+    case SAGIPS_T_REDUCED: *p = c->reduced; *bytes = 4 * c->G.nw; return true;
+    case SAGIPS_T_STATS: *p = c->stats; *bytes = sizeof(sagips_step_stats); return true;
+    case SAGIPS_T_REFERENCE: *p = c->ref; *bytes = 4 * 2 * g.reference_rows; return true;
+    case SAGIPS_T_SHARD: *p = c->shard; *bytes = 4 * 2 * g.shard_rows; return true;
+    default: return false;
+  }
+}
+
+sagips_status sagips_tensor_bytes(const sagips_ctx* ctx, int32_t which, size_t* bytes) {
+  if (!ctx || !bytes) return SAGIPS_ERR_INVALID_ARG;
+  void* p;
+  return tensor_ref(const_cast<sagips_ctx*>(ctx), which, &p, bytes) ? SAGIPS_OK : SAGIPS_ERR_INVALID_ARG;
+}
+
+static sagips_status copy_adam(sagips_ctx* ctx, bool gen, void* host, bool to_host) {
+  const MlpLayout& L = gen ? ctx->G : ctx->D;
+  float* segs[4] = {gen ? ctx->gmW : ctx->dmW, gen ? ctx->gvW : ctx->dvW, gen ? ctx->gmB : ctx->dmB,
+                    gen ? ctx->gvB : ctx->dvB};
+  int64_t n[4] = {L.nw, L.nw, L.nb, L.nb};
+  char* h = (char*)host;
+  for (int i = 0; i < 4; ++i) {
+    CK(to_host ? cudaMemcpy(h, segs[i], 4 * n[i], cudaMemcpyDeviceToHost)
+               : cudaMemcpy(segs[i], h, 4 * n[i], cudaMemcpyHostToDevice));
+    h += 4 * n[i];
+  }
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_get(sagips_ctx* ctx, int32_t which, void* host, size_t bytes) {
+  if (!ctx || !host) return SAGIPS_ERR_INVALID_ARG;
+  void* p;
+  size_t nb;
+  if (!tensor_ref(ctx, which, &p, &nb) || nb != bytes)
+    return fail(ctx, SAGIPS_ERR_INVALID_ARG, "tensor %d: size %zu != %zu", which, bytes, nb);
+  CK(cudaDeviceSynchronize());
+  if (which == SAGIPS_T_GEN_ADAM || which == SAGIPS_T_DISC_ADAM) return copy_adam(ctx, which == SAGIPS_T_GEN_ADAM, host, true);
+  CK(cudaMemcpy(host, p, bytes, cudaMemcpyDeviceToHost));
+  if (which == SAGIPS_T_STATS) {
+    auto* s = reinterpret_cast<sagips_step_stats*>(host);
+    s->step = ctx->last_step;
+    if (s->nonfinite) return fail(ctx, SAGIPS_ERR_NONFINITE, "non-finite loss");
+  }
+  return exchange_check(ctx);
+}
+
+sagips_status sagips_set(sagips_ctx* ctx, int32_t which, const void* host, size_t bytes) {
+  if (!ctx || !host) return SAGIPS_ERR_INVALID_ARG;
+  void* p;
+  size_t nb;
+  if (!tensor_ref(ctx, which, &p, &nb) || nb != bytes)
+    return fail(ctx, SAGIPS_ERR_INVALID_ARG, "tensor %d: size %zu != %zu", which, bytes, nb);
+  CK(cudaDeviceSynchronize());
+  if (which == SAGIPS_T_GEN_ADAM || which == SAGIPS_T_DISC_ADAM)
+    return copy_adam(ctx, which == SAGIPS_T_GEN_ADAM, const_cast<void*>(host), false);
+  CK(cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice));
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_launch_count(const sagips_ctx* ctx, uint64_t* count) {
+  if (!count) return SAGIPS_ERR_INVALID_ARG;
+  *count = launches_total() - (ctx ? ctx->launch_base : 0);
+  return SAGIPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,210 @@
+"""GPU-vs-oracle parity of libsagips on one B200 (through the C ABI).
+
+Tolerances (from BASELINE.json north_star): bit-exact
+RNG counters, bootstrap indices, histogram counts and reference / shard
+rows; 1e-5 relative for fp32 events and losses; 1e-3 relative (with the R24
+floor) for fp32 gradients; parameters after one Adam step within 2 lr."""
+import numpy as np
+import pytest
+
+from oracle import exchange as xc
+from oracle import gan, mlp, proxy
+from oracle import philox as px
+from tests import inputs
+from tests.gpu_util import assert_grad_close, assert_rel, flat, lib, oracle_config, sync_params
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.init()
+
+
+def _stream():
+    import ctypes
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def make_ctx(cfg):
+    from paper_2407_00051_b200 import runtime
+    return runtime.make_context(cfg)
+
+
+# ---------------------------------------------------------------- sampler
+@pytest.mark.parametrize("k,m", [(1, 1), (3, 5), (64, 16), (7, 1023), (1024, 1024)])
+def test_sample_events_parity(k, m):
+    L = lib()
+    seed, step, rank = 0xC0FFEE12345678, 123457, 3
+    c32 = inputs.coefficients(k * 31 + m, k).astype(np.float32)
+    c_t = torch.tensor(c32, device="cuda")
+    ev = torch.empty(k * m * 2, dtype=torch.float32, device="cuda")
+    bins = 64
+    hist = torch.zeros(2 * (bins + 2), dtype=torch.int32, device="cuda")
+    L.sample_events(c_t.data_ptr(), k, m, seed, step, rank, px.STREAM_FAKE, ev.data_ptr(), hist.data_ptr(), bins,
+                    (0.0, 0.0), (4.0, 4.0), _stream())
+    torch.cuda.synchronize()
+    y_gpu = ev.cpu().numpy().reshape(-1, 2)
+    u = proxy.fake_uniforms(seed, step, rank, k * m)
+    y32 = proxy.sample_events_f32(c32, m, u)
+    assert np.array_equal(y_gpu, y32)                       # same fp32 operations -> bit-exact
+    assert_rel(y_gpu, proxy.sample_events(c32.astype(np.float64), m, u), 1e-5, 1e-6, "events vs fp64")
+    h = hist.cpu().numpy().astype(np.int64).reshape(2, bins + 2)
+    for o in range(2):
+        assert np.array_equal(h[o], proxy.histogram_f32(y32[:, o], 0.0, 4.0, bins))
+
+
+def test_sample_events_rejects_bad_args():
+    L = lib()
+    with pytest.raises(L.SagipsError):
+        L.sample_events(None, 1, 1, 0, 0, 0, 5, None)
+
+
+# ---------------------------------------------------------------- init
+@pytest.mark.parametrize("preset,kw", [(0, {}), (1, dict(param_samples=16, events_per_sample=61))])
+def test_create_matches_oracle_init(preset, kw):
+    L = lib()
+    cfg = L.config_init(preset, rank=0, **kw)
+    cfg.reference_rows = 2 * cfg.param_samples * cfg.events_per_sample + 7   # ragged
+    cfg.shard_rows = cfg.param_samples * cfg.events_per_sample + 3
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, 0)
+    ref32 = proxy.make_reference_f32(ocfg.seed, ocfg.true_params, ocfg.reference_rows)
+    assert np.array_equal(ctx.get(L.T_REFERENCE).reshape(-1, 2), ref32)
+    assert np.array_equal(ctx.get(L.T_SHARD).reshape(-1, 2), st.shard32)
+    for which, ws in ((L.T_GEN_W, st.gW), (L.T_DISC_W, st.dW)):
+        assert_rel(ctx.get(which), flat(ws), 2e-5, 2e-6, "kaiming init")
+    assert np.all(ctx.get(L.T_GEN_B) == 0) and np.all(ctx.get(L.T_DISC_B) == 0)
+
+
+# ---------------------------------------------------------------- one step
+def _check_step(cfg, t=0):
+    L = lib()
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, cfg.rank)
+    sync_params(ctx, st)
+    d_before = flat(st.dW).copy()
+    ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
+    out = gan.local_step(ocfg, st, t)
+    N = ocfg.n_events
+    stats = ctx.get(L.T_STATS)
+    assert stats.nonfinite == 0
+    assert_rel(ctx.get(L.T_NOISE), out["z"].reshape(-1), 1e-5, 1e-6, "noise")
+    assert_rel(ctx.get(L.T_RAW), out["raw"].reshape(-1), 1e-5, 1e-5, "raw")
+    assert np.array_equal(ctx.get(L.T_REAL_IDX), out["real_idx"].astype(np.uint32))   # bootstrap indices
+    ev = ctx.get(L.T_EVENTS).reshape(-1, 2)
+    assert np.array_equal(ev[:N], st.shard32[out["real_idx"]])                           # real rows exact
+    assert_rel(ev[N:], out["y"], 1e-5, 1e-5, "fake events")
+    hist = ctx.get(L.T_HIST).astype(np.int64).reshape(2, 2, -1)
+    assert np.array_equal(hist[0], out["hist"][0])                                       # real hist exact
+    assert np.abs(hist[1] - out["hist"][1]).sum() <= max(4, N // 20000)                   # R22: ULP edges
+    assert_rel(ctx.get(L.T_LOGITS_D), out["logits_d"], 1e-4, 1e-4, "D logits")
+    assert stats.loss_d == pytest.approx(out["loss_d"], rel=1e-5)
+    assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
+    assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
+    # one Adam step moves each parameter by at most ~lr; allow 2 lr
+    assert np.max(np.abs(ctx.get(L.T_DISC_W) - flat(st.dW))) <= 2.0 * ocfg.disc_lr + 1e-6
+    assert np.max(np.abs(ctx.get(L.T_DISC_W) - d_before)) > 0
+    assert stats.loss_g == pytest.approx(out["loss_g"], rel=1e-5)
+    assert_rel(ctx.get(L.T_LOGITS_G), out["logits_g"], 1e-4, 1e-4, "G logits")
+    assert_grad_close(ctx.get(L.T_DY), out["dy"], 1e-3, "dy")
+    assert_grad_close(ctx.get(L.T_DRAW), out["draw"], 1e-3, "draw")
+    assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
+    assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G")
+    return ctx, st, out
+
+
+def test_step_desk():
+    _check_step(lib().config_init(0, seed=5))
+
+
+def test_step_paper_widths_ragged():
+    # paper widths, 2N = 7,808 rows (ragged 128-row tiles), step 3, rank 1
+    L = lib()
+    _check_step(L.config_init(1, seed=9, param_samples=64, events_per_sample=61, world=2, rank=1, group_size=2), t=3)
+
+
+def test_full_step_applies_generator_update():
+    L = lib()
+    cfg = L.config_init(0, seed=11)
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, 0)
+    sync_params(ctx, st)
+    ctx.train_step(0, 0, _stream())
+    out = gan.local_step(ocfg, st, 0)
+    gan.apply_generator(ocfg, st, out["packet"], out["db_g"])
+    assert_grad_close(ctx.get(L.T_REDUCED), out["packet"], 1e-3, "reduced (mode NONE)")
+    assert np.max(np.abs(ctx.get(L.T_GEN_W) - flat(st.gW))) <= 2.0 * ocfg.gen_lr + 1e-7
+    assert np.max(np.abs(ctx.get(L.T_GEN_B) - flat(st.gb))) <= 2.0 * ocfg.gen_lr + 1e-7
+
+
+def test_loss_curves_200_steps_desk():
+    """C1: 200 steps; 10-step moving averages of L_D and L_G within 2% (R25)."""
+    L = lib()
+    cfg = L.config_init(0, seed=3)
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, 0)
+    sync_params(ctx, st)
+    gl, ol = [], []
+    for t in range(200):
+        ctx.train_step(t, 0, _stream())
+        s = ctx.get(L.T_STATS)
+        gl.append((s.loss_d, s.loss_g))
+        o = gan.local_step(ocfg, st, t)
+        gan.apply_generator(ocfg, st, o["packet"], o["db_g"])
+        ol.append((o["loss_d"], o["loss_g"]))
+    g = np.array(gl)
+    o = np.array(ol)
+    kern = np.ones(10) / 10
+    for j in range(2):
+        gm = np.convolve(g[:, j], kern, mode="valid")
+        om = np.convolve(o[:, j], kern, mode="valid")
+        assert np.max(np.abs(gm - om) / np.abs(om)) < 0.02
+
+
+def test_step_order_and_exchange_state_errors():
+    L = lib()
+    ctx = make_ctx(L.config_init(0))
+    ctx.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    with pytest.raises(L.SagipsError) as e:
+        ctx.pull_generator_grad(0, _stream())
+    assert e.value.status == 6
+    ctx.push_generator_grad(0, _stream())
+    ctx.pull_generator_grad(0, _stream())
+    with pytest.raises(L.SagipsError) as e:
+        ctx.train_step(0, 0, _stream())
+    assert e.value.status == 6
+
+
+def test_full_size_paper_step_sampled():
+    """C2 at full size (k = m = 1024, 2N = 2^21 rows) in the launch
+    configuration bench.py times: both losses, the histograms and sampled
+    events / indices against the oracle."""
+    L = lib()
+    cfg = L.config_init(1, seed=2)
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, 0)
+    sync_params(ctx, st)
+    ctx.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    out = gan.local_step(ocfg, st, 0)
+    N = ocfg.n_events
+    s = ctx.get(L.T_STATS)
+    assert s.loss_d == pytest.approx(out["loss_d"], rel=1e-5)
+    assert s.loss_g == pytest.approx(out["loss_g"], rel=1e-5)
+    idx = inputs.sample_indices(1, N, 4096)
+    ev = ctx.get(L.T_EVENTS).reshape(-1, 2)
+    assert np.array_equal(ctx.get(L.T_REAL_IDX)[idx], out["real_idx"][idx].astype(np.uint32))
+    assert_rel(ev[N + idx], out["y"][idx], 1e-5, 1e-5, "fake events (sampled)")
+    hist = ctx.get(L.T_HIST).astype(np.int64).reshape(2, 2, -1)
+    assert np.array_equal(hist[0], out["hist"][0])
+    assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
+    assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
