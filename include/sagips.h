@@ -71,6 +71,12 @@ typedef enum {
 } sagips_precision;
 
 typedef enum {
+  SAGIPS_DISC_AUTO = 0,     /* tcgen05 for 128-wide hidden layers, else CUDA-core fp32 */
+  SAGIPS_DISC_SIMT = 1,     /* CUDA-core FFMA everywhere (fp32 only) */
+  SAGIPS_DISC_TCGEN05 = 2   /* tcgen05 (requires disc_hidden == 128); FP32 precision runs bf16x3 */
+} sagips_disc_impl;
+
+typedef enum {
   SAGIPS_PRESET_DESK = 0,  /* C1: G [8,64,64,6], D [2,64,64,1], k=64, m=16 */
   SAGIPS_PRESET_PAPER = 1  /* C2: G [6,128x4,6], D [2,128x4,1] (51,206 / 50,049 params), k=1024, m=1024 */
 } sagips_preset;
@@ -106,7 +112,8 @@ typedef struct {
   uint64_t seed;              /* Philox key (R-RNG) */
   int32_t exchange_timeout_ms;/* bound on every exchange wait (0 = 10000) */
   int32_t phase_timing;       /* 1: record CUDA events at the phase boundaries of every step */
-  int32_t reserved[6];
+  int32_t disc_impl;          /* sagips_disc_impl: kernels of the discriminator hidden layers */
+  int32_t reserved[5];
 } sagips_config;
 
 typedef struct sagips_ctx sagips_ctx;

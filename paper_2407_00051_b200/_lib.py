@@ -16,6 +16,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "CUDA", 4: "NONFINITE", 5: 
 
 MODE_NONE, MODE_ARAR, MODE_ARAR_ARAR, MODE_RMA_ARAR_ARAR, MODE_SYNC_ALLREDUCE = range(5)
 PREC_FP32, PREC_BF16 = 0, 1
+DISC_AUTO, DISC_SIMT, DISC_TCGEN05 = 0, 1, 2
 PRESET_DESK, PRESET_PAPER = 0, 1
 STEP_LOCAL_ONLY, STEP_NO_ADAM_G = 1, 2
 IPC_HANDLE_BYTES = 64
@@ -49,7 +50,7 @@ class Config(ctypes.Structure):
         ("hist_bins", ctypes.c_int32), ("hist_lo", ctypes.c_float * 2), ("hist_hi", ctypes.c_float * 2),
         ("seed", ctypes.c_uint64),
         ("exchange_timeout_ms", ctypes.c_int32), ("phase_timing", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 6),
+        ("disc_impl", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5),
     ]
 
 

@@ -58,6 +58,7 @@ struct sagips_ctx {
   sagips_step_stats* stats = nullptr;
   // step bookkeeping
   int64_t g_tau = 0, d_tau = 0;
+  bool use_tc = false;  // discriminator 128 -> 128 layers on tcgen05
   bool have_step = false;
   uint64_t last_step = 0;
   uint64_t local_done_step = ~0ull;
@@ -86,10 +87,4 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st);
 sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st);
 sagips_status exchange_check(sagips_ctx* c);
 void exchange_destroy(sagips_ctx* c);
-// k_disc_tc.cu (bf16 tcgen05 discriminator)
-bool tc_disc_supported(const sagips_config* cfg);
-sagips_status tc_disc_init(sagips_ctx* c);
-void tc_disc_destroy(sagips_ctx* c);
-void tc_disc_step(sagips_ctx* c, cudaStream_t st);
-void tc_gen_loss(sagips_ctx* c, cudaStream_t st);
 }  // namespace sagips

@@ -62,6 +62,13 @@ void launch_head(const float* H, int M, int hd, const float* w, const float* b, 
 void launch_finish_loss(const double* loss_part, int nparts, double scale, float* out, uint32_t* nonfinite,
                         cudaStream_t st);
 
+// k_tc_gemm.cu (tcgen05, 128 -> 128 layers)
+void launch_tc_rows(bool split, bool dgrad, const float* A, const float* W, float* C, int64_t rows, int epi,
+                    const float* bias, const float* Hprev, float alpha, cudaStream_t st);
+int tc_wgrad_grid();
+void launch_tc_wgrad(bool split, const float* dZ, const float* H, int64_t rows, float* part, float* part_db,
+                     cudaStream_t st);
+
 // k_adam.cu
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,
                  double b2, double eps, cudaStream_t st);

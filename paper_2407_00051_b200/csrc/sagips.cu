@@ -148,6 +148,10 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
     if (!(g->true_params[3 * o + 1] > 0.f) || !(g->true_params[3 * o + 2] > 0.f))
       return bad("true c1, c2 must be > 0 (softplus range)");
   if (g->hist_bins < 1 || g->hist_bins > 4096) return bad("hist_bins in [1, 4096]");
+  if (g->disc_impl < SAGIPS_DISC_AUTO || g->disc_impl > SAGIPS_DISC_TCGEN05) return bad("unknown disc_impl");
+  if (g->disc_impl == SAGIPS_DISC_TCGEN05 && hd != 128) return bad("tcgen05 layers need disc_hidden == 128");
+  if (g->precision == SAGIPS_PREC_BF16 && (hd != 128 || g->disc_impl == SAGIPS_DISC_SIMT))
+    return bad("BF16 precision runs on tcgen05 (disc_hidden == 128, disc_impl != SIMT)");
   for (int o = 0; o < 2; ++o)
     if (!(g->hist_hi[o] > g->hist_lo[o])) return bad("hist_hi must exceed hist_lo");
   return SAGIPS_OK;
@@ -219,11 +223,11 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
     fprintf(stderr, "sagips_create: %s\n", why.c_str());
     return s;
   }
-  if (cfg->precision == SAGIPS_PREC_BF16 && !tc_disc_supported(cfg)) return SAGIPS_ERR_UNSUPPORTED;
   sagips_ctx* ctx = new sagips_ctx();
   ctx->cfg = *cfg;
   if (ctx->cfg.exchange_timeout_ms <= 0) ctx->cfg.exchange_timeout_ms = 10000;
   setup_dims(ctx);
+  ctx->use_tc = ctx->cfg.disc_impl != SAGIPS_DISC_SIMT && ctx->cfg.disc_hidden == 128;
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
   carve(ctx, base);
   if ((size_t)(base - (char*)workspace) + ctx->ws_bytes > workspace_bytes) {
@@ -265,10 +269,6 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
     delete ctx;
     return bail(SAGIPS_ERR_CUDA);
   }
-  if (g.precision == SAGIPS_PREC_BF16) {
-    sagips_status r = tc_disc_init(ctx);
-    if (r != SAGIPS_OK) { delete ctx; return bail(r); }
-  }
   *out = ctx;
   return SAGIPS_OK;
 }
@@ -276,7 +276,6 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
 sagips_status sagips_destroy(sagips_ctx* ctx) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
   exchange_destroy(ctx);
-  tc_disc_destroy(ctx);
   for (auto& row : ctx->pev)
     for (auto& e : row)
       if (e) cudaEventDestroy(e);
@@ -300,14 +299,26 @@ sagips_status sagips_sample_events(const float* c, int32_t k, int32_t m, uint64_
 // ---------------------------------------------------------------- the step
 namespace sagips {
 
+// A 128 -> 128 discriminator layer runs on the tensor cores (tcgen05) unless
+// disc_impl == SIMT; FP32 precision uses the bf16x3 split (fp32-class).
+static bool tc_layer(const sagips_ctx* c, int l) {
+  return c->use_tc && c->D.sizes[l] == 128 && c->D.sizes[l + 1] == 128;
+}
+static bool tc_split(const sagips_ctx* c) { return c->cfg.precision == SAGIPS_PREC_FP32; }
+
 // Hidden layers of the discriminator on `rows` rows of X -> dAct[0..L-2].
-static void disc_hidden_forward_simt(sagips_ctx* c, const float* X, int rows, cudaStream_t st) {
+static void disc_hidden_forward(sagips_ctx* c, const float* X, int rows, cudaStream_t st) {
   const auto& D = c->D;
   const float* in = X;
   for (int l = 0; l < D.L - 1; ++l) {
-    Epi ep{EPI_BIAS_ACT, c->dB + D.b_off[l], 1, c->cfg.leaky_slope, nullptr, 0};
-    launch_gemm(false, true, rows, D.sizes[l + 1], D.sizes[l], in, D.sizes[l], c->dW + D.w_off[l], D.sizes[l],
-                c->dAct[l], D.sizes[l + 1], ep, 1, 0, st);
+    if (tc_layer(c, l)) {
+      launch_tc_rows(tc_split(c), false, in, c->dW + D.w_off[l], c->dAct[l], rows, EPI_BIAS_ACT, c->dB + D.b_off[l],
+                     nullptr, c->cfg.leaky_slope, st);
+    } else {
+      Epi ep{EPI_BIAS_ACT, c->dB + D.b_off[l], 1, c->cfg.leaky_slope, nullptr, 0};
+      launch_gemm(false, true, rows, D.sizes[l + 1], D.sizes[l], in, D.sizes[l], c->dW + D.w_off[l], D.sizes[l],
+                  c->dAct[l], D.sizes[l + 1], ep, 1, 0, st);
+    }
     in = c->dAct[l];
   }
 }
@@ -324,14 +335,38 @@ static void layer_wgrad(sagips_ctx* c, const float* dZ, const float* Hin, int ro
   launch_reduce_parts(c->colpart, S2, out, db, 1.0f, st);
 }
 
-static void disc_step_simt(sagips_ctx* c, cudaStream_t st) {
+static void disc_layer_wgrad(sagips_ctx* c, int l, const float* dZ, const float* Hin, int rows, cudaStream_t st) {
+  const auto& D = c->D;
+  if (tc_layer(c, l)) {
+    launch_tc_wgrad(tc_split(c), dZ, Hin, rows, c->part, c->colpart, st);
+    launch_reduce_parts(c->part, tc_wgrad_grid(), 128 * 128, c->d_dW + D.w_off[l], 1.0f, st);
+    launch_reduce_parts(c->colpart, tc_wgrad_grid(), 128, c->d_dB + D.b_off[l], 1.0f, st);
+  } else {
+    layer_wgrad(c, dZ, Hin, rows, D.sizes[l + 1], D.sizes[l], c->d_dW + D.w_off[l], c->d_dB + D.b_off[l], st);
+  }
+}
+
+// dZ_{l-1} = (dZ_l W_l) * LeakyReLU'(H_{l-1})
+static void disc_layer_dgrad(sagips_ctx* c, int l, const float* dZ, float* out_dZ, int rows, cudaStream_t st) {
+  const auto& D = c->D;
+  const int out = D.sizes[l + 1], in = D.sizes[l];
+  if (tc_layer(c, l)) {
+    launch_tc_rows(tc_split(c), true, dZ, c->dW + D.w_off[l], out_dZ, rows, EPI_ACT_GRAD, nullptr, c->dAct[l - 1],
+                   c->cfg.leaky_slope, st);
+  } else {
+    Epi ep{EPI_ACT_GRAD, nullptr, 0, c->cfg.leaky_slope, c->dAct[l - 1], in};
+    launch_gemm(false, false, rows, in, out, dZ, out, c->dW + D.w_off[l], in, out_dZ, in, ep, 1, 0, st);
+  }
+}
+
+static void disc_step(sagips_ctx* c, cudaStream_t st) {
   const auto& D = c->D;
   const int N = (int)c->N;
   const int rows = 2 * N;
   const float a = c->cfg.leaky_slope;
   const int Lh = D.L - 1;  // index of the head layer
   const int hd = D.sizes[Lh];
-  disc_hidden_forward_simt(c, c->X, rows, st);
+  disc_hidden_forward(c, c->X, rows, st);
   // head: logits, BCE (labels: real rows 1, fake rows 0; mean over 2N), dz
   launch_head(c->dAct[Lh - 1], rows, hd, c->dW + D.w_off[Lh], c->dB + D.b_off[Lh], N, 0.0f, 1.0f / (float)rows, a,
               c->logits_d, c->dZb[0], c->part, c->loss_part, true, st);
@@ -342,25 +377,22 @@ static void disc_step_simt(sagips_ctx* c, cudaStream_t st) {
   int cur = 0;
   for (int l = Lh - 1; l >= 0; --l) {
     const float* Hin = (l == 0) ? c->X : c->dAct[l - 1];
-    const int out = D.sizes[l + 1], in = D.sizes[l];
-    layer_wgrad(c, c->dZb[cur], Hin, rows, out, in, c->d_dW + D.w_off[l], c->d_dB + D.b_off[l], st);
+    disc_layer_wgrad(c, l, c->dZb[cur], Hin, rows, st);
     if (l > 0) {
-      Epi ep{EPI_ACT_GRAD, nullptr, 0, a, c->dAct[l - 1], in};
-      launch_gemm(false, false, rows, in, out, c->dZb[cur], out, c->dW + D.w_off[l], in, c->dZb[cur ^ 1], in, ep, 1,
-                  0, st);
+      disc_layer_dgrad(c, l, c->dZb[cur], c->dZb[cur ^ 1], rows, st);
       cur ^= 1;
     }
   }
 }
 
-static void gen_loss_through_disc_simt(sagips_ctx* c, cudaStream_t st) {
+static void gen_loss_through_disc(sagips_ctx* c, cudaStream_t st) {
   const auto& D = c->D;
   const int N = (int)c->N;
   const float a = c->cfg.leaky_slope;
   const int Lh = D.L - 1;
   const int hd = D.sizes[Lh];
   const float* Y = c->X + 2 * (int64_t)N;  // fake rows
-  disc_hidden_forward_simt(c, Y, N, st);
+  disc_hidden_forward(c, Y, N, st);
   // non-saturating generator loss: label 1 on fake rows, mean over N
   launch_head(c->dAct[Lh - 1], N, hd, c->dW + D.w_off[Lh], c->dB + D.b_off[Lh], 0, 1.0f, 1.0f / (float)N, a,
               c->logits_g, c->dZb[0], c->part, c->loss_part, false, st);
@@ -369,9 +401,7 @@ static void gen_loss_through_disc_simt(sagips_ctx* c, cudaStream_t st) {
   for (int l = Lh - 1; l >= 0; --l) {
     const int out = D.sizes[l + 1], in = D.sizes[l];
     if (l > 0) {
-      Epi ep{EPI_ACT_GRAD, nullptr, 0, a, c->dAct[l - 1], in};
-      launch_gemm(false, false, N, in, out, c->dZb[cur], out, c->dW + D.w_off[l], in, c->dZb[cur ^ 1], in, ep, 1, 0,
-                  st);
+      disc_layer_dgrad(c, l, c->dZb[cur], c->dZb[cur ^ 1], N, st);
       cur ^= 1;
     } else {
       Epi ep{EPI_STORE, nullptr, 0, 0.f, nullptr, 0};
@@ -420,17 +450,10 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
                      g.hist_bins, g.hist_lo, g.hist_hi, st);
   mark(c, 2, st);
   // a7 discriminator step + Adam(D) ; a8 generator loss through the updated D
-  if (g.precision == SAGIPS_PREC_BF16) {
-    tc_disc_step(c, st);
-    adam_disc(c, st);
-    mark(c, 3, st);
-    tc_gen_loss(c, st);
-  } else {
-    disc_step_simt(c, st);
-    adam_disc(c, st);
-    mark(c, 3, st);
-    gen_loss_through_disc_simt(c, st);
-  }
+  disc_step(c, st);
+  adam_disc(c, st);
+  mark(c, 3, st);
+  gen_loss_through_disc(c, st);
   mark(c, 4, st);
   // a9 sampler backward
   launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st);

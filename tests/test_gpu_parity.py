@@ -124,10 +124,34 @@ def test_step_desk():
     _check_step(lib().config_init(0, seed=5))
 
 
-def test_step_paper_widths_ragged():
-    # paper widths, 2N = 7,808 rows (ragged 128-row tiles), step 3, rank 1
+@pytest.mark.parametrize("impl", [0, 1])
+def test_step_paper_widths_ragged(impl):
+    """paper widths, 2N = 7,808 rows (ragged 128-row tiles), step 3, rank 1;
+    impl 0 = tcgen05 bf16x3 hidden layers, 1 = CUDA-core fp32."""
     L = lib()
-    _check_step(L.config_init(1, seed=9, param_samples=64, events_per_sample=61, world=2, rank=1, group_size=2), t=3)
+    _check_step(L.config_init(1, seed=9, param_samples=64, events_per_sample=61, world=2, rank=1, group_size=2,
+                              disc_impl=impl), t=3)
+
+
+def test_bf16_step_within_bf16_tolerances():
+    """SAGIPS_PREC_BF16 (C5's precision): discriminator GEMMs in bf16 with fp32
+    accumulation.  Stated tolerances (Parity): losses within
+    5e-3 relative; every gradient tensor within 5e-2 in relative L2 norm."""
+    L = lib()
+    cfg = L.config_init(1, seed=4, param_samples=64, events_per_sample=64, precision=L.PREC_BF16)
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(ocfg, 0)
+    sync_params(ctx, st)
+    ctx.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    out = gan.local_step(ocfg, st, 0)
+    s = ctx.get(L.T_STATS)
+    assert s.loss_d == pytest.approx(out["loss_d"], rel=5e-3)
+    assert s.loss_g == pytest.approx(out["loss_g"], rel=5e-3)
+    for which, ref in ((L.T_DISC_DW, flat(out["dW_d"])), (L.T_DY, out["dy"]), (L.T_GEN_DW, out["packet"])):
+        g = ctx.get(which).astype(np.float64)
+        r = np.asarray(ref, dtype=np.float64).reshape(-1)
+        assert np.linalg.norm(g - r) <= 5e-2 * np.linalg.norm(r), which
 
 
 def test_full_step_applies_generator_update():
