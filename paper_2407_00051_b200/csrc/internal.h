@@ -13,6 +13,7 @@ namespace sagips {
 
 constexpr int kMaxLayers = 16;
 constexpr int kMaxWorld = 64;
+constexpr int kMaxSms = 256;  // bound on the persistent grids (B200: 148)
 
 void count_launch();
 uint64_t launches_total();

@@ -296,6 +296,7 @@ static int num_sms() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
+    g_num_sms = std::min(g_num_sms, kMaxSms);
   }
   return g_num_sms;
 }

@@ -94,9 +94,10 @@ static void carve(sagips_ctx* c, char* base) {
     pf = std::max<int64_t>(pf, (int64_t)wgrad_splits(D.sizes[l + 1], D.sizes[l], 2 * N) * D.sizes[l + 1] * D.sizes[l]);
   for (int l = 0; l < G.L; ++l)
     pf = std::max<int64_t>(pf, (int64_t)wgrad_splits(G.sizes[l + 1], G.sizes[l], k) * G.sizes[l + 1] * G.sizes[l]);
+  pf = std::max<int64_t>(pf, (int64_t)kMaxSms * 128 * 128);  // tcgen05 wgrad: one partial per CTA
   c->part = cv.take<float>(pf);
   c->part_floats = pf;
-  c->colpart = cv.take<float>(296 * std::max(D.maxw, G.maxw));
+  c->colpart = cv.take<float>(std::max(296, kMaxSms) * std::max(128, std::max(D.maxw, G.maxw)));
   c->head_tmp = cv.take<float>(D.maxw + 1);
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
