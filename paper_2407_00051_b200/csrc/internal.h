@@ -70,6 +70,52 @@ int tc_wgrad_grid();
 void launch_tc_wgrad(bool split, const float* dZ, const float* H, int64_t rows, float* part, float* part_db,
                      cudaStream_t st);
 
+// k_tc_layers.cu (warp-specialised tcgen05 layer passes, disc_depth >= 3)
+struct FwdLaunch {
+  const float* A = nullptr;   // input activation [rows][128] (mid, head)
+  const float* X = nullptr;   // [rows][2] (first)
+  const float* W0 = nullptr;  // [128][2] (first)
+  const float* b0 = nullptr;  // [128] (first)
+  const float* W = nullptr;   // [128][128]
+  const float* bias = nullptr;
+  float* C = nullptr;         // output activation (first, mid)
+  int64_t rows = 0;
+  float alpha = 0.01f;
+  const float* w_head = nullptr;
+  const float* b_head = nullptr;
+  int64_t n_real = 0;
+  float label_rest = 0.f;
+  float scale = 1.f;
+  float* logits = nullptr;
+  float* dZ = nullptr;
+  float* part_head = nullptr;
+  double* loss_part = nullptr;
+  int want_wgrad = 0;
+};
+struct BwdLaunch {
+  const float* dZ = nullptr;
+  const float* H = nullptr;
+  const float* X = nullptr;
+  const float* W0 = nullptr;
+  const float* b0 = nullptr;
+  const float* W = nullptr;
+  int64_t rows = 0;
+  float alpha = 0.01f;
+  float* dZout = nullptr;
+  float* dy = nullptr;
+  int want_wgrad = 0;
+  float* part = nullptr;
+  float* part_db = nullptr;
+};
+enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
+int tc_layers_grid(int64_t rows);
+void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st);
+void launch_tc_bwd(bool split, bool first, bool dy, const BwdLaunch& L, cudaStream_t st);
+int l0_grad_blocks();
+void launch_l0_grads(const float* dZ1, const float* X, int64_t rows, float* part, float* dW0, float* db0,
+                     cudaStream_t st);
+void launch_head_finish(const float* part, int nparts, float* dw, float* db, cudaStream_t st);
+
 // k_adam.cu
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,
                  double b2, double eps, cudaStream_t st);

@@ -360,7 +360,92 @@ static void disc_layer_dgrad(sagips_ctx* c, int l, const float* dZ, float* out_d
   }
 }
 
+// ---- warp-specialised tcgen05 layer passes (k_tc_layers.cu), depth >= 3.
+// Layer 0 is recomputed from X inside the first pass; the head + BCE is the
+// epilogue of the last hidden layer; dgrad and wgrad share one pass.
+static bool use_layers_v2(const sagips_ctx* c) { return c->use_tc && c->cfg.disc_depth >= 3; }
+
+static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
+                            float scale, float* logits, bool want_head_grad, cudaStream_t st) {
+  const auto& D = c->D;
+  const int Lh = D.L - 1;
+  const bool split = tc_split(c);
+  FwdLaunch f;
+  f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0];
+  f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.C = c->dAct[1];
+  f.rows = rows; f.alpha = c->cfg.leaky_slope;
+  launch_tc_fwd(split, FWD_FIRST, f, st);
+  for (int l = 2; l <= Lh - 2; ++l) {
+    FwdLaunch m;
+    m.A = c->dAct[l - 1]; m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l]; m.C = c->dAct[l];
+    m.rows = rows; m.alpha = c->cfg.leaky_slope;
+    launch_tc_fwd(split, FWD_MID, m, st);
+  }
+  FwdLaunch h;
+  h.A = c->dAct[Lh - 2]; h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
+  h.rows = rows; h.alpha = c->cfg.leaky_slope;
+  h.w_head = c->dW + D.w_off[Lh]; h.b_head = c->dB + D.b_off[Lh];
+  h.n_real = n_real; h.label_rest = label_rest; h.scale = scale;
+  h.logits = logits; h.dZ = c->dZb[0]; h.part_head = c->part; h.loss_part = c->loss_part;
+  h.want_wgrad = want_head_grad ? 1 : 0;
+  launch_tc_fwd(split, FWD_HEAD, h, st);
+}
+
+static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
+  const auto& D = c->D;
+  const int64_t N = c->N, rows = 2 * N;
+  const int Lh = D.L - 1;
+  const bool split = tc_split(c);
+  const int grid = tc_layers_grid(rows);
+  disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
+  launch_head_finish(c->part, grid, c->d_dW + D.w_off[Lh], c->d_dB + D.b_off[Lh], st);
+  launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
+  int cur = 0;
+  for (int l = Lh - 1; l >= 1; --l) {
+    BwdLaunch b;
+    b.dZ = c->dZb[cur]; b.W = c->dW + D.w_off[l]; b.rows = rows; b.alpha = c->cfg.leaky_slope;
+    b.dZout = c->dZb[cur ^ 1]; b.want_wgrad = 1; b.part = c->part; b.part_db = c->colpart;
+    if (l == 1) {
+      b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0];
+    } else {
+      b.H = c->dAct[l - 1];
+    }
+    launch_tc_bwd(split, l == 1, false, b, st);
+    launch_reduce_parts(c->part, grid, 128 * 128, c->d_dW + D.w_off[l], 1.0f, st);
+    launch_reduce_parts(c->colpart, grid, 128, c->d_dB + D.b_off[l], 1.0f, st);
+    cur ^= 1;
+  }
+  launch_l0_grads(c->dZb[cur], c->X, rows, c->part, c->d_dW + D.w_off[0], c->d_dB + D.b_off[0], st);
+}
+
+static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
+  const auto& D = c->D;
+  const int64_t N = c->N;
+  const int Lh = D.L - 1;
+  const bool split = tc_split(c);
+  const float* Y = c->X + 2 * N;  // fake rows
+  disc_forward_v2(c, Y, N, 0, 1.0f, 1.0f / (float)N, c->logits_g, false, st);
+  launch_finish_loss(c->loss_part, tc_layers_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
+  int cur = 0;
+  for (int l = Lh - 1; l >= 1; --l) {
+    BwdLaunch b;
+    b.dZ = c->dZb[cur]; b.W = c->dW + D.w_off[l]; b.rows = N; b.alpha = c->cfg.leaky_slope;
+    b.dZout = c->dZb[cur ^ 1]; b.want_wgrad = 0;
+    if (l == 1) {
+      b.X = Y; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.dy = c->dy;
+    } else {
+      b.H = c->dAct[l - 1];
+    }
+    launch_tc_bwd(split, l == 1, l == 1, b, st);
+    cur ^= 1;
+  }
+}
+
 static void disc_step(sagips_ctx* c, cudaStream_t st) {
+  if (use_layers_v2(c)) {
+    disc_step_v2(c, st);
+    return;
+  }
   const auto& D = c->D;
   const int N = (int)c->N;
   const int rows = 2 * N;
@@ -387,6 +472,10 @@ static void disc_step(sagips_ctx* c, cudaStream_t st) {
 }
 
 static void gen_loss_through_disc(sagips_ctx* c, cudaStream_t st) {
+  if (use_layers_v2(c)) {
+    gen_loss_v2(c, st);
+    return;
+  }
   const auto& D = c->D;
   const int N = (int)c->N;
   const float a = c->cfg.leaky_slope;

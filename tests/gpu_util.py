@@ -48,7 +48,7 @@ def sync_params(ctx, st):
         setattr(st, name, unflat(v.astype(np.float64), ws))
 
 
-def grad_close(gpu, ref, rel=1e-3):
+def grad_close(gpu, ref, rel=1e-3, extra=None):
     """|a - b| <= rel * max(|b|, 1e-2 * max|b|) elementwise (R24): entries
     that cancel to below 1% of the tensor's largest carry no 1e-3 relative
     information in fp32 -- a sum over R rows has error ~ sqrt(R) u sum|terms|;
@@ -57,13 +57,21 @@ def grad_close(gpu, ref, rel=1e-3):
     ref = np.asarray(ref, dtype=np.float64).reshape(-1)
     floor = 1e-2 * np.max(np.abs(ref)) if ref.size else 0.0
     tol = rel * np.maximum(np.abs(ref), floor)
+    if extra is not None:  # LeakyReLU kink ambiguity (tests/kink.py, R27)
+        tol = tol + np.asarray(extra, dtype=np.float64).reshape(-1)
     bad = np.abs(gpu - ref) > tol
     return (not bad.any()), int(bad.sum()), float(np.max(np.abs(gpu - ref) / np.maximum(tol, 1e-300)) * rel)
 
 
-def assert_grad_close(gpu, ref, rel=1e-3, what=""):
-    ok, nbad, worst = grad_close(gpu, ref, rel)
-    assert ok, f"{what}: {nbad} elements outside {rel} (worst scaled err {worst:.3g})"
+def assert_grad_close(gpu, ref, rel=1e-3, what="", extra=None):
+    ok, nbad, worst = grad_close(gpu, ref, rel, extra)
+    if not ok:
+        g = np.asarray(gpu, dtype=np.float64).reshape(-1)
+        r = np.asarray(ref, dtype=np.float64).reshape(-1)
+        order = np.argsort(-np.abs(g - r) / np.maximum(np.abs(r), 1e-2 * np.max(np.abs(r))))[:4]
+        detail = ", ".join(f"[{i}] gpu {g[i]:.6g} ref {r[i]:.6g}" for i in order)
+        raise AssertionError(f"{what}: {nbad} elements outside {rel} (worst scaled err {worst:.3g}; max|ref| "
+                             f"{np.max(np.abs(r)):.3g}): {detail}")
 
 
 def assert_rel(gpu, ref, rel, atol=0.0, what=""):

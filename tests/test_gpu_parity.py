@@ -10,7 +10,7 @@ import pytest
 from oracle import exchange as xc
 from oracle import gan, mlp, proxy
 from oracle import philox as px
-from tests import inputs
+from tests import inputs, kink
 from tests.gpu_util import assert_grad_close, assert_rel, flat, lib, oracle_config, sync_params
 
 pytestmark = pytest.mark.gpu
@@ -90,8 +90,11 @@ def _check_step(cfg, t=0):
     st = gan.RankState(ocfg, cfg.rank)
     sync_params(ctx, st)
     d_before = flat(st.dW).copy()
+    d_params0 = ([w.copy() for w in st.dW], [b.copy() for b in st.db])
+    g_params0 = ([w.copy() for w in st.gW], [b.copy() for b in st.gb])
     ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
     out = gan.local_step(ocfg, st, t)
+    kd = kink.step_deviation(ocfg, d_params0, (st.dW, st.db), g_params0, out)
     N = ocfg.n_events
     stats = ctx.get(L.T_STATS)
     assert stats.nonfinite == 0
@@ -106,17 +109,17 @@ def _check_step(cfg, t=0):
     assert np.abs(hist[1] - out["hist"][1]).sum() <= max(4, N // 20000)                   # R22: ULP edges
     assert_rel(ctx.get(L.T_LOGITS_D), out["logits_d"], 1e-4, 1e-4, "D logits")
     assert stats.loss_d == pytest.approx(out["loss_d"], rel=1e-5)
-    assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
-    assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
+    assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D", kd["dW_d"])
+    assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D", kd["db_d"])
     # one Adam step moves each parameter by at most ~lr; allow 2 lr
     assert np.max(np.abs(ctx.get(L.T_DISC_W) - flat(st.dW))) <= 2.0 * ocfg.disc_lr + 1e-6
     assert np.max(np.abs(ctx.get(L.T_DISC_W) - d_before)) > 0
     assert stats.loss_g == pytest.approx(out["loss_g"], rel=1e-5)
     assert_rel(ctx.get(L.T_LOGITS_G), out["logits_g"], 1e-4, 1e-4, "G logits")
-    assert_grad_close(ctx.get(L.T_DY), out["dy"], 1e-3, "dy")
-    assert_grad_close(ctx.get(L.T_DRAW), out["draw"], 1e-3, "draw")
-    assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
-    assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G")
+    assert_grad_close(ctx.get(L.T_DY), out["dy"], 1e-3, "dy", kd["dy"])
+    assert_grad_close(ctx.get(L.T_DRAW), out["draw"], 1e-3, "draw", kd["draw"])
+    assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G", kd["packet"])
+    assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G", kd["db_g"])
     return ctx, st, out
 
 
