@@ -36,52 +36,70 @@ using namespace tc;
 
 namespace {
 
-constexpr int kWarpsProd = 4;
+constexpr int kWarpsProd = 8;
 constexpr int kWarpsEpi = 4;
-constexpr int kThreads = 32 * (kWarpsProd + kWarpsEpi + 1);  // 288
-constexpr int kMmaWarp = kWarpsProd + kWarpsEpi;             // warp 8
+constexpr int kThreads = 32 * (kWarpsProd + kWarpsEpi + 1);  // 416
+constexpr int kProdThreads = 32 * kWarpsProd;
+constexpr int kEpiWarp0 = kWarpsProd;                        // warps 8..11 (warp % 4 = TMEM lane quarter)
+constexpr int kMmaWarp = kWarpsProd + kWarpsEpi;             // warp 12
 constexpr uint32_t kTile = 128 * 128 * 2;                    // [128][128] bf16 SW128 tile
+constexpr int kBatch = (128 * 16) / kProdThreads;            // chunk tasks per producer thread (8)
 
-struct Params0 {  // layer-0 parameters for the on-the-fly H1
-  float w0[128][2];
+struct Params0 {  // layer-0 parameters for the on-the-fly H1, column-contiguous
+  float w0x[128];
+  float w0y[128];
   float b0[128];
 };
 
 __device__ __forceinline__ float lrelu(float z, float a) { return z > 0.f ? z : z * a; }
 
+// write 8 values of row r, columns 8j..8j+7, into the SW128 planes (+ sign bits)
+template <bool kSplit>
+__device__ __forceinline__ void put_chunk(const float* x, int r, int j, uint8_t* hi, uint8_t* lo, uint8_t* mask) {
+  const uint32_t off = sw128_chunk(r, j, 128);
+  if (kSplit) {
+    uint4 h, l;
+    split_bf16(x, h, l);
+    *reinterpret_cast<uint4*>(hi + off) = h;
+    *reinterpret_cast<uint4*>(lo + off) = l;
+  } else {
+    *reinterpret_cast<uint4*>(hi + off) =
+        make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
+  }
+  if (mask) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m |= (x[i] > 0.f ? 1u : 0u) << i;
+    mask[r * 16 + j] = (uint8_t)m;
+  }
+}
+
 // stage rows [r0, r0+128) of a row-major [rows][128] fp32 matrix (zero rows
-// beyond `rows`); optionally record the sign bits (> 0) of every value.
+// beyond `rows`); all kBatch x 2 LDG.128 of a thread are issued before any is
+// consumed (memory-level parallelism: 256 threads x 256 B in flight).
 template <bool kSplit>
 __device__ __forceinline__ void stage_from_global(const float* __restrict__ g, int64_t r0, int64_t rows, uint8_t* hi,
                                                   uint8_t* lo, uint8_t* mask, int t) {
-  for (int q = t; q < 128 * 16; q += 32 * kWarpsProd) {
+  float4 buf[kBatch][2];
+#pragma unroll
+  for (int b = 0; b < kBatch; ++b) {
+    const int q = t + b * kProdThreads;
     const int r = q >> 4, j = q & 15;
     const int64_t gr = r0 + r;
-    float x[8];
     if (gr < rows) {
       const float4* p = reinterpret_cast<const float4*>(g + gr * 128 + 8 * j);
-      const float4 u = __ldg(p), v = __ldg(p + 1);
-      x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w; x[4] = v.x; x[5] = v.y; x[6] = v.z; x[7] = v.w;
+      buf[b][0] = __ldg(p);
+      buf[b][1] = __ldg(p + 1);
     } else {
+      buf[b][0] = buf[b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = 0.f;
-    }
-    const uint32_t off = sw128_chunk(r, j, 128);
-    if (kSplit) {
-      uint4 h, l;
-      split_bf16(x, h, l);
-      *reinterpret_cast<uint4*>(hi + off) = h;
-      *reinterpret_cast<uint4*>(lo + off) = l;
-    } else {
-      *reinterpret_cast<uint4*>(hi + off) =
-          make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-    }
-    if (mask) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m |= (x[i] > 0.f ? 1u : 0u) << i;
-      mask[r * 16 + j] = (uint8_t)m;
-    }
+  for (int b = 0; b < kBatch; ++b) {
+    const int q = t + b * kProdThreads;
+    const float x[8] = {buf[b][0].x, buf[b][0].y, buf[b][0].z, buf[b][0].w,
+                        buf[b][1].x, buf[b][1].y, buf[b][1].z, buf[b][1].w};
+    put_chunk<kSplit>(x, q >> 4, q & 15, hi, lo, mask);
   }
 }
 
@@ -89,37 +107,35 @@ __device__ __forceinline__ void stage_from_global(const float* __restrict__ g, i
 template <bool kSplit>
 __device__ __forceinline__ void stage_h1(const float2* __restrict__ X, const Params0& p0, float alpha, int64_t r0,
                                          int64_t rows, uint8_t* hi, uint8_t* lo, uint8_t* mask, int t) {
-  for (int q = t; q < 128 * 16; q += 32 * kWarpsProd) {
-    const int r = q >> 4, j = q & 15;
-    const int64_t gr = r0 + r;
-    float x[8];
-    if (gr < rows) {
-      const float2 xv = __ldg(X + gr);
+  float2 xv[kBatch];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int c = 8 * j + i;
-        x[i] = lrelu(fmaf(xv.x, p0.w0[c][0], fmaf(xv.y, p0.w0[c][1], p0.b0[c])), alpha);
-      }
+  for (int b = 0; b < kBatch; ++b) {
+    const int q = t + b * kProdThreads;
+    const int64_t gr = r0 + (q >> 4);
+    xv[b] = gr < rows ? __ldg(X + gr) : make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int b = 0; b < kBatch; ++b) {
+    const int q = t + b * kProdThreads;
+    const int r = q >> 4, j = q & 15;
+    float x[8];
+    if (r0 + r < rows) {
+      const float4 wa0 = *reinterpret_cast<const float4*>(&p0.w0x[8 * j]);
+      const float4 wa1 = *reinterpret_cast<const float4*>(&p0.w0x[8 * j + 4]);
+      const float4 wb0 = *reinterpret_cast<const float4*>(&p0.w0y[8 * j]);
+      const float4 wb1 = *reinterpret_cast<const float4*>(&p0.w0y[8 * j + 4]);
+      const float4 c0 = *reinterpret_cast<const float4*>(&p0.b0[8 * j]);
+      const float4 c1 = *reinterpret_cast<const float4*>(&p0.b0[8 * j + 4]);
+      const float wx[8] = {wa0.x, wa0.y, wa0.z, wa0.w, wa1.x, wa1.y, wa1.z, wa1.w};
+      const float wy[8] = {wb0.x, wb0.y, wb0.z, wb0.w, wb1.x, wb1.y, wb1.z, wb1.w};
+      const float bb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = lrelu(fmaf(xv[b].x, wx[i], fmaf(xv[b].y, wy[i], bb[i])), alpha);
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = 0.f;
     }
-    const uint32_t off = sw128_chunk(r, j, 128);
-    if (kSplit) {
-      uint4 h, l;
-      split_bf16(x, h, l);
-      *reinterpret_cast<uint4*>(hi + off) = h;
-      *reinterpret_cast<uint4*>(lo + off) = l;
-    } else {
-      *reinterpret_cast<uint4*>(hi + off) =
-          make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-    }
-    if (mask) {
-      uint32_t m = 0;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) m |= (x[i] > 0.f ? 1u : 0u) << i;
-      mask[r * 16 + j] = (uint8_t)m;
-    }
+    put_chunk<kSplit>(x, r, j, hi, lo, mask);
   }
 }
 
@@ -188,8 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
     sbias[i] = a.bias[i];
     if (kHead) swh[i] = a.w_head[i];
     if (kFirst) {
-      p0->w0[i][0] = a.W0[2 * i];
-      p0->w0[i][1] = a.W0[2 * i + 1];
+      p0->w0x[i] = a.W0[2 * i];
+      p0->w0y[i] = a.W0[2 * i + 1];
       p0->b0[i] = a.b0[i];
     }
   }
@@ -426,8 +442,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   for (int i = tid; i < 128; i += kThreads) {
     if (kFirst) {
-      p0->w0[i][0] = a.W0[2 * i];
-      p0->w0[i][1] = a.W0[2 * i + 1];
+      p0->w0x[i] = a.W0[2 * i];
+      p0->w0y[i] = a.W0[2 * i + 1];
       p0->b0[i] = a.b0[i];
     }
     if (kDy) {

@@ -19,15 +19,17 @@ from oracle import mlp, proxy
 
 U32 = 2.0 ** -24
 C_BAND = 16.0
+BAND_FP32 = C_BAND * 2.0 ** -24          # CUDA-core fp32 dot products
+BAND_BF16X3 = 4.0 * 2.0 ** -16           # bf16x3 tensor-core products: hi+lo = x(1+d), |d| <= 2^-16, three terms
 
 
-def _forward(Ws, bs, x, alpha):
+def _forward(Ws, bs, x, alpha, band_rel=BAND_FP32):
     h = np.asarray(x, dtype=np.float64)
     cache = []
     L = len(Ws)
     for l in range(L):
         z = h @ Ws[l].T + bs[l]
-        band = C_BAND * U32 * (np.abs(h) @ np.abs(Ws[l]).T + np.abs(bs[l]))
+        band = band_rel * (np.abs(h) @ np.abs(Ws[l]).T + np.abs(bs[l]))
         cache.append((h, z, band))
         h = mlp.lrelu(z, alpha) if l < L - 1 else z
     return h, cache
@@ -59,7 +61,7 @@ def _flat(ws):
     return np.concatenate([w.reshape(-1) for w in ws])
 
 
-def step_deviation(cfg, d_before, d_after, g_params, out):
+def step_deviation(cfg, d_before, d_after, g_params, out, disc_band=BAND_FP32):
     """Elementwise kink deviations of the D-step grads (dW_D, db_D) and of
     the G-step quantities (dy, draw, packet, db_G) of one oracle step.
     d_before / d_after: (Ws, bs) of the discriminator before / after Adam;
@@ -69,7 +71,7 @@ def step_deviation(cfg, d_before, d_after, g_params, out):
     # D step
     X = np.concatenate([out["x"], out["y"]])
     labels = np.concatenate([np.ones(N), np.zeros(N)])
-    zD, cD = _forward(d_before[0], d_before[1], X, a)
+    zD, cD = _forward(d_before[0], d_before[1], X, a, disc_band)
     dzD = mlp.bce_grad(zD[:, 0], labels)[:, None]
     ref = _backward(d_before[0], cD, dzD, a, 0)
     devW = np.zeros(sum(w.size for w in d_before[0]))
@@ -79,7 +81,7 @@ def step_deviation(cfg, d_before, d_after, g_params, out):
         devW = np.maximum(devW, np.abs(_flat(alt[0]) - _flat(ref[0])))
         devB = np.maximum(devB, np.abs(_flat(alt[1]) - _flat(ref[1])))
     # G step through the updated D, then the sampler and the generator
-    zG, cG = _forward(d_after[0], d_after[1], out["y"], a)
+    zG, cG = _forward(d_after[0], d_after[1], out["y"], a, disc_band)
     dzG = mlp.bce_grad(zG[:, 0], np.ones(N))[:, None]
     _, gcache = _forward(g_params[0], g_params[1], out["z"], a)
     raw = gcache[-1][1]

@@ -83,7 +83,7 @@ def test_create_matches_oracle_init(preset, kw):
 
 
 # ---------------------------------------------------------------- one step
-def _check_step(cfg, t=0):
+def _check_step(cfg, t=0, disc_band=kink.BAND_FP32):
     L = lib()
     ctx = make_ctx(cfg)
     ocfg = oracle_config(cfg)
@@ -94,7 +94,7 @@ def _check_step(cfg, t=0):
     g_params0 = ([w.copy() for w in st.gW], [b.copy() for b in st.gb])
     ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
     out = gan.local_step(ocfg, st, t)
-    kd = kink.step_deviation(ocfg, d_params0, (st.dW, st.db), g_params0, out)
+    kd = kink.step_deviation(ocfg, d_params0, (st.dW, st.db), g_params0, out, disc_band)
     N = ocfg.n_events
     stats = ctx.get(L.T_STATS)
     assert stats.nonfinite == 0
@@ -133,7 +133,7 @@ def test_step_paper_widths_ragged(impl):
     impl 0 = tcgen05 bf16x3 hidden layers, 1 = CUDA-core fp32."""
     L = lib()
     _check_step(L.config_init(1, seed=9, param_samples=64, events_per_sample=61, world=2, rank=1, group_size=2,
-                              disc_impl=impl), t=3)
+                              disc_impl=impl), t=3, disc_band=kink.BAND_BF16X3 if impl == 0 else kink.BAND_FP32)
 
 
 def test_bf16_step_within_bf16_tolerances():
