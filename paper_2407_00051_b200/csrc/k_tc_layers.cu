@@ -2,31 +2,34 @@
 // P:297, R4) on the 5th-generation tensor cores, one kernel per layer pass,
 // warp-specialised and persistent (one CTA per SM):
 //
-//   warps 0-3  producers: global fp32 rows -> bf16 (hi[, lo]) 128-byte-swizzled
-//              shared-memory operand tiles (tc_util.cuh layout)
-//   warps 4-7  epilogue : tcgen05.ld of the TMEM accumulator, fused math,
-//              global stores (TMEM lane quarter = warp % 4)
-//   warp  8    MMA      : one thread issues tcgen05.mma (kind::f16, fp32 acc)
+//   warps 0-7   producers: global fp32 rows -> bf16 planes in 128-byte-
+//               swizzled shared-memory operand tiles (tc_util.cuh layout);
+//               every warp load instruction reads one contiguous 512-byte row
+//   warps 8-11  epilogue : tcgen05.ld of the TMEM accumulator (lane quarter =
+//               warp % 4), fused math, stores transposed through a padded
+//               per-warp smem buffer so each store instruction writes 4 lines
+//   warp 12     MMA      : one thread issues tcgen05.mma (kind::f16, fp32 acc)
 //
 // mbarrier pipeline: smem stage full/empty (producers <-> MMA), accumulator
-// full/empty (MMA <-> epilogue), so staging of tile i+1, MMAs of tile i and
-// the epilogue of tile i-1 overlap.
+// full/empty (MMA <-> epilogue): staging of tile i+1, MMAs of tile i and the
+// epilogue of tile i-1 overlap.
 //
 // k_tc_fwd<split, first, head>
 //   first: the A tile is H1 = LeakyReLU(X W0^T + b0), recomputed from the
-//          8-byte input rows instead of being stored (layer 0 never touches HBM)
+//          8-byte input rows (layer 0 never touches HBM)
 //   head : the epilogue adds the last hidden layer's bias + LeakyReLU and the
 //          head layer z = H.w + b, the BCE term, dz = (s(z) - t) * scale,
-//          dZ = dz * w * LeakyReLU'(H), logits, and the head's weight-gradient
-//          partials (warp-shuffle reduce-scatter, accumulated across tiles)
+//          dZ = dz * w * LeakyReLU'(H), the logits, and the head's weight-
+//          gradient partials (warp-shuffle reduce-scatter across tiles)
 // k_tc_bwd<split, first, dy>
-//   one pass over (dZ_l, H_{l-1}) computes both the dgrad dZ_{l-1} =
+//   one pass over (dZ_l, H_{l-1}) computes the dgrad dZ_{l-1} =
 //   (dZ_l W_l) * LeakyReLU'(H_{l-1}) and the wgrad dW_l += dZ_l^T H_{l-1},
 //   db_l += dZ_l^T 1 (persistent TMEM accumulators, one partial per CTA);
 //   first: H1 recomputed from X; dy: the epilogue folds layer 0's input
 //   gradient dy = dZ1 W0 (the G step needs dy, not dZ1).
-// Precision: split = bf16x3 (hi*hi + hi*lo + lo*hi, fp32-class, PREC_FP32);
-// !split = bf16 (PREC_BF16).
+// Precision: split = bf16x4: x = hi + lo (two bf16), A*B = hi*hi + hi*lo +
+// lo*hi + lo*lo (four MMAs; fp32-class), PREC_FP32;
+// !split = bf16, PREC_BF16.
 #include "ctx.h"
 #include "tc_util.cuh"
 
@@ -39,11 +42,11 @@ namespace {
 constexpr int kWarpsProd = 8;
 constexpr int kWarpsEpi = 4;
 constexpr int kThreads = 32 * (kWarpsProd + kWarpsEpi + 1);  // 416
-constexpr int kProdThreads = 32 * kWarpsProd;
-constexpr int kEpiWarp0 = kWarpsProd;                        // warps 8..11 (warp % 4 = TMEM lane quarter)
 constexpr int kMmaWarp = kWarpsProd + kWarpsEpi;             // warp 12
 constexpr uint32_t kTile = 128 * 128 * 2;                    // [128][128] bf16 SW128 tile
-constexpr int kBatch = (128 * 16) / kProdThreads;            // chunk tasks per producer thread (8)
+constexpr int kRowsPerWarp = 128 / kWarpsProd;               // 16 rows per producer warp per tile
+constexpr int kTStride = 36;                                 // transpose buffer row stride (floats)
+constexpr uint32_t kTransBytes = kWarpsEpi * 32 * kTStride * 4;  // 18 KB
 
 struct Params0 {  // layer-0 parameters for the on-the-fly H1, column-contiguous
   float w0x[128];
@@ -53,94 +56,106 @@ struct Params0 {  // layer-0 parameters for the on-the-fly H1, column-contiguous
 
 __device__ __forceinline__ float lrelu(float z, float a) { return z > 0.f ? z : z * a; }
 
-// write 8 values of row r, columns 8j..8j+7, into the SW128 planes (+ sign bits)
-template <bool kSplit>
-__device__ __forceinline__ void put_chunk(const float* x, int r, int j, uint8_t* hi, uint8_t* lo, uint8_t* mask) {
-  const uint32_t off = sw128_chunk(r, j, 128);
-  if (kSplit) {
-    uint4 h, l;
-    split_bf16(x, h, l);
-    *reinterpret_cast<uint4*>(hi + off) = h;
-    *reinterpret_cast<uint4*>(lo + off) = l;
-  } else {
-    *reinterpret_cast<uint4*>(hi + off) =
-        make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-  }
-  if (mask) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) m |= (x[i] > 0.f ? 1u : 0u) << i;
-    mask[r * 16 + j] = (uint8_t)m;
-  }
-}
-
-// stage rows [r0, r0+128) of a row-major [rows][128] fp32 matrix (zero rows
-// beyond `rows`); all kBatch x 2 LDG.128 of a thread are issued before any is
-// consumed (memory-level parallelism: 256 threads x 256 B in flight).
-template <bool kSplit>
-__device__ __forceinline__ void stage_from_global(const float* __restrict__ g, int64_t r0, int64_t rows, uint8_t* hi,
-                                                  uint8_t* lo, uint8_t* mask, int t) {
-  float4 buf[kBatch][2];
-#pragma unroll
-  for (int b = 0; b < kBatch; ++b) {
-    const int q = t + b * kProdThreads;
-    const int r = q >> 4, j = q & 15;
-    const int64_t gr = r0 + r;
-    if (gr < rows) {
-      const float4* p = reinterpret_cast<const float4*>(g + gr * 128 + 8 * j);
-      buf[b][0] = __ldg(p);
-      buf[b][1] = __ldg(p + 1);
-    } else {
-      buf[b][0] = buf[b][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < kBatch; ++b) {
-    const int q = t + b * kProdThreads;
-    const float x[8] = {buf[b][0].x, buf[b][0].y, buf[b][0].z, buf[b][0].w,
-                        buf[b][1].x, buf[b][1].y, buf[b][1].z, buf[b][1].w};
-    put_chunk<kSplit>(x, q >> 4, q & 15, hi, lo, mask);
-  }
-}
-
-// stage H1 = LeakyReLU(X W0^T + b0) for rows [r0, r0+128) of X [rows][2].
-template <bool kSplit>
-__device__ __forceinline__ void stage_h1(const float2* __restrict__ X, const Params0& p0, float alpha, int64_t r0,
-                                         int64_t rows, uint8_t* hi, uint8_t* lo, uint8_t* mask, int t) {
-  float2 xv[kBatch];
-#pragma unroll
-  for (int b = 0; b < kBatch; ++b) {
-    const int q = t + b * kProdThreads;
-    const int64_t gr = r0 + (q >> 4);
-    xv[b] = gr < rows ? __ldg(X + gr) : make_float2(0.f, 0.f);
-  }
-#pragma unroll
-  for (int b = 0; b < kBatch; ++b) {
-    const int q = t + b * kProdThreads;
-    const int r = q >> 4, j = q & 15;
-    float x[8];
-    if (r0 + r < rows) {
-      const float4 wa0 = *reinterpret_cast<const float4*>(&p0.w0x[8 * j]);
-      const float4 wa1 = *reinterpret_cast<const float4*>(&p0.w0x[8 * j + 4]);
-      const float4 wb0 = *reinterpret_cast<const float4*>(&p0.w0y[8 * j]);
-      const float4 wb1 = *reinterpret_cast<const float4*>(&p0.w0y[8 * j + 4]);
-      const float4 c0 = *reinterpret_cast<const float4*>(&p0.b0[8 * j]);
-      const float4 c1 = *reinterpret_cast<const float4*>(&p0.b0[8 * j + 4]);
-      const float wx[8] = {wa0.x, wa0.y, wa0.z, wa0.w, wa1.x, wa1.y, wa1.z, wa1.w};
-      const float wy[8] = {wb0.x, wb0.y, wb0.z, wb0.w, wb1.x, wb1.y, wb1.z, wb1.w};
-      const float bb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = lrelu(fmaf(xv[b].x, wx[i], fmaf(xv[b].y, wy[i], bb[i])), alpha);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = 0.f;
-    }
-    put_chunk<kSplit>(x, r, j, hi, lo, mask);
-  }
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// 4 values of row r, columns 4l..4l+3 -> the bf16 planes (8-byte halves of
+// the 16-byte swizzle chunks) and, optionally, 4 sign bits (> 0).
+template <bool kSplit>
+__device__ __forceinline__ void put4(float4 x, int r, int l, uint8_t* hi, uint8_t* lo, uint8_t* mask) {
+  const uint32_t off = sw128_chunk(r, l >> 1, 128) + 8 * (l & 1);
+  const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
+  *reinterpret_cast<uint2*>(hi + off) =
+      make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+  if (kSplit) {
+    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+    const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
+    const __nv_bfloat162 l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
+    *reinterpret_cast<uint2*>(lo + off) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+  }
+  if (mask)
+    mask[r * 32 + l] = (uint8_t)((x.x > 0.f) | ((x.y > 0.f) << 1) | ((x.z > 0.f) << 2) | ((x.w > 0.f) << 3));
+}
+
+// Producer warp w stages rows w, w+8, ..., w+120 of the tile starting at
+// global row r0 of a row-major [rows][128] fp32 matrix: all 16 LDG.128 of a
+// lane are issued before the first is consumed.
+template <bool kSplit>
+__device__ __forceinline__ void stage_rows(const float* __restrict__ g, int64_t r0, int64_t rows, uint8_t* hi,
+                                           uint8_t* lo, uint8_t* mask, int w, int l) {
+  float4 buf[kRowsPerWarp];
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) {
+    const int64_t gr = r0 + w + kWarpsProd * i;
+    buf[i] = gr < rows ? __ldg(reinterpret_cast<const float4*>(g + gr * 128) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) put4<kSplit>(buf[i], w + kWarpsProd * i, l, hi, lo, mask);
+}
+
+// H1 = LeakyReLU(X W0^T + b0) for the tile's rows (layer 0 recomputed).
+template <bool kSplit>
+__device__ __forceinline__ void stage_h1(const float2* __restrict__ X, const Params0& p0, float alpha, int64_t r0,
+                                         int64_t rows, uint8_t* hi, uint8_t* lo, uint8_t* mask, int w, int l) {
+  float2 xv[kRowsPerWarp];
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) {
+    const int64_t gr = r0 + w + kWarpsProd * i;
+    xv[i] = gr < rows ? __ldg(X + gr) : make_float2(0.f, 0.f);
+  }
+  const float4 wx = *reinterpret_cast<const float4*>(&p0.w0x[4 * l]);
+  const float4 wy = *reinterpret_cast<const float4*>(&p0.w0y[4 * l]);
+  const float4 bb = *reinterpret_cast<const float4*>(&p0.b0[4 * l]);
+#pragma unroll
+  for (int i = 0; i < kRowsPerWarp; ++i) {
+    const bool ok = r0 + w + kWarpsProd * i < rows;
+    float4 h;
+    h.x = ok ? lrelu(fmaf(xv[i].x, wx.x, fmaf(xv[i].y, wy.x, bb.x)), alpha) : 0.f;
+    h.y = ok ? lrelu(fmaf(xv[i].x, wx.y, fmaf(xv[i].y, wy.y, bb.y)), alpha) : 0.f;
+    h.z = ok ? lrelu(fmaf(xv[i].x, wx.z, fmaf(xv[i].y, wy.z, bb.z)), alpha) : 0.f;
+    h.w = ok ? lrelu(fmaf(xv[i].x, wx.w, fmaf(xv[i].y, wy.w, bb.w)), alpha) : 0.f;
+    put4<kSplit>(h, w + kWarpsProd * i, l, hi, lo, mask);
+  }
+}
+
+// W_l [128][128] fp32 -> planes (once per CTA, producer warps)
+template <bool kSplit>
+__device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint8_t* hi, uint8_t* lo, int w, int l) {
+  stage_rows<kSplit>(W, 0, 128, hi, lo, nullptr, w, l);
+}
+
+// Epilogue store of one 32x32 chunk (rows lb..lb+31 of the tile, columns
+// c0..c0+31): lane = row holds v[32]; transpose through the warp's padded
+// buffer so that 8 lanes write one contiguous 128-byte row segment.
+__device__ __forceinline__ void store_chunk(float* sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
+                                            int lb, int c0, int64_t rows, int lane) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    *reinterpret_cast<float4*>(sT + lane * kTStride + 4 * k) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int rr = it * 4 + (lane >> 3);
+    const int cc = (lane & 7) * 4;
+    const int64_t grow = tile_row0 + lb + rr;
+    if (grow < rows)
+      *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) = *reinterpret_cast<const float4*>(sT + rr * kTStride + cc);
+  }
+  __syncwarp();
+}
+
+// MMA group for one K=16 step: D (+)= A*B with bf16 planes (split: 4 products)
+template <bool kSplit>
+__device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint32_t idesc,
+                                         uint32_t acc) {
+  mma_bf16(d, ah, bh, idesc, acc);
+  if (kSplit) {
+    mma_bf16(d, ah, bl, idesc, 1);
+    mma_bf16(d, al, bh, idesc, 1);
+    mma_bf16(d, al, bl, idesc, 1);
+  }
 }
 
 }  // namespace
@@ -176,18 +191,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;
   uint8_t* sA = base + P * kTile;  // 2 stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + 2 * P * kTile);
+  float* sTrans = reinterpret_cast<float*>(sA + 2 * P * kTile);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + kTransBytes);
   uint64_t* full = bars;        // [2]
   uint64_t* empty = bars + 2;   // [2]
   uint64_t* tfull = bars + 4;   // [2]
   uint64_t* tempty = bars + 6;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  double* sloss = reinterpret_cast<double*>(bars + 8);     // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 4);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
   float* swh = sbias + 128;                                  // [128] head weights
   float* sred = swh + 128;                                   // [4][129] head partials
-  double* sloss = reinterpret_cast<double*>(sred + 4 * 129 + 3);  // [4] (8-aligned below)
-  sloss = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(sloss) + 7) & ~uintptr_t(7));
-  Params0* p0 = reinterpret_cast<Params0*>(sloss + 4);
+  Params0* p0 = reinterpret_cast<Params0*>(sred + 4 * 132);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -209,23 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
       p0->b0[i] = a.b0[i];
     }
   }
-  // the weight tile (B operand) is staged once by everyone
-  for (int q = tid; q < 128 * 16; q += kThreads) {
-    const int r = q >> 4, j = q & 15;
-    const float4* p = reinterpret_cast<const float4*>(a.W + r * 128 + 8 * j);
-    const float4 u = __ldg(p), v = __ldg(p + 1);
-    const float x[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-    const uint32_t off = sw128_chunk(r, j, 128);
-    if (kSplit) {
-      uint4 h, l;
-      split_bf16(x, h, l);
-      *reinterpret_cast<uint4*>(sW + off) = h;
-      *reinterpret_cast<uint4*>(sW + kTile + off) = l;
-    } else {
-      *reinterpret_cast<uint4*>(sW + off) =
-          make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-    }
-  }
+  if (warp < kWarpsProd) stage_weights<kSplit>(a.W, sW, sW + kTile, warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -243,9 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
       uint8_t* st = sA + s * P * kTile;
       if (kFirst)
         stage_h1<kSplit>(reinterpret_cast<const float2*>(a.X), *p0, a.alpha, t * 128, a.rows, st, st + kTile, nullptr,
-                         tid);
+                         warp, lane);
       else
-        stage_from_global<kSplit>(a.A, t * 128, a.rows, st, st + kTile, nullptr, tid);
+        stage_rows<kSplit>(a.A, t * 128, a.rows, st, st + kTile, nullptr, warp, lane);
       fence_proxy_async_smem();
       mbar_arrive(&full[s]);
     }
@@ -264,12 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
-          const uint64_t adh = make_desc(ah + off, 16, 1024), bdh = make_desc(bh + off, 16, 1024);
-          mma_bf16(d, adh, bdh, idesc, k > 0);
-          if (kSplit) {
-            mma_bf16(d, adh, make_desc(bl + off, 16, 1024), idesc, 1);
-            mma_bf16(d, make_desc(al + off, 16, 1024), bdh, idesc, 1);
-          }
+          mma_step<kSplit>(d, make_desc(ah + off, 16, 1024), make_desc(al + off, 16, 1024),
+                           make_desc(bh + off, 16, 1024), make_desc(bl + off, 16, 1024), idesc, k > 0);
         }
         mma_commit(&empty[s]);
         mma_commit(&tfull[b]);
@@ -277,9 +272,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue (warps 4..7 -> TMEM lanes 32*(warp%4))
+    // ---------------- epilogue (warps 8..11 -> TMEM lanes 32*(warp%4))
     const int q = warp & 3;
     const int lb = 32 * q;
+    float* sT = sTrans + q * 32 * kTStride;
     float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // head: sum dz*H for columns 32c + lane
     float gbacc = 0.f;
     double lacc = 0.0;
@@ -296,15 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
         for (int c = 0; c < 4; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
-          if (valid) {
-            float4* cp = reinterpret_cast<float4*>(a.C + row * 128 + 32 * c);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-              cp[k] = make_float4(lrelu(v[4 * k] + sbias[32 * c + 4 * k], a.alpha),
-                                  lrelu(v[4 * k + 1] + sbias[32 * c + 4 * k + 1], a.alpha),
-                                  lrelu(v[4 * k + 2] + sbias[32 * c + 4 * k + 2], a.alpha),
-                                  lrelu(v[4 * k + 3] + sbias[32 * c + 4 * k + 3], a.alpha));
-          }
+          for (int k = 0; k < 32; ++k) v[k] = lrelu(v[k] + sbias[32 * c + k], a.alpha);
+          store_chunk(sT, v, a.C, t * 128, lb, 32 * c, a.rows, lane);
         }
       } else {
         // pass 1: z = H . w + b
@@ -336,14 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
             g[k] = dz * lrelu(zz, a.alpha);
             v[k] = dz * swh[32 * c + k] * (zz > 0.f ? 1.f : a.alpha);
           }
-          if (valid) {
-            float4* dp = reinterpret_cast<float4*>(a.dZ + row * 128 + 32 * c);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) dp[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-          }
+          store_chunk(sT, v, a.dZ, t * 128, lb, 32 * c, a.rows, lane);
           if (a.want_wgrad) {
-            // reduce-scatter over the 32 rows of the warp: lane l ends with
-            // the sum of column 32c + l
+            // reduce-scatter over the warp's 32 rows: lane l ends with column 32c + l
 #pragma unroll
             for (int w = 16; w >= 1; w >>= 1) {
               const bool upper = (lane & w) != 0;
@@ -417,8 +402,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   uint8_t* sZ = sW + P * kTile;           // dZ planes (one stage)
   uint8_t* sH = sZ + P * kTile;           // H planes (one stage)
   uint8_t* sOnes = sH + P * kTile;        // [16][128] ones, K-major SW128 (4 KB)
-  uint8_t* sMask = sOnes + 4096;          // 2 x [128][16] sign bytes of H
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sMask + 2 * 2048);
+  uint8_t* sMask = sOnes + 4096;          // 2 x [128][32] sign nibbles of H (8 KB)
+  float* sTrans = reinterpret_cast<float*>(sMask + 2 * 4096);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + kTransBytes);
   uint64_t* full = bars;                  // [1]
   uint64_t* empty = bars + 1;             // [1]
   uint64_t* tfull = bars + 2;             // [2]
@@ -455,22 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
     const uint32_t one2 = pack_bf16(1.f, 1.f);
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(one2, one2, one2, one2);
   }
-  for (int q = tid; q < 128 * 16; q += kThreads) {
-    const int r = q >> 4, j = q & 15;
-    const float4* p = reinterpret_cast<const float4*>(a.W + r * 128 + 8 * j);
-    const float4 u = __ldg(p), v = __ldg(p + 1);
-    const float x[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-    const uint32_t off = sw128_chunk(r, j, 128);
-    if (kSplit) {
-      uint4 h, l;
-      split_bf16(x, h, l);
-      *reinterpret_cast<uint4*>(sW + off) = h;
-      *reinterpret_cast<uint4*>(sW + kTile + off) = l;
-    } else {
-      *reinterpret_cast<uint4*>(sW + off) =
-          make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-    }
-  }
+  if (warp < kWarpsProd) stage_weights<kSplit>(a.W, sW, sW + kTile, warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -485,13 +456,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
       const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
       mbar_wait(&empty[0], (i & 1) ^ 1);             // MMAs of tile i-1 done with the stage
       mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);  // epilogue of tile i-2 done with mask[i&1]
-      uint8_t* mask = sMask + (i & 1) * 2048;
-      stage_from_global<kSplit>(a.dZ, t * 128, a.rows, sZ, sZ + kTile, nullptr, tid);
+      uint8_t* mask = sMask + (i & 1) * 4096;
+      stage_rows<kSplit>(a.dZ, t * 128, a.rows, sZ, sZ + kTile, nullptr, warp, lane);
       if (kFirst)
         stage_h1<kSplit>(reinterpret_cast<const float2*>(a.X), *p0, a.alpha, t * 128, a.rows, sH, sH + kTile, mask,
-                         tid);
+                         warp, lane);
       else
-        stage_from_global<kSplit>(a.H, t * 128, a.rows, sH, sH + kTile, mask, tid);
+        stage_rows<kSplit>(a.H, t * 128, a.rows, sH, sH + kTile, mask, warp, lane);
       fence_proxy_async_smem();
       mbar_arrive(&full[0]);
     }
@@ -515,26 +486,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32;  // K-major step (16 columns)
           const uint32_t km = k * 2048;                         // MN-major step (16 rows)
           // dgrad: D[rows][in] = dZ[rows][out] * W[out][in]
-          const uint64_t zk_h = make_desc(zh + kk, 16, 1024);
-          const uint64_t w_h = make_desc(wh + km, 16384, 1024);
-          mma_bf16(d, zk_h, w_h, id_d, k > 0);
-          if (kSplit) {
-            mma_bf16(d, zk_h, make_desc(wl + km, 16384, 1024), id_d, 1);
-            mma_bf16(d, make_desc(zl + kk, 16, 1024), w_h, id_d, 1);
-          }
+          mma_step<kSplit>(d, make_desc(zh + kk, 16, 1024), make_desc(zl + kk, 16, 1024),
+                           make_desc(wh + km, 16384, 1024), make_desc(wl + km, 16384, 1024), id_d, k > 0);
           if (a.want_wgrad) {
             const uint32_t acc0 = (i > 0 || k > 0) ? 1u : 0u;
-            const uint64_t zm_h = make_desc(zh + km, 16384, 1024);
-            const uint64_t h_h = make_desc(hh + km, 16384, 1024);
+            const uint64_t zm_h = make_desc(zh + km, 16384, 1024), zm_l = make_desc(zl + km, 16384, 1024);
+            mma_step<kSplit>(acc_w, zm_h, zm_l, make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024),
+                             id_w, acc0);
             const uint64_t od = make_desc(on + (k >> 2) * 2048 + (k & 3) * 32, 16, 1024);
-            mma_bf16(acc_w, zm_h, h_h, id_w, acc0);
             mma_bf16(acc_b, zm_h, od, id_b, acc0);
-            if (kSplit) {
-              const uint64_t zm_l = make_desc(zl + km, 16384, 1024);
-              mma_bf16(acc_w, zm_h, make_desc(hl + km, 16384, 1024), id_w, 1);
-              mma_bf16(acc_w, zm_l, h_h, id_w, 1);
-              mma_bf16(acc_b, zm_l, od, id_b, 1);
-            }
+            if (kSplit) mma_bf16(acc_b, zm_l, od, id_b, 1);
           }
         }
         mma_commit(&empty[0]);
@@ -546,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   } else {
     const int q = warp & 3;
     const int lb = 32 * q;
+    float* sT = sTrans + q * 32 * kTStride;
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
       const int b = i & 1;
@@ -554,26 +516,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
       const int r = lb + lane;
       const int64_t row = t * 128 + r;
       const bool valid = row < a.rows;
-      const uint8_t* mask = sMask + b * 2048 + r * 16;
+      const uint8_t* mask = sMask + b * 4096 + r * 32;
       const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)lb << 16);
       float dy0 = 0.f, dy1 = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         float v[32];
         tmem_ld32(acc + 32 * c, v);
-        const uint32_t mbits = *reinterpret_cast<const uint32_t*>(mask + 4 * c);
+        const uint2 mb = *reinterpret_cast<const uint2*>(mask + 8 * c);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] *= ((mbits >> k) & 1u) ? 1.f : a.alpha;
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t word = k < 16 ? mb.x : mb.y;
+          const uint32_t bit = ((k & 15) >> 2) * 8 + (k & 3);
+          v[k] *= ((word >> bit) & 1u) ? 1.f : a.alpha;
+        }
         if (kDy) {
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
             dy0 = fmaf(v[k], sW0[2 * (32 * c + k)], dy0);
             dy1 = fmaf(v[k], sW0[2 * (32 * c + k) + 1], dy1);
           }
-        } else if (valid) {
-          float4* dp = reinterpret_cast<float4*>(a.dZout + row * 128 + 32 * c);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) dp[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+          store_chunk(sT, v, a.dZout, t * 128, lb, 32 * c, a.rows, lane);
         }
       }
       if (kDy && valid) reinterpret_cast<float2*>(a.dy)[row] = make_float2(dy0, dy1);
@@ -583,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
     if (a.want_wgrad) {
       // TMEM lane = output feature o; 128 columns = input features
       const int o = lb + lane;
-      float* dst = a.part + (int64_t)blockIdx.x * 128 * 128 + (int64_t)o * 128;
+      float* dst = a.part + (int64_t)blockIdx.x * 128 * 128;
       if (nmine > 0) {
         mbar_wait(&wdone[0], 0);
         tc_fence_after();
@@ -591,15 +555,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
         for (int c = 0; c < 4; ++c) {
           float v[32];
           tmem_ld32(acc_w + 32 * c + ((uint32_t)lb << 16), v);
-          float4* p = reinterpret_cast<float4*>(dst + 32 * c);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) p[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          store_chunk(sT, v, dst, 0, lb, 32 * c, 128, lane);
         }
         float v[32];
         tmem_ld32(acc_b + ((uint32_t)lb << 16), v);
         a.part_db[(int64_t)blockIdx.x * 128 + o] = v[0];
       } else {
-        for (int c = 0; c < 128; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = 0; c < 128; c += 4) *reinterpret_cast<float4*>(dst + (int64_t)o * 128 + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         a.part_db[(int64_t)blockIdx.x * 128 + o] = 0.f;
       }
     }
@@ -615,28 +577,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
 // ============================================================== layer 0 grads
 // dW0[c][0] = sum_r dZ1[r][c] x0_r, dW0[c][1] = sum_r dZ1[r][c] x1_r,
 // db0[c] = sum_r dZ1[r][c]; per-block partials part[blk][c][3], fixed order.
+// 32 rows per warp iteration, lane = 4 columns (float4): coalesced 512-B rows.
 __global__ void __launch_bounds__(256) k_l0_grads(const float* __restrict__ dZ1, const float2* __restrict__ X,
                                                   int64_t rows, int64_t rpb, float* __restrict__ part) {
-  const int c = threadIdx.x & 127, half = threadIdx.x >> 7;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   const int64_t r0 = blockIdx.x * rpb, r1 = min(rows, r0 + rpb);
-  float s0 = 0.f, s1 = 0.f, sb = 0.f;
-  for (int64_t r = r0 + half; r < r1; r += 2) {
-    const float g = dZ1[r * 128 + c];
-    const float2 x = __ldg(X + r);
-    s0 = fmaf(g, x.x, s0);
-    s1 = fmaf(g, x.y, s1);
-    sb += g;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, sb = s0;
+  for (int64_t r = r0 + w; r < r1; r += 8 * 4) {
+    float4 g[4];
+    float2 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t rr = r + 8 * u;
+      g[u] = rr < r1 ? __ldg(reinterpret_cast<const float4*>(dZ1 + rr * 128) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x[u] = rr < r1 ? __ldg(X + rr) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s0.x = fmaf(g[u].x, x[u].x, s0.x); s0.y = fmaf(g[u].y, x[u].x, s0.y);
+      s0.z = fmaf(g[u].z, x[u].x, s0.z); s0.w = fmaf(g[u].w, x[u].x, s0.w);
+      s1.x = fmaf(g[u].x, x[u].y, s1.x); s1.y = fmaf(g[u].y, x[u].y, s1.y);
+      s1.z = fmaf(g[u].z, x[u].y, s1.z); s1.w = fmaf(g[u].w, x[u].y, s1.w);
+      sb.x += g[u].x; sb.y += g[u].y; sb.z += g[u].z; sb.w += g[u].w;
+    }
   }
-  __shared__ float red[2][128][3];
-  red[half][c][0] = s0;
-  red[half][c][1] = s1;
-  red[half][c][2] = sb;
+  __shared__ float red[8][128][3];
+  const float a0[4] = {s0.x, s0.y, s0.z, s0.w}, a1[4] = {s1.x, s1.y, s1.z, s1.w}, ab[4] = {sb.x, sb.y, sb.z, sb.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    red[w][4 * l + k][0] = a0[k];
+    red[w][4 * l + k][1] = a1[k];
+    red[w][4 * l + k][2] = ab[k];
+  }
   __syncthreads();
-  if (half == 0) {
-    float* p = part + (int64_t)blockIdx.x * 384 + 3 * c;
-    p[0] = red[0][c][0] + red[1][c][0];
-    p[1] = red[0][c][1] + red[1][c][1];
-    p[2] = red[0][c][2] + red[1][c][2];
+  for (int j = threadIdx.x; j < 384; j += 256) {
+    const int c = j / 3, e = j % 3;
+    float v = 0.f;
+    for (int i = 0; i < 8; ++i) v += red[i][c][e];
+    part[(int64_t)blockIdx.x * 384 + j] = v;
   }
 }
 
@@ -679,11 +657,12 @@ static int sm_count() {
 
 static size_t fwd_smem(bool split) {
   const int P = split ? 2 : 1;
-  return 1024 + (size_t)3 * P * kTile + 8 * 8 + 16 + 4 * (128 + 128 + 4 * 129 + 4) + 8 * 4 + sizeof(Params0) + 64;
+  return 1024 + (size_t)3 * P * kTile + kTransBytes + 8 * 8 + 8 * 4 + 16 + 4 * (128 + 128 + 4 * 132) +
+         sizeof(Params0) + 64;
 }
 static size_t bwd_smem(bool split) {
   const int P = split ? 2 : 1;
-  return 1024 + (size_t)3 * P * kTile + 4096 + 4096 + 8 * 8 + 16 + 4 * 256 + sizeof(Params0) + 64;
+  return 1024 + (size_t)3 * P * kTile + 4096 + 8192 + kTransBytes + 8 * 8 + 16 + 4 * 256 + sizeof(Params0) + 64;
 }
 
 template <typename K>
@@ -717,12 +696,12 @@ void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = fwd_smem(split);
   if (split) {
-    if (kind == 0) k_tc_fwd<true, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == 1) k_tc_fwd<true, false, false><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_tc_fwd<true, true, false><<<grid, kThreads, sm, st>>>(a);
+    else if (kind == FWD_MID) k_tc_fwd<true, false, false><<<grid, kThreads, sm, st>>>(a);
     else k_tc_fwd<true, false, true><<<grid, kThreads, sm, st>>>(a);
   } else {
-    if (kind == 0) k_tc_fwd<false, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == 1) k_tc_fwd<false, false, false><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_tc_fwd<false, true, false><<<grid, kThreads, sm, st>>>(a);
+    else if (kind == FWD_MID) k_tc_fwd<false, false, false><<<grid, kThreads, sm, st>>>(a);
     else k_tc_fwd<false, false, true><<<grid, kThreads, sm, st>>>(a);
   }
   count_launch();

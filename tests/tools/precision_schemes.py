@@ -25,6 +25,8 @@ def mm(a,b,mode):
         ah,al=split(a,bf16); bh,bl=split(b,bf16); return ah@bh+ah@bl+al@bh
     if mode=='f16x3':
         ah,al=split(a,f16,2048.); bh,bl=split(b,f16,2048.); return ah@bh+ah@bl+al@bh
+    if mode=='bf16x4':
+        ah,al=split(a,bf16); bh,bl=split(b,bf16); return ah@bh+ah@bl+al@bh+al@bl
     if mode=='tf32x3':
         ah,al=split(a,tf32); bh,bl=split(b,tf32); return ah@bh+ah@bl+al@bh
 def run(fwd_mode,bwd_mode,rows=1<<16,seed=1):
@@ -54,6 +56,6 @@ def run(fwd_mode,bwd_mode,rows=1<<16,seed=1):
 ref_loss,ref_dW=run('f64','f64')
 def gerr(a,b):
     fl=1e-2*np.max(np.abs(b)); return np.max(np.abs(a-b)/np.maximum(np.abs(b),fl))
-for fm,bm in [('tf32','tf32'),('bf16','bf16'),('bf16x3','bf16'),('bf16x3','bf16x3'),('f16x3','f16'),('tf32x3','tf32'),('bf16x3','tf32')]:
+for fm,bm in [('bf16x4','bf16x4'),('bf16x3','bf16x4'),('tf32','tf32'),('bf16','bf16'),('bf16x3','bf16'),('bf16x3','bf16x3'),('f16x3','f16'),('tf32x3','tf32'),('bf16x3','tf32')]:
     l,dW=run(fm,bm)
     print(f"fwd {fm:7s} bwd {bm:7s} loss rel {abs(l-ref_loss)/ref_loss:.2e}  grad max rel(floor1%) {max(gerr(dW[i],ref_dW[i]) for i in range(len(dW))):.2e}")
