@@ -255,6 +255,14 @@ SAGIPS_API sagips_status sagips_connect_nccl(sagips_ctx* ctx, const void* host_i
  * n >= SAGIPS_NUM_PHASES floats. [sync]  Errors: STATE if timing is off. */
 SAGIPS_API sagips_status sagips_phase_times(sagips_ctx* ctx, float* host_ms, int32_t n, int32_t* steps_averaged);
 
+/* Debugging aid: with the environment variable SAGIPS_TRACE=1 set before the
+ * first step, the tensor-core layer kernels record globaltimer stamps per
+ * tile (CTAs 0-3, first 32 launches): [launch][cta][tile][4] uint64 =
+ * producer done, MMA start, epilogue start, epilogue done.  Copies and
+ * rearms the buffer; `bytes` must equal the size returned for host == NULL.
+ * [sync] */
+SAGIPS_API sagips_status sagips_debug_trace(void* host, size_t* bytes);
+
 /* Number of this library's kernels launched since create (all streams). */
 SAGIPS_API sagips_status sagips_launch_count(const sagips_ctx* ctx, uint64_t* count);
 

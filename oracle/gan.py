@@ -150,21 +150,29 @@ def local_step(cfg: Config, st: RankState, t: int):
     for l in range(len(st.dW)):
         st.dW[l], st.d_mW[l], st.d_vW[l] = mlp.adam_update(st.dW[l], dWd[l], st.d_mW[l], st.d_vW[l], st.d_tau, cfg.disc_lr)
         st.db[l], st.d_mb[l], st.d_vb[l] = mlp.adam_update(st.db[l], dbd[l], st.d_mb[l], st.d_vb[l], st.d_tau, cfg.disc_lr)
-    # 8 generator loss through the updated discriminator (non-saturating)
-    zG, g_d_cache = mlp.forward(st.dW, st.db, y, a)
+    # 8-9 generator step through the updated discriminator
+    out.update(z=z, raw=raw, c=c, u=u, y=y, real_idx=ridx, x=x, hist=hist,
+               logits_d=zD, loss_d=loss_d, dW_d=dWd, db_d=dbd)
+    out.update(generator_step(cfg, st.dW, st.db, st.gW, g_cache, raw, u, y))
+    return out
+
+
+def generator_step(cfg: Config, dW, db, gW, g_cache, raw, u, y):
+    """Steps 8-9: the non-saturating generator loss L_G = mean softplus(-D(y))
+    through the given (updated) discriminator, backprop to dy, through the
+    sampler (dc, draw) and the generator (dW_G, db_G); the weights-only
+    packet (P:305)."""
+    a = cfg.leaky_slope
+    N, m = cfg.n_events, cfg.events_per_sample
+    zG, g_d_cache = mlp.forward(dW, db, y, a)
     zG = zG[:, 0]
     loss_g = mlp.bce_with_logits(zG, np.ones(N))
     dzG = mlp.bce_grad(zG, np.ones(N))
-    _, _, dy = mlp.backward(st.dW, g_d_cache, dzG[:, None], a)
+    _, _, dy = mlp.backward(dW, g_d_cache, dzG[:, None], a)
     dc, draw = proxy.sampler_backward(dy, u, raw, m)
-    dWg, dbg, _ = mlp.backward(st.gW, g_cache, draw, a)
-    # 9 weights-only packet
+    dWg, dbg, _ = mlp.backward(gW, g_cache, draw, a)
     packet = np.concatenate([w.reshape(-1) for w in dWg])
-    out.update(z=z, raw=raw, c=c, u=u, y=y, real_idx=ridx, x=x, hist=hist,
-               logits_d=zD, loss_d=loss_d, dW_d=dWd, db_d=dbd,
-               logits_g=zG, loss_g=loss_g, dy=dy, dc=dc, draw=draw,
-               dW_g=dWg, db_g=dbg, packet=packet)
-    return out
+    return dict(logits_g=zG, loss_g=loss_g, dy=dy, dc=dc, draw=draw, dW_g=dWg, db_g=dbg, packet=packet)
 
 
 def apply_generator(cfg: Config, st: RankState, R, db_local):

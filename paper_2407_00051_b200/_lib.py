@@ -87,6 +87,7 @@ def _load():
         "sagips_connect_nccl": ([vp, vp, sz], st),
         "sagips_launch_count": ([vp, P(ctypes.c_uint64)], st),
         "sagips_phase_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
+        "sagips_debug_trace": ([vp, P(ctypes.c_size_t)], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -103,7 +104,7 @@ EXPORTED = [
     "sagips_last_error", "sagips_sample_events", "sagips_train_step", "sagips_push_generator_grad",
     "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
-    "sagips_phase_times"]
+    "sagips_phase_times", "sagips_debug_trace"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 
@@ -226,3 +227,13 @@ class Context:
         n = ctypes.c_uint64()
         _check(lib.sagips_launch_count(self.h, ctypes.byref(n)), self.h)
         return n.value
+
+
+def debug_trace():
+    """Timeline stamps of the tensor-core layer kernels (SAGIPS_TRACE=1):
+    uint64 array [32 launches][4 CTAs][256 tiles][4]."""
+    n = ctypes.c_size_t()
+    _check(lib.sagips_debug_trace(None, ctypes.byref(n)))
+    out = np.zeros(n.value // 8, dtype=np.uint64)
+    _check(lib.sagips_debug_trace(out.ctypes.data, ctypes.byref(n)))
+    return out.reshape(32, 4, 256, 4)

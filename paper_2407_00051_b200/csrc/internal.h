@@ -115,6 +115,8 @@ int l0_grad_blocks();
 void launch_l0_grads(const float* dZ1, const float* X, int64_t rows, float* part, float* dW0, float* db0,
                      cudaStream_t st);
 void launch_head_finish(const float* part, int nparts, float* dw, float* db, cudaStream_t st);
+size_t tc_trace_bytes();
+int tc_trace_copy(void* host);
 
 // k_adam.cu
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,

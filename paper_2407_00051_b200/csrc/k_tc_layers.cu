@@ -2,26 +2,30 @@
 // P:297, R4) on the 5th-generation tensor cores, one kernel per layer pass,
 // warp-specialised and persistent (one CTA per SM):
 //
-//   warps 0-7   producers: global fp32 rows -> bf16 planes in 128-byte-
-//               swizzled shared-memory operand tiles (tc_util.cuh layout);
-//               every warp load instruction reads one contiguous 512-byte row
-//   warps 8-11  epilogue : tcgen05.ld of the TMEM accumulator (lane quarter =
-//               warp % 4), fused math, stores transposed through a padded
-//               per-warp smem buffer so each store instruction writes 4 lines
-//   warp 12     MMA      : one thread issues tcgen05.mma (kind::f16, fp32 acc)
+//   producer warps  global fp32 rows -> bf16 planes in 128-byte-swizzled
+//                   shared-memory operand tiles (tc_util.cuh layout); each warp
+//                   load instruction reads one contiguous 512-byte row; lane 0
+//                   of warp 0 bulk-prefetches the tiles two ahead into L2
+//                   (cp.async.bulk.prefetch.L2, no registers), so the register-
+//                   buffered loads see L2 latency
+//   epilogue warps  tcgen05.ld of the TMEM accumulator (lane quarter = warp % 4,
+//                   8 warps split the 128 columns in halves), fused math,
+//                   stores transposed through a padded per-warp smem buffer so
+//                   each store instruction writes 4 full lines
+//   MMA warp        one thread issues tcgen05.mma (kind::f16, fp32 accumulate)
 //
 // mbarrier pipeline: smem stage full/empty (producers <-> MMA), accumulator
 // full/empty (MMA <-> epilogue): staging of tile i+1, MMAs of tile i and the
-// epilogue of tile i-1 overlap.
+// epilogue of tile i-1 overlap.  SAGIPS_TRACE=1 records a per-tile timeline.
 //
-// k_tc_fwd<split, first, head>
+// k_tc_fwd<split, first, head>   (4 producer + 8 epilogue warps)
 //   first: the A tile is H1 = LeakyReLU(X W0^T + b0), recomputed from the
 //          8-byte input rows (layer 0 never touches HBM)
 //   head : the epilogue adds the last hidden layer's bias + LeakyReLU and the
 //          head layer z = H.w + b, the BCE term, dz = (s(z) - t) * scale,
 //          dZ = dz * w * LeakyReLU'(H), the logits, and the head's weight-
 //          gradient partials (warp-shuffle reduce-scatter across tiles)
-// k_tc_bwd<split, first, dy>
+// k_tc_bwd<split, first, dy>     (8 producer + 4 epilogue warps)
 //   one pass over (dZ_l, H_{l-1}) computes the dgrad dZ_{l-1} =
 //   (dZ_l W_l) * LeakyReLU'(H_{l-1}) and the wgrad dW_l += dZ_l^T H_{l-1},
 //   db_l += dZ_l^T 1 (persistent TMEM accumulators, one partial per CTA);
@@ -30,6 +34,8 @@
 // Precision: split = bf16x4: x = hi + lo (two bf16), A*B = hi*hi + hi*lo +
 // lo*hi + lo*lo (four MMAs; fp32-class), PREC_FP32;
 // !split = bf16, PREC_BF16.
+#include <cstdlib>
+
 #include "ctx.h"
 #include "tc_util.cuh"
 
@@ -39,14 +45,9 @@ using namespace tc;
 
 namespace {
 
-constexpr int kWarpsProd = 8;
-constexpr int kWarpsEpi = 4;
-constexpr int kThreads = 32 * (kWarpsProd + kWarpsEpi + 1);  // 416
-constexpr int kMmaWarp = kWarpsProd + kWarpsEpi;             // warp 12
-constexpr uint32_t kTile = 128 * 128 * 2;                    // [128][128] bf16 SW128 tile
-constexpr int kRowsPerWarp = 128 / kWarpsProd;               // 16 rows per producer warp per tile
-constexpr int kTStride = 36;                                 // transpose buffer row stride (floats)
-constexpr uint32_t kTransBytes = kWarpsEpi * 32 * kTStride * 4;  // 18 KB
+constexpr uint32_t kTile = 128 * 128 * 2;  // [128][128] bf16 SW128 tile
+constexpr int kTStride = 36;               // transpose buffer row stride (floats)
+constexpr uint32_t kTransWarp = 32 * kTStride * 4;  // 4.5 KB per epilogue warp
 
 struct Params0 {  // layer-0 parameters for the on-the-fly H1, column-contiguous
   float w0x[128];
@@ -58,6 +59,28 @@ __device__ __forceinline__ float lrelu(float z, float a) { return z > 0.f ? z : 
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// named barrier among the epilogue warps
+template <int EW>
+__device__ __forceinline__ void epi_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+}
+
+// ---- optional timeline trace (SAGIPS_TRACE=1): globaltimer stamps per tile
+// for CTAs 0..3: 0 producer arrived full, 1 MMA started, 2 epilogue got the
+// accumulator, 3 epilogue released it.
+constexpr int kTraceLaunches = 32, kTraceCtas = 4, kTraceTiles = 256;
+__device__ __forceinline__ void trace_pt(unsigned long long* tr, int i, int k) {
+  if (tr && blockIdx.x < kTraceCtas && i < kTraceTiles) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    tr[((size_t)blockIdx.x * kTraceTiles + i) * 4 + k] = t;
+  }
 }
 
 // 4 values of row r, columns 4l..4l+3 -> the bf16 planes (8-byte halves of
@@ -79,51 +102,101 @@ __device__ __forceinline__ void put4(float4 x, int r, int l, uint8_t* hi, uint8_
     mask[r * 32 + l] = (uint8_t)((x.x > 0.f) | ((x.y > 0.f) << 1) | ((x.z > 0.f) << 2) | ((x.w > 0.f) << 3));
 }
 
-// Producer warp w stages rows w, w+8, ..., w+120 of the tile starting at
-// global row r0 of a row-major [rows][128] fp32 matrix: all 16 LDG.128 of a
-// lane are issued before the first is consumed.
-template <bool kSplit>
-__device__ __forceinline__ void stage_rows(const float* __restrict__ g, int64_t r0, int64_t rows, uint8_t* hi,
-                                           uint8_t* lo, uint8_t* mask, int w, int l) {
-  float4 buf[kRowsPerWarp];
+// ---- software-pipelined producers.  A "unit" is 8*PW consecutive rows of one
+// staged tensor of one tile; lane l of producer warp w owns column float4 l
+// of rows w, w+PW, ... (8 rows).  The loads of unit u+1 are issued before
+// unit u is converted.
+constexpr int kUnitPerWarp = 8;
+
+struct Unit {
+  const float* g;      // [rows][128] source (g == nullptr: H1 recomputed from X)
+  const float2* X;
+  int64_t r0;          // first global row of the unit
+  int64_t rows;
+  int trow;            // first tile row of the unit
+};
+
+template <int PW>
+__device__ __forceinline__ void load_unit(float4 (&buf)[kUnitPerWarp], const Unit& u, int w, int l) {
 #pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) {
-    const int64_t gr = r0 + w + kWarpsProd * i;
-    buf[i] = gr < rows ? __ldg(reinterpret_cast<const float4*>(g + gr * 128) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < kUnitPerWarp; ++i) {
+    const int64_t gr = u.r0 + w + PW * i;
+    if (u.g) {
+      buf[i] = gr < u.rows ? __ldg(reinterpret_cast<const float4*>(u.g + gr * 128) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      const float2 x = gr < u.rows ? __ldg(u.X + gr) : make_float2(0.f, 0.f);
+      buf[i] = make_float4(x.x, x.y, gr < u.rows ? 1.f : 0.f, 0.f);
+    }
   }
-#pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) put4<kSplit>(buf[i], w + kWarpsProd * i, l, hi, lo, mask);
 }
 
-// H1 = LeakyReLU(X W0^T + b0) for the tile's rows (layer 0 recomputed).
-template <bool kSplit>
-__device__ __forceinline__ void stage_h1(const float2* __restrict__ X, const Params0& p0, float alpha, int64_t r0,
-                                         int64_t rows, uint8_t* hi, uint8_t* lo, uint8_t* mask, int w, int l) {
-  float2 xv[kRowsPerWarp];
-#pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) {
-    const int64_t gr = r0 + w + kWarpsProd * i;
-    xv[i] = gr < rows ? __ldg(X + gr) : make_float2(0.f, 0.f);
+template <bool kSplit, int PW>
+__device__ __forceinline__ void put_unit(const float4 (&buf)[kUnitPerWarp], const Unit& u, const Params0* p0,
+                                         float alpha, uint8_t* hi, uint8_t* lo, uint8_t* mask, int w, int l) {
+  float4 wx = make_float4(0.f, 0.f, 0.f, 0.f), wy = wx, bb = wx;
+  if (!u.g) {
+    wx = *reinterpret_cast<const float4*>(&p0->w0x[4 * l]);
+    wy = *reinterpret_cast<const float4*>(&p0->w0y[4 * l]);
+    bb = *reinterpret_cast<const float4*>(&p0->b0[4 * l]);
   }
-  const float4 wx = *reinterpret_cast<const float4*>(&p0.w0x[4 * l]);
-  const float4 wy = *reinterpret_cast<const float4*>(&p0.w0y[4 * l]);
-  const float4 bb = *reinterpret_cast<const float4*>(&p0.b0[4 * l]);
 #pragma unroll
-  for (int i = 0; i < kRowsPerWarp; ++i) {
-    const bool ok = r0 + w + kWarpsProd * i < rows;
-    float4 h;
-    h.x = ok ? lrelu(fmaf(xv[i].x, wx.x, fmaf(xv[i].y, wy.x, bb.x)), alpha) : 0.f;
-    h.y = ok ? lrelu(fmaf(xv[i].x, wx.y, fmaf(xv[i].y, wy.y, bb.y)), alpha) : 0.f;
-    h.z = ok ? lrelu(fmaf(xv[i].x, wx.z, fmaf(xv[i].y, wy.z, bb.z)), alpha) : 0.f;
-    h.w = ok ? lrelu(fmaf(xv[i].x, wx.w, fmaf(xv[i].y, wy.w, bb.w)), alpha) : 0.f;
-    put4<kSplit>(h, w + kWarpsProd * i, l, hi, lo, mask);
+  for (int i = 0; i < kUnitPerWarp; ++i) {
+    const int r = u.trow + w + PW * i;
+    float4 x = buf[i];
+    if (!u.g) {  // H1 = LeakyReLU(X W0^T + b0); buf = (x0, x1, valid, 0)
+      const float x0 = x.x, x1 = x.y;
+      const bool ok = x.z != 0.f;
+      x.x = ok ? lrelu(fmaf(x0, wx.x, fmaf(x1, wy.x, bb.x)), alpha) : 0.f;
+      x.y = ok ? lrelu(fmaf(x0, wx.y, fmaf(x1, wy.y, bb.y)), alpha) : 0.f;
+      x.z = ok ? lrelu(fmaf(x0, wx.z, fmaf(x1, wy.z, bb.z)), alpha) : 0.f;
+      x.w = ok ? lrelu(fmaf(x0, wx.w, fmaf(x1, wy.w, bb.w)), alpha) : 0.f;
+    }
+    put4<kSplit>(x, r, l, hi, lo, mask);
+  }
+}
+
+// Drive `nunits` units through a two-register-buffer pipeline.
+template <bool kSplit, int PW, class UnitOf, class Before, class Dest, class After>
+__device__ __forceinline__ void produce(int nunits, const Params0* p0, float alpha, int w, int l, UnitOf unit_of,
+                                        Before before_put, Dest dest, After after_put) {
+  float4 bufA[kUnitPerWarp], bufB[kUnitPerWarp];
+  if (nunits > 0) load_unit<PW>(bufA, unit_of(0), w, l);
+  for (int u = 0; u < nunits; u += 2) {
+    if (u + 1 < nunits) load_unit<PW>(bufB, unit_of(u + 1), w, l);
+    {
+      uint8_t *hi, *lo, *m;
+      before_put(u);
+      dest(u, hi, lo, m);
+      put_unit<kSplit, PW>(bufA, unit_of(u), p0, alpha, hi, lo, m, w, l);
+      after_put(u);
+    }
+    if (u + 2 < nunits) load_unit<PW>(bufA, unit_of(u + 2), w, l);
+    if (u + 1 < nunits) {
+      uint8_t *hi, *lo, *m;
+      before_put(u + 1);
+      dest(u + 1, hi, lo, m);
+      put_unit<kSplit, PW>(bufB, unit_of(u + 1), p0, alpha, hi, lo, m, w, l);
+      after_put(u + 1);
+    }
   }
 }
 
 // W_l [128][128] fp32 -> planes (once per CTA, producer warps)
-template <bool kSplit>
+template <bool kSplit, int PW>
 __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint8_t* hi, uint8_t* lo, int w, int l) {
-  stage_rows<kSplit>(W, 0, 128, hi, lo, nullptr, w, l);
+  for (int t0 = 0; t0 < 128; t0 += 8 * PW) {
+    float4 buf[kUnitPerWarp];
+    const Unit u{W, nullptr, t0, 128, t0};
+    load_unit<PW>(buf, u, w, l);
+    put_unit<kSplit, PW>(buf, u, nullptr, 0.f, hi, lo, nullptr, w, l);
+  }
+}
+
+// bytes of tile t (rows [128t, 128t+128) clipped) of a [rows][cols] fp32 matrix
+__device__ __forceinline__ uint32_t tile_bytes(int64_t t, int64_t rows, int cols) {
+  const int64_t r0 = t * 128;
+  if (r0 >= rows) return 0;
+  return (uint32_t)(min((int64_t)128, rows - r0) * cols * 4);
 }
 
 // Epilogue store of one 32x32 chunk (rows lb..lb+31 of the tile, columns
@@ -146,6 +219,29 @@ __device__ __forceinline__ void store_chunk(float* sT, const float* v, float* __
   __syncwarp();
 }
 
+// Same for a 32x16 chunk through a smaller (32 x 20 floats) buffer: the
+// forward kernel's 8 epilogue warps cannot afford 4.5 KB each.
+constexpr int kTStride16 = 20;
+constexpr uint32_t kTransWarp16 = 32 * kTStride16 * 4;  // 2.5 KB
+__device__ __forceinline__ void store_chunk16(float* sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
+                                              int lb, int c0, int64_t rows, int lane) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<float4*>(sT + lane * kTStride16 + 4 * k) =
+        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int rr = it * 8 + (lane >> 2);
+    const int cc = (lane & 3) * 4;
+    const int64_t grow = tile_row0 + lb + rr;
+    if (grow < rows)
+      *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) =
+          *reinterpret_cast<const float4*>(sT + rr * kTStride16 + cc);
+  }
+  __syncwarp();
+}
+
 // MMA group for one K=16 step: D (+)= A*B with bf16 planes (split: 4 products)
 template <bool kSplit>
 __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint32_t idesc,
@@ -161,6 +257,10 @@ __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, u
 }  // namespace
 
 // ============================================================== forward
+constexpr int kFwdPW = 4, kFwdEW = 8;
+constexpr int kFwdThreads = 32 * (kFwdPW + kFwdEW + 1);  // 416
+constexpr int kFwdMma = kFwdPW + kFwdEW;
+
 struct FwdArgs {
   const float* A;       // [rows][128] input activation (not first)
   const float* X;       // [rows][2] (first)
@@ -182,17 +282,20 @@ struct FwdArgs {
   float* part_head;     // [grid][129]: sum dz*H (128), sum dz
   double* loss_part;    // [grid]
   int want_wgrad;
+  unsigned long long* trace;
 };
 
 template <bool kSplit, bool kFirst, bool kHead>
-__global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
+  constexpr int PW = kFwdPW, EW = kFwdEW;
   constexpr int P = kSplit ? 2 : 1;
+  constexpr int kUnits = 128 / (8 * PW);  // units per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;
   uint8_t* sA = base + P * kTile;  // 2 stages
   float* sTrans = reinterpret_cast<float*>(sA + 2 * P * kTile);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + kTransBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + EW * kTransWarp16);
   uint64_t* full = bars;        // [2]
   uint64_t* empty = bars + 2;   // [2]
   uint64_t* tfull = bars + 4;   // [2]
@@ -201,21 +304,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 4);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
   float* swh = sbias + 128;                                  // [128] head weights
-  float* sred = swh + 128;                                   // [4][129] head partials
-  Params0* p0 = reinterpret_cast<Params0*>(sred + 4 * 132);
+  float* sred = swh + 128;                                   // [4][129] head partials (+pad)
+  float* pdot = sred + 4 * 132;                              // [2 parity][2 halves][128] partial dots
+  Params0* p0 = reinterpret_cast<Params0*>(pdot + 512);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&full[i], 32 * kWarpsProd);
+      mbar_init(&full[i], 32 * PW);
       mbar_init(&empty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kWarpsEpi);
+      mbar_init(&tempty[i], 32 * EW);
     }
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<256>(tmem_slot);
-  for (int i = tid; i < 128; i += kThreads) {
+  if (warp == kFwdMma) tmem_alloc<256>(tmem_slot);
+  for (int i = tid; i < 128; i += kFwdThreads) {
     sbias[i] = a.bias[i];
     if (kHead) swh[i] = a.w_head[i];
     if (kFirst) {
@@ -224,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
       p0->b0[i] = a.b0[i];
     }
   }
-  if (warp < kWarpsProd) stage_weights<kSplit>(a.W, sW, sW + kTile, warp, lane);
+  if (warp < PW) stage_weights<kSplit, PW>(a.W, sW, sW + kTile, warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -232,23 +336,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (a.rows + 127) / 128;
   const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto tile_of = [&](int i) { return blockIdx.x + (int64_t)i * gridDim.x; };
 
-  if (warp < kWarpsProd) {
+  if (warp < PW) {
     // ---------------- producers
-    for (int i = 0; i < nmine; ++i) {
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
-      const int s = i & 1;
-      mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
-      uint8_t* st = sA + s * P * kTile;
-      if (kFirst)
-        stage_h1<kSplit>(reinterpret_cast<const float2*>(a.X), *p0, a.alpha, t * 128, a.rows, st, st + kTile, nullptr,
-                         warp, lane);
-      else
-        stage_rows<kSplit>(a.A, t * 128, a.rows, st, st + kTile, nullptr, warp, lane);
-      fence_proxy_async_smem();
-      mbar_arrive(&full[s]);
+    const float2* X2 = reinterpret_cast<const float2*>(a.X);
+    auto prefetch_tile = [&](int i) {
+      if (i >= nmine) return;
+      const int64_t t = tile_of(i);
+      if (kFirst) prefetch_l2(X2 + t * 128, tile_bytes(t, a.rows, 2));
+      else prefetch_l2(a.A + t * 128 * 128, tile_bytes(t, a.rows, 128));
+    };
+    if (warp == 0 && lane == 0) {
+      prefetch_tile(1);
+      prefetch_tile(2);
     }
-  } else if (warp == kMmaWarp) {
+    produce<kSplit, PW>(
+        kUnits * nmine, p0, a.alpha, warp, lane,
+        [&](int u) {
+          const int64_t t = tile_of(u / kUnits);
+          const int trow = (u % kUnits) * 8 * PW;
+          return Unit{kFirst ? nullptr : a.A, X2, t * 128 + trow, a.rows, trow};
+        },
+        [&](int u) {
+          if (u % kUnits == 0) {
+            const int i = u / kUnits;
+            if (warp == 0 && lane == 0 && i > 0) prefetch_tile(i + 2);
+            mbar_wait(&empty[i & 1], ((i >> 1) & 1) ^ 1);
+          }
+        },
+        [&](int u, uint8_t*& hi, uint8_t*& lo, uint8_t*& m) {
+          uint8_t* st = sA + ((u / kUnits) & 1) * P * kTile;
+          hi = st;
+          lo = st + kTile;
+          m = nullptr;
+        },
+        [&](int u) {
+          if (u % kUnits == kUnits - 1) {
+            fence_proxy_async_smem();
+            mbar_arrive(&full[(u / kUnits) & 1]);
+            if (warp == 0 && lane == 0) trace_pt(a.trace, u / kUnits, 0);
+          }
+        });
+  } else if (warp == kFwdMma) {
     // ---------------- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
@@ -257,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
         const int s = i & 1, b = i & 1;
         mbar_wait(&full[s], (i >> 1) & 1);
         mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
+        trace_pt(a.trace, i, 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(sA + s * P * kTile), al = ah + kTile;
         const uint32_t d = tmem + (uint32_t)(b * 128);
@@ -272,63 +403,76 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue (warps 8..11 -> TMEM lanes 32*(warp%4))
+    // ---------------- epilogue: warp e -> TMEM lane quarter q, column half h
+    const int e = warp - PW;
     const int q = warp & 3;
+    const int h = e >> 2;
     const int lb = 32 * q;
-    float* sT = sTrans + q * 32 * kTStride;
-    float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // head: sum dz*H for columns 32c + lane
+    const int c_base = 64 * h;
+    float* sT = sTrans + e * 32 * kTStride16;
+    float gacc[2] = {0.f, 0.f};  // head: sum dz*H for columns c_base + 32c + lane
     float gbacc = 0.f;
     double lacc = 0.0;
     for (int i = 0; i < nmine; ++i) {
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
+      const int64_t t = tile_of(i);
       const int b = i & 1;
       mbar_wait(&tfull[b], (i >> 1) & 1);
+      if (e == 0 && lane == 0) trace_pt(a.trace, i, 2);
       tc_fence_after();
       const int64_t row = t * 128 + lb + lane;
       const bool valid = row < a.rows;
-      const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)lb << 16);
+      const uint32_t acc = tmem + (uint32_t)(b * 128 + c_base) + ((uint32_t)lb << 16);
       if (!kHead) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = lrelu(v[k] + sbias[32 * c + k], a.alpha);
-          store_chunk(sT, v, a.C, t * 128, lb, 32 * c, a.rows, lane);
+          for (int k = 0; k < 32; ++k) v[k] = lrelu(v[k] + sbias[c_base + 32 * c + k], a.alpha);
+          store_chunk16(sT, v, a.C, t * 128, lb, c_base + 32 * c, a.rows, lane);
+          store_chunk16(sT, v + 16, a.C, t * 128, lb, c_base + 32 * c + 16, a.rows, lane);
         }
       } else {
-        // pass 1: z = H . w + b
+        // pass 1: partial z = H . w over this warp's 64 columns
         float dot = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) dot = fmaf(lrelu(v[k] + sbias[32 * c + k], a.alpha), swh[32 * c + k], dot);
+          for (int k = 0; k < 32; ++k) {
+            const int cc = c_base + 32 * c + k;
+            dot = fmaf(lrelu(v[k] + sbias[cc], a.alpha), swh[cc], dot);
+          }
         }
-        const float z = dot + *a.b_head;
+        float* pd = pdot + (i & 1) * 256;
+        pd[h * 128 + lb + lane] = dot;
+        epi_sync<EW>();
+        const float z = pd[lb + lane] + pd[128 + lb + lane] + *a.b_head;
         const float tl = (row < a.n_real) ? 1.f : a.label_rest;
         const float dz = valid ? (sigmoid_f(z) - tl) * a.scale : 0.f;
-        if (valid) {
+        if (valid && h == 0) {
           a.logits[row] = z;
           lacc += (double)(tl * softplus_neg(z) + (1.f - tl) * softplus_neg(-z));
           gbacc += dz;
         }
         // pass 2: dZ = dz * w * LeakyReLU'(H) ; head weight gradient dz * H
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
           float g[32];
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            const float zz = v[k] + sbias[32 * c + k];
+            const int cc = c_base + 32 * c + k;
+            const float zz = v[k] + sbias[cc];
             g[k] = dz * lrelu(zz, a.alpha);
-            v[k] = dz * swh[32 * c + k] * (zz > 0.f ? 1.f : a.alpha);
+            v[k] = dz * swh[cc] * (zz > 0.f ? 1.f : a.alpha);
           }
-          store_chunk(sT, v, a.dZ, t * 128, lb, 32 * c, a.rows, lane);
+          store_chunk16(sT, v, a.dZ, t * 128, lb, c_base + 32 * c, a.rows, lane);
+          store_chunk16(sT, v + 16, a.dZ, t * 128, lb, c_base + 32 * c + 16, a.rows, lane);
           if (a.want_wgrad) {
-            // reduce-scatter over the warp's 32 rows: lane l ends with column 32c + l
+            // reduce-scatter over the warp's 32 rows: lane l ends with column c_base + 32c + l
 #pragma unroll
             for (int w = 16; w >= 1; w >>= 1) {
               const bool upper = (lane & w) != 0;
@@ -345,23 +489,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
       }
       tc_fence_before();
       mbar_arrive(&tempty[b]);
+      if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
     }
     if (kHead) {
       // per-CTA partials: loss (fp64), head weight gradient, head bias gradient
-      for (int c = 0; c < 4; ++c) sred[q * 129 + 32 * c + lane] = gacc[c];
+      for (int c = 0; c < 2; ++c) sred[q * 132 + c_base + 32 * c + lane] = gacc[c];
 #pragma unroll
       for (int w = 16; w >= 1; w >>= 1) {
         gbacc += __shfl_xor_sync(0xffffffffu, gbacc, w);
         lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
       }
-      if (lane == 0) {
-        sred[q * 129 + 128] = gbacc;
+      if (lane == 0 && h == 0) {
+        sred[q * 132 + 128] = gbacc;
         sloss[q] = lacc;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kWarpsEpi));
-      if (q == 0) {
+      epi_sync<EW>();
+      if (e == 0) {
         for (int j = lane; j <= 128; j += 32) {
-          const float v = sred[j] + sred[129 + j] + sred[2 * 129 + j] + sred[3 * 129 + j];
+          const float v = sred[j] + sred[132 + j] + sred[2 * 132 + j] + sred[3 * 132 + j];
           if (a.want_wgrad) a.part_head[(int64_t)blockIdx.x * 129 + j] = v;
         }
         if (lane == 0) a.loss_part[blockIdx.x] = sloss[0] + sloss[1] + sloss[2] + sloss[3];
@@ -370,13 +515,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_fwd(FwdArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == kFwdMma) {
     tc_fence_after();
     tmem_dealloc<256>(tmem);
   }
 }
 
 // ============================================================== backward
+constexpr int kBwdPW = 8, kBwdEW = 4;
+constexpr int kBwdThreads = 32 * (kBwdPW + kBwdEW + 1);  // 416
+constexpr int kBwdMma = kBwdPW + kBwdEW;
+
 struct BwdArgs {
   const float* dZ;     // [rows][128] gradient at layer l's pre-activation
   const float* H;      // [rows][128] H_{l-1} (not first)
@@ -391,11 +540,15 @@ struct BwdArgs {
   int want_wgrad;
   float* part;         // [grid][128][128]
   float* part_db;      // [grid][128]
+  unsigned long long* trace;
 };
 
 template <bool kSplit, bool kFirst, bool kDy>
-__global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
+__global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
+  constexpr int PW = kBwdPW, EW = kBwdEW;
   constexpr int P = kSplit ? 2 : 1;
+  constexpr int kUnitsT = 128 / (8 * PW);  // units per tensor per tile
+  constexpr int kUnits = 2 * kUnitsT;      // dZ units then H units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;                     // W_l planes
@@ -404,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   uint8_t* sOnes = sH + P * kTile;        // [16][128] ones, K-major SW128 (4 KB)
   uint8_t* sMask = sOnes + 4096;          // 2 x [128][32] sign nibbles of H (8 KB)
   float* sTrans = reinterpret_cast<float*>(sMask + 2 * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + kTransBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + EW * kTransWarp);
   uint64_t* full = bars;                  // [1]
   uint64_t* empty = bars + 1;             // [1]
   uint64_t* tfull = bars + 2;             // [2]
@@ -416,17 +569,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    mbar_init(&full[0], 32 * kWarpsProd);
+    mbar_init(&full[0], 32 * PW);
     mbar_init(&empty[0], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kWarpsEpi);
+      mbar_init(&tempty[i], 32 * EW);
     }
     mbar_init(&wdone[0], 1);
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
-  for (int i = tid; i < 128; i += kThreads) {
+  if (warp == kBwdMma) tmem_alloc<512>(tmem_slot);
+  for (int i = tid; i < 128; i += kBwdThreads) {
     if (kFirst) {
       p0->w0x[i] = a.W0[2 * i];
       p0->w0y[i] = a.W0[2 * i + 1];
@@ -437,11 +590,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
       sW0[2 * i + 1] = a.W0[2 * i + 1];
     }
   }
-  for (int i = tid; i < 4096 / 16; i += kThreads) {
+  for (int i = tid; i < 4096 / 16; i += kBwdThreads) {
     const uint32_t one2 = pack_bf16(1.f, 1.f);
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(one2, one2, one2, one2);
   }
-  if (warp < kWarpsProd) stage_weights<kSplit>(a.W, sW, sW + kTile, warp, lane);
+  if (warp < PW) stage_weights<kSplit, PW>(a.W, sW, sW + kTile, warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -450,23 +603,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   const uint32_t acc_w = tmem + 256, acc_b = tmem + 384;
   const int64_t ntiles = (a.rows + 127) / 128;
   const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto tile_of = [&](int i) { return blockIdx.x + (int64_t)i * gridDim.x; };
 
-  if (warp < kWarpsProd) {
-    for (int i = 0; i < nmine; ++i) {
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
-      mbar_wait(&empty[0], (i & 1) ^ 1);             // MMAs of tile i-1 done with the stage
-      mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);  // epilogue of tile i-2 done with mask[i&1]
-      uint8_t* mask = sMask + (i & 1) * 4096;
-      stage_rows<kSplit>(a.dZ, t * 128, a.rows, sZ, sZ + kTile, nullptr, warp, lane);
-      if (kFirst)
-        stage_h1<kSplit>(reinterpret_cast<const float2*>(a.X), *p0, a.alpha, t * 128, a.rows, sH, sH + kTile, mask,
-                         warp, lane);
-      else
-        stage_rows<kSplit>(a.H, t * 128, a.rows, sH, sH + kTile, mask, warp, lane);
-      fence_proxy_async_smem();
-      mbar_arrive(&full[0]);
+  if (warp < PW) {
+    const float2* X2 = reinterpret_cast<const float2*>(a.X);
+    auto prefetch_tile = [&](int i) {
+      if (i >= nmine) return;
+      const int64_t t = tile_of(i);
+      prefetch_l2(a.dZ + t * 128 * 128, tile_bytes(t, a.rows, 128));
+      if (kFirst) prefetch_l2(X2 + t * 128, tile_bytes(t, a.rows, 2));
+      else prefetch_l2(a.H + t * 128 * 128, tile_bytes(t, a.rows, 128));
+    };
+    if (warp == 0 && lane == 0) {
+      prefetch_tile(1);
+      prefetch_tile(2);
     }
-  } else if (warp == kMmaWarp) {
+    produce<kSplit, PW>(
+        kUnits * nmine, p0, a.alpha, warp, lane,
+        [&](int u) {
+          const int64_t t = tile_of(u / kUnits);
+          const int k = u % kUnits;
+          const bool isH = k >= kUnitsT;
+          const int trow = (k % kUnitsT) * 8 * PW;
+          return Unit{isH ? (kFirst ? nullptr : a.H) : a.dZ, X2, t * 128 + trow, a.rows, trow};
+        },
+        [&](int u) {
+          if (u % kUnits == 0) {
+            const int i = u / kUnits;
+            if (warp == 0 && lane == 0 && i > 0) prefetch_tile(i + 2);
+            mbar_wait(&empty[0], (i & 1) ^ 1);             // MMAs of tile i-1 done with the stage
+            mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);  // epilogue of tile i-2 done with mask[i&1]
+          }
+        },
+        [&](int u, uint8_t*& hi, uint8_t*& lo, uint8_t*& m) {
+          const bool isH = (u % kUnits) >= kUnitsT;
+          hi = isH ? sH : sZ;
+          lo = hi + kTile;
+          m = isH ? sMask + ((u / kUnits) & 1) * 4096 : nullptr;
+        },
+        [&](int u) {
+          if (u % kUnits == kUnits - 1) {
+            fence_proxy_async_smem();
+            mbar_arrive(&full[0]);
+            if (warp == 0 && lane == 0) trace_pt(a.trace, u / kUnits, 0);
+          }
+        });
+  } else if (warp == kBwdMma) {
     if (lane == 0) {
       constexpr uint32_t id_d = make_idesc_bf16(128, 128, 0, 1);  // A = dZ (K-major), B = W (MN-major)
       constexpr uint32_t id_w = make_idesc_bf16(128, 128, 1, 1);  // A = dZ^T, B = H (both MN-major)
@@ -479,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
         const int b = i & 1;
         mbar_wait(&full[0], i & 1);
         mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
+        trace_pt(a.trace, i, 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
@@ -505,13 +688,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
     }
     __syncwarp();
   } else {
+    const int e = warp - PW;
     const int q = warp & 3;
     const int lb = 32 * q;
-    float* sT = sTrans + q * 32 * kTStride;
+    float* sT = sTrans + e * 32 * kTStride;
     for (int i = 0; i < nmine; ++i) {
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
+      const int64_t t = tile_of(i);
       const int b = i & 1;
       mbar_wait(&tfull[b], (i >> 1) & 1);
+      if (e == 0 && lane == 0) trace_pt(a.trace, i, 2);
       tc_fence_after();
       const int r = lb + lane;
       const int64_t row = t * 128 + r;
@@ -543,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
       if (kDy && valid) reinterpret_cast<float2*>(a.dy)[row] = make_float2(dy0, dy1);
       tc_fence_before();
       mbar_arrive(&tempty[b]);
+      if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
     }
     if (a.want_wgrad) {
       // TMEM lane = output feature o; 128 columns = input features
@@ -568,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tc_bwd(BwdArgs a) {
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == kMmaWarp) {
+  if (warp == kBwdMma) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -657,12 +843,13 @@ static int sm_count() {
 
 static size_t fwd_smem(bool split) {
   const int P = split ? 2 : 1;
-  return 1024 + (size_t)3 * P * kTile + kTransBytes + 8 * 8 + 8 * 4 + 16 + 4 * (128 + 128 + 4 * 132) +
-         sizeof(Params0) + 64;
+  return 1024 + (size_t)3 * P * kTile + kFwdEW * kTransWarp16 + 8 * 8 + 8 * 4 + 16 +
+         4 * (128 + 128 + 4 * 132 + 512) + sizeof(Params0) + 64;
 }
 static size_t bwd_smem(bool split) {
   const int P = split ? 2 : 1;
-  return 1024 + (size_t)3 * P * kTile + 4096 + 8192 + kTransBytes + 8 * 8 + 16 + 4 * 256 + sizeof(Params0) + 64;
+  return 1024 + (size_t)3 * P * kTile + 4096 + 8192 + kBwdEW * kTransWarp + 8 * 8 + 16 + 4 * 256 + sizeof(Params0) +
+         64;
 }
 
 template <typename K>
@@ -684,6 +871,26 @@ static void configure_layers() {
 #undef SAGIPS_BWD
 }
 
+__device__ unsigned long long g_trace[kTraceLaunches][kTraceCtas * kTraceTiles * 4];
+static int g_trace_on = -1;
+static int g_trace_next = 0;
+static unsigned long long* trace_slot() {
+  if (g_trace_on < 0) {
+    const char* e = getenv("SAGIPS_TRACE");
+    g_trace_on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!g_trace_on || g_trace_next >= kTraceLaunches) return nullptr;
+  void* p = nullptr;
+  cudaGetSymbolAddress(&p, g_trace);
+  return reinterpret_cast<unsigned long long*>(p) + (size_t)(g_trace_next++) * kTraceCtas * kTraceTiles * 4;
+}
+
+size_t tc_trace_bytes() { return sizeof(unsigned long long) * kTraceLaunches * kTraceCtas * kTraceTiles * 4; }
+int tc_trace_copy(void* host) {
+  g_trace_next = 0;
+  return cudaMemcpyFromSymbol(host, g_trace, tc_trace_bytes()) == cudaSuccess ? 0 : -1;
+}
+
 int tc_layers_grid(int64_t rows) { return (int)std::min<int64_t>(std::max<int64_t>((rows + 127) / 128, 1), sm_count()); }
 
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
@@ -693,16 +900,17 @@ void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
   a.alpha = L.alpha; a.w_head = L.w_head; a.b_head = L.b_head; a.n_real = L.n_real; a.label_rest = L.label_rest;
   a.scale = L.scale; a.logits = L.logits; a.dZ = L.dZ; a.part_head = L.part_head; a.loss_part = L.loss_part;
   a.want_wgrad = L.want_wgrad;
+  a.trace = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = fwd_smem(split);
   if (split) {
-    if (kind == FWD_FIRST) k_tc_fwd<true, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == FWD_MID) k_tc_fwd<true, false, false><<<grid, kThreads, sm, st>>>(a);
-    else k_tc_fwd<true, false, true><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_tc_fwd<true, true, false><<<grid, kFwdThreads, sm, st>>>(a);
+    else if (kind == FWD_MID) k_tc_fwd<true, false, false><<<grid, kFwdThreads, sm, st>>>(a);
+    else k_tc_fwd<true, false, true><<<grid, kFwdThreads, sm, st>>>(a);
   } else {
-    if (kind == FWD_FIRST) k_tc_fwd<false, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == FWD_MID) k_tc_fwd<false, false, false><<<grid, kThreads, sm, st>>>(a);
-    else k_tc_fwd<false, false, true><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_tc_fwd<false, true, false><<<grid, kFwdThreads, sm, st>>>(a);
+    else if (kind == FWD_MID) k_tc_fwd<false, false, false><<<grid, kFwdThreads, sm, st>>>(a);
+    else k_tc_fwd<false, false, true><<<grid, kFwdThreads, sm, st>>>(a);
   }
   count_launch();
 }
@@ -712,16 +920,17 @@ void launch_tc_bwd(bool split, bool first, bool dy, const BwdLaunch& L, cudaStre
   BwdArgs a{};
   a.dZ = L.dZ; a.H = L.H; a.X = L.X; a.W0 = L.W0; a.b0 = L.b0; a.W = L.W; a.rows = L.rows; a.alpha = L.alpha;
   a.dZout = L.dZout; a.dy = L.dy; a.want_wgrad = L.want_wgrad; a.part = L.part; a.part_db = L.part_db;
+  a.trace = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = bwd_smem(split);
   if (split) {
-    if (!first) k_tc_bwd<true, false, false><<<grid, kThreads, sm, st>>>(a);
-    else if (!dy) k_tc_bwd<true, true, false><<<grid, kThreads, sm, st>>>(a);
-    else k_tc_bwd<true, true, true><<<grid, kThreads, sm, st>>>(a);
+    if (!first) k_tc_bwd<true, false, false><<<grid, kBwdThreads, sm, st>>>(a);
+    else if (!dy) k_tc_bwd<true, true, false><<<grid, kBwdThreads, sm, st>>>(a);
+    else k_tc_bwd<true, true, true><<<grid, kBwdThreads, sm, st>>>(a);
   } else {
-    if (!first) k_tc_bwd<false, false, false><<<grid, kThreads, sm, st>>>(a);
-    else if (!dy) k_tc_bwd<false, true, false><<<grid, kThreads, sm, st>>>(a);
-    else k_tc_bwd<false, true, true><<<grid, kThreads, sm, st>>>(a);
+    if (!first) k_tc_bwd<false, false, false><<<grid, kBwdThreads, sm, st>>>(a);
+    else if (!dy) k_tc_bwd<false, true, false><<<grid, kBwdThreads, sm, st>>>(a);
+    else k_tc_bwd<false, true, true><<<grid, kBwdThreads, sm, st>>>(a);
   }
   count_launch();
 }

@@ -726,6 +726,18 @@ sagips_status sagips_set(sagips_ctx* ctx, int32_t which, const void* host, size_
   return SAGIPS_OK;
 }
 
+sagips_status sagips_debug_trace(void* host, size_t* bytes) {
+  if (!bytes) return SAGIPS_ERR_INVALID_ARG;
+  const size_t need = tc_trace_bytes();
+  if (!host) {
+    *bytes = need;
+    return SAGIPS_OK;
+  }
+  if (*bytes != need) return SAGIPS_ERR_INVALID_ARG;
+  if (cudaDeviceSynchronize() != cudaSuccess) return SAGIPS_ERR_CUDA;
+  return tc_trace_copy(host) == 0 ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
 sagips_status sagips_launch_count(const sagips_ctx* ctx, uint64_t* count) {
   if (!count) return SAGIPS_ERR_INVALID_ARG;
   *count = launches_total() - (ctx ? ctx->launch_base : 0);
