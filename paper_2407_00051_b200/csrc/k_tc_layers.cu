@@ -4,21 +4,20 @@
 //
 //   producer warps  global fp32 rows -> bf16 planes in 128-byte-swizzled
 //                   shared-memory operand tiles (tc_util.cuh layout); each warp
-//                   load instruction reads one contiguous 512-byte row; lane 0
-//                   of warp 0 bulk-prefetches the tiles two ahead into L2
-//                   (cp.async.bulk.prefetch.L2, no registers), so the register-
-//                   buffered loads see L2 latency
-//   epilogue warps  tcgen05.ld of the TMEM accumulator (lane quarter = warp % 4,
+//                   load instruction reads one contiguous 512-byte row; four
+//                   register buffers keep three 4-row units of loads in
+//                   flight; lane 0 of warp 0 bulk-prefetches the tiles two
+//                   ahead into L2 (cp.async.bulk.prefetch.L2, no registers)
+//   epilogue warps  tcgen05.ld of the TMEM accumulator (lane quarter = warp % 4;
 //                   8 warps split the 128 columns in halves), fused math,
 //                   stores transposed through a padded per-warp smem buffer so
-//                   each store instruction writes 4 full lines
+//                   each store instruction writes whole lines
 //   MMA warp        one thread issues tcgen05.mma (kind::f16, fp32 accumulate)
 //
-// mbarrier pipeline: smem stage full/empty (producers <-> MMA), accumulator
-// full/empty (MMA <-> epilogue): staging of tile i+1, MMAs of tile i and the
-// epilogue of tile i-1 overlap.  SAGIPS_TRACE=1 records a per-tile timeline.
+// mbarrier pipeline: smem stage full/free (producers <-> MMA), accumulator
+// full/empty (MMA <-> epilogue).  SAGIPS_TRACE=1 records a per-tile timeline.
 //
-// k_tc_fwd<split, first, head>   (4 producer + 8 epilogue warps)
+// k_tc_fwd<split, first, head>   (4 producer + 8 epilogue warps, 2 stages)
 //   first: the A tile is H1 = LeakyReLU(X W0^T + b0), recomputed from the
 //          8-byte input rows (layer 0 never touches HBM)
 //   head : the epilogue adds the last hidden layer's bias + LeakyReLU and the
@@ -26,11 +25,13 @@
 //          dZ = dz * w * LeakyReLU'(H), the logits, and the head's weight-
 //          gradient partials (warp-shuffle reduce-scatter across tiles)
 // k_tc_bwd<split, first, dy>     (8 producer + 4 epilogue warps)
-//   one pass over (dZ_l, H_{l-1}) computes the dgrad dZ_{l-1} =
-//   (dZ_l W_l) * LeakyReLU'(H_{l-1}) and the wgrad dW_l += dZ_l^T H_{l-1},
-//   db_l += dZ_l^T 1 (persistent TMEM accumulators, one partial per CTA);
-//   first: H1 recomputed from X; dy: the epilogue folds layer 0's input
-//   gradient dy = dZ1 W0 (the G step needs dy, not dZ1).
+//   one pass over (dZ_l, H_{l-1}) computes the wgrad dW_l += dZ_l^T H_{l-1},
+//   db_l += dZ_l^T 1 (persistent TMEM accumulators, one partial per CTA) and
+//   then the dgrad dZ_{l-1} = (dZ_l W_l) * LeakyReLU'(H_{l-1}).  The H planes
+//   are released as soon as the wgrad MMAs finish, so the producers write
+//   H(i+1) while the dgrad of tile i runs.  Without wgrad (G step) only the
+//   sign mask of H is staged.  first: H1 recomputed from X; dy: the epilogue
+//   folds layer 0's input gradient dy = dZ1 W0 (the G step needs dy).
 // Precision: split = bf16x4: x = hi + lo (two bf16), A*B = hi*hi + hi*lo +
 // lo*hi + lo*lo (four MMAs; fp32-class), PREC_FP32;
 // !split = bf16, PREC_BF16.
@@ -46,8 +47,10 @@ using namespace tc;
 namespace {
 
 constexpr uint32_t kTile = 128 * 128 * 2;  // [128][128] bf16 SW128 tile
-constexpr int kTStride = 36;               // transpose buffer row stride (floats)
-constexpr uint32_t kTransWarp = 32 * kTStride * 4;  // 4.5 KB per epilogue warp
+constexpr int kTStride = 36;               // 32-column transpose buffer row stride (floats)
+constexpr uint32_t kTransWarp = 32 * kTStride * 4;
+constexpr int kTStride16 = 20;             // 16-column transpose buffer row stride
+constexpr uint32_t kTransWarp16 = 32 * kTStride16 * 4;
 
 struct Params0 {  // layer-0 parameters for the on-the-fly H1, column-contiguous
   float w0x[128];
@@ -63,6 +66,26 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void sts64(uint32_t a, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t x) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(x) : "memory");
+}
+__device__ __forceinline__ void sts128f(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
 }
 
 // named barrier among the epilogue warps
@@ -83,30 +106,36 @@ __device__ __forceinline__ void trace_pt(unsigned long long* tr, int i, int k) {
   }
 }
 
+// Shared-memory destinations of a staged tensor (0 = absent).
+struct Dst {
+  uint32_t hi, lo, mask;
+};
+
 // 4 values of row r, columns 4l..4l+3 -> the bf16 planes (8-byte halves of
-// the 16-byte swizzle chunks) and, optionally, 4 sign bits (> 0).
+// the 16-byte swizzle chunks) and/or 4 sign bits (> 0).
 template <bool kSplit>
-__device__ __forceinline__ void put4(float4 x, int r, int l, uint8_t* hi, uint8_t* lo, uint8_t* mask) {
-  const uint32_t off = sw128_chunk(r, l >> 1, 128) + 8 * (l & 1);
-  const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
-  *reinterpret_cast<uint2*>(hi + off) =
-      make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
-  if (kSplit) {
-    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-    const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
-    const __nv_bfloat162 l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
-    *reinterpret_cast<uint2*>(lo + off) =
-        make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+__device__ __forceinline__ void put4(float4 x, int r, int l, const Dst& d) {
+  if (d.hi) {
+    const uint32_t off = sw128_chunk(r, l >> 1, 128) + 8 * (l & 1);
+    const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
+    sts64(d.hi + off, *reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+    if (kSplit) {
+      const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+      const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y);
+      const __nv_bfloat162 l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
+      sts64(d.lo + off, *reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23));
+    }
   }
-  if (mask)
-    mask[r * 32 + l] = (uint8_t)((x.x > 0.f) | ((x.y > 0.f) << 1) | ((x.z > 0.f) << 2) | ((x.w > 0.f) << 3));
+  if (d.mask)
+    sts8(d.mask + r * 32 + l, (x.x > 0.f) | ((x.y > 0.f) << 1) | ((x.z > 0.f) << 2) | ((x.w > 0.f) << 3));
 }
 
-// ---- software-pipelined producers.  A "unit" is 8*PW consecutive rows of one
-// staged tensor of one tile; lane l of producer warp w owns column float4 l
-// of rows w, w+PW, ... (8 rows).  The loads of unit u+1 are issued before
-// unit u is converted.
-constexpr int kUnitPerWarp = 8;
+// ---- software-pipelined producers.  A "unit" is 4*PW consecutive rows of
+// one staged tensor of one tile; lane l of producer warp w owns column
+// float4 l of rows w, w+PW, w+2PW, w+3PW.  NB register buffers rotate: the
+// loads of unit u+NB-1 are issued before unit u is converted.
+constexpr int kRowsPerUnit = 8;  // rows per producer warp per unit
+constexpr int kNB = 2;           // register buffers
 
 struct Unit {
   const float* g;      // [rows][128] source (g == nullptr: H1 recomputed from X)
@@ -117,9 +146,9 @@ struct Unit {
 };
 
 template <int PW>
-__device__ __forceinline__ void load_unit(float4 (&buf)[kUnitPerWarp], const Unit& u, int w, int l) {
+__device__ __forceinline__ void load_unit(float4 (&buf)[kRowsPerUnit], const Unit& u, int w, int l) {
 #pragma unroll
-  for (int i = 0; i < kUnitPerWarp; ++i) {
+  for (int i = 0; i < kRowsPerUnit; ++i) {
     const int64_t gr = u.r0 + w + PW * i;
     if (u.g) {
       buf[i] = gr < u.rows ? __ldg(reinterpret_cast<const float4*>(u.g + gr * 128) + l) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -131,8 +160,8 @@ __device__ __forceinline__ void load_unit(float4 (&buf)[kUnitPerWarp], const Uni
 }
 
 template <bool kSplit, int PW>
-__device__ __forceinline__ void put_unit(const float4 (&buf)[kUnitPerWarp], const Unit& u, const Params0* p0,
-                                         float alpha, uint8_t* hi, uint8_t* lo, uint8_t* mask, int w, int l) {
+__device__ __forceinline__ void put_unit(const float4 (&buf)[kRowsPerUnit], const Unit& u, const Params0* p0,
+                                         float alpha, const Dst& d, int w, int l) {
   float4 wx = make_float4(0.f, 0.f, 0.f, 0.f), wy = wx, bb = wx;
   if (!u.g) {
     wx = *reinterpret_cast<const float4*>(&p0->w0x[4 * l]);
@@ -140,7 +169,7 @@ __device__ __forceinline__ void put_unit(const float4 (&buf)[kUnitPerWarp], cons
     bb = *reinterpret_cast<const float4*>(&p0->b0[4 * l]);
   }
 #pragma unroll
-  for (int i = 0; i < kUnitPerWarp; ++i) {
+  for (int i = 0; i < kRowsPerUnit; ++i) {
     const int r = u.trow + w + PW * i;
     float4 x = buf[i];
     if (!u.g) {  // H1 = LeakyReLU(X W0^T + b0); buf = (x0, x1, valid, 0)
@@ -151,44 +180,40 @@ __device__ __forceinline__ void put_unit(const float4 (&buf)[kUnitPerWarp], cons
       x.z = ok ? lrelu(fmaf(x0, wx.z, fmaf(x1, wy.z, bb.z)), alpha) : 0.f;
       x.w = ok ? lrelu(fmaf(x0, wx.w, fmaf(x1, wy.w, bb.w)), alpha) : 0.f;
     }
-    put4<kSplit>(x, r, l, hi, lo, mask);
+    put4<kSplit>(x, r, l, d);
   }
 }
 
-// Drive `nunits` units through a two-register-buffer pipeline.
-template <bool kSplit, int PW, class UnitOf, class Before, class Dest, class After>
+// Drive `nunits` units through the kNB-buffer pipeline.
+//   unit_of(u) -> Unit ; before_put(u) waits ; dest(u) -> Dst ; after_put(u) signals
+template <bool kSplit, int PW, class UnitOf, class Before, class DestF, class After>
 __device__ __forceinline__ void produce(int nunits, const Params0* p0, float alpha, int w, int l, UnitOf unit_of,
-                                        Before before_put, Dest dest, After after_put) {
-  float4 bufA[kUnitPerWarp], bufB[kUnitPerWarp];
-  if (nunits > 0) load_unit<PW>(bufA, unit_of(0), w, l);
-  for (int u = 0; u < nunits; u += 2) {
-    if (u + 1 < nunits) load_unit<PW>(bufB, unit_of(u + 1), w, l);
-    {
-      uint8_t *hi, *lo, *m;
-      before_put(u);
-      dest(u, hi, lo, m);
-      put_unit<kSplit, PW>(bufA, unit_of(u), p0, alpha, hi, lo, m, w, l);
-      after_put(u);
-    }
-    if (u + 2 < nunits) load_unit<PW>(bufA, unit_of(u + 2), w, l);
-    if (u + 1 < nunits) {
-      uint8_t *hi, *lo, *m;
-      before_put(u + 1);
-      dest(u + 1, hi, lo, m);
-      put_unit<kSplit, PW>(bufB, unit_of(u + 1), p0, alpha, hi, lo, m, w, l);
-      after_put(u + 1);
+                                        Before before_put, DestF dest, After after_put) {
+  float4 buf[kNB][kRowsPerUnit];
+#pragma unroll
+  for (int j = 0; j < kNB - 1; ++j)
+    if (j < nunits) load_unit<PW>(buf[j], unit_of(j), w, l);
+  for (int u = 0; u < nunits; u += kNB) {
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+      if (u + j < nunits) {
+        if (u + j + kNB - 1 < nunits) load_unit<PW>(buf[(j + kNB - 1) % kNB], unit_of(u + j + kNB - 1), w, l);
+        before_put(u + j);
+        put_unit<kSplit, PW>(buf[j], unit_of(u + j), p0, alpha, dest(u + j), w, l);
+        after_put(u + j);
+      }
     }
   }
 }
 
 // W_l [128][128] fp32 -> planes (once per CTA, producer warps)
 template <bool kSplit, int PW>
-__device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint8_t* hi, uint8_t* lo, int w, int l) {
-  for (int t0 = 0; t0 < 128; t0 += 8 * PW) {
-    float4 buf[kUnitPerWarp];
+__device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint32_t hi, uint32_t lo, int w, int l) {
+  for (int t0 = 0; t0 < 128; t0 += kRowsPerUnit * PW) {
+    float4 buf[kRowsPerUnit];
     const Unit u{W, nullptr, t0, 128, t0};
     load_unit<PW>(buf, u, w, l);
-    put_unit<kSplit, PW>(buf, u, nullptr, 0.f, hi, lo, nullptr, w, l);
+    put_unit<kSplit, PW>(buf, u, nullptr, 0.f, Dst{hi, lo, 0}, w, l);
   }
 }
 
@@ -199,45 +224,40 @@ __device__ __forceinline__ uint32_t tile_bytes(int64_t t, int64_t rows, int cols
   return (uint32_t)(min((int64_t)128, rows - r0) * cols * 4);
 }
 
-// Epilogue store of one 32x32 chunk (rows lb..lb+31 of the tile, columns
+// Epilogue store of a 32-row x 32-column chunk (tile rows lb..lb+31, columns
 // c0..c0+31): lane = row holds v[32]; transpose through the warp's padded
-// buffer so that 8 lanes write one contiguous 128-byte row segment.
-__device__ __forceinline__ void store_chunk(float* sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
+// buffer (shared address sT) so 8 lanes write one contiguous 128-byte segment.
+__device__ __forceinline__ void store_chunk(uint32_t sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
                                             int lb, int c0, int64_t rows, int lane) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    *reinterpret_cast<float4*>(sT + lane * kTStride + 4 * k) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  for (int k = 0; k < 8; ++k) sts128f(sT + 4 * (lane * kTStride + 4 * k), v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
 #pragma unroll
   for (int it = 0; it < 8; ++it) {
     const int rr = it * 4 + (lane >> 3);
     const int cc = (lane & 7) * 4;
     const int64_t grow = tile_row0 + lb + rr;
-    if (grow < rows)
-      *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) = *reinterpret_cast<const float4*>(sT + rr * kTStride + cc);
+    const float4 x = lds128f(sT + 4 * (rr * kTStride + cc));
+    if (grow < rows) *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) = x;
   }
   __syncwarp();
 }
 
-// Same for a 32x16 chunk through a smaller (32 x 20 floats) buffer: the
-// forward kernel's 8 epilogue warps cannot afford 4.5 KB each.
-constexpr int kTStride16 = 20;
-constexpr uint32_t kTransWarp16 = 32 * kTStride16 * 4;  // 2.5 KB
-__device__ __forceinline__ void store_chunk16(float* sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
+// Same for 32 rows x 16 columns through a 32 x 20 buffer (the forward kernel's
+// 8 epilogue warps cannot afford 4.5 KB each).
+__device__ __forceinline__ void store_chunk16(uint32_t sT, const float* v, float* __restrict__ gbase, int64_t tile_row0,
                                               int lb, int c0, int64_t rows, int lane) {
 #pragma unroll
   for (int k = 0; k < 4; ++k)
-    *reinterpret_cast<float4*>(sT + lane * kTStride16 + 4 * k) =
-        make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    sts128f(sT + 4 * (lane * kTStride16 + 4 * k), v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     const int rr = it * 8 + (lane >> 2);
     const int cc = (lane & 3) * 4;
     const int64_t grow = tile_row0 + lb + rr;
-    if (grow < rows)
-      *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) =
-          *reinterpret_cast<const float4*>(sT + rr * kTStride16 + cc);
+    const float4 x = lds128f(sT + 4 * (rr * kTStride16 + cc));
+    if (grow < rows) *reinterpret_cast<float4*>(gbase + grow * 128 + c0 + cc) = x;
   }
   __syncwarp();
 }
@@ -289,13 +309,13 @@ template <bool kSplit, bool kFirst, bool kHead>
 __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
   constexpr int PW = kFwdPW, EW = kFwdEW;
   constexpr int P = kSplit ? 2 : 1;
-  constexpr int kUnits = 128 / (8 * PW);  // units per tile
+  constexpr int kUnits = 128 / (kRowsPerUnit * PW);  // units per tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;
   uint8_t* sA = base + P * kTile;  // 2 stages
-  float* sTrans = reinterpret_cast<float*>(sA + 2 * P * kTile);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + EW * kTransWarp16);
+  uint8_t* sTrans = sA + 2 * P * kTile;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sTrans + EW * kTransWarp16);
   uint64_t* full = bars;        // [2]
   uint64_t* empty = bars + 2;   // [2]
   uint64_t* tfull = bars + 4;   // [2]
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 4);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
   float* swh = sbias + 128;                                  // [128] head weights
-  float* sred = swh + 128;                                   // [4][129] head partials (+pad)
+  float* sred = swh + 128;                                   // [4][132] head partials
   float* pdot = sred + 4 * 132;                              // [2 parity][2 halves][128] partial dots
   Params0* p0 = reinterpret_cast<Params0*>(pdot + 512);
 
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
       p0->b0[i] = a.b0[i];
     }
   }
-  if (warp < PW) stage_weights<kSplit, PW>(a.W, sW, sW + kTile, warp, lane);
+  if (warp < PW) stage_weights<kSplit, PW>(a.W, smem_u32(sW), smem_u32(sW + kTile), warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -351,11 +371,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
       prefetch_tile(1);
       prefetch_tile(2);
     }
+    const uint32_t sA32 = smem_u32(sA);
     produce<kSplit, PW>(
         kUnits * nmine, p0, a.alpha, warp, lane,
         [&](int u) {
           const int64_t t = tile_of(u / kUnits);
-          const int trow = (u % kUnits) * 8 * PW;
+          const int trow = (u % kUnits) * kRowsPerUnit * PW;
           return Unit{kFirst ? nullptr : a.A, X2, t * 128 + trow, a.rows, trow};
         },
         [&](int u) {
@@ -365,11 +386,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
             mbar_wait(&empty[i & 1], ((i >> 1) & 1) ^ 1);
           }
         },
-        [&](int u, uint8_t*& hi, uint8_t*& lo, uint8_t*& m) {
-          uint8_t* st = sA + ((u / kUnits) & 1) * P * kTile;
-          hi = st;
-          lo = st + kTile;
-          m = nullptr;
+        [&](int u) {
+          const uint32_t st = sA32 + ((u / kUnits) & 1) * P * kTile;
+          return Dst{st, st + kTile, 0};
         },
         [&](int u) {
           if (u % kUnits == kUnits - 1) {
@@ -409,7 +428,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1) k_tc_fwd(FwdArgs a) {
     const int h = e >> 2;
     const int lb = 32 * q;
     const int c_base = 64 * h;
-    float* sT = sTrans + e * 32 * kTStride16;
+    const uint32_t sT = smem_u32(sTrans) + e * kTransWarp16;
     float gacc[2] = {0.f, 0.f};  // head: sum dz*H for columns c_base + 32c + lane
     float gbacc = 0.f;
     double lacc = 0.0;
@@ -547,8 +566,8 @@ template <bool kSplit, bool kFirst, bool kDy>
 __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
   constexpr int PW = kBwdPW, EW = kBwdEW;
   constexpr int P = kSplit ? 2 : 1;
-  constexpr int kUnitsT = 128 / (8 * PW);  // units per tensor per tile
-  constexpr int kUnits = 2 * kUnitsT;      // dZ units then H units
+  constexpr int kUnitsT = 128 / (kRowsPerUnit * PW);  // units per tensor per tile
+  constexpr int kUnits = 2 * kUnitsT;                 // H units first, then dZ units
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = base;                     // W_l planes
@@ -556,21 +575,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
   uint8_t* sH = sZ + P * kTile;           // H planes (one stage)
   uint8_t* sOnes = sH + P * kTile;        // [16][128] ones, K-major SW128 (4 KB)
   uint8_t* sMask = sOnes + 4096;          // 2 x [128][32] sign nibbles of H (8 KB)
-  float* sTrans = reinterpret_cast<float*>(sMask + 2 * 4096);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sTrans) + EW * kTransWarp);
-  uint64_t* full = bars;                  // [1]
-  uint64_t* empty = bars + 1;             // [1]
-  uint64_t* tfull = bars + 2;             // [2]
-  uint64_t* tempty = bars + 4;            // [2]
-  uint64_t* wdone = bars + 6;             // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint8_t* sTrans = sMask + 2 * 4096;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sTrans + EW * kTransWarp);
+  uint64_t* full_h = bars;                // [1] producers -> MMA: H planes (or mask) staged
+  uint64_t* full_z = bars + 1;            // [1] producers -> MMA: dZ planes staged
+  uint64_t* free_h = bars + 2;            // [1] MMA -> producers: wgrad done with H
+  uint64_t* free_z = bars + 3;            // [1] MMA -> producers: all MMAs done with dZ
+  uint64_t* tfull = bars + 4;             // [2]
+  uint64_t* tempty = bars + 6;            // [2]
+  uint64_t* wdone = bars + 8;             // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
   float* sW0 = reinterpret_cast<float*>(tmem_slot + 4);  // [128][2] (dy mode)
   Params0* p0 = reinterpret_cast<Params0*>(sW0 + 256);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool wgrad = a.want_wgrad != 0;
   if (tid == 0) {
-    mbar_init(&full[0], 32 * PW);
-    mbar_init(&empty[0], 1);
+    mbar_init(&full_h[0], 32 * PW);
+    mbar_init(&full_z[0], 32 * PW);
+    mbar_init(&free_h[0], 1);
+    mbar_init(&free_z[0], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * EW);
@@ -594,7 +618,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
     const uint32_t one2 = pack_bf16(1.f, 1.f);
     reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(one2, one2, one2, one2);
   }
-  if (warp < PW) stage_weights<kSplit, PW>(a.W, sW, sW + kTile, warp, lane);
+  if (warp < PW) stage_weights<kSplit, PW>(a.W, smem_u32(sW), smem_u32(sW + kTile), warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -618,34 +642,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
       prefetch_tile(1);
       prefetch_tile(2);
     }
+    const uint32_t zh = smem_u32(sZ), hh = smem_u32(sH), mk = smem_u32(sMask);
     produce<kSplit, PW>(
         kUnits * nmine, p0, a.alpha, warp, lane,
         [&](int u) {
           const int64_t t = tile_of(u / kUnits);
           const int k = u % kUnits;
-          const bool isH = k >= kUnitsT;
-          const int trow = (k % kUnitsT) * 8 * PW;
+          const bool isH = k < kUnitsT;
+          const int trow = (k % kUnitsT) * kRowsPerUnit * PW;
           return Unit{isH ? (kFirst ? nullptr : a.H) : a.dZ, X2, t * 128 + trow, a.rows, trow};
         },
         [&](int u) {
-          if (u % kUnits == 0) {
-            const int i = u / kUnits;
+          const int i = u / kUnits, k = u % kUnits;
+          if (k == 0) {
             if (warp == 0 && lane == 0 && i > 0) prefetch_tile(i + 2);
-            mbar_wait(&empty[0], (i & 1) ^ 1);             // MMAs of tile i-1 done with the stage
-            mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);  // epilogue of tile i-2 done with mask[i&1]
+            if (wgrad) mbar_wait(&free_h[0], (i & 1) ^ 1);   // wgrad of tile i-1 done with the H planes
+            mbar_wait(&tempty[i & 1], ((i >> 1) & 1) ^ 1);   // epilogue of tile i-2 done with mask[i&1]
+          } else if (k == kUnitsT) {
+            mbar_wait(&free_z[0], (i & 1) ^ 1);              // all MMAs of tile i-1 done with dZ
           }
         },
-        [&](int u, uint8_t*& hi, uint8_t*& lo, uint8_t*& m) {
-          const bool isH = (u % kUnits) >= kUnitsT;
-          hi = isH ? sH : sZ;
-          lo = hi + kTile;
-          m = isH ? sMask + ((u / kUnits) & 1) * 4096 : nullptr;
+        [&](int u) {
+          const int i = u / kUnits, k = u % kUnits;
+          if (k < kUnitsT) return Dst{wgrad ? hh : 0u, wgrad ? hh + kTile : 0u, mk + (i & 1) * 4096};
+          return Dst{zh, zh + kTile, 0u};
         },
         [&](int u) {
-          if (u % kUnits == kUnits - 1) {
+          const int i = u / kUnits, k = u % kUnits;
+          if (k == kUnitsT - 1) {
             fence_proxy_async_smem();
-            mbar_arrive(&full[0]);
-            if (warp == 0 && lane == 0) trace_pt(a.trace, u / kUnits, 0);
+            mbar_arrive(&full_h[0]);
+          } else if (k == kUnits - 1) {
+            fence_proxy_async_smem();
+            mbar_arrive(&full_z[0]);
+            if (warp == 0 && lane == 0) trace_pt(a.trace, i, 0);
           }
         });
   } else if (warp == kBwdMma) {
@@ -659,19 +689,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
       const uint32_t on = smem_u32(sOnes);
       for (int i = 0; i < nmine; ++i) {
         const int b = i & 1;
-        mbar_wait(&full[0], i & 1);
+        mbar_wait(&full_h[0], i & 1);
+        mbar_wait(&full_z[0], i & 1);
         mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
         trace_pt(a.trace, i, 1);
         tc_fence_after();
-        const uint32_t d = tmem + (uint32_t)(b * 128);
+        if (wgrad) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32;  // K-major step (16 columns)
-          const uint32_t km = k * 2048;                         // MN-major step (16 rows)
-          // dgrad: D[rows][in] = dZ[rows][out] * W[out][in]
-          mma_step<kSplit>(d, make_desc(zh + kk, 16, 1024), make_desc(zl + kk, 16, 1024),
-                           make_desc(wh + km, 16384, 1024), make_desc(wl + km, 16384, 1024), id_d, k > 0);
-          if (a.want_wgrad) {
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t km = k * 2048;  // MN-major step (16 rows)
             const uint32_t acc0 = (i > 0 || k > 0) ? 1u : 0u;
             const uint64_t zm_h = make_desc(zh + km, 16384, 1024), zm_l = make_desc(zl + km, 16384, 1024);
             mma_step<kSplit>(acc_w, zm_h, zm_l, make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024),
@@ -680,8 +706,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
             mma_bf16(acc_b, zm_h, od, id_b, acc0);
             if (kSplit) mma_bf16(acc_b, zm_l, od, id_b, 1);
           }
+          mma_commit(&free_h[0]);
         }
-        mma_commit(&empty[0]);
+        const uint32_t d = tmem + (uint32_t)(b * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32;  // K-major step (16 columns)
+          const uint32_t km = k * 2048;
+          // dgrad: D[rows][in] = dZ[rows][out] * W[out][in]
+          mma_step<kSplit>(d, make_desc(zh + kk, 16, 1024), make_desc(zl + kk, 16, 1024),
+                           make_desc(wh + km, 16384, 1024), make_desc(wl + km, 16384, 1024), id_d, k > 0);
+        }
+        mma_commit(&free_z[0]);
         mma_commit(&tfull[b]);
       }
       mma_commit(&wdone[0]);
@@ -691,7 +727,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
     const int e = warp - PW;
     const int q = warp & 3;
     const int lb = 32 * q;
-    float* sT = sTrans + e * 32 * kTStride;
+    const uint32_t sT = smem_u32(sTrans) + e * kTransWarp;
+    const uint32_t mk = smem_u32(sMask);
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int b = i & 1;
@@ -701,14 +738,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
       const int r = lb + lane;
       const int64_t row = t * 128 + r;
       const bool valid = row < a.rows;
-      const uint8_t* mask = sMask + b * 4096 + r * 32;
+      const uint32_t mask = mk + b * 4096 + r * 32;
       const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)lb << 16);
       float dy0 = 0.f, dy1 = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         float v[32];
         tmem_ld32(acc + 32 * c, v);
-        const uint2 mb = *reinterpret_cast<const uint2*>(mask + 8 * c);
+        const uint2 mb = lds64(mask + 8 * c);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           const uint32_t word = k < 16 ? mb.x : mb.y;
@@ -730,7 +767,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1) k_tc_bwd(BwdArgs a) {
       mbar_arrive(&tempty[b]);
       if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
     }
-    if (a.want_wgrad) {
+    if (wgrad) {
       // TMEM lane = output feature o; 128 columns = input features
       const int o = lb + lane;
       float* dst = a.part + (int64_t)blockIdx.x * 128 * 128;
@@ -848,7 +885,7 @@ static size_t fwd_smem(bool split) {
 }
 static size_t bwd_smem(bool split) {
   const int P = split ? 2 : 1;
-  return 1024 + (size_t)3 * P * kTile + 4096 + 8192 + kBwdEW * kTransWarp + 8 * 8 + 16 + 4 * 256 + sizeof(Params0) +
+  return 1024 + (size_t)3 * P * kTile + 4096 + 8192 + kBwdEW * kTransWarp + 10 * 8 + 16 + 4 * 256 + sizeof(Params0) +
          64;
 }
 
