@@ -273,9 +273,15 @@ def ours_arm(args):
     peaks, peak_src = load_peaks()
     disc_ms = phases["disc_step"] + phases["gen_loss_through_disc"]
     disc_flops = disc_flops_per_event(cfg) * N
+    tc = cfg.disc_impl != L.DISC_SIMT and cfg.disc_hidden == 128
     if cfg.precision == L.PREC_BF16:
         peak = peaks.get("bf16_tflops_sustained", 1400.0)
-        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak_src": f"{peak_src} bf16 sustained"}
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak_src": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json)"}
+    elif tc:
+        # fp32-class bf16x4: every fp32 multiply-add is 4 bf16 tensor-core MACs
+        peak = peaks.get("bf16_tflops_sustained", 1400.0) / 4.0
+        roof = {"bound": "tensor", "unit": "TFLOP/s",
+                "peak_src": f"{peak_src} bf16 sustained / 4 (bf16x4 split: 4 MMAs per fp32-class product)"}
     else:
         # FP32 FFMA on CUDA cores: 148 SMs x 128 lanes x 2 flop x max SM clock
         peak = SM_COUNT * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
