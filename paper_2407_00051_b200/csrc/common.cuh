@@ -21,18 +21,17 @@ __host__ __device__ inline PhiloxKey make_key(uint64_t seed) {
   return PhiloxKey{static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)};
 }
 
-// Ten rounds; mulhi/mullo map to IMAD.WIDE on sm_100a.
+// Ten rounds.  Each 32x32 -> 64-bit product is one IMAD.WIDE.U32 (hi and lo
+// together); the key bumps k + r*W are compile-time-unrolled adds that the
+// compiler hoists out of grid-stride loops.
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, PhiloxKey key) {
-  uint32_t k0 = key.k0, k1 = key.k1;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
-    const uint32_t lo1 = 0xCD9E8D57u * c.z;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
-    k0 += 0x9E3779B9u;
-    k1 += 0xBB67AE85u;
+    const uint32_t k0 = key.k0 + (uint32_t)r * 0x9E3779B9u;
+    const uint32_t k1 = key.k1 + (uint32_t)r * 0xBB67AE85u;
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0);
   }
   return c;
 }
@@ -46,9 +45,13 @@ __device__ __forceinline__ uint32_t word_of(uint4 r, int lane) {
   return lane == 0 ? r.x : lane == 1 ? r.y : lane == 2 ? r.z : r.w;
 }
 
-// u = (2 * (w >> 9) + 1) * 2^-24 in (0, 1), exact in fp32 (R-UNIF).
+// u = (2 * (w >> 9) + 1) * 2^-24 in (0, 1), exact in fp32 (R-UNIF), built
+// from the bits: 1 + (w >> 9) 2^-23 is the float 0x3F800000 | (w >> 9), and
+// subtracting (1 - 2^-24) leaves (2 (w >> 9) + 1) 2^-24, which has <= 24
+// significant bits, so the one rounded subtraction is exact.
 __device__ __forceinline__ float uniform_open01(uint32_t w) {
-  return __uint2float_rn(2u * (w >> 9) + 1u) * 5.9604644775390625e-8f;
+  const float one_m = __uint_as_float(0x3F800000u | (w >> 9));
+  return __fsub_rn(one_m, 0.99999994039535522461f);
 }
 
 // Lemire multiply-shift (R-BOOT): (w * n) >> 32.
@@ -65,12 +68,12 @@ __device__ __forceinline__ float quantile_f32(float u, float c0, float c1, float
   return __fadd_rn(c0, d);
 }
 
-// histogram bin: 0 underflow/NaN, 1..bins, bins+1 overflow.
+// histogram bin: 0 underflow/NaN, 1..bins, bins+1 overflow.  t = (y-lo)*scale
+// in fp32 (two roundings, as R22); clamping t to [-1, bins] (fmaxf drops a
+// NaN) and flooring gives -1 for t < 0 or NaN, bins for t >= bins.
 __device__ __forceinline__ int hist_bin(float y, float lo, float scale, int bins) {
   const float t = __fmul_rn(__fsub_rn(y, lo), scale);
-  if (!(t >= 0.0f)) return 0;
-  if (t >= static_cast<float>(bins)) return bins + 1;
-  return static_cast<int>(t) + 1;
+  return __float2int_rd(fminf(fmaxf(t, -1.0f), static_cast<float>(bins))) + 1;
 }
 
 __device__ __forceinline__ float softplus_f(float x) {

@@ -118,65 +118,125 @@ void launch_constrain(const float* raw, float* c, int k, cudaStream_t st) {
 // One thread = one group of 4 consecutive events e = 4g..4g+3:
 //   fake: Philox calls 2g and 2g+1 of stream FAKE give the 8 words 2e+o;
 //   real: call g of stream REAL gives the 4 bootstrap words (word e).
-// Rows of X: [0, N) real, [N, 2N) fake (R9).  Histograms are privatised in
-// shared memory (uint32, exact) and merged with integer atomics.
-template <bool kReal>
+// Histogram increment (shared-memory atomic into the warp's private copy).
+__device__ __forceinline__ void hist_add(uint32_t* h, int bin) { atomicAdd(h + bin, 1u); }
+
+// Rows of X: [0, N) real, [N, 2N) fake (R9).  Persistent grid (grid-stride
+// over groups).  Histograms are privatised per warp in shared memory when they
+// fit (no inter-warp contention), summed per block, and merged with integer
+// atomics (exact and order-independent).  The common group (all 4 events in
+// range and in one sample, 16-B aligned rows) runs a branch-free body; the
+// ragged tail and m % 4 != 0 take the general one.
+template <bool kReal, bool kHist>
 __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int m, int64_t n_events,
                                                 const float2* __restrict__ shard, uint32_t n_shard,
                                                 PhiloxKey key, uint32_t step, uint32_t rank,
                                                 uint32_t fake_stream, float2* __restrict__ x_real,
                                                 float2* __restrict__ y_fake, uint32_t* __restrict__ real_idx,
                                                 uint32_t* __restrict__ hist, int bins, float lo0, float sc0,
-                                                float lo1, float sc1) {
-  extern __shared__ uint32_t sh_hist[];  // [2 sets][2 obs][bins+2]
+                                                float lo1, float sc1, int per_warp, int vec_ok) {
+  extern __shared__ uint32_t sh_hist[];  // [copies][2 sets][2 obs][bins+2]
   const int hsz = 4 * (bins + 2);
-  if (hist) {
-    for (int i = threadIdx.x; i < hsz; i += blockDim.x) sh_hist[i] = 0;
+  const int copies = per_warp ? (int)(blockDim.x >> 5) : 1;
+  uint32_t* my = sh_hist + (per_warp ? (int)(threadIdx.x >> 5) * hsz : 0);
+  if (kHist) {
+    for (int i = threadIdx.x; i < hsz * copies; i += blockDim.x) sh_hist[i] = 0;
     __syncthreads();
   }
-  const int64_t ngroups = (n_events + 3) / 4;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ngroups;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 wa = philox_call(key, (uint32_t)(2 * g), step, rank, fake_stream);
-    const uint4 wb = philox_call(key, (uint32_t)(2 * g + 1), step, rank, fake_stream);
+  // event counts are < 2^31 (validated at the ABI), so 32-bit indices
+  const uint32_t n = (uint32_t)n_events;
+  const uint32_t ngroups = (n + 3) / 4;
+  const bool m4 = (m & 3) == 0 && vec_ok;
+  uint32_t* hx0 = my;
+  uint32_t* hx1 = my + (bins + 2);
+  uint32_t* hy0 = my + 2 * (bins + 2);
+  uint32_t* hy1 = my + 3 * (bins + 2);
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const uint4 wa = philox_call(key, 2 * g, step, rank, fake_stream);
+    const uint4 wb = philox_call(key, 2 * g + 1, step, rank, fake_stream);
     const uint32_t wf[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
     uint4 wr = make_uint4(0, 0, 0, 0);
-    if (kReal) wr = philox_call(key, (uint32_t)g, step, rank, kStreamReal);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int64_t e = 4 * g + q;
-      if (e >= n_events) break;
-      const int64_t s = e / m;
-      const float* cs = c + 6 * s;
-      const float y0 = quantile_f32(uniform_open01(wf[2 * q]), __ldg(cs + 0), __ldg(cs + 1), __ldg(cs + 2));
-      const float y1 = quantile_f32(uniform_open01(wf[2 * q + 1]), __ldg(cs + 3), __ldg(cs + 4), __ldg(cs + 5));
-      y_fake[e] = make_float2(y0, y1);
-      if (hist) {
-        atomicAdd(&sh_hist[2 * (bins + 2) + hist_bin(y0, lo0, sc0, bins)], 1u);
-        atomicAdd(&sh_hist[3 * (bins + 2) + hist_bin(y1, lo1, sc1, bins)], 1u);
+    if (kReal) wr = philox_call(key, g, step, rank, kStreamReal);
+    // sample of the group's first event: one division per group
+    const uint32_t s = 4 * g / (uint32_t)m;
+    const float* cs = c + 6 * (size_t)s;
+    float c0 = __ldg(cs + 0), c1 = __ldg(cs + 1), c2 = __ldg(cs + 2);
+    float c3 = __ldg(cs + 3), c4 = __ldg(cs + 4), c5 = __ldg(cs + 5);
+    float2 yv[4], xv[4];
+    uint32_t iv[4];
+    auto event = [&](int q) {
+      yv[q].x = quantile_f32(uniform_open01(wf[2 * q]), c0, c1, c2);
+      yv[q].y = quantile_f32(uniform_open01(wf[2 * q + 1]), c3, c4, c5);
+      if (kHist) {
+        hist_add(hy0, hist_bin(yv[q].x, lo0, sc0, bins));
+        hist_add(hy1, hist_bin(yv[q].y, lo1, sc1, bins));
       }
       if (kReal) {
-        const uint32_t idx = lemire(word_of(wr, q), n_shard);
-        const float2 xv = __ldg(shard + idx);
-        x_real[e] = xv;
-        real_idx[e] = idx;
-        if (hist) {
-          atomicAdd(&sh_hist[0 * (bins + 2) + hist_bin(xv.x, lo0, sc0, bins)], 1u);
-          atomicAdd(&sh_hist[1 * (bins + 2) + hist_bin(xv.y, lo1, sc1, bins)], 1u);
+        iv[q] = lemire(word_of(wr, q), n_shard);
+        xv[q] = __ldg(shard + iv[q]);
+        if (kHist) {
+          hist_add(hx0, hist_bin(xv[q].x, lo0, sc0, bins));
+          hist_add(hx1, hist_bin(xv[q].y, lo1, sc1, bins));
+        }
+      }
+    };
+    if (m4 && 4 * g + 3 < n) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) event(q);
+      float4* yf = reinterpret_cast<float4*>(y_fake + 4 * (size_t)g);
+      yf[0] = make_float4(yv[0].x, yv[0].y, yv[1].x, yv[1].y);
+      yf[1] = make_float4(yv[2].x, yv[2].y, yv[3].x, yv[3].y);
+      if (kReal) {
+        float4* xr = reinterpret_cast<float4*>(x_real + 4 * (size_t)g);
+        xr[0] = make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y);
+        xr[1] = make_float4(xv[2].x, xv[2].y, xv[3].x, xv[3].y);
+        *reinterpret_cast<uint4*>(real_idx + 4 * (size_t)g) = make_uint4(iv[0], iv[1], iv[2], iv[3]);
+      }
+    } else {
+      // general group: step across sample boundaries, stop at n
+      uint32_t r = 4 * g - s * (uint32_t)m;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t e = 4 * g + q;
+        if (e >= n) break;
+        if (r == (uint32_t)m) {
+          r = 0;
+          cs += 6;
+          c0 = __ldg(cs + 0); c1 = __ldg(cs + 1); c2 = __ldg(cs + 2);
+          c3 = __ldg(cs + 3); c4 = __ldg(cs + 4); c5 = __ldg(cs + 5);
+        }
+        ++r;
+        event(q);
+        y_fake[e] = yv[q];
+        if (kReal) {
+          x_real[e] = xv[q];
+          real_idx[e] = iv[q];
         }
       }
     }
   }
-  if (hist) {
+  if (kHist) {
     __syncthreads();
     const int off = kReal ? 0 : 2 * (bins + 2);
-    for (int i = off + threadIdx.x; i < hsz; i += blockDim.x)
-      if (sh_hist[i]) atomicAdd(&hist[i - off], sh_hist[i]);
+    for (int i = off + threadIdx.x; i < hsz; i += blockDim.x) {
+      uint32_t v = 0;
+      for (int w = 0; w < copies; ++w) v += sh_hist[w * hsz + i];
+      if (v) atomicAdd(&hist[i - off], v);
+    }
   }
 }
 
 static void hist_params(const float lo[2], const float hi[2], int bins, float* sc) {
   for (int o = 0; o < 2; ++o) sc[o] = (float)bins / (hi[o] - lo[o]);  // fp32, as the oracle
+}
+
+// persistent launch shape: 2 blocks per SM; per-warp histogram copies when
+// 8 x 4 x (bins+2) counters fit comfortably in shared memory
+static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* smem, int* per_warp) {
+  const int64_t ngroups = (n + 3) / 4;
+  *blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + 255) / 256, 148 * 8));
+  *per_warp = hist && (8 * 4 * (bins + 2) * 4 <= 48 * 1024);
+  *smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) * (*per_warp ? 8 : 1) : 0;
 }
 
 void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard,
@@ -187,13 +247,17 @@ void launch_sample_step(const float* c, int k, int m, const float* shard, int64_
   float sc[2];
   hist_params(lo, hi, bins, sc);
   if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * (bins + 2), st);
-  const int64_t ngroups = (n + 3) / 4;
-  const int blocks = (int)std::min<int64_t>((ngroups + 255) / 256, 148 * 8);
-  const size_t smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) : 0;
+  int blocks, per_warp;
+  size_t smem;
+  sample_shape(n, bins, hist != nullptr, &blocks, &smem, &per_warp);
   float2* x = reinterpret_cast<float2*>(x_events);
-  k_sample<true><<<blocks, 256, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard),
+  const int vec_ok = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(x_events) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(real_idx) % 16 == 0);
+  auto kern = hist ? k_sample<true, true> : k_sample<true, false>;
+  kern<<<blocks, 256, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard),
                                             (uint32_t)n_shard, make_key(seed), step, rank, kStreamFake,
-                                            x, x + n, real_idx, hist, bins, lo[0], sc[0], lo[1], sc[1]);
+                                            x, x + n, real_idx, hist, bins, lo[0], sc[0], lo[1], sc[1], per_warp,
+                                            vec_ok);
   count_launch();
 }
 
@@ -209,12 +273,14 @@ void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t 
     l[1] = lo[1];
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * (bins + 2), st);
   }
-  const int64_t ngroups = (n + 3) / 4;
-  const int blocks = (int)std::min<int64_t>((ngroups + 255) / 256, 148 * 8);
-  const size_t smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) : 0;
-  k_sample<false><<<blocks, 256, smem, st>>>(c, m, n, nullptr, 1, make_key(seed), step, rank, stream_id,
+  int blocks, per_warp;
+  size_t smem;
+  sample_shape(n, bins, hist != nullptr, &blocks, &smem, &per_warp);
+  const int vec_ok = reinterpret_cast<uintptr_t>(events) % 16 == 0;
+  auto kern = hist ? k_sample<false, true> : k_sample<false, false>;
+  kern<<<blocks, 256, smem, st>>>(c, m, n, nullptr, 1, make_key(seed), step, rank, stream_id,
                                              nullptr, reinterpret_cast<float2*>(events), nullptr, hist,
-                                             bins, l[0], sc[0], l[1], sc[1]);
+                                             bins, l[0], sc[0], l[1], sc[1], per_warp, vec_ok);
   count_launch();
 }
 
