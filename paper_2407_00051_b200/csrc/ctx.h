@@ -47,6 +47,7 @@ struct sagips_ctx {
   float* X = nullptr;
   uint32_t* real_idx = nullptr;
   float* dAct[sagips::kMaxLayers] = {};
+  uint4* dMask[sagips::kMaxLayers] = {};  // sign masks of the hidden activations (tcgen05 layers)
   float* dZb[2] = {};
   float *logits_d = nullptr, *logits_g = nullptr, *dy = nullptr;
   uint32_t* hist = nullptr;

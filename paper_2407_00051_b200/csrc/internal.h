@@ -70,15 +70,17 @@ int tc_wgrad_grid();
 void launch_tc_wgrad(bool split, const float* dZ, const float* H, int64_t rows, float* part, float* part_db,
                      cudaStream_t st);
 
-// k_tc_layers.cu (warp-specialised tcgen05 layer passes, disc_depth >= 3)
+// k_tc_layers.cu (warp-specialised tcgen05 layer passes on bf16 plane tiles,
+// disc_depth >= 3; see the file header for the tensor formats)
 struct FwdLaunch {
-  const float* A = nullptr;   // input activation [rows][128] (mid, head)
-  const float* X = nullptr;   // [rows][2] (first)
-  const float* W0 = nullptr;  // [128][2] (first)
-  const float* b0 = nullptr;  // [128] (first)
-  const float* W = nullptr;   // [128][128]
+  const uint8_t* A = nullptr;  // input plane tiles (mid, head)
+  const float* X = nullptr;    // [rows][2] (first)
+  const float* W0 = nullptr;   // [128][2] (first)
+  const float* b0 = nullptr;   // [128] (first)
+  const float* W = nullptr;    // [128][128]
   const float* bias = nullptr;
-  float* C = nullptr;         // output activation (first, mid)
+  uint8_t* C = nullptr;        // output plane tiles (H; head: G)
+  uint4* mask = nullptr;       // sign masks of H (first, mid)
   int64_t rows = 0;
   float alpha = 0.01f;
   const float* w_head = nullptr;
@@ -87,34 +89,33 @@ struct FwdLaunch {
   float label_rest = 0.f;
   float scale = 1.f;
   float* logits = nullptr;
-  float* dZ = nullptr;
-  float* part_head = nullptr;
+  float* part_head = nullptr;  // [grid*4][129]
+  float* part_db = nullptr;    // [grid*4][128]
   double* loss_part = nullptr;
   int want_wgrad = 0;
 };
 struct BwdLaunch {
-  const float* dZ = nullptr;
-  const float* H = nullptr;
+  const uint8_t* G = nullptr;  // G_{l+1} plane tiles
+  const uint8_t* H = nullptr;  // H_l plane tiles (wgrad, not first)
+  const uint4* mask = nullptr; // sign masks of H_l (not first)
   const float* X = nullptr;
   const float* W0 = nullptr;
   const float* b0 = nullptr;
   const float* W = nullptr;
   int64_t rows = 0;
   float alpha = 0.01f;
-  float* dZout = nullptr;
-  float* dy = nullptr;
-  int want_wgrad = 0;
-  float* part = nullptr;
-  float* part_db = nullptr;
+  uint8_t* Gout = nullptr;     // G_l plane tiles (not first)
+  float* dy = nullptr;         // (first, no wgrad)
+  float* part = nullptr;       // [grid][128][128]
+  float* part_db = nullptr;    // [grid*4][128]
+  float* part_l0 = nullptr;    // [grid*4][384]
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
 int tc_layers_grid(int64_t rows);
+size_t plane_tile_bytes(bool split);
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st);
-void launch_tc_bwd(bool split, bool first, bool dy, const BwdLaunch& L, cudaStream_t st);
-int l0_grad_blocks();
-void launch_l0_grads(const float* dZ1, const float* X, int64_t rows, float* part, float* dW0, float* db0,
-                     cudaStream_t st);
-void launch_head_finish(const float* part, int nparts, float* dw, float* db, cudaStream_t st);
+void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaStream_t st);
+void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st);
 size_t tc_trace_bytes();
 int tc_trace_copy(void* host);
 

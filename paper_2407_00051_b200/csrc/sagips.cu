@@ -81,9 +81,12 @@ static void carve(sagips_ctx* c, char* base) {
   c->draw = cv.take<float>(6 * k);
   c->X = cv.take<float>(4 * N);
   c->real_idx = cv.take<uint32_t>(N);
-  for (int l = 0; l < D.L - 1; ++l) c->dAct[l] = cv.take<float>(2 * N * D.sizes[l + 1]);
-  c->dZb[0] = cv.take<float>(2 * N * D.maxw);
-  c->dZb[1] = cv.take<float>(2 * N * D.maxw);
+  // rows rounded up to whole 128-row tiles (plane-tile format, k_tc_layers.cu)
+  const int64_t rows_t = (2 * N + 127) / 128 * 128;
+  for (int l = 0; l < D.L - 1; ++l) c->dAct[l] = cv.take<float>(rows_t * D.sizes[l + 1]);
+  for (int l = 0; l < D.L - 1; ++l) c->dMask[l] = cv.take<uint4>(rows_t);
+  c->dZb[0] = cv.take<float>(rows_t * D.maxw);
+  c->dZb[1] = cv.take<float>(rows_t * D.maxw);
   c->logits_d = cv.take<float>(2 * N);
   c->logits_g = cv.take<float>(N);
   c->dy = cv.take<float>(2 * N);
@@ -97,7 +100,8 @@ static void carve(sagips_ctx* c, char* base) {
   pf = std::max<int64_t>(pf, (int64_t)kMaxSms * 128 * 128);  // tcgen05 wgrad: one partial per CTA
   c->part = cv.take<float>(pf);
   c->part_floats = pf;
-  c->colpart = cv.take<float>(std::max(296, kMaxSms) * std::max(128, std::max(D.maxw, G.maxw)));
+  c->colpart = cv.take<float>(std::max<int64_t>((int64_t)std::max(296, kMaxSms) * std::max(128, std::max(D.maxw, G.maxw)),
+                                                (int64_t)kMaxSms * 4 * 384));
   c->head_tmp = cv.take<float>(D.maxw + 1);
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
@@ -366,28 +370,29 @@ static void disc_layer_dgrad(sagips_ctx* c, int l, const float* dZ, float* out_d
 static bool use_layers_v2(const sagips_ctx* c) { return c->use_tc && c->cfg.disc_depth >= 3; }
 
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
-                            float scale, float* logits, bool want_head_grad, cudaStream_t st) {
+                            float scale, float* logits, bool want_grads, cudaStream_t st) {
   const auto& D = c->D;
   const int Lh = D.L - 1;
   const bool split = tc_split(c);
-  FwdLaunch f;
+  auto planes = [&](int l) { return reinterpret_cast<uint8_t*>(c->dAct[l]); };
+  FwdLaunch f;  // H_2 = LeakyReLU(H_1 W_1^T + b_1), H_1 recomputed from X
   f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0];
-  f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.C = c->dAct[1];
+  f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.C = planes(1); f.mask = c->dMask[1];
   f.rows = rows; f.alpha = c->cfg.leaky_slope;
   launch_tc_fwd(split, FWD_FIRST, f, st);
-  for (int l = 2; l <= Lh - 2; ++l) {
+  for (int l = 2; l <= Lh - 2; ++l) {  // H_{l+1} = LeakyReLU(H_l W_l^T + b_l)
     FwdLaunch m;
-    m.A = c->dAct[l - 1]; m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l]; m.C = c->dAct[l];
+    m.A = planes(l - 1); m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l]; m.C = planes(l); m.mask = c->dMask[l];
     m.rows = rows; m.alpha = c->cfg.leaky_slope;
     launch_tc_fwd(split, FWD_MID, m, st);
   }
-  FwdLaunch h;
-  h.A = c->dAct[Lh - 2]; h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
+  FwdLaunch h;  // last hidden layer + head + BCE -> G_{Lh} planes
+  h.A = planes(Lh - 2); h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
   h.rows = rows; h.alpha = c->cfg.leaky_slope;
   h.w_head = c->dW + D.w_off[Lh]; h.b_head = c->dB + D.b_off[Lh];
   h.n_real = n_real; h.label_rest = label_rest; h.scale = scale;
-  h.logits = logits; h.dZ = c->dZb[0]; h.part_head = c->part; h.loss_part = c->loss_part;
-  h.want_wgrad = want_head_grad ? 1 : 0;
+  h.logits = logits; h.C = reinterpret_cast<uint8_t*>(c->dZb[0]); h.part_head = c->part; h.part_db = c->colpart;
+  h.loss_part = c->loss_part; h.want_wgrad = want_grads ? 1 : 0;
   launch_tc_fwd(split, FWD_HEAD, h, st);
 }
 
@@ -398,24 +403,32 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const bool split = tc_split(c);
   const int grid = tc_layers_grid(rows);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
-  launch_head_finish(c->part, grid, c->d_dW + D.w_off[Lh], c->d_dB + D.b_off[Lh], st);
+  // head: dW (128) + db (1); colsum of G_{Lh} -> db of the last hidden layer
+  launch_sum_parts(c->part, 4 * grid, 129, 128, c->d_dW + D.w_off[Lh], st);
+  launch_sum_parts(c->part + 128, 4 * grid, 129, 1, c->d_dB + D.b_off[Lh], st);
+  launch_sum_parts(c->colpart, 4 * grid, 128, 128, c->d_dB + D.b_off[Lh - 1], st);
   launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
-    b.dZ = c->dZb[cur]; b.W = c->dW + D.w_off[l]; b.rows = rows; b.alpha = c->cfg.leaky_slope;
-    b.dZout = c->dZb[cur ^ 1]; b.want_wgrad = 1; b.part = c->part; b.part_db = c->colpart;
+    b.G = reinterpret_cast<const uint8_t*>(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
+    b.alpha = c->cfg.leaky_slope; b.part = c->part;
     if (l == 1) {
-      b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0];
+      b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
     } else {
-      b.H = c->dAct[l - 1];
+      b.H = reinterpret_cast<const uint8_t*>(c->dAct[l - 1]); b.mask = c->dMask[l - 1];
+      b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]); b.part_db = c->colpart;
     }
-    launch_tc_bwd(split, l == 1, false, b, st);
-    launch_reduce_parts(c->part, grid, 128 * 128, c->d_dW + D.w_off[l], 1.0f, st);
-    launch_reduce_parts(c->colpart, grid, 128, c->d_dB + D.b_off[l], 1.0f, st);
+    launch_tc_bwd(split, l == 1, true, b, st);
+    launch_sum_parts(c->part, grid, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
+    if (l == 1) {  // dW_0 [128][2] row-major, db_0
+      launch_sum_parts(c->colpart, 4 * grid, 384, 256, c->d_dW + D.w_off[0], st);
+      launch_sum_parts(c->colpart + 256, 4 * grid, 384, 128, c->d_dB + D.b_off[0], st);
+    } else {
+      launch_sum_parts(c->colpart, 4 * grid, 128, 128, c->d_dB + D.b_off[l - 1], st);
+    }
     cur ^= 1;
   }
-  launch_l0_grads(c->dZb[cur], c->X, rows, c->part, c->d_dW + D.w_off[0], c->d_dB + D.b_off[0], st);
 }
 
 static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
@@ -429,14 +442,14 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
-    b.dZ = c->dZb[cur]; b.W = c->dW + D.w_off[l]; b.rows = N; b.alpha = c->cfg.leaky_slope;
-    b.dZout = c->dZb[cur ^ 1]; b.want_wgrad = 0;
+    b.G = reinterpret_cast<const uint8_t*>(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = N;
+    b.alpha = c->cfg.leaky_slope;
     if (l == 1) {
       b.X = Y; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.dy = c->dy;
     } else {
-      b.H = c->dAct[l - 1];
+      b.mask = c->dMask[l - 1]; b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]);
     }
-    launch_tc_bwd(split, l == 1, l == 1, b, st);
+    launch_tc_bwd(split, l == 1, false, b, st);
     cur ^= 1;
   }
 }
