@@ -55,6 +55,7 @@ struct sagips_ctx {
   int64_t part_floats = 0;
   float* colpart = nullptr;
   float* head_tmp = nullptr;
+  float* dbpart = nullptr;  // [grid][128] bias-gradient partials (tcgen05 layers)
   double* loss_part = nullptr;
   sagips_step_stats* stats = nullptr;
   // step bookkeeping

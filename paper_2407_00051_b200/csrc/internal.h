@@ -90,7 +90,6 @@ struct FwdLaunch {
   float scale = 1.f;
   float* logits = nullptr;
   float* part_head = nullptr;  // [grid*4][129]
-  float* part_db = nullptr;    // [grid*4][128]
   double* loss_part = nullptr;
   int want_wgrad = 0;
 };
@@ -107,7 +106,7 @@ struct BwdLaunch {
   uint8_t* Gout = nullptr;     // G_l plane tiles (not first)
   float* dy = nullptr;         // (first, no wgrad)
   float* part = nullptr;       // [grid][128][128]
-  float* part_db = nullptr;    // [grid*4][128]
+  float* part_db = nullptr;    // [grid][128]
   float* part_l0 = nullptr;    // [grid*4][384]
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };

@@ -31,11 +31,12 @@
 //   mid/first: H = LeakyReLU(Z) -> planes + mask.
 //   head: H_{L-1} = LeakyReLU(Z), z = H.w + b, BCE term, logits,
 //         dz = (sigmoid(z) - t) * scale, G = dz * w * LeakyReLU'(Z) -> planes;
-//         head gradient partials (dz*H, dz) and colsum(G) partials.
-// k_bwd<split, first, wgrad>: per tile, wgrad dW += G^T H (persistent TMEM
-//   accumulator) then dgrad G' = (G W) * LeakyReLU'(H) (the H stage is
-//   released as soon as the wgrad MMAs finish).  Outputs: G' planes +
-//   colsum(G') partials (mid), or, for the first layer, the layer-0 gradients
+//         head gradient partials (dz*H, dz).
+// k_bwd<split, first, wgrad>: per tile, wgrad dW += G^T H and db += G^T 1
+//   (persistent TMEM accumulators; the ones operand is a 512-byte
+//   non-swizzled block) then dgrad G' = (G W) * LeakyReLU'(H) (the H stage is
+//   released as soon as the wgrad MMAs finish).  Outputs: G' planes (mid), or,
+//   for the first layer, the layer-0 gradients
 //   dW_0 = G_1^T X, db_0 = colsum(G_1) (D step) or dy = G_1 W_0 (G step) in the
 //   epilogue.  Without wgrad (G step) the H stage becomes a second G stage.
 #include <cstdlib>
@@ -143,14 +144,20 @@ __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, u
 // W [128][128] fp32 -> hi/lo planes (once per CTA; warps 0-3)
 template <bool kSplit>
 __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint32_t hi, uint32_t lo, int w, int l) {
-  for (int r = w; r < 128; r += kPW) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(W + r * 128) + l);
-    const uint32_t off = sw128_chunk(r, l >> 1, 128) + 8 * (l & 1);
-    uint32_t h0, h1, l0, l1;
-    split2(x.x, x.y, h0, l0);
-    split2(x.z, x.w, h1, l1);
-    sts64(hi + off, h0, h1);
-    if (kSplit) sts64(lo + off, l0, l1);
+#pragma unroll 1
+  for (int r0 = w; r0 < 128; r0 += 8 * kPW) {
+    float4 x[8];  // 8 independent loads in flight
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldg(reinterpret_cast<const float4*>(W + (r0 + kPW * u) * 128) + l);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint32_t off = sw128_chunk(r0 + kPW * u, l >> 1, 128) + 8 * (l & 1);
+      uint32_t h0, h1, l0, l1;
+      split2(x[u].x, x[u].y, h0, l0);
+      split2(x[u].z, x[u].w, h1, l1);
+      sts64(hi + off, h0, h1);
+      if (kSplit) sts64(lo + off, l0, l1);
+    }
   }
 }
 
@@ -163,21 +170,30 @@ __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0
   const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[4 * l]);
   const float4 bb = *reinterpret_cast<const float4*>(&p0->b0[4 * l]);
   const unsigned vbits = __ballot_sync(0xffffffffu, xvalid);
-#pragma unroll 4
-  for (int i = 0; i < 32; ++i) {
-    const float x0 = __shfl_sync(0xffffffffu, xr.x, i), x1 = __shfl_sync(0xffffffffu, xr.y, i);
-    const bool ok = (vbits >> i) & 1u;
-    const int r = 32 * w + i;
-    const float a = ok ? lrelu(fmaf(x0, wx.x, fmaf(x1, wy.x, bb.x)), alpha) : 0.f;
-    const float b = ok ? lrelu(fmaf(x0, wx.y, fmaf(x1, wy.y, bb.y)), alpha) : 0.f;
-    const float c = ok ? lrelu(fmaf(x0, wx.z, fmaf(x1, wy.z, bb.z)), alpha) : 0.f;
-    const float d = ok ? lrelu(fmaf(x0, wx.w, fmaf(x1, wy.w, bb.w)), alpha) : 0.f;
-    const uint32_t off = sw128_chunk(r, l >> 1, 128) + 8 * (l & 1);
-    uint32_t h0, h1, l0, l1;
-    split2(a, b, h0, l0);
-    split2(c, d, h1, l1);
-    sts64(hi + off, h0, h1);
-    if (kSplit) sts64(lo + off, l0, l1);
+  const uint32_t cbase = (uint32_t)(l >> 4) * 16384u + 8u * (uint32_t)(l & 1);
+  const int jj = (l >> 1) & 7;
+#pragma unroll 1
+  for (int i0 = 0; i0 < 32; i0 += 4) {
+    uint32_t hw[4][2], lw[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 4 independent rows in flight
+      const float x0 = __shfl_sync(0xffffffffu, xr.x, i0 + u), x1 = __shfl_sync(0xffffffffu, xr.y, i0 + u);
+      // branch-free: rows past the end are multiplied by 0 (their x is 0, so the values are finite)
+      const float ok = ((vbits >> (i0 + u)) & 1u) ? 1.f : 0.f;
+      const float a = ok * lrelu(fmaf(x0, wx.x, fmaf(x1, wy.x, bb.x)), alpha);
+      const float b = ok * lrelu(fmaf(x0, wx.y, fmaf(x1, wy.y, bb.y)), alpha);
+      const float c = ok * lrelu(fmaf(x0, wx.z, fmaf(x1, wy.z, bb.z)), alpha);
+      const float d = ok * lrelu(fmaf(x0, wx.w, fmaf(x1, wy.w, bb.w)), alpha);
+      split2(a, b, hw[u][0], lw[u][0]);
+      split2(c, d, hw[u][1], lw[u][1]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = 32 * w + i0 + u;
+      const uint32_t off = cbase + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u + ((uint32_t)(jj ^ (r & 7)) << 4);
+      sts64(hi + off, hw[u][0], hw[u][1]);
+      if (kSplit) sts64(lo + off, lw[u][0], lw[u][1]);
+    }
   }
 }
 
@@ -219,7 +235,6 @@ struct FwdArgs {
   float scale;          // 1/(number of rows in the mean)
   float* logits;        // [rows]
   float* part_head;     // [grid*4][129]: sum dz*H (128), sum dz
-  float* part_db;       // [grid*4][128]: colsum(G)
   double* loss_part;    // [grid]
   int want_wgrad;
   unsigned long long* trace;
@@ -347,7 +362,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
     const int cb = 64 * h;
     const uint32_t stg = smem_u32(sStg) + e * kStg;
     float gacc[2] = {0.f, 0.f};   // head: sum dz*H, columns cb + 32c + lane
-    float dbacc[2] = {0.f, 0.f};  // head: colsum(G)
     float gbacc = 0.f;
     double lacc = 0.0;
     for (int i = 0; i < nmine; ++i) {
@@ -427,10 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
 #pragma unroll
           for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
           stage_words(stg, lane, c, hw);
-          if (a.want_wgrad) {
-            gacc[c] += colsum32(g, lane);
-            dbacc[c] += colsum32(v, lane);
-          }
+          if (a.want_wgrad) gacc[c] += colsum32(g, lane);
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
@@ -450,10 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
       const int64_t pq = (int64_t)blockIdx.x * 4 + q;
       if (a.want_wgrad) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          a.part_head[pq * 129 + cb + 32 * c + lane] = gacc[c];
-          a.part_db[pq * 128 + cb + 32 * c + lane] = dbacc[c];
-        }
+        for (int c = 0; c < 2; ++c) a.part_head[pq * 129 + cb + 32 * c + lane] = gacc[c];
       }
 #pragma unroll
       for (int w = 16; w >= 1; w >>= 1) {
@@ -494,7 +502,7 @@ struct BwdArgs {
   uint8_t* Gout;        // G_l plane tiles (not first)
   float* dy;            // [rows][2] (first, no wgrad)
   float* part;          // [grid][128][128] dW_l partials (wgrad)
-  float* part_db;       // [grid*4][128] colsum(G_l) (not first, wgrad)
+  float* part_db;       // [grid][128] db_l partials (wgrad)
   float* part_l0;       // [grid*4][384] dW_0 (256, row-major) + db_0 (128) (first, wgrad)
   unsigned long long* trace;
 };
@@ -518,7 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
   uint64_t* tempty = bars + 8;  // [2]
   uint64_t* wdone = bars + 10;  // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  Params0* p0 = reinterpret_cast<Params0*>(tmem_slot + 4);  // (first)
+  uint32_t* sOnes = tmem_slot + 4;                           // 512 B of bf16 1.0 (db MMA operand)
+  Params0* p0 = reinterpret_cast<Params0*>(sOnes + 128);    // (first)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -535,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
+  for (int i = tid; i < 128; i += kThreads) sOnes[i] = 0x3F803F80u;
   if (kFirst) {
     for (int i = tid; i < 128; i += kThreads) {
       p0->w0x[i] = a.W0[2 * i];
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t acc_w = tmem + 256;
+  const uint32_t acc_w = tmem + 256, acc_b = tmem + 384;
   const int64_t ntiles = (a.rows + 127) / 128;
   const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   auto tile_of = [&](int i) { return blockIdx.x + (int64_t)i * gridDim.x; };
@@ -607,6 +617,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     if (lane == 0) {
       constexpr uint32_t id_d = make_idesc_bf16(128, 128, 0, 1);  // A = G (K-major), B = W (MN-major)
       constexpr uint32_t id_w = make_idesc_bf16(128, 128, 1, 1);  // A = G^T, B = H (both MN-major)
+      constexpr uint32_t id_b = make_idesc_bf16(128, 16, 1, 0);   // A = G^T, B = ones (K-major)
+      const uint64_t ones = make_desc(smem_u32(sOnes), 128, 256, 0);  // no swizzle: any layout reads 1.0
       const uint32_t wh = smem_u32(sW), wl = wh + kPlane;
       const uint32_t hh = smem_u32(sH), hl = hh + kPlane;
       for (int i = 0; i < nmine; ++i) {
@@ -621,9 +633,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const uint32_t km = k * 2048;  // MN-major step (16 rows)
-            mma_step<kSplit>(acc_w, make_desc(zh + km, 16384, 1024), make_desc(zl + km, 16384, 1024),
-                             make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024), id_w,
-                             (i > 0 || k > 0) ? 1u : 0u);
+            const uint32_t acc0 = (i > 0 || k > 0) ? 1u : 0u;
+            const uint64_t gh = make_desc(zh + km, 16384, 1024), gl = make_desc(zl + km, 16384, 1024);
+            mma_step<kSplit>(acc_w, gh, gl, make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024), id_w,
+                             acc0);
+            mma_bf16(acc_b, gh, ones, id_b, acc0);
+            if (kSplit) mma_bf16(acc_b, gl, ones, id_b, 1);
           }
           mma_commit(&emptyH[0]);
         }
@@ -653,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     const int cb = 64 * h;
     const uint32_t stg = smem_u32(sStg) + e * kStg;
     float2* pdy = reinterpret_cast<float2*>(sStg);  // dy: [2][128] partial dots
-    float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, sb[2] = {0.f, 0.f};  // l0 grads / colsum(G_l)
+    float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, sb[2] = {0.f, 0.f};  // layer-0 gradients
     const float2* X2 = reinterpret_cast<const float2*>(a.X);
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
@@ -686,7 +701,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
 #pragma unroll
           for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
           stage_words(stg, lane, c, hw);
-          if (kWgrad) sb[c] += colsum32(v, lane);
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
@@ -745,10 +759,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     }
     if (lane == 0) bulk_wait0();
     const int64_t pq = (int64_t)blockIdx.x * 4 + q;
-    if (kWgrad && !kFirst) {
-#pragma unroll
-      for (int c = 0; c < 2; ++c) a.part_db[pq * 128 + cb + 32 * c + lane] = sb[c];
-    }
     if (kWgrad && kFirst) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -777,6 +787,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       } else {
         for (int k = 0; k < 64; k += 4) *reinterpret_cast<float4*>(dst + cb + k) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      if (h == 0) {
+        float v[32];
+        if (nmine > 0) tmem_ld32(acc_b + ((uint32_t)(32 * q) << 16), v);
+        a.part_db[(int64_t)blockIdx.x * 128 + o] = nmine > 0 ? v[0] : 0.f;
+      }
     }
   }
   tc_fence_before();
@@ -788,13 +803,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
 }
 
 // ============================================================== partial sums
-// out[j] = sum_p part[p*ld + j] (fixed order), j < n
-__global__ void k_sum_parts(const float* __restrict__ part, int nparts, int64_t ld, int n, float* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+// out[j] = sum_p part[p*ld + j], j < n: 32 outputs x 8 part groups per block
+// (group g sums parts g, g+8, ... in order; the 8 group sums are added in
+// order -- deterministic)
+__global__ void __launch_bounds__(256) k_sum_parts(const float* __restrict__ part, int nparts, int64_t ld, int n,
+                                                   float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int jl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + jl;
   float s = 0.f;
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * ld + j];
-  out[j] = s;
+  if (j < n) {
+#pragma unroll 4
+    for (int p = g; p < nparts; p += 8) s += __ldg(part + (int64_t)p * ld + j);
+  }
+  red[g][jl] = s;
+  __syncthreads();
+  if (g == 0 && j < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][jl];
+    out[j] = t;
+  }
 }
 
 // ============================================================== host
@@ -815,7 +844,7 @@ static size_t fwd_smem(bool split) {
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 12 * 8 + 16 + sizeof(Params0);
+  return 3 * TB + kEW * kStg + 12 * 8 + 16 + 512 + sizeof(Params0);
 }
 
 template <typename K>
@@ -868,7 +897,7 @@ void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
   a.A = L.A; a.X = L.X; a.W0 = L.W0; a.b0 = L.b0; a.W = L.W; a.bias = L.bias; a.C = L.C; a.mask = L.mask;
   a.rows = L.rows; a.alpha = L.alpha; a.w_head = L.w_head; a.b_head = L.b_head; a.n_real = L.n_real;
   a.label_rest = L.label_rest; a.scale = L.scale; a.logits = L.logits; a.part_head = L.part_head;
-  a.part_db = L.part_db; a.loss_part = L.loss_part; a.want_wgrad = L.want_wgrad;
+  a.loss_part = L.loss_part; a.want_wgrad = L.want_wgrad;
   a.trace = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = fwd_smem(split);
@@ -907,7 +936,7 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
 }
 
 void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st) {
-  k_sum_parts<<<(n + 127) / 128, 128, 0, st>>>(part, nparts, ld, n, out);
+  k_sum_parts<<<(n + 31) / 32, 256, 0, st>>>(part, nparts, ld, n, out);
   count_launch();
 }
 

@@ -103,6 +103,7 @@ static void carve(sagips_ctx* c, char* base) {
   c->colpart = cv.take<float>(std::max<int64_t>((int64_t)std::max(296, kMaxSms) * std::max(128, std::max(D.maxw, G.maxw)),
                                                 (int64_t)kMaxSms * 4 * 384));
   c->head_tmp = cv.take<float>(D.maxw + 1);
+  c->dbpart = cv.take<float>((int64_t)kMaxSms * 128);
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
   c->ws_bytes = cv.off;
@@ -391,7 +392,7 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
   h.rows = rows; h.alpha = c->cfg.leaky_slope;
   h.w_head = c->dW + D.w_off[Lh]; h.b_head = c->dB + D.b_off[Lh];
   h.n_real = n_real; h.label_rest = label_rest; h.scale = scale;
-  h.logits = logits; h.C = reinterpret_cast<uint8_t*>(c->dZb[0]); h.part_head = c->part; h.part_db = c->colpart;
+  h.logits = logits; h.C = reinterpret_cast<uint8_t*>(c->dZb[0]); h.part_head = c->part;
   h.loss_part = c->loss_part; h.want_wgrad = want_grads ? 1 : 0;
   launch_tc_fwd(split, FWD_HEAD, h, st);
 }
@@ -403,29 +404,27 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const bool split = tc_split(c);
   const int grid = tc_layers_grid(rows);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
-  // head: dW (128) + db (1); colsum of G_{Lh} -> db of the last hidden layer
+  // head: dW (128) + db (1)
   launch_sum_parts(c->part, 4 * grid, 129, 128, c->d_dW + D.w_off[Lh], st);
   launch_sum_parts(c->part + 128, 4 * grid, 129, 1, c->d_dB + D.b_off[Lh], st);
-  launch_sum_parts(c->colpart, 4 * grid, 128, 128, c->d_dB + D.b_off[Lh - 1], st);
   launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
     b.G = reinterpret_cast<const uint8_t*>(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
-    b.alpha = c->cfg.leaky_slope; b.part = c->part;
+    b.alpha = c->cfg.leaky_slope; b.part = c->part; b.part_db = c->dbpart;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
     } else {
       b.H = reinterpret_cast<const uint8_t*>(c->dAct[l - 1]); b.mask = c->dMask[l - 1];
-      b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]); b.part_db = c->colpart;
+      b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]);
     }
     launch_tc_bwd(split, l == 1, true, b, st);
     launch_sum_parts(c->part, grid, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
+    launch_sum_parts(c->dbpart, grid, 128, 128, c->d_dB + D.b_off[l], st);
     if (l == 1) {  // dW_0 [128][2] row-major, db_0
       launch_sum_parts(c->colpart, 4 * grid, 384, 256, c->d_dW + D.w_off[0], st);
       launch_sum_parts(c->colpart + 256, 4 * grid, 384, 128, c->d_dB + D.b_off[0], st);
-    } else {
-      launch_sum_parts(c->colpart, 4 * grid, 128, 128, c->d_dB + D.b_off[l - 1], st);
     }
     cur ^= 1;
   }
