@@ -56,6 +56,13 @@ struct sagips_ctx {
   float* colpart = nullptr;
   float* head_tmp = nullptr;
   float* dbpart = nullptr;  // [grid][128] bias-gradient partials (tcgen05 layers)
+  // pipelined step (k_pipe): rings G4, G3, G2 (ring[2..4]); H2, H3 use dAct; per-tile flags
+  static constexpr int kRingG = 256;
+  uint8_t* ring[5] = {};
+  uint32_t* flags = nullptr;
+  float* pipe_part[3] = {};
+  float* pipe_db[3] = {};
+  bool pipe_ok = true;
   double* loss_part = nullptr;
   sagips_step_stats* stats = nullptr;
   // step bookkeeping

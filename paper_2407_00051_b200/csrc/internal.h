@@ -70,17 +70,32 @@ int tc_wgrad_grid();
 void launch_tc_wgrad(bool split, const float* dZ, const float* H, int64_t rows, float* part, float* part_db,
                      cudaStream_t st);
 
-// k_tc_layers.cu (warp-specialised tcgen05 layer passes on bf16 plane tiles,
-// disc_depth >= 3; see the file header for the tensor formats)
+// k_tc_layers.cu: warp-specialised tcgen05 layer passes on bf16 plane tiles
+// (disc_depth >= 3; see the file header for the tensor formats), as one
+// kernel per layer pass or as one pipelined kernel for the whole D / G step.
+//
+// A tensor of plane tiles: the whole tensor (slots == 0: tile t at t*TB) or a
+// ring of `slots` tiles (tile t in slot t % slots) with per-tile counters:
+// rdy[t] counts producer epilogue warps whose stores of tile t are complete
+// (ready at 8), done[t] counts consumer completions (the slot may be
+// overwritten by tile t + slots once done[t] == done_target).
+struct Ring {
+  uint8_t* base = nullptr;
+  uint4* mask = nullptr;      // sign masks (hidden activations), [slots or tiles][128]
+  uint32_t slots = 0;
+  uint32_t* rdy = nullptr;
+  uint32_t* done = nullptr;
+  uint32_t done_target = 0;
+};
 struct FwdLaunch {
-  const uint8_t* A = nullptr;  // input plane tiles (mid, head)
+  Ring in;                     // input plane tiles (mid, head)
+  Ring out;                    // output plane tiles (H + mask; head: G)
+  Ring h1;                     // first, pipelined D step: H_1 planes for the backward (base == nullptr: none)
   const float* X = nullptr;    // [rows][2] (first)
   const float* W0 = nullptr;   // [128][2] (first)
   const float* b0 = nullptr;   // [128] (first)
   const float* W = nullptr;    // [128][128]
   const float* bias = nullptr;
-  uint8_t* C = nullptr;        // output plane tiles (H; head: G)
-  uint4* mask = nullptr;       // sign masks of H (first, mid)
   int64_t rows = 0;
   float alpha = 0.01f;
   const float* w_head = nullptr;
@@ -89,25 +104,24 @@ struct FwdLaunch {
   float label_rest = 0.f;
   float scale = 1.f;
   float* logits = nullptr;
-  float* part_head = nullptr;  // [grid*4][129]
-  double* loss_part = nullptr;
+  float* part_head = nullptr;  // [ctas*4][129]
+  double* loss_part = nullptr; // [ctas]
   int want_wgrad = 0;
 };
 struct BwdLaunch {
-  const uint8_t* G = nullptr;  // G_{l+1} plane tiles
-  const uint8_t* H = nullptr;  // H_l plane tiles (wgrad, not first)
-  const uint4* mask = nullptr; // sign masks of H_l (not first)
+  Ring g;                      // G_{l+1} plane tiles
+  Ring h;                      // H_l plane tiles (wgrad, not first) + masks (not first)
+  Ring gout;                   // G_l plane tiles (not first)
   const float* X = nullptr;
   const float* W0 = nullptr;
   const float* b0 = nullptr;
   const float* W = nullptr;
   int64_t rows = 0;
   float alpha = 0.01f;
-  uint8_t* Gout = nullptr;     // G_l plane tiles (not first)
   float* dy = nullptr;         // (first, no wgrad)
-  float* part = nullptr;       // [grid][128][128]
-  float* part_db = nullptr;    // [grid][128]
-  float* part_l0 = nullptr;    // [grid*4][384]
+  float* part = nullptr;       // [ctas][128][128]
+  float* part_db = nullptr;    // [ctas][128]
+  float* part_l0 = nullptr;    // [ctas*4][384]
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
 int tc_layers_grid(int64_t rows);
@@ -117,6 +131,17 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
 void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st);
 size_t tc_trace_bytes();
 int tc_trace_copy(void* host);
+// the pipelined step (disc_depth == 4): roles first, mid, head, bwd3, bwd2, bwd1
+constexpr int kPipeRoles = 6;
+struct PipeLaunch {
+  FwdLaunch f[3];
+  BwdLaunch b[3];              // b[0] = layer 3, b[1] = layer 2, b[2] = layer 1
+  int ctas[kPipeRoles];
+  unsigned long long* trace[kPipeRoles] = {};
+  unsigned long long* waits = nullptr;  // [grid][8] wait accounting (tracing only)
+};
+int pipe_sm_count();
+bool launch_tc_pipe(bool split, bool dstep, const PipeLaunch& L, cudaStream_t st);
 
 // k_adam.cu
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,

@@ -201,11 +201,11 @@ __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0
 // for CTAs 0..3: 0 operands staged, 1 MMA started, 2 epilogue got the
 // accumulator, 3 epilogue released it.
 constexpr int kTraceLaunches = 32, kTraceCtas = 4, kTraceTiles = 256;
-__device__ __forceinline__ void trace_pt(unsigned long long* tr, int i, int k) {
-  if (tr && blockIdx.x < kTraceCtas && i < kTraceTiles) {
+__device__ __forceinline__ void trace_pt(unsigned long long* tr, int j, int i, int k) {
+  if (tr && j < kTraceCtas && i < kTraceTiles) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    tr[((size_t)blockIdx.x * kTraceTiles + i) * 4 + k] = t;
+    tr[((size_t)j * kTraceTiles + i) * 4 + k] = t;
   }
 }
 
@@ -213,35 +213,112 @@ __device__ __forceinline__ void check_smem_alignment(const void* p) {
   if (smem_u32(p) & 1023u) __trap();  // SW128 operands need 1024-byte alignment
 }
 
+// ---- inter-CTA dataflow (the pipelined step, k_pipe): plane tiles pass
+// between layer roles through ring buffers in global memory (L2-resident);
+// per-tile counters carry release/acquire ordering.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// relaxed poll (an acquire load invalidates the SM's L1 on every poll)
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// spin (relaxed) until *p >= target, then one acquire load; a dataflow stall
+// of > 4 s is a bug -> trap (no hang)
+__device__ __noinline__ void wait_flag(const uint32_t* p, uint32_t target) {
+  if (ld_relaxed(p) < target) {
+    const unsigned long long t0 = globaltimer();
+    while (ld_relaxed(p) < target) {
+      __nanosleep(64);
+      if (globaltimer() - t0 > 4000000000ull) __trap();
+    }
+  }
+  (void)ld_acquire(p);
+}
+// ---- wait accounting (SAGIPS_TRACE=1, pipelined step): ns per CTA spent in
+// 0 loader: upstream tile ready  1 loader: stage free  2 MMA: operands  3 MMA:
+// accumulator free  4 epilogue: output slot free  5 epilogue: accumulator  6
+// epilogue: mask ready  7 CTA wall time (thread 0)
+struct WaitAcct {
+  unsigned long long* w;  // [8] of this CTA, or nullptr
+};
+#define SAGIPS_TIMED(acct, k, expr)                                   \
+  do {                                                                \
+    if ((acct).w) {                                                   \
+      const unsigned long long t0_ = globaltimer();                   \
+      expr;                                                           \
+      atomicAdd((acct).w + (k), globaltimer() - t0_);                 \
+    } else {                                                          \
+      expr;                                                           \
+    }                                                                 \
+  } while (0)
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_groups() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+}  // namespace
+
+namespace {
+__device__ __forceinline__ int64_t ring_slot(const Ring& r, int64_t t) { return r.slots ? t % r.slots : t; }
+
+// producer side: is the slot of tile t free right now?
+__device__ __forceinline__ bool ring_slot_free(const Ring& r, int64_t t) {
+  return !r.slots || t < (int64_t)r.slots || ld_relaxed(r.done + (t - r.slots)) >= r.done_target;
+}
+// producer side: wait until tile t may be written (slot free); whole warp
+__device__ __forceinline__ void ring_acquire_slot(const Ring& r, int64_t t, int lane, WaitAcct wa = {}) {
+  if (r.slots && t >= (int64_t)r.slots) {
+    if (lane == 0) {
+      SAGIPS_TIMED(wa, 4, wait_flag(r.done + (t - r.slots), r.done_target));
+      fence_proxy_async_global();
+    }
+    __syncwarp();
+  }
+}
+// producer side: publish tile `pend` once its bulk stores are complete.
+// kKeep = bulk groups of later tiles that may stay in flight.
+template <int kKeep>
+__device__ __forceinline__ void ring_publish(const Ring& r, int64_t pend, int lane) {
+  if (r.rdy && pend >= 0 && lane == 0) {
+    bulk_wait_groups<kKeep>();
+    fence_proxy_async_global();
+    red_release_add(r.rdy + pend, 1);
+  }
+}
+// consumer side (single thread): wait for tile t, then order later async-proxy reads
+__device__ __forceinline__ void ring_wait_ready(const Ring& r, int64_t t, WaitAcct wa = {}) {
+  if (r.rdy) {
+    SAGIPS_TIMED(wa, 0, wait_flag(r.rdy + t, kEW));
+    fence_proxy_async_global();
+  }
+}
+__device__ __forceinline__ void ring_consumed(const Ring& r, int64_t t) {
+  if (r.done) red_release_add(r.done + t, 1);
+}
+
 }  // namespace
 
 // ============================================================== forward
-struct FwdArgs {
-  const uint8_t* A;     // input plane tiles (mid, head)
-  const float* X;       // [rows][2] (first)
-  const float* W0;      // [128][2] (first)
-  const float* b0;      // [128] (first)
-  const float* W;       // [128][128] this layer
-  const float* bias;    // [128]
-  uint8_t* C;           // output plane tiles (mid, first: H; head: G)
-  uint4* mask;          // [tiles*128] sign masks of H (mid, first)
-  int64_t rows;
-  float alpha;
-  // head
-  const float* w_head;  // [128]
-  const float* b_head;  // [1]
-  int64_t n_real;       // rows < n_real carry label 1, the rest label_rest
-  float label_rest;
-  float scale;          // 1/(number of rows in the mean)
-  float* logits;        // [rows]
-  float* part_head;     // [grid*4][129]: sum dz*H (128), sum dz
-  double* loss_part;    // [grid]
-  int want_wgrad;
-  unsigned long long* trace;
-};
-
+// Body of one forward layer role.  This CTA is number j of n CTAs of the
+// role and processes tiles j, j + n, j + 2n, ...
 template <bool kSplit, bool kFirst, bool kHead>
-__global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
+__device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsigned long long* trace,
+                                         WaitAcct wa = {}) {
   constexpr int P = kSplit ? 2 : 1;
   constexpr uint32_t TB = P * kPlane;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -271,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
     }
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc<256>(tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   for (int i = tid; i < 128; i += kThreads) {
     sbias[i] = a.bias[i];
     if (kHead) swh[i] = a.w_head[i];
@@ -288,8 +365,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t ntiles = (a.rows + 127) / 128;
-  const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  auto tile_of = [&](int i) { return blockIdx.x + (int64_t)i * gridDim.x; };
+  const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
+  auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
 
   if (warp < kPW) {
     // ---------------- SIMT producers of H_1 (first layer only)
@@ -304,18 +381,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
       };
       bool ok;
       float2 xr = load_x(0, ok);
+      const bool store_h1 = a.h1.base != nullptr;  // D step, pipelined: the backward reads H_1 planes
+      int64_t pend = -1;
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1;
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
+        if (store_h1) {
+          // the stage about to be rewritten must have been read by its bulk
+          // store (two tiles ago; the previous tile's store may be in flight)
+          if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+        }
         mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
         const uint32_t st = smem_u32(sA + s * TB);
         produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, warp, lane);
         fence_proxy_async_smem();
         mbar_arrive(&full[s]);
-        if (warp == 0 && lane == 0) trace_pt(a.trace, i, 0);
+        if (store_h1) {
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+          if (tid == 0) {
+            bulk_s2g(a.h1.base + tile_of(i) * TB, st, TB);
+            bulk_commit();
+            if (pend >= 0) {  // publish the previous tile once its store is complete
+              bulk_wait_groups<1>();
+              fence_proxy_async_global();
+              red_release_add(a.h1.rdy + pend, kEW);
+            }
+          }
+          pend = tile_of(i);
+        }
+        if (warp == 0 && lane == 0) trace_pt(trace, j, i, 0);
         xr = xn;
         ok = ok_next;
+      }
+      if (store_h1 && tid == 0) {
+        bulk_wait0();
+        if (pend >= 0) {
+          fence_proxy_async_global();
+          red_release_add(a.h1.rdy + pend, kEW);
+        }
       }
     }
   } else if (warp == kLoadWarp) {
@@ -323,11 +428,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
     if (!kFirst && lane == 0) {
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1;
-        if (i + 1 < nmine) prefetch_l2(a.A + tile_of(i + 1) * TB, TB);
-        mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
+        const int64_t t = tile_of(i);
+        if (!a.in.slots && i + 1 < nmine) prefetch_l2(a.in.base + tile_of(i + 1) * TB, TB);
+        ring_wait_ready(a.in, t, wa);
+        SAGIPS_TIMED(wa, 1, mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1));
         mbar_arrive_expect_tx(&full[s], TB);
-        bulk_g2s(smem_u32(sA + s * TB), a.A + tile_of(i) * TB, TB, &full[s]);
-        trace_pt(a.trace, i, 0);
+        bulk_g2s(smem_u32(sA + s * TB), a.in.base + ring_slot(a.in, t) * TB, TB, &full[s]);
+        trace_pt(trace, j, i, 0);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -337,9 +444,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
       const uint32_t bh = smem_u32(sW), bl = bh + kPlane;
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1, b = i & 1;
-        mbar_wait(&full[s], (i >> 1) & 1);
-        mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
-        trace_pt(a.trace, i, 1);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&full[s], (i >> 1) & 1));
+        if (!kFirst) ring_consumed(a.in, tile_of(i));  // the input slot has been read
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(sA + s * TB), al = ah + kPlane;
         const uint32_t d = tmem + (uint32_t)(b * 128);
@@ -364,14 +472,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
     float gacc[2] = {0.f, 0.f};   // head: sum dz*H, columns cb + 32c + lane
     float gbacc = 0.f;
     double lacc = 0.0;
+    int64_t pend = -1;            // tile whose stores are in flight, not yet published
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int b = i & 1;
       const int64_t row = t * 128 + 32 * q + lane;
       const bool valid = row < a.rows;
-      uint8_t* dst = a.C + t * TB + h * 16384 + q * 4096;
-      mbar_wait(&tfull[b], (i >> 1) & 1);
-      if (e == 0 && lane == 0) trace_pt(a.trace, i, 2);
+      const int64_t slot = ring_slot(a.out, t);
+      uint8_t* dst = a.out.base + slot * TB + h * 16384 + q * 4096;
+      // the previous tile is published after this tile's stores are issued
+      // (its own stores have completed by then), unless this tile has to
+      // wait for a free output slot: then publish first, or ring back-pressure
+      // would feed into the pipeline latency
+      {
+        bool free_now = true;
+        if (lane == 0) free_now = ring_slot_free(a.out, t);
+        if (!__shfl_sync(0xffffffffu, free_now ? 1 : 0, 0)) {
+          ring_publish<0>(a.out, pend, lane);
+          pend = -1;
+        }
+      }
+      ring_acquire_slot(a.out, t, lane, lane == 0 ? wa : WaitAcct{});
+      SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+      if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128 + cb) + ((uint32_t)(32 * q) << 16);
       uint32_t lo[32];
@@ -397,9 +520,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
+        // mask stores, then flush_stage's __syncwarp orders them before lane
+        // 0's later release of this tile
+        reinterpret_cast<uint2*>(a.out.mask + slot * 128 + 32 * q + lane)[h] = make_uint2(mb[0], mb[1]);
         flush_stage(stg, dst, lane);
-        reinterpret_cast<uint2*>(a.mask + t * 128 + 32 * q + lane)[h] = make_uint2(mb[0], mb[1]);
       } else {
         // pass 1: partial z = H . w over this warp's 64 columns
         float dot = 0.f;
@@ -445,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
         flush_stage(stg, dst, lane);
       }
       if (kSplit) {
@@ -454,11 +579,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
         stage_words(stg, lane, 1, lo + 16);
         flush_stage(stg, dst + kPlane, lane);
       }
+      ring_publish<P>(a.out, pend, lane);  // the previous tile's stores are complete
+      pend = t;
     }
     if (lane == 0) bulk_wait0();
+    ring_publish<0>(a.out, pend, lane);
     if (kHead) {
       // per-(CTA, lane quarter) partials; loss per CTA in fp64, fixed order
-      const int64_t pq = (int64_t)blockIdx.x * 4 + q;
+      const int64_t pq = (int64_t)j * 4 + q;
       if (a.want_wgrad) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) a.part_head[pq * 129 + cb + 32 * c + lane] = gacc[c];
@@ -474,9 +602,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
       }
       epi_sync();
       if (e == 0 && lane == 0) {
-        double s = 0.0;
-        for (int j = 0; j < kEW; ++j) s += sloss[j];
-        a.loss_part[blockIdx.x] = s;
+        double sum = 0.0;
+        for (int k = 0; k < kEW; ++k) sum += sloss[k];
+        a.loss_part[j] = sum;
       }
     }
   }
@@ -484,39 +612,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(FwdArgs a) {
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
 // ============================================================== backward
-struct BwdArgs {
-  const uint8_t* G;     // G_{l+1} plane tiles
-  const uint8_t* H;     // H_l plane tiles (wgrad, not first)
-  const uint4* mask;    // sign mask of H_l (not first)
-  const float* X;       // [rows][2] (first)
-  const float* W0;      // [128][2] (first)
-  const float* b0;      // [128] (first)
-  const float* W;       // [128][128] W_l
-  int64_t rows;
-  float alpha;
-  uint8_t* Gout;        // G_l plane tiles (not first)
-  float* dy;            // [rows][2] (first, no wgrad)
-  float* part;          // [grid][128][128] dW_l partials (wgrad)
-  float* part_db;       // [grid][128] db_l partials (wgrad)
-  float* part_l0;       // [grid*4][384] dW_0 (256, row-major) + db_0 (128) (first, wgrad)
-  unsigned long long* trace;
-};
-
-template <bool kSplit, bool kFirst, bool kWgrad>
-__global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
+// kH1Load (first layer, wgrad): the H_1 planes are bulk-loaded (written by the
+// pipelined forward first-layer role) instead of recomputed by SIMT producers
+template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
+__device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsigned long long* trace,
+                                         WaitAcct wa = {}) {
   constexpr int P = kSplit ? 2 : 1;
   constexpr uint32_t TB = P * kPlane;
   constexpr bool kDy = kFirst && !kWgrad;
+  // kPR (wgrad, split): operands move as 32 KiB planes through plane slots
+  // with their own barriers, so the next tile's planes load while this
+  // tile's MMAs run (see the MMA issuer for the order)
+  constexpr bool kPR = kSplit && kWgrad;
+  constexpr bool kLoadH = kWgrad && (!kFirst || kH1Load);  // H planes come from global memory
+  constexpr bool kFifoG = kFirst && !kH1Load;               // plane slots: H_1 fixed, G FIFO
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
-  uint8_t* sG = sW + TB;     // G stage 0
-  uint8_t* sH = sG + TB;     // H stage (wgrad) or G stage 1
-  uint8_t* sStg = sH + TB;   // 8 x 4 KiB (dy: the partial-dot exchange)
+  uint8_t* sG = sW + TB;     // G stage 0 (kPR: plane slots 0, 1)
+  uint8_t* sH = sG + TB;     // H stage (wgrad) or G stage 1 (kPR: plane slots 2, 3)
+  uint8_t* sStg = sH + TB;   // 8 x 4 KiB (dy: the partial-dot exchange; kPR first: plane slot 4)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + kEW * kStg);
   uint64_t* fullG = bars;       // [2]
   uint64_t* emptyG = bars + 2;  // [2]
@@ -525,7 +644,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
   uint64_t* tfull = bars + 6;   // [2]
   uint64_t* tempty = bars + 8;  // [2]
   uint64_t* wdone = bars + 10;  // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* pfull = bars + 12;  // [5] (kPR)
+  uint64_t* pempty = bars + 17; // [5] (kPR)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
   uint32_t* sOnes = tmem_slot + 4;                           // 512 B of bf16 1.0 (db MMA operand)
   Params0* p0 = reinterpret_cast<Params0*>(sOnes + 128);    // (first)
 
@@ -538,9 +659,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * kEW);
     }
-    mbar_init(&fullH[0], kFirst ? 32 * kPW : 1);
+    mbar_init(&fullH[0], kLoadH ? 1 : 32 * kPW);
     mbar_init(&emptyH[0], 1);
     mbar_init(&wdone[0], 1);
+    for (int k = 0; k < 5; ++k) {
+      mbar_init(&pfull[k], (kFifoG && k < 2) ? 32 * kPW : 1);  // H_1 planes in slots 0, 1 (producers)
+      mbar_init(&pempty[k], 1);
+    }
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
@@ -560,14 +685,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
   const uint32_t tmem = *tmem_slot;
   const uint32_t acc_w = tmem + 256, acc_b = tmem + 384;
   const int64_t ntiles = (a.rows + 127) / 128;
-  const int nmine = ntiles > blockIdx.x ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
-  auto tile_of = [&](int i) { return blockIdx.x + (int64_t)i * gridDim.x; };
+  const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
+  auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
   // G stage of tile i: wgrad -> single stage; else a ring of 2 (sG, sH)
   auto g_stage = [&](int i) -> uint8_t* { return (!kWgrad && (i & 1)) ? sH : sG; };
+  // kPR plane slots {slot, use}: use = how many times the slot was filled before
+  //   mid:   Gh, Hh, Hl rotate through slots 0-2 (period 3), Gl in slot 3
+  //   first: Hh, Hl in slots 0, 1 (SIMT producers); Gh, Gl a FIFO over slots 2-4
+  struct PS {
+    int slot, use;
+  };
+  auto pl_gh = [&](int i) -> PS { return kFifoG ? PS{2 + (2 * i) % 3, (2 * i) / 3} : PS{(3 - i % 3) % 3, i}; };
+  auto pl_gl = [&](int i) -> PS { return kFifoG ? PS{2 + (2 * i + 1) % 3, (2 * i + 1) / 3} : PS{3, i}; };
+  auto pl_hh = [&](int i) -> PS { return kFifoG ? PS{0, i} : PS{(4 - i % 3) % 3, i}; };
+  auto pl_hl = [&](int i) -> PS { return kFifoG ? PS{1, i} : PS{(5 - i % 3) % 3, i}; };
+  auto pl_addr = [&](int slot) -> uint32_t { return smem_u32(sG) + (uint32_t)slot * kPlane; };
 
   if (warp < kPW) {
     // ---------------- SIMT producers of H_1 planes (first layer, wgrad)
-    if (kFirst && kWgrad) {
+    if (kFirst && kWgrad && !kH1Load) {
       const float2* X2 = reinterpret_cast<const float2*>(a.X);
       auto load_x = [&](int i, bool& ok) {
         ok = false;
@@ -578,38 +714,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       };
       bool ok;
       float2 xr = load_x(0, ok);
-      const uint32_t hh = smem_u32(sH);
+      const uint32_t hh = kPR ? pl_addr(0) : smem_u32(sH);
+      const uint32_t hl = kPR ? pl_addr(1) : smem_u32(sH) + kPlane;
       for (int i = 0; i < nmine; ++i) {
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
-        mbar_wait(&emptyH[0], (i & 1) ^ 1);
-        produce_h1<kSplit>(xr, ok, p0, a.alpha, hh, hh + kPlane, warp, lane);
+        if (kPR) {
+          mbar_wait(&pempty[0], (i & 1) ^ 1);
+          mbar_wait(&pempty[1], (i & 1) ^ 1);
+        } else {
+          mbar_wait(&emptyH[0], (i & 1) ^ 1);
+        }
+        produce_h1<kSplit>(xr, ok, p0, a.alpha, hh, hl, warp, lane);
         fence_proxy_async_smem();
-        mbar_arrive(&fullH[0]);
+        if (kPR) {
+          mbar_arrive(&pfull[0]);
+          mbar_arrive(&pfull[1]);
+        } else {
+          mbar_arrive(&fullH[0]);
+        }
         xr = xn;
         ok = ok_next;
       }
     }
   } else if (warp == kLoadWarp) {
     // ---------------- bulk loader
-    if (lane == 0) {
+    if (kPR && lane == 0) {
+      auto load = [&](PS ps, const uint8_t* src) {
+        SAGIPS_TIMED(wa, 1, mbar_wait(&pempty[ps.slot], (ps.use & 1) ^ 1));
+        mbar_arrive_expect_tx(&pfull[ps.slot], kPlane);
+        bulk_g2s(pl_addr(ps.slot), src, kPlane, &pfull[ps.slot]);
+      };
       for (int i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
         if (i + 1 < nmine) {
-          prefetch_l2(a.G + tile_of(i + 1) * TB, TB);
-          if (kWgrad && !kFirst) prefetch_l2(a.H + tile_of(i + 1) * TB, TB);
+          if (!a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
+          if (kLoadH && !a.h.slots && !a.h.rdy) prefetch_l2(a.h.base + tile_of(i + 1) * TB, TB);
         }
-        if (kWgrad && !kFirst) {
-          mbar_wait(&emptyH[0], (i & 1) ^ 1);
+        const uint8_t* gsrc = a.g.base + ring_slot(a.g, t) * TB;
+        ring_wait_ready(a.g, t, wa);
+        load(pl_gh(i), gsrc);
+        if (kLoadH) {
+          const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
+          ring_wait_ready(a.h, t, wa);
+          load(pl_hh(i), hsrc);
+          load(pl_hl(i), hsrc + kPlane);
+        }
+        load(pl_gl(i), gsrc + kPlane);
+        trace_pt(trace, j, i, 0);
+      }
+    } else if (!kPR && lane == 0) {
+      for (int i = 0; i < nmine; ++i) {
+        const int64_t t = tile_of(i);
+        if (i + 1 < nmine) {
+          if (!a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
+          if (kWgrad && !kFirst && !a.h.slots) prefetch_l2(a.h.base + tile_of(i + 1) * TB, TB);
+        }
+        if (kLoadH) {
+          ring_wait_ready(a.h, t, wa);
+          SAGIPS_TIMED(wa, 1, mbar_wait(&emptyH[0], (i & 1) ^ 1));
           mbar_arrive_expect_tx(&fullH[0], TB);
-          bulk_g2s(smem_u32(sH), a.H + t * TB, TB, &fullH[0]);
+          bulk_g2s(smem_u32(sH), a.h.base + ring_slot(a.h, t) * TB, TB, &fullH[0]);
         }
         const int s = kWgrad ? 0 : (i & 1);
         const uint32_t ph = kWgrad ? ((i & 1) ^ 1) : (((i >> 1) & 1) ^ 1);
-        mbar_wait(&emptyG[s], ph);
+        ring_wait_ready(a.g, t, wa);
+        SAGIPS_TIMED(wa, 1, mbar_wait(&emptyG[s], ph));
         mbar_arrive_expect_tx(&fullG[s], TB);
-        bulk_g2s(smem_u32(g_stage(i)), a.G + t * TB, TB, &fullG[s]);
-        trace_pt(a.trace, i, 0);
+        bulk_g2s(smem_u32(g_stage(i)), a.g.base + ring_slot(a.g, t) * TB, TB, &fullG[s]);
+        trace_pt(trace, j, i, 0);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -621,14 +794,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       const uint64_t ones = make_desc(smem_u32(sOnes), 128, 256, 0);  // no swizzle: any layout reads 1.0
       const uint32_t wh = smem_u32(sW), wl = wh + kPlane;
       const uint32_t hh = smem_u32(sH), hl = hh + kPlane;
-      for (int i = 0; i < nmine; ++i) {
+      // kPR order per tile (each plane slot is released right after its last MMA):
+      //  1 Gh.Hh, Gh.1 (wgrad, db)  2 Gh.Hl -> Hl free  3 dgrad Gh.Wh, Gh.Wl -> Gh free
+      //  4 Gl.Hh, Gl.1 -> Hh free  5 dgrad Gl.Wh -> Gl free, accumulator full
+      for (int i = 0; kPR && i < nmine; ++i) {
+        const int64_t t = tile_of(i);
+        const int b = i & 1;
+        const PS gh = pl_gh(i), gl = pl_gl(i), ph = pl_hh(i), pl = pl_hl(i);
+        const uint32_t agh = pl_addr(gh.slot), agl = pl_addr(gl.slot), ahh = pl_addr(ph.slot), ahl = pl_addr(pl.slot);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        trace_pt(trace, j, i, 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
+          const uint64_t g = make_desc(agh + km, 16384, 1024);
+          mma_bf16(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, acc0);
+          mma_bf16(acc_b, g, ones, id_b, acc0);
+        }
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[pl.slot], pl.use & 1));
+        if (kLoadH) ring_consumed(a.h, t);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t km = k * 2048;
+          mma_bf16(acc_w, make_desc(agh + km, 16384, 1024), make_desc(ahl + km, 16384, 1024), id_w, 1);
+        }
+        mma_commit(&pempty[pl.slot]);
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
+          const uint64_t g = make_desc(agh + kk, 16, 1024);
+          mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
+          mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
+        }
+        mma_commit(&pempty[gh.slot]);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
+        ring_consumed(a.g, t);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t km = k * 2048;
+          const uint64_t g = make_desc(agl + km, 16384, 1024);
+          mma_bf16(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, 1);
+          mma_bf16(acc_b, g, ones, id_b, 1);
+        }
+        mma_commit(&pempty[ph.slot]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
+          mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
+        }
+        mma_commit(&pempty[gl.slot]);
+        mma_commit(&tfull[b]);
+      }
+      for (int i = 0; !kPR && i < nmine; ++i) {
+        const int64_t t = tile_of(i);
         const int b = i & 1;
         const int s = kWgrad ? 0 : (i & 1);
-        mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1));
+        SAGIPS_TIMED(wa, 2, mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1)));
+        ring_consumed(a.g, t);
         const uint32_t zh = smem_u32(g_stage(i)), zl = zh + kPlane;
         if (kWgrad) {
           mbar_wait(&fullH[0], i & 1);
-          trace_pt(a.trace, i, 1);
+          if (kLoadH) ring_consumed(a.h, t);
+          trace_pt(trace, j, i, 1);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -642,8 +876,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
           }
           mma_commit(&emptyH[0]);
         }
-        mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1);
-        if (!kWgrad) trace_pt(a.trace, i, 1);
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        if (!kWgrad) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
@@ -670,6 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     float2* pdy = reinterpret_cast<float2*>(sStg);  // dy: [2][128] partial dots
     float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, sb[2] = {0.f, 0.f};  // layer-0 gradients
     const float2* X2 = reinterpret_cast<const float2*>(a.X);
+    int64_t pend = -1;
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int b = i & 1;
@@ -680,14 +915,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       if (kFirst) {
         if (valid) x = __ldg(X2 + row);
       } else {
-        mk = __ldg(reinterpret_cast<const uint2*>(a.mask + row) + h);
+        // sign mask of H_l (written by its producer role with the H planes)
+        if (a.h.rdy) {
+          if (lane == 0) SAGIPS_TIMED(wa, 6, wait_flag(a.h.rdy + t, kEW));
+          __syncwarp();
+        }
+        mk = __ldcg(reinterpret_cast<const uint2*>(a.h.mask + ring_slot(a.h, t) * 128 + 32 * q + lane) + h);
+        {  // see fwd_body
+          bool free_now = true;
+          if (lane == 0) free_now = ring_slot_free(a.gout, t);
+          if (!__shfl_sync(0xffffffffu, free_now ? 1 : 0, 0)) {
+            ring_publish<0>(a.gout, pend, lane);
+            pend = -1;
+          }
+        }
+        ring_acquire_slot(a.gout, t, lane, lane == 0 ? wa : WaitAcct{});
       }
-      mbar_wait(&tfull[b], (i >> 1) & 1);
-      if (e == 0 && lane == 0) trace_pt(a.trace, i, 2);
+      SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+      if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128 + cb) + ((uint32_t)(32 * q) << 16);
       if (!kFirst) {
-        uint8_t* dst = a.Gout + t * TB + h * 16384 + q * 4096;
+        const int64_t slot = ring_slot(a.gout, t);
+        uint8_t* dst = a.gout.base + slot * TB + h * 16384 + q * 4096;
         uint32_t lo[32];
         stage_free(lane);
 #pragma unroll
@@ -704,7 +954,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
+        if (a.h.done) {  // this warp's mask reads are complete
+          __syncwarp();
+          if (lane == 0) red_release_add(a.h.done + t, 1);
+        }
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
         flush_stage(stg, dst, lane);
         if (kSplit) {
           stage_free(lane);
@@ -712,6 +966,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
           stage_words(stg, lane, 1, lo + 16);
           flush_stage(stg, dst + kPlane, lane);
         }
+        ring_publish<P>(a.gout, pend, lane);
+        pend = t;
       } else {
         // G_1 = acc * LeakyReLU'(Z_1), Z_1 = x W_0^T + b_0 recomputed exactly as the producers do
         float d0 = 0.f, d1 = 0.f;
@@ -745,7 +1001,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
         }
         tc_fence_before();
         mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(a.trace, i, 3);
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
         if (kDy) {
           epi_sync();  // previous tile's reads of pdy done
           pdy[h * 128 + 32 * q + lane] = make_float2(d0, d1);
@@ -758,7 +1014,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       }
     }
     if (lane == 0) bulk_wait0();
-    const int64_t pq = (int64_t)blockIdx.x * 4 + q;
+    if (!kFirst) ring_publish<0>(a.gout, pend, lane);
+    const int64_t pq = (int64_t)j * 4 + q;
     if (kWgrad && kFirst) {
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -772,7 +1029,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       // TMEM lane = output feature o, columns = input features; warp (q, h)
       // writes rows 32q.., columns 64h..64h+63 of this CTA's partial
       const int o = 32 * q + lane;
-      float* dst = a.part + (int64_t)blockIdx.x * 128 * 128 + (int64_t)o * 128;
+      float* dst = a.part + (int64_t)j * 128 * 128 + (int64_t)o * 128;
       if (nmine > 0) {
         mbar_wait(&wdone[0], 0);
         tc_fence_after();
@@ -790,7 +1047,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
       if (h == 0) {
         float v[32];
         if (nmine > 0) tmem_ld32(acc_b + ((uint32_t)(32 * q) << 16), v);
-        a.part_db[(int64_t)blockIdx.x * 128 + o] = nmine > 0 ? v[0] : 0.f;
+        a.part_db[(int64_t)j * 128 + o] = nmine > 0 ? v[0] : 0.f;
       }
     }
   }
@@ -800,6 +1057,39 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(BwdArgs a) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
+}
+
+// ============================================================== kernels
+template <bool kSplit, bool kFirst, bool kHead>
+__global__ void __launch_bounds__(kThreads, 1) k_fwd(const __grid_constant__ FwdLaunch a, unsigned long long* trace) {
+  fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace);
+}
+template <bool kSplit, bool kFirst, bool kWgrad>
+__global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ BwdLaunch a, unsigned long long* trace) {
+  bwd_body<kSplit, kFirst, kWgrad>(a, blockIdx.x, gridDim.x, trace);
+}
+
+// The whole D step (kD: wgrad, head and layer-0 gradients) or G step (dy) as
+// one dataflow pipeline: CTAs are partitioned into the six layer roles (first,
+// mid, head, bwd3, bwd2, bwd1), all co-resident (cooperative launch); tiles
+// stream between roles through L2-resident rings.
+template <bool kSplit, bool kD>
+__global__ void __launch_bounds__(kThreads, 1) k_pipe(const __grid_constant__ PipeLaunch a) {
+  int j = blockIdx.x, r = 0;
+  while (r < kPipeRoles - 1 && j >= a.ctas[r]) j -= a.ctas[r++];
+  const int n = a.ctas[r];
+  unsigned long long* tr = a.trace[r];
+  const WaitAcct wa{a.waits ? a.waits + (size_t)blockIdx.x * 8 : nullptr};
+  const unsigned long long t_start = wa.w ? globaltimer() : 0;
+  switch (r) {
+    case 0: fwd_body<kSplit, true, false>(a.f[0], j, n, tr, wa); break;
+    case 1: fwd_body<kSplit, false, false>(a.f[1], j, n, tr, wa); break;
+    case 2: fwd_body<kSplit, false, true>(a.f[2], j, n, tr, wa); break;
+    case 3: bwd_body<kSplit, false, kD>(a.b[0], j, n, tr, wa); break;
+    case 4: bwd_body<kSplit, false, kD>(a.b[1], j, n, tr, wa); break;
+    default: bwd_body<kSplit, true, kD, kD>(a.b[2], j, n, tr, wa); break;
+  }
+  if (wa.w && threadIdx.x == 0) wa.w[7] = globaltimer() - t_start;
 }
 
 // ============================================================== partial sums
@@ -837,6 +1127,7 @@ static int sm_count() {
   }
   return n;
 }
+int pipe_sm_count() { return sm_count(); }
 
 static size_t fwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
@@ -844,7 +1135,7 @@ static size_t fwd_smem(bool split) {
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 12 * 8 + 16 + 512 + sizeof(Params0);
+  return 3 * TB + kEW * kStg + 22 * 8 + 16 + 512 + sizeof(Params0);
 }
 
 template <typename K>
@@ -866,6 +1157,16 @@ static void configure_layers() {
   SAGIPS_BWD(true, true, false) SAGIPS_BWD(false, false, true) SAGIPS_BWD(false, true, true)
   SAGIPS_BWD(false, false, false) SAGIPS_BWD(false, true, false)
 #undef SAGIPS_BWD
+  for (bool s : {true, false}) {
+    const size_t sm = std::max(fwd_smem(s), bwd_smem(s));
+    if (s) {
+      allow_smem(k_pipe<true, true>, sm);
+      allow_smem(k_pipe<true, false>, sm);
+    } else {
+      allow_smem(k_pipe<false, true>, sm);
+      allow_smem(k_pipe<false, false>, sm);
+    }
+  }
 }
 
 __device__ unsigned long long g_trace[kTraceLaunches][kTraceCtas * kTraceTiles * 4];
@@ -893,39 +1194,31 @@ size_t plane_tile_bytes(bool split) { return (split ? 2 : 1) * (size_t)kPlane; }
 
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
   configure_layers();
-  FwdArgs a{};
-  a.A = L.A; a.X = L.X; a.W0 = L.W0; a.b0 = L.b0; a.W = L.W; a.bias = L.bias; a.C = L.C; a.mask = L.mask;
-  a.rows = L.rows; a.alpha = L.alpha; a.w_head = L.w_head; a.b_head = L.b_head; a.n_real = L.n_real;
-  a.label_rest = L.label_rest; a.scale = L.scale; a.logits = L.logits; a.part_head = L.part_head;
-  a.loss_part = L.loss_part; a.want_wgrad = L.want_wgrad;
-  a.trace = trace_slot();
+  unsigned long long* tr = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = fwd_smem(split);
   if (split) {
-    if (kind == FWD_FIRST) k_fwd<true, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == FWD_MID) k_fwd<true, false, false><<<grid, kThreads, sm, st>>>(a);
-    else k_fwd<true, false, true><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_fwd<true, true, false><<<grid, kThreads, sm, st>>>(L, tr);
+    else if (kind == FWD_MID) k_fwd<true, false, false><<<grid, kThreads, sm, st>>>(L, tr);
+    else k_fwd<true, false, true><<<grid, kThreads, sm, st>>>(L, tr);
   } else {
-    if (kind == FWD_FIRST) k_fwd<false, true, false><<<grid, kThreads, sm, st>>>(a);
-    else if (kind == FWD_MID) k_fwd<false, false, false><<<grid, kThreads, sm, st>>>(a);
-    else k_fwd<false, false, true><<<grid, kThreads, sm, st>>>(a);
+    if (kind == FWD_FIRST) k_fwd<false, true, false><<<grid, kThreads, sm, st>>>(L, tr);
+    else if (kind == FWD_MID) k_fwd<false, false, false><<<grid, kThreads, sm, st>>>(L, tr);
+    else k_fwd<false, false, true><<<grid, kThreads, sm, st>>>(L, tr);
   }
   count_launch();
 }
 
 void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaStream_t st) {
   configure_layers();
-  BwdArgs a{};
-  a.G = L.G; a.H = L.H; a.mask = L.mask; a.X = L.X; a.W0 = L.W0; a.b0 = L.b0; a.W = L.W; a.rows = L.rows;
-  a.alpha = L.alpha; a.Gout = L.Gout; a.dy = L.dy; a.part = L.part; a.part_db = L.part_db; a.part_l0 = L.part_l0;
-  a.trace = trace_slot();
+  unsigned long long* tr = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = bwd_smem(split);
 #define SAGIPS_BWD_LAUNCH(S)                                                                   \
-  if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(a);                   \
-  else if (first && wgrad) k_bwd<S, true, true><<<grid, kThreads, sm, st>>>(a);                \
-  else if (!first) k_bwd<S, false, false><<<grid, kThreads, sm, st>>>(a);                      \
-  else k_bwd<S, true, false><<<grid, kThreads, sm, st>>>(a);
+  if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(L, tr);               \
+  else if (first && wgrad) k_bwd<S, true, true><<<grid, kThreads, sm, st>>>(L, tr);            \
+  else if (!first) k_bwd<S, false, false><<<grid, kThreads, sm, st>>>(L, tr);                  \
+  else k_bwd<S, true, false><<<grid, kThreads, sm, st>>>(L, tr);
   if (split) {
     SAGIPS_BWD_LAUNCH(true)
   } else {
@@ -933,6 +1226,29 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
   }
 #undef SAGIPS_BWD_LAUNCH
   count_launch();
+}
+
+// Cooperative launch (all CTAs co-resident, one per SM): returns false if the
+// device cannot host the grid.
+bool launch_tc_pipe(bool split, bool dstep, const PipeLaunch& L, cudaStream_t st) {
+  configure_layers();
+  int grid = 0;
+  for (int r = 0; r < kPipeRoles; ++r) grid += L.ctas[r];
+  const size_t sm = std::max(fwd_smem(split), bwd_smem(split));
+  PipeLaunch P = L;
+  for (int r = 0; r < kPipeRoles; ++r) P.trace[r] = trace_slot();
+  if (P.trace[0]) {  // wait accounting in trace launch slots 31 (D step) / 30 (G step)
+    void* p = nullptr;
+    cudaGetSymbolAddress(&p, g_trace);
+    P.waits = reinterpret_cast<unsigned long long*>(p) + (size_t)(dstep ? 31 : 30) * kTraceCtas * kTraceTiles * 4;
+    cudaMemsetAsync(P.waits, 0, sizeof(unsigned long long) * 8 * kMaxSms, st);
+  }
+  void* args[] = {&P};
+  const void* fn = split ? (dstep ? (const void*)k_pipe<true, true> : (const void*)k_pipe<true, false>)
+                         : (dstep ? (const void*)k_pipe<false, true> : (const void*)k_pipe<false, false>);
+  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, sm, st);
+  count_launch();
+  return e == cudaSuccess;
 }
 
 void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st) {

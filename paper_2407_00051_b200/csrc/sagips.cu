@@ -4,6 +4,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -104,6 +105,14 @@ static void carve(sagips_ctx* c, char* base) {
                                                 (int64_t)kMaxSms * 4 * 384));
   c->head_tmp = cv.take<float>(D.maxw + 1);
   c->dbpart = cv.take<float>((int64_t)kMaxSms * 128);
+  // pipelined step: rings (L2-resident), per-tile flags, per-role partials
+  if (c->cfg.disc_depth == 4 && c->cfg.disc_hidden == 128) {
+    const size_t tb = plane_tile_bytes(true);
+    for (int k = 2; k < 5; ++k) c->ring[k] = cv.take<uint8_t>((int64_t)sagips_ctx::kRingG * tb);
+    c->flags = cv.take<uint32_t>(12 * (rows_t / 128));
+    for (int k = 0; k < 3; ++k) c->pipe_part[k] = cv.take<float>((int64_t)kMaxSms * 128 * 128);
+    for (int k = 0; k < 3; ++k) c->pipe_db[k] = cv.take<float>((int64_t)kMaxSms * 128);
+  }
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
   c->ws_bytes = cv.off;
@@ -370,29 +379,37 @@ static void disc_layer_dgrad(sagips_ctx* c, int l, const float* dZ, float* out_d
 // epilogue of the last hidden layer; dgrad and wgrad share one pass.
 static bool use_layers_v2(const sagips_ctx* c) { return c->use_tc && c->cfg.disc_depth >= 3; }
 
+// plane tiles of a whole tensor (per-layer kernels)
+static Ring whole(void* base, uint4* mask = nullptr) {
+  Ring r;
+  r.base = reinterpret_cast<uint8_t*>(base);
+  r.mask = mask;
+  return r;
+}
+
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
   const auto& D = c->D;
   const int Lh = D.L - 1;
   const bool split = tc_split(c);
-  auto planes = [&](int l) { return reinterpret_cast<uint8_t*>(c->dAct[l]); };
   FwdLaunch f;  // H_2 = LeakyReLU(H_1 W_1^T + b_1), H_1 recomputed from X
   f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0];
-  f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.C = planes(1); f.mask = c->dMask[1];
+  f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.out = whole(c->dAct[1], c->dMask[1]);
   f.rows = rows; f.alpha = c->cfg.leaky_slope;
   launch_tc_fwd(split, FWD_FIRST, f, st);
   for (int l = 2; l <= Lh - 2; ++l) {  // H_{l+1} = LeakyReLU(H_l W_l^T + b_l)
     FwdLaunch m;
-    m.A = planes(l - 1); m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l]; m.C = planes(l); m.mask = c->dMask[l];
+    m.in = whole(c->dAct[l - 1]); m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l];
+    m.out = whole(c->dAct[l], c->dMask[l]);
     m.rows = rows; m.alpha = c->cfg.leaky_slope;
     launch_tc_fwd(split, FWD_MID, m, st);
   }
   FwdLaunch h;  // last hidden layer + head + BCE -> G_{Lh} planes
-  h.A = planes(Lh - 2); h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
+  h.in = whole(c->dAct[Lh - 2]); h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
   h.rows = rows; h.alpha = c->cfg.leaky_slope;
   h.w_head = c->dW + D.w_off[Lh]; h.b_head = c->dB + D.b_off[Lh];
   h.n_real = n_real; h.label_rest = label_rest; h.scale = scale;
-  h.logits = logits; h.C = reinterpret_cast<uint8_t*>(c->dZb[0]); h.part_head = c->part;
+  h.logits = logits; h.out = whole(c->dZb[0]); h.part_head = c->part;
   h.loss_part = c->loss_part; h.want_wgrad = want_grads ? 1 : 0;
   launch_tc_fwd(split, FWD_HEAD, h, st);
 }
@@ -411,13 +428,13 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
-    b.G = reinterpret_cast<const uint8_t*>(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
+    b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
     b.alpha = c->cfg.leaky_slope; b.part = c->part; b.part_db = c->dbpart;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
     } else {
-      b.H = reinterpret_cast<const uint8_t*>(c->dAct[l - 1]); b.mask = c->dMask[l - 1];
-      b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]);
+      b.h = whole(c->dAct[l - 1], c->dMask[l - 1]);
+      b.gout = whole(c->dZb[cur ^ 1]);
     }
     launch_tc_bwd(split, l == 1, true, b, st);
     launch_sum_parts(c->part, grid, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
@@ -441,19 +458,153 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
-    b.G = reinterpret_cast<const uint8_t*>(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = N;
+    b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = N;
     b.alpha = c->cfg.leaky_slope;
     if (l == 1) {
       b.X = Y; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.dy = c->dy;
     } else {
-      b.mask = c->dMask[l - 1]; b.Gout = reinterpret_cast<uint8_t*>(c->dZb[cur ^ 1]);
+      b.h = whole(nullptr, c->dMask[l - 1]); b.gout = whole(c->dZb[cur ^ 1]);
     }
     launch_tc_bwd(split, l == 1, false, b, st);
     cur ^= 1;
   }
 }
 
+// ---- the pipelined step (k_pipe): depth-4 paper discriminator, every layer
+// pass of the D step (or the G step) in one cooperative launch
+static bool use_pipe(const sagips_ctx* c, int64_t rows) {
+  // SAGIPS_PIPE: 1 = pipelined when every role gets several tiles per CTA,
+  // 2 = pipelined at any size, unset / 0 = per-layer kernels (faster today:
+  // the roles are bound by their epilogues, profiles/r01_pipe_*)
+  const char* e = getenv("SAGIPS_PIPE");
+  const int mode = e ? atoi(e) : 0;
+  if (mode == 0 || !c->pipe_ok || !c->use_tc || c->cfg.disc_depth != 4 || c->cfg.disc_hidden != 128) return false;
+  return mode == 2 || (rows + 127) / 128 >= 4 * (int64_t)pipe_sm_count();
+}
+
+// CTAs per role, proportional to the measured per-tile cost of each role
+// (SAGIPS_PIPE_SPLIT_D / _G = "n0,n1,n2,n3,n4,n5" overrides)
+static void pipe_split(bool dstep, int ctas[kPipeRoles]) {
+  const int sms = pipe_sm_count();
+  const char* e = getenv(dstep ? "SAGIPS_PIPE_SPLIT_D" : "SAGIPS_PIPE_SPLIT_G");
+  if (e) {
+    int v[kPipeRoles], tot = 0;
+    if (sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == kPipeRoles) {
+      for (int r = 0; r < kPipeRoles; ++r) tot += v[r];
+      bool ok = tot <= sms;
+      for (int r = 0; r < kPipeRoles; ++r) ok = ok && v[r] > 0;
+      if (ok) {
+        for (int r = 0; r < kPipeRoles; ++r) ctas[r] = v[r];
+        return;
+      }
+    }
+  }
+  const double cd[kPipeRoles] = {3.0, 1.6, 3.2, 3.0, 3.0, 3.0};
+  const double cg[kPipeRoles] = {3.0, 1.6, 3.0, 1.4, 1.4, 1.6};
+  const double* cost = dstep ? cd : cg;
+  double tot = 0;
+  for (int r = 0; r < kPipeRoles; ++r) tot += cost[r];
+  int used = 0;
+  for (int r = 0; r < kPipeRoles; ++r) {
+    ctas[r] = std::max(1, (int)(sms * cost[r] / tot));
+    used += ctas[r];
+  }
+  for (int r = 0; used < sms; r = (r + 1) % kPipeRoles, ++used) ctas[r]++;  // remainder round-robin
+}
+
+// 0 = H2, 1 = H3: whole tensors (their backward consumers run ~4 pipeline
+// hops later, so a wrapping ring would throttle the forward roles);
+// 2 = G4, 3 = G3, 4 = G2: rings (one hop each)
+static Ring ring_of(sagips_ctx* c, int k, uint32_t target) {
+  Ring r;
+  const int64_t nt = (2 * c->N + 127) / 128;
+  // SAGIPS_PIPE_RING=1: G hand-offs through wrapping rings (L2-sized);
+  // default: whole tensors (no back-pressure)
+  const char* e = getenv("SAGIPS_PIPE_RING");
+  const bool rings = e && e[0] == '1';
+  if (k < 2) {
+    r.base = reinterpret_cast<uint8_t*>(c->dAct[1 + k]);
+    r.mask = c->dMask[1 + k];
+  } else if (rings) {
+    r.base = c->ring[k];
+    r.slots = sagips_ctx::kRingG;
+  } else {
+    r.base = reinterpret_cast<uint8_t*>(k == 2 ? c->dZb[0] : k == 3 ? c->dZb[1] : c->dAct[3]);
+  }
+  r.rdy = c->flags + (int64_t)k * nt;
+  r.done = c->flags + (int64_t)(5 + k) * nt;
+  r.done_target = target;
+  return r;
+}
+
+// tensors between the roles: see ring_of
+static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, int64_t n_real, float label_rest,
+                     float scale, float* logits, cudaStream_t st) {
+  const auto& D = c->D;
+  const bool split = tc_split(c);
+  const float a = c->cfg.leaky_slope;
+  const int64_t nt = (2 * c->N + 127) / 128;
+  cudaMemsetAsync(c->flags, 0, sizeof(uint32_t) * 12 * nt, st);
+  // H rings are read by the next forward role (1) and the backward role's H
+  // loader (1, D step) and its 8 epilogue warps (masks)
+  const uint32_t th = dstep ? 10u : 9u;
+  const Ring H2 = ring_of(c, 0, th), H3 = ring_of(c, 1, th);
+  const Ring G4 = ring_of(c, 2, 1), G3 = ring_of(c, 3, 1), G2 = ring_of(c, 4, 1);
+  PipeLaunch P;
+  pipe_split(dstep, P.ctas);
+  FwdLaunch& f1 = P.f[0];
+  f1.X = X; f1.W0 = c->dW + D.w_off[0]; f1.b0 = c->dB + D.b_off[0];
+  f1.W = c->dW + D.w_off[1]; f1.bias = c->dB + D.b_off[1]; f1.out = H2; f1.rows = rows; f1.alpha = a;
+  FwdLaunch& f2 = P.f[1];
+  f2.in = H2; f2.W = c->dW + D.w_off[2]; f2.bias = c->dB + D.b_off[2]; f2.out = H3; f2.rows = rows; f2.alpha = a;
+  FwdLaunch& f3 = P.f[2];
+  f3.in = H3; f3.W = c->dW + D.w_off[3]; f3.bias = c->dB + D.b_off[3]; f3.out = G4; f3.rows = rows; f3.alpha = a;
+  f3.w_head = c->dW + D.w_off[4]; f3.b_head = c->dB + D.b_off[4];
+  f3.n_real = n_real; f3.label_rest = label_rest; f3.scale = scale; f3.logits = logits;
+  f3.part_head = c->part; f3.loss_part = c->loss_part; f3.want_wgrad = dstep ? 1 : 0;
+  BwdLaunch& b3 = P.b[0];
+  b3.g = G4; b3.h = H3; b3.gout = G3; b3.W = c->dW + D.w_off[3]; b3.rows = rows; b3.alpha = a;
+  b3.part = c->pipe_part[0]; b3.part_db = c->pipe_db[0];
+  BwdLaunch& b2 = P.b[1];
+  b2.g = G3; b2.h = H2; b2.gout = G2; b2.W = c->dW + D.w_off[2]; b2.rows = rows; b2.alpha = a;
+  b2.part = c->pipe_part[1]; b2.part_db = c->pipe_db[1];
+  BwdLaunch& b1 = P.b[2];
+  if (dstep) {  // H_1 planes: written by the first-layer role, read by the layer-1 backward
+    Ring h1;
+    h1.base = reinterpret_cast<uint8_t*>(c->dAct[0]);
+    h1.rdy = c->flags + 10 * nt;
+    h1.done = c->flags + 11 * nt;
+    f1.h1 = h1;
+    b1.h = h1;
+  }
+  b1.g = G2; b1.X = X; b1.W0 = c->dW + D.w_off[0]; b1.b0 = c->dB + D.b_off[0]; b1.W = c->dW + D.w_off[1];
+  b1.rows = rows; b1.alpha = a; b1.dy = c->dy;
+  b1.part = c->pipe_part[2]; b1.part_db = c->pipe_db[2]; b1.part_l0 = c->colpart;
+  if (!launch_tc_pipe(split, dstep, P, st)) {
+    cudaGetLastError();  // clear; fall back to the per-layer kernels from now on
+    c->pipe_ok = false;
+    return false;
+  }
+  const int nh = P.ctas[2];
+  launch_finish_loss(c->loss_part, nh, 1.0 / rows, dstep ? &c->stats->loss_d : &c->stats->loss_g,
+                     &c->stats->nonfinite, st);
+  if (dstep) {
+    launch_sum_parts(c->part, 4 * nh, 129, 128, c->d_dW + D.w_off[4], st);
+    launch_sum_parts(c->part + 128, 4 * nh, 129, 1, c->d_dB + D.b_off[4], st);
+    for (int k = 0; k < 3; ++k) {
+      const int l = 3 - k, n = P.ctas[3 + k];
+      launch_sum_parts(c->pipe_part[k], n, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
+      launch_sum_parts(c->pipe_db[k], n, 128, 128, c->d_dB + D.b_off[l], st);
+    }
+    launch_sum_parts(c->colpart, 4 * P.ctas[5], 384, 256, c->d_dW + D.w_off[0], st);
+    launch_sum_parts(c->colpart + 256, 4 * P.ctas[5], 384, 128, c->d_dB + D.b_off[0], st);
+  }
+  return true;
+}
+
 static void disc_step(sagips_ctx* c, cudaStream_t st) {
+  if (use_pipe(c, 2 * c->N) && run_pipe(c, true, c->X, 2 * c->N, c->N, 0.0f, 1.0f / (float)(2 * c->N), c->logits_d, st))
+    return;
   if (use_layers_v2(c)) {
     disc_step_v2(c, st);
     return;
@@ -484,6 +635,8 @@ static void disc_step(sagips_ctx* c, cudaStream_t st) {
 }
 
 static void gen_loss_through_disc(sagips_ctx* c, cudaStream_t st) {
+  if (use_pipe(c, c->N) && run_pipe(c, false, c->X + 2 * c->N, c->N, 0, 1.0f, 1.0f / (float)c->N, c->logits_g, st))
+    return;
   if (use_layers_v2(c)) {
     gen_loss_v2(c, st);
     return;

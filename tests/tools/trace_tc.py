@@ -22,6 +22,7 @@ ctx.train_step(1, 0, sp)
 tr = L.debug_trace().astype(np.int64)
 names = ["fwd-first", "fwd-mid", "fwd-head", "bwd-L3", "bwd-L2", "bwd-L1", "G fwd-first", "G fwd-mid", "G fwd-head",
          "G bwd-L3", "G bwd-L2", "G bwd-dy"]
+g0 = min(int(tr[li, 0][tr[li, 0][:, 0] > 0, 0].min()) for li in range(12) if (tr[li, 0][:, 0] > 0).sum() >= 3)
 for li in range(12):
     t = tr[li, 0]
     n = int((t[:, 0] > 0).sum())
@@ -30,8 +31,40 @@ for li in range(12):
     t = t[:n]
     t0 = t[0, 0]
     prod = np.diff(t[:, 0]).mean()
+    period = np.diff(t[:, 3]).mean()
     mma_wait = (t[:, 1] - t[:, 0]).mean()
     mma_to_epi = (t[:, 2] - t[:, 1]).mean()
     epi = (t[:, 3] - t[:, 2]).mean()
-    print(f"{names[li]:12s} tiles {n:3d} span {(t[-1, 3] - t0) / 1e3:8.1f} us  per-tile producer {prod:7.0f} ns  "
-          f"full->mma {mma_wait:7.0f}  mma->epi {mma_to_epi:7.0f}  epi {epi:7.0f}")
+    print(f"{names[li]:12s} tiles {n:3d} start {(t0 - g0) / 1e3:7.1f} us span {(t[-1, 3] - t0) / 1e3:8.1f} us  "
+          f"period {period:6.0f} ns  staged {prod:6.0f}  staged->mma {mma_wait:6.0f}  mma->epi {mma_to_epi:6.0f}  "
+          f"epi {epi:6.0f}")
+
+
+def pipe_split(dstep, sms=148):
+    """mirror of pipe_split() in sagips.cu (default costs)"""
+    env = os.environ.get("SAGIPS_PIPE_SPLIT_D" if dstep else "SAGIPS_PIPE_SPLIT_G")
+    if env:
+        return [int(x) for x in env.split(",")]
+    cost = [3.0, 1.6, 3.2, 3.0, 3.0, 3.0] if dstep else [3.0, 1.6, 3.0, 1.4, 1.4, 1.6]
+    tot = sum(cost)
+    c = [max(1, int(sms * x / tot)) for x in cost]
+    r = 0
+    while sum(c) < sms:
+        c[r] += 1
+        r = (r + 1) % 6
+    return c
+
+
+if os.environ.get("SAGIPS_PIPE", "0") != "0":
+    roles = ["first", "mid", "head", "bwd3", "bwd2", "bwd1"]
+    cols = ["ld-up", "ld-stage", "mma-data", "mma-acc", "epi-slot", "epi-acc", "epi-mask", "wall"]
+    for dstep, slot in ((True, 31), (False, 30)):
+        w = tr[slot].reshape(-1)[:148 * 8].reshape(148, 8) / 1e3  # us
+        split = pipe_split(dstep)
+        print(("D" if dstep else "G") + " step waits (us, mean over the role's CTAs): split", split)
+        print("      " + " ".join(f"{c:>9s}" for c in cols))
+        b = 0
+        for r, n in enumerate(split):
+            m = w[b:b + n].mean(axis=0)
+            b += n
+            print(f"{roles[r]:6s}" + " ".join(f"{x:9.1f}" for x in m))
