@@ -188,6 +188,65 @@ def reference_arm(args):
     return 0
 
 
+# ---------------------------------------------------------------- roofline
+def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
+    """Roofline of the dominant kernel, from the per-kernel CUDA-event times of
+    the timed steps (sagips_kernel_times, events on the step stream around
+    each launch).  Algorithmic bytes / FLOPs per row of each layer pass
+    (DESIGN.md §7): plane tiles are E = 128 x 4 B per row (bf16 hi + lo) or
+    128 x 2 B (PREC_BF16); masks 16 B/row; X 8 B/row; useful FLOPs 2*128*128
+    per row per GEMM (forward, dgrad, wgrad)."""
+    split = cfg.precision != L.PREC_BF16
+    E = 128 * (4 if split else 2)
+    G = 2 * 128 * 128
+    rows_d, rows_g = 2 * N, N
+    mids = max(0, cfg.disc_depth - 3)
+    spec = {  # class: (rows, bytes/row, flops/row, launches)
+        "d_fwd_first": (rows_d, 8 + E + 16, G, 1), "d_fwd_mid": (rows_d, 2 * E + 16, G, mids),
+        "d_fwd_head": (rows_d, 2 * E + 4, G, 1), "d_bwd_last": (rows_d, 3 * E + 16, 2 * G, 1),
+        "d_bwd_mid": (rows_d, 3 * E + 16, 2 * G, mids), "d_bwd_first": (rows_d, E + 8, 2 * G, 1),
+        "g_fwd_first": (rows_g, 8 + E + 16, G, 1), "g_fwd_mid": (rows_g, 2 * E + 16, G, mids),
+        "g_fwd_head": (rows_g, 2 * E + 4, G, 1), "g_bwd_last": (rows_g, 2 * E + 16, G, 1),
+        "g_bwd_mid": (rows_g, 2 * E + 16, G, mids), "g_bwd_dy": (rows_g, E + 16, G, 1)}
+    try:
+        kt, _ = ctx.kernel_times()
+    except Exception:
+        return None, None
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    products = 3 if split else 1
+    tc_peak = peaks.get("bf16_tflops_sustained", 1400.0) / products
+    out = {}
+    for k, (rows, bpr, fpr, nl) in spec.items():
+        ms = kt.get(k, 0.0)
+        if ms <= 0 or nl == 0:
+            continue
+        by, fl = rows * bpr * nl, rows * fpr * nl
+        out[k] = {"ms": ms, "launches_per_step": nl, "GBps": by / (ms * 1e-3) / 1e9,
+                  "TFLOPs": fl / (ms * 1e-3) / 1e12, "bytes": by, "flops": fl,
+                  "t_hbm_ms": by / hbm / 1e6, "t_tensor_ms": fl / tc_peak / 1e9}
+    if not out:
+        return None, None
+    dom = max(out, key=lambda k: out[k]["ms"])
+    d = out[dom]
+    if d["t_hbm_ms"] >= d["t_tensor_ms"]:
+        roof = {"bound": "hbm", "unit": "GB/s", "achieved": d["GBps"], "peak": hbm,
+                "peak_src": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                "algorithmic": f"{spec[dom][1]} B/row x {spec[dom][0]} rows per launch"}
+    else:
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "achieved": d["TFLOPs"], "peak": tc_peak,
+                "peak_src": f"{peak_src} bf16_tflops_sustained / {products} (bf16x{products} split products)",
+                "algorithmic": f"{spec[dom][2]} FLOP/row x {spec[dom][0]} rows per launch"}
+    roof.update({"kernel": f"{dom} (k_bwd/k_fwd tcgen05 layer pass, {d['launches_per_step']} launch(es)/step)",
+                 "frac": roof["achieved"] / roof["peak"], "traffic": None, "ms_per_launch": d["ms"] / d["launches_per_step"],
+                 "timing": "CUDA events on the step stream around each launch, mean over the timed steps"})
+    # whole discriminator MLP (a7 + a8) on the tensor cores
+    tot_ms = sum(v["ms"] for v in out.values())
+    tot_fl = sum(v["flops"] for v in out.values())
+    mlp = {"ms": tot_ms, "TFLOPs": tot_fl / (tot_ms * 1e-3) / 1e12, "tensor_peak": tc_peak,
+           "frac": tot_fl / (tot_ms * 1e-3) / 1e12 / tc_peak}
+    return roof, {"per_kernel": out, "mlp_total": mlp}
+
+
 # ---------------------------------------------------------------- ours
 def ours_arm(args):
     import torch
@@ -216,6 +275,7 @@ def ours_arm(args):
         ctx.train_step(step, 0, sp)
         step += 1
     torch.cuda.synchronize()
+    ctx.timing_reset()  # phase / kernel times: timed steps only (warm-up includes lazy module loading)
     barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -271,26 +331,7 @@ def ours_arm(args):
         return 0
 
     peaks, peak_src = load_peaks()
-    disc_ms = phases["disc_step"] + phases["gen_loss_through_disc"]
-    disc_flops = disc_flops_per_event(cfg) * N
-    tc = cfg.disc_impl != L.DISC_SIMT and cfg.disc_hidden == 128
-    if cfg.precision == L.PREC_BF16:
-        peak = peaks.get("bf16_tflops_sustained", 1400.0)
-        roof = {"bound": "tensor", "unit": "TFLOP/s", "peak_src": f"{peak_src} bf16 sustained (MEASURED_PEAKS.json)"}
-    elif tc:
-        # fp32-class bf16x4: every fp32 multiply-add is 4 bf16 tensor-core MACs
-        peak = peaks.get("bf16_tflops_sustained", 1400.0) / 4.0
-        roof = {"bound": "tensor", "unit": "TFLOP/s",
-                "peak_src": f"{peak_src} bf16 sustained / 4 (bf16x4 split: 4 MMAs per fp32-class product)"}
-    else:
-        # FP32 FFMA on CUDA cores: 148 SMs x 128 lanes x 2 flop x max SM clock
-        peak = SM_COUNT * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        roof = {"bound": "alu", "unit": "TFLOP/s",
-                "peak_src": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md unit counts)"}
-    achieved = disc_flops / (disc_ms * 1e-3) / 1e12
-    roof.update({"kernel": "discriminator MLP (a7+a8: D step fwd/bwd on 2N rows + G-step fwd/bwd on N rows)",
-                 "achieved": achieved, "peak": peak, "frac": achieved / peak, "traffic": None,
-                 "algorithmic": f"8F = {disc_flops_per_event(cfg)} FLOP/event x {N} events"})
+    roof, kernels = layer_roofline(cfg, L, N, ctx, peaks, peak_src)
     samp_ms = phases["sampler"]
     samp_bytes = 16 * N + 4 * N  # fake + real rows written (8 B + 8 B) + 4 B real index
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -339,7 +380,8 @@ def ours_arm(args):
                        "l2": "step working set (D activations ~4 GB at C2) exceeds the 126 MB L2",
                        "mode": args.mode if world > 1 else "none"},
             "clocks": clk, "gpu_launches": launches, "phases_ms": phases, "phase_steps_averaged": nph,
-            "roofline": roof, "roofline_sampler": roof_sampler, "roofline_sampler_2p24": roof_sampler_24,
+            "roofline": roof, "kernels": kernels, "roofline_sampler": roof_sampler,
+            "roofline_sampler_2p24": roof_sampler_24,
             "cpu_baseline": cpu, "e2e": e2e,
             "loss_d": stats.loss_d, "loss_g": stats.loss_g}
     print(json.dumps(line), flush=True)

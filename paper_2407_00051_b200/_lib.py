@@ -87,6 +87,8 @@ def _load():
         "sagips_connect_nccl": ([vp, vp, sz], st),
         "sagips_launch_count": ([vp, P(ctypes.c_uint64)], st),
         "sagips_phase_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
+        "sagips_kernel_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
+        "sagips_timing_reset": ([vp], st),
         "sagips_debug_trace": ([vp, P(ctypes.c_size_t)], st),
     }
     for name, (args, res) in sig.items():
@@ -104,9 +106,12 @@ EXPORTED = [
     "sagips_last_error", "sagips_sample_events", "sagips_train_step", "sagips_push_generator_grad",
     "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
-    "sagips_phase_times", "sagips_debug_trace"]
+    "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
+NUM_KERNELS = 12
+KERNELS = ["d_fwd_first", "d_fwd_mid", "d_fwd_head", "d_bwd_last", "d_bwd_mid", "d_bwd_first",
+           "g_fwd_first", "g_fwd_mid", "g_fwd_head", "g_bwd_last", "g_bwd_mid", "g_bwd_dy"]
 
 
 def _check(status, ctx=None):
@@ -222,6 +227,16 @@ class Context:
         n = ctypes.c_int32()
         _check(lib.sagips_phase_times(self.h, arr, NUM_PHASES, ctypes.byref(n)), self.h)
         return dict(zip(PHASES, list(arr))), n.value
+
+    def kernel_times(self):
+        """Mean device milliseconds per step of each tensor-core layer-pass class."""
+        arr = (ctypes.c_float * NUM_KERNELS)()
+        n = ctypes.c_int32()
+        _check(lib.sagips_kernel_times(self.h, arr, NUM_KERNELS, ctypes.byref(n)), self.h)
+        return dict(zip(KERNELS, list(arr))), n.value
+
+    def timing_reset(self):
+        _check(lib.sagips_timing_reset(self.h), self.h)
 
     def launch_count(self):
         n = ctypes.c_uint64()

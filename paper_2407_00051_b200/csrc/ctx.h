@@ -81,11 +81,36 @@ struct sagips_ctx {
   cudaEvent_t pev[kTimingRing][SAGIPS_NUM_PHASES + 1] = {};
   int64_t timed_steps = 0;
   int pslot = 0;
+  // per-kernel timing of the tensor-core layer passes (sagips_kernel_times):
+  // start/stop events per launch, up to kKernelSlots launches per step
+  static constexpr int kKernelSlots = 16;
+  cudaEvent_t kev[kTimingRing][kKernelSlots][2] = {};
+  int kclass[kTimingRing][kKernelSlots] = {};
+  int kcount[kTimingRing] = {};
 };
 
 namespace sagips {
 inline void mark(sagips_ctx* c, int boundary, cudaStream_t st) {
   if (c->cfg.phase_timing) cudaEventRecord(c->pev[c->pslot][boundary], st);
+}
+// bracket one kernel launch of class k (SAGIPS_NUM_KERNELS) with events
+inline void kernel_begin(sagips_ctx* c, int k, cudaStream_t st) {
+  if (!c->cfg.phase_timing) return;
+  const int i = c->kcount[c->pslot];
+  if (i >= sagips_ctx::kKernelSlots) return;
+  if (!c->kev[c->pslot][i][0]) {
+    cudaEventCreate(&c->kev[c->pslot][i][0]);
+    cudaEventCreate(&c->kev[c->pslot][i][1]);
+  }
+  c->kclass[c->pslot][i] = k;
+  cudaEventRecord(c->kev[c->pslot][i][0], st);
+}
+inline void kernel_end(sagips_ctx* c, cudaStream_t st) {
+  if (!c->cfg.phase_timing) return;
+  const int i = c->kcount[c->pslot];
+  if (i >= sagips_ctx::kKernelSlots) return;
+  cudaEventRecord(c->kev[c->pslot][i][1], st);
+  c->kcount[c->pslot] = i + 1;
 }
 }  // namespace sagips
 

@@ -104,7 +104,7 @@ struct FwdLaunch {
   float label_rest = 0.f;
   float scale = 1.f;
   float* logits = nullptr;
-  float* part_head = nullptr;  // [ctas*4][129]
+  float* part_head = nullptr;  // [ctas*8][129]
   double* loss_part = nullptr; // [ctas]
   int want_wgrad = 0;
 };

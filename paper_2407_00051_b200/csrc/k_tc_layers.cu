@@ -292,12 +292,13 @@ __device__ __forceinline__ void ring_acquire_slot(const Ring& r, int64_t t, int 
 }
 // producer side: publish tile `pend` once its bulk stores are complete.
 // kKeep = bulk groups of later tiles that may stay in flight.
+// (inc: this warp's share of the kEW completions that make a tile ready)
 template <int kKeep>
-__device__ __forceinline__ void ring_publish(const Ring& r, int64_t pend, int lane) {
+__device__ __forceinline__ void ring_publish(const Ring& r, int64_t pend, int lane, uint32_t inc = 1) {
   if (r.rdy && pend >= 0 && lane == 0) {
     bulk_wait_groups<kKeep>();
     fence_proxy_async_global();
-    red_release_add(r.rdy + pend, 1);
+    red_release_add(r.rdy + pend, inc);
   }
 }
 // consumer side (single thread): wait for tile t, then order later async-proxy reads
@@ -334,8 +335,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 8);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
   float* swh = sbias + 128;                                 // [128] (head)
-  float* pdot = swh + 128;                                  // [2 halves][128] (head)
-  Params0* p0 = reinterpret_cast<Params0*>(swh);            // (first; aliases swh + pdot)
+  Params0* p0 = reinterpret_cast<Params0*>(swh);            // (first; aliases swh and the 1 KiB after it)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -344,7 +344,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       mbar_init(&full[i], kFirst ? 32 * kPW : 1);
       mbar_init(&empty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kEW);
+      mbar_init(&tempty[i], 32 * (kHead ? kEW / 2 : kEW));  // head: 4 warps per tile (see the epilogue)
     }
     fence_barrier_init();
   }
@@ -403,7 +403,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           if (tid == 0) {
             bulk_s2g(a.h1.base + tile_of(i) * TB, st, TB);
             bulk_commit();
-            if (pend >= 0) {  // publish the previous tile once its store is complete
+            if (pend >= 0 && a.h1.rdy) {  // publish the previous tile once its store is complete
               bulk_wait_groups<1>();
               fence_proxy_async_global();
               red_release_add(a.h1.rdy + pend, kEW);
@@ -417,7 +417,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       }
       if (store_h1 && tid == 0) {
         bulk_wait0();
-        if (pend >= 0) {
+        if (pend >= 0 && a.h1.rdy) {
           fence_proxy_async_global();
           red_release_add(a.h1.rdy + pend, kEW);
         }
@@ -462,6 +462,122 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       }
     }
     __syncwarp();
+  } else if (kHead) {
+    // ---------------- head epilogue: warp e -> TMEM lane quarter q; the two
+    // warps of a quarter take alternate tiles (h = tile parity = accumulator
+    // buffer), each all 128 columns -- z needs no cross-warp exchange
+    const int e = warp - kPW;
+    const int q = warp & 3;
+    const int h = e >> 2;
+    const uint32_t stg = smem_u32(sStg) + e * kStg;
+    float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // sum dz*H, columns 32c + lane
+    float gbacc = 0.f;
+    double lacc = 0.0;
+    int64_t pend = -1;
+    for (int i = h; i < nmine; i += 2) {
+      const int64_t t = tile_of(i);
+      const int b = i & 1;
+      const int64_t row = t * 128 + 32 * q + lane;
+      const bool valid = row < a.rows;
+      const int64_t slot = ring_slot(a.out, t);
+      uint8_t* dst0 = a.out.base + slot * TB + q * 4096;
+      {
+        bool free_now = true;
+        if (lane == 0) free_now = ring_slot_free(a.out, t);
+        if (!__shfl_sync(0xffffffffu, free_now ? 1 : 0, 0)) {
+          ring_publish<0>(a.out, pend, lane, 2);
+          pend = -1;
+        }
+      }
+      ring_acquire_slot(a.out, t, lane, lane == 0 ? wa : WaitAcct{});
+      SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+      if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
+      tc_fence_after();
+      const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)(32 * q) << 16);
+      // pass 1: z = H . w + b over all 128 columns of this lane's row
+      float dot = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld32(acc + 32 * c, v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) dot = fmaf(lrelu(v[k] + sbias[32 * c + k], a.alpha), swh[32 * c + k], dot);
+      }
+      const float z = dot + *a.b_head;
+      const float tl = (row < a.n_real) ? 1.f : a.label_rest;
+      const float dz = valid ? (sigmoid_f(z) - tl) * a.scale : 0.f;
+      if (valid) {
+        a.logits[row] = z;
+        lacc += (double)(tl * softplus_neg(z) + (1.f - tl) * softplus_neg(-z));
+        gbacc += dz;
+      }
+      // pass 2, per 64-column region: G = dz * w * LeakyReLU'(Z) -> planes;
+      // head gradient sum dz * H
+#pragma unroll 1
+      for (int rr = 0; rr < 2; ++rr) {
+        uint32_t lo[32];
+        stage_free(lane);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int c0 = 64 * rr + 32 * c;
+          float v[32];
+          tmem_ld32(acc + c0, v);
+          float g[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const float zz = v[k] + sbias[c0 + k];
+            g[k] = dz * lrelu(zz, a.alpha);
+            v[k] = dz * swh[c0 + k] * (zz > 0.f ? 1.f : a.alpha);
+          }
+          uint32_t hw[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
+          stage_words(stg, lane, c, hw);
+          if (a.want_wgrad) {
+            const float cs = colsum32(g, lane);
+            if (rr == 0) gacc[c] += cs;
+            else gacc[2 + c] += cs;
+          }
+        }
+        if (rr == 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty[b]);
+          if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
+        }
+        flush_stage(stg, dst0 + rr * 16384, lane);
+        if (kSplit) {
+          stage_free(lane);
+          stage_words(stg, lane, 0, lo);
+          stage_words(stg, lane, 1, lo + 16);
+          flush_stage(stg, dst0 + rr * 16384 + kPlane, lane);
+        }
+      }
+      ring_publish<2 * P>(a.out, pend, lane, 2);  // the previous tile's stores are complete (4 warps x 2)
+      pend = t;
+    }
+    if (lane == 0) bulk_wait0();
+    ring_publish<0>(a.out, pend, lane, 2);
+    // per-(CTA, epilogue warp) partials; loss per CTA in fp64, fixed order
+    const int64_t pe = (int64_t)j * kEW + e;
+    if (a.want_wgrad) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) a.part_head[pe * 129 + 32 * c + lane] = gacc[c];
+    }
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+      gbacc += __shfl_xor_sync(0xffffffffu, gbacc, w);
+      lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
+    }
+    if (lane == 0) {
+      if (a.want_wgrad) a.part_head[pe * 129 + 128] = gbacc;
+      sloss[e] = lacc;
+    }
+    epi_sync();
+    if (e == 0 && lane == 0) {
+      double sum = 0.0;
+      for (int k = 0; k < kEW; ++k) sum += sloss[k];
+      a.loss_part[j] = sum;
+    }
   } else {
     // ---------------- epilogue: warp e -> TMEM lane quarter q, column half h
     const int e = warp - kPW;
@@ -469,9 +585,6 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     const int h = e >> 2;
     const int cb = 64 * h;
     const uint32_t stg = smem_u32(sStg) + e * kStg;
-    float gacc[2] = {0.f, 0.f};   // head: sum dz*H, columns cb + 32c + lane
-    float gbacc = 0.f;
-    double lacc = 0.0;
     int64_t pend = -1;            // tile whose stores are in flight, not yet published
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
@@ -499,80 +612,31 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       const uint32_t acc = tmem + (uint32_t)(b * 128 + cb) + ((uint32_t)(32 * q) << 16);
       uint32_t lo[32];
       stage_free(lane);
-      if (!kHead) {
-        uint32_t mb[2];
+      uint32_t mb[2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          tmem_ld32(acc + 32 * c, v);
-          uint32_t m = 0;
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(acc + 32 * c, v);
+        uint32_t m = 0;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float z = v[k] + sbias[cb + 32 * c + k];
-            m |= (z > 0.f ? 1u : 0u) << k;
-            v[k] = valid ? lrelu(z, a.alpha) : 0.f;
-          }
-          mb[c] = valid ? m : 0u;
-          uint32_t hw[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
-          stage_words(stg, lane, c, hw);
+        for (int k = 0; k < 32; ++k) {
+          const float z = v[k] + sbias[cb + 32 * c + k];
+          m |= (z > 0.f ? 1u : 0u) << k;
+          v[k] = valid ? lrelu(z, a.alpha) : 0.f;
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
-        // mask stores, then flush_stage's __syncwarp orders them before lane
-        // 0's later release of this tile
-        reinterpret_cast<uint2*>(a.out.mask + slot * 128 + 32 * q + lane)[h] = make_uint2(mb[0], mb[1]);
-        flush_stage(stg, dst, lane);
-      } else {
-        // pass 1: partial z = H . w over this warp's 64 columns
-        float dot = 0.f;
+        mb[c] = valid ? m : 0u;
+        uint32_t hw[16];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          tmem_ld32(acc + 32 * c, v);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int cc = cb + 32 * c + k;
-            dot = fmaf(lrelu(v[k] + sbias[cc], a.alpha), swh[cc], dot);
-          }
-        }
-        epi_sync();  // previous tile's reads of pdot done
-        pdot[h * 128 + 32 * q + lane] = dot;
-        epi_sync();
-        const float z = pdot[32 * q + lane] + pdot[128 + 32 * q + lane] + *a.b_head;
-        const float tl = (row < a.n_real) ? 1.f : a.label_rest;
-        const float dz = valid ? (sigmoid_f(z) - tl) * a.scale : 0.f;
-        if (valid && h == 0) {
-          a.logits[row] = z;
-          lacc += (double)(tl * softplus_neg(z) + (1.f - tl) * softplus_neg(-z));
-          gbacc += dz;
-        }
-        // pass 2: G = dz * w * LeakyReLU'(Z) -> planes; head gradient dz * H
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
-          tmem_ld32(acc + 32 * c, v);
-          float g[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int cc = cb + 32 * c + k;
-            const float zz = v[k] + sbias[cc];
-            g[k] = dz * lrelu(zz, a.alpha);
-            v[k] = dz * swh[cc] * (zz > 0.f ? 1.f : a.alpha);
-          }
-          uint32_t hw[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
-          stage_words(stg, lane, c, hw);
-          if (a.want_wgrad) gacc[c] += colsum32(g, lane);
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[b]);
-        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
-        flush_stage(stg, dst, lane);
+        for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
+        stage_words(stg, lane, c, hw);
       }
+      tc_fence_before();
+      mbar_arrive(&tempty[b]);
+      if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
+      // mask stores, then flush_stage's __syncwarp orders them before lane
+      // 0's later release of this tile
+      reinterpret_cast<uint2*>(a.out.mask + slot * 128 + 32 * q + lane)[h] = make_uint2(mb[0], mb[1]);
+      flush_stage(stg, dst, lane);
       if (kSplit) {
         stage_free(lane);
         stage_words(stg, lane, 0, lo);
@@ -584,29 +648,6 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     }
     if (lane == 0) bulk_wait0();
     ring_publish<0>(a.out, pend, lane);
-    if (kHead) {
-      // per-(CTA, lane quarter) partials; loss per CTA in fp64, fixed order
-      const int64_t pq = (int64_t)j * 4 + q;
-      if (a.want_wgrad) {
-#pragma unroll
-        for (int c = 0; c < 2; ++c) a.part_head[pq * 129 + cb + 32 * c + lane] = gacc[c];
-      }
-#pragma unroll
-      for (int w = 16; w >= 1; w >>= 1) {
-        gbacc += __shfl_xor_sync(0xffffffffu, gbacc, w);
-        lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
-      }
-      if (lane == 0) {
-        if (a.want_wgrad && h == 0) a.part_head[pq * 129 + 128] = gbacc;
-        sloss[e] = lacc;
-      }
-      epi_sync();
-      if (e == 0 && lane == 0) {
-        double sum = 0.0;
-        for (int k = 0; k < kEW; ++k) sum += sloss[k];
-        a.loss_part[j] = sum;
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -628,9 +669,11 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   // kPR (wgrad, split): operands move as 32 KiB planes through plane slots
   // with their own barriers, so the next tile's planes load while this
   // tile's MMAs run (see the MMA issuer for the order)
-  constexpr bool kPR = kSplit && kWgrad;
   constexpr bool kLoadH = kWgrad && (!kFirst || kH1Load);  // H planes come from global memory
-  constexpr bool kFifoG = kFirst && !kH1Load;               // plane slots: H_1 fixed, G FIFO
+  // the plane ring only where H is loaded: with SIMT-produced H_1 planes the
+  // whole-tile H stage (released right after the wgrad MMAs) overlaps better
+  constexpr bool kPR = kSplit && kLoadH;
+  constexpr bool kFifoG = false;                            // (plane slots: H_1 fixed, G FIFO)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sG = sW + TB;     // G stage 0 (kPR: plane slots 0, 1)
@@ -745,12 +788,10 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         mbar_arrive_expect_tx(&pfull[ps.slot], kPlane);
         bulk_g2s(pl_addr(ps.slot), src, kPlane, &pfull[ps.slot]);
       };
+      // no L2 prefetch: the plane ring issues each load a tile ahead, and
+      // prefetched lines were evicted before use (ncu: +33% DRAM reads)
       for (int i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
-        if (i + 1 < nmine) {
-          if (!a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
-          if (kLoadH && !a.h.slots && !a.h.rdy) prefetch_l2(a.h.base + tile_of(i + 1) * TB, TB);
-        }
         const uint8_t* gsrc = a.g.base + ring_slot(a.g, t) * TB;
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
@@ -1064,9 +1105,9 @@ template <bool kSplit, bool kFirst, bool kHead>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd(const __grid_constant__ FwdLaunch a, unsigned long long* trace) {
   fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace);
 }
-template <bool kSplit, bool kFirst, bool kWgrad>
+template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ BwdLaunch a, unsigned long long* trace) {
-  bwd_body<kSplit, kFirst, kWgrad>(a, blockIdx.x, gridDim.x, trace);
+  bwd_body<kSplit, kFirst, kWgrad, kH1Load>(a, blockIdx.x, gridDim.x, trace);
 }
 
 // The whole D step (kD: wgrad, head and layer-0 gradients) or G step (dy) as
@@ -1157,6 +1198,8 @@ static void configure_layers() {
   SAGIPS_BWD(true, true, false) SAGIPS_BWD(false, false, true) SAGIPS_BWD(false, true, true)
   SAGIPS_BWD(false, false, false) SAGIPS_BWD(false, true, false)
 #undef SAGIPS_BWD
+  allow_smem(k_bwd<true, true, true, true>, bwd_smem(true));
+  allow_smem(k_bwd<false, true, true, true>, bwd_smem(false));
   for (bool s : {true, false}) {
     const size_t sm = std::max(fwd_smem(s), bwd_smem(s));
     if (s) {
@@ -1214,8 +1257,10 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
   unsigned long long* tr = trace_slot();
   const int grid = tc_layers_grid(L.rows);
   const size_t sm = bwd_smem(split);
+  const bool h1load = first && wgrad && L.h.base != nullptr;
 #define SAGIPS_BWD_LAUNCH(S)                                                                   \
   if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(L, tr);               \
+  else if (h1load) k_bwd<S, true, true, true><<<grid, kThreads, sm, st>>>(L, tr);              \
   else if (first && wgrad) k_bwd<S, true, true><<<grid, kThreads, sm, st>>>(L, tr);            \
   else if (!first) k_bwd<S, false, false><<<grid, kThreads, sm, st>>>(L, tr);                  \
   else k_bwd<S, true, false><<<grid, kThreads, sm, st>>>(L, tr);

@@ -389,20 +389,26 @@ static Ring whole(void* base, uint4* mask = nullptr) {
 
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
+  const int kc = want_grads ? 0 : 6;  // kernel-timing classes
+  const bool split = tc_split(c);
   const auto& D = c->D;
   const int Lh = D.L - 1;
-  const bool split = tc_split(c);
   FwdLaunch f;  // H_2 = LeakyReLU(H_1 W_1^T + b_1), H_1 recomputed from X
   f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0];
   f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.out = whole(c->dAct[1], c->dMask[1]);
   f.rows = rows; f.alpha = c->cfg.leaky_slope;
+  if (want_grads && split) f.h1 = whole(c->dAct[0]);  // H_1 planes for the layer-1 wgrad (one bulk store per tile)
+  kernel_begin(c, kc + 0, st);
   launch_tc_fwd(split, FWD_FIRST, f, st);
+  kernel_end(c, st);
   for (int l = 2; l <= Lh - 2; ++l) {  // H_{l+1} = LeakyReLU(H_l W_l^T + b_l)
     FwdLaunch m;
     m.in = whole(c->dAct[l - 1]); m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l];
     m.out = whole(c->dAct[l], c->dMask[l]);
     m.rows = rows; m.alpha = c->cfg.leaky_slope;
+    kernel_begin(c, kc + 1, st);
     launch_tc_fwd(split, FWD_MID, m, st);
+    kernel_end(c, st);
   }
   FwdLaunch h;  // last hidden layer + head + BCE -> G_{Lh} planes
   h.in = whole(c->dAct[Lh - 2]); h.W = c->dW + D.w_off[Lh - 1]; h.bias = c->dB + D.b_off[Lh - 1];
@@ -411,7 +417,9 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
   h.n_real = n_real; h.label_rest = label_rest; h.scale = scale;
   h.logits = logits; h.out = whole(c->dZb[0]); h.part_head = c->part;
   h.loss_part = c->loss_part; h.want_wgrad = want_grads ? 1 : 0;
+  kernel_begin(c, kc + 2, st);
   launch_tc_fwd(split, FWD_HEAD, h, st);
+  kernel_end(c, st);
 }
 
 static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
@@ -422,8 +430,8 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const int grid = tc_layers_grid(rows);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
   // head: dW (128) + db (1)
-  launch_sum_parts(c->part, 4 * grid, 129, 128, c->d_dW + D.w_off[Lh], st);
-  launch_sum_parts(c->part + 128, 4 * grid, 129, 1, c->d_dB + D.b_off[Lh], st);
+  launch_sum_parts(c->part, 8 * grid, 129, 128, c->d_dW + D.w_off[Lh], st);
+  launch_sum_parts(c->part + 128, 8 * grid, 129, 1, c->d_dB + D.b_off[Lh], st);
   launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
   int cur = 0;
   for (int l = Lh - 1; l >= 1; --l) {
@@ -432,11 +440,14 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     b.alpha = c->cfg.leaky_slope; b.part = c->part; b.part_db = c->dbpart;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
+      if (split) b.h = whole(c->dAct[0]);  // H_1 planes stored by the forward first layer
     } else {
       b.h = whole(c->dAct[l - 1], c->dMask[l - 1]);
       b.gout = whole(c->dZb[cur ^ 1]);
     }
+    kernel_begin(c, l == Lh - 1 ? 3 : l == 1 ? 5 : 4, st);
     launch_tc_bwd(split, l == 1, true, b, st);
+    kernel_end(c, st);
     launch_sum_parts(c->part, grid, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
     launch_sum_parts(c->dbpart, grid, 128, 128, c->d_dB + D.b_off[l], st);
     if (l == 1) {  // dW_0 [128][2] row-major, db_0
@@ -465,7 +476,9 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
     } else {
       b.h = whole(nullptr, c->dMask[l - 1]); b.gout = whole(c->dZb[cur ^ 1]);
     }
+    kernel_begin(c, l == Lh - 1 ? 9 : l == 1 ? 11 : 10, st);
     launch_tc_bwd(split, l == 1, false, b, st);
+    kernel_end(c, st);
     cur ^= 1;
   }
 }
@@ -580,7 +593,10 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   b1.g = G2; b1.X = X; b1.W0 = c->dW + D.w_off[0]; b1.b0 = c->dB + D.b_off[0]; b1.W = c->dW + D.w_off[1];
   b1.rows = rows; b1.alpha = a; b1.dy = c->dy;
   b1.part = c->pipe_part[2]; b1.part_db = c->pipe_db[2]; b1.part_l0 = c->colpart;
-  if (!launch_tc_pipe(split, dstep, P, st)) {
+  kernel_begin(c, dstep ? 0 : 6, st);
+  const bool launched = launch_tc_pipe(split, dstep, P, st);
+  kernel_end(c, st);
+  if (!launched) {
     cudaGetLastError();  // clear; fall back to the per-layer kernels from now on
     c->pipe_ok = false;
     return false;
@@ -589,8 +605,8 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   launch_finish_loss(c->loss_part, nh, 1.0 / rows, dstep ? &c->stats->loss_d : &c->stats->loss_g,
                      &c->stats->nonfinite, st);
   if (dstep) {
-    launch_sum_parts(c->part, 4 * nh, 129, 128, c->d_dW + D.w_off[4], st);
-    launch_sum_parts(c->part + 128, 4 * nh, 129, 1, c->d_dB + D.b_off[4], st);
+    launch_sum_parts(c->part, 8 * nh, 129, 128, c->d_dW + D.w_off[4], st);
+    launch_sum_parts(c->part + 128, 8 * nh, 129, 1, c->d_dB + D.b_off[4], st);
     for (int k = 0; k < 3; ++k) {
       const int l = 3 - k, n = P.ctas[3 + k];
       launch_sum_parts(c->pipe_part[k], n, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
@@ -744,6 +760,7 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
       for (auto& row : ctx->pev)
         for (auto& e : row) CK(cudaEventCreate(&e));
     ctx->pslot = (int)(ctx->timed_steps % sagips_ctx::kTimingRing);
+    ctx->kcount[ctx->pslot] = 0;
   }
   local_step(ctx, step, st);
   CK(cudaGetLastError());
@@ -804,6 +821,31 @@ sagips_status sagips_phase_times(sagips_ctx* ctx, float* host_ms, int32_t n, int
       acc[p] += ms;
     }
   for (int p = 0; p < SAGIPS_NUM_PHASES; ++p) host_ms[p] = (float)(acc[p] / cnt);
+  if (steps_averaged) *steps_averaged = cnt;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_timing_reset(sagips_ctx* ctx) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  CK(cudaDeviceSynchronize());
+  ctx->timed_steps = 0;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_kernel_times(sagips_ctx* ctx, float* host_ms, int32_t n, int32_t* steps_averaged) {
+  if (!ctx || !host_ms || n < SAGIPS_NUM_KERNELS) return SAGIPS_ERR_INVALID_ARG;
+  if (!ctx->cfg.phase_timing || ctx->timed_steps == 0) return fail(ctx, SAGIPS_ERR_STATE, "no timed steps");
+  CK(cudaDeviceSynchronize());
+  const int cnt = (int)std::min<int64_t>(ctx->timed_steps, sagips_ctx::kTimingRing);
+  double acc[SAGIPS_NUM_KERNELS] = {};
+  for (int s = 0; s < cnt; ++s)
+    for (int i = 0; i < ctx->kcount[s]; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ctx->kev[s][i][0], ctx->kev[s][i][1]));
+      const int k = ctx->kclass[s][i];
+      if (k >= 0 && k < SAGIPS_NUM_KERNELS) acc[k] += ms;
+    }
+  for (int k = 0; k < SAGIPS_NUM_KERNELS; ++k) host_ms[k] = (float)(acc[k] / cnt);
   if (steps_averaged) *steps_averaged = cnt;
   return SAGIPS_OK;
 }
