@@ -42,6 +42,7 @@ struct sagips_ctx {
   float* noise = nullptr;
   float* gAct[sagips::kMaxLayers] = {};
   float* gdZ[2] = {};
+  float* gdz_all[sagips::kMaxLayers] = {};  // fused generator backward: dZ of every hidden layer
   float *cbuf = nullptr, *draw = nullptr;
   // discriminator input/activations (fp32 path)
   float* X = nullptr;
@@ -116,6 +117,10 @@ inline void kernel_end(sagips_ctx* c, cudaStream_t st) {
 
 namespace sagips {
 void adam_gen(sagips_ctx* c, cudaStream_t st);
+// k_gen.cu: fused generator passes (widths <= 128)
+bool gen_fused_ok(const sagips_ctx* c);
+void launch_gen_fwd(sagips_ctx* c, cudaStream_t st);
+void launch_gen_bwd(sagips_ctx* c, cudaStream_t st);
 // exchange.cu
 sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st);
 sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st);

@@ -1,0 +1,259 @@
+// k_gen.cu -- the generator MLP (R4: [noise, H x depth, 6],
+// LeakyReLU hidden layers, linear output) as three fused kernels: the
+// generator is small (k = 1024 rows x ~51k parameters, ~0.3 GFLOP per step)
+// and latency-bound, so each pass is one launch instead of a GEMM per layer.
+//
+//   k_gen_fwd   rows in blocks of kR per CTA through all layers (activations
+//               in shared memory), every layer's output stored for the
+//               backward, constrain (R1) fused on the output layer
+//   k_gen_dgrad the same row blocks back through the layers:
+//               dZ_{l-1} = (dZ_l W_l) * LeakyReLU'(H_{l-1})
+//   k_gen_wgrad one CTA per 32 x 32 tile of every layer's weight gradient:
+//               dW_l = dZ_l^T H_{l-1} over all rows (fixed order), plus
+//               db_l = colsum(dZ_l); dW lands in the packet layout
+// All sums run in a fixed order (deterministic); fp32 throughout.
+#include "ctx.h"
+
+namespace sagips {
+
+namespace {
+constexpr int kR = 8;         // rows per CTA (forward / dgrad)
+constexpr int kGenMaxW = 128; // widest layer these kernels handle
+constexpr int kGenThreads = 256;
+
+__device__ __forceinline__ float lrelu_g(float z, float a) { return z > 0.f ? z : z * a; }
+}  // namespace
+
+struct GenArgs {
+  int L;                          // linear layers
+  int sizes[kMaxLayers + 1];
+  int64_t w_off[kMaxLayers], b_off[kMaxLayers];
+  const float* W;                 // all weights, layer l at w_off[l], [out][in] row-major
+  const float* B;
+  const float* noise;             // [k][sizes[0]]
+  float* act[kMaxLayers];         // [k][sizes[l+1]] outputs of layer l (last: raw)
+  float* dz[kMaxLayers];          // [k][sizes[l+1]] dLoss/dZ of layer l (last: draw, input)
+  float* cbuf;                    // [k][6] constrained parameters
+  float* dW;                      // packet layout (= W layout)
+  float* dB;
+  int k;
+  float alpha;
+  // wgrad tiles: tile_base[l] = first blockIdx of layer l; tiles_i[l] = in-tiles per out-tile row
+  int tile_base[kMaxLayers + 1];
+  int tiles_i[kMaxLayers];
+};
+
+// ---------------------------------------------------------------- forward
+// Each layer's W is staged in shared memory with rows padded to in + 1 floats
+// (lanes = consecutive outputs read conflict-free), then thread (r, o)
+// accumulates its dot product in input order.
+__global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__ GenArgs a) {
+  extern __shared__ float gsm[];
+  float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
+  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][in + 1]
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * kR;
+  const int in0 = a.sizes[0];
+  for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
+    const int r = idx / in0, i = idx % in0;
+    buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
+  }
+  for (int l = 0; l < a.L; ++l) {
+    const int in = a.sizes[l], out = a.sizes[l + 1], ld = in + 1;
+    const float* W = a.W + a.w_off[l];
+    const float* bias = a.B + a.b_off[l];
+    __syncthreads();  // previous layer done with Ws / buf
+    for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[(idx / in) * ld + idx % in] = __ldg(W + idx);
+    __syncthreads();
+    const float(*src)[kGenMaxW] = buf[l & 1];
+    float(*dst)[kGenMaxW] = buf[(l + 1) & 1];
+    const bool hidden = l < a.L - 1;
+    for (int idx = tid; idx < kR * out; idx += kGenThreads) {
+      const int r = idx / out, o = idx % out;
+      const float* w = Ws + o * ld;
+      float acc = 0.f;
+      for (int i = 0; i < in; ++i) acc = fmaf(src[r][i], w[i], acc);
+      acc += __ldg(bias + o);
+      if (hidden) acc = lrelu_g(acc, a.alpha);
+      dst[r][o] = acc;
+      if (r0 + r < a.k) {
+        a.act[l][(int64_t)(r0 + r) * out + o] = acc;
+        if (!hidden) {  // a3: constrain (R1): c0 = raw, c1/c2 = softplus(raw)
+          const int j = o % 3;
+          a.cbuf[(int64_t)(r0 + r) * out + o] = (j == 0) ? acc : softplus_f(acc);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- dgrad chain
+// W_l staged in shared memory (lanes = consecutive inputs i read W[o][i]
+// conflict-free), then thread (r, i) accumulates over o in order.
+__global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant__ GenArgs a) {
+  extern __shared__ float gsm[];
+  float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
+  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][in]
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * kR;
+  const int last = a.L - 1;
+  const int outL = a.sizes[a.L];
+  for (int idx = tid; idx < kR * outL; idx += kGenThreads) {
+    const int r = idx / outL, o = idx % outL;
+    buf[last & 1][r][o] = (r0 + r < a.k) ? a.dz[last][(int64_t)(r0 + r) * outL + o] : 0.f;
+  }
+  for (int l = last; l >= 1; --l) {
+    const int in = a.sizes[l], out = a.sizes[l + 1];
+    const float* W = a.W + a.w_off[l];
+    __syncthreads();  // previous layer done with Ws / buf
+    for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[idx] = __ldg(W + idx);
+    __syncthreads();
+    const float(*src)[kGenMaxW] = buf[l & 1];
+    float(*dst)[kGenMaxW] = buf[(l - 1) & 1];
+    for (int idx = tid; idx < kR * in; idx += kGenThreads) {
+      const int r = idx / in, i = idx % in;
+      float acc = 0.f;
+      for (int o = 0; o < out; ++o) acc = fmaf(src[r][o], Ws[o * in + i], acc);
+      float h = 0.f;
+      if (r0 + r < a.k) h = a.act[l - 1][(int64_t)(r0 + r) * in + i];
+      acc *= (h > 0.f) ? 1.f : a.alpha;  // LeakyReLU'(Z) from the sign of H (R6)
+      if (r0 + r >= a.k) acc = 0.f;
+      dst[r][i] = acc;
+      if (r0 + r < a.k) a.dz[l - 1][(int64_t)(r0 + r) * in + i] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- wgrad
+// blockIdx -> (layer l, out tile ob, in tile ib); thread (ty, tx) of 16 x 16
+// owns outputs (32ob + 2ty + {0,1}, 32ib + 2tx + {0,1}); rows in chunks of
+// 32, the next chunk's loads in flight (registers) while this one is summed.
+__global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant__ GenArgs a) {
+  __shared__ float sA[2][32][33];
+  __shared__ float sB[2][32][33];
+  int l = 0;
+  while (l + 1 < a.L && (int)blockIdx.x >= a.tile_base[l + 1]) ++l;
+  const int tb = blockIdx.x - a.tile_base[l];
+  const int ob = tb / a.tiles_i[l], ib = tb % a.tiles_i[l];
+  const int in = a.sizes[l], out = a.sizes[l + 1];
+  const float* dZ = a.dz[l];
+  const float* H = (l == 0) ? a.noise : a.act[l - 1];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  float dbacc = 0.f;
+  float ra[4], rb[4];
+  auto load = [&](int rc) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + u * kGenThreads;
+      const int rr = idx >> 5, cc = idx & 31;
+      const int r = rc + rr, o = 32 * ob + cc, i = 32 * ib + cc;
+      ra[u] = (r < a.k && o < out) ? __ldg(dZ + (int64_t)r * out + o) : 0.f;
+      rb[u] = (r < a.k && i < in) ? __ldg(H + (int64_t)r * in + i) : 0.f;
+    }
+  };
+  auto stash = [&](int s) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + u * kGenThreads;
+      sA[s][idx >> 5][idx & 31] = ra[u];
+      sB[s][idx >> 5][idx & 31] = rb[u];
+    }
+  };
+  load(0);
+  stash(0);
+  __syncthreads();
+  int s = 0;
+  for (int rc = 0; rc < a.k; rc += 32) {
+    const bool more = rc + 32 < a.k;
+    if (more) load(rc + 32);
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const float a0 = sA[s][rr][2 * ty], a1 = sA[s][rr][2 * ty + 1];
+      const float b0 = sB[s][rr][2 * tx], b1 = sB[s][rr][2 * tx + 1];
+      acc[0][0] = fmaf(a0, b0, acc[0][0]);
+      acc[0][1] = fmaf(a0, b1, acc[0][1]);
+      acc[1][0] = fmaf(a1, b0, acc[1][0]);
+      acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
+    if (ib == 0 && tid < 32) {
+#pragma unroll 8
+      for (int rr = 0; rr < 32; ++rr) dbacc += sA[s][rr][tid];
+    }
+    if (more) stash(s ^ 1);
+    __syncthreads();
+    s ^= 1;
+  }
+  float* dW = a.dW + a.w_off[l];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int o = 32 * ob + 2 * ty + u, i = 32 * ib + 2 * tx + v;
+      if (o < out && i < in) dW[(int64_t)o * in + i] = acc[u][v];
+    }
+  if (ib == 0 && tid < 32 && 32 * ob + tid < out) a.dB[a.b_off[l] + 32 * ob + tid] = dbacc;
+}
+
+// ---------------------------------------------------------------- host
+bool gen_fused_ok(const sagips_ctx* c) {
+  for (int l = 0; l <= c->G.L; ++l)
+    if (c->G.sizes[l] > kGenMaxW) return false;
+  return true;
+}
+
+static GenArgs gen_args(sagips_ctx* c) {
+  GenArgs a{};
+  const auto& G = c->G;
+  a.L = G.L;
+  for (int l = 0; l <= G.L; ++l) a.sizes[l] = G.sizes[l];
+  int tb = 0;
+  for (int l = 0; l < G.L; ++l) {
+    a.w_off[l] = G.w_off[l];
+    a.b_off[l] = G.b_off[l];
+    a.act[l] = c->gAct[l];
+    a.dz[l] = c->gdz_all[l];
+    a.tile_base[l] = tb;
+    a.tiles_i[l] = (G.sizes[l] + 31) / 32;
+    tb += ((G.sizes[l + 1] + 31) / 32) * a.tiles_i[l];
+  }
+  a.tile_base[G.L] = tb;
+  a.dz[G.L - 1] = c->draw;  // the output layer is linear: dZ_L = draw
+  a.W = c->gW;
+  a.B = c->gB;
+  a.noise = c->noise;
+  a.cbuf = c->cbuf;
+  a.dW = c->g_dW;
+  a.dB = c->g_dB;
+  a.k = c->cfg.param_samples;
+  a.alpha = c->cfg.leaky_slope;
+  return a;
+}
+
+static size_t gen_fwd_smem() { return sizeof(float) * (2 * kR * kGenMaxW + kGenMaxW * (kGenMaxW + 1)); }
+
+void launch_gen_fwd(sagips_ctx* c, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_gen_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_fwd_smem());
+    configured = true;
+  }
+  const GenArgs a = gen_args(c);
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  count_launch();
+}
+
+void launch_gen_bwd(sagips_ctx* c, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_gen_dgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_fwd_smem());
+    configured = true;
+  }
+  const GenArgs a = gen_args(c);
+  k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  count_launch();
+  k_gen_wgrad<<<a.tile_base[a.L], kGenThreads, 0, st>>>(a);
+  count_launch();
+}
+
+}  // namespace sagips

@@ -78,6 +78,7 @@ static void carve(sagips_ctx* c, char* base) {
   for (int l = 0; l < G.L; ++l) c->gAct[l] = cv.take<float>(k * G.sizes[l + 1]);
   c->gdZ[0] = cv.take<float>(k * G.maxw);
   c->gdZ[1] = cv.take<float>(k * G.maxw);
+  for (int l = 0; l + 1 < G.L; ++l) c->gdz_all[l] = cv.take<float>(k * G.sizes[l + 1]);
   c->cbuf = cv.take<float>(6 * k);
   c->draw = cv.take<float>(6 * k);
   c->X = cv.take<float>(4 * N);
@@ -705,17 +706,22 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   mark(c, 0, st);
   // a1 noise ~ N(0,1)
   launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
-  // a2 generator forward (hidden LeakyReLU, linear output)
-  const float* in = c->noise;
-  for (int l = 0; l < G.L; ++l) {
-    Epi ep{EPI_BIAS_ACT, c->gB + G.b_off[l], l < G.L - 1, a, nullptr, 0};
-    launch_gemm(false, true, k, G.sizes[l + 1], G.sizes[l], in, G.sizes[l], c->gW + G.w_off[l], G.sizes[l],
-                c->gAct[l], G.sizes[l + 1], ep, 1, 0, st);
-    in = c->gAct[l];
+  // a2 generator forward (hidden LeakyReLU, linear output) + a3 constrain
+  const bool fused_gen = gen_fused_ok(c);
+  if (fused_gen) {
+    launch_gen_fwd(c, st);
+  } else {
+    const float* in = c->noise;
+    for (int l = 0; l < G.L; ++l) {
+      Epi ep{EPI_BIAS_ACT, c->gB + G.b_off[l], l < G.L - 1, a, nullptr, 0};
+      launch_gemm(false, true, k, G.sizes[l + 1], G.sizes[l], in, G.sizes[l], c->gW + G.w_off[l], G.sizes[l],
+                  c->gAct[l], G.sizes[l + 1], ep, 1, 0, st);
+      in = c->gAct[l];
+    }
+    launch_constrain(c->gAct[G.L - 1], c->cbuf, k, st);
   }
   const float* raw = c->gAct[G.L - 1];
-  // a3 constrain ; a4-a6 fused sampler + bootstrap + histograms
-  launch_constrain(raw, c->cbuf, k, st);
+  // a4-a6 fused sampler + bootstrap + histograms
   mark(c, 1, st);
   launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
                      g.hist_bins, g.hist_lo, g.hist_hi, st);
@@ -731,6 +737,11 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   mark(c, 5, st);
   // a10 generator backward (the output layer is linear: dZ_L = draw);
   // a11 the weight gradients land in g_dW, which *is* the packet layout
+  if (fused_gen) {
+    launch_gen_bwd(c, st);
+    mark(c, 6, st);
+    return;
+  }
   const float* cur = c->draw;
   int buf = 0;
   for (int l = G.L - 1; l >= 0; --l) {
