@@ -61,8 +61,9 @@ struct sagips_ctx {
   static constexpr int kRingG = 256;
   uint8_t* ring[5] = {};
   uint32_t* flags = nullptr;
-  float* pipe_part[3] = {};
-  float* pipe_db[3] = {};
+  float* lpart[sagips::kMaxLayers] = {};  // [ctas][128][128] wgrad partials of hidden layer l
+  float* ldb[sagips::kMaxLayers] = {};    // [ctas][128] bias-gradient partials
+  bool d_adam_done = false;               // the D step already applied Adam(D) (fused reduction)
   bool pipe_ok = true;
   double* loss_part = nullptr;
   sagips_step_stats* stats = nullptr;

@@ -144,6 +144,22 @@ int pipe_sm_count();
 bool launch_tc_pipe(bool split, bool dstep, const PipeLaunch& L, cudaStream_t st);
 
 // k_adam.cu
+struct RedSeg {              // one parameter tensor: partials [nparts][ld] -> gradient g[n] -> Adam on p, m, v
+  const float* part = nullptr;
+  int64_t ld = 0;
+  int nparts = 0;
+  int n = 0;
+  float *g = nullptr, *p = nullptr, *m = nullptr, *v = nullptr;
+  int block0 = 0;            // (set by the launcher)
+};
+constexpr int kMaxRedSegs = 2 * kMaxLayers;
+struct RedAdamArgs {
+  RedSeg seg[kMaxRedSegs];
+  int nseg = 0;
+  int adam = 1;
+  float step_size = 0.f, bc2_sqrt = 1.f, b1 = 0.f, b2 = 0.f, eps = 0.f;  // (set by the launcher)
+};
+void launch_reduce_adam(RedAdamArgs& a, double lr, int64_t tau, double b1, double b2, double eps, cudaStream_t st);
 void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double lr, int64_t tau, double b1,
                  double b2, double eps, cudaStream_t st);
 void launch_fold(const PacketList& pl, int64_t n, float* out, float divisor, cudaStream_t st);

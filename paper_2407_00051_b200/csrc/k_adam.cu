@@ -32,6 +32,58 @@ void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double
   count_launch();
 }
 
+// Fused gradient reduction + Adam for the discriminator (one launch per D
+// step): each segment is one parameter tensor whose gradient arrives as
+// per-CTA partials; block = 32 elements x 8 part groups (group g sums parts
+// g, g+8, ... in order, the 8 group sums are added in order -- deterministic),
+// then the element's Adam update (the same arithmetic as k_adam).
+__global__ void __launch_bounds__(256) k_reduce_adam(const __grid_constant__ RedAdamArgs a) {
+  __shared__ float red[8][33];
+  int si = 0;
+  while (si + 1 < a.nseg && (int)blockIdx.x >= a.seg[si + 1].block0) ++si;
+  const RedSeg& sg = a.seg[si];
+  const int jl = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int j = (blockIdx.x - sg.block0) * 32 + jl;
+  float s = 0.f;
+  if (j < sg.n) {
+#pragma unroll 4
+    for (int p = grp; p < sg.nparts; p += 8) s += __ldg(sg.part + (int64_t)p * sg.ld + j);
+  }
+  red[grp][jl] = s;
+  __syncthreads();
+  if (grp == 0 && j < sg.n) {
+    float gi = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) gi += red[k][jl];
+    sg.g[j] = gi;
+    if (a.adam) {
+      const float mi = a.b1 * sg.m[j] + (1.f - a.b1) * gi;
+      const float vi = a.b2 * sg.v[j] + (1.f - a.b2) * gi * gi;
+      sg.m[j] = mi;
+      sg.v[j] = vi;
+      const float denom = sqrtf(vi) / a.bc2_sqrt + a.eps;
+      sg.p[j] -= a.step_size * (mi / denom);
+    }
+  }
+}
+
+void launch_reduce_adam(RedAdamArgs& a, double lr, int64_t tau, double b1, double b2, double eps, cudaStream_t st) {
+  int blocks = 0;
+  for (int i = 0; i < a.nseg; ++i) {
+    a.seg[i].block0 = blocks;
+    blocks += (a.seg[i].n + 31) / 32;
+  }
+  const double bc1 = 1.0 - std::pow(b1, (double)tau);
+  const double bc2 = 1.0 - std::pow(b2, (double)tau);
+  a.step_size = (float)(lr / bc1);
+  a.bc2_sqrt = (float)std::sqrt(bc2);
+  a.b1 = (float)b1;
+  a.b2 = (float)b2;
+  a.eps = (float)eps;
+  k_reduce_adam<<<blocks, 256, 0, st>>>(a);
+  count_launch();
+}
+
 // out[i] = (((P_0[i] + P_1[i]) + P_2[i]) + ...)  / divisor over the given
 // packets in the given (ascending origin) order (R10).  Pointers may be
 // local or peer-mapped (NVLink) addresses.

@@ -161,11 +161,12 @@ __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint3
   }
 }
 
-// SIMT producer of H_1 planes for one tile (warps 0-3, warp w: rows 32w..32w+31;
-// lane l: columns 4l..4l+3).  xr = this lane's prefetched input row 32w + l.
+// SIMT producer of H_1 planes: rows row0 .. row0 + nrows - 1 of one tile
+// (nrows a multiple of 4, <= 32); lane l: columns 4l..4l+3; xr = lane i's
+// prefetched input row row0 + i (i < nrows).
 template <bool kSplit>
 __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0* p0, float alpha, uint32_t hi,
-                                           uint32_t lo, int w, int l) {
+                                           uint32_t lo, int row0, int nrows, int l) {
   const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[4 * l]);
   const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[4 * l]);
   const float4 bb = *reinterpret_cast<const float4*>(&p0->b0[4 * l]);
@@ -173,7 +174,7 @@ __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0
   const uint32_t cbase = (uint32_t)(l >> 4) * 16384u + 8u * (uint32_t)(l & 1);
   const int jj = (l >> 1) & 7;
 #pragma unroll 1
-  for (int i0 = 0; i0 < 32; i0 += 4) {
+  for (int i0 = 0; i0 < nrows; i0 += 4) {
     uint32_t hw[4][2], lw[4][2];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {  // 4 independent rows in flight
@@ -189,7 +190,7 @@ __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int r = 32 * w + i0 + u;
+      const int r = row0 + i0 + u;
       const uint32_t off = cbase + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u + ((uint32_t)(jj ^ (r & 7)) << 4);
       sts64(hi + off, hw[u][0], hw[u][1]);
       if (kSplit) sts64(lo + off, lw[u][0], lw[u][1]);
@@ -341,8 +342,9 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   if (tid == 0) {
     check_smem_alignment(smem);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&full[i], kFirst ? 32 * kPW : 1);
-      mbar_init(&empty[i], 1);
+      // first layer: H_1 rows 0-63 by the producer warps, 64-127 by the epilogue warps
+      mbar_init(&full[i], kFirst ? 32 * (kPW + kEW) : 1);
+      mbar_init(&empty[i], (kFirst && a.h1.base) ? 2 : 1);  // + the H_1 store's read of the stage
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * (kHead ? kEW / 2 : kEW));  // head: 4 warps per tile (see the epilogue)
     }
@@ -374,53 +376,25 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       const float2* X2 = reinterpret_cast<const float2*>(a.X);
       auto load_x = [&](int i, bool& ok) {
         ok = false;
-        if (i >= nmine) return make_float2(0.f, 0.f);
-        const int64_t r = tile_of(i) * 128 + 32 * warp + lane;
+        if (i >= nmine || lane >= 16) return make_float2(0.f, 0.f);
+        const int64_t r = tile_of(i) * 128 + 16 * warp + lane;
         ok = r < a.rows;
         return ok ? __ldg(X2 + r) : make_float2(0.f, 0.f);
       };
       bool ok;
       float2 xr = load_x(0, ok);
-      const bool store_h1 = a.h1.base != nullptr;  // D step, pipelined: the backward reads H_1 planes
-      int64_t pend = -1;
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1;
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
-        if (store_h1) {
-          // the stage about to be rewritten must have been read by its bulk
-          // store (two tiles ago; the previous tile's store may be in flight)
-          if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
-        }
         mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
         const uint32_t st = smem_u32(sA + s * TB);
-        produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, warp, lane);
+        produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, 16 * warp, 16, lane);
         fence_proxy_async_smem();
         mbar_arrive(&full[s]);
-        if (store_h1) {
-          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
-          if (tid == 0) {
-            bulk_s2g(a.h1.base + tile_of(i) * TB, st, TB);
-            bulk_commit();
-            if (pend >= 0 && a.h1.rdy) {  // publish the previous tile once its store is complete
-              bulk_wait_groups<1>();
-              fence_proxy_async_global();
-              red_release_add(a.h1.rdy + pend, kEW);
-            }
-          }
-          pend = tile_of(i);
-        }
         if (warp == 0 && lane == 0) trace_pt(trace, j, i, 0);
         xr = xn;
         ok = ok_next;
-      }
-      if (store_h1 && tid == 0) {
-        bulk_wait0();
-        if (pend >= 0 && a.h1.rdy) {
-          fence_proxy_async_global();
-          red_release_add(a.h1.rdy + pend, kEW);
-        }
       }
     }
   } else if (warp == kLoadWarp) {
@@ -442,10 +416,15 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
       const uint32_t bh = smem_u32(sW), bl = bh + kPlane;
+      const bool store_h1 = kFirst && a.h1.base != nullptr;  // D step: H_1 planes for the layer-1 wgrad
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1, b = i & 1;
         SAGIPS_TIMED(wa, 2, mbar_wait(&full[s], (i >> 1) & 1));
         if (!kFirst) ring_consumed(a.in, tile_of(i));  // the input slot has been read
+        if (store_h1) {
+          bulk_s2g(a.h1.base + tile_of(i) * TB, smem_u32(sA + s * TB), TB);
+          bulk_commit();
+        }
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         trace_pt(trace, j, i, 1);
         tc_fence_after();
@@ -459,6 +438,21 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         }
         mma_commit(&empty[s]);
         mma_commit(&tfull[b]);
+        if (store_h1 && i > 0) {  // the previous tile's H_1 store is complete: publish it, free its stage
+          bulk_wait_groups<1>();
+          if (a.h1.rdy) {
+            fence_proxy_async_global();
+            red_release_add(a.h1.rdy + tile_of(i - 1), kEW);
+          }
+          mbar_arrive(&empty[s ^ 1]);
+        }
+      }
+      if (store_h1 && nmine > 0) {
+        bulk_wait0();
+        if (a.h1.rdy) {
+          fence_proxy_async_global();
+          red_release_add(a.h1.rdy + tile_of(nmine - 1), kEW);
+        }
       }
     }
     __syncwarp();
@@ -491,7 +485,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       }
       ring_acquire_slot(a.out, t, lane, lane == 0 ? wa : WaitAcct{});
       SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
-      if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
+      if ((e & 3) == 0 && lane == 0) trace_pt(trace, j, i, 2);  // warps 0 / 4: even / odd tiles
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)(32 * q) << 16);
       // pass 1: z = H . w + b over all 128 columns of this lane's row
@@ -542,7 +536,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         if (rr == 1) {
           tc_fence_before();
           mbar_arrive(&tempty[b]);
-          if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
+          if ((e & 3) == 0 && lane == 0) trace_pt(trace, j, i, 3);
         }
         flush_stage(stg, dst0 + rr * 16384, lane);
         if (kSplit) {
@@ -586,6 +580,33 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     const int cb = 64 * h;
     const uint32_t stg = smem_u32(sStg) + e * kStg;
     int64_t pend = -1;            // tile whose stores are in flight, not yet published
+    // first layer: this warp also produces H_1 rows 64 + 8e .. 64 + 8e + 7 of
+    // the tile two ahead (the producer warps do rows 0-63): the stage of tile
+    // i + 2 is free once the MMAs of tile i -- whose accumulator this warp
+    // has just read -- are done
+    const float2* X2 = reinterpret_cast<const float2*>(a.X);
+    auto help_x = [&](int i, bool& ok) {
+      ok = false;
+      if (!kFirst || i >= nmine || lane >= 8) return make_float2(0.f, 0.f);
+      const int64_t r = tile_of(i) * 128 + 64 + 8 * e + lane;
+      ok = r < a.rows;
+      return ok ? __ldg(X2 + r) : make_float2(0.f, 0.f);
+    };
+    auto help = [&](int i, float2 xr, bool ok) {
+      if (!kFirst || i >= nmine) return;
+      const int s = i & 1;
+      mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
+      const uint32_t st = smem_u32(sA + s * TB);
+      produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, 64 + 8 * e, 8, lane);
+      fence_proxy_async_smem();
+      mbar_arrive(&full[s]);
+    };
+    if (kFirst) {
+      bool ok0, ok1;
+      const float2 x0 = help_x(0, ok0), x1 = help_x(1, ok1);
+      help(0, x0, ok0);
+      help(1, x1, ok1);
+    }
     for (int i = 0; i < nmine; ++i) {
       const int64_t t = tile_of(i);
       const int b = i & 1;
@@ -593,6 +614,8 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       const bool valid = row < a.rows;
       const int64_t slot = ring_slot(a.out, t);
       uint8_t* dst = a.out.base + slot * TB + h * 16384 + q * 4096;
+      bool hok = false;
+      const float2 hx = help_x(i + 2, hok);  // in flight during this tile's epilogue
       // the previous tile is published after this tile's stores are issued
       // (its own stores have completed by then), unless this tile has to
       // wait for a free output slot: then publish first, or ring back-pressure
@@ -645,6 +668,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       }
       ring_publish<P>(a.out, pend, lane);  // the previous tile's stores are complete
       pend = t;
+      help(i + 2, hx, hok);
     }
     if (lane == 0) bulk_wait0();
     ring_publish<0>(a.out, pend, lane);
@@ -768,7 +792,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         } else {
           mbar_wait(&emptyH[0], (i & 1) ^ 1);
         }
-        produce_h1<kSplit>(xr, ok, p0, a.alpha, hh, hl, warp, lane);
+        produce_h1<kSplit>(xr, ok, p0, a.alpha, hh, hl, 32 * warp, 32, lane);
         fence_proxy_async_smem();
         if (kPR) {
           mbar_arrive(&pfull[0]);

@@ -111,8 +111,12 @@ static void carve(sagips_ctx* c, char* base) {
     const size_t tb = plane_tile_bytes(true);
     for (int k = 2; k < 5; ++k) c->ring[k] = cv.take<uint8_t>((int64_t)sagips_ctx::kRingG * tb);
     c->flags = cv.take<uint32_t>(12 * (rows_t / 128));
-    for (int k = 0; k < 3; ++k) c->pipe_part[k] = cv.take<float>((int64_t)kMaxSms * 128 * 128);
-    for (int k = 0; k < 3; ++k) c->pipe_db[k] = cv.take<float>((int64_t)kMaxSms * 128);
+  }
+  if (c->cfg.disc_hidden == 128) {  // per-layer wgrad partials of the tcgen05 layer passes (reduced + Adam at the end)
+    for (int l = 1; l + 1 < D.L; ++l) {
+      c->lpart[l] = cv.take<float>((int64_t)kMaxSms * 128 * 128);
+      c->ldb[l] = cv.take<float>((int64_t)kMaxSms * 128);
+    }
   }
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
@@ -423,6 +427,36 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
   kernel_end(c, st);
 }
 
+// All discriminator gradients of a tcgen05 D step from their per-CTA partials
+// (head [hparts][129], hidden layer l: lpart/ldb [nparts[l]], layer 0
+// colpart [l0parts][384]) -> d_dW / d_dB, then Adam(D): one launch.
+static void disc_reduce_adam(sagips_ctx* c, int hparts, const int* nparts, int l0parts, cudaStream_t st) {
+  const auto& D = c->D;
+  const auto& g = c->cfg;
+  const int Lh = D.L - 1;
+  RedAdamArgs A;
+  auto seg = [&](const float* part, int np, int64_t ld, int n, bool w, int l) {
+    RedSeg& s = A.seg[A.nseg++];
+    const int64_t off = w ? D.w_off[l] : D.b_off[l];
+    s.part = part; s.nparts = np; s.ld = ld; s.n = n;
+    s.g = (w ? c->d_dW : c->d_dB) + off;
+    s.p = (w ? c->dW : c->dB) + off;
+    s.m = (w ? c->dmW : c->dmB) + off;
+    s.v = (w ? c->dvW : c->dvB) + off;
+  };
+  seg(c->part, hparts, 129, 128, true, Lh);        // head weights
+  seg(c->part + 128, hparts, 129, 1, false, Lh);   // head bias
+  for (int l = Lh - 1; l >= 1; --l) {
+    seg(c->lpart[l], nparts[l], 128 * 128, 128 * 128, true, l);
+    seg(c->ldb[l], nparts[l], 128, 128, false, l);
+  }
+  seg(c->colpart, l0parts, 384, 256, true, 0);     // dW_0 [128][2]
+  seg(c->colpart + 256, l0parts, 384, 128, false, 0);
+  c->d_tau += 1;
+  launch_reduce_adam(A, g.disc_lr, c->d_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+  c->d_adam_done = true;
+}
+
 static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const auto& D = c->D;
   const int64_t N = c->N, rows = 2 * N;
@@ -430,15 +464,14 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const bool split = tc_split(c);
   const int grid = tc_layers_grid(rows);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
-  // head: dW (128) + db (1)
-  launch_sum_parts(c->part, 8 * grid, 129, 128, c->d_dW + D.w_off[Lh], st);
-  launch_sum_parts(c->part + 128, 8 * grid, 129, 1, c->d_dB + D.b_off[Lh], st);
   launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
   int cur = 0;
+  int nparts[kMaxLayers] = {};
   for (int l = Lh - 1; l >= 1; --l) {
     BwdLaunch b;
     b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
-    b.alpha = c->cfg.leaky_slope; b.part = c->part; b.part_db = c->dbpart;
+    b.alpha = c->cfg.leaky_slope; b.part = c->lpart[l]; b.part_db = c->ldb[l];
+    nparts[l] = grid;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
       if (split) b.h = whole(c->dAct[0]);  // H_1 planes stored by the forward first layer
@@ -449,14 +482,9 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     kernel_begin(c, l == Lh - 1 ? 3 : l == 1 ? 5 : 4, st);
     launch_tc_bwd(split, l == 1, true, b, st);
     kernel_end(c, st);
-    launch_sum_parts(c->part, grid, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
-    launch_sum_parts(c->dbpart, grid, 128, 128, c->d_dB + D.b_off[l], st);
-    if (l == 1) {  // dW_0 [128][2] row-major, db_0
-      launch_sum_parts(c->colpart, 4 * grid, 384, 256, c->d_dW + D.w_off[0], st);
-      launch_sum_parts(c->colpart + 256, 4 * grid, 384, 128, c->d_dB + D.b_off[0], st);
-    }
     cur ^= 1;
   }
+  disc_reduce_adam(c, 8 * grid, nparts, 4 * grid, st);
 }
 
 static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
@@ -578,10 +606,10 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   f3.part_head = c->part; f3.loss_part = c->loss_part; f3.want_wgrad = dstep ? 1 : 0;
   BwdLaunch& b3 = P.b[0];
   b3.g = G4; b3.h = H3; b3.gout = G3; b3.W = c->dW + D.w_off[3]; b3.rows = rows; b3.alpha = a;
-  b3.part = c->pipe_part[0]; b3.part_db = c->pipe_db[0];
+  b3.part = c->lpart[3]; b3.part_db = c->ldb[3];
   BwdLaunch& b2 = P.b[1];
   b2.g = G3; b2.h = H2; b2.gout = G2; b2.W = c->dW + D.w_off[2]; b2.rows = rows; b2.alpha = a;
-  b2.part = c->pipe_part[1]; b2.part_db = c->pipe_db[1];
+  b2.part = c->lpart[2]; b2.part_db = c->ldb[2];
   BwdLaunch& b1 = P.b[2];
   if (dstep) {  // H_1 planes: written by the first-layer role, read by the layer-1 backward
     Ring h1;
@@ -593,7 +621,7 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   }
   b1.g = G2; b1.X = X; b1.W0 = c->dW + D.w_off[0]; b1.b0 = c->dB + D.b_off[0]; b1.W = c->dW + D.w_off[1];
   b1.rows = rows; b1.alpha = a; b1.dy = c->dy;
-  b1.part = c->pipe_part[2]; b1.part_db = c->pipe_db[2]; b1.part_l0 = c->colpart;
+  b1.part = c->lpart[1]; b1.part_db = c->ldb[1]; b1.part_l0 = c->colpart;
   kernel_begin(c, dstep ? 0 : 6, st);
   const bool launched = launch_tc_pipe(split, dstep, P, st);
   kernel_end(c, st);
@@ -606,15 +634,9 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   launch_finish_loss(c->loss_part, nh, 1.0 / rows, dstep ? &c->stats->loss_d : &c->stats->loss_g,
                      &c->stats->nonfinite, st);
   if (dstep) {
-    launch_sum_parts(c->part, 8 * nh, 129, 128, c->d_dW + D.w_off[4], st);
-    launch_sum_parts(c->part + 128, 8 * nh, 129, 1, c->d_dB + D.b_off[4], st);
-    for (int k = 0; k < 3; ++k) {
-      const int l = 3 - k, n = P.ctas[3 + k];
-      launch_sum_parts(c->pipe_part[k], n, 128 * 128, 128 * 128, c->d_dW + D.w_off[l], st);
-      launch_sum_parts(c->pipe_db[k], n, 128, 128, c->d_dB + D.b_off[l], st);
-    }
-    launch_sum_parts(c->colpart, 4 * P.ctas[5], 384, 256, c->d_dW + D.w_off[0], st);
-    launch_sum_parts(c->colpart + 256, 4 * P.ctas[5], 384, 128, c->d_dB + D.b_off[0], st);
+    int nparts[kMaxLayers] = {};
+    for (int k = 0; k < 3; ++k) nparts[3 - k] = P.ctas[3 + k];
+    disc_reduce_adam(c, 8 * nh, nparts, 4 * P.ctas[5], st);
   }
   return true;
 }
@@ -728,7 +750,8 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   mark(c, 2, st);
   // a7 discriminator step + Adam(D) ; a8 generator loss through the updated D
   disc_step(c, st);
-  adam_disc(c, st);
+  if (c->d_adam_done) c->d_adam_done = false;  // applied by the fused gradient reduction
+  else adam_disc(c, st);
   mark(c, 3, st);
   gen_loss_through_disc(c, st);
   mark(c, 4, st);
