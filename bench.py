@@ -194,36 +194,47 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     the timed steps (sagips_kernel_times, events on the step stream around
     each launch).  Algorithmic bytes / FLOPs per row of each layer pass
     (DESIGN.md §7): plane tiles are E = 128 x 4 B per row (bf16 hi + lo) or
-    128 x 2 B (PREC_BF16); masks 16 B/row; X 8 B/row; useful FLOPs 2*128*128
-    per row per GEMM (forward, dgrad, wgrad)."""
+    128 x 2 B (PREC_BF16, hi only); the wgrad reads only the hi plane of H
+    (E/2, R28) and the first forward pass stores the H_1 hi plane for it;
+    masks 16 B/row; X 8 B/row.  Useful FLOPs: 2*128*128 per row per GEMM
+    (forward, dgrad, wgrad); executed tensor FLOPs count the split products
+    (bf16x3 forward / dgrad, bf16x2 wgrad; 1 for PREC_BF16)."""
     split = cfg.precision != L.PREC_BF16
     E = 128 * (4 if split else 2)
+    Eh = E // 2 if split else E            # the hi plane of H read by the wgrad
     G = 2 * 128 * 128
+    px, pw = (3, 2) if split else (1, 1)   # products per fwd/dgrad GEMM, per wgrad GEMM
     rows_d, rows_g = 2 * N, N
     mids = max(0, cfg.disc_depth - 3)
-    spec = {  # class: (rows, bytes/row, flops/row, launches)
-        "d_fwd_first": (rows_d, 8 + E + 16, G, 1), "d_fwd_mid": (rows_d, 2 * E + 16, G, mids),
-        "d_fwd_head": (rows_d, 2 * E + 4, G, 1), "d_bwd_last": (rows_d, 3 * E + 16, 2 * G, 1),
-        "d_bwd_mid": (rows_d, 3 * E + 16, 2 * G, mids), "d_bwd_first": (rows_d, E + 8, 2 * G, 1),
-        "g_fwd_first": (rows_g, 8 + E + 16, G, 1), "g_fwd_mid": (rows_g, 2 * E + 16, G, mids),
-        "g_fwd_head": (rows_g, 2 * E + 4, G, 1), "g_bwd_last": (rows_g, 2 * E + 16, G, 1),
-        "g_bwd_mid": (rows_g, 2 * E + 16, G, mids), "g_bwd_dy": (rows_g, E + 16, G, 1)}
+    h1 = Eh if split else 0                # H_1 hi plane stored by the first forward pass (split)
+    spec = {  # class: (rows, bytes/row, useful flops/row, executed flops/row, launches)
+        "d_fwd_first": (rows_d, 8 + E + 16 + h1, G, px * G, 1),
+        "d_fwd_mid": (rows_d, 2 * E + 16, G, px * G, mids),
+        "d_fwd_head": (rows_d, 2 * E + 4, G, px * G, 1),
+        "d_bwd_last": (rows_d, 2 * E + Eh + 16, 2 * G, (px + pw) * G, 1),
+        "d_bwd_mid": (rows_d, 2 * E + Eh + 16, 2 * G, (px + pw) * G, mids),
+        "d_bwd_first": (rows_d, E + h1 + 8, 2 * G, (px + pw) * G, 1),
+        "g_fwd_first": (rows_g, 8 + E + 16, G, px * G, 1),
+        "g_fwd_mid": (rows_g, 2 * E + 16, G, px * G, mids),
+        "g_fwd_head": (rows_g, 2 * E + 4, G, px * G, 1),
+        "g_bwd_last": (rows_g, 2 * E + 16, G, px * G, 1),
+        "g_bwd_mid": (rows_g, 2 * E + 16, G, px * G, mids),
+        "g_bwd_dy": (rows_g, E + 16, G, px * G, 1)}
     try:
         kt, _ = ctx.kernel_times()
     except Exception:
         return None, None
     hbm = peaks.get("hbm_gbs", 6650.0)
-    products = 3 if split else 1
-    tc_peak = peaks.get("bf16_tflops_sustained", 1400.0) / products
+    tc = peaks.get("bf16_tflops_sustained", 1400.0)
     out = {}
-    for k, (rows, bpr, fpr, nl) in spec.items():
+    for k, (rows, bpr, fpr, xpr, nl) in spec.items():
         ms = kt.get(k, 0.0)
         if ms <= 0 or nl == 0:
             continue
-        by, fl = rows * bpr * nl, rows * fpr * nl
+        by, fl, xf = rows * bpr * nl, rows * fpr * nl, rows * xpr * nl
         out[k] = {"ms": ms, "launches_per_step": nl, "GBps": by / (ms * 1e-3) / 1e9,
-                  "TFLOPs": fl / (ms * 1e-3) / 1e12, "bytes": by, "flops": fl,
-                  "t_hbm_ms": by / hbm / 1e6, "t_tensor_ms": fl / tc_peak / 1e9}
+                  "TFLOPs": fl / (ms * 1e-3) / 1e12, "tensor_TFLOPs_executed": xf / (ms * 1e-3) / 1e12,
+                  "bytes": by, "flops": fl, "t_hbm_ms": by / hbm / 1e6, "t_tensor_ms": xf / tc / 1e9}
     if not out:
         return None, None
     dom = max(out, key=lambda k: out[k]["ms"])
@@ -233,17 +244,21 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
                 "peak_src": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
                 "algorithmic": f"{spec[dom][1]} B/row x {spec[dom][0]} rows per launch"}
     else:
-        roof = {"bound": "tensor", "unit": "TFLOP/s", "achieved": d["TFLOPs"], "peak": tc_peak,
-                "peak_src": f"{peak_src} bf16_tflops_sustained / {products} (bf16x{products} split products)",
-                "algorithmic": f"{spec[dom][2]} FLOP/row x {spec[dom][0]} rows per launch"}
+        roof = {"bound": "tensor", "unit": "TFLOP/s", "achieved": d["tensor_TFLOPs_executed"], "peak": tc,
+                "peak_src": f"{peak_src} bf16_tflops_sustained (executed bf16 MMA FLOPs incl. split products)",
+                "algorithmic": f"{spec[dom][3]} executed FLOP/row ({spec[dom][2]} useful) x {spec[dom][0]} rows"}
     roof.update({"kernel": f"{dom} (k_bwd/k_fwd tcgen05 layer pass, {d['launches_per_step']} launch(es)/step)",
                  "frac": roof["achieved"] / roof["peak"], "traffic": None, "ms_per_launch": d["ms"] / d["launches_per_step"],
+                 "floors_ms": {"hbm": d["t_hbm_ms"], "tensor": d["t_tensor_ms"]},
                  "timing": "CUDA events on the step stream around each launch, mean over the timed steps"})
     # whole discriminator MLP (a7 + a8) on the tensor cores
     tot_ms = sum(v["ms"] for v in out.values())
     tot_fl = sum(v["flops"] for v in out.values())
-    mlp = {"ms": tot_ms, "TFLOPs": tot_fl / (tot_ms * 1e-3) / 1e12, "tensor_peak": tc_peak,
-           "frac": tot_fl / (tot_ms * 1e-3) / 1e12 / tc_peak}
+    tot_x = sum(rows * xpr * nl for k, (rows, bpr, fpr, xpr, nl) in spec.items() if k in out)
+    mlp = {"ms": tot_ms, "useful_TFLOPs": tot_fl / (tot_ms * 1e-3) / 1e12,
+           "executed_tensor_TFLOPs": tot_x / (tot_ms * 1e-3) / 1e12, "tensor_peak": tc,
+           "frac_executed": tot_x / (tot_ms * 1e-3) / 1e12 / tc,
+           "hbm_floor_ms": sum(v["t_hbm_ms"] for v in out.values())}
     return roof, {"per_kernel": out, "mlp_total": mlp}
 
 

@@ -113,6 +113,12 @@ __device__ __forceinline__ void stage_free(int lane) {
   if (lane == 0) bulk_wait_read0();
   __syncwarp();
 }
+// double-buffered staging: the buffer about to be written was used by the
+// warp's second-to-last bulk store (the last one may still be reading)
+__device__ __forceinline__ void stage_free_dbl(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  __syncwarp();
+}
 
 // reduce-scatter over the warp's 32 rows: on return lane l holds the sum over
 // lanes of g[l] (fixed order; g is destroyed)
@@ -324,15 +330,22 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   constexpr int P = kSplit ? 2 : 1;
   constexpr uint32_t TB = P * kPlane;
   extern __shared__ __align__(1024) uint8_t smem[];
+  // first layer: two whole-tile operand stages (SIMT-produced) + one 4 KiB
+  // staging buffer per epilogue warp; other layers: a FIFO of 3 operand
+  // plane slots (the lo plane is consumed first and frees early) + two
+  // staging buffers per epilogue warp (no wait for the bulk engine's reads)
+  constexpr bool kFifo = !kFirst;
+  constexpr uint32_t kRegion = 3 * kPlane + 2 * kEW * kStg;  // >= 2 TB + kEW kStg
+  static_assert(kRegion >= 2 * TB + kEW * kStg, "fwd region");
   uint8_t* sW = smem;
-  uint8_t* sA = sW + TB;          // 2 stages
-  uint8_t* sStg = sA + 2 * TB;    // 8 x 4 KiB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + kEW * kStg);
-  uint64_t* full = bars;          // [2]
-  uint64_t* empty = bars + 2;     // [2]
-  uint64_t* tfull = bars + 4;     // [2]
-  uint64_t* tempty = bars + 6;    // [2]
-  double* sloss = reinterpret_cast<double*>(bars + 8);  // [8]
+  uint8_t* sA = sW + TB;                                  // stages / plane slots
+  uint8_t* sStg = sA + (kFifo ? 3 * kPlane : 2 * TB);    // staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + kRegion);
+  uint64_t* full = bars;          // [3] (first: [2] stages; FIFO: plane slots)
+  uint64_t* empty = bars + 3;     // [3]
+  uint64_t* tfull = bars + 6;     // [2]
+  uint64_t* tempty = bars + 8;    // [2]
+  double* sloss = reinterpret_cast<double*>(bars + 10);  // [8]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 8);
   float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
   float* swh = sbias + 128;                                 // [128] (head)
@@ -341,10 +354,12 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     check_smem_alignment(smem);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
       // first layer: H_1 rows 0-63 by the producer warps, 64-127 by the epilogue warps
       mbar_init(&full[i], kFirst ? 32 * (kPW + kEW) : 1);
       mbar_init(&empty[i], (kFirst && a.h1.base) ? 2 : 1);  // + the H_1 store's read of the stage
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * (kHead ? kEW / 2 : kEW));  // head: 4 warps per tile (see the epilogue)
     }
@@ -402,12 +417,19 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     if (!kFirst && lane == 0) {
       for (int i = 0; i < nmine; ++i) {
         const int s = i & 1;
+        (void)s;
         const int64_t t = tile_of(i);
-        if (!a.in.slots && i + 1 < nmine) prefetch_l2(a.in.base + tile_of(i + 1) * TB, TB);
         ring_wait_ready(a.in, t, wa);
-        SAGIPS_TIMED(wa, 1, mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1));
-        mbar_arrive_expect_tx(&full[s], TB);
-        bulk_g2s(smem_u32(sA + s * TB), a.in.base + ring_slot(a.in, t) * TB, TB, &full[s]);
+        const uint8_t* src = a.in.base + ring_slot(a.in, t) * TB;
+        // planes in consumption order: lo (split only), then hi; plane p -> slot p % 3
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const int p = P * i + q;
+          const int slot = p % 3;
+          SAGIPS_TIMED(wa, 1, mbar_wait(&empty[slot], ((p / 3) & 1) ^ 1));
+          mbar_arrive_expect_tx(&full[slot], kPlane);
+          bulk_g2s(smem_u32(sA) + slot * kPlane, src + ((kSplit && q == 0) ? kPlane : 0), kPlane, &full[slot]);
+        }
         trace_pt(trace, j, i, 0);
       }
     }
@@ -417,12 +439,45 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       constexpr uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
       const uint32_t bh = smem_u32(sW), bl = bh + kPlane;
       const bool store_h1 = kFirst && a.h1.base != nullptr;  // D step: H_1 planes for the layer-1 wgrad
-      for (int i = 0; i < nmine; ++i) {
+      for (int i = 0; kFifo && i < nmine; ++i) {
+        const int b = i & 1;
+        // lo plane first: Al.Wh, then Ah.Wh + Ah.Wl (bf16: Ah.W only)
+        const int ph = P * i + (P - 1), sh = ph % 3;
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        const uint32_t d = tmem + (uint32_t)(b * 128);
+        if (kSplit) {
+          const int pl = P * i, sl = pl % 3;
+          SAGIPS_TIMED(wa, 2, mbar_wait(&full[sl], (pl / 3) & 1));
+          trace_pt(trace, j, i, 1);
+          tc_fence_after();
+          const uint32_t al = smem_u32(sA) + sl * kPlane;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+            mma_bf16(d, make_desc(al + off, 16, 1024), make_desc(bh + off, 16, 1024), idesc, k > 0);
+          }
+          mma_commit(&empty[sl]);
+        }
+        SAGIPS_TIMED(wa, 2, mbar_wait(&full[sh], (ph / 3) & 1));
+        ring_consumed(a.in, tile_of(i));  // both planes have been read from the input tensor
+        if (!kSplit) trace_pt(trace, j, i, 1);
+        tc_fence_after();
+        const uint32_t ah = smem_u32(sA) + sh * kPlane;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+          const uint64_t ad = make_desc(ah + off, 16, 1024);
+          mma_bf16(d, ad, make_desc(bh + off, 16, 1024), idesc, (kSplit || k > 0) ? 1u : 0u);
+          if (kSplit) mma_bf16(d, ad, make_desc(bl + off, 16, 1024), idesc, 1);
+        }
+        mma_commit(&empty[sh]);
+        mma_commit(&tfull[b]);
+      }
+      for (int i = 0; !kFifo && i < nmine; ++i) {
         const int s = i & 1, b = i & 1;
         SAGIPS_TIMED(wa, 2, mbar_wait(&full[s], (i >> 1) & 1));
-        if (!kFirst) ring_consumed(a.in, tile_of(i));  // the input slot has been read
         if (store_h1) {
-          bulk_s2g(a.h1.base + tile_of(i) * TB, smem_u32(sA + s * TB), TB);
+          bulk_s2g(a.h1.base + tile_of(i) * TB, smem_u32(sA + s * TB), kPlane);  // hi plane (the wgrad reads only hi, R28)
           bulk_commit();
         }
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
@@ -463,7 +518,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     const int e = warp - kPW;
     const int q = warp & 3;
     const int h = e >> 2;
-    const uint32_t stg = smem_u32(sStg) + e * kStg;
+    const uint32_t stgA = smem_u32(sStg) + (2 * e) * kStg, stgB = stgA + kStg;  // hi / lo staging
     float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // sum dz*H, columns 32c + lane
     float gbacc = 0.f;
     double lacc = 0.0;
@@ -510,7 +565,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
 #pragma unroll 1
       for (int rr = 0; rr < 2; ++rr) {
         uint32_t lo[32];
-        stage_free(lane);
+        stage_free_dbl(lane);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int c0 = 64 * rr + 32 * c;
@@ -526,7 +581,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           uint32_t hw[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
-          stage_words(stg, lane, c, hw);
+          stage_words((kSplit || rr == 0) ? stgA : stgB, lane, c, hw);
           if (a.want_wgrad) {
             const float cs = colsum32(g, lane);
             if (rr == 0) gacc[c] += cs;
@@ -538,12 +593,12 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           mbar_arrive(&tempty[b]);
           if ((e & 3) == 0 && lane == 0) trace_pt(trace, j, i, 3);
         }
-        flush_stage(stg, dst0 + rr * 16384, lane);
+        flush_stage((kSplit || rr == 0) ? stgA : stgB, dst0 + rr * 16384, lane);
         if (kSplit) {
-          stage_free(lane);
-          stage_words(stg, lane, 0, lo);
-          stage_words(stg, lane, 1, lo + 16);
-          flush_stage(stg, dst0 + rr * 16384 + kPlane, lane);
+          stage_free_dbl(lane);
+          stage_words(stgB, lane, 0, lo);
+          stage_words(stgB, lane, 1, lo + 16);
+          flush_stage(stgB, dst0 + rr * 16384 + kPlane, lane);
         }
       }
       ring_publish<2 * P>(a.out, pend, lane, 2);  // the previous tile's stores are complete (4 warps x 2)
@@ -578,7 +633,8 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     const int q = warp & 3;
     const int h = e >> 2;
     const int cb = 64 * h;
-    const uint32_t stg = smem_u32(sStg) + e * kStg;
+    // staging: first layer one buffer per warp; others hi / lo double buffers
+    const uint32_t stgA = smem_u32(sStg) + (kFifo ? 2 * e : e) * kStg, stgB = kFifo ? stgA + kStg : stgA;
     int64_t pend = -1;            // tile whose stores are in flight, not yet published
     // first layer: this warp also produces H_1 rows 64 + 8e .. 64 + 8e + 7 of
     // the tile two ahead (the producer warps do rows 0-63): the stage of tile
@@ -634,7 +690,10 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128 + cb) + ((uint32_t)(32 * q) << 16);
       uint32_t lo[32];
-      stage_free(lane);
+      // hi staging buffer: A (split: lo goes to B); bf16 alternates A / B by tile
+      const uint32_t stgH = (kSplit || !(i & 1)) ? stgA : stgB;
+      if (kFifo) stage_free_dbl(lane);
+      else stage_free(lane);
       uint32_t mb[2];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -651,7 +710,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         uint32_t hw[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
-        stage_words(stg, lane, c, hw);
+        stage_words(stgH, lane, c, hw);
       }
       tc_fence_before();
       mbar_arrive(&tempty[b]);
@@ -659,12 +718,13 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       // mask stores, then flush_stage's __syncwarp orders them before lane
       // 0's later release of this tile
       reinterpret_cast<uint2*>(a.out.mask + slot * 128 + 32 * q + lane)[h] = make_uint2(mb[0], mb[1]);
-      flush_stage(stg, dst, lane);
+      flush_stage(stgH, dst, lane);
       if (kSplit) {
-        stage_free(lane);
-        stage_words(stg, lane, 0, lo);
-        stage_words(stg, lane, 1, lo + 16);
-        flush_stage(stg, dst + kPlane, lane);
+        if (kFifo) stage_free_dbl(lane);
+        else stage_free(lane);
+        stage_words(stgB, lane, 0, lo);
+        stage_words(stgB, lane, 1, lo + 16);
+        flush_stage(stgB, dst + kPlane, lane);
       }
       ring_publish<P>(a.out, pend, lane);  // the previous tile's stores are complete
       pend = t;
@@ -756,16 +816,17 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
   // G stage of tile i: wgrad -> single stage; else a ring of 2 (sG, sH)
   auto g_stage = [&](int i) -> uint8_t* { return (!kWgrad && (i & 1)) ? sH : sG; };
-  // kPR plane slots {slot, use}: use = how many times the slot was filled before
-  //   mid:   Gh, Hh, Hl rotate through slots 0-2 (period 3), Gl in slot 3
-  //   first: Hh, Hl in slots 0, 1 (SIMT producers); Gh, Gl a FIFO over slots 2-4
+  // kPR plane slots {slot, use}: use = how many times the slot was filled
+  // before.  Three planes per tile, Gh, Hh, Gl (the wgrad reads only the hi
+  // plane of H, R28), in a FIFO over slots 0-3 (plane p = 3i + k -> slot
+  // p % 4); the MMA order releases them in the same order.
   struct PS {
     int slot, use;
   };
-  auto pl_gh = [&](int i) -> PS { return kFifoG ? PS{2 + (2 * i) % 3, (2 * i) / 3} : PS{(3 - i % 3) % 3, i}; };
-  auto pl_gl = [&](int i) -> PS { return kFifoG ? PS{2 + (2 * i + 1) % 3, (2 * i + 1) / 3} : PS{3, i}; };
-  auto pl_hh = [&](int i) -> PS { return kFifoG ? PS{0, i} : PS{(4 - i % 3) % 3, i}; };
-  auto pl_hl = [&](int i) -> PS { return kFifoG ? PS{1, i} : PS{(5 - i % 3) % 3, i}; };
+  auto pl_of = [&](int i, int k) -> PS { return PS{(3 * i + k) % 4, (3 * i + k) / 4}; };
+  auto pl_gh = [&](int i) -> PS { return pl_of(i, 0); };
+  auto pl_hh = [&](int i) -> PS { return pl_of(i, 1); };
+  auto pl_gl = [&](int i) -> PS { return pl_of(i, 2); };
   auto pl_addr = [&](int slot) -> uint32_t { return smem_u32(sG) + (uint32_t)slot * kPlane; };
 
   if (warp < kPW) {
@@ -819,12 +880,9 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         const uint8_t* gsrc = a.g.base + ring_slot(a.g, t) * TB;
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
-        if (kLoadH) {
-          const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
-          ring_wait_ready(a.h, t, wa);
-          load(pl_hh(i), hsrc);
-          load(pl_hl(i), hsrc + kPlane);
-        }
+        const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
+        ring_wait_ready(a.h, t, wa);
+        load(pl_hh(i), hsrc);
         load(pl_gl(i), gsrc + kPlane);
         trace_pt(trace, j, i, 0);
       }
@@ -860,15 +918,16 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       const uint32_t wh = smem_u32(sW), wl = wh + kPlane;
       const uint32_t hh = smem_u32(sH), hl = hh + kPlane;
       // kPR order per tile (each plane slot is released right after its last MMA):
-      //  1 Gh.Hh, Gh.1 (wgrad, db)  2 Gh.Hl -> Hl free  3 dgrad Gh.Wh, Gh.Wl -> Gh free
-      //  4 Gl.Hh, Gl.1 -> Hh free  5 dgrad Gl.Wh -> Gl free, accumulator full
+      //  1 Gh.Hh, Gh.1 (wgrad, db)  2 dgrad Gh.Wh, Gh.Wl -> Gh free
+      //  3 Gl.Hh, Gl.1 -> Hh free  4 dgrad Gl.Wh -> Gl free, accumulator full
       for (int i = 0; kPR && i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1;
-        const PS gh = pl_gh(i), gl = pl_gl(i), ph = pl_hh(i), pl = pl_hl(i);
-        const uint32_t agh = pl_addr(gh.slot), agl = pl_addr(gl.slot), ahh = pl_addr(ph.slot), ahl = pl_addr(pl.slot);
+        const PS gh = pl_gh(i), ph = pl_hh(i), gl = pl_gl(i);
+        const uint32_t agh = pl_addr(gh.slot), ahh = pl_addr(ph.slot), agl = pl_addr(gl.slot);
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        ring_consumed(a.h, t);  // the H plane has been read
         trace_pt(trace, j, i, 1);
         tc_fence_after();
 #pragma unroll
@@ -878,15 +937,6 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           mma_bf16(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, acc0);
           mma_bf16(acc_b, g, ones, id_b, acc0);
         }
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[pl.slot], pl.use & 1));
-        if (kLoadH) ring_consumed(a.h, t);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t km = k * 2048;
-          mma_bf16(acc_w, make_desc(agh + km, 16384, 1024), make_desc(ahl + km, 16384, 1024), id_w, 1);
-        }
-        mma_commit(&pempty[pl.slot]);
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
@@ -1040,11 +1090,19 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
+          const float vmul = valid ? 1.f : 0.f;
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
+          for (int k = 0; k < 32; k += 4) {  // layer-0 parameters as float4 (broadcast) loads
             const int cc = cb + 32 * c + k;
-            const float z1 = fmaf(x.x, p0->w0x[cc], fmaf(x.y, p0->w0y[cc], p0->b0[cc]));
-            v[k] = valid ? v[k] * (z1 > 0.f ? 1.f : a.alpha) : 0.f;
+            const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[cc]);
+            const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[cc]);
+            const float4 bb = *reinterpret_cast<const float4*>(&p0->b0[cc]);
+            const float z0 = fmaf(x.x, wx.x, fmaf(x.y, wy.x, bb.x)), z1 = fmaf(x.x, wx.y, fmaf(x.y, wy.y, bb.y));
+            const float z2 = fmaf(x.x, wx.z, fmaf(x.y, wy.z, bb.z)), z3 = fmaf(x.x, wx.w, fmaf(x.y, wy.w, bb.w));
+            v[k] *= vmul * (z0 > 0.f ? 1.f : a.alpha);
+            v[k + 1] *= vmul * (z1 > 0.f ? 1.f : a.alpha);
+            v[k + 2] *= vmul * (z2 > 0.f ? 1.f : a.alpha);
+            v[k + 3] *= vmul * (z3 > 0.f ? 1.f : a.alpha);
           }
           if (kWgrad) {
             float g[32];
@@ -1057,10 +1115,12 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
             sb[c] += colsum32(v, lane);
           } else {
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
+            for (int k = 0; k < 32; k += 4) {
               const int cc = cb + 32 * c + k;
-              d0 = fmaf(v[k], p0->w0x[cc], d0);
-              d1 = fmaf(v[k], p0->w0y[cc], d1);
+              const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[cc]);
+              const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[cc]);
+              d0 = fmaf(v[k + 3], wx.w, fmaf(v[k + 2], wx.z, fmaf(v[k + 1], wx.y, fmaf(v[k], wx.x, d0))));
+              d1 = fmaf(v[k + 3], wy.w, fmaf(v[k + 2], wy.z, fmaf(v[k + 1], wy.y, fmaf(v[k], wy.x, d1))));
             }
           }
         }
@@ -1196,7 +1256,7 @@ int pipe_sm_count() { return sm_count(); }
 
 static size_t fwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 8 * 8 + 8 * 8 + 16 + 4 * (128 + 128 + 256);  // bias, w_head, pdot / Params0
+  return TB + 3 * (size_t)kPlane + 2 * kEW * kStg + 10 * 8 + 8 * 8 + 16 + 4 * (128 + 128 + 256);  // bias, w_head / Params0
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;

@@ -11,5 +11,5 @@ print(round(d['ms_per_step'], 3), {k: round(v, 3) for k, v in d['phases_ms'].ite
 print('roofline', d['roofline']['kernel'], round(d['roofline']['achieved']), round(d['roofline']['frac'], 3))
 for k, v in d['kernels']['per_kernel'].items():
     print(f"{k:12s} {v['ms']:.3f} ms {v['GBps']:6.0f} GB/s {v['TFLOPs']:6.1f} TF/s hbm-floor {v['t_hbm_ms']:.3f} tensor-floor {v['t_tensor_ms']:.3f}")
-print(d['kernels']['mlp_total'])
+print(d["kernels"]["mlp_total"])
 PY

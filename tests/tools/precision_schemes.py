@@ -29,6 +29,8 @@ def mm(a,b,mode):
         ah,al=split(a,bf16); bh,bl=split(b,bf16); return ah@bh+ah@bl+al@bh+al@bl
     if mode=='tf32x3':
         ah,al=split(a,tf32); bh,bl=split(b,tf32); return ah@bh+ah@bl+al@bh
+    if mode=='bf16x2b':  # second operand (B) in bf16 hi only: Ah Bh + Al Bh
+        ah,al=split(a,bf16); bh,_=split(b,bf16); return ah@bh+al@bh
 def run(fwd_mode,bwd_mode,rows=1<<16,seed=1):
     cfg=gan.paper_config(param_samples=64,events_per_sample=rows//128,reference_rows=rows,shard_rows=rows//2)
     st=gan.RankState(cfg,0)
@@ -50,12 +52,13 @@ def run(fwd_mode,bwd_mode,rows=1<<16,seed=1):
     for l in reversed(range(L)):
         h,zz=cache[l]
         d=g if l==L-1 else g*mlp.lrelu_grad(zz)
-        if 0<l<L-1: dW[l]=mm(d.T,h,bwd_mode); g=mm(d,Ws[l],bwd_mode)
+        wm,dm=(bwd_mode.split(':')[1].split('/') if bwd_mode.startswith('wg:') else (bwd_mode,bwd_mode))
+        if 0<l<L-1: dW[l]=mm(d.T,h,wm); g=mm(d,Ws[l],dm)
         else: dW[l]=d.T@h; g=d@Ws[l]
     return loss,dW
 ref_loss,ref_dW=run('f64','f64')
 def gerr(a,b):
     fl=1e-2*np.max(np.abs(b)); return np.max(np.abs(a-b)/np.maximum(np.abs(b),fl))
-for fm,bm in [('bf16x4','bf16x4'),('bf16x3','bf16x4'),('tf32','tf32'),('bf16','bf16'),('bf16x3','bf16'),('bf16x3','bf16x3'),('f16x3','f16'),('tf32x3','tf32'),('bf16x3','tf32')]:
+for fm,bm in [('bf16x3','wg:bf16x2b/bf16x3'),('bf16x4','bf16x4'),('bf16x3','bf16x4'),('tf32','tf32'),('bf16','bf16'),('bf16x3','bf16'),('bf16x3','bf16x3'),('f16x3','f16'),('tf32x3','tf32'),('bf16x3','tf32')]:
     l,dW=run(fm,bm)
     print(f"fwd {fm:7s} bwd {bm:7s} loss rel {abs(l-ref_loss)/ref_loss:.2e}  grad max rel(floor1%) {max(gerr(dW[i],ref_dW[i]) for i in range(len(dW))):.2e}")
