@@ -275,7 +275,8 @@ SAGIPS_API sagips_status sagips_timing_reset(sagips_ctx* ctx);
 /* Debugging aid: with the environment variable SAGIPS_TRACE=1 set before the
  * first step, the tensor-core layer kernels record globaltimer stamps per
  * tile (CTAs 0-3, first 32 launches): [launch][cta][tile][4] uint64 =
- * producer done, MMA start, epilogue start, epilogue done.  Copies and
+ * producer done, MMA start, epilogue start, epilogue done, followed by
+ * [launch][256 CTAs][4] uint64 per-CTA (start, end, -, -) stamps.  Copies and
  * rearms the buffer; `bytes` must equal the size returned for host == NULL.
  * [sync] */
 SAGIPS_API sagips_status sagips_debug_trace(void* host, size_t* bytes);

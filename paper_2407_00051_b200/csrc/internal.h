@@ -91,6 +91,7 @@ struct FwdLaunch {
   Ring in;                     // input plane tiles (mid, head)
   Ring out;                    // output plane tiles (H + mask; head: G)
   Ring h1;                     // first, pipelined D step: H_1 planes for the backward (base == nullptr: none)
+  uint32_t* tile_ctr = nullptr;  // middle layers: dynamic tile schedule counter (zeroed before the launch)
   const float* X = nullptr;    // [rows][2] (first)
   const float* W0 = nullptr;   // [128][2] (first)
   const float* b0 = nullptr;   // [128] (first)
@@ -122,6 +123,7 @@ struct BwdLaunch {
   float* part = nullptr;       // [ctas][128][128]
   float* part_db = nullptr;    // [ctas][128]
   float* part_l0 = nullptr;    // [ctas*4][384]
+  uint32_t* tile_ctr = nullptr;  // no wgrad (G step): dynamic tile schedule counter (zeroed before the launch)
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
 int tc_layers_grid(int64_t rows);

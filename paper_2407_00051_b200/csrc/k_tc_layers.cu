@@ -39,6 +39,7 @@
 //   for the first layer, the layer-0 gradients
 //   dW_0 = G_1^T X, db_0 = colsum(G_1) (D step) or dy = G_1 W_0 (G step) in the
 //   epilogue.  Without wgrad (G step) the H stage becomes a second G stage.
+#include <cstdio>
 #include <cstdlib>
 
 #include "ctx.h"
@@ -347,7 +348,8 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   uint64_t* tempty = bars + 8;    // [2]
   double* sloss = reinterpret_cast<double*>(bars + 10);  // [8]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 8);
-  float* sbias = reinterpret_cast<float*>(tmem_slot + 4);  // [128]
+  int* sTile = reinterpret_cast<int*>(tmem_slot + 4);      // [8] dynamic schedule: tile of local iteration i (i % 8)
+  float* sbias = reinterpret_cast<float*>(sTile + 8);      // [128]
   float* swh = sbias + 128;                                 // [128] (head)
   Params0* p0 = reinterpret_cast<Params0*>(swh);            // (first; aliases swh and the 1 KiB after it)
 
@@ -357,7 +359,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     for (int i = 0; i < 3; ++i) {
       // first layer: H_1 rows 0-63 by the producer warps, 64-127 by the epilogue warps
       mbar_init(&full[i], kFirst ? 32 * (kPW + kEW) : 1);
-      mbar_init(&empty[i], (kFirst && a.h1.base) ? 2 : 1);  // + the H_1 store's read of the stage
+      mbar_init(&empty[i], (kFirst && a.h1.base) ? 2 : 1);  // + the H_1 hi-plane store's read (lo: immediate)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -384,6 +386,19 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   const int64_t ntiles = (a.rows + 127) / 128;
   const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
   auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
+  // dynamic tile schedule (middle layers, per-layer kernels): the loader takes
+  // tiles from a global counter and passes their ids through sTile; a tile's
+  // output does not depend on which CTA computes it (no per-CTA partials)
+  const bool dyn = kFifo && !kFirst && !kHead && a.tile_ctr != nullptr;
+  // first layer: wait for tile i's whole-tile stage, write its H_1 rows, signal it
+  auto produce_rows = [&](int i, float2 xr, bool ok, int row0, int nrows) {
+    const int s = i & 1;
+    mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
+    const uint32_t st = smem_u32(sA + s * TB);
+    produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, row0, nrows, lane);
+    fence_proxy_async_smem();
+    mbar_arrive(&full[s]);
+  };
 
   if (warp < kPW) {
     // ---------------- SIMT producers of H_1 (first layer only)
@@ -399,14 +414,9 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       bool ok;
       float2 xr = load_x(0, ok);
       for (int i = 0; i < nmine; ++i) {
-        const int s = i & 1;
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
-        mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
-        const uint32_t st = smem_u32(sA + s * TB);
-        produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, 16 * warp, 16, lane);
-        fence_proxy_async_smem();
-        mbar_arrive(&full[s]);
+        produce_rows(i, xr, ok, 16 * warp, 16);
         if (warp == 0 && lane == 0) trace_pt(trace, j, i, 0);
         xr = xn;
         ok = ok_next;
@@ -415,10 +425,23 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   } else if (warp == kLoadWarp) {
     // ---------------- bulk loader
     if (!kFirst && lane == 0) {
-      for (int i = 0; i < nmine; ++i) {
-        const int s = i & 1;
-        (void)s;
-        const int64_t t = tile_of(i);
+      for (int i = 0;; ++i) {
+        int64_t t = -1;
+        if (dyn) {
+          t = atomicAdd(a.tile_ctr, 1u);
+          if (t >= ntiles) t = -1;
+        } else if (i < nmine) {
+          t = tile_of(i);
+        }
+        if (dyn) sTile[i & 7] = (int)t;
+        if (t < 0) {
+          if (dyn) {  // sentinel: a plain arrival on the first plane slot of iteration i
+            const int p = P * i, slot = p % 3;
+            mbar_wait(&empty[slot], ((p / 3) & 1) ^ 1);
+            mbar_arrive(&full[slot]);
+          }
+          break;
+        }
         ring_wait_ready(a.in, t, wa);
         const uint8_t* src = a.in.base + ring_slot(a.in, t) * TB;
         // planes in consumption order: lo (split only), then hi; plane p -> slot p % 3
@@ -439,10 +462,21 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       constexpr uint32_t idesc = make_idesc_bf16(128, 128, 0, 0);
       const uint32_t bh = smem_u32(sW), bl = bh + kPlane;
       const bool store_h1 = kFirst && a.h1.base != nullptr;  // D step: H_1 planes for the layer-1 wgrad
-      for (int i = 0; kFifo && i < nmine; ++i) {
+      for (int i = 0; kFifo && (dyn || i < nmine); ++i) {
         const int b = i & 1;
         // lo plane first: Al.Wh, then Ah.Wh + Ah.Wl (bf16: Ah.W only)
         const int ph = P * i + (P - 1), sh = ph % 3;
+        int64_t t = dyn ? -1 : tile_of(i);
+        if (dyn) {  // the tile id is valid once the first plane slot's barrier completed
+          const int p0 = P * i;
+          SAGIPS_TIMED(wa, 2, mbar_wait(&full[p0 % 3], (p0 / 3) & 1));
+          t = sTile[i & 7];
+          if (t < 0) {  // forward the sentinel to the epilogue through the accumulator barrier
+            SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+            mbar_arrive(&tfull[b]);
+            break;
+          }
+        }
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         const uint32_t d = tmem + (uint32_t)(b * 128);
         if (kSplit) {
@@ -459,7 +493,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           mma_commit(&empty[sl]);
         }
         SAGIPS_TIMED(wa, 2, mbar_wait(&full[sh], (ph / 3) & 1));
-        ring_consumed(a.in, tile_of(i));  // both planes have been read from the input tensor
+        ring_consumed(a.in, t);  // both planes have been read from the input tensor
         if (!kSplit) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(sA) + sh * kPlane;
@@ -650,12 +684,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     };
     auto help = [&](int i, float2 xr, bool ok) {
       if (!kFirst || i >= nmine) return;
-      const int s = i & 1;
-      mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
-      const uint32_t st = smem_u32(sA + s * TB);
-      produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, 64 + 8 * e, 8, lane);
-      fence_proxy_async_smem();
-      mbar_arrive(&full[s]);
+      produce_rows(i, xr, ok, 64 + 8 * e, 8);
     };
     if (kFirst) {
       bool ok0, ok1;
@@ -663,9 +692,16 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       help(0, x0, ok0);
       help(1, x1, ok1);
     }
-    for (int i = 0; i < nmine; ++i) {
-      const int64_t t = tile_of(i);
+    for (int i = 0; dyn || i < nmine; ++i) {
       const int b = i & 1;
+      int64_t t;
+      if (dyn) {  // tile id known once the accumulator is full (a sentinel ends the loop)
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+        t = sTile[i & 7];
+        if (t < 0) break;
+      } else {
+        t = tile_of(i);
+      }
       const int64_t row = t * 128 + 32 * q + lane;
       const bool valid = row < a.rows;
       const int64_t slot = ring_slot(a.out, t);
@@ -685,7 +721,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         }
       }
       ring_acquire_slot(a.out, t, lane, lane == 0 ? wa : WaitAcct{});
-      SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+      if (!dyn) SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
       if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128 + cb) + ((uint32_t)(32 * q) << 16);
@@ -776,6 +812,8 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
   uint32_t* sOnes = tmem_slot + 4;                           // 512 B of bf16 1.0 (db MMA operand)
   Params0* p0 = reinterpret_cast<Params0*>(sOnes + 128);    // (first)
+  int* sTile = reinterpret_cast<int*>(p0 + 1);              // [8] dynamic schedule: tile of local iteration i
+  uint64_t* tidbar = reinterpret_cast<uint64_t*>(sTile + 8); // [8] loader -> epilogue: sTile[i % 8] written
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -789,6 +827,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     mbar_init(&fullH[0], kLoadH ? 1 : 32 * kPW);
     mbar_init(&emptyH[0], 1);
     mbar_init(&wdone[0], 1);
+    for (int k = 0; k < 8; ++k) mbar_init(&tidbar[k], 1);
     for (int k = 0; k < 5; ++k) {
       mbar_init(&pfull[k], (kFifoG && k < 2) ? 32 * kPW : 1);  // H_1 planes in slots 0, 1 (producers)
       mbar_init(&pempty[k], 1);
@@ -816,6 +855,10 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
   // G stage of tile i: wgrad -> single stage; else a ring of 2 (sG, sH)
   auto g_stage = [&](int i) -> uint8_t* { return (!kWgrad && (i & 1)) ? sH : sG; };
+  // dynamic tile schedule (G step: no per-CTA partial sums): the loader takes
+  // tiles from a global counter; MMA warp reads ids after the stage barrier,
+  // the epilogue after tidbar (so its mask loads are issued early)
+  const bool dyn = !kWgrad && a.tile_ctr != nullptr;
   // kPR plane slots {slot, use}: use = how many times the slot was filled
   // before.  Three planes per tile, Gh, Hh, Gl (the wgrad reads only the hi
   // plane of H, R28), in a FIFO over slots 0-3 (plane p = 3i + k -> slot
@@ -887,9 +930,23 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         trace_pt(trace, j, i, 0);
       }
     } else if (!kPR && lane == 0) {
-      for (int i = 0; i < nmine; ++i) {
-        const int64_t t = tile_of(i);
-        if (i + 1 < nmine) {
+      for (int i = 0; dyn || i < nmine; ++i) {
+        int64_t t = -1;
+        if (dyn) {
+          t = atomicAdd(a.tile_ctr, 1u);
+          if (t >= ntiles) t = -1;
+          sTile[i & 7] = (int)t;
+          mbar_arrive(&tidbar[i & 7]);
+          if (t < 0) {  // sentinel to the MMA warp through the stage barrier
+            const int s = i & 1;
+            mbar_wait(&emptyG[s], ((i >> 1) & 1) ^ 1);
+            mbar_arrive(&fullG[s]);
+            break;
+          }
+        } else {
+          t = tile_of(i);
+        }
+        if (!dyn && i + 1 < nmine) {
           if (!a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
           if (kWgrad && !kFirst && !a.h.slots) prefetch_l2(a.h.base + tile_of(i + 1) * TB, TB);
         }
@@ -967,11 +1024,12 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         mma_commit(&pempty[gl.slot]);
         mma_commit(&tfull[b]);
       }
-      for (int i = 0; !kPR && i < nmine; ++i) {
-        const int64_t t = tile_of(i);
+      for (int i = 0; !kPR && (dyn || i < nmine); ++i) {
         const int b = i & 1;
         const int s = kWgrad ? 0 : (i & 1);
         SAGIPS_TIMED(wa, 2, mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1)));
+        const int64_t t = dyn ? (int64_t)sTile[i & 7] : tile_of(i);
+        if (t < 0) break;  // sentinel (the epilogue stops at its own tidbar)
         ring_consumed(a.g, t);
         const uint32_t zh = smem_u32(g_stage(i)), zl = zh + kPlane;
         if (kWgrad) {
@@ -1020,8 +1078,15 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, sb[2] = {0.f, 0.f};  // layer-0 gradients
     const float2* X2 = reinterpret_cast<const float2*>(a.X);
     int64_t pend = -1;
-    for (int i = 0; i < nmine; ++i) {
-      const int64_t t = tile_of(i);
+    for (int i = 0; dyn || i < nmine; ++i) {
+      int64_t t;
+      if (dyn) {
+        mbar_wait(&tidbar[i & 7], (i >> 3) & 1);
+        t = sTile[i & 7];
+        if (t < 0) break;
+      } else {
+        t = tile_of(i);
+      }
       const int b = i & 1;
       const int64_t row = t * 128 + 32 * q + lane;
       const bool valid = row < a.rows;
@@ -1185,13 +1250,21 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
 }
 
 // ============================================================== kernels
+// trace: per-CTA launch stamps (start, end) next to the per-tile ones
+__device__ __forceinline__ unsigned long long* cta_stamps(unsigned long long* trace);
 template <bool kSplit, bool kFirst, bool kHead>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd(const __grid_constant__ FwdLaunch a, unsigned long long* trace) {
+  unsigned long long* cs = cta_stamps(trace);
+  if (cs && threadIdx.x == 0) cs[0] = globaltimer();
   fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace);
+  if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
 template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ BwdLaunch a, unsigned long long* trace) {
+  unsigned long long* cs = cta_stamps(trace);
+  if (cs && threadIdx.x == 0) cs[0] = globaltimer();
   bwd_body<kSplit, kFirst, kWgrad, kH1Load>(a, blockIdx.x, gridDim.x, trace);
+  if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
 
 // The whole D step (kD: wgrad, head and layer-0 gradients) or G step (dy) as
@@ -1256,11 +1329,11 @@ int pipe_sm_count() { return sm_count(); }
 
 static size_t fwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return TB + 3 * (size_t)kPlane + 2 * kEW * kStg + 10 * 8 + 8 * 8 + 16 + 4 * (128 + 128 + 256);  // bias, w_head / Params0
+  return TB + 3 * (size_t)kPlane + 2 * kEW * kStg + 10 * 8 + 8 * 8 + 16 + 32 + 4 * (128 + 128 + 256);  // tiles, bias, w_head / Params0
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 22 * 8 + 16 + 512 + sizeof(Params0);
+  return 3 * TB + kEW * kStg + 22 * 8 + 16 + 512 + sizeof(Params0) + 32 + 64;
 }
 
 template <typename K>
@@ -1297,6 +1370,8 @@ static void configure_layers() {
 }
 
 __device__ unsigned long long g_trace[kTraceLaunches][kTraceCtas * kTraceTiles * 4];
+// per-CTA [start, first tile staged, end] globaltimer stamps of each traced launch
+__device__ unsigned long long g_ctatime[kTraceLaunches][kMaxSms][4];
 static int g_trace_on = -1;
 static int g_trace_next = 0;
 static unsigned long long* trace_slot() {
@@ -1310,10 +1385,31 @@ static unsigned long long* trace_slot() {
   return reinterpret_cast<unsigned long long*>(p) + (size_t)(g_trace_next++) * kTraceCtas * kTraceTiles * 4;
 }
 
-size_t tc_trace_bytes() { return sizeof(unsigned long long) * kTraceLaunches * kTraceCtas * kTraceTiles * 4; }
+__device__ __forceinline__ unsigned long long* cta_stamps(unsigned long long* trace) {
+  if (!trace) return nullptr;
+  const size_t li = (size_t)(trace - &g_trace[0][0]) / (kTraceCtas * kTraceTiles * 4);
+  if (li >= (size_t)kTraceLaunches || blockIdx.x >= (unsigned)kMaxSms) return nullptr;
+  return g_ctatime[li][blockIdx.x];
+}
+
+size_t tc_trace_bytes() { return sizeof(g_trace) + sizeof(g_ctatime); }
 int tc_trace_copy(void* host) {
   g_trace_next = 0;
-  return cudaMemcpyFromSymbol(host, g_trace, tc_trace_bytes()) == cudaSuccess ? 0 : -1;
+  if (cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)) != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(static_cast<char*>(host) + sizeof(g_trace), g_ctatime, sizeof(g_ctatime)) == cudaSuccess
+             ? 0 : -1;
+}
+
+// SAGIPS_SYNC=1 (debugging): synchronize after every layer launch and report
+static void debug_sync(const char* what, int kind, cudaStream_t st) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SAGIPS_SYNC");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!on) return;
+  const cudaError_t e = cudaStreamSynchronize(st);
+  fprintf(stderr, "[sagips] %s kind %d: %s\n", what, kind, cudaGetErrorString(e));
 }
 
 int tc_layers_grid(int64_t rows) { return (int)std::min<int64_t>(std::max<int64_t>((rows + 127) / 128, 1), sm_count()); }
@@ -1334,6 +1430,7 @@ void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st) {
     else k_fwd<false, false, true><<<grid, kThreads, sm, st>>>(L, tr);
   }
   count_launch();
+  debug_sync("k_fwd", kind, st);
 }
 
 void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaStream_t st) {
@@ -1355,6 +1452,7 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
   }
 #undef SAGIPS_BWD_LAUNCH
   count_launch();
+  debug_sync("k_bwd", (first ? 1 : 0) + (wgrad ? 2 : 0), st);
 }
 
 // Cooperative launch (all CTAs co-resident, one per SM): returns false if the

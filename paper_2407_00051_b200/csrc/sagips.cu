@@ -106,6 +106,7 @@ static void carve(sagips_ctx* c, char* base) {
                                                 (int64_t)kMaxSms * 4 * 384));
   c->head_tmp = cv.take<float>(D.maxw + 1);
   c->dbpart = cv.take<float>((int64_t)kMaxSms * 128);
+  c->tile_ctrs = cv.take<uint32_t>(sagips_ctx::kTileCtrs);
   // pipelined step: rings (L2-resident), per-tile flags, per-role partials
   if (c->cfg.disc_depth == 4 && c->cfg.disc_hidden == 128) {
     const size_t tb = plane_tile_bytes(true);
@@ -392,6 +393,22 @@ static Ring whole(void* base, uint4* mask = nullptr) {
   return r;
 }
 
+// dynamic tile-schedule counters: one per launch of a step, zeroed at the
+// start of each D / G step (SAGIPS_DYN=0 disables the dynamic schedule)
+static uint32_t* next_tile_ctr(sagips_ctx* c) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SAGIPS_DYN");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!env || c->tile_ctr_next >= sagips_ctx::kTileCtrs) return nullptr;
+  return c->tile_ctrs + c->tile_ctr_next++;
+}
+static void reset_tile_ctrs(sagips_ctx* c, cudaStream_t st) {
+  cudaMemsetAsync(c->tile_ctrs, 0, sizeof(uint32_t) * sagips_ctx::kTileCtrs, st);
+  c->tile_ctr_next = 0;
+}
+
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
   const int kc = want_grads ? 0 : 6;  // kernel-timing classes
@@ -411,6 +428,7 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     m.in = whole(c->dAct[l - 1]); m.W = c->dW + D.w_off[l]; m.bias = c->dB + D.b_off[l];
     m.out = whole(c->dAct[l], c->dMask[l]);
     m.rows = rows; m.alpha = c->cfg.leaky_slope;
+    m.tile_ctr = next_tile_ctr(c);
     kernel_begin(c, kc + 1, st);
     launch_tc_fwd(split, FWD_MID, m, st);
     kernel_end(c, st);
@@ -463,6 +481,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const int Lh = D.L - 1;
   const bool split = tc_split(c);
   const int grid = tc_layers_grid(rows);
+  reset_tile_ctrs(c, st);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
   launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
   int cur = 0;
@@ -493,6 +512,7 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
   const int Lh = D.L - 1;
   const bool split = tc_split(c);
   const float* Y = c->X + 2 * N;  // fake rows
+  reset_tile_ctrs(c, st);
   disc_forward_v2(c, Y, N, 0, 1.0f, 1.0f / (float)N, c->logits_g, false, st);
   launch_finish_loss(c->loss_part, tc_layers_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
   int cur = 0;
@@ -500,6 +520,7 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
     BwdLaunch b;
     b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = N;
     b.alpha = c->cfg.leaky_slope;
+    b.tile_ctr = next_tile_ctr(c);
     if (l == 1) {
       b.X = Y; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.dy = c->dy;
     } else {

@@ -19,7 +19,9 @@ sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 ctx.train_step(0, 0, sp)
 L.debug_trace()  # discard warm-up
 ctx.train_step(1, 0, sp)
-tr = L.debug_trace().astype(np.int64)
+tr, ctas = L.debug_trace(with_ctas=True)
+tr = tr.astype(np.int64)
+ctas = ctas.astype(np.int64)
 names = ["fwd-first", "fwd-mid", "fwd-head", "bwd-L3", "bwd-L2", "bwd-L1", "G fwd-first", "G fwd-mid", "G fwd-head",
          "G bwd-L3", "G bwd-L2", "G bwd-dy"]
 g0 = min(int(tr[li, 0][tr[li, 0][:, 0] > 0, 0].min()) for li in range(12) if (tr[li, 0][:, 0] > 0).sum() >= 3)
@@ -38,6 +40,13 @@ for li in range(12):
     print(f"{names[li]:12s} tiles {n:3d} start {(t0 - g0) / 1e3:7.1f} us span {(t[-1, 3] - t0) / 1e3:8.1f} us  "
           f"period {period:6.0f} ns  staged {prod:6.0f}  staged->mma {mma_wait:6.0f}  mma->epi {mma_to_epi:6.0f}  "
           f"epi {epi:6.0f}")
+    c = ctas[li]
+    c = c[c[:, 0] > 0]
+    if len(c):
+        st, en = c[:, 0], c[:, 1]
+        print(f"{'':12s} CTAs {len(c)}: start spread {(st.max() - st.min()) / 1e3:6.1f} us, end spread "
+              f"{(en.max() - en.min()) / 1e3:6.1f} us, first start -> first tile {(t0 - st.min()) / 1e3:6.1f} us, "
+              f"kernel {(en.max() - st.min()) / 1e3:7.1f} us, CTA0 last tile -> last CTA end {(en.max() - t[-1, 3]) / 1e3:6.1f} us")
 
 
 def pipe_split(dstep, sms=148):
