@@ -60,6 +60,7 @@ struct ExchangeState {
   uint64_t ring_step[2] = {0, 0};
   // device error word and wait accounting
   unsigned int* err = nullptr;      // device: 1 timeout, 2 protocol
+  uint32_t* one = nullptr;          // device constant 1 (stats.outer_fired)
 };
 
 static size_t slot_floats(const sagips_ctx* c) { return (size_t)c->G.nw; }
@@ -250,6 +251,7 @@ void exchange_destroy(sagips_ctx* c) {
   cudaFree(x->gather[0]);
   cudaFree(x->gather[1]);
   cudaFree(x->outer_buf);
+  if (x->one) cudaFree(x->one);
   cudaFree(x->err);
   for (int i = 0; i < 2; ++i) {
     if (x->ev_ready[i]) cudaEventDestroy(x->ev_ready[i]);
@@ -349,9 +351,7 @@ static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   pl.count = nlead;
   for (int i = 0; i < nlead; ++i) pl.p[i] = x->outer_buf + i * pw;
   launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)nlead : 1.0f, st);
-  uint32_t one = 1;
-  XCK(cudaMemcpyAsync(&c->stats->outer_fired, &one, sizeof one, cudaMemcpyHostToDevice, st));
-  XCK(cudaStreamSynchronize(st));  // `one` is on the host stack
+  XCK(cudaMemcpyAsync(&c->stats->outer_fired, x->one, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   return SAGIPS_OK;
 }
 
@@ -481,6 +481,33 @@ sagips_status sagips_connect_nccl(sagips_ctx* c, const void* host_id, size_t byt
   std::memcpy(&id, host_id, sizeof id);
   NCK(ncclCommInitRank(&x->comm_main, c->cfg.world, id, c->cfg.rank));
   NCK(ncclCommSplit(x->comm_main, 0, c->cfg.rank, &x->comm_ring, nullptr));
+  if (!x->one) {
+    XCK(cudaMalloc(&x->one, sizeof(uint32_t)));
+    const uint32_t one = 1;
+    XCK(cudaMemcpy(x->one, &one, sizeof one, cudaMemcpyHostToDevice));
+  }
+  // NCCL sets up peer connections lazily, on the first send/recv between two
+  // ranks (hundreds of ms): exercise the leaders' outer ring and the inner
+  // two-sided ring here, so no training step pays for it
+  const auto& g = c->cfg;
+  const int nlead = g.world / std::max(1, g.group_size);
+  float* tmp = nullptr;
+  XCK(cudaMalloc(&tmp, 2 * sizeof(float)));
+  if (nlead >= 2 && g.outer_every > 0 && g.rank % g.group_size == 0) {
+    const int lp = g.rank / g.group_size;
+    NCK(ncclGroupStart());
+    NCK(ncclSend(tmp, 1, ncclFloat32, ((lp + 1) % nlead) * g.group_size, x->comm_main, x->side));
+    NCK(ncclRecv(tmp + 1, 1, ncclFloat32, ((lp + nlead - 1) % nlead) * g.group_size, x->comm_main, x->side));
+    NCK(ncclGroupEnd());
+  }
+  if (x->g > 1) {
+    NCK(ncclGroupStart());
+    NCK(ncclSend(tmp, 1, ncclFloat32, x->succ, x->comm_ring, x->side));
+    NCK(ncclRecv(tmp + 1, 1, ncclFloat32, x->pred, x->comm_ring, x->side));
+    NCK(ncclGroupEnd());
+  }
+  XCK(cudaStreamSynchronize(x->side));
+  XCK(cudaFree(tmp));
   return SAGIPS_OK;
 }
 
