@@ -562,8 +562,9 @@ static void pipe_split(bool dstep, int ctas[kPipeRoles]) {
       }
     }
   }
-  const double cd[kPipeRoles] = {3.0, 1.6, 3.2, 3.0, 3.0, 3.0};
-  const double cg[kPipeRoles] = {3.0, 1.6, 3.0, 1.4, 1.4, 1.6};
+  // per-tile costs (us) of the roles, from the split sweep of profiles/r01_pipe_sweep_v7.txt
+  const double cd[kPipeRoles] = {3.3, 3.3, 3.9, 3.9, 3.9, 3.9};
+  const double cg[kPipeRoles] = {3.0, 2.8, 2.8, 2.4, 2.4, 1.4};
   const double* cost = dstep ? cd : cg;
   double tot = 0;
   for (int r = 0; r < kPipeRoles; ++r) tot += cost[r];

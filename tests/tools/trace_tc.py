@@ -54,7 +54,7 @@ def pipe_split(dstep, sms=148):
     env = os.environ.get("SAGIPS_PIPE_SPLIT_D" if dstep else "SAGIPS_PIPE_SPLIT_G")
     if env:
         return [int(x) for x in env.split(",")]
-    cost = [3.0, 1.6, 3.2, 3.0, 3.0, 3.0] if dstep else [3.0, 1.6, 3.0, 1.4, 1.4, 1.6]
+    cost = [3.3, 3.3, 3.9, 3.9, 3.9, 3.9] if dstep else [3.0, 2.8, 2.8, 2.4, 2.4, 1.4]
     tot = sum(cost)
     c = [max(1, int(sms * x / tot)) for x in cost]
     r = 0
