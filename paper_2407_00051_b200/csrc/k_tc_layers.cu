@@ -58,6 +58,9 @@ constexpr int kMmaWarp = kPW + kEW;          // 12
 constexpr int kLoadWarp = kMmaWarp + 1;      // 13
 constexpr int kThreads = 32 * (kLoadWarp + 1);  // 448
 constexpr int kSmemLimit = 232448;           // 227 KiB opt-in per CTA
+// first forward layer: plane FIFO + double-buffered staging (as the middle
+// layers) instead of two whole-tile stages
+constexpr bool kFirstFifo = false;  // measured slower (0.48 vs 0.43 ms, D step): producers wait on two plane slots
 
 struct Params0 {  // layer-0 parameters, column-contiguous
   float w0x[128];
@@ -335,7 +338,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   // staging buffer per epilogue warp; other layers: a FIFO of 3 operand
   // plane slots (the lo plane is consumed first and frees early) + two
   // staging buffers per epilogue warp (no wait for the bulk engine's reads)
-  constexpr bool kFifo = !kFirst;
+  constexpr bool kFifo = !kFirst || kFirstFifo;
   constexpr uint32_t kRegion = 3 * kPlane + 2 * kEW * kStg;  // >= 2 TB + kEW kStg
   static_assert(kRegion >= 2 * TB + kEW * kStg, "fwd region");
   uint8_t* sW = smem;
@@ -390,14 +393,30 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   // tiles from a global counter and passes their ids through sTile; a tile's
   // output does not depend on which CTA computes it (no per-CTA partials)
   const bool dyn = kFifo && !kFirst && !kHead && a.tile_ctr != nullptr;
-  // first layer: wait for tile i's whole-tile stage, write its H_1 rows, signal it
+  // plane FIFO: tile i's planes are p = P i (lo, split) and P i + P - 1 (hi), slot p % 3
+  auto slot_lo = [&](int i) { return (P * i) % 3; };
+  auto slot_hi = [&](int i) { return (P * i + P - 1) % 3; };
+  auto use_lo = [&](int i) { return (P * i) / 3; };
+  auto use_hi = [&](int i) { return (P * i + P - 1) / 3; };
+  // first layer: wait for tile i's operand space, write its H_1 rows, signal it
   auto produce_rows = [&](int i, float2 xr, bool ok, int row0, int nrows) {
-    const int s = i & 1;
-    mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
-    const uint32_t st = smem_u32(sA + s * TB);
-    produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, row0, nrows, lane);
-    fence_proxy_async_smem();
-    mbar_arrive(&full[s]);
+    if (kFifo) {
+      const int sl = slot_lo(i), sh = slot_hi(i);
+      if (kSplit) mbar_wait(&empty[sl], (use_lo(i) & 1) ^ 1);
+      mbar_wait(&empty[sh], (use_hi(i) & 1) ^ 1);
+      const uint32_t base = smem_u32(sA);
+      produce_h1<kSplit>(xr, ok, p0, a.alpha, base + sh * kPlane, base + sl * kPlane, row0, nrows, lane);
+      fence_proxy_async_smem();
+      if (kSplit) mbar_arrive(&full[sl]);
+      mbar_arrive(&full[sh]);
+    } else {
+      const int s = i & 1;
+      mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
+      const uint32_t st = smem_u32(sA + s * TB);
+      produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, row0, nrows, lane);
+      fence_proxy_async_smem();
+      mbar_arrive(&full[s]);
+    }
   };
 
   if (warp < kPW) {
@@ -493,7 +512,11 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           mma_commit(&empty[sl]);
         }
         SAGIPS_TIMED(wa, 2, mbar_wait(&full[sh], (ph / 3) & 1));
-        ring_consumed(a.in, t);  // both planes have been read from the input tensor
+        if (!kFirst) ring_consumed(a.in, t);  // both planes have been read from the input tensor
+        if (store_h1) {  // the H_1 hi plane for the layer-1 wgrad (R28)
+          bulk_s2g(a.h1.base + t * TB, smem_u32(sA) + sh * kPlane, kPlane);
+          bulk_commit();
+        }
         if (!kSplit) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t ah = smem_u32(sA) + sh * kPlane;
@@ -506,6 +529,24 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         }
         mma_commit(&empty[sh]);
         mma_commit(&tfull[b]);
+        if (store_h1) {
+          if (kSplit) mbar_arrive(&empty[slot_lo(i)]);  // (the lo plane is not stored)
+          if (i > 0) {  // the previous tile's H_1 store is complete: publish it, free its hi slot
+            bulk_wait_groups<1>();
+            if (a.h1.rdy) {
+              fence_proxy_async_global();
+              red_release_add(a.h1.rdy + tile_of(i - 1), kEW);
+            }
+            mbar_arrive(&empty[slot_hi(i - 1)]);
+          }
+        }
+      }
+      if (kFifo && store_h1 && nmine > 0) {
+        bulk_wait0();
+        if (a.h1.rdy) {
+          fence_proxy_async_global();
+          red_release_add(a.h1.rdy + tile_of(nmine - 1), kEW);
+        }
       }
       for (int i = 0; !kFifo && i < nmine; ++i) {
         const int s = i & 1, b = i & 1;
@@ -536,7 +577,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
           mbar_arrive(&empty[s ^ 1]);
         }
       }
-      if (store_h1 && nmine > 0) {
+      if (!kFifo && store_h1 && nmine > 0) {
         bulk_wait0();
         if (a.h1.rdy) {
           fence_proxy_async_global();

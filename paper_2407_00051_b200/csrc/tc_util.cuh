@@ -11,6 +11,7 @@
 // physical copy serves the forward, dgrad and wgrad GEMMs.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_bf16.h>
 
 namespace sagips {
@@ -83,7 +84,11 @@ static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parit
       if (mbar_try_wait(bar, parity)) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    if (t - t0 > 8000000000ull) __trap();
+    if (t - t0 > 8000000000ull) {
+      printf("sagips: mbarrier wait timed out: block %d thread %d smem 0x%x parity %u\n", (int)blockIdx.x,
+             (int)threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
   }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
