@@ -105,7 +105,7 @@ struct FwdLaunch {
   float label_rest = 0.f;
   float scale = 1.f;
   float* logits = nullptr;
-  float* part_head = nullptr;  // [ctas*8][129]
+  float* part_head = nullptr;  // [ctas][129]
   double* loss_part = nullptr; // [ctas]
   int want_wgrad = 0;
 };
@@ -122,7 +122,7 @@ struct BwdLaunch {
   float* dy = nullptr;         // (first, no wgrad)
   float* part = nullptr;       // [ctas][128][128]
   float* part_db = nullptr;    // [ctas][128]
-  float* part_l0 = nullptr;    // [ctas*4][384]
+  float* part_l0 = nullptr;    // [ctas][384]
   uint32_t* tile_ctr = nullptr;  // no wgrad (G step): dynamic tile schedule counter (zeroed before the launch)
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };

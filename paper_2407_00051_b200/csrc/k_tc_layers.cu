@@ -681,22 +681,29 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     }
     if (lane == 0) bulk_wait0();
     ring_publish<0>(a.out, pend, lane, 2);
-    // per-(CTA, epilogue warp) partials; loss per CTA in fp64, fixed order
-    const int64_t pe = (int64_t)j * kEW + e;
-    if (a.want_wgrad) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) a.part_head[pe * 129 + 32 * c + lane] = gacc[c];
-    }
+    // per-CTA partials: the 8 warps' head gradients summed in shared memory
+    // (the staging area is free now) in warp order; loss in fp64
 #pragma unroll
     for (int w = 16; w >= 1; w >>= 1) {
       gbacc += __shfl_xor_sync(0xffffffffu, gbacc, w);
       lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
     }
-    if (lane == 0) {
-      if (a.want_wgrad) a.part_head[pe * 129 + 128] = gbacc;
-      sloss[e] = lacc;
+    float* sred = reinterpret_cast<float*>(sStg);  // [8][129]
+    epi_sync();  // every warp is done with its staging (its bulk stores have completed)
+    if (a.want_wgrad) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sred[e * 129 + 32 * c + lane] = gacc[c];
+      if (lane == 0) sred[e * 129 + 128] = gbacc;
     }
+    if (lane == 0) sloss[e] = lacc;
     epi_sync();
+    if (a.want_wgrad && e < 5) {
+      for (int k = 32 * e + lane; k < 129 && k < 32 * (e + 1); k += 32) {
+        float v = 0.f;
+        for (int w = 0; w < kEW; ++w) v += sred[w * 129 + k];
+        a.part_head[(int64_t)j * 129 + k] = v;
+      }
+    }
     if (e == 0 && lane == 0) {
       double sum = 0.0;
       for (int k = 0; k < kEW; ++k) sum += sloss[k];
@@ -1248,12 +1255,24 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     if (!kFirst) ring_publish<0>(a.gout, pend, lane);
     const int64_t pq = (int64_t)j * 4 + q;
     if (kWgrad && kFirst) {
+      // per-CTA layer-0 partials: the 4 lane quarters summed in shared memory
+      // (the plane slots are free now; fixed order)
+      (void)pq;
+      tc_fence_before();
+      epi_sync();  // all epilogue warps are past their last tile
+      float* sred = reinterpret_cast<float*>(sG);  // [4 quarters][384]
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int cc = cb + 32 * c + lane;
-        a.part_l0[pq * 384 + 2 * cc] = s0[c];
-        a.part_l0[pq * 384 + 2 * cc + 1] = s1[c];
-        a.part_l0[pq * 384 + 256 + cc] = sb[c];
+        sred[q * 384 + 2 * cc] = s0[c];
+        sred[q * 384 + 2 * cc + 1] = s1[c];
+        sred[q * 384 + 256 + cc] = sb[c];
+      }
+      epi_sync();
+      for (int k = e * 32 + lane; k < 384; k += 32 * kEW) {
+        float v = 0.f;
+        for (int qq = 0; qq < 4; ++qq) v += sred[qq * 384 + k];
+        a.part_l0[(int64_t)j * 384 + k] = v;
       }
     }
     if (kWgrad) {

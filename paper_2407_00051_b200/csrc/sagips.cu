@@ -503,7 +503,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     kernel_end(c, st);
     cur ^= 1;
   }
-  disc_reduce_adam(c, 8 * grid, nparts, 4 * grid, st);
+  disc_reduce_adam(c, grid, nparts, grid, st);
 }
 
 static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
@@ -658,7 +658,7 @@ static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, in
   if (dstep) {
     int nparts[kMaxLayers] = {};
     for (int k = 0; k < 3; ++k) nparts[3 - k] = P.ctas[3 + k];
-    disc_reduce_adam(c, 8 * nh, nparts, 4 * P.ctas[5], st);
+    disc_reduce_adam(c, nh, nparts, P.ctas[5], st);
   }
   return true;
 }

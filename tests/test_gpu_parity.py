@@ -256,3 +256,44 @@ def test_full_size_paper_step_sampled():
     assert np.array_equal(hist[0], out["hist"][0])
     assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
     assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
+
+
+def test_step_is_deterministic():
+    """Two contexts from the same state produce bit-identical losses,
+    gradients, events and parameters (fixed-order reductions everywhere; the
+    dynamic tile schedule only moves tiles whose outputs do not depend on the
+    CTA).  Paper widths, 2N = 2^18 rows (several tiles per CTA)."""
+    L = lib()
+    outs = []
+    for _ in range(2):
+        cfg = L.config_init(1, seed=13, param_samples=128, events_per_sample=1024)
+        ctx = make_ctx(cfg)
+        for t in range(2):
+            ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
+        torch.cuda.synchronize()
+        outs.append({w: ctx.get(w) for w in (L.T_DISC_DW, L.T_DISC_DB, L.T_DISC_W, L.T_DY, L.T_GEN_DW, L.T_LOGITS_D,
+                                              L.T_EVENTS)})
+        s = ctx.get(L.T_STATS)
+        outs[-1]["loss"] = np.array([s.loss_d, s.loss_g])
+    for k in outs[0]:
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+def test_kernel_times_cover_the_layer_passes():
+    """sagips_kernel_times: the 12 tcgen05 layer-pass classes of a paper-width
+    step are all timed (positive), and their sum fits inside the D + G
+    phases."""
+    L = lib()
+    cfg = L.config_init(1, seed=3, param_samples=64, events_per_sample=1024)
+    cfg.phase_timing = 1
+    ctx = make_ctx(cfg)
+    for t in range(3):
+        ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
+    ctx.timing_reset()
+    for t in range(3, 6):
+        ctx.train_step(t, L.STEP_LOCAL_ONLY, _stream())
+    kt, n = ctx.kernel_times()
+    ph, _ = ctx.phase_times()
+    assert n == 3
+    assert all(v > 0 for v in kt.values()), kt
+    assert sum(kt.values()) <= ph["disc_step"] + ph["gen_loss_through_disc"] + 1e-3
