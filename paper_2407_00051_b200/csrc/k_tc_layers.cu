@@ -842,6 +842,11 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   // whole-tile H stage (released right after the wgrad MMAs) overlaps better
   constexpr bool kPR = kSplit && kLoadH;
   constexpr bool kFifoG = false;                            // (plane slots: H_1 fixed, G FIFO)
+  // kT (D step, first layer, plane ring): the dgrad computes G_1^T (A = W_1
+  // MN-major, B = G_2 K-major), so TMEM lane = channel c and column = row:
+  // dW_0 = G_1^T X and db_0 accumulate per thread over rows (no shuffles),
+  // with the tile's X rows bulk-loaded into shared memory
+  constexpr bool kT = kFirst && kWgrad && kPR;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sG = sW + TB;     // G stage 0 (kPR: plane slots 0, 1)
@@ -857,9 +862,12 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   uint64_t* wdone = bars + 10;  // [1]
   uint64_t* pfull = bars + 12;  // [5] (kPR)
   uint64_t* pempty = bars + 17; // [5] (kPR)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint64_t* xfull = bars + 22;  // [2] (kT) loader -> epilogue: X rows of a tile in sX
+  uint64_t* xempty = bars + 24; // [2] (kT) epilogue -> loader
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
   uint32_t* sOnes = tmem_slot + 4;                           // 512 B of bf16 1.0 (db MMA operand)
   Params0* p0 = reinterpret_cast<Params0*>(sOnes + 128);    // (first)
+  float2* sX = reinterpret_cast<float2*>(p0);               // (kT) [2][128] X rows, overlays p0 .. tidbar
   int* sTile = reinterpret_cast<int*>(p0 + 1);              // [8] dynamic schedule: tile of local iteration i
   uint64_t* tidbar = reinterpret_cast<uint64_t*>(sTile + 8); // [8] loader -> epilogue: sTile[i % 8] written
 
@@ -876,6 +884,10 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     mbar_init(&emptyH[0], 1);
     mbar_init(&wdone[0], 1);
     for (int k = 0; k < 8; ++k) mbar_init(&tidbar[k], 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&xfull[k], 1);
+      mbar_init(&xempty[k], 32 * kEW);
+    }
     for (int k = 0; k < 5; ++k) {
       mbar_init(&pfull[k], (kFifoG && k < 2) ? 32 * kPW : 1);  // H_1 planes in slots 0, 1 (producers)
       mbar_init(&pempty[k], 1);
@@ -884,7 +896,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   }
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   for (int i = tid; i < 128; i += kThreads) sOnes[i] = 0x3F803F80u;
-  if (kFirst) {
+  if (kFirst && !kT) {
     for (int i = tid; i < 128; i += kThreads) {
       p0->w0x[i] = a.W0[2 * i];
       p0->w0y[i] = a.W0[2 * i + 1];
@@ -969,6 +981,14 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       for (int i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const uint8_t* gsrc = a.g.base + ring_slot(a.g, t) * TB;
+        if (kT) {  // the tile's X rows (1 KiB; the epilogue zeroes rows past the end)
+          const int xb = i & 1;
+          mbar_wait(&xempty[xb], ((i >> 1) & 1) ^ 1);
+          const int64_t r0 = t * 128;
+          const uint32_t bytes = (uint32_t)((min((int64_t)128, a.rows - r0) * 8 + 15) & ~15);
+          mbar_arrive_expect_tx(&xfull[xb], bytes);
+          bulk_g2s(smem_u32(sX + xb * 128), reinterpret_cast<const float2*>(a.X) + r0, bytes, &xfull[xb]);
+        }
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
         const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
@@ -1045,12 +1065,18 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
+        constexpr uint32_t id_dT = make_idesc_bf16(128, 128, 1, 0);  // A = W (MN-major), B = G (K-major)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
           const uint64_t g = make_desc(agh + kk, 16, 1024);
-          mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
-          mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
+          if (kT) {  // D = G_1^T [channels][rows]
+            mma_bf16(d, make_desc(wh + km, 16384, 1024), g, id_dT, k > 0);
+            mma_bf16(d, make_desc(wl + km, 16384, 1024), g, id_dT, 1);
+          } else {
+            mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
+            mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
+          }
         }
         mma_commit(&pempty[gh.slot]);
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
@@ -1067,7 +1093,8 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
-          mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
+          if (kT) mma_bf16(d, make_desc(wh + km, 16384, 1024), make_desc(agl + kk, 16, 1024), id_dT, 1);
+          else mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
         }
         mma_commit(&pempty[gl.slot]);
         mma_commit(&tfull[b]);
@@ -1126,7 +1153,46 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, sb[2] = {0.f, 0.f};  // layer-0 gradients
     const float2* X2 = reinterpret_cast<const float2*>(a.X);
     int64_t pend = -1;
-    for (int i = 0; dyn || i < nmine; ++i) {
+    if (kT) {
+      // thread = channel c = 32q + lane (TMEM lane); warp half h = rows 64h..64h+63
+      const int c = 32 * q + lane;
+      const float w0x = __ldg(a.W0 + 2 * c), w0y = __ldg(a.W0 + 2 * c + 1), b0c = __ldg(a.b0 + c);
+      float t0 = 0.f, t1 = 0.f, tb = 0.f;  // sum over rows of g x_0, g x_1, g (fixed row order)
+      for (int i = 0; i < nmine; ++i) {
+        const int64_t t = tile_of(i);
+        const int b = i & 1, xb = i & 1;
+        mbar_wait(&xfull[xb], (i >> 1) & 1);
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
+        tc_fence_after();
+        const float2* xs = sX + xb * 128;
+        const int64_t valid_rows = a.rows - t * 128;
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          float v[32];  // G_1^T[c][rows 64h + 32ch + k] before LeakyReLU'
+          tmem_ld32(tmem + (uint32_t)(b * 128 + 64 * h + 32 * ch) + ((uint32_t)(32 * q) << 16), v);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const int r = 64 * h + 32 * ch + k;
+            const float2 x = (r < valid_rows) ? xs[r] : make_float2(0.f, 0.f);
+            // Z_1 recomputed exactly as the forward's producers do
+            const float z1 = fmaf(x.x, w0x, fmaf(x.y, w0y, b0c));
+            const float g = v[k] * (z1 > 0.f ? 1.f : a.alpha);
+            t0 = fmaf(g, x.x, t0);
+            t1 = fmaf(g, x.y, t1);
+            tb += g;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[b]);
+        mbar_arrive(&xempty[xb]);
+        if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
+      }
+      s0[0] = t0;
+      s1[0] = t1;
+      sb[0] = tb;
+    }
+    for (int i = 0; !kT && (dyn || i < nmine); ++i) {
       int64_t t;
       if (dyn) {
         mbar_wait(&tidbar[i & 7], (i >> 3) & 1);
@@ -1255,23 +1321,31 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     if (!kFirst) ring_publish<0>(a.gout, pend, lane);
     const int64_t pq = (int64_t)j * 4 + q;
     if (kWgrad && kFirst) {
-      // per-CTA layer-0 partials: the 4 lane quarters summed in shared memory
-      // (the plane slots are free now; fixed order)
+      // per-CTA layer-0 partials summed in shared memory (the plane slots are
+      // free now; fixed order): kT -- the two row halves of each channel;
+      // otherwise the 4 lane quarters of each column
       (void)pq;
       tc_fence_before();
       epi_sync();  // all epilogue warps are past their last tile
-      float* sred = reinterpret_cast<float*>(sG);  // [4 quarters][384]
+      float* sred = reinterpret_cast<float*>(sG);  // [4][384]
+      if (kT) {
+        const int c = 32 * q + lane;
+        sred[h * 384 + 2 * c] = s0[0];
+        sred[h * 384 + 2 * c + 1] = s1[0];
+        sred[h * 384 + 256 + c] = sb[0];
+      } else {
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cc = cb + 32 * c + lane;
-        sred[q * 384 + 2 * cc] = s0[c];
-        sred[q * 384 + 2 * cc + 1] = s1[c];
-        sred[q * 384 + 256 + cc] = sb[c];
+        for (int c = 0; c < 2; ++c) {
+          const int cc = cb + 32 * c + lane;
+          sred[q * 384 + 2 * cc] = s0[c];
+          sred[q * 384 + 2 * cc + 1] = s1[c];
+          sred[q * 384 + 256 + cc] = sb[c];
+        }
       }
       epi_sync();
       for (int k = e * 32 + lane; k < 384; k += 32 * kEW) {
         float v = 0.f;
-        for (int qq = 0; qq < 4; ++qq) v += sred[qq * 384 + k];
+        for (int qq = 0; qq < (kT ? 2 : 4); ++qq) v += sred[qq * 384 + k];
         a.part_l0[(int64_t)j * 384 + k] = v;
       }
     }
@@ -1393,7 +1467,7 @@ static size_t fwd_smem(bool split) {
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 22 * 8 + 16 + 512 + sizeof(Params0) + 32 + 64;
+  return 3 * TB + kEW * kStg + 26 * 8 + 16 + 512 + std::max<size_t>(sizeof(Params0) + 32 + 64, 2 * 128 * 8);
 }
 
 template <typename K>
