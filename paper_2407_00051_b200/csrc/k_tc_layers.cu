@@ -68,7 +68,9 @@ struct Params0 {  // layer-0 parameters, column-contiguous
   float b0[128];
 };
 
-__device__ __forceinline__ float lrelu(float z, float a) { return z > 0.f ? z : z * a; }
+// LeakyReLU for 0 <= a < 1 (validated, R6): max(z, a z) equals (z > 0 ? z : a z)
+// bit for bit (also for -0 and NaN) in two instructions
+__device__ __forceinline__ float lrelu(float z, float a) { return fmaxf(z, z * a); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");

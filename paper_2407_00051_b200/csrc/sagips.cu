@@ -169,6 +169,7 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
     if (!(g->true_params[3 * o + 1] > 0.f) || !(g->true_params[3 * o + 2] > 0.f))
       return bad("true c1, c2 must be > 0 (softplus range)");
   if (g->hist_bins < 1 || g->hist_bins > 4096) return bad("hist_bins in [1, 4096]");
+  if (!(g->leaky_slope >= 0.f && g->leaky_slope < 1.f)) return bad("leaky_slope must be in [0, 1) (R6)");
   if (g->disc_impl < SAGIPS_DISC_AUTO || g->disc_impl > SAGIPS_DISC_TCGEN05) return bad("unknown disc_impl");
   if (g->disc_impl == SAGIPS_DISC_TCGEN05 && hd != 128) return bad("tcgen05 layers need disc_hidden == 128");
   if (g->precision == SAGIPS_PREC_BF16 && (hd != 128 || g->disc_impl == SAGIPS_DISC_SIMT))
