@@ -41,6 +41,31 @@ __device__ __forceinline__ uint4 philox_call(PhiloxKey key, uint32_t index, uint
   return philox4x32_10(make_uint4(index, step, rank, stream), key);
 }
 
+// The ten round keys, computed once per thread (a grid-stride loop calling
+// philox4x32_10 recomputes k + r*W every call).
+struct PhiloxRoundKeys {
+  uint32_t k0[10], k1[10];
+};
+__device__ __forceinline__ PhiloxRoundKeys round_keys(PhiloxKey key) {
+  PhiloxRoundKeys rk;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    rk.k0[r] = key.k0 + (uint32_t)r * 0x9E3779B9u;
+    rk.k1[r] = key.k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  return rk;
+}
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const PhiloxRoundKeys& rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ rk.k0[r], (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ rk.k1[r],
+                   (uint32_t)p0);
+  }
+  return c;
+}
+
 __device__ __forceinline__ uint32_t word_of(uint4 r, int lane) {
   return lane == 0 ? r.x : lane == 1 ? r.y : lane == 2 ? r.z : r.w;
 }
@@ -71,9 +96,13 @@ __device__ __forceinline__ float quantile_f32(float u, float c0, float c1, float
 // histogram bin: 0 underflow/NaN, 1..bins, bins+1 overflow.  t = (y-lo)*scale
 // in fp32 (two roundings, as R22); clamping t to [-1, bins] (fmaxf drops a
 // NaN) and flooring gives -1 for t < 0 or NaN, bins for t >= bins.
+// floor(t) for t in [-1, bins] (bins <= 4096) without the quarter-rate F2I:
+// t + 1.5 * 2^23 rounded down is exactly 1.5 * 2^23 + floor(t) (unit ulp
+// there), whose bits are 0x4B400000 + floor(t).
 __device__ __forceinline__ int hist_bin(float y, float lo, float scale, int bins) {
   const float t = __fmul_rn(__fsub_rn(y, lo), scale);
-  return __float2int_rd(fminf(fmaxf(t, -1.0f), static_cast<float>(bins))) + 1;
+  const float c = fminf(fmaxf(t, -1.0f), static_cast<float>(bins));
+  return __float_as_int(__fadd_rd(c, 12582912.0f)) - 0x4B400000 + 1;
 }
 
 __device__ __forceinline__ float softplus_f(float x) {

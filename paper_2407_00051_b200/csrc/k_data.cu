@@ -151,12 +151,13 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
   uint32_t* hx1 = my + (bins + 2);
   uint32_t* hy0 = my + 2 * (bins + 2);
   uint32_t* hy1 = my + 3 * (bins + 2);
+  const PhiloxRoundKeys rk = round_keys(key);
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
-    const uint4 wa = philox_call(key, 2 * g, step, rank, fake_stream);
-    const uint4 wb = philox_call(key, 2 * g + 1, step, rank, fake_stream);
+    const uint4 wa = philox4x32_10(make_uint4(2 * g, step, rank, fake_stream), rk);
+    const uint4 wb = philox4x32_10(make_uint4(2 * g + 1, step, rank, fake_stream), rk);
     const uint32_t wf[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
     uint4 wr = make_uint4(0, 0, 0, 0);
-    if (kReal) wr = philox_call(key, g, step, rank, kStreamReal);
+    if (kReal) wr = philox4x32_10(make_uint4(g, step, rank, kStreamReal), rk);
     // sample of the group's first event: one division per group
     const uint32_t s = 4 * g / (uint32_t)m;
     const float* cs = c + 6 * (size_t)s;
