@@ -95,6 +95,7 @@ struct FwdLaunch {
   const float* X = nullptr;    // [rows][2] (first)
   const float* W0 = nullptr;   // [128][2] (first)
   const float* b0 = nullptr;   // [128] (first)
+  int first_help = 0;          // first: the epilogue warps produce H_1 rows 64-127 (else the producer warps do all)
   const float* W = nullptr;    // [128][128]
   const float* bias = nullptr;
   int64_t rows = 0;

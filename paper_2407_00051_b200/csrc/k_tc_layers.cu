@@ -41,6 +41,7 @@
 //   epilogue.  Without wgrad (G step) the H stage becomes a second G stage.
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ctx.h"
 #include "tc_util.cuh"
@@ -85,14 +86,70 @@ __device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint3
 // named barrier among the 8 epilogue warps
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEW) : "memory"); }
 
+// ---- packed fp32 pairs: FADD2 / FMUL2 / FFMA2 (sm_100a), each lane rounded
+// exactly as the scalar instruction (RN), one issue slot per pair
+__device__ __forceinline__ uint64_t pk2(float2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(d);
+}
+// a * b + c, fused (as fmaf)
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(d);
+}
+
+// bf16x2 word {low half: bf16(a), high half: bf16(b)}, round to nearest even
+__device__ __forceinline__ uint32_t bf16x2_rn(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
 // hi = bf16(a,b), lo = bf16(a - hi, b - hi)
 __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  const float2 hf = __bfloat1622float2(h);
-  const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
+  hi = bf16x2_rn(a, b);
+  const float2 hf = make_float2(__uint_as_float(hi << 16), __uint_as_float(hi & 0xffff0000u));
+  const float2 d = sub2(make_float2(a, b), hf);
+  lo = bf16x2_rn(d.x, d.y);
 }
+// h = LeakyReLU(z) of a pair, split into hi / lo words
+__device__ __forceinline__ void lrelu_split2(float2 z, float2 alpha2, uint32_t& hi, uint32_t& lo) {
+  const float2 t = mul2(z, alpha2);
+  split2(fmaxf(z.x, t.x), fmaxf(z.y, t.y), hi, lo);
+}
+// Activation sign masks (16 B per row, 32 bits per 32-column block): in each
+// block, column 2k is bit k and column 2k+1 is bit 16 + k, set iff
+// bf16(H) > 0, from the packed hi word of the pair in one compare.  This is
+// [Z > 0] except for 0 < Z < 2^-134 (bf16(H) underflows to +0), far below the
+// GEMM's own rounding (R30).
+__device__ __forceinline__ uint32_t pos_bits(uint32_t hi, int k) {
+  uint32_t gt;
+  asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(gt) : "r"(hi), "r"(0u));
+  return gt & (0x00010001u << k);
+}
+// bit of column k (0..31) of a 32-column block in that layout
+__host__ __device__ constexpr int mask_bit(int k) { return (k >> 1) + 16 * (k & 1); }
 
 // 16 packed words = columns 32c..32c+31 of the warp's 64-column region, row
 // `lane` of the warp's 32-row block -> the staging buffer (SW128 layout of
@@ -173,41 +230,60 @@ __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint3
   }
 }
 
-// SIMT producer of H_1 planes: rows row0 .. row0 + nrows - 1 of one tile
-// (nrows a multiple of 4, <= 32); lane l: columns 4l..4l+3; xr = lane i's
-// prefetched input row row0 + i (i < nrows).
-template <bool kSplit>
+// SIMT producer of H_1 planes: rows row0 .. row0 + kRows - 1 of one tile
+// (row0 % 8 == 0); lane l: channels 8(l % 16) .. 8(l % 16) + 7 (one 16-byte
+// chunk) of the rows of parity l / 16, two rows per warp instruction; xr =
+// lane i's prefetched input row row0 + i (i < kRows).  Z_1 = fma(x0, w0x,
+// fma(x1, w0y, b0)) per channel, the order the backward recomputes it in.
+// Rows past the end (ragged last tile) are written as zeros.
+template <bool kSplit, int kRows>
 __device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0* p0, float alpha, uint32_t hi,
-                                           uint32_t lo, int row0, int nrows, int l) {
-  const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[4 * l]);
-  const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[4 * l]);
-  const float4 bb = *reinterpret_cast<const float4*>(&p0->b0[4 * l]);
-  const unsigned vbits = __ballot_sync(0xffffffffu, xvalid);
-  const uint32_t cbase = (uint32_t)(l >> 4) * 16384u + 8u * (uint32_t)(l & 1);
-  const int jj = (l >> 1) & 7;
-#pragma unroll 1
-  for (int i0 = 0; i0 < nrows; i0 += 4) {
-    uint32_t hw[4][2], lw[4][2];
+                                           uint32_t lo, int row0, int l) {
+  static_assert(kRows % 8 == 0 && kRows <= 32, "rows");
+  const int jc = l & 15, par = l >> 4;
+  float2 wx[4], wy[4], bb[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // 4 independent rows in flight
-      const float x0 = __shfl_sync(0xffffffffu, xr.x, i0 + u), x1 = __shfl_sync(0xffffffffu, xr.y, i0 + u);
-      // branch-free: rows past the end are multiplied by 0 (their x is 0, so the values are finite)
-      const float ok = ((vbits >> (i0 + u)) & 1u) ? 1.f : 0.f;
-      const float a = ok * lrelu(fmaf(x0, wx.x, fmaf(x1, wy.x, bb.x)), alpha);
-      const float b = ok * lrelu(fmaf(x0, wx.y, fmaf(x1, wy.y, bb.y)), alpha);
-      const float c = ok * lrelu(fmaf(x0, wx.z, fmaf(x1, wy.z, bb.z)), alpha);
-      const float d = ok * lrelu(fmaf(x0, wx.w, fmaf(x1, wy.w, bb.w)), alpha);
-      split2(a, b, hw[u][0], lw[u][0]);
-      split2(c, d, hw[u][1], lw[u][1]);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int r = row0 + i0 + u;
-      const uint32_t off = cbase + (uint32_t)(r >> 3) * 1024u + (uint32_t)(r & 7) * 128u + ((uint32_t)(jj ^ (r & 7)) << 4);
-      sts64(hi + off, hw[u][0], hw[u][1]);
-      if (kSplit) sts64(lo + off, lw[u][0], lw[u][1]);
-    }
+  for (int p = 0; p < 4; ++p) {
+    wx[p] = *reinterpret_cast<const float2*>(&p0->w0x[8 * jc + 2 * p]);
+    wy[p] = *reinterpret_cast<const float2*>(&p0->w0y[8 * jc + 2 * p]);
+    bb[p] = *reinterpret_cast<const float2*>(&p0->b0[8 * jc + 2 * p]);
   }
+  const float2 alpha2 = make_float2(alpha, alpha);
+  constexpr unsigned kNeed = kRows == 32 ? 0xffffffffu : ((1u << kRows) - 1u);
+  const unsigned vbits = __ballot_sync(0xffffffffu, xvalid) & kNeed;
+  // SW128 offset of (row row0 + 8 b + 2 u + par, chunk jc) = base + 1024 b + sw[u]
+  const uint32_t base = (uint32_t)(jc >> 3) * 16384u + (uint32_t)(row0 >> 3) * 1024u;
+  const int jp = (jc & 7) ^ par;
+  uint32_t sw[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) sw[u] = (uint32_t)(2 * u + par) * 128u + ((uint32_t)(jp ^ (2 * u)) << 4);
+  auto rows = [&](auto ragged) {
+#pragma unroll
+    for (int it = 0; it < kRows / 2; ++it) {
+      const int src = 2 * it + par;
+      const float x0 = __shfl_sync(0xffffffffu, xr.x, src), x1 = __shfl_sync(0xffffffffu, xr.y, src);
+      const float2 X0 = make_float2(x0, x0), X1 = make_float2(x1, x1);
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const float2 z = fma2(X0, wx[p], fma2(X1, wy[p], bb[p]));
+        if constexpr (decltype(ragged)::value) {
+          const float ok = ((vbits >> src) & 1u) ? 1.f : 0.f;
+          const float2 t = mul2(z, alpha2);
+          split2(ok * fmaxf(z.x, t.x), ok * fmaxf(z.y, t.y), hw[p], lw[p]);
+        } else {
+          lrelu_split2(z, alpha2, hw[p], lw[p]);
+        }
+      }
+      const uint32_t off = base + (uint32_t)(it >> 2) * 1024u + sw[it & 3];
+      sts128(hi + off, hw[0], hw[1], hw[2], hw[3]);
+      if (kSplit) sts128(lo + off, lw[0], lw[1], lw[2], lw[3]);
+    }
+  };
+  if (vbits == kNeed)
+    rows(std::false_type{});
+  else
+    rows(std::true_type{});
 }
 
 // ---- optional timeline trace (SAGIPS_TRACE=1): globaltimer stamps per tile
@@ -363,7 +439,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     check_smem_alignment(smem);
     for (int i = 0; i < 3; ++i) {
       // first layer: H_1 rows 0-63 by the producer warps, 64-127 by the epilogue warps
-      mbar_init(&full[i], kFirst ? 32 * (kPW + kEW) : 1);
+      mbar_init(&full[i], kFirst ? 32 * (kPW + (a.first_help ? kEW : 0)) : 1);
       mbar_init(&empty[i], (kFirst && a.h1.base) ? 2 : 1);  // + the H_1 hi-plane store's read (lo: immediate)
     }
     for (int i = 0; i < 2; ++i) {
@@ -401,13 +477,15 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   auto use_lo = [&](int i) { return (P * i) / 3; };
   auto use_hi = [&](int i) { return (P * i + P - 1) / 3; };
   // first layer: wait for tile i's operand space, write its H_1 rows, signal it
-  auto produce_rows = [&](int i, float2 xr, bool ok, int row0, int nrows) {
+  // (nrows: std::integral_constant, 16 for the producer warps, 8 for the helpers)
+  auto produce_rows = [&](int i, float2 xr, bool ok, int row0, auto nrows) {
+    constexpr int kRows = decltype(nrows)::value;
     if (kFifo) {
       const int sl = slot_lo(i), sh = slot_hi(i);
       if (kSplit) mbar_wait(&empty[sl], (use_lo(i) & 1) ^ 1);
       mbar_wait(&empty[sh], (use_hi(i) & 1) ^ 1);
       const uint32_t base = smem_u32(sA);
-      produce_h1<kSplit>(xr, ok, p0, a.alpha, base + sh * kPlane, base + sl * kPlane, row0, nrows, lane);
+      produce_h1<kSplit, kRows>(xr, ok, p0, a.alpha, base + sh * kPlane, base + sl * kPlane, row0, lane);
       fence_proxy_async_smem();
       if (kSplit) mbar_arrive(&full[sl]);
       mbar_arrive(&full[sh]);
@@ -415,7 +493,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       const int s = i & 1;
       mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
       const uint32_t st = smem_u32(sA + s * TB);
-      produce_h1<kSplit>(xr, ok, p0, a.alpha, st, st + kPlane, row0, nrows, lane);
+      produce_h1<kSplit, kRows>(xr, ok, p0, a.alpha, st, st + kPlane, row0, lane);
       fence_proxy_async_smem();
       mbar_arrive(&full[s]);
     }
@@ -424,11 +502,13 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   if (warp < kPW) {
     // ---------------- SIMT producers of H_1 (first layer only)
     if (kFirst) {
+      // rows 16 w .. 16 w + 15 (with helpers) or 32 w .. 32 w + 31
+      const int nr = a.first_help ? 16 : 32;
       const float2* X2 = reinterpret_cast<const float2*>(a.X);
       auto load_x = [&](int i, bool& ok) {
         ok = false;
-        if (i >= nmine || lane >= 16) return make_float2(0.f, 0.f);
-        const int64_t r = tile_of(i) * 128 + 16 * warp + lane;
+        if (i >= nmine || lane >= nr) return make_float2(0.f, 0.f);
+        const int64_t r = tile_of(i) * 128 + nr * warp + lane;
         ok = r < a.rows;
         return ok ? __ldg(X2 + r) : make_float2(0.f, 0.f);
       };
@@ -437,7 +517,10 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       for (int i = 0; i < nmine; ++i) {
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
-        produce_rows(i, xr, ok, 16 * warp, 16);
+        if (a.first_help)
+          produce_rows(i, xr, ok, 16 * warp, std::integral_constant<int, 16>{});
+        else
+          produce_rows(i, xr, ok, 32 * warp, std::integral_constant<int, 32>{});
         if (warp == 0 && lane == 0) trace_pt(trace, j, i, 0);
         xr = xn;
         ok = ok_next;
@@ -725,16 +808,17 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     // i + 2 is free once the MMAs of tile i -- whose accumulator this warp
     // has just read -- are done
     const float2* X2 = reinterpret_cast<const float2*>(a.X);
+    const bool helping = kFirst && a.first_help;
     auto help_x = [&](int i, bool& ok) {
       ok = false;
-      if (!kFirst || i >= nmine || lane >= 8) return make_float2(0.f, 0.f);
+      if (!helping || i >= nmine || lane >= 8) return make_float2(0.f, 0.f);
       const int64_t r = tile_of(i) * 128 + 64 + 8 * e + lane;
       ok = r < a.rows;
       return ok ? __ldg(X2 + r) : make_float2(0.f, 0.f);
     };
     auto help = [&](int i, float2 xr, bool ok) {
-      if (!kFirst || i >= nmine) return;
-      produce_rows(i, xr, ok, 64 + 8 * e, 8);
+      if (!helping || i >= nmine) return;
+      produce_rows(i, xr, ok, 64 + 8 * e, std::integral_constant<int, 8>{});
     };
     if (kFirst) {
       bool ok0, ok1;
@@ -781,21 +865,25 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       if (kFifo) stage_free_dbl(lane);
       else stage_free(lane);
       uint32_t mb[2];
+      const float2 alpha2 = make_float2(a.alpha, a.alpha);
+      const bool full_tile = (t + 1) * 128 <= a.rows;  // warp-uniform: only a ragged last tile has rows past the end
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         float v[32];
         tmem_ld32(acc + 32 * c, v);
-        uint32_t m = 0;
+        const float2* b2 = reinterpret_cast<const float2*>(sbias + cb + 32 * c);
+        uint32_t hw[16], m = 0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const float z = v[k] + sbias[cb + 32 * c + k];
-          m |= (z > 0.f ? 1u : 0u) << k;
-          v[k] = valid ? lrelu(z, a.alpha) : 0.f;
+        for (int k = 0; k < 16; ++k) {  // Z = acc + b, H = LeakyReLU(Z), pairwise
+          lrelu_split2(add2(make_float2(v[2 * k], v[2 * k + 1]), b2[k]), alpha2, hw[k], lo[16 * c + k]);
+          m |= pos_bits(hw[k], k);
         }
-        mb[c] = valid ? m : 0u;
-        uint32_t hw[16];
+        if (!full_tile && !valid) {  // rows past the end are zeros
 #pragma unroll
-        for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
+          for (int k = 0; k < 16; ++k) hw[k] = lo[16 * c + k] = 0u;
+          m = 0u;
+        }
+        mb[c] = m;
         stage_words(stgH, lane, c, hw);
       }
       tc_fence_before();
@@ -958,7 +1046,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         } else {
           mbar_wait(&emptyH[0], (i & 1) ^ 1);
         }
-        produce_h1<kSplit>(xr, ok, p0, a.alpha, hh, hl, 32 * warp, 32, lane);
+        produce_h1<kSplit, 32>(xr, ok, p0, a.alpha, hh, hl, 32 * warp, lane);
         fence_proxy_async_smem();
         if (kPR) {
           mbar_arrive(&pfull[0]);
@@ -1206,6 +1294,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       const int b = i & 1;
       const int64_t row = t * 128 + 32 * q + lane;
       const bool valid = row < a.rows;
+      const bool full_tile = (t + 1) * 128 <= a.rows;  // warp-uniform
       uint2 mk = make_uint2(0u, 0u);
       float2 x = make_float2(0.f, 0.f);
       if (kFirst) {
@@ -1241,11 +1330,18 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           float v[32];
           tmem_ld32(acc + 32 * c, v);
           const uint32_t m = c ? mk.y : mk.x;
-#pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = valid ? v[k] * (((m >> k) & 1u) ? 1.f : a.alpha) : 0.f;
           uint32_t hw[16];
 #pragma unroll
-          for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
+          for (int k = 0; k < 16; ++k) {  // G' = acc * LeakyReLU'(Z), pairwise (columns 2k, 2k + 1)
+            const float d0 = ((m >> mask_bit(2 * k)) & 1u) ? 1.f : a.alpha;
+            const float d1 = ((m >> mask_bit(2 * k + 1)) & 1u) ? 1.f : a.alpha;
+            const float2 g = mul2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(d0, d1));
+            split2(g.x, g.y, hw[k], lo[16 * c + k]);
+          }
+          if (!full_tile && !valid) {  // rows past the end are zeros
+#pragma unroll
+            for (int k = 0; k < 16; ++k) hw[k] = lo[16 * c + k] = 0u;
+          }
           stage_words(stg, lane, c, hw);
         }
         tc_fence_before();
