@@ -69,9 +69,6 @@ struct Params0 {  // layer-0 parameters, column-contiguous
   float b0[128];
 };
 
-// LeakyReLU for 0 <= a < 1 (validated, R6): max(z, a z) equals (z > 0 ? z : a z)
-// bit for bit (also for -0 and NaN) in two instructions
-__device__ __forceinline__ float lrelu(float z, float a) { return fmaxf(z, z * a); }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -133,7 +130,9 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   const float2 d = sub2(make_float2(a, b), hf);
   lo = bf16x2_rn(d.x, d.y);
 }
-// h = LeakyReLU(z) of a pair, split into hi / lo words
+// h = LeakyReLU(z) of a pair, split into hi / lo words.  LeakyReLU is
+// max(z, a z): for 0 <= a < 1 (validated, R6) it equals (z > 0 ? z : a z) bit
+// for bit (also for -0 and NaN) in two instructions.
 __device__ __forceinline__ void lrelu_split2(float2 z, float2 alpha2, uint32_t& hi, uint32_t& lo) {
   const float2 t = mul2(z, alpha2);
   split2(fmaxf(z.x, t.x), fmaxf(z.y, t.y), hi, lo);
@@ -431,7 +430,8 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sloss + 8);
   int* sTile = reinterpret_cast<int*>(tmem_slot + 4);      // [8] dynamic schedule: tile of local iteration i (i % 8)
   float* sbias = reinterpret_cast<float*>(sTile + 8);      // [128]
-  float* swh = sbias + 128;                                 // [128] (head)
+  float* swh = sbias + 128;                                 // [128] (head) w
+  float* swa = swh + 128;                                   // [128] (head) alpha * w
   Params0* p0 = reinterpret_cast<Params0*>(swh);            // (first; aliases swh and the 1 KiB after it)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -451,7 +451,10 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
   if (warp == kMmaWarp) tmem_alloc<512>(tmem_slot);
   for (int i = tid; i < 128; i += kThreads) {
     sbias[i] = a.bias[i];
-    if (kHead) swh[i] = a.w_head[i];
+    if (kHead) {
+      swh[i] = a.w_head[i];
+      swa[i] = a.alpha * a.w_head[i];
+    }
     if (kFirst) {
       p0->w0x[i] = a.W0[2 * i];
       p0->w0y[i] = a.W0[2 * i + 1];
@@ -679,10 +682,59 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
     const int q = warp & 3;
     const int h = e >> 2;
     const uint32_t stgA = smem_u32(sStg) + (2 * e) * kStg, stgB = stgA + kStg;  // hi / lo staging
-    float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // sum dz*H, columns 32c + lane
+    // sum over this CTA's tiles of dz * H at this warp's row positions,
+    // accumulated in the free TMEM columns 256 + 128 h .. (one column block
+    // per tile parity, so the two warps of a lane quarter never share one);
+    // summed over the rows once, at the end
+    const uint32_t gsum = tmem + 256u + (uint32_t)(128 * h) + ((uint32_t)(32 * q) << 16);
+    const float2 alpha2 = make_float2(a.alpha, a.alpha);
+    const float2* b2 = reinterpret_cast<const float2*>(sbias);
+    const float2* w2 = reinterpret_cast<const float2*>(swh);
+    const float2* wa2 = reinterpret_cast<const float2*>(swa);
+    if (a.want_wgrad) {
+      float zero[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) zero[k] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st32(gsum + 32 * c, zero);
+    }
     float gbacc = 0.f;
     double lacc = 0.0;
     int64_t pend = -1;
+    // pass 2 of one 64-column region: G = dz * (Z > 0 ? w : alpha w) -> planes
+    // (hi staging A, lo staging B; bf16: A / B alternate by region) and,
+    // with the head gradient, gsum += dz * H
+    auto region = [&](auto want, uint32_t acc, int rr, float dz, uint8_t* dst0) {
+      const float2 dz2 = make_float2(dz, dz);
+      const uint32_t stgH = (kSplit || rr == 0) ? stgA : stgB;
+      if (kSplit) stage_free(lane);
+      else stage_free_dbl(lane);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int c0 = 64 * rr + 32 * c;
+        float v[32], ga[32];
+        if constexpr (decltype(want)::value) tmem_ld32x2(acc + c0, gsum + c0, v, ga);
+        else tmem_ld32(acc + c0, v);
+        uint32_t hw[16], lw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), b2[c0 / 2 + k]);
+          if constexpr (decltype(want)::value) {
+            const float2 t = mul2(z, alpha2);
+            const float2 g = fma2(dz2, make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), make_float2(ga[2 * k], ga[2 * k + 1]));
+            ga[2 * k] = g.x;
+            ga[2 * k + 1] = g.y;
+          }
+          const float2 w = w2[c0 / 2 + k], wa = wa2[c0 / 2 + k];
+          const float2 G = mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y));
+          split2(G.x, G.y, hw[k], lw[k]);
+        }
+        stage_words(stgH, lane, c, hw);
+        if (kSplit) stage_words(stgB, lane, c, lw);
+        if constexpr (decltype(want)::value) tmem_st32(gsum + c0, ga);
+      }
+      return stgH;
+    };
     for (int i = h; i < nmine; i += 2) {
       const int64_t t = tile_of(i);
       const int b = i & 1;
@@ -703,16 +755,22 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       if ((e & 3) == 0 && lane == 0) trace_pt(trace, j, i, 2);  // warps 0 / 4: even / odd tiles
       tc_fence_after();
       const uint32_t acc = tmem + (uint32_t)(b * 128) + ((uint32_t)(32 * q) << 16);
-      // pass 1: z = H . w + b over all 128 columns of this lane's row
-      float dot = 0.f;
+      // pass 1: z = LeakyReLU(Z) . w + b over all 128 columns of this lane's row
+      float2 dot2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        tmem_ld32(acc + 32 * c, v);
+      for (int c = 0; c < 4; c += 2) {
+        float v[32], u[32];
+        tmem_ld32x2(acc + 32 * c, acc + 32 * (c + 1), v, u);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) dot = fmaf(lrelu(v[k] + sbias[32 * c + k], a.alpha), swh[32 * c + k], dot);
+        for (int k = 0; k < 32; ++k) {
+          const float* x = k < 16 ? v : u;
+          const int kk = k & 15, col2 = 16 * c + k;  // column pair index
+          const float2 zz = add2(make_float2(x[2 * kk], x[2 * kk + 1]), b2[col2]);
+          const float2 tt = mul2(zz, alpha2);
+          dot2 = fma2(make_float2(fmaxf(zz.x, tt.x), fmaxf(zz.y, tt.y)), w2[col2], dot2);
+        }
       }
-      const float z = dot + *a.b_head;
+      const float z = (dot2.x + dot2.y) + *a.b_head;
       const float tl = (row < a.n_real) ? 1.f : a.label_rest;
       const float dz = valid ? (sigmoid_f(z) - tl) * a.scale : 0.f;
       if (valid) {
@@ -720,49 +778,31 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
         lacc += (double)(tl * softplus_neg(z) + (1.f - tl) * softplus_neg(-z));
         gbacc += dz;
       }
-      // pass 2, per 64-column region: G = dz * w * LeakyReLU'(Z) -> planes;
-      // head gradient sum dz * H
 #pragma unroll 1
       for (int rr = 0; rr < 2; ++rr) {
-        uint32_t lo[32];
-        stage_free_dbl(lane);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int c0 = 64 * rr + 32 * c;
-          float v[32];
-          tmem_ld32(acc + c0, v);
-          float g[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const float zz = v[k] + sbias[c0 + k];
-            g[k] = dz * lrelu(zz, a.alpha);
-            v[k] = dz * swh[c0 + k] * (zz > 0.f ? 1.f : a.alpha);
-          }
-          uint32_t hw[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) split2(v[2 * k], v[2 * k + 1], hw[k], lo[16 * c + k]);
-          stage_words((kSplit || rr == 0) ? stgA : stgB, lane, c, hw);
-          if (a.want_wgrad) {
-            const float cs = colsum32(g, lane);
-            if (rr == 0) gacc[c] += cs;
-            else gacc[2 + c] += cs;
-          }
-        }
+        const uint32_t stgH = a.want_wgrad ? region(std::true_type{}, acc, rr, dz, dst0)
+                                           : region(std::false_type{}, acc, rr, dz, dst0);
         if (rr == 1) {
           tc_fence_before();
           mbar_arrive(&tempty[b]);
           if ((e & 3) == 0 && lane == 0) trace_pt(trace, j, i, 3);
         }
-        flush_stage((kSplit || rr == 0) ? stgA : stgB, dst0 + rr * 16384, lane);
-        if (kSplit) {
-          stage_free_dbl(lane);
-          stage_words(stgB, lane, 0, lo);
-          stage_words(stgB, lane, 1, lo + 16);
-          flush_stage(stgB, dst0 + rr * 16384 + kPlane, lane);
-        }
+        flush_stage(stgH, dst0 + rr * 16384, lane);
+        if (kSplit) flush_stage(stgB, dst0 + rr * 16384 + kPlane, lane);
       }
       ring_publish<2 * P>(a.out, pend, lane, 2);  // the previous tile's stores are complete (4 warps x 2)
       pend = t;
+    }
+    // this warp's head-gradient partial: the column sums over its 32 rows
+    float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // columns 32c + lane
+    if (a.want_wgrad) {
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float g[32];
+        tmem_ld32(gsum + 32 * c, g);
+        gacc[c] = colsum32(g, lane);
+      }
     }
     if (lane == 0) bulk_wait0();
     ring_publish<0>(a.out, pend, lane, 2);
