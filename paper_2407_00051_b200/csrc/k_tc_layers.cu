@@ -1287,7 +1287,8 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       // thread = channel c = 32q + lane (TMEM lane); warp half h = rows 64h..64h+63
       const int c = 32 * q + lane;
       const float w0x = __ldg(a.W0 + 2 * c), w0y = __ldg(a.W0 + 2 * c + 1), b0c = __ldg(a.b0 + c);
-      float t0 = 0.f, t1 = 0.f, tb = 0.f;  // sum over rows of g x_0, g x_1, g (fixed row order)
+      // sums over rows of g x_0, g x_1 (in row order) and of g (even / odd rows)
+      float2 T = make_float2(0.f, 0.f), TB = make_float2(0.f, 0.f);
       for (int i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1, xb = i & 1;
@@ -1297,30 +1298,42 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         tc_fence_after();
         const float2* xs = sX + xb * 128;
         const int64_t valid_rows = a.rows - t * 128;
+        // ragged last tile: rows past the end read as x = 0 (their sX bytes were not loaded)
+        auto rows = [&](auto ragged) {
 #pragma unroll 1
-        for (int ch = 0; ch < 2; ++ch) {
-          float v[32];  // G_1^T[c][rows 64h + 32ch + k] before LeakyReLU'
-          tmem_ld32(tmem + (uint32_t)(b * 128 + 64 * h + 32 * ch) + ((uint32_t)(32 * q) << 16), v);
+          for (int ch = 0; ch < 2; ++ch) {
+            float v[32];  // G_1^T[c][rows 64h + 32ch + k] before LeakyReLU'
+            tmem_ld32(tmem + (uint32_t)(b * 128 + 64 * h + 32 * ch) + ((uint32_t)(32 * q) << 16), v);
+            const float4* x4 = reinterpret_cast<const float4*>(xs + 64 * h + 32 * ch);
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const int r = 64 * h + 32 * ch + k;
-            const float2 x = (r < valid_rows) ? xs[r] : make_float2(0.f, 0.f);
-            // Z_1 recomputed exactly as the forward's producers do
-            const float z1 = fmaf(x.x, w0x, fmaf(x.y, w0y, b0c));
-            const float g = v[k] * (z1 > 0.f ? 1.f : a.alpha);
-            t0 = fmaf(g, x.x, t0);
-            t1 = fmaf(g, x.y, t1);
-            tb += g;
+            for (int k = 0; k < 32; k += 2) {  // rows r, r + 1
+              float4 xx = x4[k / 2];
+              if constexpr (decltype(ragged)::value) {
+                const int r = 64 * h + 32 * ch + k;
+                if (r >= valid_rows) xx.x = xx.y = 0.f;
+                if (r + 1 >= valid_rows) xx.z = xx.w = 0.f;
+              }
+              // Z_1 recomputed exactly as the forward's producers do
+              const float za = fmaf(xx.x, w0x, fmaf(xx.y, w0y, b0c));
+              const float zb = fmaf(xx.z, w0x, fmaf(xx.w, w0y, b0c));
+              const float2 g = mul2(make_float2(v[k], v[k + 1]),
+                                    make_float2(za > 0.f ? 1.f : a.alpha, zb > 0.f ? 1.f : a.alpha));
+              T = fma2(make_float2(g.x, g.x), make_float2(xx.x, xx.y), T);
+              T = fma2(make_float2(g.y, g.y), make_float2(xx.z, xx.w), T);
+              TB = add2(g, TB);
+            }
           }
-        }
+        };
+        if (valid_rows >= 128) rows(std::false_type{});
+        else rows(std::true_type{});
         tc_fence_before();
         mbar_arrive(&tempty[b]);
         mbar_arrive(&xempty[xb]);
         if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
       }
-      s0[0] = t0;
-      s1[0] = t1;
-      sb[0] = tb;
+      s0[0] = T.x;
+      s1[0] = T.y;
+      sb[0] = TB.x + TB.y;
     }
     for (int i = 0; !kT && (dyn || i < nmine); ++i) {
       int64_t t;
