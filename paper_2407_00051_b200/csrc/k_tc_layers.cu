@@ -1414,25 +1414,39 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         ring_publish<P>(a.gout, pend, lane);
         pend = t;
       } else {
-        // G_1 = acc * LeakyReLU'(Z_1), Z_1 = x W_0^T + b_0 recomputed exactly as the producers do
-        float d0 = 0.f, d1 = 0.f;
+        // G_1 = acc * LeakyReLU'(Z_1), Z_1 = x W_0^T + b_0 recomputed exactly as
+        // the producers do (pairwise FFMA2 = fmaf per lane).  Rows past the
+        // end need no mask: their accumulator rows are exactly 0 (G_2 rows
+        // are zero there) and x = 0.
+        float2 D0 = make_float2(0.f, 0.f), D1 = make_float2(0.f, 0.f);  // dy partial dots (column pairs)
+        const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           float v[32];
           tmem_ld32(acc + 32 * c, v);
-          const float vmul = valid ? 1.f : 0.f;
 #pragma unroll
           for (int k = 0; k < 32; k += 4) {  // layer-0 parameters as float4 (broadcast) loads
             const int cc = cb + 32 * c + k;
             const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[cc]);
             const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[cc]);
             const float4 bb = *reinterpret_cast<const float4*>(&p0->b0[cc]);
-            const float z0 = fmaf(x.x, wx.x, fmaf(x.y, wy.x, bb.x)), z1 = fmaf(x.x, wx.y, fmaf(x.y, wy.y, bb.y));
-            const float z2 = fmaf(x.x, wx.z, fmaf(x.y, wy.z, bb.z)), z3 = fmaf(x.x, wx.w, fmaf(x.y, wy.w, bb.w));
-            v[k] *= vmul * (z0 > 0.f ? 1.f : a.alpha);
-            v[k + 1] *= vmul * (z1 > 0.f ? 1.f : a.alpha);
-            v[k + 2] *= vmul * (z2 > 0.f ? 1.f : a.alpha);
-            v[k + 3] *= vmul * (z3 > 0.f ? 1.f : a.alpha);
+            const float2 wxa = make_float2(wx.x, wx.y), wxb = make_float2(wx.z, wx.w);
+            const float2 wya = make_float2(wy.x, wy.y), wyb = make_float2(wy.z, wy.w);
+            const float2 za = fma2(X0, wxa, fma2(X1, wya, make_float2(bb.x, bb.y)));
+            const float2 zb = fma2(X0, wxb, fma2(X1, wyb, make_float2(bb.z, bb.w)));
+            const float2 ga = mul2(make_float2(v[k], v[k + 1]),
+                                   make_float2(za.x > 0.f ? 1.f : a.alpha, za.y > 0.f ? 1.f : a.alpha));
+            const float2 gb = mul2(make_float2(v[k + 2], v[k + 3]),
+                                   make_float2(zb.x > 0.f ? 1.f : a.alpha, zb.y > 0.f ? 1.f : a.alpha));
+            if (kWgrad) {
+              v[k] = ga.x;
+              v[k + 1] = ga.y;
+              v[k + 2] = gb.x;
+              v[k + 3] = gb.y;
+            } else {
+              D0 = fma2(gb, wxb, fma2(ga, wxa, D0));
+              D1 = fma2(gb, wyb, fma2(ga, wya, D1));
+            }
           }
           if (kWgrad) {
             float g[32];
@@ -1443,17 +1457,9 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
             for (int k = 0; k < 32; ++k) g[k] = v[k] * x.y;
             s1[c] += colsum32(g, lane);
             sb[c] += colsum32(v, lane);
-          } else {
-#pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const int cc = cb + 32 * c + k;
-              const float4 wx = *reinterpret_cast<const float4*>(&p0->w0x[cc]);
-              const float4 wy = *reinterpret_cast<const float4*>(&p0->w0y[cc]);
-              d0 = fmaf(v[k + 3], wx.w, fmaf(v[k + 2], wx.z, fmaf(v[k + 1], wx.y, fmaf(v[k], wx.x, d0))));
-              d1 = fmaf(v[k + 3], wy.w, fmaf(v[k + 2], wy.z, fmaf(v[k + 1], wy.y, fmaf(v[k], wy.x, d1))));
-            }
           }
         }
+        const float d0 = D0.x + D0.y, d1 = D1.x + D1.y;
         tc_fence_before();
         mbar_arrive(&tempty[b]);
         if (e == 0 && lane == 0) trace_pt(trace, j, i, 3);
