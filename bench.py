@@ -195,7 +195,8 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     each launch).  Algorithmic bytes / FLOPs per row of each layer pass
     (DESIGN.md §7): plane tiles are E = 128 x 4 B per row (bf16 hi + lo) or
     128 x 2 B (PREC_BF16, hi only); the wgrad reads only the hi plane of H
-    (E/2, R28) and the first forward pass stores the H_1 hi plane for it;
+    (E/2, R28); the layer-1 backward recomputes H_1 from X (with
+    SAGIPS_H1_STORE=1 the first forward pass stores its hi plane instead);
     masks 16 B/row; X 8 B/row.  Useful FLOPs: 2*128*128 per row per GEMM
     (forward, dgrad, wgrad); executed tensor FLOPs count the split products
     (bf16x3 forward / dgrad, bf16x2 wgrad; 1 for PREC_BF16)."""
@@ -206,7 +207,8 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     px, pw = (3, 2) if split else (1, 1)   # products per fwd/dgrad GEMM, per wgrad GEMM
     rows_d, rows_g = 2 * N, N
     mids = max(0, cfg.disc_depth - 3)
-    h1 = Eh if split else 0                # H_1 hi plane stored by the first forward pass (split)
+    # H_1 hi plane stored by the first forward pass and read back (split, SAGIPS_H1_STORE=1)
+    h1 = Eh if (split and os.environ.get("SAGIPS_H1_STORE") == "1") else 0
     spec = {  # class: (rows, bytes/row, useful flops/row, executed flops/row, launches)
         "d_fwd_first": (rows_d, 8 + E + 16 + h1, G, px * G, 1),
         "d_fwd_mid": (rows_d, 2 * E + 16, G, px * G, mids),

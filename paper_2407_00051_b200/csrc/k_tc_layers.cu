@@ -235,18 +235,41 @@ __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint3
 // lane i's prefetched input row row0 + i (i < kRows).  Z_1 = fma(x0, w0x,
 // fma(x1, w0y, b0)) per channel, the order the backward recomputes it in.
 // Rows past the end (ragged last tile) are written as zeros.
+// Layer-0 parameters of lane l's channels 8(l % 16) .. + 7 as pairs, from the
+// shared-memory copy or from global memory (W_0 [128][2], b_0 [128])
+struct W0Lane {
+  float2 wx[4], wy[4], bb[4];
+};
+__device__ __forceinline__ W0Lane w0_lane(const Params0* p0, int l) {
+  const int jc = l & 15;
+  W0Lane w;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    w.wx[p] = *reinterpret_cast<const float2*>(&p0->w0x[8 * jc + 2 * p]);
+    w.wy[p] = *reinterpret_cast<const float2*>(&p0->w0y[8 * jc + 2 * p]);
+    w.bb[p] = *reinterpret_cast<const float2*>(&p0->b0[8 * jc + 2 * p]);
+  }
+  return w;
+}
+__device__ __forceinline__ W0Lane w0_lane(const float* __restrict__ W0, const float* __restrict__ b0, int l) {
+  const int jc = l & 15;
+  W0Lane w;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(W0 + 2 * (8 * jc + 2 * p)));  // (x, y) of 2 channels
+    w.wx[p] = make_float2(q.x, q.z);
+    w.wy[p] = make_float2(q.y, q.w);
+    w.bb[p] = __ldg(reinterpret_cast<const float2*>(b0 + 8 * jc + 2 * p));
+  }
+  return w;
+}
+
 template <bool kSplit, int kRows>
-__device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const Params0* p0, float alpha, uint32_t hi,
+__device__ __forceinline__ void produce_h1(float2 xr, bool xvalid, const W0Lane& w, float alpha, uint32_t hi,
                                            uint32_t lo, int row0, int l) {
   static_assert(kRows % 8 == 0 && kRows <= 32, "rows");
   const int jc = l & 15, par = l >> 4;
-  float2 wx[4], wy[4], bb[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    wx[p] = *reinterpret_cast<const float2*>(&p0->w0x[8 * jc + 2 * p]);
-    wy[p] = *reinterpret_cast<const float2*>(&p0->w0y[8 * jc + 2 * p]);
-    bb[p] = *reinterpret_cast<const float2*>(&p0->b0[8 * jc + 2 * p]);
-  }
+  const float2 *wx = w.wx, *wy = w.wy, *bb = w.bb;
   const float2 alpha2 = make_float2(alpha, alpha);
   constexpr unsigned kNeed = kRows == 32 ? 0xffffffffu : ((1u << kRows) - 1u);
   const unsigned vbits = __ballot_sync(0xffffffffu, xvalid) & kNeed;
@@ -488,7 +511,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       if (kSplit) mbar_wait(&empty[sl], (use_lo(i) & 1) ^ 1);
       mbar_wait(&empty[sh], (use_hi(i) & 1) ^ 1);
       const uint32_t base = smem_u32(sA);
-      produce_h1<kSplit, kRows>(xr, ok, p0, a.alpha, base + sh * kPlane, base + sl * kPlane, row0, lane);
+      produce_h1<kSplit, kRows>(xr, ok, w0_lane(p0, lane), a.alpha, base + sh * kPlane, base + sl * kPlane, row0, lane);
       fence_proxy_async_smem();
       if (kSplit) mbar_arrive(&full[sl]);
       mbar_arrive(&full[sh]);
@@ -496,7 +519,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       const int s = i & 1;
       mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
       const uint32_t st = smem_u32(sA + s * TB);
-      produce_h1<kSplit, kRows>(xr, ok, p0, a.alpha, st, st + kPlane, row0, lane);
+      produce_h1<kSplit, kRows>(xr, ok, w0_lane(p0, lane), a.alpha, st, st + kPlane, row0, lane);
       fence_proxy_async_smem();
       mbar_arrive(&full[s]);
     }
@@ -968,10 +991,9 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   // with their own barriers, so the next tile's planes load while this
   // tile's MMAs run (see the MMA issuer for the order)
   constexpr bool kLoadH = kWgrad && (!kFirst || kH1Load);  // H planes come from global memory
-  // the plane ring only where H is loaded: with SIMT-produced H_1 planes the
-  // whole-tile H stage (released right after the wgrad MMAs) overlaps better
-  constexpr bool kPR = kSplit && kLoadH;
-  constexpr bool kFifoG = false;                            // (plane slots: H_1 fixed, G FIFO)
+  // (split wgrad passes; the layer-1 H_1 hi plane is either bulk-loaded,
+  // kH1Load, or recomputed from X by the SIMT producers into its plane slot)
+  constexpr bool kPR = kSplit && kWgrad;
   // kT (D step, first layer, plane ring): the dgrad computes G_1^T (A = W_1
   // MN-major, B = G_2 K-major), so TMEM lane = channel c and column = row:
   // dW_0 = G_1^T X and db_0 accumulate per thread over rows (no shuffles),
@@ -1019,7 +1041,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       mbar_init(&xempty[k], 32 * kEW);
     }
     for (int k = 0; k < 5; ++k) {
-      mbar_init(&pfull[k], (kFifoG && k < 2) ? 32 * kPW : 1);  // H_1 planes in slots 0, 1 (producers)
+      mbar_init(&pfull[k], 1);
       mbar_init(&pempty[k], 1);
     }
     fence_barrier_init();
@@ -1075,23 +1097,24 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       };
       bool ok;
       float2 xr = load_x(0, ok);
-      const uint32_t hh = kPR ? pl_addr(0) : smem_u32(sH);
-      const uint32_t hl = kPR ? pl_addr(1) : smem_u32(sH) + kPlane;
+      // kT: sX overlays the shared Params0, so W_0 comes from global memory
+      const W0Lane w0 = kT ? w0_lane(a.W0, a.b0, lane) : w0_lane(p0, lane);
       for (int i = 0; i < nmine; ++i) {
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
         if (kPR) {
-          mbar_wait(&pempty[0], (i & 1) ^ 1);
-          mbar_wait(&pempty[1], (i & 1) ^ 1);
+          // the H_1 hi plane (all the wgrad reads, R28) into its FIFO slot;
+          // the 4 producer warps meet at a named barrier, one thread arrives
+          const PS ph = pl_hh(i);
+          mbar_wait(&pempty[ph.slot], (ph.use & 1) ^ 1);
+          produce_h1<false, 32>(xr, ok, w0, a.alpha, pl_addr(ph.slot), 0u, 32 * warp, lane);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+          if (warp == 0 && lane == 0) mbar_arrive(&pfull[ph.slot]);
         } else {
           mbar_wait(&emptyH[0], (i & 1) ^ 1);
-        }
-        produce_h1<kSplit, 32>(xr, ok, p0, a.alpha, hh, hl, 32 * warp, lane);
-        fence_proxy_async_smem();
-        if (kPR) {
-          mbar_arrive(&pfull[0]);
-          mbar_arrive(&pfull[1]);
-        } else {
+          produce_h1<kSplit, 32>(xr, ok, w0, a.alpha, smem_u32(sH), smem_u32(sH) + kPlane, 32 * warp, lane);
+          fence_proxy_async_smem();
           mbar_arrive(&fullH[0]);
         }
         xr = xn;
@@ -1121,9 +1144,11 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         }
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
-        const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
-        ring_wait_ready(a.h, t, wa);
-        load(pl_hh(i), hsrc);
+        if (kLoadH) {  // (else the producers write it)
+          const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
+          ring_wait_ready(a.h, t, wa);
+          load(pl_hh(i), hsrc);
+        }
         load(pl_gl(i), gsrc + kPlane);
         trace_pt(trace, j, i, 0);
       }
@@ -1182,7 +1207,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         const uint32_t agh = pl_addr(gh.slot), ahh = pl_addr(ph.slot), agl = pl_addr(gl.slot);
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
-        ring_consumed(a.h, t);  // the H plane has been read
+        if (kLoadH) ring_consumed(a.h, t);  // the H plane has been read
         trace_pt(trace, j, i, 1);
         tc_fence_after();
 #pragma unroll

@@ -422,6 +422,18 @@ static int first_help() {
   return v;
 }
 
+// SAGIPS_H1_STORE=1: the D forward's first layer stores the H_1 hi plane and
+// the layer-1 backward bulk-loads it; default: the backward's producer warps
+// recompute it from X (512 B/row less HBM traffic)
+static bool h1_store() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAGIPS_H1_STORE");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
   const int kc = want_grads ? 0 : 6;  // kernel-timing classes
@@ -432,7 +444,7 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
   f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0]; f.first_help = first_help();
   f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.out = whole(c->dAct[1], c->dMask[1]);
   f.rows = rows; f.alpha = c->cfg.leaky_slope;
-  if (want_grads && split) f.h1 = whole(c->dAct[0]);  // H_1 planes for the layer-1 wgrad (one bulk store per tile)
+  if (want_grads && split && h1_store()) f.h1 = whole(c->dAct[0]);  // H_1 hi plane for the layer-1 wgrad
   kernel_begin(c, kc + 0, st);
   launch_tc_fwd(split, FWD_FIRST, f, st);
   kernel_end(c, st);
@@ -506,7 +518,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     nparts[l] = grid;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
-      if (split) b.h = whole(c->dAct[0]);  // H_1 planes stored by the forward first layer
+      if (split && h1_store()) b.h = whole(c->dAct[0]);  // H_1 hi plane stored by the forward first layer
     } else {
       b.h = whole(c->dAct[l - 1], c->dMask[l - 1]);
       b.gout = whole(c->dZb[cur ^ 1]);

@@ -1,7 +1,8 @@
 """Executed-instruction mix of one kernel launch in an ncu report: per SASS
 opcode and per CUDA source line (ncu --page source, cuda+sass view; the page
 has one section per (function, source file), repeated per launch).
-usage: ncu_mix.py REPORT FUNCTION-REGEX [launch-index] [top]"""
+usage: ncu_mix.py REPORT FUNCTION-REGEX [launch-index] [top] [--stalls]
+(--stalls: source lines by warp-stall samples with their top reasons)"""
 import collections
 import csv
 import re
@@ -61,6 +62,21 @@ def main(rep, fre, launch=0, top=30):
     lines.sort(reverse=True)
     for n, l, s in lines[:top]:
         print(f"{n / 1e6:8.2f}M {l:>22s} {s}")
+    if "--stalls" in sys.argv:
+        ks = hdr.index("Warp Stall Sampling (All Samples)")
+        sc = [(i, c[6:]) for i, c in enumerate(hdr) if c.startswith("stall_") and "(Not Issued)" not in c]
+        st = []
+        for k in keys:
+            for path, r in sections[k]:
+                if r[0] not in ("-", ""):
+                    v = num(r[ks])
+                    why = sorted(((num(r[i]), c) for i, c in sc), reverse=True)[:3]
+                    st.append((v, path.split("/")[-1] + ":" + r[0], r[1].strip()[:60], why))
+        tot_s = sum(x[0] for x in st) or 1
+        st.sort(key=lambda x: -x[0])
+        print("--- stall samples by line")
+        for v, l, s, why in st[:top]:
+            print(f"{100 * v / tot_s:5.1f}% {l:>22s} {s:60s} " + " ".join(f"{c}:{100 * x / max(v, 1):.0f}%" for x, c in why if x > 0))
 
 
 if __name__ == "__main__":
