@@ -253,6 +253,18 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
                  "frac": roof["achieved"] / roof["peak"], "traffic": None, "ms_per_launch": d["ms"] / d["launches_per_step"],
                  "floors_ms": {"hbm": d["t_hbm_ms"], "tensor": d["t_tensor_ms"]},
                  "timing": "CUDA events on the step stream around each launch, mean over the timed steps"})
+    # measured DRAM bytes per launch of this kernel class from the committed
+    # ncu --set full capture of the same workload (tests/tools/ncu_traffic.py)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            tr = json.load(f)
+        c = tr["classes"].get(dom)
+        if c and tr.get("rows_d") == rows_d and tr.get("split") == split:
+            roof["traffic"] = c["traffic_bytes"]
+            roof["traffic_algorithmic"] = spec[dom][0] * spec[dom][1]
+            roof["traffic_src"] = "profiles/r01_ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, B/launch)"
+    except (OSError, ValueError, KeyError):
+        pass
     # whole discriminator MLP (a7 + a8) on the tensor cores
     tot_ms = sum(v["ms"] for v in out.values())
     tot_fl = sum(v["flops"] for v in out.values())

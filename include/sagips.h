@@ -276,8 +276,11 @@ SAGIPS_API sagips_status sagips_timing_reset(sagips_ctx* ctx);
  * first step, the tensor-core layer kernels record globaltimer stamps per
  * tile (CTAs 0-3, first 32 launches): [launch][cta][tile][4] uint64 =
  * producer done, MMA start, epilogue start, epilogue done, followed by
- * [launch][256 CTAs][4] uint64 per-CTA (start, end, -, -) stamps.  Copies and
- * rearms the buffer; `bytes` must equal the size returned for host == NULL.
+ * [launch][256 CTAs][12] uint64 per-CTA records: start and end stamps (0, 1)
+ * and, for the per-layer kernels, summed wait times in ns (4 + k: k = 1
+ * loader slot, 2 MMA operands, 3 MMA accumulator, 4 producers' slot, 5
+ * epilogue accumulator, 6 mask flag, 7 epilogue X rows).  Copies and rearms
+ * the buffer; `bytes` must equal the size returned for host == NULL.
  * [sync] */
 SAGIPS_API sagips_status sagips_debug_trace(void* host, size_t* bytes);
 

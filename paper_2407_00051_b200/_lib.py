@@ -247,11 +247,12 @@ class Context:
 def debug_trace(with_ctas=False):
     """Timeline stamps of the tensor-core layer kernels (SAGIPS_TRACE=1):
     uint64 array [32 launches][4 CTAs][256 tiles][4]; with_ctas: also the
-    per-CTA [32 launches][256 CTAs][4] (start, end) stamps."""
+    per-CTA [32 launches][256 CTAs][12] records: (start, end) stamps in
+    0, 1 and summed wait times (ns) per role in 4 + k (include/sagips.h)."""
     n = ctypes.c_size_t()
     _check(lib.sagips_debug_trace(None, ctypes.byref(n)))
     out = np.zeros(n.value // 8, dtype=np.uint64)
     _check(lib.sagips_debug_trace(out.ctypes.data, ctypes.byref(n)))
     k = 32 * 4 * 256 * 4
     tiles = out[:k].reshape(32, 4, 256, 4)
-    return (tiles, out[k:].reshape(32, -1, 4)) if with_ctas else tiles
+    return (tiles, out[k:].reshape(32, -1, 12)) if with_ctas else tiles

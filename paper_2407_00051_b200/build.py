@@ -44,6 +44,8 @@ def build(force=False, verbose=True):
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
              "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
              "-I", inc, "-I", os.path.join(ROOT, "include")]
+    if os.environ.get("SAGIPS_BUILD_WAITS") == "1":  # diagnostic build: per-role wait accounting (trace mode)
+        flags.append("-DSAGIPS_WAIT_ACCT")
     procs = []
     for s in srcs:
         o = os.path.join(HERE, "build", os.path.basename(s) + ".o")

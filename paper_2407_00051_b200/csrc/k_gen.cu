@@ -20,6 +20,8 @@ namespace {
 constexpr int kR = 8;         // rows per CTA (forward / dgrad)
 constexpr int kGenMaxW = 128; // widest layer these kernels handle
 constexpr int kGenThreads = 256;
+static_assert(kR == 8 && kGenThreads == 2 * kGenMaxW, "the 128 x 128 fast paths map 256 threads to 2 x 4 rows");
+constexpr int kGenSplits = 8;  // wgrad: row splits (one partial each, reduced in a fixed order)
 
 __device__ __forceinline__ float lrelu_g(float z, float a) { return z > 0.f ? z : z * a; }
 }  // namespace
@@ -41,16 +43,25 @@ struct GenArgs {
   // wgrad tiles: tile_base[l] = first blockIdx of layer l; tiles_i[l] = in-tiles per out-tile row
   int tile_base[kMaxLayers + 1];
   int tiles_i[kMaxLayers];
+  // wgrad row splits (blockIdx.y): rows [y * split_rows, (y + 1) * split_rows);
+  // with more than one, split y writes part + y * (wtot + btot) (dW then db, packet offsets)
+  int split_rows;
+  float* part;
+  int64_t wtot, btot;
 };
 
 // ---------------------------------------------------------------- forward
-// Each layer's W is staged in shared memory with rows padded to in + 1 floats
-// (lanes = consecutive outputs read conflict-free), then thread (r, o)
-// accumulates its dot product in input order.
+// Each layer's W is staged in shared memory, then each output accumulates its
+// dot product in input order.  128 x 128 layers (the hidden ones): W staged
+// with float4 loads all in flight (rows padded to 132 floats), thread (rb, o)
+// computes output o of rows rb, rb + 2, rb + 4, rb + 6 from float4 reads of W
+// and of the (broadcast) rows.  Other shapes: thread per (row, output), W rows
+// padded to in + 1.
+constexpr int kLdFast = kGenMaxW + 4;
 __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__ GenArgs a) {
-  extern __shared__ float gsm[];
+  extern __shared__ __align__(16) float gsm[];
   float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
-  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][in + 1]
+  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][ld]
   const int tid = threadIdx.x;
   const int r0 = blockIdx.x * kR;
   const int in0 = a.sizes[0];
@@ -59,20 +70,29 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
     buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
   }
   for (int l = 0; l < a.L; ++l) {
-    const int in = a.sizes[l], out = a.sizes[l + 1], ld = in + 1;
+    const int in = a.sizes[l], out = a.sizes[l + 1];
+    const bool fast = in == kGenMaxW && out == kGenMaxW;
+    const int ld = fast ? kLdFast : in + 1;
     const float* W = a.W + a.w_off[l];
     const float* bias = a.B + a.b_off[l];
     __syncthreads();  // previous layer done with Ws / buf
-    for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[(idx / in) * ld + idx % in] = __ldg(W + idx);
+    if (fast) {
+      float4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = tid + u * kGenThreads;  // float4 index: row idx / 32, columns 4 (idx % 32) ..
+        *reinterpret_cast<float4*>(Ws + (idx >> 5) * kLdFast + 4 * (idx & 31)) = v[u];
+      }
+    } else {
+      for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[(idx / in) * ld + idx % in] = __ldg(W + idx);
+    }
     __syncthreads();
     const float(*src)[kGenMaxW] = buf[l & 1];
     float(*dst)[kGenMaxW] = buf[(l + 1) & 1];
     const bool hidden = l < a.L - 1;
-    for (int idx = tid; idx < kR * out; idx += kGenThreads) {
-      const int r = idx / out, o = idx % out;
-      const float* w = Ws + o * ld;
-      float acc = 0.f;
-      for (int i = 0; i < in; ++i) acc = fmaf(src[r][i], w[i], acc);
+    auto finish = [&](int r, int o, float acc) {
       acc += __ldg(bias + o);
       if (hidden) acc = lrelu_g(acc, a.alpha);
       dst[r][o] = acc;
@@ -83,15 +103,41 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
           a.cbuf[(int64_t)(r0 + r) * out + o] = (j == 0) ? acc : softplus_f(acc);
         }
       }
+    };
+    if (fast) {
+      const int o = tid & (kGenMaxW - 1), rb = tid >> 7;
+      const float* w = Ws + o * kLdFast;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int i = 0; i < kGenMaxW; i += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(w + i);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 2 * u][i]);
+          acc[u] = fmaf(x.w, w4.w, fmaf(x.z, w4.z, fmaf(x.y, w4.y, fmaf(x.x, w4.x, acc[u]))));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) finish(rb + 2 * u, o, acc[u]);
+    } else {
+      for (int idx = tid; idx < kR * out; idx += kGenThreads) {
+        const int r = idx / out, o = idx % out;
+        const float* w = Ws + o * ld;
+        float acc = 0.f;
+        for (int i = 0; i < in; ++i) acc = fmaf(src[r][i], w[i], acc);
+        finish(r, o, acc);
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- dgrad chain
 // W_l staged in shared memory (lanes = consecutive inputs i read W[o][i]
-// conflict-free), then thread (r, i) accumulates over o in order.
+// conflict-free), then each input accumulates over o in order; 128 x 128
+// layers: thread (rb, i) does rows rb, rb + 2, rb + 4, rb + 6 with float4
+// (broadcast) reads of the rows.
 __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant__ GenArgs a) {
-  extern __shared__ float gsm[];
+  extern __shared__ __align__(16) float gsm[];
   float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
   float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][in]
   const int tid = threadIdx.x;
@@ -104,30 +150,65 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
   }
   for (int l = last; l >= 1; --l) {
     const int in = a.sizes[l], out = a.sizes[l + 1];
+    const bool fast = in == kGenMaxW && out == kGenMaxW;
     const float* W = a.W + a.w_off[l];
     __syncthreads();  // previous layer done with Ws / buf
-    for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[idx] = __ldg(W + idx);
+    if (fast) {
+      float4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) reinterpret_cast<float4*>(Ws)[tid + u * kGenThreads] = v[u];
+    } else {
+      for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[idx] = __ldg(W + idx);
+    }
     __syncthreads();
     const float(*src)[kGenMaxW] = buf[l & 1];
     float(*dst)[kGenMaxW] = buf[(l - 1) & 1];
-    for (int idx = tid; idx < kR * in; idx += kGenThreads) {
-      const int r = idx / in, i = idx % in;
-      float acc = 0.f;
-      for (int o = 0; o < out; ++o) acc = fmaf(src[r][o], Ws[o * in + i], acc);
-      float h = 0.f;
-      if (r0 + r < a.k) h = a.act[l - 1][(int64_t)(r0 + r) * in + i];
+    auto finish = [&](int r, int i, float acc, float h) {
       acc *= (h > 0.f) ? 1.f : a.alpha;  // LeakyReLU'(Z) from the sign of H (R6)
       if (r0 + r >= a.k) acc = 0.f;
       dst[r][i] = acc;
       if (r0 + r < a.k) a.dz[l - 1][(int64_t)(r0 + r) * in + i] = acc;
+    };
+    if (fast) {
+      const int i = tid & (kGenMaxW - 1), rb = tid >> 7;
+      float h[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {  // in flight during the sums
+        const int r = rb + 2 * u;
+        h[u] = (r0 + r < a.k) ? a.act[l - 1][(int64_t)(r0 + r) * in + i] : 0.f;
+      }
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int o = 0; o < kGenMaxW; o += 4) {
+        const float w0 = Ws[o * kGenMaxW + i], w1 = Ws[(o + 1) * kGenMaxW + i];
+        const float w2 = Ws[(o + 2) * kGenMaxW + i], w3 = Ws[(o + 3) * kGenMaxW + i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 2 * u][o]);
+          acc[u] = fmaf(x.w, w3, fmaf(x.z, w2, fmaf(x.y, w1, fmaf(x.x, w0, acc[u]))));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) finish(rb + 2 * u, i, acc[u], h[u]);
+    } else {
+      for (int idx = tid; idx < kR * in; idx += kGenThreads) {
+        const int r = idx / in, i = idx % in;
+        float acc = 0.f;
+        for (int o = 0; o < out; ++o) acc = fmaf(src[r][o], Ws[o * in + i], acc);
+        const float h = (r0 + r < a.k) ? a.act[l - 1][(int64_t)(r0 + r) * in + i] : 0.f;
+        finish(r, i, acc, h);
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- wgrad
-// blockIdx -> (layer l, out tile ob, in tile ib); thread (ty, tx) of 16 x 16
-// owns outputs (32ob + 2ty + {0,1}, 32ib + 2tx + {0,1}); rows in chunks of
-// 32, the next chunk's loads in flight (registers) while this one is summed.
+// blockIdx.x -> (layer l, out tile ob, in tile ib), blockIdx.y -> row split;
+// thread (ty, tx) of 16 x 16 owns outputs (32ob + 2ty + {0,1}, 32ib + 2tx +
+// {0,1}); the split's rows in chunks of 32, the next chunk's loads in flight
+// (registers) while this one is summed.
 __global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant__ GenArgs a) {
   __shared__ float sA[2][32][33];
   __shared__ float sB[2][32][33];
@@ -142,14 +223,15 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant
   float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
   float dbacc = 0.f;
   float ra[4], rb[4];
+  const int rs = blockIdx.y * a.split_rows, re = min(a.k, rs + a.split_rows);
   auto load = [&](int rc) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int idx = tid + u * kGenThreads;
       const int rr = idx >> 5, cc = idx & 31;
       const int r = rc + rr, o = 32 * ob + cc, i = 32 * ib + cc;
-      ra[u] = (r < a.k && o < out) ? __ldg(dZ + (int64_t)r * out + o) : 0.f;
-      rb[u] = (r < a.k && i < in) ? __ldg(H + (int64_t)r * in + i) : 0.f;
+      ra[u] = (r < re && o < out) ? __ldg(dZ + (int64_t)r * out + o) : 0.f;
+      rb[u] = (r < re && i < in) ? __ldg(H + (int64_t)r * in + i) : 0.f;
     }
   };
   auto stash = [&](int s) {
@@ -160,12 +242,12 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant
       sB[s][idx >> 5][idx & 31] = rb[u];
     }
   };
-  load(0);
+  load(rs);
   stash(0);
   __syncthreads();
   int s = 0;
-  for (int rc = 0; rc < a.k; rc += 32) {
-    const bool more = rc + 32 < a.k;
+  for (int rc = rs; rc < re; rc += 32) {
+    const bool more = rc + 32 < re;
     if (more) load(rc + 32);
 #pragma unroll 8
     for (int rr = 0; rr < 32; ++rr) {
@@ -184,7 +266,10 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant
     __syncthreads();
     s ^= 1;
   }
-  float* dW = a.dW + a.w_off[l];
+  const bool split = gridDim.y > 1;
+  float* pbase = a.part + (int64_t)blockIdx.y * (a.wtot + a.btot);
+  float* dW = (split ? pbase : a.dW) + a.w_off[l];
+  float* dB = split ? pbase + a.wtot : a.dB;
 #pragma unroll
   for (int u = 0; u < 2; ++u)
 #pragma unroll
@@ -192,7 +277,19 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_wgrad(const __grid_constant
       const int o = 32 * ob + 2 * ty + u, i = 32 * ib + 2 * tx + v;
       if (o < out && i < in) dW[(int64_t)o * in + i] = acc[u][v];
     }
-  if (ib == 0 && tid < 32 && 32 * ob + tid < out) a.dB[a.b_off[l] + 32 * ob + tid] = dbacc;
+  if (ib == 0 && tid < 32 && 32 * ob + tid < out) dB[a.b_off[l] + 32 * ob + tid] = dbacc;
+}
+
+// dW / db = sum over the row splits in split order
+__global__ void __launch_bounds__(256) k_gen_wgrad_reduce(const float* __restrict__ part, int splits, int64_t wtot,
+                                                          int64_t btot, float* __restrict__ dW, float* __restrict__ dB) {
+  const int64_t n = wtot + btot;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int y = 0; y < splits; ++y) v += part[(int64_t)y * n + e];
+    if (e < wtot) dW[e] = v;
+    else dB[e - wtot] = v;
+  }
 }
 
 // ---------------------------------------------------------------- host
@@ -227,10 +324,17 @@ static GenArgs gen_args(sagips_ctx* c) {
   a.dB = c->g_dB;
   a.k = c->cfg.param_samples;
   a.alpha = c->cfg.leaky_slope;
+  a.wtot = G.nw;
+  a.btot = G.nb;
+  // row splits of 32-row multiples while the partials fit the scratch
+  int splits = kGenSplits;
+  while (splits > 1 && (int64_t)splits * (a.wtot + a.btot) > c->part_floats) splits >>= 1;
+  a.split_rows = ((a.k + splits - 1) / splits + 31) / 32 * 32;
+  a.part = c->part;
   return a;
 }
 
-static size_t gen_fwd_smem() { return sizeof(float) * (2 * kR * kGenMaxW + kGenMaxW * (kGenMaxW + 1)); }
+static size_t gen_fwd_smem() { return sizeof(float) * (2 * kR * kGenMaxW + kGenMaxW * kLdFast); }
 
 void launch_gen_fwd(sagips_ctx* c, cudaStream_t st) {
   static bool configured = false;
@@ -252,8 +356,15 @@ void launch_gen_bwd(sagips_ctx* c, cudaStream_t st) {
   const GenArgs a = gen_args(c);
   k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
   count_launch();
-  k_gen_wgrad<<<a.tile_base[a.L], kGenThreads, 0, st>>>(a);
+  const int splits = (a.k + a.split_rows - 1) / a.split_rows;
+  k_gen_wgrad<<<dim3(a.tile_base[a.L], splits), kGenThreads, 0, st>>>(a);
   count_launch();
+  if (splits > 1) {
+    const int64_t n = a.wtot + a.btot;
+    k_gen_wgrad_reduce<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(a.part, splits, a.wtot,
+                                                                                          a.btot, a.dW, a.dB);
+    count_launch();
+  }
 }
 
 }  // namespace sagips

@@ -517,7 +517,7 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
       mbar_arrive(&full[sh]);
     } else {
       const int s = i & 1;
-      mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1);
+      SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&empty[s], ((i >> 1) & 1) ^ 1));
       const uint32_t st = smem_u32(sA + s * TB);
       produce_h1<kSplit, kRows>(xr, ok, w0_lane(p0, lane), a.alpha, st, st + kPlane, row0, lane);
       fence_proxy_async_smem();
@@ -1078,10 +1078,13 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   struct PS {
     int slot, use;
   };
-  auto pl_of = [&](int i, int k) -> PS { return PS{(3 * i + k) % 4, (3 * i + k) / 4}; };
+  // kT: planes Gh, Gl, Hh over 5 slots (its staging area is the 5th; every
+  // plane is held until the end of its tile's MMAs, see the MMA issuer)
+  constexpr int kSlots = kT ? 5 : 4;
+  auto pl_of = [&](int i, int k) -> PS { return PS{(3 * i + k) % kSlots, (3 * i + k) / kSlots}; };
   auto pl_gh = [&](int i) -> PS { return pl_of(i, 0); };
-  auto pl_hh = [&](int i) -> PS { return pl_of(i, 1); };
-  auto pl_gl = [&](int i) -> PS { return pl_of(i, 2); };
+  auto pl_hh = [&](int i) -> PS { return pl_of(i, kT ? 2 : 1); };
+  auto pl_gl = [&](int i) -> PS { return pl_of(i, kT ? 1 : 2); };
   auto pl_addr = [&](int slot) -> uint32_t { return smem_u32(sG) + (uint32_t)slot * kPlane; };
 
   if (warp < kPW) {
@@ -1098,7 +1101,9 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       bool ok;
       float2 xr = load_x(0, ok);
       // kT: sX overlays the shared Params0, so W_0 comes from global memory
-      const W0Lane w0 = kT ? w0_lane(a.W0, a.b0, lane) : w0_lane(p0, lane);
+      // (held in registers); otherwise from the shared copy, per tile
+      W0Lane w0g;
+      if (kT) w0g = w0_lane(a.W0, a.b0, lane);
       for (int i = 0; i < nmine; ++i) {
         bool ok_next;
         const float2 xn = load_x(i + 1, ok_next);
@@ -1106,14 +1111,15 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           // the H_1 hi plane (all the wgrad reads, R28) into its FIFO slot;
           // the 4 producer warps meet at a named barrier, one thread arrives
           const PS ph = pl_hh(i);
-          mbar_wait(&pempty[ph.slot], (ph.use & 1) ^ 1);
-          produce_h1<false, 32>(xr, ok, w0, a.alpha, pl_addr(ph.slot), 0u, 32 * warp, lane);
+          SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[ph.slot], (ph.use & 1) ^ 1));
+          produce_h1<false, 32>(xr, ok, w0g, a.alpha, pl_addr(ph.slot), 0u, 32 * warp, lane);
           fence_proxy_async_smem();
           asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
           if (warp == 0 && lane == 0) mbar_arrive(&pfull[ph.slot]);
         } else {
           mbar_wait(&emptyH[0], (i & 1) ^ 1);
-          produce_h1<kSplit, 32>(xr, ok, w0, a.alpha, smem_u32(sH), smem_u32(sH) + kPlane, 32 * warp, lane);
+          produce_h1<kSplit, 32>(xr, ok, w0_lane(p0, lane), a.alpha, smem_u32(sH), smem_u32(sH) + kPlane, 32 * warp,
+                                 lane);
           fence_proxy_async_smem();
           mbar_arrive(&fullH[0]);
         }
@@ -1144,12 +1150,13 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         }
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
+        if (kT) load(pl_gl(i), gsrc + kPlane);
         if (kLoadH) {  // (else the producers write it)
           const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
           ring_wait_ready(a.h, t, wa);
           load(pl_hh(i), hsrc);
         }
-        load(pl_gl(i), gsrc + kPlane);
+        if (!kT) load(pl_gl(i), gsrc + kPlane);
         trace_pt(trace, j, i, 0);
       }
     } else if (!kPR && lane == 0) {
@@ -1200,7 +1207,52 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       // kPR order per tile (each plane slot is released right after its last MMA):
       //  1 Gh.Hh, Gh.1 (wgrad, db)  2 dgrad Gh.Wh, Gh.Wl -> Gh free
       //  3 Gl.Hh, Gl.1 -> Hh free  4 dgrad Gl.Wh -> Gl free, accumulator full
-      for (int i = 0; kPR && i < nmine; ++i) {
+      // kT order per tile, maximising operand reuse between consecutive MMAs
+      // (the tensor pipe is bound by its shared-memory operand reads,
+      // tests/tools/mma_rate.cu) and handing the accumulator to the epilogue
+      // first:  1 dgrad G_1^T per K step: Wl.Gh, Wh.Gh, Wh.Gl -> accumulator
+      // full  2 wgrad + db per K step: Gh^T.1, Gh^T.Hh, Gl^T.Hh, Gl^T.1 ->
+      // all three planes free
+      constexpr uint32_t id_dT = make_idesc_bf16(128, 128, 1, 0);  // A = W (MN-major), B = G (K-major)
+      for (int i = 0; kT && i < nmine; ++i) {
+        const int64_t t = tile_of(i);
+        const int b = i & 1;
+        const PS gh = pl_gh(i), gl = pl_gl(i), ph = pl_hh(i);
+        const uint32_t agh = pl_addr(gh.slot), agl = pl_addr(gl.slot), ahh = pl_addr(ph.slot);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
+        ring_consumed(a.g, t);  // both G planes have been read
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        trace_pt(trace, j, i, 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
+          const uint64_t gk = make_desc(agh + kk, 16, 1024), wk = make_desc(wh + km, 16384, 1024);
+          mma_bf16(d, make_desc(wl + km, 16384, 1024), gk, id_dT, k > 0);
+          mma_bf16(d, wk, gk, id_dT, 1);
+          mma_bf16(d, wk, make_desc(agl + kk, 16, 1024), id_dT, 1);
+        }
+        mma_commit(&tfull[b]);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        if (kLoadH) ring_consumed(a.h, t);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
+          const uint64_t gh_k = make_desc(agh + km, 16384, 1024), gl_k = make_desc(agl + km, 16384, 1024);
+          const uint64_t hh_k = make_desc(ahh + km, 16384, 1024);
+          mma_bf16(acc_b, gh_k, ones, id_b, acc0);
+          mma_bf16(acc_w, gh_k, hh_k, id_w, acc0);
+          mma_bf16(acc_w, gl_k, hh_k, id_w, 1);
+          mma_bf16(acc_b, gl_k, ones, id_b, 1);
+        }
+        mma_commit(&pempty[gh.slot]);
+        mma_commit(&pempty[gl.slot]);
+        mma_commit(&pempty[ph.slot]);
+      }
+      for (int i = 0; kPR && !kT && i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1;
         const PS gh = pl_gh(i), ph = pl_hh(i), gl = pl_gl(i);
@@ -1220,18 +1272,12 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
-        constexpr uint32_t id_dT = make_idesc_bf16(128, 128, 1, 0);  // A = W (MN-major), B = G (K-major)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
           const uint64_t g = make_desc(agh + kk, 16, 1024);
-          if (kT) {  // D = G_1^T [channels][rows]
-            mma_bf16(d, make_desc(wh + km, 16384, 1024), g, id_dT, k > 0);
-            mma_bf16(d, make_desc(wl + km, 16384, 1024), g, id_dT, 1);
-          } else {
-            mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
-            mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
-          }
+          mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
+          mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
         }
         mma_commit(&pempty[gh.slot]);
         SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
@@ -1248,8 +1294,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
-          if (kT) mma_bf16(d, make_desc(wh + km, 16384, 1024), make_desc(agl + kk, 16, 1024), id_dT, 1);
-          else mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
+          mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
         }
         mma_commit(&pempty[gl.slot]);
         mma_commit(&tfull[b]);
@@ -1317,7 +1362,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       for (int i = 0; i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1, xb = i & 1;
-        mbar_wait(&xfull[xb], (i >> 1) & 1);
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 7, mbar_wait(&xfull[xb], (i >> 1) & 1));
         SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 5, mbar_wait(&tfull[b], (i >> 1) & 1));
         if (e == 0 && lane == 0) trace_pt(trace, j, i, 2);
         tc_fence_after();
@@ -1566,20 +1611,32 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
 }
 
 // ============================================================== kernels
-// trace: per-CTA launch stamps (start, end) next to the per-tile ones
+// trace: per-CTA launch stamps (start, end) next to the per-tile ones, and
+// (diagnostic build SAGIPS_BUILD_WAITS=1 only: the accounting costs
+// registers) the CTA's summed wait times per role (slots 4 + k, k as in
+// SAGIPS_TIMED: 1 loader slot, 2 MMA operands, 3 MMA accumulator, 4
+// producers' slot, 5 epilogue accumulator, 6 mask flag, 7 epilogue X rows)
 __device__ __forceinline__ unsigned long long* cta_stamps(unsigned long long* trace);
+__device__ __forceinline__ WaitAcct cta_waits(unsigned long long* cs) {
+#ifdef SAGIPS_WAIT_ACCT
+  return WaitAcct{cs ? cs + 4 : nullptr};
+#else
+  (void)cs;
+  return WaitAcct{};
+#endif
+}
 template <bool kSplit, bool kFirst, bool kHead>
 __global__ void __launch_bounds__(kThreads, 1) k_fwd(const __grid_constant__ FwdLaunch a, unsigned long long* trace) {
   unsigned long long* cs = cta_stamps(trace);
   if (cs && threadIdx.x == 0) cs[0] = globaltimer();
-  fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace);
+  fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
   if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
 template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ BwdLaunch a, unsigned long long* trace) {
   unsigned long long* cs = cta_stamps(trace);
   if (cs && threadIdx.x == 0) cs[0] = globaltimer();
-  bwd_body<kSplit, kFirst, kWgrad, kH1Load>(a, blockIdx.x, gridDim.x, trace);
+  bwd_body<kSplit, kFirst, kWgrad, kH1Load>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
   if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
 
@@ -1687,7 +1744,7 @@ static void configure_layers() {
 
 __device__ unsigned long long g_trace[kTraceLaunches][kTraceCtas * kTraceTiles * 4];
 // per-CTA [start, first tile staged, end] globaltimer stamps of each traced launch
-__device__ unsigned long long g_ctatime[kTraceLaunches][kMaxSms][4];
+__device__ unsigned long long g_ctatime[kTraceLaunches][kMaxSms][12];
 static int g_trace_on = -1;
 static int g_trace_next = 0;
 static unsigned long long* trace_slot() {

@@ -20,7 +20,8 @@ def main(rep):
         rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
         unit = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
         print(f"{d['Kernel Name'][:40]:40s} {dur:9.1f} {rows[1][hdr.index('gpu__time_duration.sum')]} "
-              f"dram {f('dram__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f}% "
+              f"dram {f('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):5.1f}% "
+              f"({(rd * unit.get(rows[1][hdr.index('dram__bytes_read.sum')], 1) + wr * unit.get(rows[1][hdr.index('dram__bytes_write.sum')], 1)) / 1e9:.2f} GB) "
               f"issue {f('sm__inst_issued.avg.pct_of_peak_sustained_active'):5.1f}% "
               f"tensor {f('sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active') or f('sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active'):5.1f}% "
               f"l1 {f('l1tex__throughput.avg.pct_of_peak_sustained_active'):5.1f}% lts {f('lts__throughput.avg.pct_of_peak_sustained_elapsed'):5.1f}% | "

@@ -1,6 +1,8 @@
 """Run one C2 step with SAGIPS_TRACE=1 and summarise the per-tile timeline of
 each tensor-core layer launch (CTA 0): producer-done / MMA-start /
-epilogue-start / epilogue-done intervals."""
+epilogue-start / epilogue-done intervals, and the per-CTA wait times per role
+(summed over the timed threads: the loader / MMA threads, lane 0 of each
+producer / epilogue warp)."""
 import ctypes
 import os
 import sys
@@ -47,6 +49,11 @@ for li in range(12):
         print(f"{'':12s} CTAs {len(c)}: start spread {(st.max() - st.min()) / 1e3:6.1f} us, end spread "
               f"{(en.max() - en.min()) / 1e3:6.1f} us, first start -> first tile {(t0 - st.min()) / 1e3:6.1f} us, "
               f"kernel {(en.max() - st.min()) / 1e3:7.1f} us, CTA0 last tile -> last CTA end {(en.max() - t[-1, 3]) / 1e3:6.1f} us")
+        # summed waits per CTA (mean over CTAs; one timed thread per role / warp)
+        wn = {1: "loader-slot", 2: "mma-operands", 3: "mma-acc", 4: "producer-slot", 5: "epi-acc(warp0..)",
+              6: "mask-flag", 7: "epi-X"}
+        w = c[:, 4:12].mean(axis=0) / 1e3
+        print(f"{'':12s} waits (us per CTA): " + ", ".join(f"{wn[k]} {w[k]:.0f}" for k in wn if w[k] > 0.5))
 
 
 def pipe_split(dstep, sms=148):
