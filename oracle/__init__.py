@@ -26,6 +26,8 @@ Modules
                outer leaders' ring every h steps, modes (Tab. III)
   gan       -- the whole per-rank step and a lockstep
                multi-rank driver
+  ensemble  -- ensemble response (Eq. 7/8), normalised residuals (Eq. 6)
+               and the split-batch rule (Eq. 10)
 
 Every function here is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against something other than itself (published
