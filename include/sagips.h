@@ -204,6 +204,29 @@ SAGIPS_API sagips_status sagips_sample_events(const float* c, int32_t k, int32_t
                                    float* events, uint32_t* hist, int32_t bins,
                                    const float* lo, const float* hi, void* stream);
 
+/* Generator prediction G(n) (the G_i(n) of Eq. 7): the constrained
+ * parameters c = constrain(G(noise)) (R1) of this rank's current generator
+ * for a caller-given noise batch, for the ensemble analysis.
+ * noise: dev [k][noise_dim] fp32; c_out: dev [k][6] fp32, row s = c of noise
+ * vector s; 1 <= k <= cfg.param_samples.  Call between training steps: it
+ * reuses the step's generator activation buffers (the next step recomputes
+ * them).  [async]  Errors: INVALID_ARG (NULL, k out of range), UNSUPPORTED
+ * (a generator layer wider than 128). */
+SAGIPS_API sagips_status sagips_predict_params(sagips_ctx* ctx, const float* noise, int32_t k, float* c_out,
+                                               void* stream);
+
+/* Ensemble response and normalised residuals (§8(f) rows 2 and 4): preds is
+ * dev [M][k][P] fp32, preds[i][s][j] = parameter j predicted by ensemble
+ * member i for noise vector s.  out (host, 3P doubles):
+ *   out[j]        p_hat_j = (1/k) sum_s (1/M) sum_i preds[i][s][j]   (Eq. 7)
+ *   out[P + j]    sigma_j = (1/k) sum_s sqrt((1/M) sum_i (preds[i][s][j] - mean_s)^2)  (Eq. 8)
+ *   out[2P + j]   r_hat_j = (p_true[j] - p_hat_j) / p_true[j]   (Eq. 6; NaN if p_true is NULL)
+ * p_true: host [P] doubles or NULL.  Sums in fp64 in a fixed order
+ * (deterministic).  M, k >= 1, 1 <= P <= 16.  [sync]  Errors: INVALID_ARG;
+ * CUDA. */
+SAGIPS_API sagips_status sagips_ensemble_stats(const float* preds, int32_t M, int32_t k, int32_t P,
+                                               const double* p_true, double* out, void* stream);
+
 /* One training step t of this rank: noise -> G -> constrain ->
  * sampler -> bootstrap real batch -> D step + Adam(D) -> G loss through the
  * updated D -> backprop through the sampler and G -> weights-only packet

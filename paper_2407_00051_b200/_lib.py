@@ -90,6 +90,8 @@ def _load():
         "sagips_kernel_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
         "sagips_timing_reset": ([vp], st),
         "sagips_debug_trace": ([vp, P(ctypes.c_size_t)], st),
+        "sagips_predict_params": ([vp, vp, ctypes.c_int32, vp, vp], st),
+        "sagips_ensemble_stats": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp, vp], st),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -106,7 +108,8 @@ EXPORTED = [
     "sagips_last_error", "sagips_sample_events", "sagips_train_step", "sagips_push_generator_grad",
     "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
-    "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace"]
+    "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace",
+    "sagips_predict_params", "sagips_ensemble_stats"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 NUM_KERNELS = 12
@@ -154,6 +157,18 @@ def sample_events(c_ptr, k, m, seed, step, rank, stream_id, events_ptr, hist_ptr
                                     ctypes.cast(lo_a, ctypes.c_void_p), ctypes.cast(hi_a, ctypes.c_void_p), stream))
 
 
+def ensemble_stats(preds_ptr, M, k, P, p_true=None, stream=None):
+    """Eq. 6-8 over dev preds [M][k][P] fp32 (see sagips.h): returns
+    (p_hat, sigma, r_hat) as numpy float64 arrays of length P."""
+    out = np.zeros(3 * P, dtype=np.float64)
+    pt = None
+    if p_true is not None:
+        pt = np.ascontiguousarray(p_true, dtype=np.float64)
+    _check(lib.sagips_ensemble_stats(preds_ptr, M, k, P, None if pt is None else pt.ctypes.data, out.ctypes.data,
+                                     stream))
+    return out[:P], out[P:2 * P], out[2 * P:]
+
+
 class Context:
     """One rank.  `workspace_ptr` is a device allocation of at least
     workspace_size(cfg) bytes owned by the caller (e.g. a torch uint8 tensor
@@ -181,6 +196,11 @@ class Context:
 
     def train_step(self, step, flags=0, stream=None):
         _check(lib.sagips_train_step(self.h, step, flags, stream), self.h)
+
+    def predict_params(self, noise_ptr, k, c_out_ptr, stream=None):
+        """Constrained parameters of the current generator for a dev noise
+        batch [k][noise_dim] -> dev c_out [k][6] (sagips_predict_params)."""
+        _check(lib.sagips_predict_params(self.h, noise_ptr, k, c_out_ptr, stream), self.h)
 
     def push_generator_grad(self, step, stream=None):
         _check(lib.sagips_push_generator_grad(self.h, step, stream), self.h)

@@ -18,6 +18,11 @@ constexpr int kMaxSms = 256;  // bound on the persistent grids (B200: 148)
 void count_launch();
 uint64_t launches_total();
 
+// k_ensemble.cu: Eq. 6-8 over preds [M][k][P] -> out_dev [3][P] (p_hat, sigma, r_hat)
+constexpr int kEnsMaxParams = 16;
+int launch_ensemble_stats(const float* preds, int M, int k, int P, const double* p_true, double* out_dev,
+                          cudaStream_t st);
+
 struct Coef6 { float v[6]; };
 
 enum EpiKind { EPI_STORE = 0, EPI_BIAS_ACT = 1, EPI_ACT_GRAD = 2 };

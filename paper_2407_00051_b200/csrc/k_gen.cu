@@ -347,6 +347,20 @@ void launch_gen_fwd(sagips_ctx* c, cudaStream_t st) {
   count_launch();
 }
 
+void launch_gen_predict(sagips_ctx* c, const float* noise, int k, float* c_out, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_gen_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_fwd_smem());
+    configured = true;
+  }
+  GenArgs a = gen_args(c);
+  a.noise = noise;
+  a.k = k;
+  a.cbuf = c_out;
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  count_launch();
+}
+
 void launch_gen_bwd(sagips_ctx* c, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {

@@ -316,6 +316,26 @@ sagips_status sagips_sample_events(const float* c, int32_t k, int32_t m, uint64_
   return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
 }
 
+sagips_status sagips_predict_params(sagips_ctx* ctx, const float* noise, int32_t k, float* c_out, void* stream) {
+  if (!ctx || !noise || !c_out || k < 1 || k > ctx->cfg.param_samples) return SAGIPS_ERR_INVALID_ARG;
+  if (!gen_fused_ok(ctx)) return SAGIPS_ERR_UNSUPPORTED;
+  launch_gen_predict(ctx, noise, k, c_out, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
+sagips_status sagips_ensemble_stats(const float* preds, int32_t M, int32_t k, int32_t P, const double* p_true,
+                                    double* out, void* stream) {
+  if (!preds || !out || M < 1 || k < 1 || P < 1 || P > kEnsMaxParams) return SAGIPS_ERR_INVALID_ARG;
+  const cudaStream_t st = (cudaStream_t)stream;
+  double* d_out = nullptr;
+  if (cudaMalloc(&d_out, sizeof(double) * 3 * P) != cudaSuccess) return SAGIPS_ERR_CUDA;
+  const int rc = launch_ensemble_stats(preds, M, k, P, p_true, d_out, st);
+  cudaError_t e = cudaMemcpyAsync(out, d_out, sizeof(double) * 3 * P, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(d_out);
+  return (rc == 0 && e == cudaSuccess) ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------- the step
