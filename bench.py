@@ -38,7 +38,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=["c2", "c1", "c5"], default="c2")
-    p.add_argument("--mode", choices=["rma", "arar", "arar-arar", "sync", "none"], default="rma")
+    p.add_argument("--mode", choices=["rma", "rma-ag", "arar", "arar-arar", "sync", "none"], default="rma")
     p.add_argument("--group-size", type=int, default=0)
     p.add_argument("--staleness", type=int, default=1)
     p.add_argument("--outer-every", type=int, default=1000)
@@ -124,7 +124,7 @@ def lib_config(args, L, rank, world):
             cfg.precision = L.PREC_BF16
             workload = "C5: paper MLPs, k=1024 m=16384 (2^24 events/rank/step), bf16 D GEMMs"
     cfg.world, cfg.rank = world, rank
-    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
+    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
              "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
     cfg.mode = modes[args.mode] if world > 1 else L.MODE_NONE
     cfg.group_size = args.group_size if (args.group_size and world > 1) else world

@@ -62,7 +62,10 @@ typedef enum {
   SAGIPS_MODE_ARAR = 1,           /* ungrouped ring over all ranks */
   SAGIPS_MODE_ARAR_ARAR = 2,      /* inner ring (two-sided) + outer ring every h */
   SAGIPS_MODE_RMA_ARAR_ARAR = 3,  /* inner ring one-sided (RMA) + outer ring */
-  SAGIPS_MODE_SYNC_ALLREDUCE = 4  /* synchronous all-reduce sum (the Horovod role) */
+  SAGIPS_MODE_SYNC_ALLREDUCE = 4, /* synchronous all-reduce sum (the Horovod role) */
+  SAGIPS_MODE_RMA_ALLGATHER = 5   /* as RMA_ARAR_ARAR, but the inner group exchanges by a one-hop
+                                     all-gather over NVSwitch: every member stores its packet into
+                                     every other member's window (no pass-along); same sums (§8(f) row 3) */
 } sagips_mode;
 
 typedef enum {

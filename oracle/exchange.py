@@ -15,7 +15,8 @@ Paper:
   outer result is used by the leader only, no rebroadcast).
 * Modes (Tab. III, P:233-247): ARAR (ungrouped), ARAR-ARAR, RMA-ARAR-ARAR.
   Numerically the last two are the same reduction (they differ in the
-  transport); mode NONE is the ensemble of P:131; SYNC_ALLREDUCE is the
+  transport), and so is the one-hop all-gather variant of the inner group
+  (mode 5: every member receives every packet directly); mode NONE is the ensemble of P:131; SYNC_ALLREDUCE is the
   synchronous baseline sum over all ranks.
 * Only generator *weight* gradients travel.
 * Staleness (R12): with s = 1 a rank combines its own packet of step t with
@@ -28,6 +29,7 @@ MODE_ARAR = 1
 MODE_ARAR_ARAR = 2
 MODE_RMA_ARAR_ARAR = 3
 MODE_SYNC_ALLREDUCE = 4
+MODE_RMA_ALLGATHER = 5  # §8(f) row 3: the inner group by a one-hop all-gather -- same sums as 2 / 3
 
 
 def group_layout(world, group_size):

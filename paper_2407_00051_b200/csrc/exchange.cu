@@ -14,6 +14,9 @@
 //    ncclSend/ncclRecv on the side stream.
 //  * outer leaders' ring every h steps (R13): NCCL send/recv
 //    among the first rank of each inner group.
+//  * one-hop all-gather (SAGIPS_MODE_RMA_ALLGATHER, §8(f) row 3): push(t)
+//    stores the packet into every group member's window at once (NVSwitch
+//    gives every pair a direct path); pull is the same wait + ascending fold.
 //  * SYNC_ALLREDUCE: ncclAllReduce (the synchronous baseline).
 //  * staleness s (R12): pull(t) folds the own packet of step t with the
 //    others' packets of step t-s, so with s = 1 the ring of step t runs on
@@ -123,6 +126,23 @@ __global__ void __launch_bounds__(1024) k_push(const float* __restrict__ packet,
   }
 }
 
+// push, one-hop all-gather (SAGIPS_MODE_RMA_ALLGATHER): CTA q stores the own
+// packet into destination q's slot (origin = me) and releases its tag; over
+// NVSwitch every member is one hop away, so there is no forwarding agent.
+struct PushAllArgs {
+  float* dst[kMaxWorld];
+  unsigned long long* dst_flag[kMaxWorld];
+};
+__global__ void __launch_bounds__(1024) k_push_all(const float* __restrict__ packet, int64_t n, PushAllArgs a,
+                                                   unsigned long long tag) {
+  block_copy(a.dst[blockIdx.x], packet, n);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(a.dst_flag[blockIdx.x], tag);
+  }
+}
+
 struct FwdArgs {
   float* src[kMaxWorld];               // own window slots, in hop order
   float* dst[kMaxWorld];               // successor's slots
@@ -183,11 +203,13 @@ __global__ void k_wait(WaitArgs a, unsigned long long timeout_ns, unsigned int* 
     }                                                                                      \
   } while (0)
 
-static bool one_sided(const sagips_ctx* c) { return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR; }
+static bool one_sided(const sagips_ctx* c) {
+  return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR || c->cfg.mode == SAGIPS_MODE_RMA_ALLGATHER;
+}
 static bool needs_nccl(const sagips_ctx* c) {
   const auto& g = c->cfg;
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) return false;
-  if (g.mode == SAGIPS_MODE_RMA_ARAR_ARAR) return g.outer_every > 0 && g.group_size < g.world;
+  if (one_sided(c)) return g.outer_every > 0 && g.group_size < g.world;
   return true;
 }
 
@@ -293,6 +315,17 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   if (one_sided(c)) {
     if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
     char* sb = x->peer_base[x->succ];
+    if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) {
+      PushAllArgs pa{};
+      for (int j = 1; j < x->g; ++j) {  // destinations pos+1, pos+2, ... (one CTA each)
+        char* db = x->peer_base[x->first + (x->pos + j) % x->g];
+        pa.dst[j - 1] = slot_ptr(db, c, g.rank, step);
+        pa.dst_flag[j - 1] = &flags_ptr(db, c)->tag[g.rank][step % kVersions];
+      }
+      k_push_all<<<x->g - 1, 1024, 0, st>>>(c->g_dW, (int64_t)pw, pa, step + 1);
+      count_launch();
+      return SAGIPS_OK;
+    }
     k_push<<<1, 1024, 0, st>>>(c->g_dW, (int64_t)pw, slot_ptr(sb, c, g.rank, step),
                                &flags_ptr(sb, c)->tag[g.rank][step % kVersions], step + 1);
     count_launch();

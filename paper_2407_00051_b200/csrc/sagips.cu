@@ -153,7 +153,7 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
   if (g->world < 1 || g->world > kMaxWorld) return bad("world must be in [1, 64]");
   if (g->rank < 0 || g->rank >= g->world) return bad("rank out of range");
   if (g->group_size < 1 || g->world % g->group_size != 0) return bad("world % group_size != 0");
-  if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_SYNC_ALLREDUCE) return bad("unknown mode");
+  if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_RMA_ALLGATHER) return bad("unknown mode");
   if (g->staleness < 0 || g->staleness > 1) return bad("staleness must be 0 or 1");
   if (g->precision != SAGIPS_PREC_FP32 && g->precision != SAGIPS_PREC_BF16) return bad("unknown precision");
   if (g->noise_dim < 1 || g->gen_hidden < 1 || g->gen_depth < 1 || g->disc_depth < 1) return bad("model dims");

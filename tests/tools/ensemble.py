@@ -38,7 +38,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--steps", type=int, default=20000)
     p.add_argument("--every", type=int, default=1000)
-    p.add_argument("--mode", choices=["rma", "arar", "arar-arar", "sync", "none"], default="none")
+    p.add_argument("--mode", choices=["rma", "rma-ag", "arar", "arar-arar", "sync", "none"], default="none")
     p.add_argument("--group-size", type=int, default=0)
     p.add_argument("--outer-every", type=int, default=10)
     p.add_argument("--seed-per-rank", action="store_true")
@@ -52,7 +52,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
+    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
              "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
     cfg = L.config_init(L.PRESET_PAPER)
     k = 1024 // world if a.split_batch else 1024  # Eq. 10
