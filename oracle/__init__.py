@@ -28,6 +28,9 @@ Modules
                multi-rank driver
   ensemble  -- ensemble response (Eq. 7/8), normalised residuals (Eq. 6)
                and the split-batch rule (Eq. 10)
+  tabulated -- the tabulated-CDF sampler variant:
+               density on a grid, trapezoid CDF, binary-search inversion,
+               exact backward of the tabulated inverse
 
 Every function here is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against something other than itself (published
