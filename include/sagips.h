@@ -207,6 +207,29 @@ SAGIPS_API sagips_status sagips_sample_events(const float* c, int32_t k, int32_t
                                    float* events, uint32_t* hist, int32_t bins,
                                    const float* lo, const float* hi, void* stream);
 
+/* Tabulated-CDF sampler variant (reading R32;
+ * the inverse-CDF method of P:295 on a tabulated density): for parameter
+ * sample s and observable o, (w, b, c) = (sigmoid(r0), softplus(r1),
+ * softplus(r2)) of (r0, r1, r2) = raw[s][3o..3o+2] and the density
+ * f(x) = w x^b (1-x)^c + (1-w) x^c (1-x)^b on [0, 1], tabulated on G nodes
+ * t_i = i/(G-1) with a trapezoid CDF F_i = S_i / S_{G-1} (fp64); event e of
+ * sample s = e / m: events[e][o] = t_i + (u - F_i) / (F_{i+1} - F_i) / (G-1)
+ * for the cell i with F_i <= u < F_{i+1}, u = uniform(word 2e+o of Philox
+ * stream (step, rank, stream_id)) as in sagips_sample_events.  raw: dev
+ * [k][6] fp32; events: dev [k*m][2] fp32; 3 <= G <= 2048.  [async]
+ * Errors: INVALID_ARG (NULL, k < 1, m < 1, G out of range, k*m >= 2^31). */
+SAGIPS_API sagips_status sagips_sample_tabulated(const float* raw, int32_t k, int32_t m, int32_t G, uint64_t seed,
+                                                 uint64_t step, uint32_t rank, uint32_t stream_id, float* events,
+                                                 void* stream);
+/* Its backward (R32): draw[s][3o+j] = dtheta_j/dr_j * sum over the sample's
+ * events of dy[e][o] dx_e/dtheta_j, the exact derivative of the tabulated
+ * inverse (theta = (w, b, c)); the same u as the forward; fixed-order fp64
+ * sums.  dy: dev [k*m][2] fp32; draw: dev [k][6] fp32.  [async]
+ * Errors: as sagips_sample_tabulated, and NULL dy / draw. */
+SAGIPS_API sagips_status sagips_sample_tabulated_bwd(const float* raw, int32_t k, int32_t m, int32_t G, uint64_t seed,
+                                                     uint64_t step, uint32_t rank, uint32_t stream_id,
+                                                     const float* dy, float* draw, void* stream);
+
 /* Generator prediction G(n) (the G_i(n) of Eq. 7): the constrained
  * parameters c = constrain(G(noise)) (R1) of this rank's current generator
  * for a caller-given noise batch, for the ensemble analysis.

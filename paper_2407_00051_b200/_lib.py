@@ -91,6 +91,10 @@ def _load():
         "sagips_timing_reset": ([vp], st),
         "sagips_debug_trace": ([vp, P(ctypes.c_size_t)], st),
         "sagips_predict_params": ([vp, vp, ctypes.c_int32, vp, vp], st),
+        "sagips_sample_tabulated": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                     ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp], st),
+        "sagips_sample_tabulated_bwd": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                         ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, vp, vp, vp], st),
         "sagips_ensemble_stats": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp, vp], st),
     }
     for name, (args, res) in sig.items():
@@ -109,7 +113,7 @@ EXPORTED = [
     "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
     "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace",
-    "sagips_predict_params", "sagips_ensemble_stats"]
+    "sagips_predict_params", "sagips_ensemble_stats", "sagips_sample_tabulated", "sagips_sample_tabulated_bwd"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 NUM_KERNELS = 12
@@ -155,6 +159,16 @@ def sample_events(c_ptr, k, m, seed, step, rank, stream_id, events_ptr, hist_ptr
     hi_a = (ctypes.c_float * 2)(*hi)
     _check(lib.sagips_sample_events(c_ptr, k, m, seed, step, rank, stream_id, events_ptr, hist_ptr, bins,
                                     ctypes.cast(lo_a, ctypes.c_void_p), ctypes.cast(hi_a, ctypes.c_void_p), stream))
+
+
+def sample_tabulated(raw_ptr, k, m, G, seed, step, rank, stream_id, events_ptr, stream=None):
+    """Tabulated-CDF sampler (R32): dev raw [k][6] -> dev events [k*m][2] (see sagips.h)."""
+    _check(lib.sagips_sample_tabulated(raw_ptr, k, m, G, seed, step, rank, stream_id, events_ptr, stream))
+
+
+def sample_tabulated_bwd(raw_ptr, k, m, G, seed, step, rank, stream_id, dy_ptr, draw_ptr, stream=None):
+    """Its backward: dev dy [k*m][2] -> dev draw [k][6] (see sagips.h)."""
+    _check(lib.sagips_sample_tabulated_bwd(raw_ptr, k, m, G, seed, step, rank, stream_id, dy_ptr, draw_ptr, stream))
 
 
 def ensemble_stats(preds_ptr, M, k, P, p_true=None, stream=None):

@@ -18,6 +18,13 @@ constexpr int kMaxSms = 256;  // bound on the persistent grids (B200: 148)
 void count_launch();
 uint64_t launches_total();
 
+// k_tabulated.cu: the tabulated-CDF sampler variant (R32)
+bool tabulated_ok(int G);
+void launch_sample_tabulated(const float* raw, int k, int m, int G, uint64_t seed, uint32_t step, uint32_t rank,
+                             uint32_t stream_id, float* events, cudaStream_t st);
+void launch_sample_tabulated_bwd(const float* raw, int k, int m, int G, uint64_t seed, uint32_t step, uint32_t rank,
+                                 uint32_t stream_id, const float* dy, float* draw, cudaStream_t st);
+
 // k_ensemble.cu: Eq. 6-8 over preds [M][k][P] -> out_dev [3][P] (p_hat, sigma, r_hat)
 constexpr int kEnsMaxParams = 16;
 int launch_ensemble_stats(const float* preds, int M, int k, int P, const double* p_true, double* out_dev,

@@ -316,6 +316,23 @@ sagips_status sagips_sample_events(const float* c, int32_t k, int32_t m, uint64_
   return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
 }
 
+sagips_status sagips_sample_tabulated(const float* raw, int32_t k, int32_t m, int32_t G, uint64_t seed,
+                                      uint64_t step, uint32_t rank, uint32_t stream_id, float* events, void* stream) {
+  if (!raw || !events || k < 1 || m < 1 || !tabulated_ok(G) || (int64_t)k * m >= (1LL << 31))
+    return SAGIPS_ERR_INVALID_ARG;
+  launch_sample_tabulated(raw, k, m, G, seed, (uint32_t)step, rank, stream_id, events, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
+sagips_status sagips_sample_tabulated_bwd(const float* raw, int32_t k, int32_t m, int32_t G, uint64_t seed,
+                                          uint64_t step, uint32_t rank, uint32_t stream_id, const float* dy,
+                                          float* draw, void* stream) {
+  if (!raw || !dy || !draw || k < 1 || m < 1 || !tabulated_ok(G) || (int64_t)k * m >= (1LL << 31))
+    return SAGIPS_ERR_INVALID_ARG;
+  launch_sample_tabulated_bwd(raw, k, m, G, seed, (uint32_t)step, rank, stream_id, dy, draw, (cudaStream_t)stream);
+  return cudaGetLastError() == cudaSuccess ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
 sagips_status sagips_predict_params(sagips_ctx* ctx, const float* noise, int32_t k, float* c_out, void* stream) {
   if (!ctx || !noise || !c_out || k < 1 || k > ctx->cfg.param_samples) return SAGIPS_ERR_INVALID_ARG;
   if (!gen_fused_ok(ctx)) return SAGIPS_ERR_UNSUPPORTED;
