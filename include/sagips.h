@@ -84,6 +84,11 @@ typedef enum {
   SAGIPS_PRESET_PAPER = 1  /* C2: G [6,128x4,6], D [2,128x4,1] (51,206 / 50,049 params), k=1024, m=1024 */
 } sagips_preset;
 
+typedef enum {
+  SAGIPS_SAMPLER_QUADRATIC = 0,  /* Q(u; c) = c0 + c1 u + c2 u^2 (R1) */
+  SAGIPS_SAMPLER_TABULATED = 1   /* density on a grid, tabulated CDF, binary-search inversion (R32) */
+} sagips_sampler;
+
 typedef struct {
   /* ranks and exchange */
   int32_t world;          /* number of ranks (GPUs) */
@@ -116,7 +121,12 @@ typedef struct {
   int32_t exchange_timeout_ms;/* bound on every exchange wait (0 = 10000) */
   int32_t phase_timing;       /* 1: record CUDA events at the phase boundaries of every step */
   int32_t disc_impl;          /* sagips_disc_impl: kernels of the discriminator hidden layers */
-  int32_t reserved[5];
+  int32_t sampler;            /* sagips_sampler of a3-a9: the closed-form quadratic quantile (R1,
+                                 default) or the tabulated CDF (R32); with the
+                                 latter, true_params holds (w, b, c) per observable, w in (0,1),
+                                 b, c > 0, and the reference data are drawn with it */
+  int32_t sampler_grid;       /* G of the tabulated sampler, 3..2048 (0 = 1024) */
+  int32_t reserved[3];
 } sagips_config;
 
 typedef struct sagips_ctx sagips_ctx;

@@ -38,6 +38,9 @@ from . import exchange as xc
 from . import mlp
 from . import philox as px
 from . import proxy
+from . import tabulated as tab
+
+SAMPLER_QUADRATIC, SAMPLER_TABULATED = 0, 1
 
 
 @dataclass
@@ -65,6 +68,10 @@ class Config:
     hist_lo: List[float] = field(default_factory=lambda: [0.0, 0.0])
     hist_hi: List[float] = field(default_factory=lambda: [4.0, 4.0])
     seed: int = 1
+    # a3-a9 sampler: the quadratic quantile (R1) or the tabulated CDF (R32;
+    # true_params then hold (w, b, c) per observable)
+    sampler: int = SAMPLER_QUADRATIC
+    sampler_grid: int = 1024
 
     @property
     def n_events(self):
@@ -103,11 +110,27 @@ class RankState:
         self.d_mW, self.d_vW, self.d_mb, self.d_vb = z(self.dW), z(self.dW), z(self.db), z(self.db)
         self.g_tau = 0
         self.d_tau = 0
-        ref = proxy.make_reference(cfg.seed, cfg.true_params, cfg.reference_rows)
         self.shard_idx = proxy.shard_indices(cfg.seed, rank, cfg.reference_rows, cfg.shard_rows)
+        if cfg.sampler == SAMPLER_TABULATED:
+            # the reference drawn by the tabulated sampler at the true (w, b, c),
+            # whose raw values the library passes in fp32 (R32)
+            ref = tab.sample_events(tabulated_raw_true(cfg)[None, :], cfg.reference_rows,
+                                    proxy.reference_uniforms(cfg.seed, cfg.reference_rows), cfg.sampler_grid)
+            ref32 = ref.astype(np.float32)
+        else:
+            ref = proxy.make_reference(cfg.seed, cfg.true_params, cfg.reference_rows)
+            ref32 = proxy.make_reference_f32(cfg.seed, cfg.true_params, cfg.reference_rows)
         self.shard = ref[self.shard_idx]
-        ref32 = proxy.make_reference_f32(cfg.seed, cfg.true_params, cfg.reference_rows)
         self.shard32 = ref32[self.shard_idx]
+
+
+def tabulated_raw_true(cfg):
+    """(logit w, log expm1 b, log expm1 c) per observable, rounded to fp32 (R32)."""
+    r = []
+    for o in range(2):
+        w, b, c = (float(np.float32(v)) for v in cfg.true_params[3 * o:3 * o + 3])
+        r += [np.log(w / (1.0 - w)), b if b > 20.0 else np.log(np.expm1(b)), c if c > 20.0 else np.log(np.expm1(c))]
+    return np.array(r, dtype=np.float32).astype(np.float64)
 
 
 def noise(cfg, step, rank):
@@ -123,16 +146,23 @@ def local_step(cfg: Config, st: RankState, t: int):
     # 1-3 generator forward and constraint
     z = noise(cfg, t, st.rank)
     raw, g_cache = mlp.forward(st.gW, st.gb, z, a)
-    c = proxy.constrain(raw)
+    tabulated = cfg.sampler == SAMPLER_TABULATED
+    if tabulated:
+        c = np.array([[tab.constrain(r[3 * o:3 * o + 3]) for o in range(2)] for r in raw])
+    else:
+        c = proxy.constrain(raw)
     # 4 synthetic events
     u = proxy.fake_uniforms(cfg.seed, t, st.rank, N)
-    y = proxy.sample_events(c, m, u)
+    y = tab.sample_events(raw, m, u, cfg.sampler_grid) if tabulated else proxy.sample_events(c, m, u)
     # 5 real batch
     ridx = proxy.real_indices(cfg.seed, t, st.rank, cfg.shard_rows, N)
     x = st.shard[ridx]
     # 6 histograms (fp32 decision: real rows from the fp32 reference; fake
     #   rows from the fp32 evaluation of the oracle's c -- see R22)
-    y32 = proxy.sample_events_f32(c.astype(np.float32), m, u)
+    if tabulated:  # the kernel's decision from fp32 raw (fp64 tables, fp32 events)
+        y32 = tab.sample_events(raw.astype(np.float32).astype(np.float64), m, u, cfg.sampler_grid).astype(np.float32)
+    else:
+        y32 = proxy.sample_events_f32(c.astype(np.float32), m, u)
     x32 = st.shard32[ridx]
     hist = np.zeros((2, 2, cfg.hist_bins + 2), dtype=np.int64)
     for o in range(2):
@@ -169,7 +199,10 @@ def generator_step(cfg: Config, dW, db, gW, g_cache, raw, u, y):
     loss_g = mlp.bce_with_logits(zG, np.ones(N))
     dzG = mlp.bce_grad(zG, np.ones(N))
     _, _, dy = mlp.backward(dW, g_d_cache, dzG[:, None], a)
-    dc, draw = proxy.sampler_backward(dy, u, raw, m)
+    if cfg.sampler == SAMPLER_TABULATED:
+        dc, draw = None, tab.sampler_backward(raw, m, u, dy, cfg.sampler_grid)
+    else:
+        dc, draw = proxy.sampler_backward(dy, u, raw, m)
     dWg, dbg, _ = mlp.backward(gW, g_cache, draw, a)
     packet = np.concatenate([w.reshape(-1) for w in dWg])
     return dict(logits_g=zG, loss_g=loss_g, dy=dy, dc=dc, draw=draw, dW_g=dWg, db_g=dbg, packet=packet)

@@ -15,6 +15,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "CUDA", 4: "NONFINITE", 5: 
           6: "STATE", 7: "TIMEOUT", 8: "UNSUPPORTED"}
 
 MODE_NONE, MODE_ARAR, MODE_ARAR_ARAR, MODE_RMA_ARAR_ARAR, MODE_SYNC_ALLREDUCE, MODE_RMA_ALLGATHER = range(6)
+SAMPLER_QUADRATIC, SAMPLER_TABULATED = 0, 1
 PREC_FP32, PREC_BF16 = 0, 1
 DISC_AUTO, DISC_SIMT, DISC_TCGEN05 = 0, 1, 2
 PRESET_DESK, PRESET_PAPER = 0, 1
@@ -50,7 +51,8 @@ class Config(ctypes.Structure):
         ("hist_bins", ctypes.c_int32), ("hist_lo", ctypes.c_float * 2), ("hist_hi", ctypes.c_float * 2),
         ("seed", ctypes.c_uint64),
         ("exchange_timeout_ms", ctypes.c_int32), ("phase_timing", ctypes.c_int32),
-        ("disc_impl", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5),
+        ("disc_impl", ctypes.c_int32), ("sampler", ctypes.c_int32), ("sampler_grid", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 3),
     ]
 
 

@@ -20,8 +20,10 @@ uint64_t launches_total();
 
 // k_tabulated.cu: the tabulated-CDF sampler variant (R32)
 bool tabulated_ok(int G);
+// hist (optional): [2 obs][bins+2] uint32 counts of the events (R22 bins), added atomically
 void launch_sample_tabulated(const float* raw, int k, int m, int G, uint64_t seed, uint32_t step, uint32_t rank,
-                             uint32_t stream_id, float* events, cudaStream_t st);
+                             uint32_t stream_id, float* events, cudaStream_t st, uint32_t* hist = nullptr,
+                             int bins = 0, const float* lo = nullptr, const float* hi = nullptr);
 void launch_sample_tabulated_bwd(const float* raw, int k, int m, int G, uint64_t seed, uint32_t step, uint32_t rank,
                                  uint32_t stream_id, const float* dy, float* draw, cudaStream_t st);
 
@@ -53,10 +55,10 @@ void launch_normals(float* out, int64_t count, float scale, uint64_t seed, uint3
 void launch_reference(float* ref, int64_t n, const float c_true[6], uint64_t seed, cudaStream_t st);
 void launch_shard(const float* ref, int64_t n_ref, float* shard, int64_t n_s, uint64_t seed, uint32_t rank,
                   cudaStream_t st);
-void launch_constrain(const float* raw, float* c, int k, cudaStream_t st);
+void launch_constrain(const float* raw, float* c, int k, cudaStream_t st, bool tab = false);
 void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard, uint64_t seed,
                         uint32_t step, uint32_t rank, float* x_events, uint32_t* real_idx, uint32_t* hist,
-                        int bins, const float lo[2], const float hi[2], cudaStream_t st);
+                        int bins, const float lo[2], const float hi[2], cudaStream_t st, bool fake = true);
 void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t step, uint32_t rank,
                           uint32_t stream_id, float* events, uint32_t* hist, int bins, const float lo[2],
                           const float hi[2], cudaStream_t st);

@@ -100,17 +100,18 @@ void launch_shard(const float* ref, int64_t n_ref, float* shard, int64_t n_s, ui
 }
 
 // ---------------------------------------------------------------- constrain
-// c[s] = (raw0, softplus(raw1), softplus(raw2), raw3, softplus(raw4), softplus(raw5)) (R1)
-__global__ void k_constrain(const float* __restrict__ raw, float* __restrict__ c, int k) {
+// c[s] = (raw0, softplus(raw1), softplus(raw2), raw3, softplus(raw4), softplus(raw5)) (R1);
+// tabulated sampler (R32): (sigmoid(raw0), softplus(raw1), softplus(raw2), ...) = (w, b, c) per observable
+__global__ void k_constrain(const float* __restrict__ raw, float* __restrict__ c, int k, int tab) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= 6 * k) return;
   const int j = i % 3;
   const float x = raw[i];
-  c[i] = (j == 0) ? x : softplus_f(x);
+  c[i] = (j == 0) ? (tab ? sigmoid_f(x) : x) : softplus_f(x);
 }
 
-void launch_constrain(const float* raw, float* c, int k, cudaStream_t st) {
-  k_constrain<<<(6 * k + 255) / 256, 256, 0, st>>>(raw, c, k);
+void launch_constrain(const float* raw, float* c, int k, cudaStream_t st, bool tab) {
+  k_constrain<<<(6 * k + 255) / 256, 256, 0, st>>>(raw, c, k, tab ? 1 : 0);
   count_launch();
 }
 
@@ -127,7 +128,8 @@ __device__ __forceinline__ void hist_add(uint32_t* h, int bin) { atomicAdd(h + b
 // atomics (exact and order-independent).  The common group (all 4 events in
 // range and in one sample, 16-B aligned rows) runs a branch-free body; the
 // ragged tail and m % 4 != 0 take the general one.
-template <bool kReal, bool kHist>
+// kFake = false: the real rows only (the tabulated sampler, R32, draws the fake rows)
+template <bool kReal, bool kHist, bool kFake = true>
 __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int m, int64_t n_events,
                                                 const float2* __restrict__ shard, uint32_t n_shard,
                                                 PhiloxKey key, uint32_t step, uint32_t rank,
@@ -153,8 +155,11 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
   uint32_t* hy1 = my + 3 * (bins + 2);
   const PhiloxRoundKeys rk = round_keys(key);
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
-    const uint4 wa = philox4x32_10(make_uint4(2 * g, step, rank, fake_stream), rk);
-    const uint4 wb = philox4x32_10(make_uint4(2 * g + 1, step, rank, fake_stream), rk);
+    uint4 wa = make_uint4(0, 0, 0, 0), wb = make_uint4(0, 0, 0, 0);
+    if (kFake) {
+      wa = philox4x32_10(make_uint4(2 * g, step, rank, fake_stream), rk);
+      wb = philox4x32_10(make_uint4(2 * g + 1, step, rank, fake_stream), rk);
+    }
     const uint32_t wf[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
     uint4 wr = make_uint4(0, 0, 0, 0);
     if (kReal) wr = philox4x32_10(make_uint4(g, step, rank, kStreamReal), rk);
@@ -166,9 +171,11 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
     float2 yv[4], xv[4];
     uint32_t iv[4];
     auto event = [&](int q) {
-      yv[q].x = quantile_f32(uniform_open01(wf[2 * q]), c0, c1, c2);
-      yv[q].y = quantile_f32(uniform_open01(wf[2 * q + 1]), c3, c4, c5);
-      if (kHist) {
+      if (kFake) {
+        yv[q].x = quantile_f32(uniform_open01(wf[2 * q]), c0, c1, c2);
+        yv[q].y = quantile_f32(uniform_open01(wf[2 * q + 1]), c3, c4, c5);
+      }
+      if (kHist && kFake) {
         hist_add(hy0, hist_bin(yv[q].x, lo0, sc0, bins));
         hist_add(hy1, hist_bin(yv[q].y, lo1, sc1, bins));
       }
@@ -184,9 +191,11 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
     if (m4 && 4 * g + 3 < n) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) event(q);
-      float4* yf = reinterpret_cast<float4*>(y_fake + 4 * (size_t)g);
-      yf[0] = make_float4(yv[0].x, yv[0].y, yv[1].x, yv[1].y);
-      yf[1] = make_float4(yv[2].x, yv[2].y, yv[3].x, yv[3].y);
+      if (kFake) {
+        float4* yf = reinterpret_cast<float4*>(y_fake + 4 * (size_t)g);
+        yf[0] = make_float4(yv[0].x, yv[0].y, yv[1].x, yv[1].y);
+        yf[1] = make_float4(yv[2].x, yv[2].y, yv[3].x, yv[3].y);
+      }
       if (kReal) {
         float4* xr = reinterpret_cast<float4*>(x_real + 4 * (size_t)g);
         xr[0] = make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y);
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
         }
         ++r;
         event(q);
-        y_fake[e] = yv[q];
+        if (kFake) y_fake[e] = yv[q];
         if (kReal) {
           x_real[e] = xv[q];
           real_idx[e] = iv[q];
@@ -243,7 +252,7 @@ static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* sm
 void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard,
                         uint64_t seed, uint32_t step, uint32_t rank, float* x_events,
                         uint32_t* real_idx, uint32_t* hist, int bins, const float lo[2],
-                        const float hi[2], cudaStream_t st) {
+                        const float hi[2], cudaStream_t st, bool fake) {
   const int64_t n = (int64_t)k * m;
   float sc[2];
   hist_params(lo, hi, bins, sc);
@@ -254,7 +263,8 @@ void launch_sample_step(const float* c, int k, int m, const float* shard, int64_
   float2* x = reinterpret_cast<float2*>(x_events);
   const int vec_ok = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(x_events) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(real_idx) % 16 == 0);
-  auto kern = hist ? k_sample<true, true> : k_sample<true, false>;
+  auto kern = fake ? (hist ? k_sample<true, true> : k_sample<true, false>)
+                   : (hist ? k_sample<true, true, false> : k_sample<true, false, false>);
   kern<<<blocks, 256, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard),
                                             (uint32_t)n_shard, make_key(seed), step, rank, kStreamFake,
                                             x, x + n, real_idx, hist, bins, lo[0], sc[0], lo[1], sc[1], per_warp,

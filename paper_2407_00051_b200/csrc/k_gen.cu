@@ -40,6 +40,7 @@ struct GenArgs {
   float* dB;
   int k;
   float alpha;
+  int tab;                        // constrain for the tabulated sampler (R32): c0 = sigmoid(raw0)
   // wgrad tiles: tile_base[l] = first blockIdx of layer l; tiles_i[l] = in-tiles per out-tile row
   int tile_base[kMaxLayers + 1];
   int tiles_i[kMaxLayers];
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
         a.act[l][(int64_t)(r0 + r) * out + o] = acc;
         if (!hidden) {  // a3: constrain (R1): c0 = raw, c1/c2 = softplus(raw)
           const int j = o % 3;
-          a.cbuf[(int64_t)(r0 + r) * out + o] = (j == 0) ? acc : softplus_f(acc);
+          a.cbuf[(int64_t)(r0 + r) * out + o] = (j == 0) ? (a.tab ? sigmoid_f(acc) : acc) : softplus_f(acc);
         }
       }
     };
@@ -324,6 +325,7 @@ static GenArgs gen_args(sagips_ctx* c) {
   a.dB = c->g_dB;
   a.k = c->cfg.param_samples;
   a.alpha = c->cfg.leaky_slope;
+  a.tab = c->cfg.sampler == SAGIPS_SAMPLER_TABULATED;
   a.wtot = G.nw;
   a.btot = G.nb;
   // row splits of 32-row multiples while the partials fit the scratch

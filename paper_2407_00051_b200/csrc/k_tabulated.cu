@@ -103,11 +103,20 @@ __device__ __forceinline__ double event_u(PhiloxKey key, uint32_t step, uint32_t
 }
 }  // namespace
 
+struct TabHist {
+  uint32_t* hist;  // [2 obs][bins+2] or nullptr
+  int bins;
+  float lo0, sc0, lo1, sc1;
+};
+
 __global__ void __launch_bounds__(kTabThreads) k_tab_fwd(const float* __restrict__ raw, int m, int G, PhiloxKey key,
                                                          uint32_t step, uint32_t rank, uint32_t stream,
-                                                         float2* __restrict__ events) {
-  extern __shared__ double tsm[];  // [2][G] tables, then [kTabThreads] scan scratch
+                                                         float2* __restrict__ events, TabHist th) {
+  extern __shared__ double tsm[];  // [2][G] tables, then [kTabThreads] scan scratch, then [2][bins+2] counts
   double* s_tot = tsm + 2 * G;
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_tot + kTabThreads);
+  const int hsz = th.hist ? th.bins + 2 : 0;
+  for (int i = threadIdx.x; i < 2 * hsz; i += kTabThreads) s_hist[i] = 0;
   const int s = blockIdx.x;
   const double delta = 1.0 / (G - 1);
   for (int o = 0; o < 2; ++o) {
@@ -131,6 +140,15 @@ __global__ void __launch_bounds__(kTabThreads) k_tab_fwd(const float* __restrict
       xo[o] = (float)(i * delta + (u - F[i]) / (F[i + 1] - F[i]) * delta);
     }
     events[e] = make_float2(xo[0], xo[1]);
+    if (th.hist) {
+      atomicAdd(&s_hist[hist_bin(xo[0], th.lo0, th.sc0, th.bins)], 1u);
+      atomicAdd(&s_hist[hsz + hist_bin(xo[1], th.lo1, th.sc1, th.bins)], 1u);
+    }
+  }
+  if (th.hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * hsz; i += kTabThreads)
+      if (s_hist[i]) atomicAdd(&th.hist[i], s_hist[i]);
   }
 }
 
@@ -198,19 +216,32 @@ __global__ void __launch_bounds__(kTabThreads) k_tab_bwd(const float* __restrict
   }
 }
 
-static size_t tab_smem(int G, bool bwd) { return sizeof(double) * ((bwd ? 8 : 2) * (size_t)G + kTabThreads); }
+static size_t tab_smem(int G, bool bwd, int bins = 0) {
+  return sizeof(double) * ((bwd ? 8 : 2) * (size_t)G + kTabThreads) + (bins > 0 ? sizeof(uint32_t) * 2 * (bins + 2) : 0);
+}
 
 bool tabulated_ok(int G) { return G >= 3 && G <= kTabMaxG; }
 
 void launch_sample_tabulated(const float* raw, int k, int m, int G, uint64_t seed, uint32_t step, uint32_t rank,
-                             uint32_t stream_id, float* events, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_tab_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem(kTabMaxG, false));
-    configured = true;
+                             uint32_t stream_id, float* events, cudaStream_t st, uint32_t* hist, int bins,
+                             const float* lo, const float* hi) {
+  TabHist th{nullptr, 0, 0.f, 0.f, 0.f, 0.f};
+  if (hist && bins > 0) {
+    th.hist = hist;
+    th.bins = bins;
+    th.lo0 = lo[0];
+    th.lo1 = lo[1];
+    th.sc0 = (float)bins / (hi[0] - lo[0]);  // fp32, as the quadratic sampler (R22)
+    th.sc1 = (float)bins / (hi[1] - lo[1]);
   }
-  k_tab_fwd<<<k, kTabThreads, tab_smem(G, false), st>>>(raw, m, G, make_key(seed), step, rank, stream_id,
-                                                         reinterpret_cast<float2*>(events));
+  const size_t sm = tab_smem(G, false, th.bins);
+  static size_t configured = 0;
+  if (sm > configured) {
+    cudaFuncSetAttribute(k_tab_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = sm;
+  }
+  k_tab_fwd<<<k, kTabThreads, sm, st>>>(raw, m, G, make_key(seed), step, rank, stream_id,
+                                         reinterpret_cast<float2*>(events), th);
   count_launch();
 }
 

@@ -148,6 +148,8 @@ static sagips_status fail(sagips_ctx* c, sagips_status s, const char* fmt, ...) 
                                        cudaGetErrorString(e_), __FILE__, __LINE__);           \
   } while (0)
 
+static int tab_grid(const sagips_config& g) { return g.sampler_grid > 0 ? g.sampler_grid : 1024; }
+
 static sagips_status validate(const sagips_config* g, std::string* why) {
   auto bad = [&](const char* m) { *why = m; return SAGIPS_ERR_CONFIG; };
   if (g->world < 1 || g->world > kMaxWorld) return bad("world must be in [1, 64]");
@@ -165,9 +167,15 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
   if (2 * N >= (1LL << 31)) return bad("2N must be < 2^31");
   if (g->reference_rows < 1 || g->reference_rows >= (1LL << 32)) return bad("reference_rows in [1, 2^32)");
   if (g->shard_rows < 1 || g->shard_rows >= (1LL << 32)) return bad("shard_rows in [1, 2^32)");
+  if (g->sampler != SAGIPS_SAMPLER_QUADRATIC && g->sampler != SAGIPS_SAMPLER_TABULATED) return bad("unknown sampler");
+  if (g->sampler == SAGIPS_SAMPLER_TABULATED && g->sampler_grid != 0 && !tabulated_ok(g->sampler_grid))
+    return bad("sampler_grid must be in [3, 2048]");
   for (int o = 0; o < 2; ++o)
     if (!(g->true_params[3 * o + 1] > 0.f) || !(g->true_params[3 * o + 2] > 0.f))
-      return bad("true c1, c2 must be > 0 (softplus range)");
+      return bad("true c1, c2 (tabulated: b, c) must be > 0 (softplus range)");
+  if (g->sampler == SAGIPS_SAMPLER_TABULATED)
+    for (int o = 0; o < 2; ++o)
+      if (!(g->true_params[3 * o] > 0.f && g->true_params[3 * o] < 1.f)) return bad("true w must be in (0, 1)");
   if (g->hist_bins < 1 || g->hist_bins > 4096) return bad("hist_bins in [1, 4096]");
   if (!(g->leaky_slope >= 0.f && g->leaky_slope < 1.f)) return bad("leaky_slope must be in [0, 1) (R6)");
   if (g->disc_impl < SAGIPS_DISC_AUTO || g->disc_impl > SAGIPS_DISC_TCGEN05) return bad("unknown disc_impl");
@@ -282,7 +290,21 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
     if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(float) * (p == ctx->gmB || p == ctx->gvB ? ctx->G.nb : ctx->D.nb), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(ctx->stats, 0, sizeof(sagips_step_stats), st);
   // loop-closure reference and the rank's shard
-  launch_reference(ctx->ref, g.reference_rows, g.true_params, g.seed, st);
+  if (g.sampler == SAGIPS_SAMPLER_TABULATED) {
+    // reference events from the tabulated sampler at the true (w, b, c) (R32):
+    // raw_true = (logit w, log expm1 b, log expm1 c) in fp32, word 2e+o of the REF stream
+    float rt[6];
+    for (int o = 0; o < 2; ++o) {
+      const double w = g.true_params[3 * o], b = g.true_params[3 * o + 1], cc = g.true_params[3 * o + 2];
+      rt[3 * o] = (float)std::log(w / (1.0 - w));
+      rt[3 * o + 1] = (float)(b > 20.0 ? b : std::log(std::expm1(b)));
+      rt[3 * o + 2] = (float)(cc > 20.0 ? cc : std::log(std::expm1(cc)));
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->draw, rt, sizeof rt, cudaMemcpyHostToDevice);  // scratch
+    launch_sample_tabulated(ctx->draw, 1, (int)g.reference_rows, tab_grid(g), g.seed, 0, 0, kStreamRef, ctx->ref, st);
+  } else {
+    launch_reference(ctx->ref, g.reference_rows, g.true_params, g.seed, st);
+  }
   launch_shard(ctx->ref, g.reference_rows, ctx->shard, g.shard_rows, g.seed, g.rank, st);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -824,13 +846,19 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
                   c->gAct[l], G.sizes[l + 1], ep, 1, 0, st);
       in = c->gAct[l];
     }
-    launch_constrain(c->gAct[G.L - 1], c->cbuf, k, st);
+    launch_constrain(c->gAct[G.L - 1], c->cbuf, k, st, g.sampler == SAGIPS_SAMPLER_TABULATED);
   }
   const float* raw = c->gAct[G.L - 1];
-  // a4-a6 fused sampler + bootstrap + histograms
+  const bool tab = g.sampler == SAGIPS_SAMPLER_TABULATED;
+  // a4-a6 fused sampler + bootstrap + histograms (tabulated: the bootstrap
+  // pass draws the real rows, the tabulated sampler the fake rows N..2N-1)
   mark(c, 1, st);
   launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
-                     g.hist_bins, g.hist_lo, g.hist_hi, st);
+                     g.hist_bins, g.hist_lo, g.hist_hi, st, !tab);
+  if (tab)
+    launch_sample_tabulated(raw, k, m, tab_grid(g), g.seed, step, g.rank, kStreamFake,
+                            c->X + 2 * (int64_t)k * m, st, c->hist ? c->hist + 2 * (g.hist_bins + 2) : nullptr,
+                            g.hist_bins, g.hist_lo, g.hist_hi);
   mark(c, 2, st);
   // a7 discriminator step + Adam(D) ; a8 generator loss through the updated D
   disc_step(c, st);
@@ -840,7 +868,8 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   gen_loss_through_disc(c, st);
   mark(c, 4, st);
   // a9 sampler backward
-  launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st);
+  if (tab) launch_sample_tabulated_bwd(raw, k, m, tab_grid(g), g.seed, step, g.rank, kStreamFake, c->dy, c->draw, st);
+  else launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st);
   mark(c, 5, st);
   // a10 generator backward (the output layer is linear: dZ_L = draw);
   // a11 the weight gradients land in g_dW, which *is* the packet layout
