@@ -42,6 +42,9 @@ def parse():
     p.add_argument("--group-size", type=int, default=0)
     p.add_argument("--staleness", type=int, default=1)
     p.add_argument("--outer-every", type=int, default=1000)
+    p.add_argument("--sampler", choices=["quadratic", "tabulated"], default="quadratic",
+                   help="a3-a9 sampler: the closed-form quantile (R1) or the tabulated CDF (R32, SURVEY 8(f) row 1)")
+    p.add_argument("--sampler-grid", type=int, default=1024)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -131,6 +134,14 @@ def lib_config(args, L, rank, world):
     cfg.outer_every = args.outer_every
     cfg.staleness = args.staleness if world > 1 else 0
     cfg.phase_timing = 1
+    if getattr(args, "sampler", "quadratic") == "tabulated":
+        cfg.sampler = L.SAMPLER_TABULATED
+        cfg.sampler_grid = args.sampler_grid
+        for j, v in enumerate((0.3, 2.0, 1.2, 0.7, 1.5, 3.0)):  # true (w, b, c) per observable
+            cfg.true_params[j] = v
+        for o in range(2):
+            cfg.hist_lo[o], cfg.hist_hi[o] = 0.0, 1.0
+        workload += f", tabulated-CDF sampler G={args.sampler_grid} (R32)"
     if world > 1:
         workload = workload.replace("C2:", "C3:") + f", {args.mode} ring g={cfg.group_size} s={cfg.staleness}"
     return cfg, workload
