@@ -993,18 +993,23 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   constexpr bool kLoadH = kWgrad && (!kFirst || kH1Load);  // H planes come from global memory
   // (split wgrad passes; the layer-1 H_1 hi plane is either bulk-loaded,
   // kH1Load, or recomputed from X by the SIMT producers into its plane slot)
-  constexpr bool kPR = kSplit && kWgrad;
-  // kT (D step, first layer, plane ring): the dgrad computes G_1^T (A = W_1
-  // MN-major, B = G_2 K-major), so TMEM lane = channel c and column = row:
-  // dW_0 = G_1^T X and db_0 accumulate per thread over rows (no shuffles),
-  // with the tile's X rows bulk-loaded into shared memory
-  constexpr bool kT = kFirst && kWgrad && kPR;
+  // kT (D step, first layer, plane ring; both precisions, except the bf16
+  // pipelined role): the dgrad computes G_1^T (A = W_1 MN-major, B = G_2
+  // K-major), so TMEM lane = channel c and column = row: dW_0 = G_1^T X and
+  // db_0 accumulate per thread over rows (no shuffles), with the tile's X
+  // rows bulk-loaded into shared memory
+  constexpr bool kT = kFirst && kWgrad && (kSplit || !kH1Load);
+  constexpr bool kPR = (kSplit && kWgrad) || kT;
+  constexpr int NP = kSplit ? 3 : 2;  // kT planes per tile: Gh (, Gl), Hh
+  // operand area from sG: kT 5 plane slots (its staging area is free: no G_l
+  // output); otherwise two stages and the epilogue staging
+  constexpr uint32_t kSlotArea = kT ? 5 * kPlane : 2 * TB + kEW * kStg;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sG = sW + TB;     // G stage 0 (kPR: plane slots 0, 1)
   uint8_t* sH = sG + TB;     // H stage (wgrad) or G stage 1 (kPR: plane slots 2, 3)
   uint8_t* sStg = sH + TB;   // 8 x 4 KiB (dy: the partial-dot exchange; kPR first: plane slot 4)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sStg + kEW * kStg);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + kSlotArea);
   uint64_t* fullG = bars;       // [2]
   uint64_t* emptyG = bars + 2;  // [2]
   uint64_t* fullH = bars + 4;   // [1]
@@ -1081,10 +1086,11 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   // kT: planes Gh, Gl, Hh over 5 slots (its staging area is the 5th; every
   // plane is held until the end of its tile's MMAs, see the MMA issuer)
   constexpr int kSlots = kT ? 5 : 4;
-  auto pl_of = [&](int i, int k) -> PS { return PS{(3 * i + k) % kSlots, (3 * i + k) / kSlots}; };
+  constexpr int kNP = kT ? NP : 3;
+  auto pl_of = [&](int i, int k) -> PS { return PS{(kNP * i + k) % kSlots, (kNP * i + k) / kSlots}; };
   auto pl_gh = [&](int i) -> PS { return pl_of(i, 0); };
-  auto pl_hh = [&](int i) -> PS { return pl_of(i, kT ? 2 : 1); };
-  auto pl_gl = [&](int i) -> PS { return pl_of(i, kT ? 1 : 2); };
+  auto pl_hh = [&](int i) -> PS { return pl_of(i, kT ? kNP - 1 : 1); };
+  auto pl_gl = [&](int i) -> PS { return pl_of(i, kT ? 1 : 2); };  // (split only)
   auto pl_addr = [&](int slot) -> uint32_t { return smem_u32(sG) + (uint32_t)slot * kPlane; };
 
   if (warp < kPW) {
@@ -1150,7 +1156,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         }
         ring_wait_ready(a.g, t, wa);
         load(pl_gh(i), gsrc);
-        if (kT) load(pl_gl(i), gsrc + kPlane);
+        if (kT && kSplit) load(pl_gl(i), gsrc + kPlane);
         if (kLoadH) {  // (else the producers write it)
           const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
           ring_wait_ready(a.h, t, wa);
@@ -1214,7 +1220,37 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       // full  2 wgrad + db per K step: Gh^T.1, Gh^T.Hh, Gl^T.Hh, Gl^T.1 ->
       // all three planes free
       constexpr uint32_t id_dT = make_idesc_bf16(128, 128, 1, 0);  // A = W (MN-major), B = G (K-major)
-      for (int i = 0; kT && i < nmine; ++i) {
+      for (int i = 0; kT && !kSplit && i < nmine; ++i) {  // bf16: one G plane, W hi only
+        const int64_t t = tile_of(i);
+        const int b = i & 1;
+        const PS gh = pl_gh(i), ph = pl_hh(i);
+        const uint32_t agh = pl_addr(gh.slot), ahh = pl_addr(ph.slot);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        ring_consumed(a.g, t);
+        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        trace_pt(trace, j, i, 1);
+        tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
+          mma_bf16(d, make_desc(wh + km, 16384, 1024), make_desc(agh + kk, 16, 1024), id_dT, k > 0);
+        }
+        mma_commit(&tfull[b]);
+        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        if (kLoadH) ring_consumed(a.h, t);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
+          const uint64_t gh_k = make_desc(agh + km, 16384, 1024);
+          mma_bf16(acc_b, gh_k, ones, id_b, acc0);
+          mma_bf16(acc_w, gh_k, make_desc(ahh + km, 16384, 1024), id_w, acc0);
+        }
+        mma_commit(&pempty[gh.slot]);
+        mma_commit(&pempty[ph.slot]);
+      }
+      for (int i = 0; kT && kSplit && i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1;
         const PS gh = pl_gh(i), gl = pl_gl(i), ph = pl_hh(i);
@@ -1706,7 +1742,9 @@ static size_t fwd_smem(bool split) {
 }
 static size_t bwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
-  return 3 * TB + kEW * kStg + 26 * 8 + 16 + 512 + std::max<size_t>(sizeof(Params0) + 32 + 64, 2 * 128 * 8);
+  // operand area: two stages + staging, or the first layer's 5 plane slots (kT, bf16 too)
+  const size_t area = std::max<size_t>(2 * TB + kEW * kStg, 5 * (size_t)kPlane);
+  return TB + area + 26 * 8 + 16 + 512 + std::max<size_t>(sizeof(Params0) + 32 + 64, 2 * 128 * 8);
 }
 
 template <typename K>
