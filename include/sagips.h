@@ -271,6 +271,20 @@ SAGIPS_API sagips_status sagips_ensemble_stats(const float* preds, int32_t M, in
  * Errors: STATE if t is not the next step; CUDA. */
 SAGIPS_API sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream);
 
+/* sagips_train_step with the step's inputs supplied by the caller (host
+ * memory, pinned for asynchronous copies), for a data-loading pipeline: the
+ * generator noise of a1 (host_noise: [k][noise_dim] fp32, else drawn by
+ * Philox) and the real batch of a5 (host_real: [N][2] fp32 real rows,
+ * replacing the bootstrap from the resident shard; the real half of the
+ * histogram is then zero and SAGIPS_T_REAL_IDX is not written), copied to
+ * the device on `stream` at the start of the step; host_stats (or NULL)
+ * receives the step's stats record by an asynchronous copy at its end
+ * (valid once `stream` has completed).  [async]  Errors: as
+ * sagips_train_step. */
+SAGIPS_API sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, uint32_t flags,
+                                                const float* host_noise, const float* host_real,
+                                                sagips_step_stats* host_stats, void* stream);
+
 /* Exchange halves, for callers that overlap them with other work.  push
  * publishes the step-t packet to the ring (one-sided: a store into the
  * successor's window + release flag; two-sided: NCCL send/recv).

@@ -78,6 +78,7 @@ def _load():
         "sagips_sample_events": ([vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
                                   ctypes.c_uint32, ctypes.c_uint32, vp, vp, ctypes.c_int32, vp, vp, vp], st),
         "sagips_train_step": ([vp, ctypes.c_uint64, ctypes.c_uint32, vp], st),
+        "sagips_train_step_host": ([vp, ctypes.c_uint64, ctypes.c_uint32, vp, vp, vp, vp], st),
         "sagips_push_generator_grad": ([vp, ctypes.c_uint64, vp], st),
         "sagips_pull_generator_grad": ([vp, ctypes.c_uint64, vp], st),
         "sagips_tensor_bytes": ([vp, ctypes.c_int32, P(ctypes.c_size_t)], st),
@@ -115,7 +116,8 @@ EXPORTED = [
     "sagips_pull_generator_grad", "sagips_tensor_bytes", "sagips_get", "sagips_set", "sagips_ipc_handle",
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
     "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace",
-    "sagips_predict_params", "sagips_ensemble_stats", "sagips_sample_tabulated", "sagips_sample_tabulated_bwd"]
+    "sagips_predict_params", "sagips_ensemble_stats", "sagips_sample_tabulated", "sagips_sample_tabulated_bwd",
+    "sagips_train_step_host"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 NUM_KERNELS = 12
@@ -217,6 +219,11 @@ class Context:
         """Constrained parameters of the current generator for a dev noise
         batch [k][noise_dim] -> dev c_out [k][6] (sagips_predict_params)."""
         _check(lib.sagips_predict_params(self.h, noise_ptr, k, c_out_ptr, stream), self.h)
+
+    def train_step_host(self, step, flags=0, noise_ptr=None, real_ptr=None, stats_ptr=None, stream=None):
+        """train_step with the noise / real batch from host memory and the stats
+        record copied back asynchronously (sagips_train_step_host)."""
+        _check(lib.sagips_train_step_host(self.h, step, flags, noise_ptr, real_ptr, stats_ptr, stream), self.h)
 
     def push_generator_grad(self, step, stream=None):
         _check(lib.sagips_push_generator_grad(self.h, step, stream), self.h)

@@ -64,6 +64,8 @@ struct sagips_ctx {
   float* lpart[sagips::kMaxLayers] = {};  // [ctas][128][128] wgrad partials of hidden layer l
   float* ldb[sagips::kMaxLayers] = {};    // [ctas][128] bias-gradient partials
   bool d_adam_done = false;               // the D step already applied Adam(D) (fused reduction)
+  const float* host_noise = nullptr;      // sagips_train_step_host: this step's inputs from the caller
+  const float* host_real = nullptr;
   static constexpr int kTileCtrs = 16;
   uint32_t* tile_ctrs = nullptr;          // dynamic tile-schedule counters of the layer kernels
   int tile_ctr_next = 0;

@@ -832,8 +832,11 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   const float a = g.leaky_slope;
   const uint32_t step = (uint32_t)t;
   mark(c, 0, st);
-  // a1 noise ~ N(0,1)
-  launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
+  // a1 noise ~ N(0,1) (or the caller's, sagips_train_step_host)
+  if (c->host_noise)
+    cudaMemcpyAsync(c->noise, c->host_noise, sizeof(float) * k * g.noise_dim, cudaMemcpyHostToDevice, st);
+  else
+    launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
   // a2 generator forward (hidden LeakyReLU, linear output) + a3 constrain
   const bool fused_gen = gen_fused_ok(c);
   if (fused_gen) {
@@ -853,8 +856,18 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   // a4-a6 fused sampler + bootstrap + histograms (tabulated: the bootstrap
   // pass draws the real rows, the tabulated sampler the fake rows N..2N-1)
   mark(c, 1, st);
-  launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
-                     g.hist_bins, g.hist_lo, g.hist_hi, st, !tab);
+  if (c->host_real) {
+    // the caller's real batch (rows 0..N-1) replaces the bootstrap (a5); the
+    // fake rows and their histogram as usual, the real histogram is zero
+    cudaMemcpyAsync(c->X, c->host_real, sizeof(float) * 2 * (int64_t)k * m, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(c->hist, 0, sizeof(uint32_t) * 4 * (g.hist_bins + 2), st);
+    if (!tab)
+      launch_sample_events(c->cbuf, k, m, g.seed, step, g.rank, kStreamFake, c->X + 2 * (int64_t)k * m,
+                           c->hist + 2 * (g.hist_bins + 2), g.hist_bins, g.hist_lo, g.hist_hi, st);
+  } else {
+    launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
+                       g.hist_bins, g.hist_lo, g.hist_hi, st, !tab);
+  }
   if (tab)
     launch_sample_tabulated(raw, k, m, tab_grid(g), g.seed, step, g.rank, kStreamFake,
                             c->X + 2 * (int64_t)k * m, st, c->hist ? c->hist + 2 * (g.hist_bins + 2) : nullptr,
@@ -926,6 +939,19 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
     ctx->skip_adam_once = true;
   }
   return sagips_pull_generator_grad(ctx, step, stream);
+}
+
+sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, uint32_t flags, const float* host_noise,
+                                     const float* host_real, sagips_step_stats* host_stats, void* stream) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  ctx->host_noise = host_noise;
+  ctx->host_real = host_real;
+  const sagips_status s = sagips_train_step(ctx, step, flags, stream);
+  ctx->host_noise = ctx->host_real = nullptr;
+  if (s != SAGIPS_OK) return s;
+  if (host_stats)
+    CK(cudaMemcpyAsync(host_stats, ctx->stats, sizeof(sagips_step_stats), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  return SAGIPS_OK;
 }
 
 sagips_status sagips_push_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream) {

@@ -321,3 +321,29 @@ def test_kernel_times_cover_the_layer_passes():
     assert n == 3
     assert all(v > 0 for v in kt.values()), kt
     assert sum(kt.values()) <= ph["disc_step"] + ph["gen_loss_through_disc"] + 1e-3
+
+
+@pytest.mark.parametrize("preset", [0, 1])
+def test_train_step_host_inputs_reproduce_the_device_step(preset):
+    """sagips_train_step_host: the same step fed from pinned host memory with
+    the noise and real rows the device RNG would have produced is bit-identical
+    to the device-input step; the stats record arrives in the host buffer."""
+    import ctypes
+    L = lib()
+    kw = dict(seed=21, param_samples=32, events_per_sample=45, reference_rows=4000, shard_rows=2000)
+    ca, cb = make_ctx(L.config_init(preset, **kw)), make_ctx(L.config_init(preset, **kw))
+    ca.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    torch.cuda.synchronize()
+    N = 32 * 45
+    noise = torch.from_numpy(ca.get(L.T_NOISE).reshape(32, -1).copy()).pin_memory()
+    real = torch.from_numpy(ca.get(L.T_EVENTS).reshape(-1, 2)[:N].copy()).pin_memory()
+    stats = (ctypes.c_uint8 * ctypes.sizeof(L.StepStats))()
+    cb.train_step_host(0, L.STEP_LOCAL_ONLY, noise.data_ptr(), real.data_ptr(), ctypes.addressof(stats), _stream())
+    torch.cuda.synchronize()
+    for w in (L.T_NOISE, L.T_RAW, L.T_EVENTS, L.T_LOGITS_D, L.T_DISC_DW, L.T_DISC_DB, L.T_DY, L.T_DRAW, L.T_GEN_DW):
+        assert np.array_equal(ca.get(w), cb.get(w)), w
+    sa, sb = ca.get(L.T_STATS), L.StepStats.from_buffer_copy(stats)
+    assert sa.loss_d == sb.loss_d and sa.loss_g == sb.loss_g and sb.nonfinite == 0
+    # the real half of the histogram is zero (no bootstrap), the fake half as the device step
+    ha, hb = ca.get(L.T_HIST).reshape(2, -1), cb.get(L.T_HIST).reshape(2, -1)
+    assert np.all(hb[0] == 0) and np.array_equal(ha[1], hb[1])
