@@ -126,7 +126,10 @@ typedef struct {
                                  latter, true_params holds (w, b, c) per observable, w in (0,1),
                                  b, c > 0, and the reference data are drawn with it */
   int32_t sampler_grid;       /* G of the tabulated sampler, 3..2048 (0 = 1024) */
-  int32_t reserved[3];
+  int32_t packet_biases;      /* 1: tensor fusion: the exchanged packet
+                                 is [weights | biases] and Adam(G) applies the reduced bias
+                                 gradients; 0 (default): weights only, biases local */
+  int32_t reserved[2];
 } sagips_config;
 
 typedef struct sagips_ctx sagips_ctx;
@@ -155,7 +158,7 @@ typedef enum {
   SAGIPS_T_GEN_DB = 17,      /* [Pb] local generator bias gradient */
   SAGIPS_T_DISC_DW = 18,     /* [Qw] discriminator weight gradient of the D step */
   SAGIPS_T_DISC_DB = 19,     /* [Qb] */
-  SAGIPS_T_REDUCED = 20,     /* [Pw] reduced packet applied to the generator */
+  SAGIPS_T_REDUCED = 20,     /* [Pw] reduced packet applied to the generator ([Pw + Pb] with packet_biases) */
   SAGIPS_T_STATS = 21,       /* sagips_step_stats of the last step */
   SAGIPS_T_REFERENCE = 22,   /* [N_ref][2] reference events */
   SAGIPS_T_SHARD = 23,       /* [n_s][2] this rank's shard */

@@ -72,6 +72,9 @@ class Config:
     # true_params then hold (w, b, c) per observable)
     sampler: int = SAMPLER_QUADRATIC
     sampler_grid: int = 1024
+    # tensor fusion: the packet also carries the
+    # bias gradients and Adam(G) applies their reduction (default: P:305)
+    packet_biases: int = 0
 
     @property
     def n_events(self):
@@ -204,14 +207,20 @@ def generator_step(cfg: Config, dW, db, gW, g_cache, raw, u, y):
     else:
         dc, draw = proxy.sampler_backward(dy, u, raw, m)
     dWg, dbg, _ = mlp.backward(gW, g_cache, draw, a)
-    packet = np.concatenate([w.reshape(-1) for w in dWg])
+    packet = np.concatenate([w.reshape(-1) for w in dWg] + ([b.reshape(-1) for b in dbg] if cfg.packet_biases else []))
     return dict(logits_g=zG, loss_g=loss_g, dy=dy, dc=dc, draw=draw, dW_g=dWg, db_g=dbg, packet=packet)
 
 
 def apply_generator(cfg: Config, st: RankState, R, db_local):
     """Step 11: unflatten R into the weight gradients; biases use the local
-    gradients (P:305); Adam(G)."""
+    gradients or, with the fused packet, R's bias part; Adam(G)."""
     st.g_tau += 1
+    if cfg.packet_biases:
+        nw = sum(w.size for w in st.gW)
+        db_local, o = [], nw
+        for b in st.gb:
+            db_local.append(R[o:o + b.size].reshape(b.shape))
+            o += b.size
     off = 0
     for l in range(len(st.gW)):
         n = st.gW[l].size

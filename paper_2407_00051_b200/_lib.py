@@ -52,7 +52,7 @@ class Config(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("exchange_timeout_ms", ctypes.c_int32), ("phase_timing", ctypes.c_int32),
         ("disc_impl", ctypes.c_int32), ("sampler", ctypes.c_int32), ("sampler_grid", ctypes.c_int32),
-        ("reserved", ctypes.c_int32 * 3),
+        ("packet_biases", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
     ]
 
 

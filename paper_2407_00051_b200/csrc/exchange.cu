@@ -66,14 +66,18 @@ struct ExchangeState {
   uint32_t* one = nullptr;          // device constant 1 (stats.outer_fired)
 };
 
-static size_t slot_floats(const sagips_ctx* c) { return (size_t)c->G.nw; }
+// the packet: generator weight gradients, plus the bias gradients with the fused packet
+static size_t slot_floats(const sagips_ctx* c) { return (size_t)c->G.nw + (c->cfg.packet_biases ? c->G.nb : 0); }
+// distance between packets in windows and buffers: 256-byte aligned (float4
+// copies; the fused packet's length is not a multiple of 4)
+static size_t slot_stride(const sagips_ctx* c) { return (slot_floats(c) + 63) & ~(size_t)63; }
 
 static float* slot_ptr(char* base, const sagips_ctx* c, int origin, uint64_t version) {
-  const size_t per_origin = kVersions * slot_floats(c);
-  return reinterpret_cast<float*>(base) + origin * per_origin + (version % kVersions) * slot_floats(c);
+  const size_t per_origin = kVersions * slot_stride(c);
+  return reinterpret_cast<float*>(base) + origin * per_origin + (version % kVersions) * slot_stride(c);
 }
 static DevFlags* flags_ptr(char* base, const sagips_ctx* c) {
-  return reinterpret_cast<DevFlags*>(base + sizeof(float) * (size_t)c->cfg.world * kVersions * slot_floats(c));
+  return reinterpret_cast<DevFlags*>(base + sizeof(float) * (size_t)c->cfg.world * kVersions * slot_stride(c));
 }
 
 // ---------------------------------------------------------------- device side
@@ -235,13 +239,13 @@ static sagips_status ensure_state(sagips_ctx* c) {
   XCK(cudaMalloc(&x->err, sizeof(unsigned int)));
   XCK(cudaMemset(x->err, 0, sizeof(unsigned int)));
   if (g.world > 1 && g.mode != SAGIPS_MODE_NONE) {
-    const size_t pw = slot_floats(c);
-    XCK(cudaMalloc(&x->gather[0], sizeof(float) * pw * gs));
-    XCK(cudaMalloc(&x->gather[1], sizeof(float) * pw * gs));
+    const size_t ps = slot_stride(c);
+    XCK(cudaMalloc(&x->gather[0], sizeof(float) * ps * gs));
+    XCK(cudaMalloc(&x->gather[1], sizeof(float) * ps * gs));
     const int nlead = g.world / g.group_size;
-    XCK(cudaMalloc(&x->outer_buf, sizeof(float) * pw * std::max(nlead, 1)));
+    XCK(cudaMalloc(&x->outer_buf, sizeof(float) * ps * std::max(nlead, 1)));
     if (one_sided(c)) {
-      x->win_bytes = sizeof(float) * (size_t)g.world * kVersions * pw + sizeof(DevFlags);
+      x->win_bytes = sizeof(float) * (size_t)g.world * kVersions * ps + sizeof(DevFlags);
       XCK(cudaMalloc(&x->win, x->win_bytes));
       XCK(cudaMemset(x->win, 0, x->win_bytes));
       x->flags = flags_ptr(reinterpret_cast<char*>(x->win), c);
@@ -297,8 +301,8 @@ static sagips_status nccl_ring(sagips_ctx* c, uint64_t step) {
     const int send_pos = (x->pos - j + 1 + x->g) % x->g;
     const int recv_pos = (x->pos - j + x->g) % x->g;
     NCK(ncclGroupStart());
-    NCK(ncclSend(gbuf + send_pos * pw, pw, ncclFloat32, x->succ, x->comm_ring, x->side));
-    NCK(ncclRecv(gbuf + recv_pos * pw, pw, ncclFloat32, x->pred, x->comm_ring, x->side));
+    NCK(ncclSend(gbuf + send_pos * slot_stride(c), pw, ncclFloat32, x->succ, x->comm_ring, x->side));
+    NCK(ncclRecv(gbuf + recv_pos * slot_stride(c), pw, ncclFloat32, x->pred, x->comm_ring, x->side));
     NCK(ncclGroupEnd());
   }
   return SAGIPS_OK;
@@ -349,7 +353,7 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   } else {
     if (!x->comm_ring) { c->err = "sagips_connect_nccl not called"; return SAGIPS_ERR_STATE; }
     float* gbuf = x->gather[step & 1];
-    XCK(cudaMemcpyAsync(gbuf + x->pos * pw, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
+    XCK(cudaMemcpyAsync(gbuf + x->pos * slot_stride(c), c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
     XCK(cudaEventRecord(x->ev_ready[step & 1], st));
     XCK(cudaStreamWaitEvent(x->side, x->ev_ready[step & 1], 0));
     s = nccl_ring(c, step);
@@ -372,17 +376,18 @@ static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   const size_t pw = slot_floats(c);
   const int lp = g.rank / g.group_size;
   const int lsucc = ((lp + 1) % nlead) * g.group_size, lpred = ((lp + nlead - 1) % nlead) * g.group_size;
-  XCK(cudaMemcpyAsync(x->outer_buf + lp * pw, c->reduced, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
+  const size_t ps = slot_stride(c);
+  XCK(cudaMemcpyAsync(x->outer_buf + lp * ps, c->reduced, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
   for (int j = 1; j < nlead; ++j) {
     const int sp = (lp - j + 1 + nlead) % nlead, rp = (lp - j + nlead) % nlead;
     NCK(ncclGroupStart());
-    NCK(ncclSend(x->outer_buf + sp * pw, pw, ncclFloat32, lsucc, x->comm_main, st));
-    NCK(ncclRecv(x->outer_buf + rp * pw, pw, ncclFloat32, lpred, x->comm_main, st));
+    NCK(ncclSend(x->outer_buf + sp * ps, pw, ncclFloat32, lsucc, x->comm_main, st));
+    NCK(ncclRecv(x->outer_buf + rp * ps, pw, ncclFloat32, lpred, x->comm_main, st));
     NCK(ncclGroupEnd());
   }
   PacketList pl{};
   pl.count = nlead;
-  for (int i = 0; i < nlead; ++i) pl.p[i] = x->outer_buf + i * pw;
+  for (int i = 0; i < nlead; ++i) pl.p[i] = x->outer_buf + i * ps;
   launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)nlead : 1.0f, st);
   XCK(cudaMemcpyAsync(&c->stats->outer_fired, x->one, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   return SAGIPS_OK;
@@ -442,7 +447,7 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st) {
       XCK(cudaStreamWaitEvent(st, x->ev_done[v], 0));
     }
     for (int i = 0; i < x->g; ++i)
-      pl.p[i] = (i == x->pos) ? c->g_dW : (stale >= 0 ? x->gather[stale & 1] + i * pw : nullptr);
+      pl.p[i] = (i == x->pos) ? c->g_dW : (stale >= 0 ? x->gather[stale & 1] + i * slot_stride(c) : nullptr);
   }
   if (stale < 0 && x->g > 1) {
     // before step s the other members' packets are zero (R12): own packet only

@@ -69,9 +69,9 @@ static void carve(sagips_ctx* c, char* base) {
   c->dW = cv.take<float>(D.nw);  c->dB = cv.take<float>(D.nb);
   c->dmW = cv.take<float>(D.nw); c->dvW = cv.take<float>(D.nw);
   c->dmB = cv.take<float>(D.nb); c->dvB = cv.take<float>(D.nb);
-  c->g_dW = cv.take<float>(G.nw); c->g_dB = cv.take<float>(G.nb);
+  c->g_dW = cv.take<float>(G.nw + G.nb); c->g_dB = c->g_dW + G.nw;  // contiguous: the fused packet
   c->d_dW = cv.take<float>(D.nw); c->d_dB = cv.take<float>(D.nb);
-  c->reduced = cv.take<float>(G.nw);
+  c->reduced = cv.take<float>(G.nw + G.nb);
   c->ref = cv.take<float>(2 * g.reference_rows);
   c->shard = cv.take<float>(2 * g.shard_rows);
   c->noise = cv.take<float>(k * g.noise_dim);
@@ -168,6 +168,7 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
   if (g->reference_rows < 1 || g->reference_rows >= (1LL << 32)) return bad("reference_rows in [1, 2^32)");
   if (g->shard_rows < 1 || g->shard_rows >= (1LL << 32)) return bad("shard_rows in [1, 2^32)");
   if (g->sampler != SAGIPS_SAMPLER_QUADRATIC && g->sampler != SAGIPS_SAMPLER_TABULATED) return bad("unknown sampler");
+  if (g->packet_biases != 0 && g->packet_biases != 1) return bad("packet_biases must be 0 or 1");
   if (g->sampler == SAGIPS_SAMPLER_TABULATED && g->sampler_grid != 0 && !tabulated_ok(g->sampler_grid))
     return bad("sampler_grid must be in [3, 2048]");
   for (int o = 0; o < 2; ++o)
@@ -821,7 +822,9 @@ void adam_gen(sagips_ctx* c, cudaStream_t st) {
   const auto& g = c->cfg;
   c->g_tau += 1;
   launch_adam(c->gW, c->reduced, c->gmW, c->gvW, c->G.nw, g.gen_lr, c->g_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
-  launch_adam(c->gB, c->g_dB, c->gmB, c->gvB, c->G.nb, g.gen_lr, c->g_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
+  // biases: the local gradients, or the reduced ones with the fused packet
+  const float* gb = (g.packet_biases && g.world > 1) ? c->reduced + c->G.nw : c->g_dB;
+  launch_adam(c->gB, gb, c->gmB, c->gvB, c->G.nb, g.gen_lr, c->g_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
 }
 
 // Steps a1..a11: everything up to and including the packet.
@@ -1048,7 +1051,7 @@ static bool tensor_ref(sagips_ctx* c, int32_t which, void** p, size_t* bytes) {
     case SAGIPS_T_GEN_DB: *p = c->g_dB; *bytes = 4 * c->G.nb; return true;
     case SAGIPS_T_DISC_DW: *p = c->d_dW; *bytes = 4 * c->D.nw; return true;
     case SAGIPS_T_DISC_DB: *p = c->d_dB; *bytes = 4 * c->D.nb; return true;
-    case SAGIPS_T_REDUCED: *p = c->reduced; *bytes = 4 * c->G.nw; return true;
+    case SAGIPS_T_REDUCED: *p = c->reduced; *bytes = 4 * (c->G.nw + (c->cfg.packet_biases ? c->G.nb : 0)); return true;
     case SAGIPS_T_STATS: *p = c->stats; *bytes = sizeof(sagips_step_stats); return true;
     case SAGIPS_T_REFERENCE: *p = c->ref; *bytes = 4 * 2 * g.reference_rows; return true;
     case SAGIPS_T_SHARD: *p = c->shard; *bytes = 4 * 2 * g.shard_rows; return true;

@@ -23,7 +23,8 @@ def oracle_config(c):
                       disc_lr=float(np.float32(c.disc_lr)), leaky_slope=float(np.float32(c.leaky_slope)),
                       true_params=[float(x) for x in c.true_params], hist_bins=c.hist_bins,
                       hist_lo=[float(x) for x in c.hist_lo], hist_hi=[float(x) for x in c.hist_hi], seed=c.seed,
-                      sampler=c.sampler, sampler_grid=c.sampler_grid if c.sampler_grid > 0 else 1024)
+                      sampler=c.sampler, sampler_grid=c.sampler_grid if c.sampler_grid > 0 else 1024,
+                      packet_biases=c.packet_biases)
 
 
 def flat(ws):

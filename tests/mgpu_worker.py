@@ -28,13 +28,14 @@ MODES = {"none": 0, "arar": 1, "arar-arar": 2, "rma": 3, "sync": 4, "rma-ag": 5}
 def main():
     mode_name, group, stale, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
     outer = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+    fused = int(sys.argv[6]) if len(sys.argv) > 6 else 0  # packet_biases
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_00051_b200 import _lib as L
     from paper_2407_00051_b200 import runtime
     cfg = L.config_init(L.PRESET_DESK, world=world, rank=rank, mode=MODES[mode_name], group_size=group,
-                        staleness=stale, outer_every=outer, seed=21, exchange_timeout_ms=20000)
+                        staleness=stale, outer_every=outer, seed=21, exchange_timeout_ms=20000, packet_biases=fused)
     ctx = runtime.make_context(cfg)
     runtime.connect(ctx)
     ocfg = oracle_config(cfg)
@@ -58,6 +59,8 @@ def main():
         good, nbad, worst = grad_close(red, R[rank], 1e-3)
         # weights: within 2 lr per step of the oracle (Adam sign flips on tiny grads)
         dw = np.max(np.abs(ctx.get(L.T_GEN_W) - flat(states[rank].gW)))
+        if fused:  # the biases follow the reduced bias gradients
+            dw = max(dw, np.max(np.abs(ctx.get(L.T_GEN_B) - flat(states[rank].gb))))
         if not good or dw > 2.0 * ocfg.gen_lr * (t + 1) + 1e-7:
             print(f"rank {rank} step {t} mode {mode_name}: reduced {nbad} bad (worst {worst:.3g}), |dW| {dw:.3g}",
                   flush=True)

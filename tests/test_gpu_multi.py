@@ -42,3 +42,12 @@ def test_four_gpu_grouping(mode, group, stale, outer):
     if _ngpus() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, mode, group, stale, 6, outer)
+
+
+@pytest.mark.parametrize("mode,group,stale,outer", [("rma", 2, 1, 0), ("sync", 2, 0, 0), ("arar", 2, 0, 0)])
+def test_two_gpu_fused_bias_packet(mode, group, stale, outer):
+    """Tensor fusion: the packet carries the bias
+    gradients too and Adam(G) applies their reduction."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, mode, group, stale, 6, outer, 1)

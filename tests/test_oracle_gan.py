@@ -101,6 +101,23 @@ def test_packet_layout_weights_only():
     assert np.array_equal(out["packet"][:out["dW_g"][0].size], out["dW_g"][0].reshape(-1))
 
 
+def test_fused_packet_carries_the_biases_and_syncs_them():
+    # P:306 tensor fusion: the packet is [weights | biases]; under a
+    # synchronous ring the replicas then agree in the biases too (with the
+    # paper's weights-only packet they diverge through the local bias grads)
+    cfg = tiny_config(packet_biases=1)
+    out = gan.local_step(cfg, gan.RankState(cfg, 0), 0)
+    nw, nb = mlp.count_weights(cfg.gen_sizes()), sum(b.size for b in out["db_g"])
+    assert out["packet"].size == nw + nb
+    np.testing.assert_array_equal(out["packet"][nw:], np.concatenate([b.reshape(-1) for b in out["db_g"]]))
+    for fused in (0, 1):
+        cfgw = tiny_config(world=2, group_size=2, mode=xc.MODE_ARAR, staleness=0, packet_biases=fused)
+        states, _ = gan.run(cfgw, 3)
+        same_b = all(np.array_equal(states[1].gb[l], states[0].gb[l]) for l in range(len(states[0].gb)))
+        assert same_b == bool(fused)
+        assert all(np.array_equal(states[1].gW[l], states[0].gW[l]) for l in range(len(states[0].gW)))
+
+
 def test_step_basic_properties():
     cfg = tiny_config()
     out = gan.local_step(cfg, gan.RankState(cfg, 1), 4)
