@@ -45,6 +45,7 @@ def main():
     p.add_argument("--split-batch", action="store_true", help="Eq. 10: param_samples = 1024 // world")
     p.add_argument("--events-per-sample", type=int, default=100)  # Tab. IV
     p.add_argument("--k-eval", type=int, default=1024, help="noise vectors of the ensemble evaluation")
+    p.add_argument("--sampler", choices=["quadratic", "tabulated"], default="quadratic")
     p.add_argument("--out", default="gpurun_out/ensemble.json")
     a = p.parse_args()
     rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
@@ -67,6 +68,12 @@ def main():
     cfg.staleness = 1 if (world > 1 and a.mode not in ("sync", "none")) else 0
     if a.seed_per_rank:
         cfg.seed = cfg.seed + 7919 * rank
+    if a.sampler == "tabulated":  # R32: true (w, b, c) per observable, histograms on [0, 1]
+        cfg.sampler, cfg.sampler_grid = L.SAMPLER_TABULATED, 1024
+        for j, v in enumerate((0.3, 2.0, 1.2, 0.7, 1.5, 3.0)):
+            cfg.true_params[j] = v
+        for o in range(2):
+            cfg.hist_lo[o], cfg.hist_hi[o] = 0.0, 1.0
     ctx = runtime.make_context(cfg)
     if world > 1 and cfg.mode != L.MODE_NONE:
         runtime.connect(ctx)
@@ -113,7 +120,7 @@ def main():
         train_s += time.perf_counter() - t0
         checkpoint(t)
     if rank == 0:
-        out = {"mode": a.mode, "world": world, "group_size": cfg.group_size, "split_batch": a.split_batch,
+        out = {"mode": a.mode, "sampler": a.sampler, "world": world, "group_size": cfg.group_size, "split_batch": a.split_batch,
                "param_samples": k, "events_per_sample": a.events_per_sample, "k_eval": k_eval,
                "seed_per_rank": a.seed_per_rank, "steps": a.steps, "every": a.every, "p_star": p_star.tolist(),
                "train_s": train_s, "records": rec}
