@@ -374,6 +374,45 @@ def ours_arm(args):
                        "copied from pinned host memory (a data loader's buffers, replacing the device RNG "
                        "noise and the resident-shard bootstrap), the stats record copied back and waited for"}
 
+    # exchange alone (a12, BJ north star: "exchange GB/s against NVLink
+    # bandwidth"): local step (LOCAL_ONLY), device + host barrier, then
+    # CUDA events around push + pull (+ Adam(G), 51 k params, ~2 us).  The
+    # rank that launches last finds its peers' packets already published,
+    # so the min over ranks is the exchange's own latency; the max adds the
+    # host launch skew after the barrier.  A device-side spin ahead of the
+    # first event keeps host launch latency out of the interval.
+    xch = None
+    if world > 1 and args.mode != "none":
+        pkt = ctx.tensor_bytes(L.T_REDUCED)  # the packet as exchanged (weights; + biases when fused)
+        g = cfg.group_size
+        bytes_in = (2 * (g - 1) / g if args.mode == "sync" else (g - 1)) * pkt
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(20):
+            ctx.train_step(step, L.STEP_LOCAL_ONLY, sp)
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda._sleep(200_000)  # ~0.1 ms of device work so the host's launches run ahead, as in a step
+            a_ev.record(stream)
+            ctx.push_generator_grad(step, sp)
+            ctx.pull_generator_grad(step, sp)
+            b_ev.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a_ev.elapsed_time(b_ev))
+            step += 1
+        med = sorted(ts)[len(ts) // 2]
+        t = torch.tensor([med, -med], device="cuda")
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_max, t_min = float(t[0].item()), -float(t[1].item())
+        nv = 770.0  # B200_PROFILING.md: measured peer copy, GB/s per direction
+        xch = {"bound": "nvlink-latency", "packet_bytes": pkt, "group_size": g,
+               "bytes_in_per_rank_per_step": bytes_in, "us_min_over_ranks": t_min * 1e3,
+               "us_max_over_ranks": t_max * 1e3, "achieved": bytes_in / (t_min * 1e-3) / 1e9,
+               "peak": nv, "unit": "GB/s", "frac": bytes_in / (t_min * 1e-3) / 1e9 / nv,
+               "peak_src": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
+               "what": "push + pull (wait, forward, fold) + Adam(G) after a barrier, median of 20 per rank"}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -431,7 +470,7 @@ def ours_arm(args):
             "clocks": clk, "gpu_launches": launches, "phases_ms": phases, "phase_steps_averaged": nph,
             "roofline": roof, "kernels": kernels, "roofline_sampler": roof_sampler,
             "roofline_sampler_2p24": roof_sampler_24,
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "e2e": e2e, "exchange": xch,
             "loss_d": stats.loss_d, "loss_g": stats.loss_g}
     print(json.dumps(line), flush=True)
     if dist is not None:

@@ -132,7 +132,11 @@ void launch_gen_predict(sagips_ctx* c, const float* noise, int k, float* c_out, 
 void launch_gen_bwd(sagips_ctx* c, cudaStream_t st);
 // exchange.cu
 sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st);
-sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st);
+// adam (optional): when exchange_fuses_adam(c, step), pull runs the wait,
+// the fold and Adam(G) in one kernel with these operands
+sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const GenAdam* adam = nullptr);
+bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step);
+GenAdam gen_adam_args(sagips_ctx* c);
 sagips_status exchange_check(sagips_ctx* c);
 void exchange_destroy(sagips_ctx* c);
 }  // namespace sagips

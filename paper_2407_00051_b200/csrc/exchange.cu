@@ -63,6 +63,7 @@ struct ExchangeState {
   uint64_t ring_step[2] = {0, 0};
   // device error word and wait accounting
   unsigned int* err = nullptr;      // device: 1 timeout, 2 protocol
+  unsigned int* ticket = nullptr;   // device [kMaxWorld]: k_push's last-CTA counters (self-resetting)
   uint32_t* one = nullptr;          // device constant 1 (stats.outer_fired)
 };
 
@@ -118,32 +119,40 @@ __device__ void block_copy(float* __restrict__ dst, const float* __restrict__ sr
   for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-// push: own packet -> successor's slot (origin = me), then release the tag.
-// A single CTA: the copy is ~200 KB, latency-bound over NVLink.
-__global__ void __launch_bounds__(1024) k_push(const float* __restrict__ packet, int64_t n, float* dst_slot,
-                                               unsigned long long* dst_flag, unsigned long long tag) {
-  block_copy(dst_slot, packet, n);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    st_release_sys(dst_flag, tag);
-  }
-}
-
-// push, one-hop all-gather (SAGIPS_MODE_RMA_ALLGATHER): CTA q stores the own
-// packet into destination q's slot (origin = me) and releases its tag; over
-// NVSwitch every member is one hop away, so there is no forwarding agent.
+// push: the own packet -> destination y's slot (origin = me), then release
+// its tag.  y = blockIdx.y: the successor (pass-along ring) or every other
+// member (one-hop all-gather, SAGIPS_MODE_RMA_ALLGATHER: over NVSwitch every
+// member is one hop away, so there is no forwarding agent).  kPushCtas CTAs
+// per destination each store one contiguous chunk (measured, torch.profiler
+// at N = 2: 14.7 us with one CTA, ~10 us with 8-148 CTAs -- a ~9 us floor
+// that remains without the fences, so not the store bandwidth).
+// The last CTA to finish (ticket counter, reset by it) publishes the tag:
+// every CTA fences its stores before taking a ticket, the last fences again
+// before the release store.
+constexpr int kPushCtas = 32;
 struct PushAllArgs {
   float* dst[kMaxWorld];
   unsigned long long* dst_flag[kMaxWorld];
 };
-__global__ void __launch_bounds__(1024) k_push_all(const float* __restrict__ packet, int64_t n, PushAllArgs a,
-                                                   unsigned long long tag) {
-  block_copy(a.dst[blockIdx.x], packet, n);
+__global__ void __launch_bounds__(256) k_push(const float* __restrict__ packet, int64_t n, PushAllArgs a,
+                                              unsigned long long tag, unsigned int* ticket) {
+  const int y = blockIdx.y;
+  float* dst = a.dst[y];
+  const int64_t n4 = n / 4, per = (n4 + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = min(n4, b0 + per);
+  const float4* s4 = reinterpret_cast<const float4*>(packet);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) d4[i] = s4[i];
+  if (blockIdx.x == gridDim.x - 1)
+    for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = packet[i];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    st_release_sys(a.dst_flag[blockIdx.x], tag);
+    if (atomicAdd(&ticket[y], 1u) == gridDim.x - 1) {
+      ticket[y] = 0;
+      __threadfence_system();
+      st_release_sys(a.dst_flag[y], tag);
+    }
   }
 }
 
@@ -187,6 +196,64 @@ __global__ void k_wait(WaitArgs a, unsigned long long timeout_ns, unsigned int* 
     if (ld_acquire_sys(a.flag[i]) != a.want[i]) atomicExch(err, 2u);  // a newer packet overwrote the slot
   }
   *wait_ns = globaltimer() - t0;
+}
+
+// pull, fused (exchange_fuses_adam): k_wait, k_fold and Adam(G) in one
+// launch.  Every CTA's thread 0 waits for the tags as k_wait does (CTA 0
+// records the wait and clears stats.outer_fired), then per element: the
+// ascending fold of k_fold, reduced[i] = (sum_j p_j[i]) / divisor for
+// i < pw (loads through L2: the slots were written by peers), and the Adam
+// update of adam_elem, as k_adam -- weights from reduced[i], biases from
+// reduced[nw + j] (fused packet) or the local gradient.
+struct FoldAdamArgs {
+  PacketList pl;
+  WaitArgs w;
+  float* reduced;
+  int64_t pw;
+  float divisor;
+  GenAdam a;
+  uint32_t* outer_fired;
+  unsigned long long* wait_ns;
+};
+__global__ void __launch_bounds__(256) k_wait_fold_adam(const __grid_constant__ FoldAdamArgs f,
+                                                        unsigned long long timeout_ns, unsigned int* err) {
+  if (threadIdx.x == 0) {
+    const unsigned long long t0 = globaltimer();
+    for (int i = 0; i < f.w.count; ++i) {
+      if (!wait_tag(f.w.flag[i], f.w.want[i], timeout_ns, err)) break;
+      if (ld_acquire_sys(f.w.flag[i]) != f.w.want[i]) atomicExch(err, 2u);
+    }
+    if (blockIdx.x == 0) {
+      *f.wait_ns = globaltimer() - t0;
+      *f.outer_fired = 0u;
+    }
+  }
+  __syncthreads();
+  const GenAdam& a = f.a;
+  const int64_t n = a.nw + a.nb;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float gi = 0.f;
+    if (i < f.pw) {
+      float acc = __ldcg(f.pl.p[0] + i);
+      for (int j = 1; j < f.pl.count; ++j) acc += __ldcg(f.pl.p[j] + i);
+      gi = acc / f.divisor;
+      f.reduced[i] = gi;
+    }
+    if (i < a.nw) {
+      float p = a.pw[i], m = a.mw[i], v = a.vw[i];
+      adam_elem(p, gi, m, v, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+      a.pw[i] = p;
+      a.mw[i] = m;
+      a.vw[i] = v;
+    } else {
+      const int64_t j = i - a.nw;
+      float p = a.pb[j], m = a.mb[j], v = a.vb[j];
+      adam_elem(p, a.gb_local ? a.gb_local[j] : gi, m, v, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+      a.pb[j] = p;
+      a.mb[j] = m;
+      a.vb[j] = v;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -238,6 +305,8 @@ static sagips_status ensure_state(sagips_ctx* c) {
   }
   XCK(cudaMalloc(&x->err, sizeof(unsigned int)));
   XCK(cudaMemset(x->err, 0, sizeof(unsigned int)));
+  XCK(cudaMalloc(&x->ticket, sizeof(unsigned int) * kMaxWorld));
+  XCK(cudaMemset(x->ticket, 0, sizeof(unsigned int) * kMaxWorld));
   if (g.world > 1 && g.mode != SAGIPS_MODE_NONE) {
     const size_t ps = slot_stride(c);
     XCK(cudaMalloc(&x->gather[0], sizeof(float) * ps * gs));
@@ -279,6 +348,7 @@ void exchange_destroy(sagips_ctx* c) {
   cudaFree(x->outer_buf);
   if (x->one) cudaFree(x->one);
   cudaFree(x->err);
+  cudaFree(x->ticket);
   for (int i = 0; i < 2; ++i) {
     if (x->ev_ready[i]) cudaEventDestroy(x->ev_ready[i]);
     if (x->ev_done[i]) cudaEventDestroy(x->ev_done[i]);
@@ -319,20 +389,22 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   if (one_sided(c)) {
     if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
     char* sb = x->peer_base[x->succ];
+    PushAllArgs pa{};
+    int ndst = 1;
     if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) {
-      PushAllArgs pa{};
-      for (int j = 1; j < x->g; ++j) {  // destinations pos+1, pos+2, ... (one CTA each)
+      ndst = x->g - 1;
+      for (int j = 1; j < x->g; ++j) {  // destinations pos+1, pos+2, ...
         char* db = x->peer_base[x->first + (x->pos + j) % x->g];
         pa.dst[j - 1] = slot_ptr(db, c, g.rank, step);
         pa.dst_flag[j - 1] = &flags_ptr(db, c)->tag[g.rank][step % kVersions];
       }
-      k_push_all<<<x->g - 1, 1024, 0, st>>>(c->g_dW, (int64_t)pw, pa, step + 1);
-      count_launch();
-      return SAGIPS_OK;
+    } else {
+      pa.dst[0] = slot_ptr(sb, c, g.rank, step);
+      pa.dst_flag[0] = &flags_ptr(sb, c)->tag[g.rank][step % kVersions];
     }
-    k_push<<<1, 1024, 0, st>>>(c->g_dW, (int64_t)pw, slot_ptr(sb, c, g.rank, step),
-                               &flags_ptr(sb, c)->tag[g.rank][step % kVersions], step + 1);
+    k_push<<<dim3(kPushCtas, ndst), 256, 0, st>>>(c->g_dW, (int64_t)pw, pa, step + 1, x->ticket);
     count_launch();
+    if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) return SAGIPS_OK;
     if (x->g > 2) {
       // the agent forwards origins pos-1 .. pos-(g-2) of this version
       XCK(cudaEventRecord(x->ev_ready[step & 1], st));
@@ -365,13 +437,20 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   return SAGIPS_OK;
 }
 
+// the leaders' outer ring runs after step `step`'s inner fold on this rank
+static bool outer_fires(const sagips_ctx* c, uint64_t step) {
+  const auto& g = c->cfg;
+  const int nlead = g.world / g.group_size;
+  if (g.mode == SAGIPS_MODE_ARAR || nlead < 2 || g.outer_every <= 0) return false;
+  if ((step + 1) % (uint64_t)g.outer_every != 0) return false;
+  return g.rank % g.group_size == 0;  // leaders only
+}
+
 static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   ExchangeState* x = c->xs;
   const auto& g = c->cfg;
   const int nlead = g.world / g.group_size;
-  if (g.mode == SAGIPS_MODE_ARAR || nlead < 2 || g.outer_every <= 0) return SAGIPS_OK;
-  if ((step + 1) % (uint64_t)g.outer_every != 0) return SAGIPS_OK;
-  if (g.rank % g.group_size != 0) return SAGIPS_OK;  // leaders only
+  if (!outer_fires(c, step)) return SAGIPS_OK;
   if (!x->comm_main) { c->err = "sagips_connect_nccl not called (outer ring)"; return SAGIPS_ERR_STATE; }
   const size_t pw = slot_floats(c);
   const int lp = g.rank / g.group_size;
@@ -393,10 +472,22 @@ static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   return SAGIPS_OK;
 }
 
-sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st) {
+// pull(t) can run as one k_wait_fold_adam: one-sided, a group of >= 2 whose
+// packets of version t - s exist, and no outer ring after the fold
+bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step) {
+  const auto& g = c->cfg;
+  return g.world > 1 && one_sided(c) && c->xs && c->xs->g > 1 && c->xs->peers_ok &&
+         (int64_t)step - g.staleness >= 0 && !outer_fires(c, step);
+}
+
+sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const GenAdam* adam) {
   const auto& g = c->cfg;
   const size_t pw = slot_floats(c);
-  XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
+  if (adam && !exchange_fuses_adam(c, step)) {
+    c->err = "exchange_pull: fused Adam(G) requested where it does not apply";
+    return SAGIPS_ERR_STATE;
+  }
+  if (!adam) XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) {
     XCK(cudaMemcpyAsync(c->reduced, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
     return SAGIPS_OK;
@@ -430,8 +521,29 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st) {
         w.flag[j - 1] = &flags_ptr(own, c)->tag[o][stale % kVersions];
         w.want[j - 1] = (unsigned long long)stale + 1;
       }
-      k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), x->err, reinterpret_cast<unsigned long long*>(&c->stats->wait_ns));
-      count_launch();
+      if (!adam) {
+        k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), x->err, reinterpret_cast<unsigned long long*>(&c->stats->wait_ns));
+        count_launch();
+      } else {
+        FoldAdamArgs f{};
+        f.w = w;
+        f.pl.count = x->g;
+        for (int i = 0; i < x->g; ++i) {
+          const int o = x->first + i;
+          f.pl.p[i] = (o == g.rank) ? c->g_dW : slot_ptr(own, c, o, stale);
+        }
+        f.reduced = c->reduced;
+        f.pw = (int64_t)pw;
+        f.divisor = g.reduce_mean ? (float)x->g : 1.0f;
+        f.a = *adam;
+        f.outer_fired = &c->stats->outer_fired;
+        f.wait_ns = reinterpret_cast<unsigned long long*>(&c->stats->wait_ns);
+        const int64_t n = adam->nw + adam->nb;
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);
+        k_wait_fold_adam<<<blocks, 256, 0, st>>>(f, timeout_ns(c), x->err);
+        count_launch();
+        return SAGIPS_OK;
+      }
     }
     for (int i = 0; i < x->g; ++i) {
       const int o = x->first + i;

@@ -34,6 +34,27 @@ int launch_ensemble_stats(const float* preds, int M, int k, int P, const double*
 
 struct Coef6 { float v[6]; };
 
+// One Adam element (PyTorch form, R7): every Adam kernel uses this, so the
+// fused exchange-fold + Adam(G) of exchange.cu is bitwise the same update.
+__device__ __forceinline__ void adam_elem(float& p, float gi, float& m, float& v, float step_size, float bc2_sqrt,
+                                          float b1, float b2, float eps) {
+  const float mi = b1 * m + (1.f - b1) * gi;
+  const float vi = b2 * v + (1.f - b2) * gi * gi;
+  m = mi;
+  v = vi;
+  const float denom = sqrtf(vi) / bc2_sqrt + eps;
+  p -= step_size * (mi / denom);
+}
+
+// Adam(G) operands of one step (sagips.cu gen_adam_args; advances tau)
+struct GenAdam {
+  float *pw, *mw, *vw;    // weights [nw]
+  float *pb, *mb, *vb;    // biases [nb]
+  const float* gb_local;  // local bias gradients (weights-only packet), else nullptr: biases are in the packet
+  int64_t nw, nb;
+  float step_size, bc2_sqrt, b1, b2, eps;
+};
+
 enum EpiKind { EPI_STORE = 0, EPI_BIAS_ACT = 1, EPI_ACT_GRAD = 2 };
 struct Epi {
   int kind;

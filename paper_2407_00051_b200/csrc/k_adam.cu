@@ -11,13 +11,11 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
                        float* __restrict__ v, int64_t n, float step_size, float bc2_sqrt, float b1, float b2,
                        float eps) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
-    const float mi = b1 * m[i] + (1.f - b1) * gi;
-    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    float pi = p[i], mi = m[i], vi = v[i];
+    adam_elem(pi, g[i], mi, vi, step_size, bc2_sqrt, b1, b2, eps);
+    p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    const float denom = sqrtf(vi) / bc2_sqrt + eps;
-    p[i] -= step_size * (mi / denom);
   }
 }
 
@@ -57,12 +55,11 @@ __global__ void __launch_bounds__(256) k_reduce_adam(const __grid_constant__ Red
     for (int k = 0; k < 8; ++k) gi += red[k][jl];
     sg.g[j] = gi;
     if (a.adam) {
-      const float mi = a.b1 * sg.m[j] + (1.f - a.b1) * gi;
-      const float vi = a.b2 * sg.v[j] + (1.f - a.b2) * gi * gi;
-      sg.m[j] = mi;
-      sg.v[j] = vi;
-      const float denom = sqrtf(vi) / a.bc2_sqrt + a.eps;
-      sg.p[j] -= a.step_size * (mi / denom);
+      float pj = sg.p[j], mj = sg.m[j], vj = sg.v[j];
+      adam_elem(pj, gi, mj, vj, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+      sg.p[j] = pj;
+      sg.m[j] = mj;
+      sg.v[j] = vj;
     }
   }
 }

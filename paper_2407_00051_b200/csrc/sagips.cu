@@ -818,6 +818,26 @@ static void adam_disc(sagips_ctx* c, cudaStream_t st) {
   launch_adam(c->dB, c->d_dB, c->dmB, c->dvB, c->D.nb, g.disc_lr, c->d_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
 }
 
+GenAdam gen_adam_args(sagips_ctx* c) {
+  const auto& g = c->cfg;
+  c->g_tau += 1;
+  // bias corrections in double on the host, as launch_adam
+  const double bc1 = 1.0 - std::pow((double)g.adam_beta1, (double)c->g_tau);
+  const double bc2 = 1.0 - std::pow((double)g.adam_beta2, (double)c->g_tau);
+  GenAdam a{};
+  a.pw = c->gW; a.mw = c->gmW; a.vw = c->gvW;
+  a.pb = c->gB; a.mb = c->gmB; a.vb = c->gvB;
+  a.gb_local = (g.packet_biases && g.world > 1) ? nullptr : c->g_dB;
+  a.nw = c->G.nw;
+  a.nb = c->G.nb;
+  a.step_size = (float)((double)g.gen_lr / bc1);
+  a.bc2_sqrt = (float)std::sqrt(bc2);
+  a.b1 = g.adam_beta1;
+  a.b2 = g.adam_beta2;
+  a.eps = g.adam_eps;
+  return a;
+}
+
 void adam_gen(sagips_ctx* c, cudaStream_t st) {
   const auto& g = c->cfg;
   c->g_tau += 1;
@@ -970,12 +990,19 @@ sagips_status sagips_pull_generator_grad(sagips_ctx* ctx, uint64_t step, void* s
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
   if (!ctx->pushed || ctx->local_done_step != step) return fail(ctx, SAGIPS_ERR_STATE, "pull before push");
   cudaStream_t st = (cudaStream_t)stream;
-  sagips_status s = exchange_pull(ctx, step, st);
-  if (s != SAGIPS_OK) return s;
-  if (ctx->skip_adam_once) {
-    ctx->skip_adam_once = false;
+  if (!ctx->skip_adam_once && exchange_fuses_adam(ctx, step)) {
+    // wait + fold + Adam(G) in one kernel (the same arithmetic as below)
+    const GenAdam ga = gen_adam_args(ctx);
+    sagips_status s = exchange_pull(ctx, step, st, &ga);
+    if (s != SAGIPS_OK) return s;
   } else {
-    adam_gen(ctx, st);
+    sagips_status s = exchange_pull(ctx, step, st);
+    if (s != SAGIPS_OK) return s;
+    if (ctx->skip_adam_once) {
+      ctx->skip_adam_once = false;
+    } else {
+      adam_gen(ctx, st);
+    }
   }
   mark(ctx, 7, st);
   if (ctx->cfg.phase_timing) ctx->timed_steps++;

@@ -16,4 +16,4 @@ for n in 2 4 8; do
 done
 cat gpurun_out/pytest_multi.log
 for f in gpurun_out/bench_n*.log; do python -c "
-import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['n_gpus'], round(d['ms_per_step'],3), round(d['value']/1e6,1), 'Mev/s', d['config'].get('workload')[-40:], {k: round(v,3) for k,v in d['phases_ms'].items() if k in ('disc_step','exchange_adam_g')})"; done
+import json; d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', d['n_gpus'], round(d['ms_per_step'],3), round(d['value']/1e6,1), 'Mev/s', d['config'].get('workload')[-40:], {k: round(v,3) for k,v in d['phases_ms'].items() if k in ('disc_step','exchange_adam_g')}, {k: round(v,2) for k,v in (d.get('exchange') or {}).items() if k in ('us_min_over_ranks','us_max_over_ranks','achieved')})"; done
