@@ -24,10 +24,13 @@ it):
  10  exchange -> R (oracle/exchange.py)
  11  Adam(G) with W-grad R and the local bias grads
 
-PARITY UNPINNED for the multi-step trajectory: there is no closed form for
-a GAN's training path.  Each ingredient is pinned separately (tests/
-test_oracle_*.py), a full single step is pinned by finite differences of
-both losses, and the exchange by the ring invariants.
+The multi-step trajectory has no closed form; at N=1 it is pinned against
+the same loop written with PyTorch autograd + torch.optim.Adam (tests/
+test_oracle_gan.py::test_trajectory_matches_torch_autograd_and_adam).  Each
+ingredient is pinned separately (tests/test_oracle_*.py), a full single step
+by finite differences of both losses, and the exchange by the ring
+invariants; the multi-rank trajectory (N>1) stays PARITY UNPINNED beyond
+those per-step pins.
 """
 from dataclasses import dataclass, field
 from typing import List
