@@ -208,3 +208,73 @@ def test_trajectory_matches_torch_autograd_and_adam():
         assert np.allclose(a.detach().numpy(), b, rtol=1e-9, atol=1e-12)
     # the loop moved the parameters (the pin is not vacuous)
     assert max(np.abs(a - b).max() for a, b in zip(st.gW, init.gW)) > 1e-3
+
+
+@pytest.mark.parametrize("mode,staleness", [(xc.MODE_SYNC_ALLREDUCE, 0), (xc.MODE_ARAR, 0),
+                                            (xc.MODE_RMA_ARAR_ARAR, 1)])
+def test_two_rank_trajectory_matches_torch_loop(mode, staleness):
+    """Multi-rank pin: two ranks, each its own
+    D and shard; after every step rank r's generator weight gradient is
+    replaced by (g_r(t) + sum_{o != r} g_o(t - s)) / 2 -- s = 0: the ring's
+    fold equals the all-reduce up to summation order; s = 1: the RMA ring's
+    one-step-stale peer packets, zero before step 0 -- biases keep their
+    local gradients; written with PyTorch autograd + torch.optim.Adam."""
+    W = 2
+    cfg = tiny_config(seed=6, gen_lr=1e-2, disc_lr=1e-2, world=W, mode=mode,
+                      group_size=W, staleness=staleness)
+    states = [gan.RankState(cfg, r) for r in range(W)]
+    init = copy.deepcopy(states)
+    T = 4
+    _, log = gan.run(cfg, T, states=states)
+    N, m = cfg.n_events, cfg.events_per_sample
+    s = torch.arange(N) // m
+    lab = torch.cat([torch.ones(N, dtype=torch.float64), torch.zeros(N, dtype=torch.float64)])
+    P = []
+    for r in range(W):
+        gW = [torch.tensor(w, requires_grad=True) for w in init[r].gW]
+        gb = [torch.tensor(b, requires_grad=True) for b in init[r].gb]
+        dW = [torch.tensor(w, requires_grad=True) for w in init[r].dW]
+        db = [torch.tensor(b, requires_grad=True) for b in init[r].db]
+        P.append(dict(gW=gW, gb=gb, dW=dW, db=db,
+                      optG=torch.optim.Adam(gW + gb, lr=cfg.gen_lr, eps=1e-8),
+                      optD=torch.optim.Adam(dW + db, lr=cfg.disc_lr, eps=1e-8)))
+    hist = {}
+    for t in range(T):
+        for r, p in enumerate(P):
+            z = torch.tensor(gan.noise(cfg, t, r))
+            u = torch.tensor(proxy.fake_uniforms(cfg.seed, t, r, N))
+            x = torch.tensor(init[r].shard[proxy.real_indices(cfg.seed, t, r, cfg.shard_rows, N)])
+            raw = _torch_mlp(p["gW"], p["gb"], z).reshape(-1, 2, 3)
+            c0 = raw[:, :, 0]
+            c1 = F.softplus(raw[:, :, 1], beta=1, threshold=20)
+            c2 = F.softplus(raw[:, :, 2], beta=1, threshold=20)
+            y = c0[s] + c1[s] * u + c2[s] * u * u
+            p["optD"].zero_grad()
+            ld = F.binary_cross_entropy_with_logits(
+                _torch_mlp(p["dW"], p["db"], torch.cat([x, y.detach()]))[:, 0], lab)
+            ld.backward()
+            p["optD"].step()
+            p["optG"].zero_grad()
+            lg = F.binary_cross_entropy_with_logits(
+                _torch_mlp(p["dW"], p["db"], y)[:, 0], torch.ones(N, dtype=torch.float64))
+            lg.backward()
+            assert ld.item() == pytest.approx(log[t]["loss_d"][r], rel=1e-10)
+            assert lg.item() == pytest.approx(log[t]["loss_g"][r], rel=1e-10)
+        hist[t] = [[g.grad.clone() for g in p["gW"]] for p in P]
+        for l in range(len(P[0]["gW"])):
+            for r, p in enumerate(P):
+                tot = hist[t][r][l].clone()
+                for o in range(W):
+                    if o != r and t - staleness >= 0:
+                        tot = tot + hist[t - staleness][o][l]
+                p["gW"][l].grad = tot / W
+        for p in P:
+            p["optG"].step()
+    for r, p in enumerate(P):
+        for a, b in zip(p["gW"] + p["gb"] + p["dW"] + p["db"],
+                        states[r].gW + states[r].gb + states[r].dW + states[r].db):
+            assert np.allclose(a.detach().numpy(), b, rtol=1e-9, atol=1e-12)
+    # replicas share G weights iff the exchange is synchronous; D's differ
+    same = all(np.array_equal(a, b) for a, b in zip(states[0].gW, states[1].gW))
+    assert same == (staleness == 0)
+    assert not np.allclose(states[0].dW[0], states[1].dW[0])
