@@ -34,9 +34,7 @@ Modules
 
 Every function here is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against something other than itself (published
-known-answer vectors, closed forms, brute force, finite differences).  The
-one result with no external pin -- the grouped multi-rank training
-trajectory (N=1 and two-rank trajectories are pinned against
-torch.optim.Adam loops) -- is marked "parity unpinned" in ``gan.py`` and in
-DESIGN.md.
+known-answer vectors, closed forms, brute force, finite differences); the
+training trajectories (N=1 and multi-rank, every exchange mode) are pinned
+against the same loop written with PyTorch autograd + torch.optim.Adam.
 """

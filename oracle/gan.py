@@ -29,9 +29,9 @@ the same loop written with PyTorch autograd + torch.optim.Adam (tests/
 test_oracle_gan.py::test_trajectory_matches_torch_autograd_and_adam).  Each
 ingredient is pinned separately (tests/test_oracle_*.py), a full single step
 by finite differences of both losses, and the exchange by the ring
-invariants; two-rank trajectories (sync, ARAR, stale RMA) are pinned the
-same way; the grouped trajectory (inner groups + outer ring) stays PARITY
-UNPINNED beyond those per-step pins.
+invariants; multi-rank trajectories (sync, ARAR, stale RMA, grouped with
+the outer leader ring) are pinned the same way (test_multi_rank_trajectory_
+matches_torch_loop).
 """
 from dataclasses import dataclass, field
 from typing import List

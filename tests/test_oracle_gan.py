@@ -210,18 +210,28 @@ def test_trajectory_matches_torch_autograd_and_adam():
     assert max(np.abs(a - b).max() for a, b in zip(st.gW, init.gW)) > 1e-3
 
 
-@pytest.mark.parametrize("mode,staleness", [(xc.MODE_SYNC_ALLREDUCE, 0), (xc.MODE_ARAR, 0),
-                                            (xc.MODE_RMA_ARAR_ARAR, 1)])
-def test_two_rank_trajectory_matches_torch_loop(mode, staleness):
+@pytest.mark.parametrize("mode,staleness,W,gs,h", [(xc.MODE_SYNC_ALLREDUCE, 0, 2, 2, 0),
+                                                   (xc.MODE_ARAR, 0, 2, 2, 0),
+                                                   (xc.MODE_RMA_ARAR_ARAR, 1, 2, 2, 0),
+                                                   (xc.MODE_RMA_ARAR_ARAR, 1, 4, 2, 2),
+                                                   (xc.MODE_ARAR_ARAR, 0, 5, 2, 3)])
+def test_multi_rank_trajectory_matches_torch_loop(mode, staleness, W, gs, h):
     """Multi-rank pin: two ranks, each its own
     D and shard; after every step rank r's generator weight gradient is
     replaced by (g_r(t) + sum_{o != r} g_o(t - s)) / 2 -- s = 0: the ring's
     fold equals the all-reduce up to summation order; s = 1: the RMA ring's
     one-step-stale peer packets, zero before step 0 -- biases keep their
-    local gradients; written with PyTorch autograd + torch.optim.Adam."""
-    W = 2
+    local gradients; written with PyTorch autograd + torch.optim.Adam.
+    Grouped cases: inner groups of gs contiguous ranks (the last
+    may be smaller) average within the group; at the end of step t with
+    (t + 1) mod h == 0 the group leaders (first rank of each group) replace
+    theirs by the mean of the leaders' inner results."""
     cfg = tiny_config(seed=6, gen_lr=1e-2, disc_lr=1e-2, world=W, mode=mode,
-                      group_size=W, staleness=staleness)
+                      group_size=gs, staleness=staleness, outer_every=h)
+    if mode == xc.MODE_SYNC_ALLREDUCE or mode == xc.MODE_ARAR:
+        gs, h = W, 0
+    groups = [list(range(a, min(a + gs, W))) for a in range(0, W, gs)]
+    leaders = [g[0] for g in groups]
     states = [gan.RankState(cfg, r) for r in range(W)]
     init = copy.deepcopy(states)
     T = 4
@@ -262,19 +272,28 @@ def test_two_rank_trajectory_matches_torch_loop(mode, staleness):
             assert lg.item() == pytest.approx(log[t]["loss_g"][r], rel=1e-10)
         hist[t] = [[g.grad.clone() for g in p["gW"]] for p in P]
         for l in range(len(P[0]["gW"])):
+            R = {}
+            for g in groups:
+                for r in g:
+                    tot = hist[t][r][l].clone()
+                    for o in g:
+                        if o != r and t - staleness >= 0:
+                            tot = tot + hist[t - staleness][o][l]
+                    R[r] = tot / len(g)
+            if h > 0 and (t + 1) % h == 0 and len(leaders) > 1:
+                outer = sum(R[q] for q in leaders) / len(leaders)
+                for q in leaders:
+                    R[q] = outer
             for r, p in enumerate(P):
-                tot = hist[t][r][l].clone()
-                for o in range(W):
-                    if o != r and t - staleness >= 0:
-                        tot = tot + hist[t - staleness][o][l]
-                p["gW"][l].grad = tot / W
+                p["gW"][l].grad = R[r]
         for p in P:
             p["optG"].step()
     for r, p in enumerate(P):
         for a, b in zip(p["gW"] + p["gb"] + p["dW"] + p["db"],
                         states[r].gW + states[r].gb + states[r].dW + states[r].db):
             assert np.allclose(a.detach().numpy(), b, rtol=1e-9, atol=1e-12)
-    # replicas share G weights iff the exchange is synchronous; D's differ
+    # ranks 0 and 1 (one group) share G weights iff the exchange is
+    # synchronous and no outer step has given the leader a different R
     same = all(np.array_equal(a, b) for a, b in zip(states[0].gW, states[1].gW))
-    assert same == (staleness == 0)
+    assert same == (staleness == 0 and (h == 0 or len(leaders) == 1))
     assert not np.allclose(states[0].dW[0], states[1].dW[0])
