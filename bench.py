@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--sampler-grid", type=int, default=1024)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--nccl-algo", default="",
+                   help="NCCL_ALGO for the library's own communicators only (set after torch's "
+                        "process group exists), e.g. NVLS / Ring / Tree for --mode sync")
     return p.parse_args()
 
 
@@ -144,6 +147,8 @@ def lib_config(args, L, rank, world):
         workload += f", tabulated-CDF sampler G={args.sampler_grid} (R32)"
     if world > 1:
         workload = workload.replace("C2:", "C3:") + f", {args.mode} ring g={cfg.group_size} s={cfg.staleness}"
+        if args.nccl_algo:
+            workload += f", NCCL_ALGO={args.nccl_algo}"
     return cfg, workload
 
 
@@ -296,6 +301,8 @@ def ours_arm(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.nccl_algo:  # torch's communicator is already initialised: only the library's see it
+            os.environ["NCCL_ALGO"] = args.nccl_algo
     from paper_2407_00051_b200 import _lib as L
     from paper_2407_00051_b200 import runtime
     cfg, workload = lib_config(args, L, rank, world)

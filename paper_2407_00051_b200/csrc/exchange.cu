@@ -166,7 +166,13 @@ struct FwdArgs {
 
 // forwarding agent: for hop j, wait for the packet of origin pos-j in the own
 // window, then pass it to the successor (Alg. 1's "send to rank i+1").
-__global__ void __launch_bounds__(1024) k_forward(FwdArgs a, int64_t n, unsigned long long tag,
+// Register budget: at most 32 per thread (min 2 blocks/SM), so the agent's
+// 1024 threads fit on an SM beside the spinning CTAs of k_wait_fold_adam.
+// With 64 (the 1024-thread cap) it needed a whole SM's register file; at
+// g >= 3, staleness 0 and C2 sizes the fused pull puts a CTA on every SM and
+// waits for packets that the peers' starved agents never forward (measured:
+// exchange wait timeout at N = 4).
+__global__ void __launch_bounds__(1024, 2) k_forward(FwdArgs a, int64_t n, unsigned long long tag,
                                                   unsigned long long timeout_ns, unsigned int* err) {
   __shared__ int ok;
   for (int j = 0; j < a.hops; ++j) {

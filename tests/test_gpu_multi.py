@@ -51,3 +51,18 @@ def test_two_gpu_fused_bias_packet(mode, group, stale, outer):
     if _ngpus() < 2:
         pytest.skip("needs 2 GPUs")
     _run(2, mode, group, stale, 6, outer, 1)
+
+
+def test_four_gpu_paper_size_staleness0_ring_completes():
+    """Regression: at C2 sizes the fused pull (k_wait_fold_adam) puts a
+    spinning CTA on every SM; the one-sided ring's forwarding agent must
+    still fit beside them at g = 4, staleness 0 (it once needed a whole SM's
+    register file and the ring timed out)."""
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+           "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "bench.py"),
+           "--gpus", "4", "--mode", "rma", "--staleness", "0", "--steps", "10", "--warmup", "3",
+           "--no-cpu-baseline", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and '"n_gpus": 4' in r.stdout, (r.stdout + r.stderr)[-4000:]
