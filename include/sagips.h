@@ -69,7 +69,10 @@ typedef enum {
 } sagips_mode;
 
 typedef enum {
-  SAGIPS_PREC_FP32 = 0,  /* every GEMM in fp32 (R20) */
+  SAGIPS_PREC_FP32 = 0,  /* fp32-class (R20, R28): CUDA-core layers in fp32; the 128 -> 128
+                            discriminator GEMMs on tcgen05 with bf16-split operands x = hi + lo,
+                            fp32 accumulation -- forward/dgrad hi*hi + hi*lo + lo*hi (bf16x3),
+                            wgrad G_hi*H_hi + G_lo*H_hi (bf16x2); everything else fp32 */
   SAGIPS_PREC_BF16 = 1   /* discriminator GEMMs bf16 x bf16 -> fp32 on tcgen05, fp32 master weights */
 } sagips_precision;
 
@@ -93,7 +96,9 @@ typedef struct {
   /* ranks and exchange */
   int32_t world;          /* number of ranks (GPUs) */
   int32_t rank;           /* this rank, 0..world-1 */
-  int32_t group_size;     /* inner group size g; world % g == 0; g == world: ungrouped */
+  int32_t group_size;     /* inner group size g: contiguous groups of g ranks, the last one may be
+                             smaller; leaders = first rank of each group;
+                             g == world: ungrouped */
   int32_t outer_every;    /* h: leaders' ring fires when (step+1) % h == 0; 0 = never (R13) */
   int32_t mode;           /* sagips_mode */
   int32_t staleness;      /* s in {0,1}: other members' packets from step t-s (R12) */
@@ -129,7 +134,11 @@ typedef struct {
   int32_t packet_biases;      /* 1: tensor fusion: the exchanged packet
                                  is [weights | biases] and Adam(G) applies the reduced bias
                                  gradients; 0 (default): weights only, biases local */
-  int32_t reserved[2];
+  int32_t outer_rma;          /* one-sided modes only: 1 = the leaders' outer ring (R13) also runs
+                                 through the exchange windows (one-hop all-gather of the leaders'
+                                 inner sums over NVLink, no NCCL); 0 (default) = NCCL send/recv,
+                                 the paper's two-sided ARAR outer group (Tab. III) */
+  int32_t reserved[1];
 } sagips_config;
 
 typedef struct sagips_ctx sagips_ctx;
@@ -197,11 +206,16 @@ SAGIPS_API sagips_status sagips_workspace_size(const sagips_config* cfg, size_t*
  * rank = rank 0's data distribution, R19) and this rank's 50%
  * bootstrap shard. [sync]
  * Errors: CONFIG if the generator output is not 6 (Eq. 4) or D is not 2->1,
- * world % group_size != 0, staleness not in {0,1}, mode unknown, or a
- * constrained true parameter c1/c2 <= 0; CUDA on device errors. */
+ * group_size < 1, staleness not in {0,1}, mode unknown, outer_rma not in
+ * {0,1}, or a constrained true parameter c1/c2 <= 0; CUDA on device errors. */
 SAGIPS_API sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t workspace_bytes,
                             void* stream, sagips_ctx** out);
 
+/* Frees the context and, for world > 1, the exchange window that peers map.
+ * The caller must quiesce the ranks first: every rank synchronises its
+ * streams and passes a barrier (e.g. torch.distributed.barrier) before any
+ * rank calls destroy, so no peer store into this window is in flight
+ * (runtime.close does this). [sync] */
 SAGIPS_API sagips_status sagips_destroy(sagips_ctx* ctx);
 SAGIPS_API const char* sagips_last_error(const sagips_ctx* ctx);
 SAGIPS_API int32_t sagips_abi_version(void);
@@ -270,8 +284,13 @@ SAGIPS_API sagips_status sagips_ensemble_stats(const float* preds, int32_t M, in
  * sampler -> bootstrap real batch -> D step + Adam(D) -> G loss through the
  * updated D -> backprop through the sampler and G -> weights-only packet
  * and then, unless SAGIPS_STEP_LOCAL_ONLY, push + pull (exchange per
- * cfg.mode) + Adam(G).  Steps must be issued in increasing order. [async]
- * Errors: STATE if t is not the next step; CUDA. */
+ * cfg.mode) + Adam(G).  Steps are consecutive: t = previous t + 1 (the first
+ * call may use any t, except 0 in exchanging modes with staleness 1, whose
+ * pull(t) needs the peers' packets of t - 1). [async]
+ * Errors: STATE if t is not the next step; TIMEOUT / PROTOCOL if an earlier
+ * exchange wait of this rank failed (reported by the next call without a
+ * sync; that step's fold and Adam(G) were skipped, so the generator keeps
+ * its weights); CUDA. */
 SAGIPS_API sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream);
 
 /* sagips_train_step with the step's inputs supplied by the caller (host
@@ -294,7 +313,12 @@ SAGIPS_API sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, 
  * pull waits (bounded by exchange_timeout_ms) for the packets it needs,
  * forwards the ring, folds in ascending origin order (R10), applies the
  * outer ring when it fires (R13) and runs Adam(G). [async]
- * Errors: STATE if pull(t) precedes push(t) or train_step(t, LOCAL_ONLY). */
+ * One-sided modes: pull is a one-warp wait kernel (only one thread spins)
+ * followed by the fold + Adam(G) kernel (programmatic dependent launch); if
+ * the wait times out or finds an overrun slot, the fold and Adam(G) are
+ * skipped on the device and the error is returned by the next call.
+ * Errors: STATE if pull(t) precedes push(t) or train_step(t, LOCAL_ONLY);
+ * TIMEOUT / PROTOCOL as sagips_train_step. */
 SAGIPS_API sagips_status sagips_push_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream);
 SAGIPS_API sagips_status sagips_pull_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream);
 
@@ -312,6 +336,20 @@ SAGIPS_API sagips_status sagips_set(sagips_ctx* ctx, int32_t which, const void* 
 #define SAGIPS_IPC_HANDLE_BYTES 64
 SAGIPS_API sagips_status sagips_ipc_handle(sagips_ctx* ctx, void* host_handle, size_t bytes);
 SAGIPS_API sagips_status sagips_connect_peers(sagips_ctx* ctx, const void* host_handles, size_t bytes);
+
+/* Single-process wiring (several contexts of one process on one device, e.g.
+ * W emulated ranks in a test; CUDA IPC cannot open a handle in the process
+ * that exported it): sagips_window_ptr returns the device address of this
+ * context's exchange window (0 if the mode has none); after every context
+ * has one, sagips_connect_peers_local takes the world's window addresses in
+ * rank order (n == world) instead of IPC handles.  The one-sided modes then
+ * behave exactly as across processes (same kernels, same release/acquire
+ * tags).  The caller orders the launches so that no kernel waits on work
+ * queued behind it on the same stream (e.g. all LOCAL_ONLY steps, then all
+ * pushes, then all pulls). [sync]  Errors: INVALID_ARG (NULL, n != world,
+ * own address mismatch), STATE (already connected). */
+SAGIPS_API sagips_status sagips_window_ptr(sagips_ctx* ctx, uint64_t* dev_ptr);
+SAGIPS_API sagips_status sagips_connect_peers_local(sagips_ctx* ctx, const uint64_t* dev_ptrs, size_t n);
 
 /* NCCL (two-sided ring and the synchronous all-reduce).  Rank 0 creates the
  * id (128 bytes, ncclUniqueId), the caller broadcasts it, every rank

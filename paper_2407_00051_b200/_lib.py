@@ -52,7 +52,7 @@ class Config(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("exchange_timeout_ms", ctypes.c_int32), ("phase_timing", ctypes.c_int32),
         ("disc_impl", ctypes.c_int32), ("sampler", ctypes.c_int32), ("sampler_grid", ctypes.c_int32),
-        ("packet_biases", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2),
+        ("packet_biases", ctypes.c_int32), ("outer_rma", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1),
     ]
 
 
@@ -86,6 +86,8 @@ def _load():
         "sagips_set": ([vp, ctypes.c_int32, vp, sz], st),
         "sagips_ipc_handle": ([vp, vp, sz], st),
         "sagips_connect_peers": ([vp, vp, sz], st),
+        "sagips_window_ptr": ([vp, P(ctypes.c_uint64)], st),
+        "sagips_connect_peers_local": ([vp, vp, sz], st),
         "sagips_nccl_unique_id": ([vp, sz], st),
         "sagips_connect_nccl": ([vp, vp, sz], st),
         "sagips_launch_count": ([vp, P(ctypes.c_uint64)], st),
@@ -117,7 +119,7 @@ EXPORTED = [
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
     "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace",
     "sagips_predict_params", "sagips_ensemble_stats", "sagips_sample_tabulated", "sagips_sample_tabulated_bwd",
-    "sagips_train_step_host"]
+    "sagips_train_step_host", "sagips_window_ptr", "sagips_connect_peers_local"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 NUM_KERNELS = 12
@@ -260,6 +262,17 @@ class Context:
     def connect_peers(self, handles):
         blob = b"".join(handles)
         _check(lib.sagips_connect_peers(self.h, blob, len(blob)), self.h)
+
+    def window_ptr(self):
+        """Device address of this context's exchange window (0 if none)."""
+        p = ctypes.c_uint64()
+        _check(lib.sagips_window_ptr(self.h, ctypes.byref(p)), self.h)
+        return p.value
+
+    def connect_peers_local(self, ptrs):
+        """Single-process wiring: the world's window addresses in rank order."""
+        a = (ctypes.c_uint64 * len(ptrs))(*ptrs)
+        _check(lib.sagips_connect_peers_local(self.h, a, len(ptrs)), self.h)
 
     def connect_nccl(self, uid):
         _check(lib.sagips_connect_nccl(self.h, uid, len(uid)), self.h)

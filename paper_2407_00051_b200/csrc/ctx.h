@@ -138,5 +138,6 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
 bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step);
 GenAdam gen_adam_args(sagips_ctx* c);
 sagips_status exchange_check(sagips_ctx* c);
+sagips_status exchange_poll(sagips_ctx* c);  // non-blocking: an error raised by an earlier wait
 void exchange_destroy(sagips_ctx* c);
 }  // namespace sagips

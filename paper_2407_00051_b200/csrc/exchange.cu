@@ -22,6 +22,7 @@
 //    others' packets of step t-s, so with s = 1 the ring of step t runs on
 //    the side stream while step t+1 computes.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -39,8 +40,9 @@ struct DevFlags {
 };
 
 struct ExchangeState {
-  int pos = 0, g = 1;            // position in the inner group, group size
+  int pos = 0, g = 1;            // position in the inner group, its size (the last group may be smaller)
   int first = 0;                 // first rank of the inner group
+  int nlead = 1;                 // inner groups = leaders = ceil(world / group_size)
   int succ = 0, pred = 0;        // ring neighbours (global ranks)
   // one-sided window: slots[origin][version][Pw] fp32 + flags
   float* win = nullptr;          // own window (cudaMalloc, IPC-exported)
@@ -50,6 +52,7 @@ struct ExchangeState {
   bool have_handle = false;
   char* peer_base[kMaxWorld] = {};
   bool peers_ok = false;
+  bool local_peers = false;      // sagips_connect_peers_local: raw pointers of one process (no IPC)
   // two-sided / outer / sync
   ncclComm_t comm_ring = nullptr;   // side-stream ring
   ncclComm_t comm_main = nullptr;   // outer ring and all-reduce (main stream)
@@ -63,6 +66,8 @@ struct ExchangeState {
   uint64_t ring_step[2] = {0, 0};
   // device error word and wait accounting
   unsigned int* err = nullptr;      // device: 1 timeout, 2 protocol
+  unsigned int* herr = nullptr;     // the same code in mapped pinned host memory (read without a sync)
+  unsigned int* herr_dev = nullptr; // its device alias
   unsigned int* ticket = nullptr;   // device [kMaxWorld]: k_push's last-CTA counters (self-resetting)
   uint32_t* one = nullptr;          // device constant 1 (stats.outer_fired)
 };
@@ -96,13 +101,26 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Wait until *flag >= want; returns false on timeout (sets *err = 1).
+// Error codes: 1 timeout, 2 protocol (slot overrun).  The device word gates
+// the fold/Adam kernel of the same step; the host-mapped copy lets the next
+// API call report the error without synchronising.
+struct ErrWords {
+  unsigned int* dev;
+  unsigned int* host;  // device alias of mapped pinned host memory
+};
+__device__ __forceinline__ void raise_err(ErrWords e, unsigned int code) {
+  atomicExch(e.dev, code);
+  *reinterpret_cast<volatile unsigned int*>(e.host) = code;
+  __threadfence_system();
+}
+
+// Wait until *flag >= want; returns false on timeout (raises 1).
 __device__ bool wait_tag(const unsigned long long* flag, unsigned long long want, unsigned long long timeout_ns,
-                         unsigned int* err) {
+                         ErrWords err) {
   const unsigned long long t0 = globaltimer();
   while (ld_acquire_sys(flag) < want) {
     if (globaltimer() - t0 > timeout_ns) {
-      atomicExch(err, 1u);
+      raise_err(err, 1u);
       return false;
     }
     __nanosleep(64);
@@ -173,7 +191,7 @@ struct FwdArgs {
 // waits for packets that the peers' starved agents never forward (measured:
 // exchange wait timeout at N = 4).
 __global__ void __launch_bounds__(1024, 2) k_forward(FwdArgs a, int64_t n, unsigned long long tag,
-                                                  unsigned long long timeout_ns, unsigned int* err) {
+                                                  unsigned long long timeout_ns, ErrWords err) {
   __shared__ int ok;
   for (int j = 0; j < a.hops; ++j) {
     if (threadIdx.x == 0) ok = wait_tag(a.src_flag[j], tag, timeout_ns, err);
@@ -194,49 +212,45 @@ struct WaitArgs {
   int count;
 };
 
-__global__ void k_wait(WaitArgs a, unsigned long long timeout_ns, unsigned int* err, unsigned long long* wait_ns) {
+// The wait of a pull: ONE thread waits (bounded) for the tags it needs and
+// checks that no newer packet overwrote a slot (protocol error 2).  Only this
+// one-warp CTA spins, so the ring's forwarding agents (and any other work)
+// always find room on the SMs while a rank waits for its peers.
+__global__ void k_wait(WaitArgs a, unsigned long long timeout_ns, ErrWords err, unsigned long long* wait_ns,
+                       uint32_t* outer_fired) {
   if (threadIdx.x != 0) return;
   const unsigned long long t0 = globaltimer();
   for (int i = 0; i < a.count; ++i) {
     if (!wait_tag(a.flag[i], a.want[i], timeout_ns, err)) break;
-    if (ld_acquire_sys(a.flag[i]) != a.want[i]) atomicExch(err, 2u);  // a newer packet overwrote the slot
+    if (ld_acquire_sys(a.flag[i]) != a.want[i]) raise_err(err, 2u);  // a newer packet overwrote the slot
   }
-  *wait_ns = globaltimer() - t0;
+  if (wait_ns) *wait_ns = globaltimer() - t0;
+  if (outer_fired) *outer_fired = 0u;
 }
 
-// pull, fused (exchange_fuses_adam): k_wait, k_fold and Adam(G) in one
-// launch.  Every CTA's thread 0 waits for the tags as k_wait does (CTA 0
-// records the wait and clears stats.outer_fired), then per element: the
-// ascending fold of k_fold, reduced[i] = (sum_j p_j[i]) / divisor for
-// i < pw (loads through L2: the slots were written by peers), and the Adam
-// update of adam_elem, as k_adam -- weights from reduced[i], biases from
-// reduced[nw + j] (fused packet) or the local gradient.
+// The fold of a pull and (optionally) Adam(G), launched after k_wait with
+// programmatic dependent launch (its launch overlaps the wait; griddepcontrol
+// .wait orders it after k_wait's writes).  If a wait of this step failed
+// (err != 0) nothing is written: the generator keeps its weights and the
+// host reports the error at the next call (sagips_train_step / pull).
+// Per element: the ascending fold reduced[i] = (sum_j p_j[i]) / divisor for
+// i < pw (loads through L2: peers wrote the slots) and the Adam update of
+// adam_elem, as k_adam -- weights from reduced[i], biases from reduced[nw+j]
+// (fused packet) or the local gradient.
 struct FoldAdamArgs {
   PacketList pl;
-  WaitArgs w;
   float* reduced;
   int64_t pw;
   float divisor;
+  int do_adam;
   GenAdam a;
-  uint32_t* outer_fired;
-  unsigned long long* wait_ns;
+  const unsigned int* err;
 };
-__global__ void __launch_bounds__(256) k_wait_fold_adam(const __grid_constant__ FoldAdamArgs f,
-                                                        unsigned long long timeout_ns, unsigned int* err) {
-  if (threadIdx.x == 0) {
-    const unsigned long long t0 = globaltimer();
-    for (int i = 0; i < f.w.count; ++i) {
-      if (!wait_tag(f.w.flag[i], f.w.want[i], timeout_ns, err)) break;
-      if (ld_acquire_sys(f.w.flag[i]) != f.w.want[i]) atomicExch(err, 2u);
-    }
-    if (blockIdx.x == 0) {
-      *f.wait_ns = globaltimer() - t0;
-      *f.outer_fired = 0u;
-    }
-  }
-  __syncthreads();
+__global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldAdamArgs f) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (f.err && *reinterpret_cast<const volatile unsigned int*>(f.err) != 0u) return;
   const GenAdam& a = f.a;
-  const int64_t n = a.nw + a.nb;
+  const int64_t n = f.do_adam ? a.nw + a.nb : f.pw;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float gi = 0.f;
     if (i < f.pw) {
@@ -245,6 +259,7 @@ __global__ void __launch_bounds__(256) k_wait_fold_adam(const __grid_constant__ 
       gi = acc / f.divisor;
       f.reduced[i] = gi;
     }
+    if (!f.do_adam) continue;
     if (i < a.nw) {
       float p = a.pw[i], m = a.mw[i], v = a.vw[i];
       adam_elem(p, gi, m, v, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
@@ -260,6 +275,22 @@ __global__ void __launch_bounds__(256) k_wait_fold_adam(const __grid_constant__ 
       a.vb[j] = v;
     }
   }
+}
+
+static cudaError_t launch_fold_adam(const FoldAdamArgs& f, cudaStream_t st) {
+  const int64_t n = f.do_adam ? f.a.nw + f.a.nb : f.pw;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)std::min<int64_t>((n + 255) / 256, 148 * 2));
+  lc.blockDim = dim3(256);
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&lc, k_fold_adam, f);
+  count_launch();
+  return e;
 }
 
 // ---------------------------------------------------------------- host side
@@ -283,11 +314,23 @@ __global__ void __launch_bounds__(256) k_wait_fold_adam(const __grid_constant__ 
 static bool one_sided(const sagips_ctx* c) {
   return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR || c->cfg.mode == SAGIPS_MODE_RMA_ALLGATHER;
 }
+// the leaders' outer ring through the windows (one-hop all-gather, cfg.outer_rma)
+static bool outer_one_sided(const sagips_ctx* c) { return one_sided(c) && c->cfg.outer_rma != 0; }
+static int n_leaders(const sagips_config& g) { return (g.world + g.group_size - 1) / g.group_size; }
+static bool is_leader(const sagips_config& g) { return g.rank % g.group_size == 0; }
 static bool needs_nccl(const sagips_ctx* c) {
   const auto& g = c->cfg;
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) return false;
-  if (one_sided(c)) return g.outer_every > 0 && g.group_size < g.world;
+  if (one_sided(c)) return !outer_one_sided(c) && g.outer_every > 0 && g.group_size < g.world;
   return true;
+}
+// ranks whose window this rank maps: its inner group, and the other leaders
+// when it is a leader with the one-sided outer ring
+static bool maps_peer(const sagips_ctx* c, int q) {
+  const auto& g = c->cfg;
+  const ExchangeState* x = c->xs;
+  if (q >= x->first && q < x->first + x->g) return true;
+  return outer_one_sided(c) && is_leader(g) && q % g.group_size == 0 && g.outer_every > 0;
 }
 
 static sagips_status ensure_state(sagips_ctx* c) {
@@ -297,11 +340,12 @@ static sagips_status ensure_state(sagips_ctx* c) {
   const auto& g = c->cfg;
   int gs = g.group_size;
   if (g.mode == SAGIPS_MODE_ARAR) gs = g.world;  // ungrouped
-  x->g = gs;
   x->first = (g.rank / gs) * gs;
+  x->g = std::min(gs, g.world - x->first);  // contiguous groups; the last may be smaller
   x->pos = g.rank - x->first;
-  x->succ = x->first + (x->pos + 1) % gs;
-  x->pred = x->first + (x->pos + gs - 1) % gs;
+  x->succ = x->first + (x->pos + 1) % x->g;
+  x->pred = x->first + (x->pos + x->g - 1) % x->g;
+  x->nlead = n_leaders(g);
   int lo, hi;
   XCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   XCK(cudaStreamCreateWithPriority(&x->side, cudaStreamNonBlocking, hi));
@@ -311,15 +355,22 @@ static sagips_status ensure_state(sagips_ctx* c) {
   }
   XCK(cudaMalloc(&x->err, sizeof(unsigned int)));
   XCK(cudaMemset(x->err, 0, sizeof(unsigned int)));
+  XCK(cudaHostAlloc(&x->herr, sizeof(unsigned int), cudaHostAllocMapped));
+  *reinterpret_cast<volatile unsigned int*>(x->herr) = 0u;
+  XCK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&x->herr_dev), x->herr, 0));
   XCK(cudaMalloc(&x->ticket, sizeof(unsigned int) * kMaxWorld));
   XCK(cudaMemset(x->ticket, 0, sizeof(unsigned int) * kMaxWorld));
+  XCK(cudaMalloc(&x->one, sizeof(uint32_t)));
+  const uint32_t one = 1;
+  XCK(cudaMemcpy(x->one, &one, sizeof one, cudaMemcpyHostToDevice));
   if (g.world > 1 && g.mode != SAGIPS_MODE_NONE) {
     const size_t ps = slot_stride(c);
     XCK(cudaMalloc(&x->gather[0], sizeof(float) * ps * gs));
     XCK(cudaMalloc(&x->gather[1], sizeof(float) * ps * gs));
-    const int nlead = g.world / g.group_size;
-    XCK(cudaMalloc(&x->outer_buf, sizeof(float) * ps * std::max(nlead, 1)));
+    XCK(cudaMalloc(&x->outer_buf, sizeof(float) * ps * std::max(x->nlead, 1)));
     if (one_sided(c)) {
+      // slots[origin][version]: inner-group origins carry packets, other
+      // leaders' origins carry their inner sums (one-sided outer ring)
       x->win_bytes = sizeof(float) * (size_t)g.world * kVersions * ps + sizeof(DevFlags);
       XCK(cudaMalloc(&x->win, x->win_bytes));
       XCK(cudaMemset(x->win, 0, x->win_bytes));
@@ -331,21 +382,34 @@ static sagips_status ensure_state(sagips_ctx* c) {
   return SAGIPS_OK;
 }
 
-sagips_status exchange_check(sagips_ctx* c) {
-  if (!c->xs || !c->xs->err) return SAGIPS_OK;
-  unsigned int e = 0;
-  if (cudaMemcpy(&e, c->xs->err, sizeof e, cudaMemcpyDeviceToHost) != cudaSuccess) return SAGIPS_ERR_CUDA;
+static ErrWords err_words(const ExchangeState* x) { return ErrWords{x->err, x->herr_dev}; }
+
+static sagips_status err_status(sagips_ctx* c, unsigned int e) {
   if (e == 1) { c->err = "exchange wait timed out"; return SAGIPS_ERR_TIMEOUT; }
   if (e == 2) { c->err = "exchange slot overrun (protocol)"; return SAGIPS_ERR_PROTOCOL; }
   return SAGIPS_OK;
 }
 
+sagips_status exchange_check(sagips_ctx* c) {
+  if (!c->xs || !c->xs->err) return SAGIPS_OK;
+  unsigned int e = 0;
+  if (cudaMemcpy(&e, c->xs->err, sizeof e, cudaMemcpyDeviceToHost) != cudaSuccess) return SAGIPS_ERR_CUDA;
+  return err_status(c, e);
+}
+
+// non-blocking: an exchange error already raised by a finished wait
+sagips_status exchange_poll(sagips_ctx* c) {
+  if (!c->xs || !c->xs->herr) return SAGIPS_OK;
+  return err_status(c, *reinterpret_cast<volatile unsigned int*>(c->xs->herr));
+}
+
 void exchange_destroy(sagips_ctx* c) {
   ExchangeState* x = c->xs;
   if (!x) return;
+  // the caller quiesces the ranks first (include/sagips.h: sagips_destroy)
   cudaDeviceSynchronize();
   for (int q = 0; q < c->cfg.world; ++q)
-    if (x->peer_base[q] && q != c->cfg.rank) cudaIpcCloseMemHandle(x->peer_base[q]);
+    if (x->peer_base[q] && q != c->cfg.rank && !x->local_peers) cudaIpcCloseMemHandle(x->peer_base[q]);
   if (x->comm_ring) ncclCommDestroy(x->comm_ring);
   if (x->comm_main) ncclCommDestroy(x->comm_main);
   cudaFree(x->win);
@@ -354,6 +418,7 @@ void exchange_destroy(sagips_ctx* c) {
   cudaFree(x->outer_buf);
   if (x->one) cudaFree(x->one);
   cudaFree(x->err);
+  if (x->herr) cudaFreeHost(x->herr);
   cudaFree(x->ticket);
   for (int i = 0; i < 2; ++i) {
     if (x->ev_ready[i]) cudaEventDestroy(x->ev_ready[i]);
@@ -384,6 +449,22 @@ static sagips_status nccl_ring(sagips_ctx* c, uint64_t step) {
   return SAGIPS_OK;
 }
 
+// one-sided store of `src` (pw floats) into slot [origin = this rank][version]
+// of each destination's window, then its tag := version + 1 (release)
+static sagips_status push_to(sagips_ctx* c, const float* src, const int* dst_ranks, int ndst, uint64_t version,
+                             cudaStream_t st) {
+  ExchangeState* x = c->xs;
+  PushAllArgs pa{};
+  for (int j = 0; j < ndst; ++j) {
+    char* db = x->peer_base[dst_ranks[j]];
+    pa.dst[j] = slot_ptr(db, c, c->cfg.rank, version);
+    pa.dst_flag[j] = &flags_ptr(db, c)->tag[c->cfg.rank][version % kVersions];
+  }
+  k_push<<<dim3(kPushCtas, ndst), 256, 0, st>>>(src, (int64_t)slot_floats(c), pa, version + 1, x->ticket);
+  count_launch();
+  return SAGIPS_OK;
+}
+
 sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   const auto& g = c->cfg;
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE || g.mode == SAGIPS_MODE_SYNC_ALLREDUCE) return SAGIPS_OK;
@@ -394,25 +475,17 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   if (x->g == 1) return SAGIPS_OK;
   if (one_sided(c)) {
     if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
-    char* sb = x->peer_base[x->succ];
-    PushAllArgs pa{};
-    int ndst = 1;
+    int dst[kMaxWorld];
     if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) {
-      ndst = x->g - 1;
-      for (int j = 1; j < x->g; ++j) {  // destinations pos+1, pos+2, ...
-        char* db = x->peer_base[x->first + (x->pos + j) % x->g];
-        pa.dst[j - 1] = slot_ptr(db, c, g.rank, step);
-        pa.dst_flag[j - 1] = &flags_ptr(db, c)->tag[g.rank][step % kVersions];
-      }
-    } else {
-      pa.dst[0] = slot_ptr(sb, c, g.rank, step);
-      pa.dst_flag[0] = &flags_ptr(sb, c)->tag[g.rank][step % kVersions];
+      for (int j = 1; j < x->g; ++j) dst[j - 1] = x->first + (x->pos + j) % x->g;  // pos+1, pos+2, ...
+      return push_to(c, c->g_dW, dst, x->g - 1, step, st);
     }
-    k_push<<<dim3(kPushCtas, ndst), 256, 0, st>>>(c->g_dW, (int64_t)pw, pa, step + 1, x->ticket);
-    count_launch();
-    if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) return SAGIPS_OK;
+    dst[0] = x->succ;
+    s = push_to(c, c->g_dW, dst, 1, step, st);
+    if (s != SAGIPS_OK) return s;
     if (x->g > 2) {
       // the agent forwards origins pos-1 .. pos-(g-2) of this version
+      char* sb = x->peer_base[x->succ];
       XCK(cudaEventRecord(x->ev_ready[step & 1], st));
       XCK(cudaStreamWaitEvent(x->side, x->ev_ready[step & 1], 0));
       FwdArgs a{};
@@ -425,7 +498,7 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
         a.dst[j - 1] = slot_ptr(sb, c, o, step);
         a.dst_flag[j - 1] = &flags_ptr(sb, c)->tag[o][step % kVersions];
       }
-      k_forward<<<1, 1024, 0, x->side>>>(a, (int64_t)pw, step + 1, timeout_ns(c), x->err);
+      k_forward<<<1, 1024, 0, x->side>>>(a, (int64_t)pw, step + 1, timeout_ns(c), err_words(x));
       count_launch();
     }
   } else {
@@ -446,17 +519,17 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
 // the leaders' outer ring runs after step `step`'s inner fold on this rank
 static bool outer_fires(const sagips_ctx* c, uint64_t step) {
   const auto& g = c->cfg;
-  const int nlead = g.world / g.group_size;
-  if (g.mode == SAGIPS_MODE_ARAR || nlead < 2 || g.outer_every <= 0) return false;
+  if (g.mode == SAGIPS_MODE_ARAR || n_leaders(g) < 2 || g.outer_every <= 0) return false;
   if ((step + 1) % (uint64_t)g.outer_every != 0) return false;
-  return g.rank % g.group_size == 0;  // leaders only
+  return is_leader(g);  // leaders only
 }
 
-static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
+// the two-sided outer ring (ARAR among the leaders): pass-along
+// over NCCL send/recv, then the ascending fold into `reduced` (no Adam)
+static sagips_status outer_ring_nccl(sagips_ctx* c, cudaStream_t st) {
   ExchangeState* x = c->xs;
   const auto& g = c->cfg;
-  const int nlead = g.world / g.group_size;
-  if (!outer_fires(c, step)) return SAGIPS_OK;
+  const int nlead = x->nlead;
   if (!x->comm_main) { c->err = "sagips_connect_nccl not called (outer ring)"; return SAGIPS_ERR_STATE; }
   const size_t pw = slot_floats(c);
   const int lp = g.rank / g.group_size;
@@ -474,16 +547,100 @@ static sagips_status outer_ring(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   pl.count = nlead;
   for (int i = 0; i < nlead; ++i) pl.p[i] = x->outer_buf + i * ps;
   launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)nlead : 1.0f, st);
-  XCK(cudaMemcpyAsync(&c->stats->outer_fired, x->one, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
   return SAGIPS_OK;
 }
 
-// pull(t) can run as one k_wait_fold_adam: one-sided, a group of >= 2 whose
-// packets of version t - s exist, and no outer ring after the fold
+// pull(t) applies Adam(G) itself (k_fold_adam) for the one-sided modes
 bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step) {
+  (void)step;
   const auto& g = c->cfg;
-  return g.world > 1 && one_sided(c) && c->xs && c->xs->g > 1 && c->xs->peers_ok &&
-         (int64_t)step - g.staleness >= 0 && !outer_fires(c, step);
+  return g.world > 1 && one_sided(c) && c->xs && (c->xs->g > 1 || outer_one_sided(c)) && c->xs->peers_ok;
+}
+
+// one-sided pull (modes RMA_ARAR_ARAR, RMA_ALLGATHER): k_wait on the inner
+// tags of version t - s, k_fold_adam (ascending fold, Adam(G) unless the
+// outer ring fires or adam == NULL); when the outer ring fires on this
+// leader: the inner sum goes to the other leaders (one-sided, or NCCL) and
+// their ascending fold is applied.
+static sagips_status pull_one_sided(sagips_ctx* c, uint64_t step, cudaStream_t st, const GenAdam* adam) {
+  ExchangeState* x = c->xs;
+  const auto& g = c->cfg;
+  const size_t pw = slot_floats(c);
+  const int64_t stale = (int64_t)step - g.staleness;  // version of the others' packets
+  char* own = x->peer_base[g.rank];
+  const bool outer = outer_fires(c, step);
+  FoldAdamArgs f{};
+  f.reduced = c->reduced;
+  f.pw = (int64_t)pw;
+  f.divisor = g.reduce_mean ? (float)x->g : 1.0f;
+  f.err = x->err;
+  if (stale >= 0) {
+    WaitArgs w{};
+    w.count = x->g - 1;
+    for (int j = 1; j < x->g; ++j) {
+      const int o = x->first + (x->pos - j + x->g) % x->g;
+      w.flag[j - 1] = &flags_ptr(own, c)->tag[o][stale % kVersions];
+      w.want[j - 1] = (unsigned long long)stale + 1;
+    }
+    k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), err_words(x), reinterpret_cast<unsigned long long*>(&c->stats->wait_ns),
+                             &c->stats->outer_fired);
+    count_launch();
+    f.pl.count = x->g;
+    for (int i = 0; i < x->g; ++i) {
+      const int o = x->first + i;
+      f.pl.p[i] = (o == g.rank) ? c->g_dW : slot_ptr(own, c, o, stale);
+    }
+  } else {
+    // before step s the other members' packets are zero (R12): own packet only
+    XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
+    f.pl.count = 1;
+    f.pl.p[0] = c->g_dW;
+  }
+  if (adam && !outer) {
+    f.do_adam = 1;
+    f.a = *adam;
+  }
+  XCK(launch_fold_adam(f, st));
+  if (!outer) return SAGIPS_OK;
+  // the outer ring of the leaders (R13): fold of the leaders' inner sums of step t
+  FoldAdamArgs o{};
+  o.reduced = c->reduced;
+  o.pw = (int64_t)pw;
+  o.err = x->err;
+  if (adam) {
+    o.do_adam = 1;
+    o.a = *adam;
+  }
+  if (outer_one_sided(c)) {
+    int dst[kMaxWorld], nd = 0;
+    for (int l = 0; l < x->nlead; ++l)
+      if (l * g.group_size != g.rank) dst[nd++] = l * g.group_size;
+    sagips_status s = push_to(c, c->reduced, dst, nd, step, st);
+    if (s != SAGIPS_OK) return s;
+    WaitArgs w{};
+    w.count = nd;
+    for (int j = 0; j < nd; ++j) {
+      w.flag[j] = &flags_ptr(own, c)->tag[dst[j]][step % kVersions];
+      w.want[j] = (unsigned long long)step + 1;
+    }
+    k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), err_words(x), nullptr, nullptr);
+    count_launch();
+    o.pl.count = x->nlead;
+    for (int l = 0; l < x->nlead; ++l) {
+      const int r = l * g.group_size;
+      o.pl.p[l] = (r == g.rank) ? c->reduced : slot_ptr(own, c, r, step);
+    }
+    o.divisor = g.reduce_mean ? (float)x->nlead : 1.0f;
+  } else {
+    sagips_status s = outer_ring_nccl(c, st);
+    if (s != SAGIPS_OK) return s;
+    o.pl.count = 1;  // Adam(G) on the folded outer sum (identity fold, gated by err)
+    o.pl.p[0] = c->reduced;
+    o.divisor = 1.0f;
+  }
+  XCK(launch_fold_adam(o, st));
+  XCK(cudaMemcpyAsync(&c->stats->outer_fired, x->one, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  return SAGIPS_OK;
 }
 
 sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const GenAdam* adam) {
@@ -493,14 +650,19 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
     c->err = "exchange_pull: fused Adam(G) requested where it does not apply";
     return SAGIPS_ERR_STATE;
   }
-  if (!adam) XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) {
+    XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
     XCK(cudaMemcpyAsync(c->reduced, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
     return SAGIPS_OK;
   }
   sagips_status s = ensure_state(c);
   if (s != SAGIPS_OK) return s;
   ExchangeState* x = c->xs;
+  if (one_sided(c) && (x->g > 1 || outer_one_sided(c))) {
+    if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
+    return pull_one_sided(c, step, st, adam);
+  }
+  XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
   if (g.mode == SAGIPS_MODE_SYNC_ALLREDUCE) {
     if (!x->comm_main) { c->err = "sagips_connect_nccl not called"; return SAGIPS_ERR_STATE; }
     NCK(ncclAllReduce(c->g_dW, c->reduced, pw, ncclFloat32, ncclSum, x->comm_main, st));
@@ -517,44 +679,6 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
   pl.count = x->g;
   if (x->g == 1) {
     pl.p[0] = c->g_dW;
-  } else if (one_sided(c)) {
-    char* own = x->peer_base[g.rank];
-    if (stale >= 0) {
-      WaitArgs w{};
-      w.count = x->g - 1;
-      for (int j = 1; j < x->g; ++j) {
-        const int o = x->first + (x->pos - j + x->g) % x->g;
-        w.flag[j - 1] = &flags_ptr(own, c)->tag[o][stale % kVersions];
-        w.want[j - 1] = (unsigned long long)stale + 1;
-      }
-      if (!adam) {
-        k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), x->err, reinterpret_cast<unsigned long long*>(&c->stats->wait_ns));
-        count_launch();
-      } else {
-        FoldAdamArgs f{};
-        f.w = w;
-        f.pl.count = x->g;
-        for (int i = 0; i < x->g; ++i) {
-          const int o = x->first + i;
-          f.pl.p[i] = (o == g.rank) ? c->g_dW : slot_ptr(own, c, o, stale);
-        }
-        f.reduced = c->reduced;
-        f.pw = (int64_t)pw;
-        f.divisor = g.reduce_mean ? (float)x->g : 1.0f;
-        f.a = *adam;
-        f.outer_fired = &c->stats->outer_fired;
-        f.wait_ns = reinterpret_cast<unsigned long long*>(&c->stats->wait_ns);
-        const int64_t n = adam->nw + adam->nb;
-        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 2);
-        k_wait_fold_adam<<<blocks, 256, 0, st>>>(f, timeout_ns(c), x->err);
-        count_launch();
-        return SAGIPS_OK;
-      }
-    }
-    for (int i = 0; i < x->g; ++i) {
-      const int o = x->first + i;
-      pl.p[i] = (o == g.rank) ? c->g_dW : (stale >= 0 ? slot_ptr(own, c, o, stale) : nullptr);
-    }
   } else {
     if (stale >= 0) {
       const int v = (int)(stale & 1);
@@ -568,15 +692,18 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
       pl.p[i] = (i == x->pos) ? c->g_dW : (stale >= 0 ? x->gather[stale & 1] + i * slot_stride(c) : nullptr);
   }
   if (stale < 0 && x->g > 1) {
-    // before step s the other members' packets are zero (R12): own packet only
-    PacketList own{};
-    own.count = 1;
-    own.p[0] = c->g_dW;
-    launch_fold(own, (int64_t)pw, c->reduced, g.reduce_mean ? (float)x->g : 1.0f, st);
+    PacketList ownp{};
+    ownp.count = 1;
+    ownp.p[0] = c->g_dW;
+    launch_fold(ownp, (int64_t)pw, c->reduced, g.reduce_mean ? (float)x->g : 1.0f, st);
   } else {
     launch_fold(pl, (int64_t)pw, c->reduced, g.reduce_mean ? (float)x->g : 1.0f, st);
   }
-  return outer_ring(c, step, st);
+  if (!outer_fires(c, step)) return SAGIPS_OK;
+  s = outer_ring_nccl(c, st);
+  if (s != SAGIPS_OK) return s;
+  XCK(cudaMemcpyAsync(&c->stats->outer_fired, x->one, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  return SAGIPS_OK;
 }
 
 }  // namespace sagips
@@ -602,8 +729,10 @@ sagips_status sagips_connect_peers(sagips_ctx* c, const void* host_handles, size
   sagips_status s = ensure_state(c);
   if (s != SAGIPS_OK) return s;
   ExchangeState* x = c->xs;
+  if (x->peers_ok) { c->err = "peers already connected"; return SAGIPS_ERR_STATE; }
   const char* h = (const char*)host_handles;
-  for (int q = x->first; q < x->first + x->g; ++q) {  // only the inner group is touched
+  for (int q = 0; q < c->cfg.world; ++q) {
+    if (!maps_peer(c, q)) continue;
     if (q == c->cfg.rank) {
       x->peer_base[q] = reinterpret_cast<char*>(x->win);
       continue;
@@ -614,6 +743,34 @@ sagips_status sagips_connect_peers(sagips_ctx* c, const void* host_handles, size
     XCK(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
     x->peer_base[q] = reinterpret_cast<char*>(p);
   }
+  x->peers_ok = true;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_window_ptr(sagips_ctx* c, uint64_t* dev_ptr) {
+  if (!c || !dev_ptr) return SAGIPS_ERR_INVALID_ARG;
+  *dev_ptr = 0;
+  if (!one_sided(c) || c->cfg.world == 1) return SAGIPS_OK;
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  *dev_ptr = (uint64_t)(uintptr_t)c->xs->win;
+  return SAGIPS_OK;
+}
+
+sagips_status sagips_connect_peers_local(sagips_ctx* c, const uint64_t* dev_ptrs, size_t n) {
+  if (!c || !dev_ptrs || n != (size_t)c->cfg.world) return SAGIPS_ERR_INVALID_ARG;
+  if (!one_sided(c) || c->cfg.world == 1) return SAGIPS_OK;
+  sagips_status s = ensure_state(c);
+  if (s != SAGIPS_OK) return s;
+  ExchangeState* x = c->xs;
+  if (x->peers_ok) { c->err = "peers already connected"; return SAGIPS_ERR_STATE; }
+  if (dev_ptrs[c->cfg.rank] != (uint64_t)(uintptr_t)x->win) { c->err = "own window pointer mismatch"; return SAGIPS_ERR_INVALID_ARG; }
+  for (int q = 0; q < c->cfg.world; ++q) {
+    if (!maps_peer(c, q)) continue;
+    if (!dev_ptrs[q]) { c->err = "null peer window"; return SAGIPS_ERR_INVALID_ARG; }
+    x->peer_base[q] = reinterpret_cast<char*>((uintptr_t)dev_ptrs[q]);
+  }
+  x->local_peers = true;
   x->peers_ok = true;
   return SAGIPS_OK;
 }
@@ -637,26 +794,21 @@ sagips_status sagips_connect_nccl(sagips_ctx* c, const void* host_id, size_t byt
   std::memcpy(&id, host_id, sizeof id);
   NCK(ncclCommInitRank(&x->comm_main, c->cfg.world, id, c->cfg.rank));
   NCK(ncclCommSplit(x->comm_main, 0, c->cfg.rank, &x->comm_ring, nullptr));
-  if (!x->one) {
-    XCK(cudaMalloc(&x->one, sizeof(uint32_t)));
-    const uint32_t one = 1;
-    XCK(cudaMemcpy(x->one, &one, sizeof one, cudaMemcpyHostToDevice));
-  }
   // NCCL sets up peer connections lazily, on the first send/recv between two
   // ranks (hundreds of ms): exercise the leaders' outer ring and the inner
   // two-sided ring here, so no training step pays for it
   const auto& g = c->cfg;
-  const int nlead = g.world / std::max(1, g.group_size);
+  const int nlead = x->nlead;
   float* tmp = nullptr;
   XCK(cudaMalloc(&tmp, 2 * sizeof(float)));
-  if (nlead >= 2 && g.outer_every > 0 && g.rank % g.group_size == 0) {
+  if (nlead >= 2 && g.outer_every > 0 && is_leader(g)) {
     const int lp = g.rank / g.group_size;
     NCK(ncclGroupStart());
     NCK(ncclSend(tmp, 1, ncclFloat32, ((lp + 1) % nlead) * g.group_size, x->comm_main, x->side));
     NCK(ncclRecv(tmp + 1, 1, ncclFloat32, ((lp + nlead - 1) % nlead) * g.group_size, x->comm_main, x->side));
     NCK(ncclGroupEnd());
   }
-  if (x->g > 1) {
+  if (x->g > 1 && !one_sided(c)) {
     NCK(ncclGroupStart());
     NCK(ncclSend(tmp, 1, ncclFloat32, x->succ, x->comm_ring, x->side));
     NCK(ncclRecv(tmp + 1, 1, ncclFloat32, x->pred, x->comm_ring, x->side));

@@ -154,7 +154,8 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
   auto bad = [&](const char* m) { *why = m; return SAGIPS_ERR_CONFIG; };
   if (g->world < 1 || g->world > kMaxWorld) return bad("world must be in [1, 64]");
   if (g->rank < 0 || g->rank >= g->world) return bad("rank out of range");
-  if (g->group_size < 1 || g->world % g->group_size != 0) return bad("world % group_size != 0");
+  if (g->group_size < 1) return bad("group_size must be >= 1");
+  if (g->outer_rma != 0 && g->outer_rma != 1) return bad("outer_rma must be 0 or 1");
   if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_RMA_ALLGATHER) return bad("unknown mode");
   if (g->staleness < 0 || g->staleness > 1) return bad("staleness must be 0 or 1");
   if (g->precision != SAGIPS_PREC_FP32 && g->precision != SAGIPS_PREC_BF16) return bad("unknown precision");
@@ -936,7 +937,15 @@ extern "C" {
 
 sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
-  if (ctx->have_step && step <= ctx->last_step) return fail(ctx, SAGIPS_ERR_STATE, "steps must increase");
+  if (ctx->have_step && step != ctx->last_step + 1)
+    return fail(ctx, SAGIPS_ERR_STATE, "step %llu is not the next step (%llu)", (unsigned long long)step,
+                (unsigned long long)(ctx->last_step + 1));
+  if (!ctx->have_step && step != 0 && ctx->cfg.world > 1 && ctx->cfg.mode != SAGIPS_MODE_NONE && ctx->cfg.staleness > 0)
+    return fail(ctx, SAGIPS_ERR_STATE, "the first exchanging step with staleness 1 must be step 0");
+  {
+    const sagips_status xs = exchange_poll(ctx);
+    if (xs != SAGIPS_OK) return xs;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (ctx->cfg.phase_timing) {
     if (!ctx->pev[0][0])
@@ -989,6 +998,10 @@ sagips_status sagips_push_generator_grad(sagips_ctx* ctx, uint64_t step, void* s
 sagips_status sagips_pull_generator_grad(sagips_ctx* ctx, uint64_t step, void* stream) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
   if (!ctx->pushed || ctx->local_done_step != step) return fail(ctx, SAGIPS_ERR_STATE, "pull before push");
+  {
+    const sagips_status xs = exchange_poll(ctx);
+    if (xs != SAGIPS_OK) return xs;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (!ctx->skip_adam_once && exchange_fuses_adam(ctx, step)) {
     // wait + fold + Adam(G) in one kernel (the same arithmetic as below)

@@ -41,3 +41,17 @@ def connect(ctx, group=None):
     uid = [_lib.nccl_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(uid, src=0, group=group)
     ctx.connect_nccl(uid[0])
+
+
+def close(ctx, group=None):
+    """Quiesce, then destroy (include/sagips.h sagips_destroy): every rank
+    synchronises its device and passes a barrier before any rank frees the
+    exchange window its peers map."""
+    torch.cuda.synchronize()
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.barrier(group=group)
+    except Exception:
+        pass
+    ctx.close()

@@ -70,7 +70,7 @@ def test_presets_and_workspace():
     assert L.workspace_size(paper) > L.workspace_size(desk) > 0
 
 
-@pytest.mark.parametrize("field,value", [("group_size", 3), ("staleness", 2), ("mode", 9), ("disc_hidden", 100),
+@pytest.mark.parametrize("field,value", [("group_size", 0), ("outer_rma", 2), ("staleness", 2), ("mode", 9), ("disc_hidden", 100),
                                          ("rank", 5), ("hist_bins", 0), ("param_samples", 0)])
 def test_config_validation(field, value):
     L = _lib()
@@ -79,6 +79,14 @@ def test_config_validation(field, value):
     with pytest.raises(L.SagipsError) as e:
         L.workspace_size(cfg)
     assert e.value.status == 2
+
+
+def test_ragged_last_group_is_accepted():
+    """SPEC's (10, 4) partition {0-3},{4-7},{8-9}: world need not
+    be a multiple of the group size."""
+    L = _lib()
+    cfg = L.config_init(L.PRESET_DESK, world=10, rank=9, group_size=4, mode=L.MODE_RMA_ALLGATHER, outer_every=2)
+    assert L.workspace_size(cfg) > 0
 
 
 def test_true_params_must_be_in_softplus_range():
