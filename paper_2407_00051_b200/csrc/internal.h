@@ -79,7 +79,8 @@ void launch_shard(const float* ref, int64_t n_ref, float* shard, int64_t n_s, ui
 void launch_constrain(const float* raw, float* c, int k, cudaStream_t st, bool tab = false);
 void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard, uint64_t seed,
                         uint32_t step, uint32_t rank, float* x_events, uint32_t* real_idx, uint32_t* hist,
-                        int bins, const float lo[2], const float hi[2], cudaStream_t st, bool fake = true);
+                        int bins, const float lo[2], const float hi[2], cudaStream_t st, bool fake = true,
+                        bool hist_zeroed = false);
 void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t step, uint32_t rank,
                           uint32_t stream_id, float* events, uint32_t* hist, int bins, const float lo[2],
                           const float hi[2], cudaStream_t st);

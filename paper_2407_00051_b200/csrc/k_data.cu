@@ -116,43 +116,125 @@ void launch_constrain(const float* raw, float* c, int k, cudaStream_t st, bool t
 }
 
 // ---------------------------------------------------------------- sampler
+// Packed fp32 pairs (sm_100a FADD2 / FMUL2): each lane rounded exactly as the
+// scalar instruction, one issue slot per pair -- the two observables of an
+// event travel together.
+__device__ __forceinline__ uint64_t pk(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(uint64_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2_rm(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// the bits of 1 + (w >> 9) 2^-23 (uniform_open01) as one IMAD.HI on the FMA
+// pipe: hi(w * 2^23) + 0x3F800000 = (w >> 9) | 0x3F800000 (w >> 9 < 2^23)
+__device__ __forceinline__ uint32_t one_plus_bits(uint32_t w) {
+  uint32_t r;
+  asm("mad.hi.u32 %0, %1, 8388608, 1065353216;" : "=r"(r) : "r"(w));
+  return r;
+}
+// (u(wa), u(wb)) of R-UNIF, bitwise equal to uniform_open01 on each word
+__device__ __forceinline__ uint64_t uniform2(uint32_t wa, uint32_t wb) {
+  const uint64_t one_m = pk(__uint_as_float(one_plus_bits(wa)), __uint_as_float(one_plus_bits(wb)));
+  return fsub2(one_m, pk(0.99999994039535522461f, 0.99999994039535522461f));
+}
+// ptxas (CUDA 12.9) contracts mul.rn.f32x2 followed by add.rn.f32x2 into
+// FFMA2 -- even with -fmad=false and explicit .rn, unlike the scalar
+// instructions -- which would round u c2 + c1 once instead of twice.  An
+// XOR of the product's low word with a runtime zero (a kernel argument)
+// hides the producer from that peephole: one ALU op, bits unchanged.
+__device__ __forceinline__ uint64_t opaque(uint64_t x, uint32_t zero) {
+  uint64_t r;
+  asm("{.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\txor.b32 lo, lo, %2;\n\tmov.b64 %0, {lo, hi};}"
+      : "=l"(r) : "l"(x), "r"(zero));
+  return r;
+}
+// Q(u; c) of both observables (quantile_f32 per lane: four separately
+// rounded operations): c0 + u (c1 + u c2) with C_j = (c_j of observable 0,
+// c_j of observable 1)
+__device__ __forceinline__ uint64_t quantile2(uint64_t u, uint64_t C0, uint64_t C1, uint64_t C2, uint32_t zero) {
+  const uint64_t b = fadd2(C1, opaque(fmul2(u, C2), zero));
+  return fadd2(C0, opaque(fmul2(u, b), zero));
+}
+
+// Histogram bins of both observables (hist_bin per lane): t = (y - lo) sc,
+// clamp to [-1, bins], floor via the 1.5 * 2^23 rounding trick, + 1.
+__device__ __forceinline__ void bins2(uint64_t y, uint64_t LO, uint64_t SC, float fb, int& b0, int& b1) {
+  const float2 t = upk(fmul2(fsub2(y, LO), SC));
+  const float c0 = fminf(fmaxf(t.x, -1.0f), fb), c1 = fminf(fmaxf(t.y, -1.0f), fb);
+  const float2 r = upk(fadd2_rm(pk(c0, c1), pk(12582912.0f, 12582912.0f)));
+  b0 = __float_as_int(r.x) - 0x4B400000 + 1;
+  b1 = __float_as_int(r.y) - 0x4B400000 + 1;
+}
+
+// Shared histograms of a block: [4 = (real, fake) x obs][bins+2][32 lanes]
+// uint32 (lane-column layout: lane l of every warp increments column l, so
+// one ATOMS of a warp touches 32 distinct banks -- no intra-warp conflicts
+// however concentrated the distribution; warps meet only across
+// instructions).  Used when 512 (bins+2) bytes fit (bins <= 126); otherwise
+// one [4][bins+2] copy per block.
+constexpr int kSampleThreads = 512;
+__host__ __device__ constexpr bool hist_columns(int bins) { return bins + 2 <= 128; }
+
 // One thread = one group of 4 consecutive events e = 4g..4g+3:
 //   fake: Philox calls 2g and 2g+1 of stream FAKE give the 8 words 2e+o;
 //   real: call g of stream REAL gives the 4 bootstrap words (word e).
-// Histogram increment (shared-memory atomic into the warp's private copy).
-__device__ __forceinline__ void hist_add(uint32_t* h, int bin) { atomicAdd(h + bin, 1u); }
-
-// Rows of X: [0, N) real, [N, 2N) fake (R9).  Persistent grid (grid-stride
-// over groups).  Histograms are privatised per warp in shared memory when they
-// fit (no inter-warp contention), summed per block, and merged with integer
-// atomics (exact and order-independent).  The common group (all 4 events in
-// range and in one sample, 16-B aligned rows) runs a branch-free body; the
-// ragged tail and m % 4 != 0 take the general one.
+// Rows of X: [0, N) real, [N, 2N) fake (R9).  Persistent grid (2 blocks of
+// 512 per SM), grid-stride over groups; the common group (all 4 events in
+// range and in one sample, 16-B aligned rows) runs a branch-free body with
+// FADD2/FMUL2 pairs; the ragged tail and m % 4 != 0 take the general one.
+// Histograms: see hist_columns; per block one merge into the global counts
+// with integer atomics (exact, order-independent).
 // kFake = false: the real rows only (the tabulated sampler, R32, draws the fake rows)
 template <bool kReal, bool kHist, bool kFake = true>
-__global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int m, int64_t n_events,
-                                                const float2* __restrict__ shard, uint32_t n_shard,
-                                                PhiloxKey key, uint32_t step, uint32_t rank,
-                                                uint32_t fake_stream, float2* __restrict__ x_real,
-                                                float2* __restrict__ y_fake, uint32_t* __restrict__ real_idx,
-                                                uint32_t* __restrict__ hist, int bins, float lo0, float sc0,
-                                                float lo1, float sc1, int per_warp, int vec_ok) {
-  extern __shared__ uint32_t sh_hist[];  // [copies][2 sets][2 obs][bins+2]
-  const int hsz = 4 * (bins + 2);
-  const int copies = per_warp ? (int)(blockDim.x >> 5) : 1;
-  uint32_t* my = sh_hist + (per_warp ? (int)(threadIdx.x >> 5) * hsz : 0);
+__global__ void __launch_bounds__(kSampleThreads, 2)
+    k_sample(const float* __restrict__ c, int m, int64_t n_events, const float2* __restrict__ shard,
+             uint32_t n_shard, PhiloxKey key, uint32_t step, uint32_t rank, uint32_t fake_stream,
+             float2* __restrict__ x_real, float2* __restrict__ y_fake, uint32_t* __restrict__ real_idx,
+             uint32_t* __restrict__ hist, int bins, float lo0, float sc0, float lo1, float sc1, int vec_ok,
+             uint32_t zero) {
+  extern __shared__ uint32_t sh_hist[];
+  const int nb = bins + 2;
+  const bool cols = hist_columns(bins);
+  const int hwords = 4 * nb * (cols ? 32 : 1);
+  const int lane = threadIdx.x & 31;
   if (kHist) {
-    for (int i = threadIdx.x; i < hsz * copies; i += blockDim.x) sh_hist[i] = 0;
+    for (int i = threadIdx.x; i < hwords; i += blockDim.x) sh_hist[i] = 0;
     __syncthreads();
   }
+  // word offset of counter (h, bin) for this thread: (h nb + bin) 32 + lane, or h nb + bin
+  const int hstride = cols ? 32 : 1;
+  uint32_t* hbase = sh_hist + (cols ? lane : 0);
+  auto hadd = [&](int h, int bin) { atomicAdd(hbase + (h * nb + bin) * hstride, 1u); };
+  const float fb = (float)bins;
+  const uint64_t LO = pk(lo0, lo1), SC = pk(sc0, sc1);
   // event counts are < 2^31 (validated at the ABI), so 32-bit indices
   const uint32_t n = (uint32_t)n_events;
   const uint32_t ngroups = (n + 3) / 4;
   const bool m4 = (m & 3) == 0 && vec_ok;
-  uint32_t* hx0 = my;
-  uint32_t* hx1 = my + (bins + 2);
-  uint32_t* hy0 = my + 2 * (bins + 2);
-  uint32_t* hy1 = my + 3 * (bins + 2);
   const PhiloxRoundKeys rk = round_keys(key);
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
     uint4 wa = make_uint4(0, 0, 0, 0), wb = make_uint4(0, 0, 0, 0);
@@ -166,25 +248,37 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
     // sample of the group's first event: one division per group
     const uint32_t s = 4 * g / (uint32_t)m;
     const float* cs = c + 6 * (size_t)s;
-    float c0 = __ldg(cs + 0), c1 = __ldg(cs + 1), c2 = __ldg(cs + 2);
-    float c3 = __ldg(cs + 3), c4 = __ldg(cs + 4), c5 = __ldg(cs + 5);
+    uint64_t C0 = 0, C1 = 0, C2 = 0;
+    auto load_c = [&]() {
+      C0 = pk(__ldg(cs + 0), __ldg(cs + 3));
+      C1 = pk(__ldg(cs + 1), __ldg(cs + 4));
+      C2 = pk(__ldg(cs + 2), __ldg(cs + 5));
+    };
+    if (kFake) load_c();
     float2 yv[4], xv[4];
     uint32_t iv[4];
+    if (kReal) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) iv[q] = lemire(word_of(wr, q), n_shard);
+    }
     auto event = [&](int q) {
       if (kFake) {
-        yv[q].x = quantile_f32(uniform_open01(wf[2 * q]), c0, c1, c2);
-        yv[q].y = quantile_f32(uniform_open01(wf[2 * q + 1]), c3, c4, c5);
-      }
-      if (kHist && kFake) {
-        hist_add(hy0, hist_bin(yv[q].x, lo0, sc0, bins));
-        hist_add(hy1, hist_bin(yv[q].y, lo1, sc1, bins));
+        const uint64_t y = quantile2(uniform2(wf[2 * q], wf[2 * q + 1]), C0, C1, C2, zero);
+        yv[q] = upk(y);
+        if (kHist) {
+          int b0, b1;
+          bins2(y, LO, SC, fb, b0, b1);
+          hadd(2, b0);
+          hadd(3, b1);
+        }
       }
       if (kReal) {
-        iv[q] = lemire(word_of(wr, q), n_shard);
         xv[q] = __ldg(shard + iv[q]);
         if (kHist) {
-          hist_add(hx0, hist_bin(xv[q].x, lo0, sc0, bins));
-          hist_add(hx1, hist_bin(xv[q].y, lo1, sc1, bins));
+          int b0, b1;
+          bins2(pk(xv[q].x, xv[q].y), LO, SC, fb, b0, b1);
+          hadd(0, b0);
+          hadd(1, b1);
         }
       }
     };
@@ -193,14 +287,14 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
       for (int q = 0; q < 4; ++q) event(q);
       if (kFake) {
         float4* yf = reinterpret_cast<float4*>(y_fake + 4 * (size_t)g);
-        yf[0] = make_float4(yv[0].x, yv[0].y, yv[1].x, yv[1].y);
-        yf[1] = make_float4(yv[2].x, yv[2].y, yv[3].x, yv[3].y);
+        __stcs(yf, make_float4(yv[0].x, yv[0].y, yv[1].x, yv[1].y));
+        __stcs(yf + 1, make_float4(yv[2].x, yv[2].y, yv[3].x, yv[3].y));
       }
       if (kReal) {
         float4* xr = reinterpret_cast<float4*>(x_real + 4 * (size_t)g);
-        xr[0] = make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y);
-        xr[1] = make_float4(xv[2].x, xv[2].y, xv[3].x, xv[3].y);
-        *reinterpret_cast<uint4*>(real_idx + 4 * (size_t)g) = make_uint4(iv[0], iv[1], iv[2], iv[3]);
+        __stcs(xr, make_float4(xv[0].x, xv[0].y, xv[1].x, xv[1].y));
+        __stcs(xr + 1, make_float4(xv[2].x, xv[2].y, xv[3].x, xv[3].y));
+        __stcs(reinterpret_cast<uint4*>(real_idx + 4 * (size_t)g), make_uint4(iv[0], iv[1], iv[2], iv[3]));
       }
     } else {
       // general group: step across sample boundaries, stop at n
@@ -212,8 +306,7 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
         if (r == (uint32_t)m) {
           r = 0;
           cs += 6;
-          c0 = __ldg(cs + 0); c1 = __ldg(cs + 1); c2 = __ldg(cs + 2);
-          c3 = __ldg(cs + 3); c4 = __ldg(cs + 4); c5 = __ldg(cs + 5);
+          if (kFake) load_c();
         }
         ++r;
         event(q);
@@ -227,11 +320,20 @@ __global__ void __launch_bounds__(256) k_sample(const float* __restrict__ c, int
   }
   if (kHist) {
     __syncthreads();
-    const int off = kReal ? 0 : 2 * (bins + 2);
-    for (int i = off + threadIdx.x; i < hsz; i += blockDim.x) {
+    const int h0 = kReal ? 0 : 2, h1 = kFake ? 4 : 2;  // histograms this launch fills
+    for (int i = h0 * nb + threadIdx.x; i < h1 * nb; i += blockDim.x) {
       uint32_t v = 0;
-      for (int w = 0; w < copies; ++w) v += sh_hist[w * hsz + i];
-      if (v) atomicAdd(&hist[i - off], v);
+      if (cols) {
+        const uint4* p = reinterpret_cast<const uint4*>(sh_hist + i * 32);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 q = p[(j + threadIdx.x) & 7];  // rotated start: spread the banks
+          v += q.x + q.y + q.z + q.w;
+        }
+      } else {
+        v = sh_hist[i];
+      }
+      if (v) atomicAdd(&hist[i - (kReal ? 0 : 2 * nb)], v);
     }
   }
 }
@@ -240,35 +342,56 @@ static void hist_params(const float lo[2], const float hi[2], int bins, float* s
   for (int o = 0; o < 2; ++o) sc[o] = (float)bins / (hi[o] - lo[o]);  // fp32, as the oracle
 }
 
-// persistent launch shape: 2 blocks per SM; per-warp histogram copies when
-// 8 x 4 x (bins+2) counters fit comfortably in shared memory
-static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* smem, int* per_warp) {
+// persistent launch shape: up to 2 blocks of 512 per SM, fewer for small n
+// (about 4 groups per thread at least, so the per-block histogram set-up and
+// merge are amortised)
+static int g_sm_count = 0;
+static int sm_count() {
+  if (!g_sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sm_count <= 0) g_sm_count = 148;
+  }
+  return g_sm_count;
+}
+static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* smem) {
   const int64_t ngroups = (n + 3) / 4;
-  *blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ngroups + 255) / 256, 148 * 8));
-  *per_warp = hist && (8 * 4 * (bins + 2) * 4 <= 48 * 1024);
-  *smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) * (*per_warp ? 8 : 1) : 0;
+  const int64_t want = (ngroups + 4 * kSampleThreads - 1) / (4 * kSampleThreads);
+  *blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, 2 * (int64_t)sm_count()));
+  *smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) * (hist_columns(bins) ? 32 : 1) : 0;
+}
+
+template <bool R, bool H, bool F>
+static void set_smem_attr(size_t smem) {
+  static size_t done = 0;
+  if (smem > 48 * 1024 && smem > done) {
+    cudaFuncSetAttribute(k_sample<R, H, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    done = smem;
+  }
 }
 
 void launch_sample_step(const float* c, int k, int m, const float* shard, int64_t n_shard,
                         uint64_t seed, uint32_t step, uint32_t rank, float* x_events,
                         uint32_t* real_idx, uint32_t* hist, int bins, const float lo[2],
-                        const float hi[2], cudaStream_t st, bool fake) {
+                        const float hi[2], cudaStream_t st, bool fake, bool hist_zeroed) {
   const int64_t n = (int64_t)k * m;
   float sc[2];
   hist_params(lo, hi, bins, sc);
-  if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * (bins + 2), st);
-  int blocks, per_warp;
+  if (hist && !hist_zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * (bins + 2), st);
+  int blocks;
   size_t smem;
-  sample_shape(n, bins, hist != nullptr, &blocks, &smem, &per_warp);
+  sample_shape(n, bins, hist != nullptr, &blocks, &smem);
   float2* x = reinterpret_cast<float2*>(x_events);
   const int vec_ok = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(x_events) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(real_idx) % 16 == 0);
   auto kern = fake ? (hist ? k_sample<true, true> : k_sample<true, false>)
                    : (hist ? k_sample<true, true, false> : k_sample<true, false, false>);
-  kern<<<blocks, 256, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard),
-                                            (uint32_t)n_shard, make_key(seed), step, rank, kStreamFake,
-                                            x, x + n, real_idx, hist, bins, lo[0], sc[0], lo[1], sc[1], per_warp,
-                                            vec_ok);
+  if (fake && hist) set_smem_attr<true, true, true>(smem);
+  if (!fake && hist) set_smem_attr<true, true, false>(smem);
+  kern<<<blocks, kSampleThreads, smem, st>>>(c, m, n, reinterpret_cast<const float2*>(shard), (uint32_t)n_shard,
+                                             make_key(seed), step, rank, kStreamFake, x, x + n, real_idx, hist, bins,
+                                             lo[0], sc[0], lo[1], sc[1], vec_ok, 0u);
   count_launch();
 }
 
@@ -284,14 +407,15 @@ void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t 
     l[1] = lo[1];
     cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 2 * (bins + 2), st);
   }
-  int blocks, per_warp;
+  int blocks;
   size_t smem;
-  sample_shape(n, bins, hist != nullptr, &blocks, &smem, &per_warp);
+  sample_shape(n, bins, hist != nullptr, &blocks, &smem);
   const int vec_ok = reinterpret_cast<uintptr_t>(events) % 16 == 0;
   auto kern = hist ? k_sample<false, true> : k_sample<false, false>;
-  kern<<<blocks, 256, smem, st>>>(c, m, n, nullptr, 1, make_key(seed), step, rank, stream_id,
-                                             nullptr, reinterpret_cast<float2*>(events), nullptr, hist,
-                                             bins, l[0], sc[0], l[1], sc[1], per_warp, vec_ok);
+  if (hist) set_smem_attr<false, true, true>(smem);
+  kern<<<blocks, kSampleThreads, smem, st>>>(c, m, n, nullptr, 1, make_key(seed), step, rank, stream_id, nullptr,
+                                             reinterpret_cast<float2*>(events), nullptr, hist, bins, l[0], sc[0], l[1],
+                                             sc[1], vec_ok, 0u);
   count_launch();
 }
 

@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# the emulated-rank exchange tests (test_gpu_exchange_emulated.py) run up to
+# 16 streams of one process whose kernels wait on each other (bounded waits):
+# give every stream its own hardware queue so none is falsely serialised
+# behind another's waiting kernel (must be set before CUDA initialises)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
