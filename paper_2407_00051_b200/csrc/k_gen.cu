@@ -13,8 +13,10 @@
 //               db_l = colsum(dZ_l); dW lands in the packet layout
 // All sums run in a fixed order (deterministic); fp32 throughout.
 #include "ctx.h"
+#include "tc_util.cuh"
 
 namespace sagips {
+using tc::prefetch_l2;
 
 namespace {
 constexpr int kR = 8;         // rows per CTA (forward / dgrad)
@@ -49,6 +51,14 @@ struct GenArgs {
   int split_rows;
   float* part;
   int64_t wtot, btot;
+  // step prologue work riding on k_gen_fwd (the kernel before the sampler):
+  // an L2 prefetch of the bootstrap shard (the sampler's random 8-byte
+  // gathers then hit L2 instead of fetching 32-byte DRAM sectors) and the
+  // zeroing of the step's histograms (no separate memset node)
+  const char* prefetch;
+  int64_t prefetch_bytes;
+  uint32_t* zero_hist;
+  int zero_words;
 };
 
 // ---------------------------------------------------------------- forward
@@ -66,6 +76,14 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
   const int tid = threadIdx.x;
   const int r0 = blockIdx.x * kR;
   const int in0 = a.sizes[0];
+  if (a.prefetch && tid == 0) {  // this block's slice of the shard, in <= 32 KiB bulk prefetches
+    const int64_t per = ((a.prefetch_bytes + gridDim.x - 1) / gridDim.x + 15) & ~(int64_t)15;
+    const int64_t b0 = blockIdx.x * per, b1 = b0 + per < a.prefetch_bytes ? b0 + per : a.prefetch_bytes;
+    for (int64_t o = b0; o < b1; o += 32768)
+      prefetch_l2(a.prefetch + o, (uint32_t)(b1 - o < 32768 ? b1 - o : 32768));
+  }
+  if (a.zero_hist && blockIdx.x == 0)
+    for (int i = tid; i < a.zero_words; i += kGenThreads) a.zero_hist[i] = 0u;
   for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
     const int r = idx / in0, i = idx % in0;
     buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
@@ -338,13 +356,18 @@ static GenArgs gen_args(sagips_ctx* c) {
 
 static size_t gen_fwd_smem() { return sizeof(float) * (2 * kR * kGenMaxW + kGenMaxW * kLdFast); }
 
-void launch_gen_fwd(sagips_ctx* c, cudaStream_t st) {
+void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_t prefetch_bytes,
+                    uint32_t* zero_hist, int zero_words) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_gen_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_fwd_smem());
     configured = true;
   }
-  const GenArgs a = gen_args(c);
+  GenArgs a = gen_args(c);
+  a.prefetch = static_cast<const char*>(prefetch);
+  a.prefetch_bytes = (prefetch_bytes / 16) * 16;
+  a.zero_hist = zero_hist;
+  a.zero_words = zero_words;
   k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
   count_launch();
 }

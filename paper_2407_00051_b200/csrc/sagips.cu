@@ -863,8 +863,13 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
     launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
   // a2 generator forward (hidden LeakyReLU, linear output) + a3 constrain
   const bool fused_gen = gen_fused_ok(c);
+  const bool tab = g.sampler == SAGIPS_SAMPLER_TABULATED;
+  // the real rows come from the resident shard: prefetch it into L2 and zero
+  // the histograms inside the generator forward (the step's sampler follows)
+  const bool boot = !c->host_real;
   if (fused_gen) {
-    launch_gen_fwd(c, st);
+    launch_gen_fwd(c, st, boot ? c->shard : nullptr, boot ? 8 * g.shard_rows : 0, boot ? c->hist : nullptr,
+                   boot ? 4 * (g.hist_bins + 2) : 0);
   } else {
     const float* in = c->noise;
     for (int l = 0; l < G.L; ++l) {
@@ -876,7 +881,6 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
     launch_constrain(c->gAct[G.L - 1], c->cbuf, k, st, g.sampler == SAGIPS_SAMPLER_TABULATED);
   }
   const float* raw = c->gAct[G.L - 1];
-  const bool tab = g.sampler == SAGIPS_SAMPLER_TABULATED;
   // a4-a6 fused sampler + bootstrap + histograms (tabulated: the bootstrap
   // pass draws the real rows, the tabulated sampler the fake rows N..2N-1)
   mark(c, 1, st);
@@ -890,7 +894,7 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
                            c->hist + 2 * (g.hist_bins + 2), g.hist_bins, g.hist_lo, g.hist_hi, st);
   } else {
     launch_sample_step(c->cbuf, k, m, c->shard, g.shard_rows, g.seed, step, g.rank, c->X, c->real_idx, c->hist,
-                       g.hist_bins, g.hist_lo, g.hist_hi, st, !tab);
+                       g.hist_bins, g.hist_lo, g.hist_hi, st, !tab, fused_gen);
   }
   if (tab)
     launch_sample_tabulated(raw, k, m, tab_grid(g), g.seed, step, g.rank, kStreamFake,
