@@ -369,18 +369,20 @@ SAGIPS_API sagips_status sagips_connect_nccl(sagips_ctx* ctx, const void* host_i
  * n >= SAGIPS_NUM_PHASES floats. [sync]  Errors: STATE if timing is off. */
 SAGIPS_API sagips_status sagips_phase_times(sagips_ctx* ctx, float* host_ms, int32_t n, int32_t* steps_averaged);
 
-/* Tensor-core discriminator layer passes of a step (paper widths, depth >= 3,
- * per-layer kernels), in launch order: 0 D forward first layer, 1 D forward
- * middle layer(s), 2 D forward last hidden layer + head + BCE, 3 D backward
- * layer L-2 (wgrad + dgrad), 4 D backward middle layer(s), 5 D backward first
- * layer (+ layer-0 gradients); 6-11 the same for the G step (no wgrad; 11
- * yields dy).  With the pipelined step (SAGIPS_PIPE=1) the whole D step is
- * entry 0 and the whole G step entry 6.  Mean device ms per step (CUDA events
- * on the step stream around each launch; a class with several launches, e.g.
- * middle layers, sums them) over the last min(steps, 64) steps run with
- * cfg.phase_timing = 1; host_ms has n >= SAGIPS_NUM_KERNELS floats; unused
- * classes are 0. [sync]  Errors: STATE if timing is off or no step ran. */
-#define SAGIPS_NUM_KERNELS 12
+/* Tensor-core discriminator kernels of a step (paper widths, depth >= 3),
+ * in launch order: 0 D forward first layer, 1 D forward middle layer(s), 2 D
+ * forward last hidden layer + head + BCE, 3 D backward layer L-2 (wgrad +
+ * dgrad), 4 D backward middle layer(s), 5 D backward first layer (+ layer-0
+ * gradients); 6-11 the same for the G step (no wgrad; 11 yields dy); 12 the
+ * fused G step (k_gstep: all layers of the G step in one kernel, activations
+ * in tensor memory -- it replaces 6-11, depth 4); 13 the fused D forward
+ * (k_dfwd: layers 0-3 + head, replaces 0-2).  Mean device ms per step (CUDA
+ * events on the step stream around each launch; a class with several
+ * launches, e.g. middle layers, sums them) over the last min(steps, 64) steps
+ * run with cfg.phase_timing = 1; host_ms has n >= SAGIPS_NUM_KERNELS floats;
+ * unused classes are 0. [sync]  Errors: STATE if timing is off or no step
+ * ran. */
+#define SAGIPS_NUM_KERNELS 14
 SAGIPS_API sagips_status sagips_kernel_times(sagips_ctx* ctx, float* host_ms, int32_t n, int32_t* steps_averaged);
 /* Forget the recorded phase / kernel times (e.g. after warm-up steps, whose
  * first launches include lazy module loading). [sync] */

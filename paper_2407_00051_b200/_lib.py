@@ -122,9 +122,9 @@ EXPORTED = [
     "sagips_train_step_host", "sagips_window_ptr", "sagips_connect_peers_local"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
-NUM_KERNELS = 12
+NUM_KERNELS = 14
 KERNELS = ["d_fwd_first", "d_fwd_mid", "d_fwd_head", "d_bwd_last", "d_bwd_mid", "d_bwd_first",
-           "g_fwd_first", "g_fwd_mid", "g_fwd_head", "g_bwd_last", "g_bwd_mid", "g_bwd_dy"]
+           "g_fwd_first", "g_fwd_mid", "g_fwd_head", "g_bwd_last", "g_bwd_mid", "g_bwd_dy", "g_fused", "d_fwd_fused"]
 
 
 def _check(status, ctx=None):

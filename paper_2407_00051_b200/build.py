@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libsagips.so")
-SOURCES = ["sagips.cu", "k_data.cu", "k_mlp_simt.cu", "k_adam.cu", "exchange.cu", "k_tc_gemm.cu", "k_tc_layers.cu", "k_gen.cu", "k_ensemble.cu", "k_tabulated.cu"]
+SOURCES = ["sagips.cu", "k_data.cu", "k_mlp_simt.cu", "k_adam.cu", "exchange.cu", "k_tc_gemm.cu", "k_tc_layers.cu", "k_gen.cu", "k_ensemble.cu", "k_tabulated.cu", "k_fused.cu"]
 
 
 def nccl_dirs():

@@ -163,6 +163,22 @@ struct BwdLaunch {
   uint32_t* tile_ctr = nullptr;  // no wgrad (G step): dynamic tile schedule counter (zeroed before the launch)
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
+// k_fused.cu: the fused discriminator kernels (paper widths, depth 4)
+struct GStepArgs {
+  const float2* Y;         // [rows] fake events (D input rows)
+  int64_t rows;
+  const float* W[4];       // W_0 [128][2], W_1..W_3 [128][128]
+  const float* b[4];       // b_0..b_3 [128]
+  const float* w4;         // head [128]
+  const float* b4;         // head bias [1]
+  float alpha;
+  float scale;             // 1 / N
+  float* logits;           // [rows]
+  double* loss_part;       // [grid]
+  float2* dy;              // [rows]
+};
+int fused_grid(int64_t rows);
+void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st);
 int tc_layers_grid(int64_t rows);
 size_t plane_tile_bytes(bool split);
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st);

@@ -1,0 +1,448 @@
+// k_fused.cu -- the discriminator MLP (paper preset [2,128,128,128,128,1],
+// P:297, R4) on chip: ONE persistent kernel runs every layer of a tile,
+// forward and backward, without activations touching HBM.
+//
+// Where the data live (per CTA, one CTA per SM):
+//   shared memory  the three 128 x 128 hidden-layer weights W_1..W_3 as bf16
+//                  planes (hi, and lo = bf16(W - hi) for the fp32-class
+//                  split, R28): 6 x 32 KiB = 192 KiB, staged once per launch;
+//                  they are the B operand of every MMA -- K-major (forward,
+//                  D = A W^T) and MN-major (dgrad, D = A W) views of the same
+//                  bytes (tc_util.cuh SW128 layout);
+//   tensor memory  two tile slots of 256 columns: the fp32 accumulator of the
+//                  current layer (128 columns) and the current layer's INPUT
+//                  activations as the MMA's A operand (tcgen05.mma reads A
+//                  from TMEM: row m = lane m, bf16 pairs per 32-bit column;
+//                  hi in 64 columns, lo in 64) -- checked on B200 by
+//                  tests/tools/tmem_a_check.cu;
+//   registers      the LeakyReLU' sign bits of Z_1..Z_3 (64 bits per thread
+//                  and layer) for the backward.
+//
+// Warp roles (512 threads): warps 0-7 own tile slot 0, warps 8-15 tile slot
+// 1 (warp w of a group: TMEM lane quarter w % 4, column half w / 4 -- one
+// thread = one row, 64 columns).  When a group has written a layer's A
+// operand it meets at a named barrier and its first warp issues that layer's
+// MMAs (warp-converged, one elected lane) and commits them to the slot's
+// mbarrier.  While one slot's warps run an epilogue, the tensor core runs
+// the other slot's layer.  (A separate MMA warp would make 17 warps, 5 on one
+// SM sub-partition, capping every thread at 96 registers.)
+//
+// k_gstep (a8, the G step through the updated D, R8): per 128-row
+// tile of fake events Y:
+//   H_1 = LReLU(Y W_0^T + b_0)                       SIMT -> TMEM A
+//   Z_{l+1} = H_l W_l^T + b_l, H_{l+1} = LReLU(.)     MMA + epilogue, l = 1..3
+//   z = H_4 . w + b, L_G term softplus(-z), dz = (sigmoid(z) - 1) / N
+//   G_4 = dz w (.) LReLU'(Z_4)                        epilogue -> TMEM A
+//   G_l = (G_{l+1} W_l) (.) LReLU'(Z_l), l = 3..1     MMA (dgrad) + epilogue
+//   dy = G_1 W_0                                      epilogue -> HBM (8 B/row)
+// HBM traffic: 8 B/row in (Y), 8 B/row out (dy) + 4 B (logit); the weights
+// once per CTA.  Products (split): A*B ~= Ah*Bh + Ah*Bl + Al*Bh (bf16x3, fp32
+// accumulation), as the per-layer kernels.
+#include <cstdio>
+
+#include "ctx.h"
+#include "tc_util.cuh"
+
+namespace sagips {
+
+using namespace tc;
+
+namespace {
+
+constexpr int kGroupWarps = 8;                      // per tile slot
+constexpr int kThreadsF = 32 * 2 * kGroupWarps;     // 512
+constexpr uint32_t kPlaneF = 128 * 128 * 2;         // one bf16 plane of a 128 x 128 tile
+
+struct SmemVec {
+  float b[3][128];        // biases of W_1..W_3
+  float w4[128], aw4[128];  // head w, alpha w
+  float w0x[128], w0y[128], b0[128];
+  float xdot[2][128][2];  // per slot, per row: the two column halves' partial head dots
+  float xdy[2][128][4];   // per slot, per row: the two halves' partial dy (x, y)
+  double loss[kThreadsF / 32];
+  uint64_t acc_full[2];
+  uint32_t tmem;
+};
+
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk2(uint64_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a.x, a.y)), "l"(pk2(b.x, b.y)), "l"(pk2(c.x, c.y)));
+  return upk2(d);
+}
+// bf16x2 word {low half: bf16(a), high half: bf16(b)}, round to nearest even
+__device__ __forceinline__ uint32_t bf16x2_rn(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+// hi = bf16(a, b), lo = bf16(a - hi, b - hi)
+__device__ __forceinline__ void split2(float2 v, uint32_t& hi, uint32_t& lo) {
+  hi = bf16x2_rn(v.x, v.y);
+  const float2 d = sub2(v, make_float2(__uint_as_float(hi << 16), __uint_as_float(hi & 0xffff0000u)));
+  lo = bf16x2_rn(d.x, d.y);
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]: warp-converged, one elected lane issues
+__device__ __forceinline__ void mma_ts_warp(uint32_t d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// named barrier of one slot group (8 warps)
+__device__ __forceinline__ void group_sync(int s) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(32 * kGroupWarps) : "memory");
+}
+
+// W [128][128] fp32 -> hi (/ lo) planes, SW128 layout; all threads of the CTA
+template <bool kSplit>
+__device__ __forceinline__ void stage_w(const float* __restrict__ W, uint32_t hi, uint32_t lo) {
+  for (int idx = threadIdx.x; idx < 128 * 32; idx += kThreadsF) {
+    const int r = idx >> 5, c = 4 * (idx & 31);
+    const float4 x = __ldg(reinterpret_cast<const float4*>(W) + idx);
+    const uint32_t off = sw128_offset(r, c, 128);
+    uint32_t h0, h1, l0, l1;
+    split2(make_float2(x.x, x.y), h0, l0);
+    split2(make_float2(x.z, x.w), h1, l1);
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hi + off), "r"(h0), "r"(h1));
+    if (kSplit) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(lo + off), "r"(l0), "r"(l1));
+  }
+}
+
+}  // namespace
+
+
+
+// The MMAs of one layer of a tile slot: phases 0-2 forward W_1..W_3
+// (D = A W^T, K-major B), 3-5 dgrad W_3..W_1 (D = A W, MN-major B); A from the
+// slot's TMEM columns (hi at +128, lo at +192), accumulator at +0.  Called by
+// one whole warp (warp-converged issue, one elected lane), then committed.
+template <bool kSplit>
+__device__ __forceinline__ void issue_layer(uint32_t acc, uint32_t wbase, int p) {
+  constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
+  constexpr uint32_t idf = make_idesc_bf16(128, 128, 0, 0);  // A (TMEM, K-major) x W^T (K-major)
+  constexpr uint32_t idd = make_idesc_bf16(128, 128, 0, 1);  // A (TMEM) x W (MN-major)
+  const uint32_t ah = acc + 128u, al = acc + 192u;
+  const int l = p < 3 ? p : 5 - p;  // weight W_{l+1}
+  const uint32_t wh = wbase + l * TBw, wl = wh + kPlaneF;
+  if (p < 3) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t off = (k >> 2) * 16384 + (k & 3) * 32;
+      const uint64_t bh = make_desc(wh + off, 16, 1024);
+      mma_ts_warp(acc, ah + 8 * k, bh, idf, k > 0 ? 1u : 0u);
+      if (kSplit) {
+        mma_ts_warp(acc, al + 8 * k, bh, idf, 1u);
+        mma_ts_warp(acc, ah + 8 * k, make_desc(wl + off, 16, 1024), idf, 1u);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t off = k * 2048;
+      const uint64_t bh = make_desc(wh + off, 16384, 1024);
+      mma_ts_warp(acc, ah + 8 * k, bh, idd, k > 0 ? 1u : 0u);
+      if (kSplit) {
+        mma_ts_warp(acc, al + 8 * k, bh, idd, 1u);
+        mma_ts_warp(acc, ah + 8 * k, make_desc(wl + off, 16384, 1024), idd, 1u);
+      }
+    }
+  }
+}
+
+template <bool kSplit>
+__global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ GStepArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
+  SmemVec* sv = reinterpret_cast<SmemVec*>(smem + 3 * TBw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (smem_u32(smem) & 1023u) __trap();
+  const uint32_t wbase = smem_u32(smem);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) mbar_init(&sv->acc_full[s], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&sv->tmem);
+  for (int l = 0; l < 3; ++l) stage_w<kSplit>(a.W[l + 1], wbase + l * TBw, wbase + l * TBw + kPlaneF);
+  for (int i = tid; i < 128; i += kThreadsF) {
+    for (int l = 0; l < 3; ++l) sv->b[l][i] = a.b[l + 1][i];
+    sv->w4[i] = a.w4[i];
+    sv->aw4[i] = a.alpha * a.w4[i];
+    sv->w0x[i] = a.W[0][2 * i];
+    sv->w0y[i] = a.W[0][2 * i + 1];
+    sv->b0[i] = a.b[0][i];
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sv->tmem;
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int j = blockIdx.x, n = gridDim.x;
+  const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
+
+  // slot group s: thread = row 32 q + lane of the tile, columns 64 h .. 64 h + 63
+  const int s = warp >> 3, w8 = warp & 7, q = w8 & 3, h = w8 >> 2;
+  const int r = 32 * q + lane;
+  const uint32_t lanes = (uint32_t)(32 * q) << 16;
+  const uint32_t slot = tmem + 256u * s;
+  const uint32_t accT = slot + lanes + 64u * h;          // this thread's 64 accumulator columns
+  const uint32_t ahT = slot + 128u + lanes + 32u * h;    // its 32 A-hi columns (64 bf16)
+  const uint32_t alT = ahT + 64u;
+  const float2 alpha2 = make_float2(a.alpha, a.alpha);
+  const float b4 = *a.b4;
+  uint32_t acc_ph = 0;
+  double lacc = 0.0;
+  auto put_a = [&](int c, const uint32_t* hw, const uint32_t* lw) {
+    tmem_st16(ahT + 16u * c, hw);
+    if (kSplit) tmem_st16(alT + 16u * c, lw);
+  };
+  // the slot's A operand is complete: the group's first warp issues layer p
+  auto run_layer = [&](int p) {
+    tmem_st_wait();
+    tc_fence_before();
+    group_sync(s);
+    if (w8 == 0) {
+      tc_fence_after();
+      issue_layer<kSplit>(slot, wbase, p);
+      mma_commit_warp(&sv->acc_full[s]);
+    }
+    mbar_wait(&sv->acc_full[s], acc_ph & 1u);
+    ++acc_ph;
+    tc_fence_after();
+  };
+  for (int i = s; i < nmine; i += 2) {
+    const int64_t row = (int64_t)(j + (int64_t)i * n) * 128 + r;
+    const bool valid = row < a.rows;
+    const float2 x = valid ? __ldg(a.Y + row) : make_float2(0.f, 0.f);
+    uint32_t m1a, m1b, m2a, m2b, m3a, m3b;  // LeakyReLU' sign bits of Z_1..Z_3 (two 32-column chunks)
+    // H_1 = LeakyReLU(fma(x0, w0x, fma(x1, w0y, b0)))  (the per-layer kernels' order)
+    {
+      const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t hw[16], lw[16], m = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 wx = *reinterpret_cast<const float2*>(&sv->w0x[col]);
+          const float2 wy = *reinterpret_cast<const float2*>(&sv->w0y[col]);
+          const float2 bb = *reinterpret_cast<const float2*>(&sv->b0[col]);
+          const float2 z = fma2(X0, wx, fma2(X1, wy, bb));
+          const float2 t = mul2(z, alpha2);
+          split2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), hw[k], lw[k]);
+          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
+          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+        }
+        if (c == 0) m1a = m;
+        else m1b = m;
+        put_a(c, hw, lw);
+      }
+    }
+    // forward W_1, W_2: H_{l+1} = LeakyReLU(acc + b_l)
+#pragma unroll 1
+    for (int l = 0; l < 2; ++l) {
+      run_layer(l);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(accT + 32u * c, v);
+        uint32_t hw[16], lw[16], m = 0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[l][col]));
+          const float2 t = mul2(z, alpha2);
+          split2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), hw[k], lw[k]);
+          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
+          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+        }
+        if (l == 0) {
+          if (c == 0) m2a = m;
+          else m2b = m;
+        } else {
+          if (c == 0) m3a = m;
+          else m3b = m;
+        }
+        put_a(c, hw, lw);
+      }
+    }
+    // head: Z_4 = acc + b_3, z = LeakyReLU(Z_4) . w + b, dz, G_4 = dz (Z_4 > 0 ? w : alpha w)
+    {
+      run_layer(2);
+      uint32_t m4a = 0u, m4b = 0u;
+      float2 dot = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(accT + 32u * c, v);
+        uint32_t m = 0u;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
+          const float2 t = mul2(z, alpha2);
+          dot = fma2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), *reinterpret_cast<const float2*>(&sv->w4[col]), dot);
+          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
+          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+        }
+        if (c == 0) m4a = m;
+        else m4b = m;
+      }
+      sv->xdot[s][r][h] = dot.x + dot.y;
+      group_sync(s);
+      const float zz = (sv->xdot[s][r][0] + sv->xdot[s][r][1]) + b4;
+      const float dz = valid ? (sigmoid_f(zz) - 1.0f) * a.scale : 0.f;
+      if (valid && h == 0) {
+        a.logits[row] = zz;
+        lacc += (double)softplus_neg(zz);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint32_t m = c == 0 ? m4a : m4b;
+        uint32_t hw[16], lw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 w = *reinterpret_cast<const float2*>(&sv->w4[col]);
+          const float2 wa = *reinterpret_cast<const float2*>(&sv->aw4[col]);
+          const float2 g = make_float2(dz * (((m >> (2 * k)) & 1u) ? w.x : wa.x),
+                                       dz * (((m >> (2 * k + 1)) & 1u) ? w.y : wa.y));
+          split2(g, hw[k], lw[k]);
+        }
+        put_a(c, hw, lw);
+      }
+    }
+    // dgrad W_3, W_2: G_l = acc (.) LeakyReLU'(Z_l)
+#pragma unroll 1
+    for (int l = 0; l < 2; ++l) {
+      run_layer(3 + l);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(accT + 32u * c, v);
+        const uint32_t m = (l == 0) ? (c == 0 ? m3a : m3b) : (c == 0 ? m2a : m2b);
+        uint32_t hw[16], lw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float2 g = make_float2(v[2 * k] * (((m >> (2 * k)) & 1u) ? 1.f : a.alpha),
+                                       v[2 * k + 1] * (((m >> (2 * k + 1)) & 1u) ? 1.f : a.alpha));
+          split2(g, hw[k], lw[k]);
+        }
+        put_a(c, hw, lw);
+      }
+    }
+    // dgrad W_1: G_1 = acc (.) LeakyReLU'(Z_1), dy = G_1 W_0
+    {
+      run_layer(5);
+      float2 dx = make_float2(0.f, 0.f), dyy = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(accT + 32u * c, v);
+        const uint32_t m = c == 0 ? m1a : m1b;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 g = make_float2(v[2 * k] * (((m >> (2 * k)) & 1u) ? 1.f : a.alpha),
+                                       v[2 * k + 1] * (((m >> (2 * k + 1)) & 1u) ? 1.f : a.alpha));
+          dx = fma2(g, *reinterpret_cast<const float2*>(&sv->w0x[col]), dx);
+          dyy = fma2(g, *reinterpret_cast<const float2*>(&sv->w0y[col]), dyy);
+        }
+      }
+      *reinterpret_cast<float2*>(&sv->xdy[s][r][2 * h]) = make_float2(dx.x + dx.y, dyy.x + dyy.y);
+      tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
+      group_sync(s);
+      if (h == 0 && valid) {
+        const float4 p = *reinterpret_cast<const float4*>(&sv->xdy[s][r][0]);
+        a.dy[row] = make_float2(p.x + p.z, p.y + p.w);
+      }
+    }
+  }
+  // this CTA's loss partial (fp64), warps in order
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
+  if (lane == 0) sv->loss[warp] = lacc;
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreadsF / 32; ++w) sum += sv->loss[w];
+    a.loss_part[j] = sum;
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+static int sm_count_f() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+static size_t gstep_smem(bool split) { return 3 * (split ? 2 : 1) * kPlaneF + sizeof(SmemVec) + 1024; }
+
+int fused_grid(int64_t rows) {
+  return (int)std::min<int64_t>(std::max<int64_t>((rows + 127) / 128, 1), sm_count_f());
+}
+
+void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st) {
+  static bool configured[2] = {false, false};
+  const size_t smem = gstep_smem(split);
+  auto kern = split ? k_gstep<true> : k_gstep<false>;
+  if (!configured[split]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[split] = true;
+  }
+  kern<<<fused_grid(a.rows), kThreadsF, smem, st>>>(a);
+  count_launch();
+}
+
+}  // namespace sagips

@@ -592,12 +592,43 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   disc_reduce_adam(c, grid, nparts, grid, st);
 }
 
+// the fused G step (k_fused.cu): paper widths, depth 4; SAGIPS_FUSED=0 keeps the per-layer kernels
+static bool use_fused(const sagips_ctx* c) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SAGIPS_FUSED");
+    env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return env && c->use_tc && c->cfg.disc_depth == 4 && c->cfg.disc_hidden == 128;
+}
+
 static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
   const auto& D = c->D;
   const int64_t N = c->N;
   const int Lh = D.L - 1;
   const bool split = tc_split(c);
   const float* Y = c->X + 2 * N;  // fake rows
+  if (use_fused(c)) {
+    GStepArgs a{};
+    a.Y = reinterpret_cast<const float2*>(Y);
+    a.rows = N;
+    for (int l = 0; l < 4; ++l) {
+      a.W[l] = c->dW + D.w_off[l];
+      a.b[l] = c->dB + D.b_off[l];
+    }
+    a.w4 = c->dW + D.w_off[4];
+    a.b4 = c->dB + D.b_off[4];
+    a.alpha = c->cfg.leaky_slope;
+    a.scale = 1.0f / (float)N;
+    a.logits = c->logits_g;
+    a.loss_part = c->loss_part;
+    a.dy = reinterpret_cast<float2*>(c->dy);
+    kernel_begin(c, 12, st);
+    launch_gstep(split, a, st);
+    kernel_end(c, st);
+    launch_finish_loss(c->loss_part, fused_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
+    return;
+  }
   reset_tile_ctrs(c, st);
   disc_forward_v2(c, Y, N, 0, 1.0f, 1.0f / (float)N, c->logits_g, false, st);
   launch_finish_loss(c->loss_part, tc_layers_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
