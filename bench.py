@@ -253,7 +253,11 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
         "g_fwd_head": (rows_g, 2 * E + 4, G, px * G, 1),
         "g_bwd_last": (rows_g, 2 * E + 16, G, px * G, 1),
         "g_bwd_mid": (rows_g, 2 * E + 16, G, px * G, mids),
-        "g_bwd_dy": (rows_g, E + 16, G, px * G, 1)}
+        "g_bwd_dy": (rows_g, E + 16, G, px * G, 1),
+        # fused G step (k_gstep): 3 forward + 3 dgrad GEMMs per row, activations on chip (8 B in, 8 B out)
+        "g_fused": (rows_g, 8 + 8 + 4, 6 * G, 6 * px * G, 1),
+        # fused D forward (k_dfwd): 3 GEMMs per row; X in, H_2 / H_3 hi planes + masks and G_4 planes out
+        "d_fwd_fused": (rows_d, 8 + 2 * (E // 2 + 16) + E + 4, 3 * G, 3 * px * G, 1)}
     try:
         kt, _ = ctx.kernel_times()
     except Exception:
@@ -285,7 +289,7 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
             "executed_frac": d["tensor_TFLOPs_executed"] / tc,
             "hbm_view": {"achieved_GBps": d["GBps"], "peak": hbm, "frac": d["GBps"] / hbm,
                          "design_bytes_per_row": spec[dom][1]}}
-    roof.update({"kernel": f"{dom} (tcgen05 layer pass, {d['launches_per_step']} launch(es)/step)",
+    roof.update({"kernel": f"{dom} (tcgen05 kernel, {d['launches_per_step']} launch(es)/step)",
                  "frac": roof["achieved"] / roof["peak"], "traffic": None, "ms_per_launch": d["ms"] / d["launches_per_step"],
                  "floors_ms": {"hbm": d["t_hbm_ms"], "tensor": d["t_tensor_ms"]},
                  "timing": "CUDA events on the step stream around each launch, mean over the timed steps"})

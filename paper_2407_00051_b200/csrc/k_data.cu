@@ -342,9 +342,9 @@ static void hist_params(const float lo[2], const float hi[2], int bins, float* s
   for (int o = 0; o < 2; ++o) sc[o] = (float)bins / (hi[o] - lo[o]);  // fp32, as the oracle
 }
 
-// persistent launch shape: up to 2 blocks of 512 per SM, fewer for small n
-// (about 4 groups per thread at least, so the per-block histogram set-up and
-// merge are amortised)
+// persistent launch shape: up to 2 blocks of 512 per SM (all SMs busy: at
+// 2^20 events, ~1.7 groups per thread; the kernel is latency-bound there --
+// ncu: 25% occupancy and 35% idle SM cycles with 128 blocks)
 static int g_sm_count = 0;
 static int sm_count() {
   if (!g_sm_count) {
@@ -357,7 +357,7 @@ static int sm_count() {
 }
 static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* smem) {
   const int64_t ngroups = (n + 3) / 4;
-  const int64_t want = (ngroups + 4 * kSampleThreads - 1) / (4 * kSampleThreads);
+  const int64_t want = (ngroups + kSampleThreads - 1) / kSampleThreads;
   *blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, 2 * (int64_t)sm_count()));
   *smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) * (hist_columns(bins) ? 32 : 1) : 0;
 }
@@ -423,26 +423,40 @@ void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t 
 // One block per parameter sample s:
 //   dc[o][j] = sum_{e in s} dy[e][o] * u[e][o]^j   (dQ/dc = (1, u, u^2))
 //   draw[s][3o] = dc[o][0], draw[s][3o+1] = dc[o][1] softplus'(raw), ...
-// u is recomputed from the FAKE stream (not stored).  The block reduction has
-// a fixed order, so the result is deterministic.
+// u is recomputed from the FAKE stream (not stored): one Philox call serves
+// the event pair 2q, 2q+1 (words 0,1 and 2,3), so a thread takes pairs when
+// the sample starts on an even event (m even), else single events.  The
+// block reduction has a fixed order, so the result is deterministic.
 __global__ void __launch_bounds__(256) k_sample_bwd(const float2* __restrict__ dy, const float* __restrict__ raw,
                                                     int m, PhiloxKey key, uint32_t step, uint32_t rank,
                                                     float* __restrict__ draw) {
   const int s = blockIdx.x;
   float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  for (int i = threadIdx.x; i < m; i += blockDim.x) {
-    const int64_t e = (int64_t)s * m + i;
-    const uint4 w = philox_call(key, (uint32_t)(e >> 1), step, rank, kStreamFake);
-    const bool odd = e & 1;
-    const float u0 = uniform_open01(odd ? w.z : w.x);
-    const float u1 = uniform_open01(odd ? w.w : w.y);
-    const float2 g = dy[e];
+  auto add = [&](float2 g, float u0, float u1) {
     acc[0] += g.x;
     acc[1] += g.x * u0;
     acc[2] += g.x * u0 * u0;
     acc[3] += g.y;
     acc[4] += g.y * u1;
     acc[5] += g.y * u1 * u1;
+  };
+  const int64_t e0 = (int64_t)s * m;
+  if ((m & 1) == 0) {
+    const PhiloxRoundKeys rk = round_keys(key);
+    for (int i = 2 * threadIdx.x; i < m; i += 2 * blockDim.x) {
+      const int64_t e = e0 + i;
+      const uint4 w = philox4x32_10(make_uint4((uint32_t)(e >> 1), step, rank, kStreamFake), rk);
+      const float4 g = __ldcs(reinterpret_cast<const float4*>(dy + e));
+      add(make_float2(g.x, g.y), uniform_open01(w.x), uniform_open01(w.y));
+      add(make_float2(g.z, g.w), uniform_open01(w.z), uniform_open01(w.w));
+    }
+  } else {
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const int64_t e = e0 + i;
+      const uint4 w = philox_call(key, (uint32_t)(e >> 1), step, rank, kStreamFake);
+      const bool odd = e & 1;
+      add(dy[e], uniform_open01(odd ? w.z : w.x), uniform_open01(odd ? w.w : w.y));
+    }
   }
   __shared__ float red[6][32];
 #pragma unroll
@@ -465,7 +479,8 @@ __global__ void __launch_bounds__(256) k_sample_bwd(const float2* __restrict__ d
 
 void launch_sample_bwd(const float* dy, const float* raw, int k, int m, uint64_t seed, uint32_t step,
                        uint32_t rank, float* draw, cudaStream_t st) {
-  int threads = 32 * ((std::min(m, 256) + 31) / 32);
+  const int per = (m % 2 == 0) ? (m + 1) / 2 : m;  // work items per sample
+  int threads = 32 * ((std::min(per, 256) + 31) / 32);
   k_sample_bwd<<<k, threads, 0, st>>>(reinterpret_cast<const float2*>(dy), raw, m, make_key(seed),
                                       step, rank, draw);
   count_launch();
