@@ -177,8 +177,29 @@ struct GStepArgs {
   double* loss_part;       // [grid]
   float2* dy;              // [rows]
 };
+struct DFwdArgs {
+  const float2* X;         // [rows] D input rows (real then fake)
+  int64_t rows;
+  int64_t n_real;          // rows < n_real have label 1, the rest label_rest
+  float label_rest;
+  float scale;             // 1 / rows
+  const float* W[4];       // W_0 [128][2], W_1..W_3 [128][128]
+  const float* b[4];
+  const float* w4;
+  const float* b4;
+  float alpha;
+  float* logits;           // [rows]
+  double* loss_part;       // [grid]
+  float* part_head;        // [grid][129]: dW_head, db_head partials
+  uint8_t* h2;             // H_2 plane tiles (hi plane written) + masks
+  uint4* m2;
+  uint8_t* h3;             // H_3 plane tiles (hi plane written) + masks
+  uint4* m3;
+  uint8_t* g4;             // G_4 plane tiles (hi + lo)
+};
 int fused_grid(int64_t rows);
 void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st);
+void launch_dfwd(bool split, const DFwdArgs& a, cudaStream_t st);
 int tc_layers_grid(int64_t rows);
 size_t plane_tile_bytes(bool split);
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st);

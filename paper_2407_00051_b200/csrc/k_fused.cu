@@ -59,6 +59,7 @@ struct SmemVec {
   float w0x[128], w0y[128], b0[128];
   float xdot[2][128][2];  // per slot, per row: the two column halves' partial head dots
   float xdy[2][128][4];   // per slot, per row: the two halves' partial dy (x, y)
+  float red[16 * 65];     // per-CTA partials at the end (k_dfwd head gradient)
   double loss[kThreadsF / 32];
   uint64_t acc_full[2];
   uint32_t tmem;
@@ -146,6 +147,40 @@ __device__ __forceinline__ void stage_w(const float* __restrict__ W, uint32_t hi
     split2(make_float2(x.z, x.w), h1, l1);
     asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(hi + off), "r"(h0), "r"(h1));
     if (kSplit) asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(lo + off), "r"(l0), "r"(l1));
+  }
+}
+
+// Activation sign masks of the per-layer kernels' HBM format (16 B per row,
+// 32 bits per 32-column block: column 2k is bit k, column 2k+1 bit 16 + k,
+// set iff bf16(H) > 0, R30), from the packed hi word of a pair
+__device__ __forceinline__ uint32_t pos_bits(uint32_t hi, int k) {
+  uint32_t gt;
+  asm("set.gt.u32.bf16x2 %0, %1, %2;" : "=r"(gt) : "r"(hi), "r"(0u));
+  return gt & (0x00010001u << k);
+}
+// reduce-scatter over the warp's 32 rows: on return lane l holds the sum over
+// lanes of g[l] (fixed order; g is destroyed)
+__device__ __forceinline__ float colsum32(float (&g)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool upper = (lane & w) != 0;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float send = upper ? g[k] : g[k + w];
+      const float recv = __shfl_xor_sync(0xffffffffu, send, w);
+      g[k] = (upper ? g[k + w] : g[k]) + recv;
+    }
+  }
+  return g[0];
+}
+// 16 packed words = columns 32 c .. 32 c + 31 of column half h, row r of a
+// plane tile (SW128 layout of the per-layer kernels): 4 chunks of 16 bytes
+__device__ __forceinline__ void store_plane_words(uint8_t* plane, int r, int h, int c, const uint32_t* w) {
+  uint8_t* row = plane + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    const int jc = 4 * c + jj;
+    *reinterpret_cast<uint4*>(row + ((jc ^ (r & 7)) << 4)) = make_uint4(w[4 * jj], w[4 * jj + 1], w[4 * jj + 2], w[4 * jj + 3]);
   }
 }
 
@@ -416,6 +451,218 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
   }
 }
 
+
+// k_dfwd (a7, the forward half of the D step on [X_real; Y_fake], P:93,
+// P:146): per 128-row tile, H_1 (SIMT) -> three MMA layers with the
+// activations in TMEM (as k_gstep) -> head: z, BCE (labels 1 for rows <
+// n_real, else label_rest), dz, G_4 = dz w (.) LeakyReLU'(Z_4).  What the
+// per-layer backward passes read goes to HBM in their plane-tile format: the
+// hi planes and sign masks of H_2 and H_3 (the wgrad uses the hi plane only,
+// R28) and the G_4 planes; plus the logits, the per-CTA loss and the head
+// gradient partials (dW_head = sum dz H_4, db_head = sum dz).
+template <bool kSplit>
+__global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ DFwdArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
+  constexpr int64_t TB = (kSplit ? 2 : 1) * (int64_t)kPlaneF;  // HBM plane tile
+  SmemVec* sv = reinterpret_cast<SmemVec*>(smem + 3 * TBw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (smem_u32(smem) & 1023u) __trap();
+  const uint32_t wbase = smem_u32(smem);
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) mbar_init(&sv->acc_full[s], 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&sv->tmem);
+  for (int l = 0; l < 3; ++l) stage_w<kSplit>(a.W[l + 1], wbase + l * TBw, wbase + l * TBw + kPlaneF);
+  for (int i = tid; i < 128; i += kThreadsF) {
+    for (int l = 0; l < 3; ++l) sv->b[l][i] = a.b[l + 1][i];
+    sv->w4[i] = a.w4[i];
+    sv->aw4[i] = a.alpha * a.w4[i];
+    sv->w0x[i] = a.W[0][2 * i];
+    sv->w0y[i] = a.W[0][2 * i + 1];
+    sv->b0[i] = a.b[0][i];
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sv->tmem;
+  const int64_t ntiles = (a.rows + 127) / 128;
+  const int j = blockIdx.x, n = gridDim.x;
+  const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
+
+  const int s = warp >> 3, w8 = warp & 7, q = w8 & 3, h = w8 >> 2;
+  const int r = 32 * q + lane;
+  const uint32_t lanes = (uint32_t)(32 * q) << 16;
+  const uint32_t slot = tmem + 256u * s;
+  const uint32_t accT = slot + lanes + 64u * h;
+  const uint32_t ahT = slot + 128u + lanes + 32u * h;
+  const uint32_t alT = ahT + 64u;
+  const float2 alpha2 = make_float2(a.alpha, a.alpha);
+  const float b4 = *a.b4;
+  uint32_t acc_ph = 0;
+  double lacc = 0.0;
+  float gacc0 = 0.f, gacc1 = 0.f, gbacc = 0.f;  // head gradient partials: columns 64 h + lane, 64 h + 32 + lane; dz
+  auto put_a = [&](int c, const uint32_t* hw, const uint32_t* lw) {
+    tmem_st16(ahT + 16u * c, hw);
+    if (kSplit) tmem_st16(alT + 16u * c, lw);
+  };
+  auto run_layer = [&](int p) {
+    tmem_st_wait();
+    tc_fence_before();
+    group_sync(s);
+    if (w8 == 0) {
+      tc_fence_after();
+      issue_layer<kSplit>(slot, wbase, p);
+      mma_commit_warp(&sv->acc_full[s]);
+    }
+    mbar_wait(&sv->acc_full[s], acc_ph & 1u);
+    ++acc_ph;
+    tc_fence_after();
+  };
+  for (int i = s; i < nmine; i += 2) {
+    const int64_t t = (int64_t)j + (int64_t)i * n;
+    const int64_t row = t * 128 + r;
+    const bool valid = row < a.rows;
+    const float2 x = valid ? __ldg(a.X + row) : make_float2(0.f, 0.f);
+    {  // H_1
+      const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t hw[16], lw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 wx = *reinterpret_cast<const float2*>(&sv->w0x[col]);
+          const float2 wy = *reinterpret_cast<const float2*>(&sv->w0y[col]);
+          const float2 bb = *reinterpret_cast<const float2*>(&sv->b0[col]);
+          const float2 z = fma2(X0, wx, fma2(X1, wy, bb));
+          const float2 tt = mul2(z, alpha2);
+          split2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), hw[k], lw[k]);
+        }
+        put_a(c, hw, lw);
+      }
+    }
+    // W_1, W_2: H_{l+1} -> TMEM A and, hi plane + mask, to HBM (H_2, H_3)
+#pragma unroll 1
+    for (int l = 0; l < 2; ++l) {
+      run_layer(l);
+      uint8_t* plane = (l == 0 ? a.h2 : a.h3) + t * TB;
+      uint32_t mb[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld32(accT + 32u * c, v);
+        uint32_t hw[16], lw[16], m = 0u;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[l][col]));
+          const float2 tt = mul2(z, alpha2);
+          split2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), hw[k], lw[k]);
+          m |= pos_bits(hw[k], k);
+        }
+        put_a(c, hw, lw);
+        if (!valid) {  // rows past the end are zeros in HBM (the backward reads whole tiles)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) hw[k] = 0u;
+          m = 0u;
+        }
+        mb[c] = m;
+        store_plane_words(plane, r, h, c, hw);
+      }
+      reinterpret_cast<uint2*>((l == 0 ? a.m2 : a.m3) + t * 128 + r)[h] = make_uint2(mb[0], mb[1]);
+    }
+    // head
+    run_layer(2);
+    float2 dot = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v[32];
+      tmem_ld32(accT + 32u * c, v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int col = 64 * h + 32 * c + 2 * k;
+        const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
+        const float2 tt = mul2(z, alpha2);
+        dot = fma2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), *reinterpret_cast<const float2*>(&sv->w4[col]), dot);
+      }
+    }
+    sv->xdot[s][r][h] = dot.x + dot.y;
+    group_sync(s);
+    const float zz = (sv->xdot[s][r][0] + sv->xdot[s][r][1]) + b4;
+    const float tl = (row < a.n_real) ? 1.f : a.label_rest;
+    const float dz = valid ? (sigmoid_f(zz) - tl) * a.scale : 0.f;
+    if (valid && h == 0) {
+      a.logits[row] = zz;
+      lacc += (double)(tl * softplus_neg(zz) + (1.f - tl) * softplus_neg(-zz));
+      gbacc += dz;
+    }
+    uint8_t* gplane = a.g4 + t * TB;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float v[32];
+      tmem_ld32(accT + 32u * c, v);
+      uint32_t hw[16], lw[16];
+      float g[32];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int col = 64 * h + 32 * c + 2 * k;
+        const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
+        const float2 tt = mul2(z, alpha2);
+        g[2 * k] = dz * fmaxf(z.x, tt.x);       // dz H_4 (head weight gradient)
+        g[2 * k + 1] = dz * fmaxf(z.y, tt.y);
+        const float2 w = *reinterpret_cast<const float2*>(&sv->w4[col]);
+        const float2 wa = *reinterpret_cast<const float2*>(&sv->aw4[col]);
+        split2(make_float2(dz * (z.x > 0.f ? w.x : wa.x), dz * (z.y > 0.f ? w.y : wa.y)), hw[k], lw[k]);
+      }
+      store_plane_words(gplane, r, h, c, hw);
+      if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
+      const float cs = colsum32(g, lane);
+      if (c == 0) gacc0 += cs;
+      else gacc1 += cs;
+    }
+    tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
+  }
+  // per-CTA partials in a fixed order: head gradient [128] + bias, loss (fp64)
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
+    gbacc += __shfl_xor_sync(0xffffffffu, gbacc, w);
+  }
+  float* sred = sv->red;  // [16 warps][64 + 1]
+  tc_fence_before();
+  __syncthreads();
+  sred[warp * 65 + lane] = gacc0;
+  sred[warp * 65 + 32 + lane] = gacc1;
+  if (lane == 0) {
+    sred[warp * 65 + 64] = gbacc;
+    sv->loss[warp] = lacc;
+  }
+  __syncthreads();
+  if (tid < 129) {
+    float v = 0.f;
+    if (tid < 128) {
+      const int hh = tid >> 6, cc = tid & 63;
+      for (int ss = 0; ss < 2; ++ss)
+        for (int qq = 0; qq < 4; ++qq) v += sred[(8 * ss + 4 * hh + qq) * 65 + cc];
+    } else {
+      for (int w = 0; w < 16; ++w) v += sred[w * 65 + 64];
+    }
+    a.part_head[(int64_t)j * 129 + tid] = v;
+  }
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kThreadsF / 32; ++w) sum += sv->loss[w];
+    a.loss_part[j] = sum;
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 static int sm_count_f() {
   static int n = 0;
   if (!n) {
@@ -431,6 +678,18 @@ static size_t gstep_smem(bool split) { return 3 * (split ? 2 : 1) * kPlaneF + si
 
 int fused_grid(int64_t rows) {
   return (int)std::min<int64_t>(std::max<int64_t>((rows + 127) / 128, 1), sm_count_f());
+}
+
+void launch_dfwd(bool split, const DFwdArgs& a, cudaStream_t st) {
+  static bool configured[2] = {false, false};
+  const size_t smem = gstep_smem(split);
+  auto kern = split ? k_dfwd<true> : k_dfwd<false>;
+  if (!configured[split]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured[split] = true;
+  }
+  kern<<<fused_grid(a.rows), kThreadsF, smem, st>>>(a);
+  count_launch();
 }
 
 void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st) {

@@ -495,12 +495,43 @@ static bool h1_store() {
   return v == 1;
 }
 
+static bool use_fused(const sagips_ctx* c);
+
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
   const int kc = want_grads ? 0 : 6;  // kernel-timing classes
   const bool split = tc_split(c);
   const auto& D = c->D;
   const int Lh = D.L - 1;
+  if (want_grads && use_fused(c) && !h1_store()) {
+    // the D step's forward in one kernel (k_fused.cu): H_2 / H_3 hi planes and
+    // masks and the G_4 planes for the per-layer backward passes
+    DFwdArgs f{};
+    f.X = reinterpret_cast<const float2*>(X);
+    f.rows = rows;
+    f.n_real = n_real;
+    f.label_rest = label_rest;
+    f.scale = scale;
+    for (int l = 0; l < 4; ++l) {
+      f.W[l] = c->dW + D.w_off[l];
+      f.b[l] = c->dB + D.b_off[l];
+    }
+    f.w4 = c->dW + D.w_off[4];
+    f.b4 = c->dB + D.b_off[4];
+    f.alpha = c->cfg.leaky_slope;
+    f.logits = logits;
+    f.loss_part = c->loss_part;
+    f.part_head = c->part;
+    f.h2 = reinterpret_cast<uint8_t*>(c->dAct[1]);
+    f.m2 = c->dMask[1];
+    f.h3 = reinterpret_cast<uint8_t*>(c->dAct[2]);
+    f.m3 = c->dMask[2];
+    f.g4 = reinterpret_cast<uint8_t*>(c->dZb[0]);
+    kernel_begin(c, 13, st);
+    launch_dfwd(split, f, st);
+    kernel_end(c, st);
+    return;
+  }
   FwdLaunch f;  // H_2 = LeakyReLU(H_1 W_1^T + b_1), H_1 recomputed from X
   f.X = X; f.W0 = c->dW + D.w_off[0]; f.b0 = c->dB + D.b_off[0]; f.first_help = first_help();
   f.W = c->dW + D.w_off[1]; f.bias = c->dB + D.b_off[1]; f.out = whole(c->dAct[1], c->dMask[1]);
