@@ -176,6 +176,7 @@ struct GStepArgs {
   float* logits;           // [rows]
   double* loss_part;       // [grid]
   float2* dy;              // [rows]
+  unsigned long long* trace;  // diagnostic (SAGIPS_FUSED_TRACE=1): CTA 0 phase stamps, else nullptr
 };
 struct DFwdArgs {
   const float2* X;         // [rows] D input rows (real then fake)
@@ -196,10 +197,13 @@ struct DFwdArgs {
   uint8_t* h3;             // H_3 plane tiles (hi plane written) + masks
   uint4* m3;
   uint8_t* g4;             // G_4 plane tiles (hi + lo)
+  unsigned long long* trace;  // diagnostic (SAGIPS_FUSED_TRACE=1), else nullptr
 };
 int fused_grid(int64_t rows);
 void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st);
 void launch_dfwd(bool split, const DFwdArgs& a, cudaStream_t st);
+unsigned long long* fused_trace_buffer();  // nullptr unless SAGIPS_FUSED_TRACE=1
+void fused_trace_report();                 // prints the phase breakdown of the last traced launch
 int tc_layers_grid(int64_t rows);
 size_t plane_tile_bytes(bool split);
 void launch_tc_fwd(bool split, int kind, const FwdLaunch& L, cudaStream_t st);

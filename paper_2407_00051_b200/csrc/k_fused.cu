@@ -39,6 +39,8 @@
 // once per CTA.  Products (split): A*B ~= Ah*Bh + Ah*Bl + Al*Bh (bf16x3, fp32
 // accumulation), as the per-layer kernels.
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "ctx.h"
 #include "tc_util.cuh"
@@ -150,6 +152,21 @@ __device__ __forceinline__ void stage_w(const float* __restrict__ W, uint32_t hi
   }
 }
 
+
+// shared-memory vector reads that stay where they are written (the compiler
+// would otherwise hoist the loop-invariant parameter reads out of the tile
+// loop and spill them: LDS is cheaper than LDL)
+__device__ __forceinline__ float4 lds4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(smem_u32(p)));
+  return v;
+}
+__device__ __forceinline__ float2 lds2(const float* p) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
+
 // Activation sign masks of the per-layer kernels' HBM format (16 B per row,
 // 32 bits per 32-column block: column 2k is bit k, column 2k+1 bit 16 + k,
 // set iff bf16(H) > 0, R30), from the packed hi word of a pair
@@ -174,13 +191,23 @@ __device__ __forceinline__ float colsum32(float (&g)[32], int lane) {
   return g[0];
 }
 // 16 packed words = columns 32 c .. 32 c + 31 of column half h, row r of a
-// plane tile (SW128 layout of the per-layer kernels): 4 chunks of 16 bytes
+// plane tile (SW128 layout of the per-layer kernels): 4 chunks of 16 bytes,
+// as two 32-byte stores (STG.256, whole sectors): chunks 2m, 2m+1 land on the
+// aligned position pair {2m ^ x, 2m+1 ^ x}, x = r % 8 (swapped when x is odd)
+__device__ __forceinline__ void st256(uint8_t* p, const uint32_t* w0, const uint32_t* w1) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w0[0]), "r"(w0[1]), "r"(w0[2]),
+               "r"(w0[3]), "r"(w1[0]), "r"(w1[1]), "r"(w1[2]), "r"(w1[3])
+               : "memory");
+}
 __device__ __forceinline__ void store_plane_words(uint8_t* plane, int r, int h, int c, const uint32_t* w) {
   uint8_t* row = plane + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
+  const int x = r & 7;
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const int jc = 4 * c + jj;
-    *reinterpret_cast<uint4*>(row + ((jc ^ (r & 7)) << 4)) = make_uint4(w[4 * jj], w[4 * jj + 1], w[4 * jj + 2], w[4 * jj + 3]);
+  for (int mm = 0; mm < 2; ++mm) {
+    const int j0 = 4 * c + 2 * mm;  // even chunk
+    uint8_t* dst = row + (((j0 ^ x) & ~1) << 4);
+    if (x & 1) st256(dst, w + 8 * mm + 4, w + 8 * mm);
+    else st256(dst, w + 8 * mm, w + 8 * mm + 4);
   }
 }
 
@@ -273,24 +300,46 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
     if (kSplit) tmem_st16(alT + 16u * c, lw);
   };
   // the slot's A operand is complete: the group's first warp issues layer p
+  int cur_i = 0;
+  // diagnostic stamps (CTA 0, first thread of each group): [slot][local tile / 2][phase][4]
+  auto stamp = [&](int p, int k) {
+    if (a.trace && j == 0 && w8 == 0 && lane == 0 && cur_i / 2 < 64)
+      a.trace[((s * 64 + cur_i / 2) * 6 + p) * 4 + k] = clock64();
+  };
   auto run_layer = [&](int p) {
+    stamp(p, 0);
     tmem_st_wait();
     tc_fence_before();
     group_sync(s);
+    stamp(p, 1);
     if (w8 == 0) {
       tc_fence_after();
       issue_layer<kSplit>(slot, wbase, p);
       mma_commit_warp(&sv->acc_full[s]);
     }
+    stamp(p, 2);
     mbar_wait(&sv->acc_full[s], acc_ph & 1u);
     ++acc_ph;
     tc_fence_after();
+    stamp(p, 3);
+  };
+  // LeakyReLU of a pair z (max(z, alpha z) for 0 <= alpha < 1, R6), split into
+  // bf16 hi / lo words, sign bits in the pos_bits layout (R30)
+  auto act_pair = [&](float2 z, int k, uint32_t& hw, uint32_t& lw, uint32_t& m) {
+    const float2 t = mul2(z, alpha2);
+    split2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), hw, lw);
+    m |= pos_bits(hw, k);
+  };
+  // LeakyReLU' of columns 2k, 2k+1 from the sign bits
+  auto dact_pair = [&](float2 g, uint32_t m, int k) {
+    return make_float2(g.x * (((m >> k) & 1u) ? 1.f : a.alpha), g.y * (((m >> (16 + k)) & 1u) ? 1.f : a.alpha));
   };
   for (int i = s; i < nmine; i += 2) {
+    cur_i = i;
     const int64_t row = (int64_t)(j + (int64_t)i * n) * 128 + r;
     const bool valid = row < a.rows;
     const float2 x = valid ? __ldg(a.Y + row) : make_float2(0.f, 0.f);
-    uint32_t m1a, m1b, m2a, m2b, m3a, m3b;  // LeakyReLU' sign bits of Z_1..Z_3 (two 32-column chunks)
+    uint32_t m1[2], m2[2], m3[2];  // LeakyReLU' sign bits of Z_1..Z_3 (two 32-column chunks)
     // H_1 = LeakyReLU(fma(x0, w0x, fma(x1, w0y, b0)))  (the per-layer kernels' order)
     {
       const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
@@ -298,19 +347,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
       for (int c = 0; c < 2; ++c) {
         uint32_t hw[16], lw[16], m = 0;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 16; k += 2) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float2 wx = *reinterpret_cast<const float2*>(&sv->w0x[col]);
-          const float2 wy = *reinterpret_cast<const float2*>(&sv->w0y[col]);
-          const float2 bb = *reinterpret_cast<const float2*>(&sv->b0[col]);
-          const float2 z = fma2(X0, wx, fma2(X1, wy, bb));
-          const float2 t = mul2(z, alpha2);
-          split2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), hw[k], lw[k]);
-          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
-          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+          const float4 wx = lds4(&sv->w0x[col]);
+          const float4 wy = lds4(&sv->w0y[col]);
+          const float4 bb = lds4(&sv->b0[col]);
+          act_pair(fma2(X0, make_float2(wx.x, wx.y), fma2(X1, make_float2(wy.x, wy.y), make_float2(bb.x, bb.y))), k,
+                   hw[k], lw[k], m);
+          act_pair(fma2(X0, make_float2(wx.z, wx.w), fma2(X1, make_float2(wy.z, wy.w), make_float2(bb.z, bb.w))),
+                   k + 1, hw[k + 1], lw[k + 1], m);
         }
-        if (c == 0) m1a = m;
-        else m1b = m;
+        m1[c] = m;
         put_a(c, hw, lw);
       }
     }
@@ -318,51 +365,42 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
 #pragma unroll 1
     for (int l = 0; l < 2; ++l) {
       run_layer(l);
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(accT + 32u * c, v);
         uint32_t hw[16], lw[16], m = 0;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int col = 64 * h + 32 * c + 2 * k;
-          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[l][col]));
-          const float2 t = mul2(z, alpha2);
-          split2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), hw[k], lw[k]);
-          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
-          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+        for (int k = 0; k < 16; k += 2) {
+          const float4 bq = lds4(&sv->b[l][64 * h + 32 * c + 2 * k]);
+          act_pair(add2(make_float2(v[32 * c + 2 * k], v[32 * c + 2 * k + 1]), make_float2(bq.x, bq.y)), k, hw[k], lw[k], m);
+          act_pair(add2(make_float2(v[32 * c + 2 * k + 2], v[32 * c + 2 * k + 3]), make_float2(bq.z, bq.w)), k + 1,
+                   hw[k + 1], lw[k + 1], m);
         }
-        if (l == 0) {
-          if (c == 0) m2a = m;
-          else m2b = m;
-        } else {
-          if (c == 0) m3a = m;
-          else m3b = m;
-        }
+        if (l == 0) m2[c] = m;
+        else m3[c] = m;
         put_a(c, hw, lw);
       }
     }
     // head: Z_4 = acc + b_3, z = LeakyReLU(Z_4) . w + b, dz, G_4 = dz (Z_4 > 0 ? w : alpha w)
     {
       run_layer(2);
-      uint32_t m4a = 0u, m4b = 0u;
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
+      uint32_t m4[2] = {0u, 0u};
       float2 dot = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(accT + 32u * c, v);
-        uint32_t m = 0u;
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
+          const float2 z = add2(make_float2(v[32 * c + 2 * k], v[32 * c + 2 * k + 1]),
+                                lds2(&sv->b[2][col]));
           const float2 t = mul2(z, alpha2);
-          dot = fma2(make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y)), *reinterpret_cast<const float2*>(&sv->w4[col]), dot);
-          m |= (z.x > 0.f ? 1u : 0u) << (2 * k);
-          m |= (z.y > 0.f ? 1u : 0u) << (2 * k + 1);
+          const float2 hh = make_float2(fmaxf(z.x, t.x), fmaxf(z.y, t.y));
+          dot = fma2(hh, lds2(&sv->w4[col]), dot);
+          m4[c] |= pos_bits(bf16x2_rn(hh.x, hh.y), k);
         }
-        if (c == 0) m4a = m;
-        else m4b = m;
       }
       sv->xdot[s][r][h] = dot.x + dot.y;
       group_sync(s);
@@ -372,18 +410,18 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
         a.logits[row] = zz;
         lacc += (double)softplus_neg(zz);
       }
+      const float2 dz2 = make_float2(dz, dz);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const uint32_t m = c == 0 ? m4a : m4b;
         uint32_t hw[16], lw[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float2 w = *reinterpret_cast<const float2*>(&sv->w4[col]);
-          const float2 wa = *reinterpret_cast<const float2*>(&sv->aw4[col]);
-          const float2 g = make_float2(dz * (((m >> (2 * k)) & 1u) ? w.x : wa.x),
-                                       dz * (((m >> (2 * k + 1)) & 1u) ? w.y : wa.y));
-          split2(g, hw[k], lw[k]);
+          const float2 w = lds2(&sv->w4[col]);
+          const float2 wa = lds2(&sv->aw4[col]);
+          const uint32_t m = m4[c];
+          split2(mul2(dz2, make_float2(((m >> k) & 1u) ? w.x : wa.x, ((m >> (16 + k)) & 1u) ? w.y : wa.y)), hw[k],
+                 lw[k]);
         }
         put_a(c, hw, lw);
       }
@@ -392,44 +430,44 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
 #pragma unroll 1
     for (int l = 0; l < 2; ++l) {
       run_layer(3 + l);
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(accT + 32u * c, v);
-        const uint32_t m = (l == 0) ? (c == 0 ? m3a : m3b) : (c == 0 ? m2a : m2b);
+        const uint32_t m = (l == 0) ? m3[c] : m2[c];
         uint32_t hw[16], lw[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float2 g = make_float2(v[2 * k] * (((m >> (2 * k)) & 1u) ? 1.f : a.alpha),
-                                       v[2 * k + 1] * (((m >> (2 * k + 1)) & 1u) ? 1.f : a.alpha));
-          split2(g, hw[k], lw[k]);
-        }
+        for (int k = 0; k < 16; ++k)
+          split2(dact_pair(make_float2(v[32 * c + 2 * k], v[32 * c + 2 * k + 1]), m, k), hw[k], lw[k]);
         put_a(c, hw, lw);
       }
     }
     // dgrad W_1: G_1 = acc (.) LeakyReLU'(Z_1), dy = G_1 W_0
     {
       run_layer(5);
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
       float2 dx = make_float2(0.f, 0.f), dyy = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(accT + 32u * c, v);
-        const uint32_t m = c == 0 ? m1a : m1b;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 16; k += 2) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float2 g = make_float2(v[2 * k] * (((m >> (2 * k)) & 1u) ? 1.f : a.alpha),
-                                       v[2 * k + 1] * (((m >> (2 * k + 1)) & 1u) ? 1.f : a.alpha));
-          dx = fma2(g, *reinterpret_cast<const float2*>(&sv->w0x[col]), dx);
-          dyy = fma2(g, *reinterpret_cast<const float2*>(&sv->w0y[col]), dyy);
+          const float4 wx = lds4(&sv->w0x[col]);
+          const float4 wy = lds4(&sv->w0y[col]);
+          const float2 g0 = dact_pair(make_float2(v[32 * c + 2 * k], v[32 * c + 2 * k + 1]), m1[c], k);
+          const float2 g1 = dact_pair(make_float2(v[32 * c + 2 * k + 2], v[32 * c + 2 * k + 3]), m1[c], k + 1);
+          dx = fma2(g0, make_float2(wx.x, wx.y), dx);
+          dyy = fma2(g0, make_float2(wy.x, wy.y), dyy);
+          dx = fma2(g1, make_float2(wx.z, wx.w), dx);
+          dyy = fma2(g1, make_float2(wy.z, wy.w), dyy);
         }
       }
       *reinterpret_cast<float2*>(&sv->xdy[s][r][2 * h]) = make_float2(dx.x + dx.y, dyy.x + dyy.y);
       tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
       group_sync(s);
       if (h == 0 && valid) {
-        const float4 p = *reinterpret_cast<const float4*>(&sv->xdy[s][r][0]);
+        const float4 p = lds4(&sv->xdy[s][r][0]);
         a.dy[row] = make_float2(p.x + p.z, p.y + p.w);
       }
     }
@@ -508,20 +546,35 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     tmem_st16(ahT + 16u * c, hw);
     if (kSplit) tmem_st16(alT + 16u * c, lw);
   };
+  int cur_i = 0;
+  unsigned long long* tr = a.trace ? a.trace + 2 * 64 * 6 * 4 : nullptr;
+  auto stamp = [&](int p, int k) {
+    if (tr && j == 0 && w8 == 0 && lane == 0 && cur_i / 2 < 64) tr[((s * 64 + cur_i / 2) * 6 + p) * 4 + k] = clock64();
+  };
   auto run_layer = [&](int p) {
+    stamp(p, 0);
     tmem_st_wait();
     tc_fence_before();
     group_sync(s);
+    stamp(p, 1);
     if (w8 == 0) {
       tc_fence_after();
       issue_layer<kSplit>(slot, wbase, p);
       mma_commit_warp(&sv->acc_full[s]);
     }
+    stamp(p, 2);
     mbar_wait(&sv->acc_full[s], acc_ph & 1u);
     ++acc_ph;
     tc_fence_after();
+    stamp(p, 3);
+  };
+  auto act_pair = [&](float2 z, int k, uint32_t& hw, uint32_t& lw, uint32_t& m) {
+    const float2 tt = mul2(z, alpha2);
+    split2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), hw, lw);
+    m |= pos_bits(hw, k);
   };
   for (int i = s; i < nmine; i += 2) {
+    cur_i = i;
     const int64_t t = (int64_t)j + (int64_t)i * n;
     const int64_t row = t * 128 + r;
     const bool valid = row < a.rows;
@@ -530,16 +583,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
       const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        uint32_t hw[16], lw[16];
+        uint32_t hw[16], lw[16], m = 0u;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
+        for (int k = 0; k < 16; k += 2) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float2 wx = *reinterpret_cast<const float2*>(&sv->w0x[col]);
-          const float2 wy = *reinterpret_cast<const float2*>(&sv->w0y[col]);
-          const float2 bb = *reinterpret_cast<const float2*>(&sv->b0[col]);
-          const float2 z = fma2(X0, wx, fma2(X1, wy, bb));
-          const float2 tt = mul2(z, alpha2);
-          split2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), hw[k], lw[k]);
+          const float4 wx = lds4(&sv->w0x[col]);
+          const float4 wy = lds4(&sv->w0y[col]);
+          const float4 bb = lds4(&sv->b0[col]);
+          act_pair(fma2(X0, make_float2(wx.x, wx.y), fma2(X1, make_float2(wy.x, wy.y), make_float2(bb.x, bb.y))), k,
+                   hw[k], lw[k], m);
+          act_pair(fma2(X0, make_float2(wx.z, wx.w), fma2(X1, make_float2(wy.z, wy.w), make_float2(bb.z, bb.w))),
+                   k + 1, hw[k + 1], lw[k + 1], m);
         }
         put_a(c, hw, lw);
       }
@@ -549,19 +603,19 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     for (int l = 0; l < 2; ++l) {
       run_layer(l);
       uint8_t* plane = (l == 0 ? a.h2 : a.h3) + t * TB;
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
       uint32_t mb[2];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld32(accT + 32u * c, v);
         uint32_t hw[16], lw[16], m = 0u;
 #pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int col = 64 * h + 32 * c + 2 * k;
-          const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[l][col]));
-          const float2 tt = mul2(z, alpha2);
-          split2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), hw[k], lw[k]);
-          m |= pos_bits(hw[k], k);
+        for (int k = 0; k < 16; k += 2) {
+          const float4 bq = lds4(&sv->b[l][64 * h + 32 * c + 2 * k]);
+          act_pair(add2(make_float2(v[32 * c + 2 * k], v[32 * c + 2 * k + 1]), make_float2(bq.x, bq.y)), k, hw[k],
+                   lw[k], m);
+          act_pair(add2(make_float2(v[32 * c + 2 * k + 2], v[32 * c + 2 * k + 3]), make_float2(bq.z, bq.w)), k + 1,
+                   hw[k + 1], lw[k + 1], m);
         }
         put_a(c, hw, lw);
         if (!valid) {  // rows past the end are zeros in HBM (the backward reads whole tiles)
@@ -577,16 +631,19 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     // head
     run_layer(2);
     float2 dot = make_float2(0.f, 0.f);
+    {
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float v[32];
-      tmem_ld32(accT + 32u * c, v);
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int col = 64 * h + 32 * c + 2 * k;
-        const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
-        const float2 tt = mul2(z, alpha2);
-        dot = fma2(make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)), *reinterpret_cast<const float2*>(&sv->w4[col]), dot);
+      for (int k = 0; k < 32; k += 2) {
+        const int col = 64 * h + 2 * k;
+        const float4 bq = lds4(&sv->b[2][col]);
+        const float4 wq = lds4(&sv->w4[col]);
+        const float2 z0 = add2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(bq.x, bq.y));
+        const float2 z1 = add2(make_float2(v[2 * k + 2], v[2 * k + 3]), make_float2(bq.z, bq.w));
+        const float2 t0 = mul2(z0, alpha2), t1 = mul2(z1, alpha2);
+        dot = fma2(make_float2(fmaxf(z0.x, t0.x), fmaxf(z0.y, t0.y)), make_float2(wq.x, wq.y), dot);
+        dot = fma2(make_float2(fmaxf(z1.x, t1.x), fmaxf(z1.y, t1.y)), make_float2(wq.z, wq.w), dot);
       }
     }
     sv->xdot[s][r][h] = dot.x + dot.y;
@@ -600,30 +657,45 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
       gbacc += dz;
     }
     uint8_t* gplane = a.g4 + t * TB;
+    const float2 dz2 = make_float2(dz, dz);
+    {
+      float v[64];
+      tmem_ld32x2(accT, accT + 32u, v, v + 32);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float v[32];
-      tmem_ld32(accT + 32u * c, v);
-      uint32_t hw[16], lw[16];
-      float g[32];
+      for (int c = 0; c < 2; ++c) {
+        uint32_t hw[16], lw[16];
+        float g[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int col = 64 * h + 32 * c + 2 * k;
-        const float2 z = add2(make_float2(v[2 * k], v[2 * k + 1]), *reinterpret_cast<const float2*>(&sv->b[2][col]));
-        const float2 tt = mul2(z, alpha2);
-        g[2 * k] = dz * fmaxf(z.x, tt.x);       // dz H_4 (head weight gradient)
-        g[2 * k + 1] = dz * fmaxf(z.y, tt.y);
-        const float2 w = *reinterpret_cast<const float2*>(&sv->w4[col]);
-        const float2 wa = *reinterpret_cast<const float2*>(&sv->aw4[col]);
-        split2(make_float2(dz * (z.x > 0.f ? w.x : wa.x), dz * (z.y > 0.f ? w.y : wa.y)), hw[k], lw[k]);
+        for (int k = 0; k < 16; k += 2) {
+          const int col = 64 * h + 32 * c + 2 * k;
+          const float4 bq = lds4(&sv->b[2][col]);
+          const float4 wq = lds4(&sv->w4[col]);
+          const float4 aq = lds4(&sv->aw4[col]);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float2 z = add2(make_float2(v[32 * c + 2 * (k + u)], v[32 * c + 2 * (k + u) + 1]),
+                                  u ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y));
+            const float2 tt = mul2(z, alpha2);
+            const float2 hd = mul2(dz2, make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)));  // dz H_4
+            g[2 * (k + u)] = hd.x;
+            g[2 * (k + u) + 1] = hd.y;
+            const float2 w = u ? make_float2(wq.z, wq.w) : make_float2(wq.x, wq.y);
+            const float2 wa = u ? make_float2(aq.z, aq.w) : make_float2(aq.x, aq.y);
+            split2(mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y)), hw[k + u], lw[k + u]);
+          }
+        }
+        store_plane_words(gplane, r, h, c, hw);
+        if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
+        const float cs = colsum32(g, lane);
+        if (c == 0) gacc0 += cs;
+        else gacc1 += cs;
       }
-      store_plane_words(gplane, r, h, c, hw);
-      if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
-      const float cs = colsum32(g, lane);
-      if (c == 0) gacc0 += cs;
-      else gacc1 += cs;
     }
     tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
+    stamp(3, 0);
+    stamp(3, 1);
+    stamp(3, 2);
+    stamp(3, 3);
   }
   // per-CTA partials in a fixed order: head gradient [128] + bias, loss (fp64)
 #pragma unroll
@@ -660,6 +732,54 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  }
+}
+
+static unsigned long long* g_ftrace = nullptr;
+unsigned long long* fused_trace_buffer() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SAGIPS_FUSED_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+    if (on) {
+      cudaMalloc(&g_ftrace, sizeof(unsigned long long) * 2 * 2 * 64 * 6 * 4);
+      cudaMemset(g_ftrace, 0, sizeof(unsigned long long) * 2 * 2 * 64 * 6 * 4);
+    }
+  }
+  return g_ftrace;
+}
+void fused_trace_report() {
+  if (!g_ftrace) return;
+  std::vector<unsigned long long> h(2 * 2 * 64 * 6 * 4);
+  cudaDeviceSynchronize();
+  cudaMemcpy(h.data(), g_ftrace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+  // per phase: epilogue (previous accumulator ready -> this warp done), waiting
+  // for the group, MMA issue, MMA completion wait; cycles, mean over tiles 1..
+  for (int kern = 0; kern < 2; ++kern) {
+    const int np = kern == 0 ? 6 : 4;
+    const unsigned long long* H = h.data() + (size_t)kern * 2 * 64 * 6 * 4;
+    double acc[6][4] = {};
+    int cnt[6] = {};
+    for (int s = 0; s < 2; ++s)
+      for (int t = 1; t < 64; ++t)
+        for (int p = 0; p < np; ++p) {
+          const unsigned long long* e = &H[((s * 64 + t) * 6 + p) * 4];
+          if (!e[0] || !e[3]) continue;
+          const unsigned long long prev =
+              p > 0 ? H[((s * 64 + t) * 6 + p - 1) * 4 + 3] : H[((s * 64 + t - 1) * 6 + np - 1) * 4 + 3];
+          if (!prev || prev > e[0]) continue;
+          acc[p][0] += (double)(e[0] - prev);
+          acc[p][1] += (double)(e[1] - e[0]);
+          acc[p][2] += (double)(e[2] - e[1]);
+          acc[p][3] += (double)(e[3] - e[2]);
+          cnt[p]++;
+        }
+    fprintf(stderr, "sagips fused trace %s (CTA 0, cycles per phase: epilogue | group wait | MMA issue | MMA wait)\n",
+            kern == 0 ? "k_gstep" : "k_dfwd");
+    for (int p = 0; p < np; ++p)
+      if (cnt[p])
+        fprintf(stderr, "  phase %d: %7.0f | %6.0f | %6.0f | %6.0f  (%d samples)\n", p, acc[p][0] / cnt[p],
+                acc[p][1] / cnt[p], acc[p][2] / cnt[p], acc[p][3] / cnt[p], cnt[p]);
   }
 }
 

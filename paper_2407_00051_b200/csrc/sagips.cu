@@ -321,6 +321,7 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
 
 sagips_status sagips_destroy(sagips_ctx* ctx) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  fused_trace_report();
   exchange_destroy(ctx);
   for (auto& row : ctx->pev)
     for (auto& e : row)
@@ -527,6 +528,7 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     f.h3 = reinterpret_cast<uint8_t*>(c->dAct[2]);
     f.m3 = c->dMask[2];
     f.g4 = reinterpret_cast<uint8_t*>(c->dZb[0]);
+    f.trace = fused_trace_buffer();
     kernel_begin(c, 13, st);
     launch_dfwd(split, f, st);
     kernel_end(c, st);
@@ -654,6 +656,7 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
     a.logits = c->logits_g;
     a.loss_part = c->loss_part;
     a.dy = reinterpret_cast<float2*>(c->dy);
+    a.trace = fused_trace_buffer();
     kernel_begin(c, 12, st);
     launch_gstep(split, a, st);
     kernel_end(c, st);
