@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--sampler", choices=["quadratic", "tabulated"], default="quadratic",
                    help="a3-a9 sampler: the closed-form quantile (R1) or the tabulated CDF (R32, SURVEY 8(f) row 1)")
     p.add_argument("--sampler-grid", type=int, default=1024)
+    p.add_argument("--no-graph", action="store_true",
+                   help="launch the step's kernels one by one instead of replaying the captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--nccl-algo", default="",
@@ -343,21 +345,34 @@ def ours_arm(args):
             dist.barrier()
 
     step = 0
+    # phase / kernel times come from an eager (non-graph) pass: events are
+    # not recorded inside a captured graph step
     for _ in range(args.warmup):
         ctx.train_step(step, 0, sp)
         step += 1
     torch.cuda.synchronize()
-    ctx.timing_reset()  # phase / kernel times: timed steps only (warm-up includes lazy module loading)
+    ctx.timing_reset()
+    n_eager = max(3, min(args.steps, 10))
+    for _ in range(n_eager):
+        ctx.train_step(step, 0, sp)
+        step += 1
+    torch.cuda.synchronize()
+    gflag = 0 if args.no_graph else L.STEP_GRAPH
+    for _ in range(2):  # graph warm-up: capture + instantiate
+        ctx.train_step(step, gflag, sp)
+        step += 1
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     n0 = ctx.launch_count()
+    g0, i0 = ctx.graph_stats()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        ctx.train_step(step, 0, sp)
+        ctx.train_step(step, gflag, sp)
         step += 1
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -365,6 +380,11 @@ def ours_arm(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = ctx.launch_count() - n0
+    g1, i1 = ctx.graph_stats()
+    graph_info = {"graph_launches": g1 - g0, "graph_instantiations": i1 - i0,
+                  "kernels_per_step": launches / args.steps,
+                  "note": "with graphs, each step is one cudaGraphLaunch of the captured step; kernels are "
+                          "counted once per captured step"}
     ms = ev0.elapsed_time(ev1) / args.steps
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
@@ -501,7 +521,8 @@ def ours_arm(args):
             "config": {"workload": workload, "events_per_rank_per_step": N, "global_events_per_step": N * world,
                        "l2": "step working set (D activations ~4 GB at C2) exceeds the 126 MB L2",
                        "mode": args.mode if world > 1 else "none"},
-            "clocks": clk, "gpu_launches": launches, "phases_ms": phases, "phase_steps_averaged": nph,
+            "clocks": clk, "gpu_launches": launches, "graph": graph_info, "phases_ms": phases,
+            "phase_steps_averaged": nph, "phases_note": "phase / kernel times from an eager (non-graph) pass of the same step",
             "roofline": roof, "kernels": kernels, "roofline_sampler": roof_sampler,
             "roofline_sampler_2p24": roof_sampler_24,
             "cpu_baseline": cpu, "e2e": e2e, "exchange": xch,

@@ -187,6 +187,14 @@ typedef struct {
 /* train_step flags */
 #define SAGIPS_STEP_LOCAL_ONLY  1u  /* run steps a1-a11 (through the packet) only; no exchange, no Adam(G) */
 #define SAGIPS_STEP_NO_ADAM_G   2u  /* exchange but do not apply the generator update */
+#define SAGIPS_STEP_GRAPH       4u  /* capture the step's launches into a CUDA graph and replay it as one
+                                       graph launch (the executable graph is updated in place from step
+                                       to step); ignored on the first step, with host inputs
+                                       (sagips_train_step_host) and for the two-sided ring modes (ARAR,
+                                       ARAR_ARAR), whose pull waits on an earlier step's side-stream
+                                       ring.  Phase / kernel timing is not recorded for graph steps.
+                                       The one-sided pass-along ring joins its forwarding agent into
+                                       the step at the end of a graph step. */
 
 /* Fill *cfg with a preset (sagips_preset) on world=1, rank=0, mode NONE,
  * seed 1, lr 1e-5/1e-4, Adam (0.9, 0.999, 1e-8), slope 0.01, the
@@ -400,7 +408,13 @@ SAGIPS_API sagips_status sagips_timing_reset(sagips_ctx* ctx);
  * [sync] */
 SAGIPS_API sagips_status sagips_debug_trace(void* host, size_t* bytes);
 
-/* Number of this library's kernels launched since create (all streams). */
+/* CUDA-graph steps (SAGIPS_STEP_GRAPH): graph launches and graph
+ * instantiations (an instantiation happens when the step's topology changes,
+ * e.g. the first steps of staleness 1) since create. [sync] */
+SAGIPS_API sagips_status sagips_graph_stats(const sagips_ctx* ctx, uint64_t* graph_launches, uint64_t* instantiations);
+
+/* Number of this library's kernels launched since create (all streams;
+ * kernels inside a captured graph step count once, at capture). */
 SAGIPS_API sagips_status sagips_launch_count(const sagips_ctx* ctx, uint64_t* count);
 
 #ifdef __cplusplus

@@ -19,7 +19,7 @@ SAMPLER_QUADRATIC, SAMPLER_TABULATED = 0, 1
 PREC_FP32, PREC_BF16 = 0, 1
 DISC_AUTO, DISC_SIMT, DISC_TCGEN05 = 0, 1, 2
 PRESET_DESK, PRESET_PAPER = 0, 1
-STEP_LOCAL_ONLY, STEP_NO_ADAM_G = 1, 2
+STEP_LOCAL_ONLY, STEP_NO_ADAM_G, STEP_GRAPH = 1, 2, 4
 IPC_HANDLE_BYTES = 64
 NCCL_ID_BYTES = 128
 
@@ -91,6 +91,7 @@ def _load():
         "sagips_nccl_unique_id": ([vp, sz], st),
         "sagips_connect_nccl": ([vp, vp, sz], st),
         "sagips_launch_count": ([vp, P(ctypes.c_uint64)], st),
+        "sagips_graph_stats": ([vp, P(ctypes.c_uint64), P(ctypes.c_uint64)], st),
         "sagips_phase_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
         "sagips_kernel_times": ([vp, P(ctypes.c_float), ctypes.c_int32, P(ctypes.c_int32)], st),
         "sagips_timing_reset": ([vp], st),
@@ -119,7 +120,7 @@ EXPORTED = [
     "sagips_connect_peers", "sagips_nccl_unique_id", "sagips_connect_nccl", "sagips_launch_count",
     "sagips_phase_times", "sagips_kernel_times", "sagips_timing_reset", "sagips_debug_trace",
     "sagips_predict_params", "sagips_ensemble_stats", "sagips_sample_tabulated", "sagips_sample_tabulated_bwd",
-    "sagips_train_step_host", "sagips_window_ptr", "sagips_connect_peers_local"]
+    "sagips_train_step_host", "sagips_window_ptr", "sagips_connect_peers_local", "sagips_graph_stats"]
 NUM_PHASES = 7
 PHASES = ["gen_fwd", "sampler", "disc_step", "gen_loss_through_disc", "sampler_bwd", "gen_bwd", "exchange_adam_g"]
 NUM_KERNELS = 14
@@ -293,6 +294,12 @@ class Context:
 
     def timing_reset(self):
         _check(lib.sagips_timing_reset(self.h), self.h)
+
+    def graph_stats(self):
+        """(graph launches, graph instantiations) of SAGIPS_STEP_GRAPH steps."""
+        a, b = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(lib.sagips_graph_stats(self.h, ctypes.byref(a), ctypes.byref(b)), self.h)
+        return a.value, b.value
 
     def launch_count(self):
         n = ctypes.c_uint64()

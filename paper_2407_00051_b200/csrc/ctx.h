@@ -81,6 +81,11 @@ struct sagips_ctx {
   bool pushed = false;
   bool skip_adam_once = false;
   sagips::ExchangeState* xs = nullptr;
+  // CUDA-graph step (SAGIPS_STEP_GRAPH): the step is captured and replayed;
+  // phase / kernel timing events are not recorded while capturing
+  bool capturing = false;
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t graph_launches = 0, graph_instantiations = 0;
   sagips::TcState* tc = nullptr;
   // phase timing: events at the SAGIPS_NUM_PHASES+1 boundaries of the
   // last 64 steps (cfg.phase_timing)
@@ -97,12 +102,13 @@ struct sagips_ctx {
 };
 
 namespace sagips {
+inline bool timing_on(const sagips_ctx* c) { return c->cfg.phase_timing && !c->capturing; }
 inline void mark(sagips_ctx* c, int boundary, cudaStream_t st) {
-  if (c->cfg.phase_timing) cudaEventRecord(c->pev[c->pslot][boundary], st);
+  if (timing_on(c)) cudaEventRecord(c->pev[c->pslot][boundary], st);
 }
 // bracket one kernel launch of class k (SAGIPS_NUM_KERNELS) with events
 inline void kernel_begin(sagips_ctx* c, int k, cudaStream_t st) {
-  if (!c->cfg.phase_timing) return;
+  if (!timing_on(c)) return;
   const int i = c->kcount[c->pslot];
   if (i >= sagips_ctx::kKernelSlots) return;
   if (!c->kev[c->pslot][i][0]) {
@@ -113,7 +119,7 @@ inline void kernel_begin(sagips_ctx* c, int k, cudaStream_t st) {
   cudaEventRecord(c->kev[c->pslot][i][0], st);
 }
 inline void kernel_end(sagips_ctx* c, cudaStream_t st) {
-  if (!c->cfg.phase_timing) return;
+  if (!timing_on(c)) return;
   const int i = c->kcount[c->pslot];
   if (i >= sagips_ctx::kKernelSlots) return;
   cudaEventRecord(c->kev[c->pslot][i][1], st);
@@ -139,6 +145,10 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
 bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step);
 GenAdam gen_adam_args(sagips_ctx* c);
 sagips_status exchange_check(sagips_ctx* c);
-sagips_status exchange_poll(sagips_ctx* c);  // non-blocking: an error raised by an earlier wait
+sagips_status exchange_poll(sagips_ctx* c);
+// graph capture support: whether this configuration's step can be captured,
+// and the join of the exchange side stream into the step stream
+bool exchange_graph_ok(const sagips_ctx* c);
+sagips_status exchange_join(sagips_ctx* c, cudaStream_t st);  // non-blocking: an error raised by an earlier wait
 void exchange_destroy(sagips_ctx* c);
 }  // namespace sagips

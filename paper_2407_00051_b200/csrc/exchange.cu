@@ -550,6 +550,24 @@ static sagips_status outer_ring_nccl(sagips_ctx* c, cudaStream_t st) {
   return SAGIPS_OK;
 }
 
+// A step can be captured into a CUDA graph unless it depends on work recorded
+// outside the capture: the two-sided rings wait, in pull(t), for the side
+// stream's NCCL ring of an earlier step.  The one-sided ring's forwarding
+// agent (side stream) is joined back into the step stream at the end of the
+// captured step (exchange_join).
+bool exchange_graph_ok(const sagips_ctx* c) {
+  const auto& g = c->cfg;
+  if (g.world == 1 || g.mode == SAGIPS_MODE_NONE || g.mode == SAGIPS_MODE_SYNC_ALLREDUCE) return true;
+  return one_sided(c);
+}
+sagips_status exchange_join(sagips_ctx* c, cudaStream_t st) {
+  ExchangeState* x = c->xs;
+  if (!x || !one_sided(c) || c->cfg.mode != SAGIPS_MODE_RMA_ARAR_ARAR || x->g <= 2) return SAGIPS_OK;
+  XCK(cudaEventRecord(x->ev_done[0], x->side));
+  XCK(cudaStreamWaitEvent(st, x->ev_done[0], 0));
+  return SAGIPS_OK;
+}
+
 // pull(t) applies Adam(G) itself (k_fold_adam) for the one-sided modes
 bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step) {
   (void)step;

@@ -322,6 +322,7 @@ sagips_status sagips_create(const sagips_config* cfg, void* workspace, size_t wo
 sagips_status sagips_destroy(sagips_ctx* ctx) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
   fused_trace_report();
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   exchange_destroy(ctx);
   for (auto& row : ctx->pev)
     for (auto& e : row)
@@ -1004,19 +1005,10 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
 
 extern "C" {
 
-sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream) {
-  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
-  if (ctx->have_step && step != ctx->last_step + 1)
-    return fail(ctx, SAGIPS_ERR_STATE, "step %llu is not the next step (%llu)", (unsigned long long)step,
-                (unsigned long long)(ctx->last_step + 1));
-  if (!ctx->have_step && step != 0 && ctx->cfg.world > 1 && ctx->cfg.mode != SAGIPS_MODE_NONE && ctx->cfg.staleness > 0)
-    return fail(ctx, SAGIPS_ERR_STATE, "the first exchanging step with staleness 1 must be step 0");
-  {
-    const sagips_status xs = exchange_poll(ctx);
-    if (xs != SAGIPS_OK) return xs;
-  }
+// the step after validation: a1-a11, then push / pull (eager, or inside a capture)
+static sagips_status step_body(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (ctx->cfg.phase_timing) {
+  if (timing_on(ctx)) {
     if (!ctx->pev[0][0])
       for (auto& row : ctx->pev)
         for (auto& e : row) CK(cudaEventCreate(&e));
@@ -1031,7 +1023,7 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
   ctx->local_done_step = step;
   if (flags & SAGIPS_STEP_LOCAL_ONLY) {
     mark(ctx, 7, st);
-    if (ctx->cfg.phase_timing) ctx->timed_steps++;
+    if (timing_on(ctx)) ctx->timed_steps++;
     return SAGIPS_OK;
   }
   sagips_status s = sagips_push_generator_grad(ctx, step, stream);
@@ -1040,6 +1032,60 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
     ctx->skip_adam_once = true;
   }
   return sagips_pull_generator_grad(ctx, step, stream);
+}
+
+sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, void* stream) {
+  if (!ctx) return SAGIPS_ERR_INVALID_ARG;
+  if (ctx->have_step && step != ctx->last_step + 1)
+    return fail(ctx, SAGIPS_ERR_STATE, "step %llu is not the next step (%llu)", (unsigned long long)step,
+                (unsigned long long)(ctx->last_step + 1));
+  if (!ctx->have_step && step != 0 && ctx->cfg.world > 1 && ctx->cfg.mode != SAGIPS_MODE_NONE && ctx->cfg.staleness > 0)
+    return fail(ctx, SAGIPS_ERR_STATE, "the first exchanging step with staleness 1 must be step 0");
+  {
+    const sagips_status xs = exchange_poll(ctx);
+    if (xs != SAGIPS_OK) return xs;
+  }
+  // CUDA graph: capture this step's launches and replay them as one graph
+  // launch (the first step runs eagerly: lazy set-up, kernel attributes);
+  // an executable graph is updated in place while the topology is unchanged
+  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx) && !ctx->host_noise &&
+                     !ctx->host_real;
+  flags &= ~SAGIPS_STEP_GRAPH;
+  if (!graph) return step_body(ctx, step, flags, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  ctx->capturing = true;
+  sagips_status s = step_body(ctx, step, flags, stream);
+  if (s == SAGIPS_OK && !(flags & SAGIPS_STEP_LOCAL_ONLY)) s = exchange_join(ctx, st);
+  ctx->capturing = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(st, &g);
+  if (s != SAGIPS_OK) {
+    if (g) cudaGraphDestroy(g);
+    return s;
+  }
+  if (ec != cudaSuccess) return fail(ctx, SAGIPS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ec));
+  if (ctx->gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ctx->gexec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(ctx->gexec);
+      ctx->gexec = nullptr;
+    }
+  }
+  if (!ctx->gexec) {
+    const cudaError_t ei = cudaGraphInstantiate(&ctx->gexec, g, 0);
+    if (ei != cudaSuccess) {
+      cudaGraphDestroy(g);
+      ctx->gexec = nullptr;
+      return fail(ctx, SAGIPS_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+    }
+    ctx->graph_instantiations++;
+  }
+  cudaGraphDestroy(g);
+  CK(cudaGraphLaunch(ctx->gexec, st));
+  ctx->graph_launches++;
+  return SAGIPS_OK;
 }
 
 sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, uint32_t flags, const float* host_noise,
@@ -1087,7 +1133,7 @@ sagips_status sagips_pull_generator_grad(sagips_ctx* ctx, uint64_t step, void* s
     }
   }
   mark(ctx, 7, st);
-  if (ctx->cfg.phase_timing) ctx->timed_steps++;
+  if (timing_on(ctx)) ctx->timed_steps++;
   ctx->pushed = false;
   CK(cudaGetLastError());
   return SAGIPS_OK;
@@ -1228,6 +1274,13 @@ sagips_status sagips_debug_trace(void* host, size_t* bytes) {
   if (*bytes != need) return SAGIPS_ERR_INVALID_ARG;
   if (cudaDeviceSynchronize() != cudaSuccess) return SAGIPS_ERR_CUDA;
   return tc_trace_copy(host) == 0 ? SAGIPS_OK : SAGIPS_ERR_CUDA;
+}
+
+sagips_status sagips_graph_stats(const sagips_ctx* ctx, uint64_t* graph_launches, uint64_t* instantiations) {
+  if (!ctx || !graph_launches || !instantiations) return SAGIPS_ERR_INVALID_ARG;
+  *graph_launches = ctx->graph_launches;
+  *instantiations = ctx->graph_instantiations;
+  return SAGIPS_OK;
 }
 
 sagips_status sagips_launch_count(const sagips_ctx* ctx, uint64_t* count) {

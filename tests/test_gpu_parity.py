@@ -352,3 +352,24 @@ def test_train_step_host_inputs_reproduce_the_device_step(preset):
     # the real half of the histogram is zero (no bootstrap), the fake half as the device step
     ha, hb = ca.get(L.T_HIST).reshape(2, -1), cb.get(L.T_HIST).reshape(2, -1)
     assert np.all(hb[0] == 0) and np.array_equal(ha[1], hb[1])
+
+
+@pytest.mark.parametrize("preset", [0, 1])
+def test_graph_step_matches_eager(preset):
+    """SAGIPS_STEP_GRAPH: the captured-and-replayed step runs
+    the same kernels on the same inputs, so after several steps the parameters
+    and losses are bit-identical to the eager step's; every step after the
+    first is one graph launch, updated in place (one instantiation)."""
+    L = lib()
+    kw = dict(seed=17, param_samples=32, events_per_sample=64)
+    ca, cb = make_ctx(L.config_init(preset, **kw)), make_ctx(L.config_init(preset, **kw))
+    for t in range(5):
+        ca.train_step(t, 0, _stream())
+        cb.train_step(t, L.STEP_GRAPH, _stream())
+    torch.cuda.synchronize()
+    for w in (L.T_GEN_W, L.T_GEN_B, L.T_DISC_W, L.T_DISC_B, L.T_EVENTS, L.T_DY, L.T_HIST):
+        assert np.array_equal(ca.get(w), cb.get(w)), w
+    sa, sb = ca.get(L.T_STATS), cb.get(L.T_STATS)
+    assert sa.loss_d == sb.loss_d and sa.loss_g == sb.loss_g
+    launches, inst = cb.graph_stats()
+    assert launches == 4 and inst == 1, (launches, inst)
