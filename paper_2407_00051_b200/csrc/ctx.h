@@ -57,10 +57,6 @@ struct sagips_ctx {
   float* colpart = nullptr;
   float* head_tmp = nullptr;
   float* dbpart = nullptr;  // [grid][128] bias-gradient partials (tcgen05 layers)
-  // pipelined step (k_pipe): rings G4, G3, G2 (ring[2..4]); H2, H3 use dAct; per-tile flags
-  static constexpr int kRingG = 256;
-  uint8_t* ring[5] = {};
-  uint32_t* flags = nullptr;
   float* lpart[sagips::kMaxLayers] = {};  // [ctas][128][128] wgrad partials of hidden layer l
   float* ldb[sagips::kMaxLayers] = {};    // [ctas][128] bias-gradient partials
   bool d_adam_done = false;               // the D step already applied Adam(D) (fused reduction)
@@ -69,7 +65,6 @@ struct sagips_ctx {
   static constexpr int kTileCtrs = 16;
   uint32_t* tile_ctrs = nullptr;          // dynamic tile-schedule counters of the layer kernels
   int tile_ctr_next = 0;
-  bool pipe_ok = true;
   double* loss_part = nullptr;
   sagips_step_stats* stats = nullptr;
   // step bookkeeping
@@ -85,6 +80,7 @@ struct sagips_ctx {
   // phase / kernel timing events are not recorded while capturing
   bool capturing = false;
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cstream = nullptr;  // capture stream
   uint64_t graph_launches = 0, graph_instantiations = 0;
   sagips::TcState* tc = nullptr;
   // phase timing: events at the SAGIPS_NUM_PHASES+1 boundaries of the

@@ -211,17 +211,7 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
 void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st);
 size_t tc_trace_bytes();
 int tc_trace_copy(void* host);
-// the pipelined step (disc_depth == 4): roles first, mid, head, bwd3, bwd2, bwd1
-constexpr int kPipeRoles = 6;
-struct PipeLaunch {
-  FwdLaunch f[3];
-  BwdLaunch b[3];              // b[0] = layer 3, b[1] = layer 2, b[2] = layer 1
-  int ctas[kPipeRoles];
-  unsigned long long* trace[kPipeRoles] = {};
-  unsigned long long* waits = nullptr;  // [grid][8] wait accounting (tracing only)
-};
-int pipe_sm_count();
-bool launch_tc_pipe(bool split, bool dstep, const PipeLaunch& L, cudaStream_t st);
+
 
 // k_adam.cu
 struct RedSeg {              // one parameter tensor: partials [nparts][ld] -> gradient g[n] -> Adam on p, m, v

@@ -324,7 +324,8 @@ __device__ __forceinline__ void check_smem_alignment(const void* p) {
   if (smem_u32(p) & 1023u) __trap();  // SW128 operands need 1024-byte alignment
 }
 
-// ---- inter-CTA dataflow (the pipelined step, k_pipe): plane tiles pass
+// ---- inter-CTA dataflow (ring buffers with per-tile counters; unused by the
+// per-layer kernels, whose tensors are whole, rdy / done == nullptr): plane tiles pass
 // between layer roles through ring buffers in global memory (L2-resident);
 // per-tile counters carry release/acquire ordering.
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
@@ -1680,24 +1681,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ Bwd
 // one dataflow pipeline: CTAs are partitioned into the six layer roles (first,
 // mid, head, bwd3, bwd2, bwd1), all co-resident (cooperative launch); tiles
 // stream between roles through L2-resident rings.
-template <bool kSplit, bool kD>
-__global__ void __launch_bounds__(kThreads, 1) k_pipe(const __grid_constant__ PipeLaunch a) {
-  int j = blockIdx.x, r = 0;
-  while (r < kPipeRoles - 1 && j >= a.ctas[r]) j -= a.ctas[r++];
-  const int n = a.ctas[r];
-  unsigned long long* tr = a.trace[r];
-  const WaitAcct wa{a.waits ? a.waits + (size_t)blockIdx.x * 8 : nullptr};
-  const unsigned long long t_start = wa.w ? globaltimer() : 0;
-  switch (r) {
-    case 0: fwd_body<kSplit, true, false>(a.f[0], j, n, tr, wa); break;
-    case 1: fwd_body<kSplit, false, false>(a.f[1], j, n, tr, wa); break;
-    case 2: fwd_body<kSplit, false, true>(a.f[2], j, n, tr, wa); break;
-    case 3: bwd_body<kSplit, false, kD>(a.b[0], j, n, tr, wa); break;
-    case 4: bwd_body<kSplit, false, kD>(a.b[1], j, n, tr, wa); break;
-    default: bwd_body<kSplit, true, kD, kD>(a.b[2], j, n, tr, wa); break;
-  }
-  if (wa.w && threadIdx.x == 0) wa.w[7] = globaltimer() - t_start;
-}
 
 // ============================================================== partial sums
 // out[j] = sum_p part[p*ld + j], j < n: 32 outputs x 8 part groups per block
@@ -1734,7 +1717,6 @@ static int sm_count() {
   }
   return n;
 }
-int pipe_sm_count() { return sm_count(); }
 
 static size_t fwd_smem(bool split) {
   const size_t TB = (split ? 2 : 1) * (size_t)kPlane;
@@ -1768,16 +1750,6 @@ static void configure_layers() {
 #undef SAGIPS_BWD
   allow_smem(k_bwd<true, true, true, true>, bwd_smem(true));
   allow_smem(k_bwd<false, true, true, true>, bwd_smem(false));
-  for (bool s : {true, false}) {
-    const size_t sm = std::max(fwd_smem(s), bwd_smem(s));
-    if (s) {
-      allow_smem(k_pipe<true, true>, sm);
-      allow_smem(k_pipe<true, false>, sm);
-    } else {
-      allow_smem(k_pipe<false, true>, sm);
-      allow_smem(k_pipe<false, false>, sm);
-    }
-  }
 }
 
 __device__ unsigned long long g_trace[kTraceLaunches][kTraceCtas * kTraceTiles * 4];
@@ -1868,26 +1840,6 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
 
 // Cooperative launch (all CTAs co-resident, one per SM): returns false if the
 // device cannot host the grid.
-bool launch_tc_pipe(bool split, bool dstep, const PipeLaunch& L, cudaStream_t st) {
-  configure_layers();
-  int grid = 0;
-  for (int r = 0; r < kPipeRoles; ++r) grid += L.ctas[r];
-  const size_t sm = std::max(fwd_smem(split), bwd_smem(split));
-  PipeLaunch P = L;
-  for (int r = 0; r < kPipeRoles; ++r) P.trace[r] = trace_slot();
-  if (P.trace[0]) {  // wait accounting in trace launch slots 31 (D step) / 30 (G step)
-    void* p = nullptr;
-    cudaGetSymbolAddress(&p, g_trace);
-    P.waits = reinterpret_cast<unsigned long long*>(p) + (size_t)(dstep ? 31 : 30) * kTraceCtas * kTraceTiles * 4;
-    cudaMemsetAsync(P.waits, 0, sizeof(unsigned long long) * 8 * kMaxSms, st);
-  }
-  void* args[] = {&P};
-  const void* fn = split ? (dstep ? (const void*)k_pipe<true, true> : (const void*)k_pipe<true, false>)
-                         : (dstep ? (const void*)k_pipe<false, true> : (const void*)k_pipe<false, false>);
-  const cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, sm, st);
-  count_launch();
-  return e == cudaSuccess;
-}
 
 void launch_sum_parts(const float* part, int nparts, int64_t ld, int n, float* out, cudaStream_t st) {
   k_sum_parts<<<(n + 31) / 32, 256, 0, st>>>(part, nparts, ld, n, out);

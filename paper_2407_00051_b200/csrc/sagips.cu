@@ -107,12 +107,6 @@ static void carve(sagips_ctx* c, char* base) {
   c->head_tmp = cv.take<float>(D.maxw + 1);
   c->dbpart = cv.take<float>((int64_t)kMaxSms * 128);
   c->tile_ctrs = cv.take<uint32_t>(sagips_ctx::kTileCtrs);
-  // pipelined step: rings (L2-resident), per-tile flags, per-role partials
-  if (c->cfg.disc_depth == 4 && c->cfg.disc_hidden == 128) {
-    const size_t tb = plane_tile_bytes(true);
-    for (int k = 2; k < 5; ++k) c->ring[k] = cv.take<uint8_t>((int64_t)sagips_ctx::kRingG * tb);
-    c->flags = cv.take<uint32_t>(12 * (rows_t / 128));
-  }
   if (c->cfg.disc_hidden == 128) {  // per-layer wgrad partials of the tcgen05 layer passes (reduced + Adam at the end)
     for (int l = 1; l + 1 < D.L; ++l) {
       c->lpart[l] = cv.take<float>((int64_t)kMaxSms * 128 * 128);
@@ -323,6 +317,7 @@ sagips_status sagips_destroy(sagips_ctx* ctx) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
   fused_trace_report();
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   exchange_destroy(ctx);
   for (auto& row : ctx->pev)
     for (auto& e : row)
@@ -628,11 +623,8 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
 
 // the fused G step (k_fused.cu): paper widths, depth 4; SAGIPS_FUSED=0 keeps the per-layer kernels
 static bool use_fused(const sagips_ctx* c) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("SAGIPS_FUSED");
-    env = (e && e[0] == '0') ? 0 : 1;
-  }
+  const char* e = getenv("SAGIPS_FUSED");
+  const bool env = !(e && e[0] == '0');
   return env && c->use_tc && c->cfg.disc_depth == 4 && c->cfg.disc_hidden == 128;
 }
 
@@ -685,139 +677,7 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
   }
 }
 
-// ---- the pipelined step (k_pipe): depth-4 paper discriminator, every layer
-// pass of the D step (or the G step) in one cooperative launch
-static bool use_pipe(const sagips_ctx* c, int64_t rows) {
-  // SAGIPS_PIPE: 1 = pipelined when every role gets several tiles per CTA,
-  // 2 = pipelined at any size, unset / 0 = per-layer kernels (faster today:
-  // the roles are bound by their epilogues, profiles/r01_pipe_*)
-  const char* e = getenv("SAGIPS_PIPE");
-  const int mode = e ? atoi(e) : 0;
-  if (mode == 0 || !c->pipe_ok || !c->use_tc || c->cfg.disc_depth != 4 || c->cfg.disc_hidden != 128) return false;
-  return mode == 2 || (rows + 127) / 128 >= 4 * (int64_t)pipe_sm_count();
-}
-
-// CTAs per role, proportional to the measured per-tile cost of each role
-// (SAGIPS_PIPE_SPLIT_D / _G = "n0,n1,n2,n3,n4,n5" overrides)
-static void pipe_split(bool dstep, int ctas[kPipeRoles]) {
-  const int sms = pipe_sm_count();
-  const char* e = getenv(dstep ? "SAGIPS_PIPE_SPLIT_D" : "SAGIPS_PIPE_SPLIT_G");
-  if (e) {
-    int v[kPipeRoles], tot = 0;
-    if (sscanf(e, "%d,%d,%d,%d,%d,%d", &v[0], &v[1], &v[2], &v[3], &v[4], &v[5]) == kPipeRoles) {
-      for (int r = 0; r < kPipeRoles; ++r) tot += v[r];
-      bool ok = tot <= sms;
-      for (int r = 0; r < kPipeRoles; ++r) ok = ok && v[r] > 0;
-      if (ok) {
-        for (int r = 0; r < kPipeRoles; ++r) ctas[r] = v[r];
-        return;
-      }
-    }
-  }
-  // per-tile costs (us) of the roles, from the split sweep of profiles/r01_pipe_sweep_v7.txt
-  const double cd[kPipeRoles] = {3.3, 3.3, 3.9, 3.9, 3.9, 3.9};
-  const double cg[kPipeRoles] = {3.0, 2.8, 2.8, 2.4, 2.4, 1.4};
-  const double* cost = dstep ? cd : cg;
-  double tot = 0;
-  for (int r = 0; r < kPipeRoles; ++r) tot += cost[r];
-  int used = 0;
-  for (int r = 0; r < kPipeRoles; ++r) {
-    ctas[r] = std::max(1, (int)(sms * cost[r] / tot));
-    used += ctas[r];
-  }
-  for (int r = 0; used < sms; r = (r + 1) % kPipeRoles, ++used) ctas[r]++;  // remainder round-robin
-}
-
-// 0 = H2, 1 = H3: whole tensors (their backward consumers run ~4 pipeline
-// hops later, so a wrapping ring would throttle the forward roles);
-// 2 = G4, 3 = G3, 4 = G2: rings (one hop each)
-static Ring ring_of(sagips_ctx* c, int k, uint32_t target) {
-  Ring r;
-  const int64_t nt = (2 * c->N + 127) / 128;
-  // SAGIPS_PIPE_RING=1: G hand-offs through wrapping rings (L2-sized);
-  // default: whole tensors (no back-pressure)
-  const char* e = getenv("SAGIPS_PIPE_RING");
-  const bool rings = e && e[0] == '1';
-  if (k < 2) {
-    r.base = reinterpret_cast<uint8_t*>(c->dAct[1 + k]);
-    r.mask = c->dMask[1 + k];
-  } else if (rings) {
-    r.base = c->ring[k];
-    r.slots = sagips_ctx::kRingG;
-  } else {
-    r.base = reinterpret_cast<uint8_t*>(k == 2 ? c->dZb[0] : k == 3 ? c->dZb[1] : c->dAct[3]);
-  }
-  r.rdy = c->flags + (int64_t)k * nt;
-  r.done = c->flags + (int64_t)(5 + k) * nt;
-  r.done_target = target;
-  return r;
-}
-
-// tensors between the roles: see ring_of
-static bool run_pipe(sagips_ctx* c, bool dstep, const float* X, int64_t rows, int64_t n_real, float label_rest,
-                     float scale, float* logits, cudaStream_t st) {
-  const auto& D = c->D;
-  const bool split = tc_split(c);
-  const float a = c->cfg.leaky_slope;
-  const int64_t nt = (2 * c->N + 127) / 128;
-  cudaMemsetAsync(c->flags, 0, sizeof(uint32_t) * 12 * nt, st);
-  // H rings are read by the next forward role (1) and the backward role's H
-  // loader (1, D step) and its 8 epilogue warps (masks)
-  const uint32_t th = dstep ? 10u : 9u;
-  const Ring H2 = ring_of(c, 0, th), H3 = ring_of(c, 1, th);
-  const Ring G4 = ring_of(c, 2, 1), G3 = ring_of(c, 3, 1), G2 = ring_of(c, 4, 1);
-  PipeLaunch P;
-  pipe_split(dstep, P.ctas);
-  FwdLaunch& f1 = P.f[0];
-  f1.X = X; f1.W0 = c->dW + D.w_off[0]; f1.b0 = c->dB + D.b_off[0]; f1.first_help = first_help();
-  f1.W = c->dW + D.w_off[1]; f1.bias = c->dB + D.b_off[1]; f1.out = H2; f1.rows = rows; f1.alpha = a;
-  FwdLaunch& f2 = P.f[1];
-  f2.in = H2; f2.W = c->dW + D.w_off[2]; f2.bias = c->dB + D.b_off[2]; f2.out = H3; f2.rows = rows; f2.alpha = a;
-  FwdLaunch& f3 = P.f[2];
-  f3.in = H3; f3.W = c->dW + D.w_off[3]; f3.bias = c->dB + D.b_off[3]; f3.out = G4; f3.rows = rows; f3.alpha = a;
-  f3.w_head = c->dW + D.w_off[4]; f3.b_head = c->dB + D.b_off[4];
-  f3.n_real = n_real; f3.label_rest = label_rest; f3.scale = scale; f3.logits = logits;
-  f3.part_head = c->part; f3.loss_part = c->loss_part; f3.want_wgrad = dstep ? 1 : 0;
-  BwdLaunch& b3 = P.b[0];
-  b3.g = G4; b3.h = H3; b3.gout = G3; b3.W = c->dW + D.w_off[3]; b3.rows = rows; b3.alpha = a;
-  b3.part = c->lpart[3]; b3.part_db = c->ldb[3];
-  BwdLaunch& b2 = P.b[1];
-  b2.g = G3; b2.h = H2; b2.gout = G2; b2.W = c->dW + D.w_off[2]; b2.rows = rows; b2.alpha = a;
-  b2.part = c->lpart[2]; b2.part_db = c->ldb[2];
-  BwdLaunch& b1 = P.b[2];
-  if (dstep) {  // H_1 planes: written by the first-layer role, read by the layer-1 backward
-    Ring h1;
-    h1.base = reinterpret_cast<uint8_t*>(c->dAct[0]);
-    h1.rdy = c->flags + 10 * nt;
-    h1.done = c->flags + 11 * nt;
-    f1.h1 = h1;
-    b1.h = h1;
-  }
-  b1.g = G2; b1.X = X; b1.W0 = c->dW + D.w_off[0]; b1.b0 = c->dB + D.b_off[0]; b1.W = c->dW + D.w_off[1];
-  b1.rows = rows; b1.alpha = a; b1.dy = c->dy;
-  b1.part = c->lpart[1]; b1.part_db = c->ldb[1]; b1.part_l0 = c->colpart;
-  kernel_begin(c, dstep ? 0 : 6, st);
-  const bool launched = launch_tc_pipe(split, dstep, P, st);
-  kernel_end(c, st);
-  if (!launched) {
-    cudaGetLastError();  // clear; fall back to the per-layer kernels from now on
-    c->pipe_ok = false;
-    return false;
-  }
-  const int nh = P.ctas[2];
-  launch_finish_loss(c->loss_part, nh, 1.0 / rows, dstep ? &c->stats->loss_d : &c->stats->loss_g,
-                     &c->stats->nonfinite, st);
-  if (dstep) {
-    int nparts[kMaxLayers] = {};
-    for (int k = 0; k < 3; ++k) nparts[3 - k] = P.ctas[3 + k];
-    disc_reduce_adam(c, nh, nparts, P.ctas[5], st);
-  }
-  return true;
-}
-
 static void disc_step(sagips_ctx* c, cudaStream_t st) {
-  if (use_pipe(c, 2 * c->N) && run_pipe(c, true, c->X, 2 * c->N, c->N, 0.0f, 1.0f / (float)(2 * c->N), c->logits_d, st))
-    return;
   if (use_layers_v2(c)) {
     disc_step_v2(c, st);
     return;
@@ -848,8 +708,6 @@ static void disc_step(sagips_ctx* c, cudaStream_t st) {
 }
 
 static void gen_loss_through_disc(sagips_ctx* c, cudaStream_t st) {
-  if (use_pipe(c, c->N) && run_pipe(c, false, c->X + 2 * c->N, c->N, 0, 1.0f, 1.0f / (float)c->N, c->logits_g, st))
-    return;
   if (use_layers_v2(c)) {
     gen_loss_v2(c, st);
     return;
@@ -1052,14 +910,18 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
                      !ctx->host_real;
   flags &= ~SAGIPS_STEP_GRAPH;
   if (!graph) return step_body(ctx, step, flags, stream);
-  cudaStream_t st = (cudaStream_t)stream;
-  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  // captured on a library-owned stream (the caller's may be the legacy
+  // default stream, which cannot be captured); replayed on the caller's
+  if (!ctx->cstream) CK(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  cudaStream_t cs = ctx->cstream;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   ctx->capturing = true;
-  sagips_status s = step_body(ctx, step, flags, stream);
-  if (s == SAGIPS_OK && !(flags & SAGIPS_STEP_LOCAL_ONLY)) s = exchange_join(ctx, st);
+  sagips_status s = step_body(ctx, step, flags, cs);
+  if (s == SAGIPS_OK && !(flags & SAGIPS_STEP_LOCAL_ONLY)) s = exchange_join(ctx, cs);
   ctx->capturing = false;
   cudaGraph_t g = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(st, &g);
+  const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+  cudaStream_t st = (cudaStream_t)stream;
   if (s != SAGIPS_OK) {
     if (g) cudaGraphDestroy(g);
     return s;

@@ -159,25 +159,25 @@ def test_step_tabulated_sampler(preset, k, m, G):
 
 
 @pytest.fixture
-def pipe_env(request, monkeypatch):
-    """SAGIPS_PIPE: "0" per-layer tcgen05 kernels, "2" the pipelined step (one
-    cooperative launch per D / G step) even at small sizes."""
-    monkeypatch.setenv("SAGIPS_PIPE", request.param)
+def fused_env(request, monkeypatch):
+    """SAGIPS_FUSED: "1" the fused discriminator kernels (k_dfwd, k_gstep;
+    default), "0" the per-layer tcgen05 kernels."""
+    monkeypatch.setenv("SAGIPS_FUSED", request.param)
     return request.param
 
 
-@pytest.mark.parametrize("impl,pipe_env", [(0, "0"), (0, "2"), (1, "0")], indirect=["pipe_env"])
-def test_step_paper_widths_ragged(impl, pipe_env):
+@pytest.mark.parametrize("impl,fused_env", [(0, "1"), (0, "0"), (1, "1")], indirect=["fused_env"])
+def test_step_paper_widths_ragged(impl, fused_env):
     """paper widths, 2N = 7,808 rows (ragged 128-row tiles), step 3, rank 1;
-    impl 0 = tcgen05 bf16x3 hidden layers (per-layer kernels or the pipelined
-    step), 1 = CUDA-core fp32."""
+    impl 0 = tcgen05 bf16x3 hidden layers (fused kernels or per-layer
+    kernels), 1 = CUDA-core fp32."""
     L = lib()
     _check_step(L.config_init(1, seed=9, param_samples=64, events_per_sample=61, world=2, rank=1, group_size=2,
                               disc_impl=impl), t=3, disc_band=kink.BAND_BF16X3 if impl == 0 else kink.BAND_FP32)
 
 
-@pytest.mark.parametrize("pipe_env", ["0", "2"], indirect=True)
-def test_bf16_step_within_bf16_tolerances(pipe_env):
+@pytest.mark.parametrize("fused_env", ["1", "0"], indirect=True)
+def test_bf16_step_within_bf16_tolerances(fused_env):
     """SAGIPS_PREC_BF16 (C5's precision): discriminator GEMMs in bf16 with fp32
     accumulation.  Stated tolerances (Parity), twice the error of
     an exact-accumulation bf16 emulation of the same step
