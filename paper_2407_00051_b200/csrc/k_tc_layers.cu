@@ -209,6 +209,16 @@ __device__ __forceinline__ void mma_step(uint32_t d, uint64_t ah, uint64_t al, u
   }
 }
 
+template <bool kSplit>
+__device__ __forceinline__ void mma_step_warp(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                              uint32_t idesc, uint32_t acc) {
+  mma_bf16_warp(d, ah, bh, idesc, acc);
+  if (kSplit) {
+    mma_bf16_warp(d, ah, bl, idesc, 1);
+    mma_bf16_warp(d, al, bh, idesc, 1);
+  }
+}
+
 // W [128][128] fp32 -> hi/lo planes (once per CTA; warps 0-3)
 template <bool kSplit>
 __device__ __forceinline__ void stage_weights(const float* __restrict__ W, uint32_t hi, uint32_t lo, int w, int l) {
@@ -1203,8 +1213,11 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       }
     }
   } else if (warp == kMmaWarp) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
+    // ---------------- MMA issuer: the whole warp runs the loop, one elected
+    // lane issues each MMA (a converged warp issues an M128 N128 K16 MMA every
+    // 64 cycles; one thread of a divergent warp every 84-91)
+    const WaitAcct wq = lane == 0 ? wa : WaitAcct{};
+    {
       constexpr uint32_t id_d = make_idesc_bf16(128, 128, 0, 1);  // A = G (K-major), B = W (MN-major)
       constexpr uint32_t id_w = make_idesc_bf16(128, 128, 1, 1);  // A = G^T, B = H (both MN-major)
       constexpr uint32_t id_b = make_idesc_bf16(128, 16, 1, 0);   // A = G^T, B = ones (K-major)
@@ -1226,143 +1239,143 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         const int b = i & 1;
         const PS gh = pl_gh(i), ph = pl_hh(i);
         const uint32_t agh = pl_addr(gh.slot), ahh = pl_addr(ph.slot);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
-        ring_consumed(a.g, t);
-        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
-        trace_pt(trace, j, i, 1);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        if (lane == 0) ring_consumed(a.g, t);
+        SAGIPS_TIMED(wq, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        if (lane == 0) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
-          mma_bf16(d, make_desc(wh + km, 16384, 1024), make_desc(agh + kk, 16, 1024), id_dT, k > 0);
+          mma_bf16_warp(d, make_desc(wh + km, 16384, 1024), make_desc(agh + kk, 16, 1024), id_dT, k > 0);
         }
-        mma_commit(&tfull[b]);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
-        if (kLoadH) ring_consumed(a.h, t);
+        mma_commit_warp(&tfull[b]);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        if (kLoadH) if (lane == 0) ring_consumed(a.h, t);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
           const uint64_t gh_k = make_desc(agh + km, 16384, 1024);
-          mma_bf16(acc_b, gh_k, ones, id_b, acc0);
-          mma_bf16(acc_w, gh_k, make_desc(ahh + km, 16384, 1024), id_w, acc0);
+          mma_bf16_warp(acc_b, gh_k, ones, id_b, acc0);
+          mma_bf16_warp(acc_w, gh_k, make_desc(ahh + km, 16384, 1024), id_w, acc0);
         }
-        mma_commit(&pempty[gh.slot]);
-        mma_commit(&pempty[ph.slot]);
+        mma_commit_warp(&pempty[gh.slot]);
+        mma_commit_warp(&pempty[ph.slot]);
       }
       for (int i = 0; kT && kSplit && i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1;
         const PS gh = pl_gh(i), gl = pl_gl(i), ph = pl_hh(i);
         const uint32_t agh = pl_addr(gh.slot), agl = pl_addr(gl.slot), ahh = pl_addr(ph.slot);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
-        ring_consumed(a.g, t);  // both G planes have been read
-        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
-        trace_pt(trace, j, i, 1);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
+        if (lane == 0) ring_consumed(a.g, t);  // both G planes have been read
+        SAGIPS_TIMED(wq, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        if (lane == 0) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
           const uint64_t gk = make_desc(agh + kk, 16, 1024), wk = make_desc(wh + km, 16384, 1024);
-          mma_bf16(d, make_desc(wl + km, 16384, 1024), gk, id_dT, k > 0);
-          mma_bf16(d, wk, gk, id_dT, 1);
-          mma_bf16(d, wk, make_desc(agl + kk, 16, 1024), id_dT, 1);
+          mma_bf16_warp(d, make_desc(wl + km, 16384, 1024), gk, id_dT, k > 0);
+          mma_bf16_warp(d, wk, gk, id_dT, 1);
+          mma_bf16_warp(d, wk, make_desc(agl + kk, 16, 1024), id_dT, 1);
         }
-        mma_commit(&tfull[b]);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
-        if (kLoadH) ring_consumed(a.h, t);
+        mma_commit_warp(&tfull[b]);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        if (kLoadH) if (lane == 0) ring_consumed(a.h, t);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
           const uint64_t gh_k = make_desc(agh + km, 16384, 1024), gl_k = make_desc(agl + km, 16384, 1024);
           const uint64_t hh_k = make_desc(ahh + km, 16384, 1024);
-          mma_bf16(acc_b, gh_k, ones, id_b, acc0);
-          mma_bf16(acc_w, gh_k, hh_k, id_w, acc0);
-          mma_bf16(acc_w, gl_k, hh_k, id_w, 1);
-          mma_bf16(acc_b, gl_k, ones, id_b, 1);
+          mma_bf16_warp(acc_b, gh_k, ones, id_b, acc0);
+          mma_bf16_warp(acc_w, gh_k, hh_k, id_w, acc0);
+          mma_bf16_warp(acc_w, gl_k, hh_k, id_w, 1);
+          mma_bf16_warp(acc_b, gl_k, ones, id_b, 1);
         }
-        mma_commit(&pempty[gh.slot]);
-        mma_commit(&pempty[gl.slot]);
-        mma_commit(&pempty[ph.slot]);
+        mma_commit_warp(&pempty[gh.slot]);
+        mma_commit_warp(&pempty[gl.slot]);
+        mma_commit_warp(&pempty[ph.slot]);
       }
       for (int i = 0; kPR && !kT && i < nmine; ++i) {
         const int64_t t = tile_of(i);
         const int b = i & 1;
         const PS gh = pl_gh(i), ph = pl_hh(i), gl = pl_gl(i);
         const uint32_t agh = pl_addr(gh.slot), ahh = pl_addr(ph.slot), agl = pl_addr(gl.slot);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
-        if (kLoadH) ring_consumed(a.h, t);  // the H plane has been read
-        trace_pt(trace, j, i, 1);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[gh.slot], gh.use & 1));
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[ph.slot], ph.use & 1));
+        if (kLoadH) if (lane == 0) ring_consumed(a.h, t);  // the H plane has been read
+        if (lane == 0) trace_pt(trace, j, i, 1);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t km = k * 2048, acc0 = (i > 0 || k > 0) ? 1u : 0u;
           const uint64_t g = make_desc(agh + km, 16384, 1024);
-          mma_bf16(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, acc0);
-          mma_bf16(acc_b, g, ones, id_b, acc0);
+          mma_bf16_warp(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, acc0);
+          mma_bf16_warp(acc_b, g, ones, id_b, acc0);
         }
-        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        SAGIPS_TIMED(wq, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
           const uint64_t g = make_desc(agh + kk, 16, 1024);
-          mma_bf16(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
-          mma_bf16(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
+          mma_bf16_warp(d, g, make_desc(wh + km, 16384, 1024), id_d, k > 0);
+          mma_bf16_warp(d, g, make_desc(wl + km, 16384, 1024), id_d, 1);
         }
-        mma_commit(&pempty[gh.slot]);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
-        ring_consumed(a.g, t);
+        mma_commit_warp(&pempty[gh.slot]);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&pfull[gl.slot], gl.use & 1));
+        if (lane == 0) ring_consumed(a.g, t);
         tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t km = k * 2048;
           const uint64_t g = make_desc(agl + km, 16384, 1024);
-          mma_bf16(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, 1);
-          mma_bf16(acc_b, g, ones, id_b, 1);
+          mma_bf16_warp(acc_w, g, make_desc(ahh + km, 16384, 1024), id_w, 1);
+          mma_bf16_warp(acc_b, g, ones, id_b, 1);
         }
-        mma_commit(&pempty[ph.slot]);
+        mma_commit_warp(&pempty[ph.slot]);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32, km = k * 2048;
-          mma_bf16(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
+          mma_bf16_warp(d, make_desc(agl + kk, 16, 1024), make_desc(wh + km, 16384, 1024), id_d, 1);
         }
-        mma_commit(&pempty[gl.slot]);
-        mma_commit(&tfull[b]);
+        mma_commit_warp(&pempty[gl.slot]);
+        mma_commit_warp(&tfull[b]);
       }
       for (int i = 0; !kPR && (dyn || i < nmine); ++i) {
         const int b = i & 1;
         const int s = kWgrad ? 0 : (i & 1);
-        SAGIPS_TIMED(wa, 2, mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1)));
+        SAGIPS_TIMED(wq, 2, mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1)));
         const int64_t t = dyn ? (int64_t)sTile[i & 7] : tile_of(i);
         if (t < 0) break;  // sentinel (the epilogue stops at its own tidbar)
-        ring_consumed(a.g, t);
+        if (lane == 0) ring_consumed(a.g, t);
         const uint32_t zh = smem_u32(g_stage(i)), zl = zh + kPlane;
         if (kWgrad) {
           mbar_wait(&fullH[0], i & 1);
-          if (kLoadH) ring_consumed(a.h, t);
-          trace_pt(trace, j, i, 1);
+          if (kLoadH) if (lane == 0) ring_consumed(a.h, t);
+          if (lane == 0) trace_pt(trace, j, i, 1);
           tc_fence_after();
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const uint32_t km = k * 2048;  // MN-major step (16 rows)
             const uint32_t acc0 = (i > 0 || k > 0) ? 1u : 0u;
             const uint64_t gh = make_desc(zh + km, 16384, 1024), gl = make_desc(zl + km, 16384, 1024);
-            mma_step<kSplit>(acc_w, gh, gl, make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024), id_w,
+            mma_step_warp<kSplit>(acc_w, gh, gl, make_desc(hh + km, 16384, 1024), make_desc(hl + km, 16384, 1024), id_w,
                              acc0);
-            mma_bf16(acc_b, gh, ones, id_b, acc0);
-            if (kSplit) mma_bf16(acc_b, gl, ones, id_b, 1);
+            mma_bf16_warp(acc_b, gh, ones, id_b, acc0);
+            if (kSplit) mma_bf16_warp(acc_b, gl, ones, id_b, 1);
           }
-          mma_commit(&emptyH[0]);
+          mma_commit_warp(&emptyH[0]);
         }
-        SAGIPS_TIMED(wa, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
-        if (!kWgrad) trace_pt(trace, j, i, 1);
+        SAGIPS_TIMED(wq, 3, mbar_wait(&tempty[b], ((i >> 1) & 1) ^ 1));
+        if (!kWgrad) if (lane == 0) trace_pt(trace, j, i, 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
@@ -1370,13 +1383,13 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           const uint32_t kk = (k >> 2) * 16384 + (k & 3) * 32;  // K-major step (16 columns)
           const uint32_t km = k * 2048;
           // dgrad: D[rows][in] = G[rows][out] * W[out][in]
-          mma_step<kSplit>(d, make_desc(zh + kk, 16, 1024), make_desc(zl + kk, 16, 1024),
+          mma_step_warp<kSplit>(d, make_desc(zh + kk, 16, 1024), make_desc(zl + kk, 16, 1024),
                            make_desc(wh + km, 16384, 1024), make_desc(wl + km, 16384, 1024), id_d, k > 0);
         }
-        mma_commit(&emptyG[s]);
-        mma_commit(&tfull[b]);
+        mma_commit_warp(&emptyG[s]);
+        mma_commit_warp(&tfull[b]);
       }
-      mma_commit(&wdone[0]);
+      mma_commit_warp(&wdone[0]);
     }
     __syncwarp();
   } else {
