@@ -177,29 +177,44 @@ def test_step_paper_widths_ragged(impl, fused_env):
 
 
 @pytest.mark.parametrize("fused_env", ["1", "0"], indirect=True)
-def test_bf16_step_within_bf16_tolerances(fused_env):
+def test_bf16_step_elementwise(fused_env):
     """SAGIPS_PREC_BF16 (C5's precision): discriminator GEMMs in bf16 with fp32
-    accumulation.  Stated tolerances (Parity), twice the error of
-    an exact-accumulation bf16 emulation of the same step
-    (tests/tools/bf16_error_model.py: L_D 1.3e-3, L_G 4e-4, dW_D 1.3e-2,
-    dy 0.124 relative L2 -- dy cancels heavily): losses 5e-3 relative,
-    dW_D 5e-2, dy and the packet 0.25 in relative L2 norm."""
+    accumulation, at 2N = 2^18 rows.  Every element of dW_D, db_D, dy, draw,
+    the packet and db_G, and both losses, within the first-order bf16 error
+    bound of the oracle's own values (tests/bf16_bound.py: operand rounding
+    2^-9 propagated through |h| |W| forward and backward, x2) plus the
+    LeakyReLU kink deviation with per-element bands and a 1e-4 max|ref|
+    floor.  The G step is compared through the GPU's updated D (as the fp32
+    step tests)."""
+    from tests import bf16_bound
     L = lib()
-    cfg = L.config_init(1, seed=4, param_samples=64, events_per_sample=64, precision=L.PREC_BF16)
+    cfg = L.config_init(1, seed=4, param_samples=128, events_per_sample=1024, precision=L.PREC_BF16)
     ctx = make_ctx(cfg)
     ocfg = oracle_config(cfg)
     st = gan.RankState(ocfg, 0)
     sync_params(ctx, st)
+    d0 = ([w.copy() for w in st.dW], [b.copy() for b in st.db])
+    g0 = ([w.copy() for w in st.gW], [b.copy() for b in st.gb])
     ctx.train_step(0, L.STEP_LOCAL_ONLY, _stream())
     out = gan.local_step(ocfg, st, 0)
+    gpu_d = (unflat(ctx.get(L.T_DISC_W), st.dW), unflat(ctx.get(L.T_DISC_B), st.db))
+    _, g_cache = mlp.forward(g0[0], g0[1], out["z"], ocfg.leaky_slope)
+    og = gan.generator_step(ocfg, gpu_d[0], gpu_d[1], g0[0], g_cache, out["raw"], out["u"], out["y"])
+    tol = bf16_bound.step_tolerances(ocfg, d0, gpu_d, g0, out)
     s = ctx.get(L.T_STATS)
-    assert s.loss_d == pytest.approx(out["loss_d"], rel=5e-3)
-    assert s.loss_g == pytest.approx(out["loss_g"], rel=5e-3)
-    for which, ref, tol in ((L.T_DISC_DW, flat(out["dW_d"]), 5e-2), (L.T_DY, out["dy"], 0.25),
-                            (L.T_GEN_DW, out["packet"], 0.25)):
+    assert abs(s.loss_d - out["loss_d"]) <= 2 * tol["loss_d"] + 1e-6, (s.loss_d, out["loss_d"], tol["loss_d"])
+    assert abs(s.loss_g - og["loss_g"]) <= 2 * tol["loss_g"] + 1e-6, (s.loss_g, og["loss_g"], tol["loss_g"])
+    worst = {}
+    for name, which, ref in (("dW_d", L.T_DISC_DW, flat(out["dW_d"])), ("db_d", L.T_DISC_DB, flat(out["db_d"])),
+                             ("dy", L.T_DY, og["dy"]), ("draw", L.T_DRAW, og["draw"]),
+                             ("packet", L.T_GEN_DW, og["packet"]), ("db_g", L.T_GEN_DB, flat(og["db_g"]))):
         g = ctx.get(which).astype(np.float64)
         r = np.asarray(ref, dtype=np.float64).reshape(-1)
-        assert np.linalg.norm(g - r) <= tol * np.linalg.norm(r), which
+        allowed = tol[name] + 1e-4 * np.max(np.abs(r))
+        ratio = np.abs(g - r) / allowed
+        worst[name] = float(ratio.max())
+        assert np.all(ratio <= 1.0), f"{name}: {int(np.sum(ratio > 1))} elements outside the bf16 bound (worst {ratio.max():.3g})"
+    print("bf16 step: worst error / bound", worst)
 
 
 def test_full_step_applies_generator_update():
