@@ -5,14 +5,18 @@ What the GPU computes in bf16 (everything else is fp32): the 128 -> 128
 hidden layers' GEMMs -- forward Z = bf16(H) bf16(W)^T, dgrad with bf16(G)
 bf16(W), wgrad G^T H with bf16(G) bf16(H) and the bias gradient bf16(G)^T 1
 -- all with fp32 accumulation.  A round-to-nearest bf16 operand carries a
-relative error uniform in [-u, u], u = 2^-9 (variance u^2 / 3).
+relative error of at most u = 2^-8 (8 significant bits; the error is uniform
+in [-ulp/2, ulp/2] and ulp / x <= 2^-7), taken as uniform in [-u, u]
+(variance u^2 / 3, a slight over-estimate of the log-uniform average).
 
 Error model (a mixed bound, reading R33):
-* inside a row's forward / backward chain the rounding errors of the K = 128
-  terms of a dot product are independent, so their variances add (root sum
-  of squares): var(dz) = var(dh) W^2 + (2 u^2 / 3) h^2 W^2 per bf16 layer
-  (LeakyReLU is 1-Lipschitz: var(dh) <= var(dz)); the same backwards for the
-  dgrad chain; a row's bound is C_SIGMA = 6 standard deviations;
+* inside a row's forward / backward chain the roundings of different operand
+  elements are independent, so their variances add; a row's bound is
+  C_SIGMA = 6 standard deviations.  For dy (one row's whole G step) the
+  variance is the exact first-order one: every rounded operand times its
+  downstream sensitivity (dy_variance).  For the D step's per-row errors the
+  cheaper diagonal chain var(dz) = var(dh) W^2 + (2 u^2 / 3) h^2 W^2 is used
+  (LeakyReLU is 1-Lipschitz: var(dh) <= var(dz));
 * across rows -- the weight-gradient and loss sums, whose per-row errors share
   the weights' rounding and may add coherently -- the per-row bounds add
   linearly (worst case), plus the wgrad's own operand rounding 2.01 u |G|^T |h|.
@@ -28,7 +32,7 @@ import numpy as np
 
 from oracle import mlp, proxy
 
-U_BF16 = 2.0 ** -9
+U_BF16 = 2.0 ** -8
 VAR2 = 2.0 * U_BF16 ** 2 / 3.0   # variance of a product of two rounded operands (relative^2)
 C2U = 2.01 * U_BF16              # worst case of that product's relative error
 C_SIGMA = 6.0
@@ -63,7 +67,7 @@ def forward_var(Ws, bs, x, alpha):
     return h, cache, vz, vh
 
 
-def backward_bounds(Ws, cache, vz, vh, dout, vdout, alpha, kink_mode=0, bf16=True):
+def backward_bounds(Ws, cache, vz, vh, dout, vdout, alpha, kink_mode=0, bf16=True, values_only=False):
     """Reverse pass.  dout: gradient at the output, vdout: its per-row error
     variance.  kink_mode 0: the oracle's branches; +1 / -1: every branch with
     |z| <= C_SIGMA sqrt(vz) forced positive / negative.  Returns (dWs, dbs,
@@ -87,12 +91,15 @@ def backward_bounds(Ws, cache, vz, vh, dout, vdout, alpha, kink_mode=0, bf16=Tru
             slope = np.where(pos, 1.0, alpha)
             dz, vdz = g * slope, v * slope * slope
         bf = bf16 and _is_bf16(Ws, l)
-        sdz = C_SIGMA * np.sqrt(vdz)
         dWs[l] = dz.T @ h
+        dbs[l] = dz.sum(axis=0)
+        if values_only:
+            g = dz @ Ws[l]
+            continue
+        sdz = C_SIGMA * np.sqrt(vdz)
         edWs[l] = sdz.T @ np.abs(h) + (C2U * (np.abs(dz).T @ np.abs(h)) if bf else 0.0)
         if vh is not None:
             edWs[l] = edWs[l] + np.abs(dz).T @ (C_SIGMA * np.sqrt(vh[l]))
-        dbs[l] = dz.sum(axis=0)
         edbs[l] = sdz.sum(axis=0) + (U_BF16 * np.abs(dz).sum(axis=0) if bf else 0.0)
         W2 = Ws[l] ** 2
         g = dz @ Ws[l]
@@ -121,7 +128,7 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
     res["loss_d"] = float(np.mean(s_logit))                  # |softplus'| <= 1, linear over rows
     refs = None
     for mode in (0, 1, -1):
-        dW, db, _, edW, edb, _ = backward_bounds(d_before[0], cD, vzD, vhD, dz, vdz, a, mode)
+        dW, db, _, edW, edb, _ = backward_bounds(d_before[0], cD, vzD, vhD, dz, vdz, a, mode, values_only=mode != 0)
         if mode == 0:
             refs = (_flat(dW), _flat(db))
             res["dW_d"], res["db_d"] = _flat(edW), _flat(edb)
@@ -135,11 +142,16 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
     vdzG = ((0.25 / N) ** 2 * vzG[-1][:, 0])[:, None]
     _, gcache = mlp.forward(g_params[0], g_params[1], out["z"], a)
     raw = gcache[-1][1]
+    # dy: the exact first-order variance (dy_variance); the diagonal chain
+    # model of backward_bounds under-estimates it (a rounded operand feeds
+    # every output of its layer, so the errors of one layer's outputs are
+    # correlated) -- checked by emulating the GPU's bf16 roundings in numpy
+    edy0 = C_SIGMA * np.sqrt(dy_variance(d_after[0], d_after[1], out["y"], a, 1.0 / N))
     vals0 = None
     for mode in (0, 1, -1):
-        _, _, dy, _, _, vdy = backward_bounds(d_after[0], cG, vzG, vhG, dzG, vdzG, a, mode)
+        _, _, dy, _, _, _ = backward_bounds(d_after[0], cG, vzG, vhG, dzG, vdzG, a, mode, values_only=True)
         _, draw = proxy.sampler_backward(dy, out["u"], raw, m)
-        edy = C_SIGMA * np.sqrt(vdy)
+        edy = edy0
         # the sampler backward and the generator are linear in dy with
         # |u^j| <= 1 and |softplus'| <= 1: the bound through the same
         # functions on absolute values (raw = 50: softplus' = 1; slope 1)
@@ -147,8 +159,9 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
         dWg, dbg, _ = mlp.backward(g_params[0], gcache, draw, a)
         # the generator (fp32) propagates the draw error: within a sample's
         # chain as variance, over the k samples linearly
-        _, _, _, edWg, edbg, _ = backward_bounds(g_params[0], gcache, None, None, draw,
-                                                 (np.abs(edraw) / C_SIGMA) ** 2, a, 0, bf16=False)
+        if mode == 0:
+            _, _, _, edWg, edbg, _ = backward_bounds(g_params[0], gcache, None, None, draw,
+                                                     (np.abs(edraw) / C_SIGMA) ** 2, a, 0, bf16=False)
         vals = (dy.reshape(-1), draw.reshape(-1), _flat(dWg), _flat(dbg))
         if mode == 0:
             vals0 = vals
@@ -158,3 +171,61 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
             for k, v, r in zip(("dy", "draw", "packet", "db_g"), vals, vals0):
                 res[k] = res[k] + np.abs(v - r)
     return res
+
+
+def dy_variance(Ws, bs, y, alpha, scale):
+    """Exact first-order variance of the G step's dy under bf16 operand
+    rounding (per row, per component), by the downstream sensitivities of
+    every rounded operand: the forward layers' inputs and weights reach dy
+    through the logit (dy = dz q, dz = (sigmoid(z) - 1) scale, q = the
+    row's backward chain of a unit dz); the dgrad layers' inputs G and
+    weights reach it through S_l = d dy / d (G_{l+1} W_l).  Independent
+    roundings (relative variance u^2 / 3 each) add their variances."""
+    u2 = U_BF16 ** 2 / 3.0
+    L = len(Ws)
+    h = np.asarray(y, dtype=np.float64)
+    hs, zs = [], []
+    for l in range(L):
+        z = h @ Ws[l].T + bs[l]
+        hs.append(h)
+        zs.append(z)
+        h = mlp.lrelu(z, alpha) if l < L - 1 else z
+    logit = h[:, 0]
+    dz = (mlp.sigmoid(logit) - 1.0) * scale
+    sig_p = mlp.sigmoid(logit) * (1.0 - mlp.sigmoid(logit)) * scale
+    # d logit / d z_{l+1} and d logit / d h_l for the hidden layers (backward of a unit logit)
+    g = np.ones((h.shape[0], 1))
+    gz, gh = [None] * L, [None] * L
+    for l in reversed(range(L)):
+        dzl = g if l == L - 1 else g * mlp.lrelu_grad(zs[l], alpha)
+        gz[l] = dzl
+        g = dzl @ Ws[l]
+        gh[l] = g
+    var_logit = np.zeros(h.shape[0])
+    for l in range(L):
+        if not _is_bf16(Ws, l):
+            continue
+        # input rounding: sum_k (d logit / d h_k)^2 h_k^2 ; weight rounding: sum_j (d logit / d z_j)^2 sum_k h_k^2 W_jk^2
+        var_logit += u2 * np.sum(gh[l] ** 2 * hs[l] ** 2, axis=1)
+        var_logit += u2 * np.sum(gz[l] ** 2 * ((hs[l] ** 2) @ (Ws[l].T ** 2)), axis=1)
+    # the backward chain of a unit dz: G_4 = w m_4, G_l = (G_{l+1} W_l) m_l; q = G_1 W_0
+    Gs = [None] * L
+    G = np.repeat(Ws[L - 1][0][None, :], h.shape[0], axis=0) * mlp.lrelu_grad(zs[L - 2], alpha)
+    for l in range(L - 2, 0, -1):
+        Gs[l] = G  # G_{l+1}: the input of the dgrad with W_l
+        G = (G @ Ws[l]) * mlp.lrelu_grad(zs[l - 1], alpha)
+    q = G @ Ws[0]                                     # [rows, 2]
+    var = (sig_p ** 2 * var_logit)[:, None] * q ** 2  # through dz
+    # dgrad roundings: S_1 = m_1 W_0[:, o], S_l = m_l (W_{l-1} S_{l-1}); G's scale is dz
+    # S[o]: [rows, 128] per output component o
+    S = [mlp.lrelu_grad(zs[0], alpha) * Ws[0][:, o][None, :] for o in range(2)]
+    for l in range(1, L - 1):
+        Gl2 = (Gs[l] * dz[:, None]) ** 2                                  # G_{l+1}^2 of this row
+        GW2 = Gl2 @ (Ws[l] ** 2)
+        for o in range(2):
+            WS = S[o] @ Ws[l].T                                           # d dy_o / d G_{l+1}
+            var[:, o] += u2 * np.sum(Gl2 * WS ** 2, axis=1)               # G rounding
+            var[:, o] += u2 * np.sum(S[o] ** 2 * GW2, axis=1)             # W rounding
+            if l + 1 < L - 1:
+                S[o] = mlp.lrelu_grad(zs[l], alpha) * WS
+    return var

@@ -273,8 +273,9 @@ def test_step_order_and_exchange_state_errors():
 
 def test_full_size_paper_step_sampled():
     """C2 at full size (k = m = 1024, 2N = 2^21 rows) in the launch
-    configuration bench.py times: both losses, the histograms and sampled
-    events / indices against the oracle."""
+    configuration bench.py times (fused discriminator kernels): both losses
+    (1e-5), the histograms, sampled events / indices and every gradient
+    against the independent oracle."""
     L = lib()
     cfg = L.config_init(1, seed=2)
     ctx = make_ctx(cfg)
@@ -293,8 +294,15 @@ def test_full_size_paper_step_sampled():
     assert_rel(ev[N + idx], out["y"][idx], 1e-5, 1e-5, "fake events (sampled)")
     hist = ctx.get(L.T_HIST).astype(np.int64).reshape(2, 2, -1)
     assert np.array_equal(hist[0], out["hist"][0])
+    assert np.abs(hist[1] - out["hist"][1]).sum() <= max(4, N // 20000)  # R22: fake events within an ULP of an edge
+    # every gradient of the step against the independent oracle (its own D
+    # step and Adam, then its own G step), sampled rows for dy
     assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
+    assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G")
+    assert_grad_close(ctx.get(L.T_DRAW), out["draw"].reshape(-1), 1e-3, "draw")
+    assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], out["dy"][idx], 1e-3, "dy (sampled rows)")
     assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
+    assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
 
 
 def test_step_is_deterministic():
