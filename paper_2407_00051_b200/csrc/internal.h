@@ -198,6 +198,7 @@ struct DFwdArgs {
   uint4* m3;
   uint8_t* g4;             // G_4 plane tiles (hi + lo)
   unsigned long long* trace;  // diagnostic (SAGIPS_FUSED_TRACE=1), else nullptr
+  int exp;                 // diagnostic (SAGIPS_DFWD_EXP): 1 skip the head-gradient colsum, 2 skip the G_4 stores, 4 skip the H stores
 };
 int fused_grid(int64_t rows);
 void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st);

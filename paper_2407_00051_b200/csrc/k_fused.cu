@@ -624,7 +624,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
           m = 0u;
         }
         mb[c] = m;
-        store_plane_words(plane, r, h, c, hw);
+        if (!(a.exp & 4)) store_plane_words(plane, r, h, c, hw);
       }
       reinterpret_cast<uint2*>((l == 0 ? a.m2 : a.m3) + t * 128 + r)[h] = make_uint2(mb[0], mb[1]);
     }
@@ -684,9 +684,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
             split2(mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y)), hw[k + u], lw[k + u]);
           }
         }
-        store_plane_words(gplane, r, h, c, hw);
-        if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
-        const float cs = colsum32(g, lane);
+        if (!(a.exp & 2)) {
+          store_plane_words(gplane, r, h, c, hw);
+          if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
+        }
+        const float cs = (a.exp & 1) ? g[0] + g[31] : colsum32(g, lane);
         if (c == 0) gacc0 += cs;
         else gacc1 += cs;
       }

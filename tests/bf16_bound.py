@@ -146,7 +146,9 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
     # model of backward_bounds under-estimates it (a rounded operand feeds
     # every output of its layer, so the errors of one layer's outputs are
     # correlated) -- checked by emulating the GPU's bf16 roundings in numpy
-    edy0 = C_SIGMA * np.sqrt(dy_variance(d_after[0], d_after[1], out["y"], a, 1.0 / N))
+    # plus, for dy, the first-order bound of any pattern of LeakyReLU' flips
+    vdy, kdy = dy_variance(d_after[0], d_after[1], out["y"], a, 1.0 / N, with_kinks=True)
+    edy0 = C_SIGMA * np.sqrt(vdy) + kdy
     vals0 = None
     for mode in (0, 1, -1):
         _, _, dy, _, _, _ = backward_bounds(d_after[0], cG, vzG, vhG, dzG, vdzG, a, mode, values_only=True)
@@ -166,21 +168,28 @@ def step_tolerances(cfg, d_before, d_after, g_params, out):
         if mode == 0:
             vals0 = vals
             res["dy"], res["draw"] = edy.reshape(-1), np.abs(edraw).reshape(-1)
+            res["dy_forced"] = np.zeros_like(res["dy"])
             res["packet"], res["db_g"] = _flat(edWg), _flat(edbg)
         else:
-            for k, v, r in zip(("dy", "draw", "packet", "db_g"), vals, vals0):
+            for k, v, r in zip(("dy_forced", "draw", "packet", "db_g"), vals, vals0):
                 res[k] = res[k] + np.abs(v - r)
+    res.pop("dy_forced")  # dy carries the per-flip kink bound instead of the forced extremes
     return res
 
 
-def dy_variance(Ws, bs, y, alpha, scale):
+def dy_variance(Ws, bs, y, alpha, scale, with_kinks=False):
     """Exact first-order variance of the G step's dy under bf16 operand
     rounding (per row, per component), by the downstream sensitivities of
     every rounded operand: the forward layers' inputs and weights reach dy
     through the logit (dy = dz q, dz = (sigmoid(z) - 1) scale, q = the
     row's backward chain of a unit dz); the dgrad layers' inputs G and
     weights reach it through S_l = d dy / d (G_{l+1} W_l).  Independent
-    roundings (relative variance u^2 / 3 each) add their variances."""
+    roundings (relative variance u^2 / 3 each) add their variances.
+    with_kinks: also the first-order bound of LeakyReLU' decisions that may
+    differ (|Z| within C_SIGMA of its forward error): flipping the branch of
+    element j of layer l changes dy by (1 - alpha) |P_l[j]| |S_l[j]|, P_l =
+    G_{l+1} W_l before the mask; summed over a row's ambiguous elements
+    (any pattern of flips)."""
     u2 = U_BF16 ** 2 / 3.0
     L = len(Ws)
     h = np.asarray(y, dtype=np.float64)
@@ -209,15 +218,21 @@ def dy_variance(Ws, bs, y, alpha, scale):
         var_logit += u2 * np.sum(gh[l] ** 2 * hs[l] ** 2, axis=1)
         var_logit += u2 * np.sum(gz[l] ** 2 * ((hs[l] ** 2) @ (Ws[l].T ** 2)), axis=1)
     # the backward chain of a unit dz: G_4 = w m_4, G_l = (G_{l+1} W_l) m_l; q = G_1 W_0
-    Gs = [None] * L
-    G = np.repeat(Ws[L - 1][0][None, :], h.shape[0], axis=0) * mlp.lrelu_grad(zs[L - 2], alpha)
+    Gs, Ps = [None] * L, [None] * L
+    G = np.repeat(Ws[L - 1][0][None, :], h.shape[0], axis=0)
+    Ps[L - 1] = G                                     # the head's "pre-mask" G_4 (mask of Z_4)
+    G = G * mlp.lrelu_grad(zs[L - 2], alpha)
     for l in range(L - 2, 0, -1):
         Gs[l] = G  # G_{l+1}: the input of the dgrad with W_l
-        G = (G @ Ws[l]) * mlp.lrelu_grad(zs[l - 1], alpha)
+        Ps[l] = G @ Ws[l]
+        G = Ps[l] * mlp.lrelu_grad(zs[l - 1], alpha)
     q = G @ Ws[0]                                     # [rows, 2]
     var = (sig_p ** 2 * var_logit)[:, None] * q ** 2  # through dz
-    # dgrad roundings: S_1 = m_1 W_0[:, o], S_l = m_l (W_{l-1} S_{l-1}); G's scale is dz
-    # S[o]: [rows, 128] per output component o
+    kink = np.zeros_like(var)
+    if with_kinks:  # bands of the pre-activations Z_1..Z_4 (Z_1 is fp32: no band)
+        _, _, vz, _ = forward_var(Ws, bs, y, alpha)
+        amb = [np.abs(zs[l]) <= C_SIGMA * np.sqrt(vz[l]) for l in range(L)]
+    # S[o]: [rows, 128] per output component o; S_1 = m_1 W_0[:, o], S_l = m_l (W_{l-1} S_{l-1})
     S = [mlp.lrelu_grad(zs[0], alpha) * Ws[0][:, o][None, :] for o in range(2)]
     for l in range(1, L - 1):
         Gl2 = (Gs[l] * dz[:, None]) ** 2                                  # G_{l+1}^2 of this row
@@ -226,6 +241,8 @@ def dy_variance(Ws, bs, y, alpha, scale):
             WS = S[o] @ Ws[l].T                                           # d dy_o / d G_{l+1}
             var[:, o] += u2 * np.sum(Gl2 * WS ** 2, axis=1)               # G rounding
             var[:, o] += u2 * np.sum(S[o] ** 2 * GW2, axis=1)             # W rounding
+            if with_kinks:  # the mask of Z_{l+1}, applied to P_{l+1} (the head's G_4 for l + 1 = 4)
+                kink[:, o] += (1.0 - alpha) * np.sum(amb[l] * np.abs(Ps[l + 1] * dz[:, None]) * np.abs(WS), axis=1)
             if l + 1 < L - 1:
                 S[o] = mlp.lrelu_grad(zs[l], alpha) * WS
-    return var
+    return (var, kink) if with_kinks else var
