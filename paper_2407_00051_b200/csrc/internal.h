@@ -161,6 +161,11 @@ struct BwdLaunch {
   float* part_db = nullptr;    // [ctas][128]
   float* part_l0 = nullptr;    // [ctas][384]
   uint32_t* tile_ctr = nullptr;  // no wgrad (G step): dynamic tile schedule counter (zeroed before the launch)
+  // the fused D step's layer after the head (split): G = dz (Z > 0 ? w : alpha w)
+  // generated in shared memory instead of loading g (k_tc_layers.cu kGenG)
+  const float* gen_dz = nullptr;   // [rows_t] dz per row
+  const uint4* gen_mask = nullptr; // [rows_t] sign bits of Z_4 (per-layer mask layout)
+  const float* gen_w = nullptr;    // [128] head weights
 };
 enum { FWD_FIRST = 0, FWD_MID = 1, FWD_HEAD = 2 };
 // k_fused.cu: the fused discriminator kernels (paper widths, depth 4)
@@ -196,7 +201,9 @@ struct DFwdArgs {
   uint4* m2;
   uint8_t* h3;             // H_3 plane tiles (hi plane written) + masks
   uint4* m3;
-  uint8_t* g4;             // G_4 plane tiles (hi + lo)
+  uint8_t* g4;             // G_4 plane tiles (hi + lo), or nullptr: dz and m4 instead (split)
+  float* dz;               // [rows_t] dz per row (rows past the end: 0)
+  uint4* m4;               // [rows_t] sign bits of Z_4 (per-layer mask layout)
   unsigned long long* trace;  // diagnostic (SAGIPS_FUSED_TRACE=1), else nullptr
   int exp;                 // diagnostic (SAGIPS_DFWD_EXP): 1 skip the head-gradient colsum, 2 skip the G_4 stores, 4 skip the H stores
 };

@@ -496,8 +496,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
 // n_real, else label_rest), dz, G_4 = dz w (.) LeakyReLU'(Z_4).  What the
 // per-layer backward passes read goes to HBM in their plane-tile format: the
 // hi planes and sign masks of H_2 and H_3 (the wgrad uses the hi plane only,
-// R28) and the G_4 planes; plus the logits, the per-CTA loss and the head
-// gradient partials (dW_head = sum dz H_4, db_head = sum dz).
+// R28) and, for G_4 = dz w (.) LeakyReLU'(Z_4), either its planes (bf16) or
+// -- fp32-class -- just dz and the sign bits of Z_4 (20 B/row instead of 512:
+// the next pass regenerates the planes in shared memory, k_tc_layers.cu
+// kGenG); plus the logits, the per-CTA loss and the head gradient partials
+// (dW_head = sum dz H_4, db_head = sum dz).
 template <bool kSplit>
 __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ DFwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -656,11 +659,13 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
       lacc += (double)(tl * softplus_neg(zz) + (1.f - tl) * softplus_neg(-zz));
       gbacc += dz;
     }
-    uint8_t* gplane = a.g4 + t * TB;
+    uint8_t* gplane = a.g4 ? a.g4 + t * TB : nullptr;
     const float2 dz2 = make_float2(dz, dz);
+    if (!gplane && h == 0) a.dz[row] = dz;  // the backward generates G_4 from dz and the sign bits (kGenG)
     {
       float v[64];
       tmem_ld32x2(accT, accT + 32u, v, v + 32);
+      uint32_t mb[2] = {0u, 0u};
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t hw[16], lw[16];
@@ -679,12 +684,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
             const float2 hd = mul2(dz2, make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)));  // dz H_4
             g[2 * (k + u)] = hd.x;
             g[2 * (k + u) + 1] = hd.y;
-            const float2 w = u ? make_float2(wq.z, wq.w) : make_float2(wq.x, wq.y);
-            const float2 wa = u ? make_float2(aq.z, aq.w) : make_float2(aq.x, aq.y);
-            split2(mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y)), hw[k + u], lw[k + u]);
+            if (gplane) {
+              const float2 w = u ? make_float2(wq.z, wq.w) : make_float2(wq.x, wq.y);
+              const float2 wa = u ? make_float2(aq.z, aq.w) : make_float2(aq.x, aq.y);
+              split2(mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y)), hw[k + u], lw[k + u]);
+            } else {  // sign bits of Z_4, column 2kk -> bit kk, 2kk + 1 -> bit 16 + kk
+              mb[c] |= (z.x > 0.f ? 1u : 0u) << (k + u);
+              mb[c] |= (z.y > 0.f ? 1u : 0u) << (16 + k + u);
+            }
           }
         }
-        if (!(a.exp & 2)) {
+        if (gplane && !(a.exp & 2)) {
           store_plane_words(gplane, r, h, c, hw);
           if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
         }
@@ -692,6 +702,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
         if (c == 0) gacc0 += cs;
         else gacc1 += cs;
       }
+      if (!gplane) reinterpret_cast<uint2*>(a.m4 + t * 128 + r)[h] = make_uint2(valid ? mb[0] : 0u, valid ? mb[1] : 0u);
     }
     tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
     stamp(3, 0);

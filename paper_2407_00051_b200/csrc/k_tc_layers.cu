@@ -992,9 +992,15 @@ __device__ __forceinline__ void fwd_body(const FwdLaunch& a, int j, int n, unsig
 // ============================================================== backward
 // kH1Load (first layer, wgrad): the H_1 planes are bulk-loaded (written by the
 // pipelined forward first-layer role) instead of recomputed by SIMT producers
-template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
+template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false, bool kGenG = false>
 __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsigned long long* trace,
                                          WaitAcct wa = {}) {
+  // kGenG (fused D step, the layer after the head, split): the G_4 planes are
+  // not loaded but generated in shared memory by the producer warps from what
+  // k_dfwd stored instead -- dz per row and the sign mask of Z_4:
+  // G_4[r][c] = dz_r (Z_4[r][c] > 0 ? w_c : alpha w_c), 20 B/row instead of a
+  // 512 B/row plane pair in HBM (written once, read once)
+  static_assert(!kGenG || (kSplit && !kFirst && kWgrad), "kGenG: split, non-first wgrad pass");
   constexpr int P = kSplit ? 2 : 1;
   constexpr uint32_t TB = P * kPlane;
   constexpr bool kDy = kFirst && !kWgrad;
@@ -1071,6 +1077,12 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       p0->b0[i] = a.b0[i];
     }
   }
+  if (kGenG) {  // the head weights w and alpha w (p0 is free: not the first layer)
+    for (int i = tid; i < 128; i += kThreads) {
+      p0->w0x[i] = a.gen_w[i];
+      p0->w0y[i] = a.alpha * a.gen_w[i];
+    }
+  }
   if (warp < kPW) stage_weights<kSplit>(a.W, smem_u32(sW), smem_u32(sW + kPlane), warp, lane);
   fence_proxy_async_smem();
   tc_fence_before();
@@ -1105,6 +1117,45 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   auto pl_addr = [&](int slot) -> uint32_t { return smem_u32(sG) + (uint32_t)slot * kPlane; };
 
   if (warp < kPW) {
+    // ---------------- SIMT producers of the G_4 planes (kGenG): thread = row
+    if (kGenG) {
+      const int r = 32 * warp + lane;
+      for (int i = 0; i < nmine; ++i) {
+        const int64_t row = tile_of(i) * 128 + r;
+        const float dz = __ldg(a.gen_dz + row);
+        const uint4 mq = __ldg(a.gen_mask + row);
+        const PS gh = pl_gh(i), gl = pl_gl(i);
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
+        const uint32_t hb = pl_addr(gh.slot), lb = pl_addr(gl.slot);
+        const float2 dz2 = make_float2(dz, dz);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {  // 32-column blocks: mask word cb (bit k = column 2k, bit 16 + k = 2k + 1)
+          const uint32_t m = cb == 0 ? mq.x : cb == 1 ? mq.y : cb == 2 ? mq.z : mq.w;
+          uint32_t hw[16], lw[16];
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            const int col = 32 * cb + 2 * kk;
+            const float2 w = *reinterpret_cast<const float2*>(&p0->w0x[col]);
+            const float2 wa2 = *reinterpret_cast<const float2*>(&p0->w0y[col]);
+            const float2 g = mul2(dz2, make_float2(((m >> kk) & 1u) ? w.x : wa2.x, ((m >> (16 + kk)) & 1u) ? w.y : wa2.y));
+            split2(g.x, g.y, hw[kk], lw[kk]);
+          }
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const uint32_t off = sw128_chunk(r, 4 * cb + jj, 128);
+            sts128(hb + off, hw[4 * jj], hw[4 * jj + 1], hw[4 * jj + 2], hw[4 * jj + 3]);
+            sts128(lb + off, lw[4 * jj], lw[4 * jj + 1], lw[4 * jj + 2], lw[4 * jj + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+        if (warp == 0 && lane == 0) {
+          mbar_arrive(&pfull[gh.slot]);
+          mbar_arrive(&pfull[gl.slot]);
+        }
+      }
+    }
     // ---------------- SIMT producers of H_1 planes (first layer, wgrad)
     if (kFirst && kWgrad && !kH1Load) {
       const float2* X2 = reinterpret_cast<const float2*>(a.X);
@@ -1165,15 +1216,17 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           mbar_arrive_expect_tx(&xfull[xb], bytes);
           bulk_g2s(smem_u32(sX + xb * 128), reinterpret_cast<const float2*>(a.X) + r0, bytes, &xfull[xb]);
         }
-        ring_wait_ready(a.g, t, wa);
-        load(pl_gh(i), gsrc);
+        if (!kGenG) {
+          ring_wait_ready(a.g, t, wa);
+          load(pl_gh(i), gsrc);
+        }
         if (kT && kSplit) load(pl_gl(i), gsrc + kPlane);
         if (kLoadH) {  // (else the producers write it)
           const uint8_t* hsrc = a.h.base + ring_slot(a.h, t) * TB;
           ring_wait_ready(a.h, t, wa);
           load(pl_hh(i), hsrc);
         }
-        if (!kT) load(pl_gl(i), gsrc + kPlane);
+        if (!kT && !kGenG) load(pl_gl(i), gsrc + kPlane);
         trace_pt(trace, j, i, 0);
       }
     } else if (!kPR && lane == 0) {
@@ -1682,11 +1735,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fwd(const __grid_constant__ Fwd
   fwd_body<kSplit, kFirst, kHead>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
   if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
-template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false>
+template <bool kSplit, bool kFirst, bool kWgrad, bool kH1Load = false, bool kGenG = false>
 __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ BwdLaunch a, unsigned long long* trace) {
   unsigned long long* cs = cta_stamps(trace);
   if (cs && threadIdx.x == 0) cs[0] = globaltimer();
-  bwd_body<kSplit, kFirst, kWgrad, kH1Load>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
+  bwd_body<kSplit, kFirst, kWgrad, kH1Load, kGenG>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
   if (cs && threadIdx.x == 0) cs[1] = globaltimer();
 }
 
@@ -1762,6 +1815,7 @@ static void configure_layers() {
   SAGIPS_BWD(false, false, false) SAGIPS_BWD(false, true, false)
 #undef SAGIPS_BWD
   allow_smem(k_bwd<true, true, true, true>, bwd_smem(true));
+  allow_smem(k_bwd<true, false, true, false, true>, bwd_smem(true));
   allow_smem(k_bwd<false, true, true, true>, bwd_smem(false));
 }
 
@@ -1836,7 +1890,8 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
   const size_t sm = bwd_smem(split);
   const bool h1load = first && wgrad && L.h.base != nullptr;
 #define SAGIPS_BWD_LAUNCH(S)                                                                   \
-  if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(L, tr);               \
+  if (S && !first && wgrad && L.gen_dz) k_bwd<true, false, true, false, true><<<grid, kThreads, sm, st>>>(L, tr); \
+  else if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(L, tr);          \
   else if (h1load) k_bwd<S, true, true, true><<<grid, kThreads, sm, st>>>(L, tr);              \
   else if (first && wgrad) k_bwd<S, true, true><<<grid, kThreads, sm, st>>>(L, tr);            \
   else if (!first) k_bwd<S, false, false><<<grid, kThreads, sm, st>>>(L, tr);                  \

@@ -523,7 +523,11 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     f.m2 = c->dMask[1];
     f.h3 = reinterpret_cast<uint8_t*>(c->dAct[2]);
     f.m3 = c->dMask[2];
-    f.g4 = reinterpret_cast<uint8_t*>(c->dZb[0]);
+    // fp32-class: dz and the Z_4 sign bits (in the otherwise unused H_4
+    // buffers) replace the G_4 planes; bf16: the planes
+    f.g4 = split ? nullptr : reinterpret_cast<uint8_t*>(c->dZb[0]);
+    f.dz = c->dAct[3];
+    f.m4 = c->dMask[3];
     f.trace = fused_trace_buffer();
     {
       const char* e = getenv("SAGIPS_DFWD_EXP");
@@ -609,6 +613,11 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     BwdLaunch b;
     b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
     b.alpha = c->cfg.leaky_slope; b.part = c->lpart[l]; b.part_db = c->ldb[l];
+    if (l == Lh - 1 && split && use_fused(c) && !h1_store() && Lh == 4) {  // G_4 from k_dfwd's dz + sign bits
+      b.gen_dz = c->dAct[3];
+      b.gen_mask = c->dMask[3];
+      b.gen_w = c->dW + D.w_off[Lh];
+    }
     nparts[l] = grid;
     if (l == 1) {
       b.X = c->X; b.W0 = c->dW + D.w_off[0]; b.b0 = c->dB + D.b_off[0]; b.part_l0 = c->colpart;
