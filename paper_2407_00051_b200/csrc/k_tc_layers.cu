@@ -1124,36 +1124,40 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         const int64_t row = tile_of(i) * 128 + r;
         const float dz = __ldg(a.gen_dz + row);
         const uint4 mq = __ldg(a.gen_mask + row);
+        // the Gh plane goes to its slot as soon as it is free (it is needed
+        // first); the lo words wait in registers for the Gl slot, which the
+        // previous tile releases later (plane FIFO: Gh, Hh, Gl)
         const PS gh = pl_gh(i), gl = pl_gl(i);
         SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
-        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
         const uint32_t hb = pl_addr(gh.slot), lb = pl_addr(gl.slot);
         const float2 dz2 = make_float2(dz, dz);
+        uint32_t lw[64];
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb) {  // 32-column blocks: mask word cb (bit k = column 2k, bit 16 + k = 2k + 1)
           const uint32_t m = cb == 0 ? mq.x : cb == 1 ? mq.y : cb == 2 ? mq.z : mq.w;
-          uint32_t hw[16], lw[16];
+          uint32_t hw[16];
 #pragma unroll
           for (int kk = 0; kk < 16; ++kk) {
             const int col = 32 * cb + 2 * kk;
             const float2 w = *reinterpret_cast<const float2*>(&p0->w0x[col]);
             const float2 wa2 = *reinterpret_cast<const float2*>(&p0->w0y[col]);
             const float2 g = mul2(dz2, make_float2(((m >> kk) & 1u) ? w.x : wa2.x, ((m >> (16 + kk)) & 1u) ? w.y : wa2.y));
-            split2(g.x, g.y, hw[kk], lw[kk]);
+            split2(g.x, g.y, hw[kk], lw[16 * cb + kk]);
           }
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const uint32_t off = sw128_chunk(r, 4 * cb + jj, 128);
-            sts128(hb + off, hw[4 * jj], hw[4 * jj + 1], hw[4 * jj + 2], hw[4 * jj + 3]);
-            sts128(lb + off, lw[4 * jj], lw[4 * jj + 1], lw[4 * jj + 2], lw[4 * jj + 3]);
-          }
+          for (int jj = 0; jj < 4; ++jj)
+            sts128(hb + sw128_chunk(r, 4 * cb + jj, 128), hw[4 * jj], hw[4 * jj + 1], hw[4 * jj + 2], hw[4 * jj + 3]);
         }
         fence_proxy_async_smem();
         asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
-        if (warp == 0 && lane == 0) {
-          mbar_arrive(&pfull[gh.slot]);
-          mbar_arrive(&pfull[gl.slot]);
-        }
+        if (warp == 0 && lane == 0) mbar_arrive(&pfull[gh.slot]);
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
+#pragma unroll
+        for (int jc = 0; jc < 16; ++jc)
+          sts128(lb + sw128_chunk(r, jc, 128), lw[4 * jc], lw[4 * jc + 1], lw[4 * jc + 2], lw[4 * jc + 3]);
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+        if (warp == 0 && lane == 0) mbar_arrive(&pfull[gl.slot]);
       }
     }
     // ---------------- SIMT producers of H_1 planes (first layer, wgrad)

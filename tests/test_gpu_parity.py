@@ -299,16 +299,18 @@ def test_full_size_paper_step_sampled():
     # every gradient of the step against the independent oracle (its own D
     # step and Adam, then its own G step), sampled rows for dy.  The G-step
     # quantities per sample (draw) and per row (dy) are checked at 1e-3
-    # through the GPU's updated D and at 1e-2 against the independent
-    # trajectory: after one Adam step a near-zero D gradient of the other
-    # sign moves that weight by 2 lr, which they are sensitive to (the sums
-    # over samples, the packet and db_G, hold 1e-3 either way)
+    # through the GPU's updated D and against the independent trajectory at
+    # 1e-2 (draw elementwise, dy in relative L2 norm: single rows can cancel):
+    # after one Adam step a near-zero D gradient of the other sign moves that
+    # weight by 2 lr, which they are sensitive to (the sums over samples, the
+    # packet and db_G, hold 1e-3 either way)
     assert_grad_close(ctx.get(L.T_GEN_DW), out["packet"], 1e-3, "packet dW_G")
     assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G")
     assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
     assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
     assert_grad_close(ctx.get(L.T_DRAW), out["draw"].reshape(-1), 1e-2, "draw (independent)")
-    assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], out["dy"][idx], 1e-2, "dy (independent, sampled rows)")
+    dyg, dyo = ctx.get(L.T_DY).reshape(-1, 2).astype(np.float64), out["dy"]
+    assert np.linalg.norm(dyg - dyo) <= 1e-2 * np.linalg.norm(dyo), "dy (independent, relative L2)"
     gpu_d = (unflat(ctx.get(L.T_DISC_W), st.dW), unflat(ctx.get(L.T_DISC_B), st.db))
     _, g_cache = mlp.forward(g0[0], g0[1], out["z"], ocfg.leaky_slope)
     og = gan.generator_step(ocfg, gpu_d[0], gpu_d[1], g0[0], g_cache, out["raw"], out["u"], out["y"])
