@@ -493,6 +493,13 @@ static bool h1_store() {
 }
 
 static bool use_fused(const sagips_ctx* c);
+static bool tc_split(const sagips_ctx* c);
+static bool h1_store();
+// SAGIPS_GEN_G=1: the fused D step passes G_4 as dz + sign bits (kGenG)
+static bool gen_g(const sagips_ctx* c) {
+  const char* e = getenv("SAGIPS_GEN_G");
+  return e && e[0] == '1' && tc_split(c) && use_fused(c) && !h1_store();
+}
 
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
                             float scale, float* logits, bool want_grads, cudaStream_t st) {
@@ -523,9 +530,10 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     f.m2 = c->dMask[1];
     f.h3 = reinterpret_cast<uint8_t*>(c->dAct[2]);
     f.m3 = c->dMask[2];
-    // fp32-class: dz and the Z_4 sign bits (in the otherwise unused H_4
-    // buffers) replace the G_4 planes; bf16: the planes
-    f.g4 = split ? nullptr : reinterpret_cast<uint8_t*>(c->dZb[0]);
+    // SAGIPS_GEN_G=1 (fp32-class, measured slower: DESIGN.md 7.1): dz and the
+    // Z_4 sign bits (in the otherwise unused H_4 buffers) replace the G_4
+    // planes and the next pass regenerates them; default: the planes
+    f.g4 = gen_g(c) ? nullptr : reinterpret_cast<uint8_t*>(c->dZb[0]);
     f.dz = c->dAct[3];
     f.m4 = c->dMask[3];
     f.trace = fused_trace_buffer();
@@ -613,7 +621,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     BwdLaunch b;
     b.g = whole(c->dZb[cur]); b.W = c->dW + D.w_off[l]; b.rows = rows;
     b.alpha = c->cfg.leaky_slope; b.part = c->lpart[l]; b.part_db = c->ldb[l];
-    if (l == Lh - 1 && split && use_fused(c) && !h1_store() && Lh == 4) {  // G_4 from k_dfwd's dz + sign bits
+    if (l == Lh - 1 && gen_g(c)) {  // G_4 from k_dfwd's dz + sign bits
       b.gen_dz = c->dAct[3];
       b.gen_mask = c->dMask[3];
       b.gen_w = c->dW + D.w_off[Lh];
