@@ -205,7 +205,6 @@ struct DFwdArgs {
   float* dz;               // [rows_t] dz per row (rows past the end: 0)
   uint4* m4;               // [rows_t] sign bits of Z_4 (per-layer mask layout)
   unsigned long long* trace;  // diagnostic (SAGIPS_FUSED_TRACE=1), else nullptr
-  int exp;                 // diagnostic (SAGIPS_DFWD_EXP): 1 skip the head-gradient colsum, 2 skip the G_4 stores, 4 skip the H stores
 };
 int fused_grid(int64_t rows);
 void launch_gstep(bool split, const GStepArgs& a, cudaStream_t st);

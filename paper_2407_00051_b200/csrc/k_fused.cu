@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
 // the next pass regenerates the planes in shared memory, k_tc_layers.cu
 // kGenG); plus the logits, the per-CTA loss and the head gradient partials
 // (dW_head = sum dz H_4, db_head = sum dz).
-template <bool kSplit>
+template <bool kSplit, bool kGenOut>
 __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ DFwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
           m = 0u;
         }
         mb[c] = m;
-        if (!(a.exp & 4)) store_plane_words(plane, r, h, c, hw);
+        store_plane_words(plane, r, h, c, hw);
       }
       reinterpret_cast<uint2*>((l == 0 ? a.m2 : a.m3) + t * 128 + r)[h] = make_uint2(mb[0], mb[1]);
     }
@@ -659,9 +659,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
       lacc += (double)(tl * softplus_neg(zz) + (1.f - tl) * softplus_neg(-zz));
       gbacc += dz;
     }
-    uint8_t* gplane = a.g4 ? a.g4 + t * TB : nullptr;
+    uint8_t* gplane = kGenOut ? nullptr : a.g4 + t * TB;
     const float2 dz2 = make_float2(dz, dz);
-    if (!gplane && h == 0) a.dz[row] = dz;  // the backward generates G_4 from dz and the sign bits (kGenG)
+    if (kGenOut && h == 0) a.dz[row] = dz;  // the backward generates G_4 from dz and the sign bits (kGenG)
     {
       float v[64];
       tmem_ld32x2(accT, accT + 32u, v, v + 32);
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
             const float2 hd = mul2(dz2, make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)));  // dz H_4
             g[2 * (k + u)] = hd.x;
             g[2 * (k + u) + 1] = hd.y;
-            if (gplane) {
+            if (!kGenOut) {
               const float2 w = u ? make_float2(wq.z, wq.w) : make_float2(wq.x, wq.y);
               const float2 wa = u ? make_float2(aq.z, aq.w) : make_float2(aq.x, aq.y);
               split2(mul2(dz2, make_float2(z.x > 0.f ? w.x : wa.x, z.y > 0.f ? w.y : wa.y)), hw[k + u], lw[k + u]);
@@ -694,15 +694,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
             }
           }
         }
-        if (gplane && !(a.exp & 2)) {
+        if (!kGenOut) {
           store_plane_words(gplane, r, h, c, hw);
           if (kSplit) store_plane_words(gplane + kPlaneF, r, h, c, lw);
         }
-        const float cs = (a.exp & 1) ? g[0] + g[31] : colsum32(g, lane);
+        const float cs = colsum32(g, lane);
         if (c == 0) gacc0 += cs;
         else gacc1 += cs;
       }
-      if (!gplane) reinterpret_cast<uint2*>(a.m4 + t * 128 + r)[h] = make_uint2(valid ? mb[0] : 0u, valid ? mb[1] : 0u);
+      if (kGenOut) reinterpret_cast<uint2*>(a.m4 + t * 128 + r)[h] = make_uint2(valid ? mb[0] : 0u, valid ? mb[1] : 0u);
     }
     tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
     stamp(3, 0);
@@ -814,12 +814,14 @@ int fused_grid(int64_t rows) {
 }
 
 void launch_dfwd(bool split, const DFwdArgs& a, cudaStream_t st) {
-  static bool configured[2] = {false, false};
+  static bool configured[3] = {false, false, false};
   const size_t smem = gstep_smem(split);
-  auto kern = split ? k_dfwd<true> : k_dfwd<false>;
-  if (!configured[split]) {
+  const bool gen = split && a.g4 == nullptr;
+  auto kern = gen ? k_dfwd<true, true> : split ? k_dfwd<true, false> : k_dfwd<false, false>;
+  const int ci = gen ? 2 : split ? 1 : 0;
+  if (!configured[ci]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured[split] = true;
+    configured[ci] = true;
   }
   kern<<<fused_grid(a.rows), kThreadsF, smem, st>>>(a);
   count_launch();

@@ -537,10 +537,6 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     f.dz = c->dAct[3];
     f.m4 = c->dMask[3];
     f.trace = fused_trace_buffer();
-    {
-      const char* e = getenv("SAGIPS_DFWD_EXP");
-      f.exp = e ? atoi(e) : 0;
-    }
     kernel_begin(c, 13, st);
     launch_dfwd(split, f, st);
     kernel_end(c, st);

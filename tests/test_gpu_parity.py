@@ -300,7 +300,8 @@ def test_full_size_paper_step_sampled():
     # step and Adam, then its own G step), sampled rows for dy.  The G-step
     # quantities per sample (draw) and per row (dy) are checked at 1e-3
     # through the GPU's updated D and against the independent trajectory at
-    # 1e-2 (draw elementwise, dy in relative L2 norm: single rows can cancel):
+    # 1e-2 (draw elementwise -- both on dy's tolerance carried through the
+    # sum over events, see below --, dy in relative L2 norm: single rows can cancel):
     # after one Adam step a near-zero D gradient of the other sign moves that
     # weight by 2 lr, which they are sensitive to (the sums over samples, the
     # packet and db_G, hold 1e-3 either way)
@@ -308,14 +309,20 @@ def test_full_size_paper_step_sampled():
     assert_grad_close(ctx.get(L.T_GEN_DB), flat(out["db_g"]), 1e-3, "db_G")
     assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
     assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
-    assert_grad_close(ctx.get(L.T_DRAW), out["draw"].reshape(-1), 1e-2, "draw (independent)")
+    # draw_s = sum over the sample's 1024 events of dy u^j softplus': it
+    # cancels heavily, so its tolerance is dy's 1e-3 carried through that
+    # linear map on magnitudes: 1e-3 sum |dy| |u^j| softplus'
+    m = ocfg.events_per_sample
+    _, draw_mag = proxy.sampler_backward(np.abs(out["dy"]), out["u"], out["raw"], m)
+    tol_draw = 1e-3 * (np.abs(out["draw"]) + draw_mag).reshape(-1)
+    assert np.all(np.abs(ctx.get(L.T_DRAW) - out["draw"].reshape(-1)) <= 10 * tol_draw), "draw (independent)"
     dyg, dyo = ctx.get(L.T_DY).reshape(-1, 2).astype(np.float64), out["dy"]
     assert np.linalg.norm(dyg - dyo) <= 1e-2 * np.linalg.norm(dyo), "dy (independent, relative L2)"
     gpu_d = (unflat(ctx.get(L.T_DISC_W), st.dW), unflat(ctx.get(L.T_DISC_B), st.db))
     _, g_cache = mlp.forward(g0[0], g0[1], out["z"], ocfg.leaky_slope)
     og = gan.generator_step(ocfg, gpu_d[0], gpu_d[1], g0[0], g_cache, out["raw"], out["u"], out["y"])
     assert s.loss_g == pytest.approx(og["loss_g"], rel=1e-5)
-    assert_grad_close(ctx.get(L.T_DRAW), og["draw"].reshape(-1), 1e-3, "draw (through the GPU's D)")
+    assert np.all(np.abs(ctx.get(L.T_DRAW) - og["draw"].reshape(-1)) <= tol_draw), "draw (through the GPU's D)"
     assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], og["dy"][idx], 1e-3, "dy (through the GPU's D, sampled)")
 
 
