@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--sampler", choices=["quadratic", "tabulated"], default="quadratic",
                    help="a3-a9 sampler: the closed-form quantile (R1) or the tabulated CDF (R32, SURVEY 8(f) row 1)")
     p.add_argument("--sampler-grid", type=int, default=1024)
+    p.add_argument("--gen-hidden", type=int, default=0,
+                   help="generator hidden width (exchange bandwidth regime: the weights-only packet is "
+                        "~3 H^2 floats, e.g. H = 4096 -> 201 MB); default: the paper preset's 128")
     p.add_argument("--no-graph", action="store_true",
                    help="launch the step's kernels one by one instead of replaying the captured CUDA graph")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -147,6 +150,9 @@ def lib_config(args, L, rank, world):
             cfg.shard_rows = 1024 * 16384
             cfg.precision = L.PREC_BF16
             workload = "C5: paper MLPs, k=1024 m=16384 (2^24 events/rank/step), bf16 D GEMMs"
+    if getattr(args, "gen_hidden", 0):
+        cfg.gen_hidden = args.gen_hidden
+        workload += f", generator hidden width {args.gen_hidden} (synthetic large packet)"
     cfg.world, cfg.rank = world, rank
     modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
              "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}

@@ -310,11 +310,12 @@ def test_full_size_paper_step_sampled():
     assert_grad_close(ctx.get(L.T_DISC_DW), flat(out["dW_d"]), 1e-3, "dW_D")
     assert_grad_close(ctx.get(L.T_DISC_DB), flat(out["db_d"]), 1e-3, "db_D")
     # draw_s = sum over the sample's 1024 events of dy u^j softplus': it
-    # cancels heavily, so its tolerance is dy's 1e-3 carried through that
-    # linear map on magnitudes: 1e-3 sum |dy| |u^j| softplus'
+    # cancels heavily, so its tolerance is dy's (1e-3 with the R24 floor)
+    # carried through that linear map on magnitudes: sum tol(dy) |u^j| softplus'
     m = ocfg.events_per_sample
-    _, draw_mag = proxy.sampler_backward(np.abs(out["dy"]), out["u"], out["raw"], m)
-    tol_draw = 1e-3 * (np.abs(out["draw"]) + draw_mag).reshape(-1)
+    tol_dy = 1e-3 * np.maximum(np.abs(out["dy"]), 1e-2 * np.max(np.abs(out["dy"])))
+    _, draw_mag = proxy.sampler_backward(tol_dy, out["u"], out["raw"], m)
+    tol_draw = (1e-3 * np.abs(out["draw"]) + draw_mag).reshape(-1)
     assert np.all(np.abs(ctx.get(L.T_DRAW) - out["draw"].reshape(-1)) <= 10 * tol_draw), "draw (independent)"
     dyg, dyo = ctx.get(L.T_DY).reshape(-1, 2).astype(np.float64), out["dy"]
     assert np.linalg.norm(dyg - dyo) <= 1e-2 * np.linalg.norm(dyo), "dy (independent, relative L2)"
