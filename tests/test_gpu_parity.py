@@ -316,14 +316,19 @@ def test_full_size_paper_step_sampled():
     tol_dy = 1e-3 * np.maximum(np.abs(out["dy"]), 1e-2 * np.max(np.abs(out["dy"])))
     _, draw_mag = proxy.sampler_backward(tol_dy, out["u"], out["raw"], m)
     tol_draw = (1e-3 * np.abs(out["draw"]) + draw_mag).reshape(-1)
-    assert np.all(np.abs(ctx.get(L.T_DRAW) - out["draw"].reshape(-1)) <= 10 * tol_draw), "draw (independent)"
+    def check_draw(ref, scale, what):
+        err = np.abs(ctx.get(L.T_DRAW).astype(np.float64) - np.asarray(ref).reshape(-1))
+        ratio = err / (scale * tol_draw)
+        bad = np.flatnonzero(ratio > 1)
+        assert bad.size == 0, f"{what}: {bad.size} of {ratio.size} outside (worst {ratio.max():.3g} at {bad[:6]})"
+    check_draw(out["draw"], 10.0, "draw (independent)")
     dyg, dyo = ctx.get(L.T_DY).reshape(-1, 2).astype(np.float64), out["dy"]
     assert np.linalg.norm(dyg - dyo) <= 1e-2 * np.linalg.norm(dyo), "dy (independent, relative L2)"
     gpu_d = (unflat(ctx.get(L.T_DISC_W), st.dW), unflat(ctx.get(L.T_DISC_B), st.db))
     _, g_cache = mlp.forward(g0[0], g0[1], out["z"], ocfg.leaky_slope)
     og = gan.generator_step(ocfg, gpu_d[0], gpu_d[1], g0[0], g_cache, out["raw"], out["u"], out["y"])
     assert s.loss_g == pytest.approx(og["loss_g"], rel=1e-5)
-    assert np.all(np.abs(ctx.get(L.T_DRAW) - og["draw"].reshape(-1)) <= tol_draw), "draw (through the GPU's D)"
+    check_draw(og["draw"], 1.0, "draw (through the GPU's D)")
     assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], og["dy"][idx], 1e-3, "dy (through the GPU's D, sampled)")
 
 
