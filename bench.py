@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=["c2", "c1", "c5"], default="c2")
-    p.add_argument("--mode", choices=["rma", "rma-ag", "arar", "arar-arar", "sync", "none"], default="rma-ag",
+    p.add_argument("--mode", choices=["rma", "rma-ag", "rma-chunked", "arar", "arar-arar", "sync", "none"], default="rma-ag",
                    help="N > 1 exchange: rma-ag (default) = one-sided one-hop all-gather inside the inner group "
                         "over NVSwitch (no forwarding agent); rma = the paper's one-sided pass-along ring (Alg. 1)")
     p.add_argument("--group-size", type=int, default=0)
@@ -154,12 +154,15 @@ def lib_config(args, L, rank, world):
         cfg.gen_hidden = args.gen_hidden
         workload += f", generator hidden width {args.gen_hidden} (synthetic large packet)"
     cfg.world, cfg.rank = world, rank
-    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
+    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "rma-chunked": L.MODE_RMA_CHUNKED,
+             "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
              "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
     cfg.mode = modes[args.mode] if world > 1 else L.MODE_NONE
     cfg.group_size = args.group_size if (args.group_size and world > 1) else world
     cfg.outer_every = args.outer_every
     cfg.staleness = args.staleness if world > 1 else 0
+    if args.mode == "rma-chunked":
+        cfg.staleness = 0  # one common sum
     cfg.phase_timing = 1
     if getattr(args, "sampler", "quadratic") == "tabulated":
         cfg.sampler = L.SAMPLER_TABULATED
@@ -443,7 +446,7 @@ def ours_arm(args):
     if world > 1 and args.mode != "none":
         pkt = ctx.tensor_bytes(L.T_REDUCED)  # the packet as exchanged (weights; + biases when fused)
         g = cfg.group_size
-        bytes_in = (2 * (g - 1) / g if args.mode == "sync" else (g - 1)) * pkt
+        bytes_in = (2 * (g - 1) / g if args.mode in ("sync", "rma-chunked") else (g - 1)) * pkt
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ts = []
         for _ in range(20):

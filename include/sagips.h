@@ -63,9 +63,14 @@ typedef enum {
   SAGIPS_MODE_ARAR_ARAR = 2,      /* inner ring (two-sided) + outer ring every h */
   SAGIPS_MODE_RMA_ARAR_ARAR = 3,  /* inner ring one-sided (RMA) + outer ring */
   SAGIPS_MODE_SYNC_ALLREDUCE = 4, /* synchronous all-reduce sum (the Horovod role) */
-  SAGIPS_MODE_RMA_ALLGATHER = 5   /* as RMA_ARAR_ARAR, but the inner group exchanges by a one-hop
+  SAGIPS_MODE_RMA_ALLGATHER = 5,  /* as RMA_ARAR_ARAR, but the inner group exchanges by a one-hop
                                      all-gather over NVSwitch: every member stores its packet into
                                      every other member's window (no pass-along); same sums (§8(f) row 3) */
+  SAGIPS_MODE_RMA_CHUNKED = 6     /* as RMA_ARAR_ARAR with staleness 0 only: the inner group's sum as a
+                                     one-sided chunked reduce-scatter + all-gather (member q folds chunk
+                                     q of every packet in ascending origin order and stores the result
+                                     into every member's window): 2 (g-1)/g packets per rank instead
+                                     of g - 1, the same sums (the paper's future work) */
 } sagips_mode;
 
 typedef enum {
@@ -101,7 +106,7 @@ typedef struct {
                              g == world: ungrouped */
   int32_t outer_every;    /* h: leaders' ring fires when (step+1) % h == 0; 0 = never (R13) */
   int32_t mode;           /* sagips_mode */
-  int32_t staleness;      /* s in {0,1}: other members' packets from step t-s (R12) */
+  int32_t staleness;      /* s in {0,1}: other members' packets from step t-s (R12); 0 for RMA_CHUNKED */
   int32_t reduce_mean;    /* 1: divide the reduced packet by the number of contributors (R11) */
   int32_t precision;      /* sagips_precision for the discriminator GEMMs */
   /* model dimensions (R4, R5) */

@@ -30,6 +30,7 @@ MODE_ARAR_ARAR = 2
 MODE_RMA_ARAR_ARAR = 3
 MODE_SYNC_ALLREDUCE = 4
 MODE_RMA_ALLGATHER = 5  # §8(f) row 3: the inner group by a one-hop all-gather -- same sums as 2 / 3
+MODE_RMA_CHUNKED = 6    # §8(f) row 3: chunked reduce-scatter + all-gather (staleness 0) -- same sums as 2 / 3
 
 
 def group_layout(world, group_size):

@@ -14,7 +14,7 @@ OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "CUDA", 4: "NONFINITE", 5: "PROTOCOL",
           6: "STATE", 7: "TIMEOUT", 8: "UNSUPPORTED"}
 
-MODE_NONE, MODE_ARAR, MODE_ARAR_ARAR, MODE_RMA_ARAR_ARAR, MODE_SYNC_ALLREDUCE, MODE_RMA_ALLGATHER = range(6)
+MODE_NONE, MODE_ARAR, MODE_ARAR_ARAR, MODE_RMA_ARAR_ARAR, MODE_SYNC_ALLREDUCE, MODE_RMA_ALLGATHER, MODE_RMA_CHUNKED = range(7)
 SAMPLER_QUADRATIC, SAMPLER_TABULATED = 0, 1
 PREC_FP32, PREC_BF16 = 0, 1
 DISC_AUTO, DISC_SIMT, DISC_TCGEN05 = 0, 1, 2

@@ -37,6 +37,7 @@ enum { RING_INNER = 0 };
 
 struct DevFlags {
   unsigned long long tag[kMaxWorld][kVersions];
+  unsigned long long tag_ag[kMaxWorld][kVersions];  // RMA_CHUNKED: the reduced chunk of member q landed
 };
 
 struct ExchangeState {
@@ -151,11 +152,15 @@ constexpr int kPushCtas = 32;
 struct PushAllArgs {
   float* dst[kMaxWorld];
   unsigned long long* dst_flag[kMaxWorld];
+  int64_t off[kMaxWorld];  // source offset and length per destination (RMA_CHUNKED: chunk y; else 0, n)
+  int64_t len[kMaxWorld];
 };
-__global__ void __launch_bounds__(256) k_push(const float* __restrict__ packet, int64_t n, PushAllArgs a,
+__global__ void __launch_bounds__(256) k_push(const float* __restrict__ packet_base, int64_t n_unused, PushAllArgs a,
                                               unsigned long long tag, unsigned int* ticket) {
   const int y = blockIdx.y;
   float* dst = a.dst[y];
+  const float* packet = packet_base + a.off[y];
+  const int64_t n = a.len[y];
   const int64_t n4 = n / 4, per = (n4 + gridDim.x - 1) / gridDim.x;
   const int64_t b0 = blockIdx.x * per, b1 = min(n4, b0 + per);
   const float4* s4 = reinterpret_cast<const float4*>(packet);
@@ -245,6 +250,7 @@ struct FoldAdamArgs {
   int do_adam;
   GenAdam a;
   const unsigned int* err;
+  int64_t gather_chunk;  // RMA_CHUNKED: element i is already reduced, in pl.p[i / gather_chunk][i]; 0: fold
 };
 __global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldAdamArgs f) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -254,9 +260,13 @@ __global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldA
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float gi = 0.f;
     if (i < f.pw) {
-      float acc = __ldcg(f.pl.p[0] + i);
-      for (int j = 1; j < f.pl.count; ++j) acc += __ldcg(f.pl.p[j] + i);
-      gi = acc / f.divisor;
+      if (f.gather_chunk) {
+        gi = __ldcg(f.pl.p[i / f.gather_chunk] + i);
+      } else {
+        float acc = __ldcg(f.pl.p[0] + i);
+        for (int j = 1; j < f.pl.count; ++j) acc += __ldcg(f.pl.p[j] + i);
+        gi = acc / f.divisor;
+      }
       f.reduced[i] = gi;
     }
     if (!f.do_adam) continue;
@@ -273,6 +283,43 @@ __global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldA
       a.pb[j] = p;
       a.mb[j] = m;
       a.vb[j] = v;
+    }
+  }
+}
+
+// RMA_CHUNKED reduce-scatter step of member q: chunk q of every member's
+// packet, folded in ascending origin order (the same element-wise sum as
+// k_fold_adam's fold), divided, and stored into every member's window (the
+// all-gather); the last CTA releases the chunk's tag in the peers' windows.
+// Launched after k_wait (programmatic dependent launch).
+struct RsArgs {
+  PacketList pl;                      // the group's packets in ascending origin order
+  float* dst[kMaxWorld];              // the reduced chunk's destination in every member's window (own first)
+  unsigned long long* flag[kMaxWorld];// its tag in the peers' windows (dst[d], d >= 1)
+  int ndst;
+  int64_t off, len;                   // the chunk
+  float divisor;
+  unsigned long long tag;
+  unsigned int* ticket;
+  const unsigned int* err;
+};
+__global__ void __launch_bounds__(256) k_rs_fold(const __grid_constant__ RsArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (*reinterpret_cast<const volatile unsigned int*>(a.err) != 0u) return;  // the peers' waits time out (bounded)
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.len; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = a.off + k;
+    float acc = __ldcg(a.pl.p[0] + i);
+    for (int j = 1; j < a.pl.count; ++j) acc += __ldcg(a.pl.p[j] + i);
+    const float v = acc / a.divisor;
+    for (int d = 0; d < a.ndst; ++d) a.dst[d][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(a.ticket, 1u) == gridDim.x - 1) {
+      *a.ticket = 0;
+      __threadfence_system();
+      for (int d = 1; d < a.ndst; ++d) st_release_sys(a.flag[d], a.tag);
     }
   }
 }
@@ -312,7 +359,13 @@ static cudaError_t launch_fold_adam(const FoldAdamArgs& f, cudaStream_t st) {
   } while (0)
 
 static bool one_sided(const sagips_ctx* c) {
-  return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR || c->cfg.mode == SAGIPS_MODE_RMA_ALLGATHER;
+  return c->cfg.mode == SAGIPS_MODE_RMA_ARAR_ARAR || c->cfg.mode == SAGIPS_MODE_RMA_ALLGATHER ||
+         c->cfg.mode == SAGIPS_MODE_RMA_CHUNKED;
+}
+// RMA_CHUNKED: chunk q of the packet = [q cs, min(n, (q + 1) cs)), cs a multiple of 64 floats
+static int64_t chunk_floats(const sagips_ctx* c, int g) {
+  const int64_t n = (int64_t)slot_floats(c);
+  return ((n + g - 1) / g + 63) / 64 * 64;
 }
 // the leaders' outer ring through the windows (one-hop all-gather, cfg.outer_rma)
 static bool outer_one_sided(const sagips_ctx* c) { return one_sided(c) && c->cfg.outer_rma != 0; }
@@ -459,6 +512,8 @@ static sagips_status push_to(sagips_ctx* c, const float* src, const int* dst_ran
     char* db = x->peer_base[dst_ranks[j]];
     pa.dst[j] = slot_ptr(db, c, c->cfg.rank, version);
     pa.dst_flag[j] = &flags_ptr(db, c)->tag[c->cfg.rank][version % kVersions];
+    pa.off[j] = 0;
+    pa.len[j] = (int64_t)slot_floats(c);
   }
   k_push<<<dim3(kPushCtas, ndst), 256, 0, st>>>(src, (int64_t)slot_floats(c), pa, version + 1, x->ticket);
   count_launch();
@@ -476,6 +531,25 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
   if (one_sided(c)) {
     if (!x->peers_ok) { c->err = "sagips_connect_peers not called"; return SAGIPS_ERR_STATE; }
     int dst[kMaxWorld];
+    if (g.mode == SAGIPS_MODE_RMA_CHUNKED) {
+      // reduce-scatter: chunk q of the packet into member q's window (slot origin = me, version t)
+      const int64_t cs = chunk_floats(c, x->g), n = (int64_t)slot_floats(c);
+      PushAllArgs pa{};
+      int nd = 0;
+      for (int q = 0; q < x->g; ++q) {
+        if (q == x->pos) continue;
+        char* db = x->peer_base[x->first + q];
+        const int64_t off = std::min(n, q * cs), len = std::min(n, (q + 1) * cs) - off;
+        pa.dst[nd] = slot_ptr(db, c, g.rank, step) + off;
+        pa.dst_flag[nd] = &flags_ptr(db, c)->tag[g.rank][step % kVersions];
+        pa.off[nd] = off;
+        pa.len[nd] = len;
+        ++nd;
+      }
+      k_push<<<dim3(kPushCtas, nd), 256, 0, st>>>(c->g_dW, 0, pa, step + 1, x->ticket);
+      count_launch();
+      return SAGIPS_OK;
+    }
     if (g.mode == SAGIPS_MODE_RMA_ALLGATHER) {
       for (int j = 1; j < x->g; ++j) dst[j - 1] = x->first + (x->pos + j) % x->g;  // pos+1, pos+2, ...
       return push_to(c, c->g_dW, dst, x->g - 1, step, st);
@@ -592,7 +666,70 @@ static sagips_status pull_one_sided(sagips_ctx* c, uint64_t step, cudaStream_t s
   f.pw = (int64_t)pw;
   f.divisor = g.reduce_mean ? (float)x->g : 1.0f;
   f.err = x->err;
-  if (stale >= 0) {
+  if (g.mode == SAGIPS_MODE_RMA_CHUNKED && x->g > 1) {
+    // 1. the other members' chunk `pos` of version t in the own window
+    const int64_t cs = chunk_floats(c, x->g), n = (int64_t)pw;
+    const uint64_t vag = step + 2;  // the all-gather's slots: version t + 2 (free while staleness is 0)
+    WaitArgs w{};
+    w.count = x->g - 1;
+    for (int j = 1; j < x->g; ++j) {
+      const int o = x->first + (x->pos - j + x->g) % x->g;
+      w.flag[j - 1] = &flags_ptr(own, c)->tag[o][step % kVersions];
+      w.want[j - 1] = (unsigned long long)step + 1;
+    }
+    k_wait<<<1, 32, 0, st>>>(w, timeout_ns(c), err_words(x), reinterpret_cast<unsigned long long*>(&c->stats->wait_ns),
+                             &c->stats->outer_fired);
+    count_launch();
+    // 2. fold chunk `pos` (ascending origins) into every member's window
+    RsArgs ra{};
+    ra.pl.count = x->g;
+    for (int q = 0; q < x->g; ++q) {
+      const int o = x->first + q;
+      ra.pl.p[q] = (o == g.rank) ? c->g_dW : slot_ptr(own, c, o, step);
+    }
+    ra.ndst = 0;
+    ra.dst[ra.ndst++] = slot_ptr(own, c, g.rank, vag);
+    for (int q = 0; q < x->g; ++q) {
+      if (q == x->pos) continue;
+      char* db = x->peer_base[x->first + q];
+      ra.dst[ra.ndst] = slot_ptr(db, c, g.rank, vag);
+      ra.flag[ra.ndst] = &flags_ptr(db, c)->tag_ag[g.rank][vag % kVersions];
+      ++ra.ndst;
+    }
+    ra.off = std::min(n, x->pos * cs);
+    ra.len = std::min(n, (x->pos + 1) * cs) - ra.off;
+    ra.divisor = f.divisor;
+    ra.tag = (unsigned long long)step + 1;
+    ra.ticket = x->ticket + (kMaxWorld - 1);
+    ra.err = x->err;
+    {
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ra.len + 255) / 256, 148)));
+      lc.blockDim = dim3(256);
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      XCK(cudaLaunchKernelEx(&lc, k_rs_fold, ra));
+      count_launch();
+    }
+    // 3. the other members' reduced chunks
+    WaitArgs w2{};
+    w2.count = x->g - 1;
+    for (int j = 1; j < x->g; ++j) {
+      const int o = x->first + (x->pos - j + x->g) % x->g;
+      w2.flag[j - 1] = &flags_ptr(own, c)->tag_ag[o][vag % kVersions];
+      w2.want[j - 1] = (unsigned long long)step + 1;
+    }
+    k_wait<<<1, 32, 0, st>>>(w2, timeout_ns(c), err_words(x), nullptr, nullptr);
+    count_launch();
+    // 4. gather the chunks (+ Adam(G) below)
+    f.pl.count = x->g;
+    for (int q = 0; q < x->g; ++q) f.pl.p[q] = slot_ptr(own, c, x->first + q, vag);
+    f.gather_chunk = cs;
+  } else if (stale >= 0) {
     WaitArgs w{};
     w.count = x->g - 1;
     for (int j = 1; j < x->g; ++j) {

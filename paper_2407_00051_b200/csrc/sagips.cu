@@ -150,7 +150,9 @@ static sagips_status validate(const sagips_config* g, std::string* why) {
   if (g->rank < 0 || g->rank >= g->world) return bad("rank out of range");
   if (g->group_size < 1) return bad("group_size must be >= 1");
   if (g->outer_rma != 0 && g->outer_rma != 1) return bad("outer_rma must be 0 or 1");
-  if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_RMA_ALLGATHER) return bad("unknown mode");
+  if (g->mode < SAGIPS_MODE_NONE || g->mode > SAGIPS_MODE_RMA_CHUNKED) return bad("unknown mode");
+  if (g->mode == SAGIPS_MODE_RMA_CHUNKED && g->staleness != 0)
+    return bad("RMA_CHUNKED reduces one common sum: staleness must be 0");
   if (g->staleness < 0 || g->staleness > 1) return bad("staleness must be 0 or 1");
   if (g->precision != SAGIPS_PREC_FP32 && g->precision != SAGIPS_PREC_BF16) return bad("unknown precision");
   if (g->noise_dim < 1 || g->gen_hidden < 1 || g->gen_depth < 1 || g->disc_depth < 1) return bad("model dims");

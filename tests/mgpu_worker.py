@@ -22,7 +22,7 @@ from oracle import exchange as xc  # noqa: E402
 from oracle import gan  # noqa: E402
 from tests.gpu_util import flat, grad_close, oracle_config, sync_params  # noqa: E402
 
-MODES = {"none": 0, "arar": 1, "arar-arar": 2, "rma": 3, "sync": 4, "rma-ag": 5}
+MODES = {"none": 0, "arar": 1, "arar-arar": 2, "rma": 3, "sync": 4, "rma-ag": 5, "rma-chunked": 6}
 
 
 def main():
@@ -70,7 +70,7 @@ def main():
             print(f"rank {rank} step {t}: outer ring did not fire", flush=True)
             ok = False
     # replica invariant (mode ARAR / sync, s = 0): generator weights identical across ranks
-    if mode_name in ("arar", "sync", "rma", "rma-ag", "arar-arar") and stale == 0 and group == world and not outer:
+    if mode_name in ("arar", "sync", "rma", "rma-ag", "rma-chunked", "arar-arar") and stale == 0 and group == world and not outer:
         w = torch.tensor(ctx.get(L.T_GEN_W), device="cuda")
         w0 = w.clone()
         dist.broadcast(w0, 0)

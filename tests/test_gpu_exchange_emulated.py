@@ -40,7 +40,7 @@ from tests.gpu_util import flat, lib, oracle_config, sync_params, unflat
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-MODES = {"rma": 3, "rma-ag": 5}
+MODES = {"rma": 3, "rma-ag": 5, "rma-chunked": 6}
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -151,6 +151,19 @@ def run_emulated(mode, W, g, s, steps=6, outer=0, fused=0):
 @pytest.mark.parametrize("s", [0, 1])
 def test_emulated_exchange(mode, W, g, s):
     run_emulated(mode, W, g, s)
+
+
+@pytest.mark.parametrize("W,g,outer", [(2, 2, 0), (4, 4, 0), (8, 8, 0), (8, 4, 0), (8, 2, 3), (6, 4, 2), (4, 4, 0)])
+def test_emulated_chunked_ring(W, g, outer):
+    """The chunked reduce-scatter + all-gather (SAGIPS_MODE_RMA_CHUNKED, the
+    paper's future work P:180; staleness 0): member q folds chunk q of every
+    packet in ascending origin order, so the reduced packets are bit-identical
+    to the pass-along ring's (the oracle's reduce_step)."""
+    run_emulated("rma-chunked", W, g, 0, outer=outer)
+
+
+def test_emulated_chunked_fused_bias_packet():
+    run_emulated("rma-chunked", 4, 4, 0, fused=1)
 
 
 @pytest.mark.parametrize("mode", ["rma", "rma-ag"])

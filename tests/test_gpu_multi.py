@@ -28,7 +28,7 @@ def _run(nproc, *args, timeout=600):
 
 @pytest.mark.parametrize("mode,group,stale,outer", [
     ("rma", 2, 0, 0), ("rma", 2, 1, 0), ("arar", 2, 0, 0), ("arar", 2, 1, 0), ("sync", 2, 0, 0), ("none", 2, 0, 0),
-    ("rma-ag", 2, 1, 0)])
+    ("rma-ag", 2, 1, 0), ("rma-chunked", 2, 0, 0)])
 def test_two_gpu_exchange(mode, group, stale, outer):
     if _ngpus() < 2:
         pytest.skip("needs 2 GPUs")
@@ -37,7 +37,7 @@ def test_two_gpu_exchange(mode, group, stale, outer):
 
 @pytest.mark.parametrize("mode,group,stale,outer", [
     ("rma", 4, 0, 0), ("rma", 2, 0, 2), ("arar-arar", 2, 1, 3), ("rma", 4, 1, 0), ("rma-ag", 4, 0, 0),
-    ("rma-ag", 4, 1, 0), ("rma-ag", 2, 1, 2)])
+    ("rma-ag", 4, 1, 0), ("rma-ag", 2, 1, 2), ("rma-chunked", 4, 0, 0), ("rma-chunked", 2, 0, 2)])
 def test_four_gpu_grouping(mode, group, stale, outer):
     if _ngpus() < 4:
         pytest.skip("needs 4 GPUs")
