@@ -448,7 +448,8 @@ def ours_arm(args):
         g = cfg.group_size
         bytes_in = (2 * (g - 1) / g if args.mode in ("sync", "rma-chunked") else (g - 1)) * pkt
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ts = []
+        p_ev = torch.cuda.Event(enable_timing=True)
+        ts, tp = [], []
         for _ in range(20):
             ctx.train_step(step, L.STEP_LOCAL_ONLY, sp)
             torch.cuda.synchronize()
@@ -456,12 +457,15 @@ def ours_arm(args):
             torch.cuda._sleep(200_000)  # ~0.1 ms of device work so the host's launches run ahead, as in a step
             a_ev.record(stream)
             ctx.push_generator_grad(step, sp)
+            p_ev.record(stream)
             ctx.pull_generator_grad(step, sp)
             b_ev.record(stream)
             torch.cuda.synchronize()
             ts.append(a_ev.elapsed_time(b_ev))
+            tp.append(a_ev.elapsed_time(p_ev))
             step += 1
         med = sorted(ts)[len(ts) // 2]
+        med_push = sorted(tp)[len(tp) // 2]
         t = torch.tensor([med, -med], device="cuda")
         if dist is not None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -472,7 +476,11 @@ def ours_arm(args):
                "us_max_over_ranks": t_max * 1e3, "achieved": bytes_in / (t_min * 1e-3) / 1e9,
                "peak": nv, "unit": "GB/s", "frac": bytes_in / (t_min * 1e-3) / 1e9 / nv,
                "peak_src": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
-               "what": "push + pull (wait, forward, fold) + Adam(G) after a barrier, median of 20 per rank"}
+               "what": "push + pull (wait, forward, fold) + Adam(G) after a barrier, median of 20 per rank",
+               "push_us": med_push * 1e3,
+               "push_GBps": (bytes_in if args.mode != "rma" else pkt) / (med_push * 1e-3) / 1e9 if args.mode != "sync" else None,
+               "push_note": "the one-sided store kernel alone (this rank's outgoing bytes: one packet per peer for "
+                            "rma-ag, one to the successor for rma, (g-1)/g of a packet for rma-chunked) / its time"}
 
     if rank != 0:
         runtime.close(ctx)

@@ -149,6 +149,11 @@ __device__ void block_copy(float* __restrict__ dst, const float* __restrict__ sr
 // every CTA fences its stores before taking a ticket, the last fences again
 // before the release store.
 constexpr int kPushCtas = 32;
+// CTAs per destination: 32 for the paper's 200 KB packet (latency-bound),
+// more for large packets so that enough stores are in flight to fill NVLink
+static int push_ctas(int64_t n_floats) {
+  return (int)std::max<int64_t>(kPushCtas, std::min<int64_t>(n_floats / 16384, 4 * 148));
+}
 struct PushAllArgs {
   float* dst[kMaxWorld];
   unsigned long long* dst_flag[kMaxWorld];
@@ -515,7 +520,8 @@ static sagips_status push_to(sagips_ctx* c, const float* src, const int* dst_ran
     pa.off[j] = 0;
     pa.len[j] = (int64_t)slot_floats(c);
   }
-  k_push<<<dim3(kPushCtas, ndst), 256, 0, st>>>(src, (int64_t)slot_floats(c), pa, version + 1, x->ticket);
+  k_push<<<dim3(push_ctas((int64_t)slot_floats(c)), ndst), 256, 0, st>>>(src, (int64_t)slot_floats(c), pa, version + 1,
+                                                                       x->ticket);
   count_launch();
   return SAGIPS_OK;
 }
@@ -546,7 +552,7 @@ sagips_status exchange_push(sagips_ctx* c, uint64_t step, cudaStream_t st) {
         pa.len[nd] = len;
         ++nd;
       }
-      k_push<<<dim3(kPushCtas, nd), 256, 0, st>>>(c->g_dW, 0, pa, step + 1, x->ticket);
+      k_push<<<dim3(push_ctas(cs), nd), 256, 0, st>>>(c->g_dW, 0, pa, step + 1, x->ticket);
       count_launch();
       return SAGIPS_OK;
     }
