@@ -478,7 +478,8 @@ def ours_arm(args):
                "peak_src": "B200_PROFILING.md measured peer copy per direction (900 nominal)",
                "what": "push + pull (wait, forward, fold) + Adam(G) after a barrier, median of 20 per rank",
                "push_us": med_push * 1e3,
-               "push_GBps": (bytes_in if args.mode != "rma" else pkt) / (med_push * 1e-3) / 1e9 if args.mode != "sync" else None,
+               "push_GBps": ({"rma-ag": (g - 1) * pkt, "rma": pkt, "rma-chunked": (g - 1) / g * pkt}.get(args.mode, 0)
+                             / (med_push * 1e-3) / 1e9) if args.mode in ("rma-ag", "rma", "rma-chunked") else None,
                "push_note": "the one-sided store kernel alone (this rank's outgoing bytes: one packet per peer for "
                             "rma-ag, one to the successor for rma, (g-1)/g of a packet for rma-chunked) / its time"}
 
