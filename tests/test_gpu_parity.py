@@ -333,7 +333,11 @@ def test_full_size_paper_step_sampled():
     og = gan.generator_step(ocfg, gpu_d[0], gpu_d[1], g0[0], g_cache, out["raw"], out["u"], out["y"])
     assert s.loss_g == pytest.approx(og["loss_g"], rel=1e-5)
     check_draw(og["draw"], 1.0, "draw (through the GPU's D)")
-    assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], og["dy"][idx], 1e-3, "dy (through the GPU's D, sampled)")
+    # R27 at full size: no kink band is computed over 2^20 rows x 512
+    # LeakyReLU decisions, so up to 0.25% of the sampled elements may carry a
+    # flipped decision (observed on B200: 3 of 4,096 rows), each within max|ref|
+    assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], og["dy"][idx], 1e-3, "dy (through the GPU's D, sampled)",
+                      outliers=idx.size * 2 // 400)
 
 
 def test_step_is_deterministic():
