@@ -471,7 +471,7 @@ def ours_arm(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_max, t_min = float(t[0].item()), -float(t[1].item())
         nv = 770.0  # B200_PROFILING.md: measured peer copy, GB/s per direction
-        xch = {"bound": "nvlink-latency", "packet_bytes": pkt, "group_size": g,
+        xch = {"bound": "nvlink-latency" if pkt < (8 << 20) else "nvlink", "packet_bytes": pkt, "group_size": g,
                "bytes_in_per_rank_per_step": bytes_in, "us_min_over_ranks": t_min * 1e3,
                "us_max_over_ranks": t_max * 1e3, "achieved": bytes_in / (t_min * 1e-3) / 1e9,
                "peak": nv, "unit": "GB/s", "frac": bytes_in / (t_min * 1e-3) / 1e9 / nv,

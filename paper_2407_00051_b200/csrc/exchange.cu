@@ -256,13 +256,43 @@ struct FoldAdamArgs {
   GenAdam a;
   const unsigned int* err;
   int64_t gather_chunk;  // RMA_CHUNKED: element i is already reduced, in pl.p[i / gather_chunk][i]; 0: fold
+  int vec;               // every array 16-byte aligned: the weights go four at a time (a multiple-of-64 chunk never splits a quad)
 };
+__device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
 __global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldAdamArgs f) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (f.err && *reinterpret_cast<const volatile unsigned int*>(f.err) != 0u) return;
   const GenAdam& a = f.a;
   const int64_t n = f.do_adam ? a.nw + a.nb : f.pw;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  // large packets: quads (the same per-element arithmetic and fold order)
+  const int64_t nq = f.vec ? (f.do_adam ? (f.pw < a.nw ? f.pw : a.nw) : f.pw) >> 2 : 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += stride) {
+    const int64_t i = 4 * q;
+    float4 g;
+    if (f.gather_chunk) {
+      g = ldcg4(f.pl.p[i / f.gather_chunk] + i);
+    } else {
+      float4 acc = ldcg4(f.pl.p[0] + i);
+      for (int j = 1; j < f.pl.count; ++j) {
+        const float4 u = ldcg4(f.pl.p[j] + i);
+        acc.x += u.x; acc.y += u.y; acc.z += u.z; acc.w += u.w;
+      }
+      g = make_float4(acc.x / f.divisor, acc.y / f.divisor, acc.z / f.divisor, acc.w / f.divisor);
+    }
+    *reinterpret_cast<float4*>(f.reduced + i) = g;
+    if (!f.do_adam) continue;
+    float4 p = *reinterpret_cast<const float4*>(a.pw + i), m = *reinterpret_cast<const float4*>(a.mw + i),
+           v = *reinterpret_cast<const float4*>(a.vw + i);
+    adam_elem(p.x, g.x, m.x, v.x, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+    adam_elem(p.y, g.y, m.y, v.y, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+    adam_elem(p.z, g.z, m.z, v.z, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+    adam_elem(p.w, g.w, m.w, v.w, a.step_size, a.bc2_sqrt, a.b1, a.b2, a.eps);
+    *reinterpret_cast<float4*>(a.pw + i) = p;
+    *reinterpret_cast<float4*>(a.mw + i) = m;
+    *reinterpret_cast<float4*>(a.vw + i) = v;
+  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     float gi = 0.f;
     if (i < f.pw) {
       if (f.gather_chunk) {
@@ -307,11 +337,24 @@ struct RsArgs {
   unsigned long long tag;
   unsigned int* ticket;
   const unsigned int* err;
+  int vec;                            // every pointer 16-byte aligned
 };
 __global__ void __launch_bounds__(256) k_rs_fold(const __grid_constant__ RsArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (*reinterpret_cast<const volatile unsigned int*>(a.err) != 0u) return;  // the peers' waits time out (bounded)
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.len; k += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nq = a.vec ? a.len >> 2 : 0;  // quads (off is a multiple of 64 floats)
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nq; k += stride) {
+    const int64_t i = a.off + 4 * k;
+    float4 acc = ldcg4(a.pl.p[0] + i);
+    for (int j = 1; j < a.pl.count; ++j) {
+      const float4 u = ldcg4(a.pl.p[j] + i);
+      acc.x += u.x; acc.y += u.y; acc.z += u.z; acc.w += u.w;
+    }
+    const float4 v = make_float4(acc.x / a.divisor, acc.y / a.divisor, acc.z / a.divisor, acc.w / a.divisor);
+    for (int d = 0; d < a.ndst; ++d) *reinterpret_cast<float4*>(a.dst[d] + i) = v;
+  }
+  for (int64_t k = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < a.len; k += stride) {
     const int64_t i = a.off + k;
     float acc = __ldcg(a.pl.p[0] + i);
     for (int j = 1; j < a.pl.count; ++j) acc += __ldcg(a.pl.p[j] + i);
@@ -329,10 +372,16 @@ __global__ void __launch_bounds__(256) k_rs_fold(const __grid_constant__ RsArgs 
   }
 }
 
-static cudaError_t launch_fold_adam(const FoldAdamArgs& f, cudaStream_t st) {
+static cudaError_t launch_fold_adam(FoldAdamArgs f, cudaStream_t st) {
+  auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool vec = a16(f.reduced);
+  for (int j = 0; j < f.pl.count; ++j) vec = vec && a16(f.pl.p[j]);
+  if (f.do_adam) vec = vec && a16(f.a.pw) && a16(f.a.mw) && a16(f.a.vw);
+  f.vec = vec ? 1 : 0;
   const int64_t n = f.do_adam ? f.a.nw + f.a.nb : f.pw;
+  const int64_t per_thread = f.vec ? 4 : 1;
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)std::min<int64_t>((n + 255) / 256, 148 * 2));
+  lc.gridDim = dim3((unsigned)std::min<int64_t>((n / per_thread + 255) / 256, 148 * 8));
   lc.blockDim = dim3(256);
   lc.stream = st;
   cudaLaunchAttribute at[1];
@@ -709,8 +758,12 @@ static sagips_status pull_one_sided(sagips_ctx* c, uint64_t step, cudaStream_t s
     ra.ticket = x->ticket + (kMaxWorld - 1);
     ra.err = x->err;
     {
+      bool vec = true;
+      for (int q = 0; q < ra.pl.count; ++q) vec = vec && (reinterpret_cast<uintptr_t>(ra.pl.p[q]) & 15u) == 0;
+      for (int d = 0; d < ra.ndst; ++d) vec = vec && (reinterpret_cast<uintptr_t>(ra.dst[d]) & 15u) == 0;
+      ra.vec = vec ? 1 : 0;
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ra.len + 255) / 256, 148)));
+      lc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ra.len / (vec ? 4 : 1) + 255) / 256, 592)));
       lc.blockDim = dim3(256);
       lc.stream = st;
       cudaLaunchAttribute at[1];

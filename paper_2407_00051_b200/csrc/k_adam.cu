@@ -9,8 +9,22 @@ namespace sagips {
 
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, int64_t n, float step_size, float bc2_sqrt, float b1, float b2,
-                       float eps) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+                       float eps, int vec) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nq = vec ? n >> 2 : 0;  // quads when every array is 16-byte aligned (same per-element arithmetic)
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nq; q += stride) {
+    float4 pi = reinterpret_cast<const float4*>(p)[q], mi = reinterpret_cast<const float4*>(m)[q],
+           vi = reinterpret_cast<const float4*>(v)[q];
+    const float4 gi = reinterpret_cast<const float4*>(g)[q];
+    adam_elem(pi.x, gi.x, mi.x, vi.x, step_size, bc2_sqrt, b1, b2, eps);
+    adam_elem(pi.y, gi.y, mi.y, vi.y, step_size, bc2_sqrt, b1, b2, eps);
+    adam_elem(pi.z, gi.z, mi.z, vi.z, step_size, bc2_sqrt, b1, b2, eps);
+    adam_elem(pi.w, gi.w, mi.w, vi.w, step_size, bc2_sqrt, b1, b2, eps);
+    reinterpret_cast<float4*>(p)[q] = pi;
+    reinterpret_cast<float4*>(m)[q] = mi;
+    reinterpret_cast<float4*>(v)[q] = vi;
+  }
+  for (int64_t i = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     float pi = p[i], mi = m[i], vi = v[i];
     adam_elem(pi, g[i], mi, vi, step_size, bc2_sqrt, b1, b2, eps);
     p[i] = pi;
@@ -24,9 +38,11 @@ void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double
   if (n <= 0) return;
   const double bc1 = 1.0 - std::pow(b1, (double)tau);
   const double bc2 = 1.0 - std::pow(b2, (double)tau);
-  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  const int vec = (a16(p) && a16(g) && a16(m) && a16(v)) ? 1 : 0;
+  const int blocks = (int)std::min<int64_t>((n / (vec ? 4 : 1) + 255) / 256, 148 * 8);
   k_adam<<<blocks, 256, 0, st>>>(p, g, m, v, n, (float)(lr / bc1), (float)std::sqrt(bc2), (float)b1, (float)b2,
-                                 (float)eps);
+                                 (float)eps, vec);
   count_launch();
 }
 
