@@ -307,13 +307,13 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     # measured DRAM bytes per launch of this kernel class from the committed
     # ncu --set full capture of the same workload (tests/tools/ncu_traffic.py)
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")) as f:
             tr = json.load(f)
         c = tr["classes"].get(dom)
         if c and tr.get("rows_d") == rows_d and tr.get("split") == split:
             roof["traffic"] = c["traffic_bytes"]
             roof["traffic_algorithmic"] = spec[dom][0] * spec[dom][1]
-            roof["traffic_src"] = "profiles/r01_ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, B/launch)"
+            roof["traffic_src"] = "profiles/r02_ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum, B/launch)"
     except (OSError, ValueError, KeyError):
         pass
     # whole discriminator MLP (a7 + a8) on the tensor cores

@@ -1,12 +1,13 @@
-"""Per-launch DRAM traffic of the tcgen05 layer passes from the `ncu --set
-full` captures of tests/tools/gpurun_profile.sh, keyed by the kernel classes
-of sagips_kernel_times, for bench.py's roofline "traffic" field.
+"""Per-launch DRAM traffic of the discriminator kernels from an `ncu --set
+full` capture, keyed by the kernel classes of sagips_kernel_times, for
+bench.py's roofline "traffic" field.
 
-The captures take 3 consecutive launches from step 3 of the bench's D step:
-tc_bwd = d_bwd_last, d_bwd_mid, d_bwd_first; tc_fwd = d_fwd_first,
-d_fwd_mid, d_fwd_head.
+Round 2 (fused kernels), one capture of the first step's five tcgen05
+launches (`ncu --set full -k regex:"k_dfwd|k_gstep|k_bwd" -c 5`):
+d_fwd_fused, d_bwd_last, d_bwd_mid, d_bwd_first, g_fused.
 
-usage: ncu_traffic.py OUT.json tc_fwd.ncu-rep tc_bwd.ncu-rep"""
+usage: ncu_traffic.py OUT.json step.ncu-rep
+       ncu_traffic.py OUT.json tc_fwd.ncu-rep tc_bwd.ncu-rep   (round 1's per-layer passes)"""
 import csv
 import json
 import subprocess
@@ -23,22 +24,27 @@ def launches(rep):
     res = []
     for r in rows[2:]:
         d = {}
-        for k in ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"):
+        for k in ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                  "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"):
             i = hdr.index(k)
             d[k] = float(r[i].replace(",", "")) * SCALE.get(units[i], 1.0)
         res.append((r[hdr.index("Kernel Name")], d))
     return res
 
 
-def main(out, fwd, bwd):
-    classes = {fwd: ["d_fwd_first", "d_fwd_mid", "d_fwd_head"], bwd: ["d_bwd_last", "d_bwd_mid", "d_bwd_first"]}
+def main(out, fwd, bwd=None):
+    if bwd is None:
+        classes = {fwd: ["d_fwd_fused", "d_bwd_last", "d_bwd_mid", "d_bwd_first", "g_fused"]}
+    else:
+        classes = {fwd: ["d_fwd_first", "d_fwd_mid", "d_fwd_head"], bwd: ["d_bwd_last", "d_bwd_mid", "d_bwd_first"]}
     res = {}
     for rep, names in classes.items():
         for name, (kern, d) in zip(names, launches(rep)):
             res[name] = {"kernel": kern, "duration_s": d["gpu__time_duration.sum"],
                          "dram_read_bytes": d["dram__bytes_read.sum"], "dram_write_bytes": d["dram__bytes_write.sum"],
-                         "traffic_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"]}
-    doc = {"source": "ncu --set full --clock-control none (tests/tools/gpurun_profile.sh), one launch per class; "
+                         "traffic_bytes": d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"],
+                         "tensor_pipe_active_pct": d["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"]}
+    doc = {"source": "ncu --set full --clock-control none, one launch per class; "
                      "per-launch DRAM bytes; durations are cold-cache and serialised",
            "workload": "C2 (bench.py default), fp32-class split precision", "rows_d": 2 ** 21, "split": True,
            "classes": res}
@@ -50,4 +56,4 @@ def main(out, fwd, bwd):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:])
