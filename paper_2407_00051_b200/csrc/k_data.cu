@@ -197,6 +197,9 @@ __device__ __forceinline__ void bins2(uint64_t y, uint64_t LO, uint64_t SC, floa
 // instructions).  Used when 512 (bins+2) bytes fit (bins <= 126); otherwise
 // one [4][bins+2] copy per block.
 constexpr int kSampleThreads = 512;
+// resident blocks per SM (3 blocks at 40 registers for the variants that do
+// not spill then measured no faster at 2^24: 34.4 vs 32.8 us)
+__host__ __device__ constexpr int sample_blocks_per_sm(bool, bool, bool) { return 2; }
 __host__ __device__ constexpr bool hist_columns(int bins) { return bins + 2 <= 128; }
 
 // One thread = one group of 4 consecutive events e = 4g..4g+3:
@@ -210,7 +213,7 @@ __host__ __device__ constexpr bool hist_columns(int bins) { return bins + 2 <= 1
 // with integer atomics (exact, order-independent).
 // kFake = false: the real rows only (the tabulated sampler, R32, draws the fake rows)
 template <bool kReal, bool kHist, bool kFake = true>
-__global__ void __launch_bounds__(kSampleThreads, 2)
+__global__ void __launch_bounds__(kSampleThreads, sample_blocks_per_sm(kReal, kHist, kFake))
     k_sample(const float* __restrict__ c, int m, int64_t n_events, const float2* __restrict__ shard,
              uint32_t n_shard, PhiloxKey key, uint32_t step, uint32_t rank, uint32_t fake_stream,
              float2* __restrict__ x_real, float2* __restrict__ y_fake, uint32_t* __restrict__ real_idx,
@@ -236,7 +239,12 @@ __global__ void __launch_bounds__(kSampleThreads, 2)
   const uint32_t ngroups = (n + 3) / 4;
   const bool m4 = (m & 3) == 0 && vec_ok;
   const PhiloxRoundKeys rk = round_keys(key);
-  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+  // sample of the group's first event, s = 4g / m, and its offset r in the
+  // sample: two divisions per thread, then advanced by the grid stride
+  const uint32_t g0 = blockIdx.x * blockDim.x + threadIdx.x, gstride = gridDim.x * blockDim.x;
+  const uint32_t um = (uint32_t)m, ds = 4 * gstride / um, dr = 4 * gstride - ds * um;
+  uint32_t s = 4 * g0 / um, r0 = 4 * g0 - s * um;
+  for (uint32_t g = g0; g < ngroups; g += gstride, s += ds, r0 += dr, (r0 >= um ? (r0 -= um, ++s) : 0u)) {
     uint4 wa = make_uint4(0, 0, 0, 0), wb = make_uint4(0, 0, 0, 0);
     if (kFake) {
       wa = philox4x32_10(make_uint4(2 * g, step, rank, fake_stream), rk);
@@ -245,8 +253,6 @@ __global__ void __launch_bounds__(kSampleThreads, 2)
     const uint32_t wf[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
     uint4 wr = make_uint4(0, 0, 0, 0);
     if (kReal) wr = philox4x32_10(make_uint4(g, step, rank, kStreamReal), rk);
-    // sample of the group's first event: one division per group
-    const uint32_t s = 4 * g / (uint32_t)m;
     const float* cs = c + 6 * (size_t)s;
     uint64_t C0 = 0, C1 = 0, C2 = 0;
     auto load_c = [&]() {
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(kSampleThreads, 2)
       }
     } else {
       // general group: step across sample boundaries, stop at n
-      uint32_t r = 4 * g - s * (uint32_t)m;
+      uint32_t r = r0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t e = 4 * g + q;
@@ -355,10 +361,10 @@ static int sm_count() {
   }
   return g_sm_count;
 }
-static void sample_shape(int64_t n, int bins, bool hist, int* blocks, size_t* smem) {
+static void sample_shape(int64_t n, int bins, bool hist, int bps, int* blocks, size_t* smem) {
   const int64_t ngroups = (n + 3) / 4;
   const int64_t want = (ngroups + kSampleThreads - 1) / kSampleThreads;
-  *blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, 2 * (int64_t)sm_count()));
+  *blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, bps * (int64_t)sm_count()));
   *smem = hist ? sizeof(uint32_t) * 4 * (bins + 2) * (hist_columns(bins) ? 32 : 1) : 0;
 }
 
@@ -381,7 +387,7 @@ void launch_sample_step(const float* c, int k, int m, const float* shard, int64_
   if (hist && !hist_zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 4 * (bins + 2), st);
   int blocks;
   size_t smem;
-  sample_shape(n, bins, hist != nullptr, &blocks, &smem);
+  sample_shape(n, bins, hist != nullptr, sample_blocks_per_sm(true, hist != nullptr, fake), &blocks, &smem);
   float2* x = reinterpret_cast<float2*>(x_events);
   const int vec_ok = (n % 2 == 0) && (reinterpret_cast<uintptr_t>(x_events) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(real_idx) % 16 == 0);
@@ -409,7 +415,7 @@ void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t 
   }
   int blocks;
   size_t smem;
-  sample_shape(n, bins, hist != nullptr, &blocks, &smem);
+  sample_shape(n, bins, hist != nullptr, sample_blocks_per_sm(false, hist != nullptr, true), &blocks, &smem);
   const int vec_ok = reinterpret_cast<uintptr_t>(events) % 16 == 0;
   auto kern = hist ? k_sample<false, true> : k_sample<false, false>;
   if (hist) set_smem_attr<false, true, true>(smem);
