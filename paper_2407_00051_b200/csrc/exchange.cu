@@ -141,18 +141,18 @@ __device__ void block_copy(float* __restrict__ dst, const float* __restrict__ sr
 // push: the own packet -> destination y's slot (origin = me), then release
 // its tag.  y = blockIdx.y: the successor (pass-along ring) or every other
 // member (one-hop all-gather, SAGIPS_MODE_RMA_ALLGATHER: over NVSwitch every
-// member is one hop away, so there is no forwarding agent).  kPushCtas CTAs
-// per destination each store one contiguous chunk (measured, torch.profiler
+// member is one hop away, so there is no forwarding agent).  push_ctas CTAs
+// per destination each store one contiguous chunk (round 1, torch.profiler
 // at N = 2: 14.7 us with one CTA, ~10 us with 8-148 CTAs -- a ~9 us floor
 // that remains without the fences, so not the store bandwidth).
 // The last CTA to finish (ticket counter, reset by it) publishes the tag:
 // every CTA fences its stores before taking a ticket, the last fences again
 // before the release store.
-constexpr int kPushCtas = 32;
-// CTAs per destination: 32 for the paper's 200 KB packet (latency-bound),
-// more for large packets so that enough stores are in flight to fill NVLink
+// CTAs per destination: at least 32 (the paper's 200 KB packet: 13 CTAs of
+// one unrolled round each measured 15.4 vs 13.3 us), up to 4 x 148 for large
+// packets, each thread moving 4 float4 per round trip
 static int push_ctas(int64_t n_floats) {
-  return (int)std::max<int64_t>(kPushCtas, std::min<int64_t>(n_floats / 16384, 4 * 148));
+  return (int)std::max<int64_t>(32, std::min<int64_t>((n_floats / 4 + 1023) / 1024, 4 * 148));
 }
 struct PushAllArgs {
   float* dst[kMaxWorld];
@@ -170,7 +170,16 @@ __global__ void __launch_bounds__(256) k_push(const float* __restrict__ packet_b
   const int64_t b0 = blockIdx.x * per, b1 = min(n4, b0 + per);
   const float4* s4 = reinterpret_cast<const float4*>(packet);
   float4* d4 = reinterpret_cast<float4*>(dst);
-  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) d4[i] = s4[i];
+  // four independent loads in flight per thread before their remote stores
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += 4 * blockDim.x) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < b1) v[u] = s4[i + u * blockDim.x];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i + u * blockDim.x < b1) d4[i + u * blockDim.x] = v[u];
+  }
   if (blockIdx.x == gridDim.x - 1)
     for (int64_t i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = packet[i];
   __syncthreads();
@@ -377,9 +386,11 @@ static cudaError_t launch_fold_adam(FoldAdamArgs f, cudaStream_t st) {
   bool vec = a16(f.reduced);
   for (int j = 0; j < f.pl.count; ++j) vec = vec && a16(f.pl.p[j]);
   if (f.do_adam) vec = vec && a16(f.a.pw) && a16(f.a.mw) && a16(f.a.vw);
-  f.vec = vec ? 1 : 0;
   const int64_t n = f.do_adam ? f.a.nw + f.a.nb : f.pw;
-  const int64_t per_thread = f.vec ? 4 : 1;
+  // quads for large packets only: at the paper's 50 K parameters one element
+  // per thread over more CTAs has the shorter critical path (latency-bound)
+  f.vec = (vec && n >= (int64_t(1) << 20)) ? 1 : 0;
+  const int64_t per_thread = f.vec ? 4 : 1;  // f.vec set above
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)std::min<int64_t>((n / per_thread + 255) / 256, 148 * 8));
   lc.blockDim = dim3(256);
@@ -761,9 +772,9 @@ static sagips_status pull_one_sided(sagips_ctx* c, uint64_t step, cudaStream_t s
       bool vec = true;
       for (int q = 0; q < ra.pl.count; ++q) vec = vec && (reinterpret_cast<uintptr_t>(ra.pl.p[q]) & 15u) == 0;
       for (int d = 0; d < ra.ndst; ++d) vec = vec && (reinterpret_cast<uintptr_t>(ra.dst[d]) & 15u) == 0;
-      ra.vec = vec ? 1 : 0;
+      ra.vec = (vec && ra.len >= (int64_t(1) << 18)) ? 1 : 0;
       cudaLaunchConfig_t lc = {};
-      lc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ra.len / (vec ? 4 : 1) + 255) / 256, 592)));
+      lc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((ra.len / (ra.vec ? 4 : 1) + 255) / 256, 592)));
       lc.blockDim = dim3(256);
       lc.stream = st;
       cudaLaunchAttribute at[1];

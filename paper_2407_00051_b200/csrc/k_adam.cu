@@ -39,7 +39,7 @@ void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double
   const double bc1 = 1.0 - std::pow(b1, (double)tau);
   const double bc2 = 1.0 - std::pow(b2, (double)tau);
   auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
-  const int vec = (a16(p) && a16(g) && a16(m) && a16(v)) ? 1 : 0;
+  const int vec = (a16(p) && a16(g) && a16(m) && a16(v) && n >= (int64_t(1) << 20)) ? 1 : 0;  // large only
   const int blocks = (int)std::min<int64_t>((n / (vec ? 4 : 1) + 255) / 256, 148 * 8);
   k_adam<<<blocks, 256, 0, st>>>(p, g, m, v, n, (float)(lr / bc1), (float)std::sqrt(bc2), (float)b1, (float)b2,
                                  (float)eps, vec);
