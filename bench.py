@@ -406,22 +406,27 @@ def ours_arm(args):
     # e2e: the user-level loop through the public API with HOST inputs:
     # every step sagips_train_step_host copies the step's generator noise
     # and real batch from pinned host memory (a data loader's buffers) and
-    # the stats record back; the host waits for it before the next step
+    # the stats record back; the loop issues step t+1 and then waits for
+    # step t's stats (one step in flight: t+1's copy overlaps t's compute)
     e2e = None
     if not args.no_e2e:
         steps_e2e = max(3, args.steps // 2)
         k_, d_ = cfg.param_samples, cfg.noise_dim
         noise_h = torch.randn(k_, d_).pin_memory()
         real_h = torch.from_numpy(ctx.get(L.T_EVENTS).reshape(-1, 2)[:N].copy()).pin_memory()  # real rows
-        stats_h = torch.empty(ctypes.sizeof(L.StepStats), dtype=torch.uint8).pin_memory()
+        stats_h = [torch.empty(ctypes.sizeof(L.StepStats), dtype=torch.uint8).pin_memory() for _ in range(2)]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
         cur = torch.cuda.current_stream()
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(steps_e2e):
-            ctx.train_step_host(step, 0, noise_h.data_ptr(), real_h.data_ptr(), stats_h.data_ptr(), sp)
+        for i in range(steps_e2e):
+            ctx.train_step_host(step, 0, noise_h.data_ptr(), real_h.data_ptr(), stats_h[i & 1].data_ptr(), sp)
+            done[i & 1].record(cur)
             step += 1
-            cur.synchronize()  # the step's result (stats record) is on the host
+            if i > 0:
+                done[(i - 1) & 1].synchronize()  # step i-1's result (stats record) is on the host
+        done[(steps_e2e - 1) & 1].synchronize()
         t1 = time.perf_counter()
         e2e_ms = (t1 - t0) * 1e3 / steps_e2e
         if dist is not None:
@@ -433,7 +438,9 @@ def ours_arm(args):
                "d2h_bytes_per_step": ctypes.sizeof(L.StepStats), "ms_per_step": e2e_ms,
                "note": "sagips_train_step_host per step: the generator noise [k][d] and the real batch [N][2] "
                        "copied from pinned host memory (a data loader's buffers, replacing the device RNG "
-                       "noise and the resident-shard bootstrap), the stats record copied back and waited for"}
+                       "noise and the resident-shard bootstrap) on the library's copy stream, the stats record copied back "
+                       "and waited for; step t+1 is issued before waiting for step t's record (one step in "
+                       "flight), so t+1's copy overlaps t's compute"}
 
     # exchange alone (a12, BJ north star: "exchange GB/s against NVLink
     # bandwidth"): local step (LOCAL_ONLY), device + host barrier, then

@@ -311,11 +311,14 @@ SAGIPS_API sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint3
  * generator noise of a1 (host_noise: [k][noise_dim] fp32, else drawn by
  * Philox) and the real batch of a5 (host_real: [N][2] fp32 real rows,
  * replacing the bootstrap from the resident shard; the real half of the
- * histogram is then zero and SAGIPS_T_REAL_IDX is not written), copied to
- * the device on `stream` at the start of the step; host_stats (or NULL)
- * receives the step's stats record by an asynchronous copy at its end
- * (valid once `stream` has completed).  [async]  Errors: as
- * sagips_train_step. */
+ * histogram is then zero and SAGIPS_T_REAL_IDX is not written).  They are
+ * copied on a library-owned stream into one of two device staging buffers
+ * of the workspace (slot step & 1), which `stream` waits for, so a caller
+ * that issues step t+1 before waiting for step t overlaps t+1's host-to-
+ * device copy with t's compute; the host buffers must stay unchanged until
+ * the step's stats are valid.  host_stats (or NULL) receives the step's
+ * stats record by an asynchronous copy at its end (valid once `stream` has
+ * completed).  [async]  Errors: as sagips_train_step. */
 SAGIPS_API sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, uint32_t flags,
                                                 const float* host_noise, const float* host_real,
                                                 sagips_step_stats* host_stats, void* stream);

@@ -60,8 +60,16 @@ struct sagips_ctx {
   float* lpart[sagips::kMaxLayers] = {};  // [ctas][128][128] wgrad partials of hidden layer l
   float* ldb[sagips::kMaxLayers] = {};    // [ctas][128] bias-gradient partials
   bool d_adam_done = false;               // the D step already applied Adam(D) (fused reduction)
-  const float* host_noise = nullptr;      // sagips_train_step_host: this step's inputs from the caller
-  const float* host_real = nullptr;
+  // sagips_train_step_host: the caller's inputs are copied on copy_stream
+  // into staging buffer b = step & 1 (so the copy of step t+1 overlaps step
+  // t), the step copies them into place on its own stream
+  const float* in_noise = nullptr;        // this step's staged inputs (device), or nullptr
+  const float* in_real = nullptr;
+  float* hin[2] = {};                     // [k d noise | 2 N real] per slot
+  int in_slot = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t in_ready[2] = {}, in_free[2] = {};
+  bool in_free_recorded[2] = {};
   static constexpr int kTileCtrs = 16;
   uint32_t* tile_ctrs = nullptr;          // dynamic tile-schedule counters of the layer kernels
   int tile_ctr_next = 0;

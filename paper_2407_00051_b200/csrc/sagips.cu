@@ -115,6 +115,7 @@ static void carve(sagips_ctx* c, char* base) {
   }
   c->loss_part = cv.take<double>(head_blocks());
   c->stats = cv.take<sagips_step_stats>(1);
+  for (int b = 0; b < 2; ++b) c->hin[b] = cv.take<float>(k * g.noise_dim + 2 * N);  // host-input staging
   c->ws_bytes = cv.off;
 }
 
@@ -320,6 +321,14 @@ sagips_status sagips_destroy(sagips_ctx* ctx) {
   fused_trace_report();
   if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(ctx->in_ready[b]);
+      cudaEventDestroy(ctx->in_free[b]);
+    }
+  }
   exchange_destroy(ctx);
   for (auto& row : ctx->pev)
     for (auto& e : row)
@@ -800,8 +809,8 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   const uint32_t step = (uint32_t)t;
   mark(c, 0, st);
   // a1 noise ~ N(0,1) (or the caller's, sagips_train_step_host)
-  if (c->host_noise)
-    cudaMemcpyAsync(c->noise, c->host_noise, sizeof(float) * k * g.noise_dim, cudaMemcpyHostToDevice, st);
+  if (c->in_noise)
+    cudaMemcpyAsync(c->noise, c->in_noise, sizeof(float) * k * g.noise_dim, cudaMemcpyDeviceToDevice, st);
   else
     launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
   // a2 generator forward (hidden LeakyReLU, linear output) + a3 constrain
@@ -809,7 +818,7 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   const bool tab = g.sampler == SAGIPS_SAMPLER_TABULATED;
   // the real rows come from the resident shard: prefetch it into L2 and zero
   // the histograms inside the generator forward (the step's sampler follows)
-  const bool boot = !c->host_real;
+  const bool boot = !c->in_real;
   if (fused_gen) {
     launch_gen_fwd(c, st, boot ? c->shard : nullptr, boot ? 8 * g.shard_rows : 0, boot ? c->hist : nullptr,
                    boot ? 4 * (g.hist_bins + 2) : 0);
@@ -827,10 +836,10 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   // a4-a6 fused sampler + bootstrap + histograms (tabulated: the bootstrap
   // pass draws the real rows, the tabulated sampler the fake rows N..2N-1)
   mark(c, 1, st);
-  if (c->host_real) {
+  if (c->in_real) {
     // the caller's real batch (rows 0..N-1) replaces the bootstrap (a5); the
     // fake rows and their histogram as usual, the real histogram is zero
-    cudaMemcpyAsync(c->X, c->host_real, sizeof(float) * 2 * (int64_t)k * m, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(c->X, c->in_real, sizeof(float) * 2 * (int64_t)k * m, cudaMemcpyDeviceToDevice, st);
     cudaMemsetAsync(c->hist, 0, sizeof(uint32_t) * 4 * (g.hist_bins + 2), st);
     if (!tab)
       launch_sample_events(c->cbuf, k, m, g.seed, step, g.rank, kStreamFake, c->X + 2 * (int64_t)k * m,
@@ -925,8 +934,8 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
   // CUDA graph: capture this step's launches and replay them as one graph
   // launch (the first step runs eagerly: lazy set-up, kernel attributes);
   // an executable graph is updated in place while the topology is unchanged
-  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx) && !ctx->host_noise &&
-                     !ctx->host_real;
+  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx) && !ctx->in_noise &&
+                     !ctx->in_real;
   flags &= ~SAGIPS_STEP_GRAPH;
   if (!graph) return step_body(ctx, step, flags, stream);
   // captured on a library-owned stream (the caller's may be the legacy
@@ -972,10 +981,37 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
 sagips_status sagips_train_step_host(sagips_ctx* ctx, uint64_t step, uint32_t flags, const float* host_noise,
                                      const float* host_real, sagips_step_stats* host_stats, void* stream) {
   if (!ctx) return SAGIPS_ERR_INVALID_ARG;
-  ctx->host_noise = host_noise;
-  ctx->host_real = host_real;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (host_noise || host_real) {
+    // copy_stream: H2D into staging slot b once the step that used b last
+    // has copied it into place (in_free[b]); the step waits for in_ready[b]
+    if (!ctx->copy_stream) {
+      CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&ctx->in_ready[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->in_free[b], cudaEventDisableTiming));
+      }
+    }
+    const int b = (int)(step & 1);
+    const int64_t nz = (int64_t)ctx->cfg.param_samples * ctx->cfg.noise_dim;
+    if (ctx->in_free_recorded[b]) CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->in_free[b], 0));
+    if (host_noise)
+      CK(cudaMemcpyAsync(ctx->hin[b], host_noise, sizeof(float) * nz, cudaMemcpyHostToDevice, ctx->copy_stream));
+    if (host_real)
+      CK(cudaMemcpyAsync(ctx->hin[b] + nz, host_real, sizeof(float) * 2 * ctx->N, cudaMemcpyHostToDevice,
+                         ctx->copy_stream));
+    CK(cudaEventRecord(ctx->in_ready[b], ctx->copy_stream));
+    CK(cudaStreamWaitEvent(st, ctx->in_ready[b], 0));
+    ctx->in_noise = host_noise ? ctx->hin[b] : nullptr;
+    ctx->in_real = host_real ? ctx->hin[b] + nz : nullptr;
+    ctx->in_slot = b;
+  }
   const sagips_status s = sagips_train_step(ctx, step, flags, stream);
-  ctx->host_noise = ctx->host_real = nullptr;
+  if (ctx->in_noise || ctx->in_real) {  // slot b is free once the step's copies out of it are done
+    ctx->in_noise = ctx->in_real = nullptr;
+    CK(cudaEventRecord(ctx->in_free[ctx->in_slot], st));
+    ctx->in_free_recorded[ctx->in_slot] = true;
+  }
   if (s != SAGIPS_OK) return s;
   if (host_stats)
     CK(cudaMemcpyAsync(host_stats, ctx->stats, sizeof(sagips_step_stats), cudaMemcpyDeviceToHost, (cudaStream_t)stream));

@@ -412,6 +412,37 @@ def test_train_step_host_inputs_reproduce_the_device_step(preset):
     assert np.all(hb[0] == 0) and np.array_equal(ha[1], hb[1])
 
 
+def test_pipelined_host_input_steps_match_the_device_steps():
+    """sagips_train_step_host issued one step ahead (step t+1 before waiting
+    for step t, as bench.py's e2e loop): the two staging slots and the copy
+    stream keep every step's inputs apart -- six steps with distinct inputs
+    end in the device-input run's parameters, bit for bit."""
+    import ctypes
+    L = lib()
+    kw = dict(seed=23, param_samples=32, events_per_sample=64, reference_rows=4000, shard_rows=2000)
+    ca, cb = make_ctx(L.config_init(1, **kw)), make_ctx(L.config_init(1, **kw))
+    N, T = 32 * 64, 6
+    noises, reals = [], []
+    for t in range(T):
+        ca.train_step(t, 0, _stream())
+        torch.cuda.synchronize()
+        noises.append(torch.from_numpy(ca.get(L.T_NOISE).reshape(32, -1).copy()).pin_memory())
+        reals.append(torch.from_numpy(ca.get(L.T_EVENTS).reshape(-1, 2)[:N].copy()).pin_memory())
+    stats = [(ctypes.c_uint8 * ctypes.sizeof(L.StepStats))() for _ in range(T)]
+    cur = torch.cuda.current_stream()
+    done = [torch.cuda.Event() for _ in range(T)]
+    for t in range(T):
+        cb.train_step_host(t, 0, noises[t].data_ptr(), reals[t].data_ptr(), ctypes.addressof(stats[t]), _stream())
+        done[t].record(cur)
+        if t > 0:
+            done[t - 1].synchronize()
+    torch.cuda.synchronize()
+    for w in (L.T_GEN_W, L.T_GEN_B, L.T_DISC_W, L.T_DISC_B):
+        assert np.array_equal(ca.get(w), cb.get(w)), w
+    sa, sb = ca.get(L.T_STATS), L.StepStats.from_buffer_copy(stats[T - 1])
+    assert sa.loss_d == sb.loss_d and sa.loss_g == sb.loss_g
+
+
 @pytest.mark.parametrize("preset", [0, 1])
 def test_graph_step_matches_eager(preset):
     """SAGIPS_STEP_GRAPH: the captured-and-replayed step runs
