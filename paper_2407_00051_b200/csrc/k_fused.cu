@@ -137,6 +137,12 @@ __device__ __forceinline__ void group_sync(int s) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(32 * kGroupWarps) : "memory");
 }
 
+// named barrier of the two warps that own one row quarter q of slot s (column
+// halves h = 0, 1): the head's z / dy exchange between them needs no more
+__device__ __forceinline__ void pair_sync(int s, int q) {
+  asm volatile("bar.sync %0, 64;" ::"r"(3 + 4 * s + q) : "memory");
+}
+
 // W [128][128] fp32 -> hi (/ lo) planes, SW128 layout; all threads of the CTA
 template <bool kSplit>
 __device__ __forceinline__ void stage_w(const float* __restrict__ W, uint32_t hi, uint32_t lo) {
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
         }
       }
       sv->xdot[s][r][h] = dot.x + dot.y;
-      group_sync(s);
+      pair_sync(s, q);
       const float zz = (sv->xdot[s][r][0] + sv->xdot[s][r][1]) + b4;
       const float dz = valid ? (sigmoid_f(zz) - 1.0f) * a.scale : 0.f;
       if (valid && h == 0) {
@@ -464,8 +470,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
         }
       }
       *reinterpret_cast<float2*>(&sv->xdy[s][r][2 * h]) = make_float2(dx.x + dx.y, dyy.x + dyy.y);
-      tc_fence_before();  // this tile's accumulator reads precede the next tile's MMAs
-      group_sync(s);
+      pair_sync(s, q);  // (the next tile's MMAs follow run_layer's fence + group barrier)
       if (h == 0 && valid) {
         const float4 p = lds4(&sv->xdy[s][r][0]);
         a.dy[row] = make_float2(p.x + p.z, p.y + p.w);
@@ -631,7 +636,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
       }
       reinterpret_cast<uint2*>((l == 0 ? a.m2 : a.m3) + t * 128 + r)[h] = make_uint2(mb[0], mb[1]);
     }
-    // head
+    // head.  Pass 1: H_4 = LeakyReLU(Z_4) and its dot with w; H_4 goes back
+    // into the accumulator columns for pass 2 (its sign is Z_4's)
     run_layer(2);
     float2 dot = make_float2(0.f, 0.f);
     {
@@ -645,12 +651,20 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
         const float2 z0 = add2(make_float2(v[2 * k], v[2 * k + 1]), make_float2(bq.x, bq.y));
         const float2 z1 = add2(make_float2(v[2 * k + 2], v[2 * k + 3]), make_float2(bq.z, bq.w));
         const float2 t0 = mul2(z0, alpha2), t1 = mul2(z1, alpha2);
-        dot = fma2(make_float2(fmaxf(z0.x, t0.x), fmaxf(z0.y, t0.y)), make_float2(wq.x, wq.y), dot);
-        dot = fma2(make_float2(fmaxf(z1.x, t1.x), fmaxf(z1.y, t1.y)), make_float2(wq.z, wq.w), dot);
+        const float2 h0 = make_float2(fmaxf(z0.x, t0.x), fmaxf(z0.y, t0.y));
+        const float2 h1 = make_float2(fmaxf(z1.x, t1.x), fmaxf(z1.y, t1.y));
+        dot = fma2(h0, make_float2(wq.x, wq.y), dot);
+        dot = fma2(h1, make_float2(wq.z, wq.w), dot);
+        v[2 * k] = h0.x;
+        v[2 * k + 1] = h0.y;
+        v[2 * k + 2] = h1.x;
+        v[2 * k + 3] = h1.y;
       }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st16(accT + 16u * c, reinterpret_cast<const uint32_t*>(v + 16 * c));
     }
     sv->xdot[s][r][h] = dot.x + dot.y;
-    group_sync(s);
+    pair_sync(s, q);
     const float zz = (sv->xdot[s][r][0] + sv->xdot[s][r][1]) + b4;
     const float tl = (row < a.n_real) ? 1.f : a.label_rest;
     const float dz = valid ? (sigmoid_f(zz) - tl) * a.scale : 0.f;
@@ -664,6 +678,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     if (kGenOut && h == 0) a.dz[row] = dz;  // the backward generates G_4 from dz and the sign bits (kGenG)
     {
       float v[64];
+      tmem_st_wait();  // pass 1's H_4 stores
       tmem_ld32x2(accT, accT + 32u, v, v + 32);
       uint32_t mb[2] = {0u, 0u};
 #pragma unroll
@@ -673,15 +688,12 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
           const int col = 64 * h + 32 * c + 2 * k;
-          const float4 bq = lds4(&sv->b[2][col]);
           const float4 wq = lds4(&sv->w4[col]);
           const float4 aq = lds4(&sv->aw4[col]);
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const float2 z = add2(make_float2(v[32 * c + 2 * (k + u)], v[32 * c + 2 * (k + u) + 1]),
-                                  u ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y));
-            const float2 tt = mul2(z, alpha2);
-            const float2 hd = mul2(dz2, make_float2(fmaxf(z.x, tt.x), fmaxf(z.y, tt.y)));  // dz H_4
+            const float2 z = make_float2(v[32 * c + 2 * (k + u)], v[32 * c + 2 * (k + u) + 1]);  // H_4 (sign of Z_4)
+            const float2 hd = mul2(dz2, z);  // dz H_4
             g[2 * (k + u)] = hd.x;
             g[2 * (k + u) + 1] = hd.y;
             if (!kGenOut) {
