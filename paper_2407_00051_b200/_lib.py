@@ -8,7 +8,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsagips.so")
+# SAGIPS_LIB_VARIANT=x loads libsagips_x.so (same-box A/B builds, tests/tools/ab_lib.sh)
+LIB_PATH = os.path.join(_HERE, "libsagips" + (("_" + os.environ["SAGIPS_LIB_VARIANT"])
+                                              if os.environ.get("SAGIPS_LIB_VARIANT") else "") + ".so")
 
 OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CONFIG", 3: "CUDA", 4: "NONFINITE", 5: "PROTOCOL",

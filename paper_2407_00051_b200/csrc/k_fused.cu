@@ -132,6 +132,12 @@ __device__ __forceinline__ void mma_ts_warp(uint32_t d, uint32_t a_tmem, uint64_
       : "memory");
 }
 
+#ifdef SAGIPS_NO_XPREFETCH  // experiment builds (build.py SAGIPS_BUILD_DEFS)
+constexpr bool kPrefetchX = false;
+#else
+constexpr bool kPrefetchX = true;
+#endif
+
 // named barrier of one slot group (8 warps)
 __device__ __forceinline__ void group_sync(int s) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(32 * kGroupWarps) : "memory");
@@ -345,6 +351,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
     const int64_t row = (int64_t)(j + (int64_t)i * n) * 128 + r;
     const bool valid = row < a.rows;
     const float2 x = valid ? __ldg(a.Y + row) : make_float2(0.f, 0.f);
+    if (kPrefetchX && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
+      const int64_t r0 = (int64_t)(j + (int64_t)(i + 2) * n) * 128;
+      prefetch_l2(a.Y + r0, (uint32_t)((a.rows - r0 < 128 ? a.rows - r0 : 128) * 8) & ~15u);
+    }
     uint32_t m1[2], m2[2], m3[2];  // LeakyReLU' sign bits of Z_1..Z_3 (two 32-column chunks)
     // H_1 = LeakyReLU(fma(x0, w0x, fma(x1, w0y, b0)))  (the per-layer kernels' order)
     {
@@ -587,6 +597,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     const int64_t row = t * 128 + r;
     const bool valid = row < a.rows;
     const float2 x = valid ? __ldg(a.X + row) : make_float2(0.f, 0.f);
+    if (kPrefetchX && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
+      const int64_t r0 = (t + 2 * (int64_t)n) * 128;
+      prefetch_l2(a.X + r0, (uint32_t)((a.rows - r0 < 128 ? a.rows - r0 : 128) * 8) & ~15u);
+    }
     {  // H_1
       const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
 #pragma unroll

@@ -1120,41 +1120,54 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
     // ---------------- SIMT producers of the G_4 planes (kGenG): thread = row
     if (kGenG) {
       const int r = 32 * warp + lane;
+      // dz and the mask of the next tile are loaded one tile ahead (their
+      // HBM latency is otherwise paid by every tile's generation)
+      float dz_n = 0.f;
+      uint4 mq_n = make_uint4(0u, 0u, 0u, 0u);
+      if (nmine > 0) {
+        dz_n = __ldg(a.gen_dz + tile_of(0) * 128 + r);
+        mq_n = __ldg(a.gen_mask + tile_of(0) * 128 + r);
+      }
       for (int i = 0; i < nmine; ++i) {
-        const int64_t row = tile_of(i) * 128 + r;
-        const float dz = __ldg(a.gen_dz + row);
-        const uint4 mq = __ldg(a.gen_mask + row);
-        // the Gh plane goes to its slot as soon as it is free (it is needed
-        // first); the lo words wait in registers for the Gl slot, which the
-        // previous tile releases later (plane FIFO: Gh, Hh, Gl)
-        const PS gh = pl_gh(i), gl = pl_gl(i);
-        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
-        const uint32_t hb = pl_addr(gh.slot), lb = pl_addr(gl.slot);
-        const float2 dz2 = make_float2(dz, dz);
-        uint32_t lw[64];
-#pragma unroll
-        for (int cb = 0; cb < 4; ++cb) {  // 32-column blocks: mask word cb (bit k = column 2k, bit 16 + k = 2k + 1)
-          const uint32_t m = cb == 0 ? mq.x : cb == 1 ? mq.y : cb == 2 ? mq.z : mq.w;
-          uint32_t hw[16];
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const int col = 32 * cb + 2 * kk;
-            const float2 w = *reinterpret_cast<const float2*>(&p0->w0x[col]);
-            const float2 wa2 = *reinterpret_cast<const float2*>(&p0->w0y[col]);
-            const float2 g = mul2(dz2, make_float2(((m >> kk) & 1u) ? w.x : wa2.x, ((m >> (16 + kk)) & 1u) ? w.y : wa2.y));
-            split2(g.x, g.y, hw[kk], lw[16 * cb + kk]);
-          }
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj)
-            sts128(hb + sw128_chunk(r, 4 * cb + jj, 128), hw[4 * jj], hw[4 * jj + 1], hw[4 * jj + 2], hw[4 * jj + 3]);
+        const float dz = dz_n;
+        const uint4 mq = mq_n;
+        if (i + 1 < nmine) {
+          dz_n = __ldg(a.gen_dz + tile_of(i + 1) * 128 + r);
+          mq_n = __ldg(a.gen_mask + tile_of(i + 1) * 128 + r);
         }
+        // the Gh plane goes to its slot as soon as it is free (it is needed
+        // first); the Gl plane when the previous tile releases its slot
+        // (plane FIFO: Gh, Hh, Gl).  Each pass computes G_4 = dz (w or alpha
+        // w) and its split afresh: no lo words held across the wait, and a
+        // rolled 32-column loop keeps the kernel's code small
+        const PS gh = pl_gh(i), gl = pl_gl(i);
+        const float2 dz2 = make_float2(dz, dz);
+        auto gen_plane = [&](uint32_t base, bool lo_plane) {
+#pragma unroll 1
+          for (int cb = 0; cb < 4; ++cb) {  // 32-column blocks: mask word cb (bit k = column 2k, bit 16 + k = 2k + 1)
+            const uint32_t m = cb == 0 ? mq.x : cb == 1 ? mq.y : cb == 2 ? mq.z : mq.w;
+            uint32_t hw[16], lw[16];
+#pragma unroll
+            for (int kk = 0; kk < 16; ++kk) {
+              const int col = 32 * cb + 2 * kk;
+              const float2 w = *reinterpret_cast<const float2*>(&p0->w0x[col]);
+              const float2 wa2 = *reinterpret_cast<const float2*>(&p0->w0y[col]);
+              const float2 g = mul2(dz2, make_float2(((m >> kk) & 1u) ? w.x : wa2.x, ((m >> (16 + kk)) & 1u) ? w.y : wa2.y));
+              split2(g.x, g.y, hw[kk], lw[kk]);
+            }
+            const uint32_t* v = lo_plane ? lw : hw;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj)
+              sts128(base + sw128_chunk(r, 4 * cb + jj, 128), v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+          }
+        };
+        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
+        gen_plane(pl_addr(gh.slot), false);
         fence_proxy_async_smem();
         asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
         if (warp == 0 && lane == 0) mbar_arrive(&pfull[gh.slot]);
         SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
-#pragma unroll
-        for (int jc = 0; jc < 16; ++jc)
-          sts128(lb + sw128_chunk(r, jc, 128), lw[4 * jc], lw[4 * jc + 1], lw[4 * jc + 2], lw[4 * jc + 3]);
+        gen_plane(pl_addr(gl.slot), true);
         fence_proxy_async_smem();
         asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
         if (warp == 0 && lane == 0) mbar_arrive(&pfull[gl.slot]);
@@ -1744,7 +1757,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_bwd(const __grid_constant__ Bwd
   unsigned long long* cs = cta_stamps(trace);
   if (cs && threadIdx.x == 0) cs[0] = globaltimer();
   bwd_body<kSplit, kFirst, kWgrad, kH1Load, kGenG>(a, blockIdx.x, gridDim.x, trace, cta_waits(cs));
-  if (cs && threadIdx.x == 0) cs[1] = globaltimer();
+  if (cs && threadIdx.x == 0) {
+    cs[1] = globaltimer();
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    cs[2] = sm;
+  }
 }
 
 // The whole D step (kD: wgrad, head and layer-0 gradients) or G step (dy) as

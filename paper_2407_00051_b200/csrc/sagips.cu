@@ -506,10 +506,11 @@ static bool h1_store() {
 static bool use_fused(const sagips_ctx* c);
 static bool tc_split(const sagips_ctx* c);
 static bool h1_store();
-// SAGIPS_GEN_G=1: the fused D step passes G_4 as dz + sign bits (kGenG)
+// the fused D step passes G_4 as dz + sign bits (kGenG; default for
+// fp32-class, SAGIPS_GEN_G=0 writes the planes instead)
 static bool gen_g(const sagips_ctx* c) {
   const char* e = getenv("SAGIPS_GEN_G");
-  return e && e[0] == '1' && tc_split(c) && use_fused(c) && !h1_store();
+  return !(e && e[0] == '0') && tc_split(c) && use_fused(c) && !h1_store();
 }
 
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,
@@ -541,9 +542,9 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
     f.m2 = c->dMask[1];
     f.h3 = reinterpret_cast<uint8_t*>(c->dAct[2]);
     f.m3 = c->dMask[2];
-    // SAGIPS_GEN_G=1 (fp32-class, measured slower: DESIGN.md 7.1): dz and the
-    // Z_4 sign bits (in the otherwise unused H_4 buffers) replace the G_4
-    // planes and the next pass regenerates them; default: the planes
+    // fp32-class: dz and the Z_4 sign bits (in the otherwise
+    // unused H_4 buffers) replace the G_4 planes and the next pass
+    // regenerates them (SAGIPS_GEN_G=0: the planes)
     f.g4 = gen_g(c) ? nullptr : reinterpret_cast<uint8_t*>(c->dZb[0]);
     f.dz = c->dAct[3];
     f.m4 = c->dMask[3];

@@ -161,12 +161,15 @@ def test_step_tabulated_sampler(preset, k, m, G):
 @pytest.fixture
 def fused_env(request, monkeypatch):
     """SAGIPS_FUSED: "1" the fused discriminator kernels (k_dfwd, k_gstep;
-    default), "0" the per-layer tcgen05 kernels."""
-    monkeypatch.setenv("SAGIPS_FUSED", request.param)
+    default), "0" the per-layer tcgen05 kernels; "1p": fused, with the G_4
+    planes written by k_dfwd instead of regenerated from dz + sign bits by
+    the next pass (SAGIPS_GEN_G=0)."""
+    monkeypatch.setenv("SAGIPS_FUSED", request.param[0])
+    monkeypatch.setenv("SAGIPS_GEN_G", "0" if request.param == "1p" else "1")
     return request.param
 
 
-@pytest.mark.parametrize("impl,fused_env", [(0, "1"), (0, "0"), (1, "1")], indirect=["fused_env"])
+@pytest.mark.parametrize("impl,fused_env", [(0, "1"), (0, "1p"), (0, "0"), (1, "1")], indirect=["fused_env"])
 def test_step_paper_widths_ragged(impl, fused_env):
     """paper widths, 2N = 7,808 rows (ragged 128-row tiles), step 3, rank 1;
     impl 0 = tcgen05 bf16x3 hidden layers (fused kernels or per-layer

@@ -54,6 +54,11 @@ for li in range(12):
               6: "mask-flag", 7: "epi-X"}
         w = c[:, 4:12].mean(axis=0) / 1e3
         print(f"{'':12s} waits (us per CTA): " + ", ".join(f"{wn[k]} {w[k]:.0f}" for k in wn if w[k] > 0.5))
+        # the slowest CTAs: end time after the first start, with their SM id (bwd launches record it)
+        idx = np.argsort(en)[::-1][:12]
+        print(f"{'':12s} slowest CTAs (end us, sm): " + ", ".join(f"{(en[k] - st.min()) / 1e3:.0f}/{c[k, 2]}" for k in idx))
+        q = np.percentile((en - st.min()) / 1e3, [0, 10, 50, 90, 100])
+        print(f"{'':12s} CTA end percentiles (us): " + " ".join(f"{v:.0f}" for v in q))
 
 
 def pipe_split(dstep, sms=148):
