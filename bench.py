@@ -252,11 +252,15 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     mids = max(0, cfg.disc_depth - 3)
     # H_1 hi plane stored by the first forward pass and read back (split, SAGIPS_H1_STORE=1)
     h1 = Eh if (split and os.environ.get("SAGIPS_H1_STORE") == "1") else 0
+    # fp32-class fused D step: G_4 travels as dz + the Z_4 sign bits (20 B/row) and
+    # d_bwd_last regenerates its planes (kGenG; SAGIPS_GEN_G=0 writes the E-byte planes)
+    g4 = 20 if (split and os.environ.get("SAGIPS_FUSED", "1") != "0"
+                and os.environ.get("SAGIPS_GEN_G", "1") != "0") else E
     spec = {  # class: (rows, bytes/row, useful flops/row, executed flops/row, launches)
         "d_fwd_first": (rows_d, 8 + E + 16 + h1, G, px * G, 1),
         "d_fwd_mid": (rows_d, 2 * E + 16, G, px * G, mids),
         "d_fwd_head": (rows_d, 2 * E + 4, G, px * G, 1),
-        "d_bwd_last": (rows_d, 2 * E + Eh + 16, 2 * G, (px + pw) * G, 1),
+        "d_bwd_last": (rows_d, g4 + E + Eh + 16, 2 * G, (px + pw) * G, 1),
         "d_bwd_mid": (rows_d, 2 * E + Eh + 16, 2 * G, (px + pw) * G, mids),
         "d_bwd_first": (rows_d, E + h1 + 8, 2 * G, (px + pw) * G, 1),
         "g_fwd_first": (rows_g, 8 + E + 16, G, px * G, 1),
@@ -267,8 +271,9 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
         "g_bwd_dy": (rows_g, E + 16, G, px * G, 1),
         # fused G step (k_gstep): 3 forward + 3 dgrad GEMMs per row, activations on chip (8 B in, 8 B out)
         "g_fused": (rows_g, 8 + 8 + 4, 6 * G, 6 * px * G, 1),
-        # fused D forward (k_dfwd): 3 GEMMs per row; X in, H_2 / H_3 hi planes + masks and G_4 planes out
-        "d_fwd_fused": (rows_d, 8 + 2 * (E // 2 + 16) + E + 4, 3 * G, 3 * px * G, 1)}
+        # fused D forward (k_dfwd): 3 GEMMs per row; X in, H_2 / H_3 hi planes + masks, G_4 (planes or
+        # dz + sign bits) and the logit out
+        "d_fwd_fused": (rows_d, 8 + 2 * (Eh + 16) + g4 + 4, 3 * G, 3 * px * G, 1)}
     try:
         kt, _ = ctx.kernel_times()
     except Exception:

@@ -132,7 +132,14 @@ __device__ __forceinline__ void mma_ts_warp(uint32_t d, uint32_t a_tmem, uint64_
       : "memory");
 }
 
-#ifdef SAGIPS_NO_XPREFETCH  // experiment builds (build.py SAGIPS_BUILD_DEFS)
+// L2 prefetch of a slot's next tile's input rows (experiment builds switch
+// them off with build.py SAGIPS_BUILD_DEFS)
+#ifdef SAGIPS_NO_XPREFETCH_G
+constexpr bool kPrefetchY = false;
+#else
+constexpr bool kPrefetchY = true;
+#endif
+#ifdef SAGIPS_NO_XPREFETCH_D
 constexpr bool kPrefetchX = false;
 #else
 constexpr bool kPrefetchX = true;
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
     const int64_t row = (int64_t)(j + (int64_t)i * n) * 128 + r;
     const bool valid = row < a.rows;
     const float2 x = valid ? __ldg(a.Y + row) : make_float2(0.f, 0.f);
-    if (kPrefetchX && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
+    if (kPrefetchY && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
       const int64_t r0 = (int64_t)(j + (int64_t)(i + 2) * n) * 128;
       prefetch_l2(a.Y + r0, (uint32_t)((a.rows - r0 < 128 ? a.rows - r0 : 128) * 8) & ~15u);
     }
