@@ -209,26 +209,7 @@ __device__ __forceinline__ float colsum32(float (&g)[32], int lane) {
   }
   return g[0];
 }
-// 16 packed words = columns 32 c .. 32 c + 31 of column half h, row r of a
-// plane tile (SW128 layout of the per-layer kernels): 4 chunks of 16 bytes,
-// as two 32-byte stores (STG.256, whole sectors): chunks 2m, 2m+1 land on the
-// aligned position pair {2m ^ x, 2m+1 ^ x}, x = r % 8 (swapped when x is odd)
-__device__ __forceinline__ void st256(uint8_t* p, const uint32_t* w0, const uint32_t* w1) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w0[0]), "r"(w0[1]), "r"(w0[2]),
-               "r"(w0[3]), "r"(w1[0]), "r"(w1[1]), "r"(w1[2]), "r"(w1[3])
-               : "memory");
-}
-__device__ __forceinline__ void store_plane_words(uint8_t* plane, int r, int h, int c, const uint32_t* w) {
-  uint8_t* row = plane + h * 16384 + (r >> 3) * 1024 + (r & 7) * 128;
-  const int x = r & 7;
-#pragma unroll
-  for (int mm = 0; mm < 2; ++mm) {
-    const int j0 = 4 * c + 2 * mm;  // even chunk
-    uint8_t* dst = row + (((j0 ^ x) & ~1) << 4);
-    if (x & 1) st256(dst, w + 8 * mm + 4, w + 8 * mm);
-    else st256(dst, w + 8 * mm, w + 8 * mm + 4);
-  }
-}
+using tc::store_plane_words;  // (tc_util.cuh: STG.256 whole-sector plane stores)
 
 }  // namespace
 
