@@ -422,11 +422,14 @@ def ours_arm(args):
         stats_h = [torch.empty(ctypes.sizeof(L.StepStats), dtype=torch.uint8).pin_memory() for _ in range(2)]
         done = [torch.cuda.Event(), torch.cuda.Event()]
         cur = torch.cuda.current_stream()
+        for _ in range(2):  # warm-up: the host-input step's graph is (re)instantiated once
+            ctx.train_step_host(step, gflag, noise_h.data_ptr(), real_h.data_ptr(), stats_h[0].data_ptr(), sp)
+            step += 1
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for i in range(steps_e2e):
-            ctx.train_step_host(step, 0, noise_h.data_ptr(), real_h.data_ptr(), stats_h[i & 1].data_ptr(), sp)
+            ctx.train_step_host(step, gflag, noise_h.data_ptr(), real_h.data_ptr(), stats_h[i & 1].data_ptr(), sp)
             done[i & 1].record(cur)
             step += 1
             if i > 0:

@@ -194,8 +194,8 @@ typedef struct {
 #define SAGIPS_STEP_NO_ADAM_G   2u  /* exchange but do not apply the generator update */
 #define SAGIPS_STEP_GRAPH       4u  /* capture the step's launches into a CUDA graph and replay it as one
                                        graph launch (the executable graph is updated in place from step
-                                       to step); ignored on the first step, with host inputs
-                                       (sagips_train_step_host) and for the two-sided ring modes (ARAR,
+                                       to step; host-input steps, sagips_train_step_host, included);
+                                       ignored on the first step and for the two-sided ring modes (ARAR,
                                        ARAR_ARAR), whose pull waits on an earlier step's side-stream
                                        ring.  Phase / kernel timing is not recorded for graph steps.
                                        The one-sided pass-along ring joins its forwarding agent into

@@ -935,8 +935,9 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
   // CUDA graph: capture this step's launches and replay them as one graph
   // launch (the first step runs eagerly: lazy set-up, kernel attributes);
   // an executable graph is updated in place while the topology is unchanged
-  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx) && !ctx->in_noise &&
-                     !ctx->in_real;
+  // (host-input steps too: their staged inputs are copied into place by
+  // memcpy nodes, whose source slot alternates -- an in-place update)
+  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx);
   flags &= ~SAGIPS_STEP_GRAPH;
   if (!graph) return step_body(ctx, step, flags, stream);
   // captured on a library-owned stream (the caller's may be the legacy

@@ -415,11 +415,13 @@ def test_train_step_host_inputs_reproduce_the_device_step(preset):
     assert np.all(hb[0] == 0) and np.array_equal(ha[1], hb[1])
 
 
-def test_pipelined_host_input_steps_match_the_device_steps():
+@pytest.mark.parametrize("graph", [False, True])
+def test_pipelined_host_input_steps_match_the_device_steps(graph):
     """sagips_train_step_host issued one step ahead (step t+1 before waiting
     for step t, as bench.py's e2e loop): the two staging slots and the copy
     stream keep every step's inputs apart -- six steps with distinct inputs
-    end in the device-input run's parameters, bit for bit."""
+    end in the device-input run's parameters, bit for bit; also as CUDA-graph
+    steps (the staged-input copies are memcpy nodes updated in place)."""
     import ctypes
     L = lib()
     kw = dict(seed=23, param_samples=32, events_per_sample=64, reference_rows=4000, shard_rows=2000)
@@ -435,7 +437,8 @@ def test_pipelined_host_input_steps_match_the_device_steps():
     cur = torch.cuda.current_stream()
     done = [torch.cuda.Event() for _ in range(T)]
     for t in range(T):
-        cb.train_step_host(t, 0, noises[t].data_ptr(), reals[t].data_ptr(), ctypes.addressof(stats[t]), _stream())
+        cb.train_step_host(t, L.STEP_GRAPH if graph else 0, noises[t].data_ptr(), reals[t].data_ptr(),
+                           ctypes.addressof(stats[t]), _stream())
         done[t].record(cur)
         if t > 0:
             done[t - 1].synchronize()
