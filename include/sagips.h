@@ -195,7 +195,8 @@ typedef struct {
 #define SAGIPS_STEP_GRAPH       4u  /* capture the step's launches into a CUDA graph and replay it as one
                                        graph launch (the executable graph is updated in place from step
                                        to step; host-input steps, sagips_train_step_host, included);
-                                       ignored on the first step and for the two-sided ring modes (ARAR,
+                                       ignored on the first step, on steps whose outer ring fires on this
+                                       rank (they run eagerly) and for the two-sided ring modes (ARAR,
                                        ARAR_ARAR), whose pull waits on an earlier step's side-stream
                                        ring.  Phase / kernel timing is not recorded for graph steps.
                                        The one-sided pass-along ring joins its forwarding agent into

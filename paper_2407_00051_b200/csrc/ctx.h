@@ -153,6 +153,7 @@ sagips_status exchange_poll(sagips_ctx* c);
 // graph capture support: whether this configuration's step can be captured,
 // and the join of the exchange side stream into the step stream
 bool exchange_graph_ok(const sagips_ctx* c);
+bool exchange_outer_step(const sagips_ctx* c, uint64_t step);
 sagips_status exchange_join(sagips_ctx* c, cudaStream_t st);  // non-blocking: an error raised by an earlier wait
 void exchange_destroy(sagips_ctx* c);
 }  // namespace sagips

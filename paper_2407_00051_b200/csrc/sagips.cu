@@ -937,7 +937,8 @@ sagips_status sagips_train_step(sagips_ctx* ctx, uint64_t step, uint32_t flags, 
   // an executable graph is updated in place while the topology is unchanged
   // (host-input steps too: their staged inputs are copied into place by
   // memcpy nodes, whose source slot alternates -- an in-place update)
-  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx);
+  const bool graph = (flags & SAGIPS_STEP_GRAPH) && ctx->have_step && exchange_graph_ok(ctx) &&
+                     !exchange_outer_step(ctx, step);
   flags &= ~SAGIPS_STEP_GRAPH;
   if (!graph) return step_body(ctx, step, flags, stream);
   // captured on a library-owned stream (the caller's may be the legacy
