@@ -24,7 +24,7 @@ from oracle import mlp, proxy
 U32 = 2.0 ** -24
 C_BAND = 16.0
 BAND_FP32 = C_BAND * 2.0 ** -24          # CUDA-core fp32 dot products
-BAND_BF16X3 = 16.0 * 2.0 ** -16          # bf16x4 tensor-core layers: ~2^-15 per layer, accumulated over three layers, x2 slack
+BAND_BF16X3 = 16.0 * 2.0 ** -16          # bf16x3 tensor-core layers: ~2^-15 per layer, accumulated over three layers, x2 slack
 
 
 def _forward(Ws, bs, x, alpha, band_rel=BAND_FP32, x_dev=None):
