@@ -252,10 +252,9 @@ def layer_roofline(cfg, L, N, ctx, peaks, peak_src):
     mids = max(0, cfg.disc_depth - 3)
     # H_1 hi plane stored by the first forward pass and read back (split, SAGIPS_H1_STORE=1)
     h1 = Eh if (split and os.environ.get("SAGIPS_H1_STORE") == "1") else 0
-    # fp32-class fused D step: G_4 travels as dz + the Z_4 sign bits (20 B/row) and
-    # d_bwd_last regenerates its planes (kGenG; SAGIPS_GEN_G=0 writes the E-byte planes)
-    g4 = 20 if (split and os.environ.get("SAGIPS_FUSED", "1") != "0"
-                and os.environ.get("SAGIPS_GEN_G", "1") != "0") else E
+    # fused D step: G_4 travels as dz + the Z_4 sign bits (20 B/row) and d_bwd_last
+    # regenerates its planes (kGenG; SAGIPS_GEN_G=0 writes the E-byte planes)
+    g4 = 20 if (os.environ.get("SAGIPS_FUSED", "1") != "0" and os.environ.get("SAGIPS_GEN_G", "1") != "0") else E
     spec = {  # class: (rows, bytes/row, useful flops/row, executed flops/row, launches)
         "d_fwd_first": (rows_d, 8 + E + 16 + h1, G, px * G, 1),
         "d_fwd_mid": (rows_d, 2 * E + 16, G, px * G, mids),

@@ -828,11 +828,11 @@ int fused_grid(int64_t rows) {
 }
 
 void launch_dfwd(bool split, const DFwdArgs& a, cudaStream_t st) {
-  static bool configured[3] = {false, false, false};
+  static bool configured[4] = {false, false, false, false};
   const size_t smem = gstep_smem(split);
-  const bool gen = split && a.g4 == nullptr;
-  auto kern = gen ? k_dfwd<true, true> : split ? k_dfwd<true, false> : k_dfwd<false, false>;
-  const int ci = gen ? 2 : split ? 1 : 0;
+  const bool gen = a.g4 == nullptr;  // G_4 as dz + sign bits (the next pass regenerates it)
+  auto kern = split ? (gen ? k_dfwd<true, true> : k_dfwd<true, false>) : (gen ? k_dfwd<false, true> : k_dfwd<false, false>);
+  const int ci = 2 * (split ? 1 : 0) + (gen ? 1 : 0);
   if (!configured[ci]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured[ci] = true;

@@ -1000,7 +1000,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   // k_dfwd stored instead -- dz per row and the sign mask of Z_4:
   // G_4[r][c] = dz_r (Z_4[r][c] > 0 ? w_c : alpha w_c), 20 B/row instead of a
   // 512 B/row plane pair in HBM (written once, read once)
-  static_assert(!kGenG || (kSplit && !kFirst && kWgrad), "kGenG: split, non-first wgrad pass");
+  static_assert(!kGenG || (!kFirst && kWgrad), "kGenG: non-first wgrad pass");
   constexpr int P = kSplit ? 2 : 1;
   constexpr uint32_t TB = P * kPlane;
   constexpr bool kDy = kFirst && !kWgrad;
@@ -1020,7 +1020,13 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   constexpr int NP = kSplit ? 3 : 2;  // kT planes per tile: Gh (, Gl), Hh
   // operand area from sG: kT 5 plane slots (its staging area is free: no G_l
   // output); otherwise two stages and the epilogue staging
-  constexpr uint32_t kSlotArea = kT ? 5 * kPlane : 2 * TB + kEW * kStg;
+  // (bf16 kGenG: a second G stage after the staging, see g_stage; the
+  // allocation, bwd_smem, always has room for kT's five plane slots.  The
+  // loader-fed bf16 passes are at their HBM floor: a second stage there
+  // measured 2% slower at C5)
+  constexpr bool kG2 = kGenG && !kSplit;
+  constexpr uint32_t kSlotArea = kT ? 5 * kPlane : (kG2 ? 3 * TB : 2 * TB) + kEW * kStg;
+  static_assert(kSlotArea <= 5 * kPlane || !kG2, "bf16 kGenG: room for a second G stage");
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sW = smem;
   uint8_t* sG = sW + TB;     // G stage 0 (kPR: plane slots 0, 1)
@@ -1094,7 +1100,13 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
   const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
   auto tile_of = [&](int i) { return (int64_t)j + (int64_t)i * n; };
   // G stage of tile i: wgrad -> single stage; else a ring of 2 (sG, sH)
-  auto g_stage = [&](int i) -> uint8_t* { return (!kWgrad && (i & 1)) ? sH : sG; };
+  // bf16 kGenG (the H plane has sH): a second G stage past the staging, so
+  // tile i+1's G is generated during tile i's MMAs
+  uint8_t* sG2 = sStg + kEW * kStg;
+  auto g_stage = [&](int i) -> uint8_t* { return (i & 1) ? (kG2 ? sG2 : (!kWgrad ? sH : sG)) : sG; };
+  // stage / parity of tile i's G: one stage for the loader-fed wgrad pass, two otherwise
+  auto g_s = [&](int i) { return (kWgrad && !kG2) ? 0 : (i & 1); };
+  auto g_par = [&](int i) -> uint32_t { return (kWgrad && !kG2) ? (i & 1) : ((i >> 1) & 1); };
   // dynamic tile schedule (G step: no per-CTA partial sums): the loader takes
   // tiles from a global counter; MMA warp reads ids after the stage barrier,
   // the epilogue after tidbar (so its mask loads are issued early)
@@ -1140,7 +1152,6 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
         // (plane FIFO: Gh, Hh, Gl).  Each pass computes G_4 = dz (w or alpha
         // w) and its split afresh: no lo words held across the wait, and a
         // rolled 32-column loop keeps the kernel's code small
-        const PS gh = pl_gh(i), gl = pl_gl(i);
         const float2 dz2 = make_float2(dz, dz);
         auto gen_plane = [&](uint32_t base, bool lo_plane) {
 #pragma unroll 1
@@ -1161,16 +1172,26 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
               sts128(base + sw128_chunk(r, 4 * cb + jj, 128), v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
           }
         };
-        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
-        gen_plane(pl_addr(gh.slot), false);
-        fence_proxy_async_smem();
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
-        if (warp == 0 && lane == 0) mbar_arrive(&pfull[gh.slot]);
-        SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
-        gen_plane(pl_addr(gl.slot), true);
-        fence_proxy_async_smem();
-        asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
-        if (warp == 0 && lane == 0) mbar_arrive(&pfull[gl.slot]);
+        if constexpr (kSplit) {
+          const PS gh = pl_gh(i), gl = pl_gl(i);
+          SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gh.slot], (gh.use & 1) ^ 1));
+          gen_plane(pl_addr(gh.slot), false);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+          if (warp == 0 && lane == 0) mbar_arrive(&pfull[gh.slot]);
+          SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&pempty[gl.slot], (gl.use & 1) ^ 1));
+          gen_plane(pl_addr(gl.slot), true);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+          if (warp == 0 && lane == 0) mbar_arrive(&pfull[gl.slot]);
+        } else {  // bf16: the hi plane into G stage i % 2, in place of the loader's copy
+          const int gs = i & 1;
+          SAGIPS_TIMED(lane == 0 ? wa : WaitAcct{}, 4, mbar_wait(&emptyG[gs], ((i >> 1) & 1) ^ 1));
+          gen_plane(smem_u32(g_stage(i)), false);
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kPW) : "memory");
+          if (warp == 0 && lane == 0) mbar_arrive(&fullG[gs]);
+        }
       }
     }
     // ---------------- SIMT producers of H_1 planes (first layer, wgrad)
@@ -1264,7 +1285,7 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           t = tile_of(i);
         }
         if (!dyn && i + 1 < nmine) {
-          if (!a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
+          if (!kGenG && !a.g.slots) prefetch_l2(a.g.base + tile_of(i + 1) * TB, TB);
           if (kWgrad && !kFirst && !a.h.slots) prefetch_l2(a.h.base + tile_of(i + 1) * TB, TB);
         }
         if (kLoadH) {
@@ -1273,12 +1294,14 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
           mbar_arrive_expect_tx(&fullH[0], TB);
           bulk_g2s(smem_u32(sH), a.h.base + ring_slot(a.h, t) * TB, TB, &fullH[0]);
         }
-        const int s = kWgrad ? 0 : (i & 1);
-        const uint32_t ph = kWgrad ? ((i & 1) ^ 1) : (((i >> 1) & 1) ^ 1);
-        ring_wait_ready(a.g, t, wa);
-        SAGIPS_TIMED(wa, 1, mbar_wait(&emptyG[s], ph));
-        mbar_arrive_expect_tx(&fullG[s], TB);
-        bulk_g2s(smem_u32(g_stage(i)), a.g.base + ring_slot(a.g, t) * TB, TB, &fullG[s]);
+        if (!kGenG) {  // (kGenG: the producers write the G stage)
+          const int s = g_s(i);
+          const uint32_t ph = g_par(i) ^ 1u;
+          ring_wait_ready(a.g, t, wa);
+          SAGIPS_TIMED(wa, 1, mbar_wait(&emptyG[s], ph));
+          mbar_arrive_expect_tx(&fullG[s], TB);
+          bulk_g2s(smem_u32(g_stage(i)), a.g.base + ring_slot(a.g, t) * TB, TB, &fullG[s]);
+        }
         trace_pt(trace, j, i, 0);
       }
     }
@@ -1421,8 +1444,8 @@ __device__ __forceinline__ void bwd_body(const BwdLaunch& a, int j, int n, unsig
       }
       for (int i = 0; !kPR && (dyn || i < nmine); ++i) {
         const int b = i & 1;
-        const int s = kWgrad ? 0 : (i & 1);
-        SAGIPS_TIMED(wq, 2, mbar_wait(&fullG[s], kWgrad ? (i & 1) : ((i >> 1) & 1)));
+        const int s = g_s(i);
+        SAGIPS_TIMED(wq, 2, mbar_wait(&fullG[s], g_par(i)));
         const int64_t t = dyn ? (int64_t)sTile[i & 7] : tile_of(i);
         if (t < 0) break;  // sentinel (the epilogue stops at its own tidbar)
         if (lane == 0) ring_consumed(a.g, t);
@@ -1838,6 +1861,7 @@ static void configure_layers() {
 #undef SAGIPS_BWD
   allow_smem(k_bwd<true, true, true, true>, bwd_smem(true));
   allow_smem(k_bwd<true, false, true, false, true>, bwd_smem(true));
+  allow_smem(k_bwd<false, false, true, false, true>, bwd_smem(false));
   allow_smem(k_bwd<false, true, true, true>, bwd_smem(false));
 }
 
@@ -1912,7 +1936,7 @@ void launch_tc_bwd(bool split, bool first, bool wgrad, const BwdLaunch& L, cudaS
   const size_t sm = bwd_smem(split);
   const bool h1load = first && wgrad && L.h.base != nullptr;
 #define SAGIPS_BWD_LAUNCH(S)                                                                   \
-  if (S && !first && wgrad && L.gen_dz) k_bwd<true, false, true, false, true><<<grid, kThreads, sm, st>>>(L, tr); \
+  if (!first && wgrad && L.gen_dz) k_bwd<S, false, true, false, true><<<grid, kThreads, sm, st>>>(L, tr);       \
   else if (!first && wgrad) k_bwd<S, false, true><<<grid, kThreads, sm, st>>>(L, tr);          \
   else if (h1load) k_bwd<S, true, true, true><<<grid, kThreads, sm, st>>>(L, tr);              \
   else if (first && wgrad) k_bwd<S, true, true><<<grid, kThreads, sm, st>>>(L, tr);            \

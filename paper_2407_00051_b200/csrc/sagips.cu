@@ -506,11 +506,11 @@ static bool h1_store() {
 static bool use_fused(const sagips_ctx* c);
 static bool tc_split(const sagips_ctx* c);
 static bool h1_store();
-// the fused D step passes G_4 as dz + sign bits (kGenG; default for
-// fp32-class, SAGIPS_GEN_G=0 writes the planes instead)
+// the fused D step passes G_4 as dz + sign bits (kGenG; the default, both
+// precisions; SAGIPS_GEN_G=0 writes the planes instead)
 static bool gen_g(const sagips_ctx* c) {
   const char* e = getenv("SAGIPS_GEN_G");
-  return !(e && e[0] == '0') && tc_split(c) && use_fused(c) && !h1_store();
+  return !(e && e[0] == '0') && use_fused(c) && !h1_store();
 }
 
 static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t n_real, float label_rest,

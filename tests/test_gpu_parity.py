@@ -183,7 +183,7 @@ def test_step_paper_widths_ragged(impl, fused_env):
                               disc_impl=impl), t=3, disc_band=kink.BAND_BF16X3 if impl == 0 else kink.BAND_FP32)
 
 
-@pytest.mark.parametrize("fused_env", ["1", "0"], indirect=True)
+@pytest.mark.parametrize("fused_env", ["1", "1p", "0"], indirect=True)
 def test_bf16_step_elementwise(fused_env):
     """SAGIPS_PREC_BF16 (C5's precision): discriminator GEMMs in bf16 with fp32
     accumulation, at 2N = 2^18 rows.  Every element of dW_D, db_D, dy, draw,
