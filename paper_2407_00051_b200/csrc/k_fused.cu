@@ -41,6 +41,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 #include "ctx.h"
 #include "tc_util.cuh"
@@ -144,6 +145,26 @@ constexpr bool kPrefetchX = false;
 #else
 constexpr bool kPrefetchX = true;
 #endif
+
+// SAGIPS_FUSED_TRACE: per-CTA stamps after the phase stamps, [kernel][256 CTAs][4]:
+// kernel entry, weights staged, tile loop done, SM id (globaltimer ns)
+constexpr size_t kFTracePhaseWords = 2 * 2 * 64 * 6 * 4;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_stamp(unsigned long long* trace, int kern, int k) {
+  if (trace && threadIdx.x == 0 && blockIdx.x < 256) {
+    unsigned long long* c = trace + kFTracePhaseWords + ((size_t)kern * 256 + blockIdx.x) * 4;
+    c[k] = gtimer();
+    if (k == 0) {
+      unsigned int sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      c[3] = sm;
+    }
+  }
+}
 
 // named barrier of one slot group (8 warps)
 __device__ __forceinline__ void group_sync(int s) {
@@ -255,6 +276,7 @@ __device__ __forceinline__ void issue_layer(uint32_t acc, uint32_t wbase, int p)
 template <bool kSplit>
 __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ GStepArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  cta_stamp(a.trace, 0, 0);
   constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
   SmemVec* sv = reinterpret_cast<SmemVec*>(smem + 3 * TBw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -279,6 +301,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sv->tmem;
+  cta_stamp(a.trace, 0, 1);
   const int64_t ntiles = (a.rows + 127) / 128;
   const int j = blockIdx.x, n = gridDim.x;
   const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
@@ -475,6 +498,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
       }
     }
   }
+  cta_stamp(a.trace, 0, 2);
   // this CTA's loss partial (fp64), warps in order
 #pragma unroll
   for (int w = 16; w >= 1; w >>= 1) lacc += __shfl_xor_sync(0xffffffffu, lacc, w);
@@ -507,6 +531,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
 template <bool kSplit, bool kGenOut>
 __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ DFwdArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  cta_stamp(a.trace, 1, 0);
   constexpr uint32_t TBw = (kSplit ? 2 : 1) * kPlaneF;
   constexpr int64_t TB = (kSplit ? 2 : 1) * (int64_t)kPlaneF;  // HBM plane tile
   SmemVec* sv = reinterpret_cast<SmemVec*>(smem + 3 * TBw);
@@ -532,6 +557,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sv->tmem;
+  cta_stamp(a.trace, 1, 1);
   const int64_t ntiles = (a.rows + 127) / 128;
   const int j = blockIdx.x, n = gridDim.x;
   const int nmine = ntiles > j ? (int)((ntiles - 1 - j) / n + 1) : 0;
@@ -724,6 +750,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     stamp(3, 2);
     stamp(3, 3);
   }
+  cta_stamp(a.trace, 1, 2);
   // per-CTA partials in a fixed order: head gradient [128] + bias, loss (fp64)
 #pragma unroll
   for (int w = 16; w >= 1; w >>= 1) {
@@ -769,15 +796,15 @@ unsigned long long* fused_trace_buffer() {
     const char* e = getenv("SAGIPS_FUSED_TRACE");
     on = (e && e[0] == '1') ? 1 : 0;
     if (on) {
-      cudaMalloc(&g_ftrace, sizeof(unsigned long long) * 2 * 2 * 64 * 6 * 4);
-      cudaMemset(g_ftrace, 0, sizeof(unsigned long long) * 2 * 2 * 64 * 6 * 4);
+      cudaMalloc(&g_ftrace, sizeof(unsigned long long) * (kFTracePhaseWords + 2 * 256 * 4));
+      cudaMemset(g_ftrace, 0, sizeof(unsigned long long) * (kFTracePhaseWords + 2 * 256 * 4));
     }
   }
   return g_ftrace;
 }
 void fused_trace_report() {
   if (!g_ftrace) return;
-  std::vector<unsigned long long> h(2 * 2 * 64 * 6 * 4);
+  std::vector<unsigned long long> h(kFTracePhaseWords + 2 * 256 * 4);
   cudaDeviceSynchronize();
   cudaMemcpy(h.data(), g_ftrace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
   // per phase: epilogue (previous accumulator ready -> this warp done), waiting
@@ -807,6 +834,28 @@ void fused_trace_report() {
       if (cnt[p])
         fprintf(stderr, "  phase %d: %7.0f | %6.0f | %6.0f | %6.0f  (%d samples)\n", p, acc[p][0] / cnt[p],
                 acc[p][1] / cnt[p], acc[p][2] / cnt[p], acc[p][3] / cnt[p], cnt[p]);
+    // per-CTA timeline of the last traced launch: prologue, tile loop end spread
+    const unsigned long long* C = h.data() + kFTracePhaseWords + (size_t)kern * 256 * 4;
+    std::vector<double> pro, loop_end;
+    unsigned long long t0 = ~0ull;
+    for (int c = 0; c < 256; ++c)
+      if (C[c * 4] && C[c * 4] < t0) t0 = C[c * 4];
+    int slowest = -1;
+    double worst = 0;
+    for (int c = 0; c < 256; ++c) {
+      if (!C[c * 4] || !C[c * 4 + 2]) continue;
+      pro.push_back((double)(C[c * 4 + 1] - C[c * 4]) * 1e-3);
+      const double e = (double)(C[c * 4 + 2] - t0) * 1e-3;
+      loop_end.push_back(e);
+      if (e > worst) { worst = e; slowest = (int)C[c * 4 + 3]; }
+    }
+    if (!loop_end.empty()) {
+      std::sort(pro.begin(), pro.end());
+      std::sort(loop_end.begin(), loop_end.end());
+      const size_t n = loop_end.size();
+      fprintf(stderr, "  %zu CTAs: prologue %.2f us (median), tile loop done at %.1f / %.1f / %.1f us (min / median / max; slowest on SM %d)\n",
+              n, pro[n / 2], loop_end[0], loop_end[n / 2], loop_end[n - 1], slowest);
+    }
   }
 }
 
