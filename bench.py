@@ -136,14 +136,17 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- configs
+WORKLOAD_C2 = ("C2: paper MLPs G[6,128x4,6] D[2,128x4,1] (51,206/50,049 params), k=1024 m=1024 "
+               "(2^20 events/rank/step), fp32")
+
+
 def lib_config(args, L, rank, world):
     if args.config == "c1":
         cfg = L.config_init(L.PRESET_DESK)
         workload = "C1: 1 rank desk MLPs G[8,64,64,6] D[2,64,64,1], k=64 m=16 (1024 events/step), fp32"
     else:
         cfg = L.config_init(L.PRESET_PAPER)
-        workload = ("C2: paper MLPs G[6,128x4,6] D[2,128x4,1] (51,206/50,049 params), k=1024 m=1024 "
-                    "(2^20 events/rank/step), fp32")
+        workload = WORKLOAD_C2
         if args.config == "c5":
             cfg.events_per_sample = 16384
             cfg.reference_rows = 2 * 1024 * 16384
@@ -224,7 +227,8 @@ def reference_arm(args):
             "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (counter-based Philox, DESIGN.md input recipe)",
-            "config": {"workload": "C2 sample: paper MLPs, k=16 m=1024 per step (oracle, CPU)"},
+            "config": {"workload": WORKLOAD_C2,
+                       "sample": "each step a bounded sample of it: k=16 m=1024 (2^14 events) through the oracle, CPU"},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
