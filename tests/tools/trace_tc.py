@@ -24,10 +24,16 @@ ctx.train_step(1, 0, sp)
 tr, ctas = L.debug_trace(with_ctas=True)
 tr = tr.astype(np.int64)
 ctas = ctas.astype(np.int64)
-names = ["fwd-first", "fwd-mid", "fwd-head", "bwd-L3", "bwd-L2", "bwd-L1", "G fwd-first", "G fwd-mid", "G fwd-head",
-         "G bwd-L3", "G bwd-L2", "G bwd-dy"]
-g0 = min(int(tr[li, 0][tr[li, 0][:, 0] > 0, 0].min()) for li in range(12) if (tr[li, 0][:, 0] > 0).sum() >= 3)
-for li in range(12):
+# launch order of the traced tensor-core layer kernels (k_tc_layers.cu): with the
+# fused kernels (default) only the D step's three backward passes; with
+# SAGIPS_FUSED=0 all twelve layer passes
+if os.environ.get("SAGIPS_FUSED", "1") != "0":
+    names = ["d_bwd_last", "d_bwd_mid", "d_bwd_first"]
+else:
+    names = ["fwd-first", "fwd-mid", "fwd-head", "bwd-L3", "bwd-L2", "bwd-L1", "G fwd-first", "G fwd-mid",
+             "G fwd-head", "G bwd-L3", "G bwd-L2", "G bwd-dy"]
+g0 = min(int(tr[li, 0][tr[li, 0][:, 0] > 0, 0].min()) for li in range(len(names)) if (tr[li, 0][:, 0] > 0).sum() >= 3)
+for li in range(len(names)):
     t = tr[li, 0]
     n = int((t[:, 0] > 0).sum())
     if n < 3:
@@ -60,32 +66,3 @@ for li in range(12):
         q = np.percentile((en - st.min()) / 1e3, [0, 10, 50, 90, 100])
         print(f"{'':12s} CTA end percentiles (us): " + " ".join(f"{v:.0f}" for v in q))
 
-
-def pipe_split(dstep, sms=148):
-    """mirror of pipe_split() in sagips.cu (default costs)"""
-    env = os.environ.get("SAGIPS_PIPE_SPLIT_D" if dstep else "SAGIPS_PIPE_SPLIT_G")
-    if env:
-        return [int(x) for x in env.split(",")]
-    cost = [3.3, 3.3, 3.9, 3.9, 3.9, 3.9] if dstep else [3.0, 2.8, 2.8, 2.4, 2.4, 1.4]
-    tot = sum(cost)
-    c = [max(1, int(sms * x / tot)) for x in cost]
-    r = 0
-    while sum(c) < sms:
-        c[r] += 1
-        r = (r + 1) % 6
-    return c
-
-
-if os.environ.get("SAGIPS_PIPE", "0") != "0":
-    roles = ["first", "mid", "head", "bwd3", "bwd2", "bwd1"]
-    cols = ["ld-up", "ld-stage", "mma-data", "mma-acc", "epi-slot", "epi-acc", "epi-mask", "wall"]
-    for dstep, slot in ((True, 31), (False, 30)):
-        w = tr[slot].reshape(-1)[:148 * 8].reshape(148, 8) / 1e3  # us
-        split = pipe_split(dstep)
-        print(("D" if dstep else "G") + " step waits (us, mean over the role's CTAs): split", split)
-        print("      " + " ".join(f"{c:>9s}" for c in cols))
-        b = 0
-        for r, n in enumerate(split):
-            m = w[b:b + n].mean(axis=0)
-            b += n
-            print(f"{roles[r]:6s}" + " ".join(f"{x:9.1f}" for x in m))
