@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(256) k_reduce_adam(const __grid_constant__ Red
   const int j = (blockIdx.x - sg.block0) * 32 + jl;
   float s = 0.f;
   if (j < sg.n) {
-#pragma unroll 4
+#pragma unroll 8  // (more loads in flight; the sum order is unchanged)
     for (int p = grp; p < sg.nparts; p += 8) s += __ldg(sg.part + (int64_t)p * sg.ld + j);
   }
   red[grp][jl] = s;

@@ -24,6 +24,7 @@ constexpr int kGenMaxW = 128; // widest layer these kernels handle
 constexpr int kGenThreads = 256;
 static_assert(kR == 8 && kGenThreads == 2 * kGenMaxW, "the 128 x 128 fast paths map 256 threads to 2 x 4 rows");
 constexpr int kGenSplits = 8;  // wgrad: row splits (one partial each, reduced in a fixed order)
+constexpr size_t kGenSmemMax = 227 * 1024;  // dynamic shared memory cap (all-layer weight staging)
 
 __device__ __forceinline__ float lrelu_g(float z, float a) { return z > 0.f ? z : z * a; }
 }  // namespace
@@ -59,7 +60,37 @@ struct GenArgs {
   int64_t prefetch_bytes;
   uint32_t* zero_hist;
   int zero_words;
+  // every layer's weights staged up front (cp.async, one group per layer in
+  // use order) when they fit in shared memory: ws_off[l] = float offset of
+  // layer l's copy after the row buffers; preload = 0 stages layer by layer
+  int preload;
+  int ws_off[kMaxLayers];
+  int ws_off_b[kMaxLayers];  // the dgrad's plain [out][in] copies (layers last .. 1)
 };
+
+// ---------------------------------------------------------------- async staging
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// wait until at most n groups are pending (n is a small run-time count)
+__device__ __forceinline__ void cp_async_wait(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.wait_group 6;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 7;" ::: "memory"); break;
+  }
+}
 
 // ---------------------------------------------------------------- forward
 // Each layer's W is staged in shared memory, then each output accumulates its
@@ -72,7 +103,7 @@ constexpr int kLdFast = kGenMaxW + 4;
 __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__ GenArgs a) {
   extern __shared__ __align__(16) float gsm[];
   float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
-  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][ld]
+  float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][ld] (preload: base)
   const int tid = threadIdx.x;
   const int r0 = blockIdx.x * kR;
   const int in0 = a.sizes[0];
@@ -84,6 +115,20 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
   }
   if (a.zero_hist && blockIdx.x == 0)
     for (int i = tid; i < a.zero_words; i += kGenThreads) a.zero_hist[i] = 0u;
+  if (a.preload) {  // every layer's weights, layer order, one cp.async group each (same padded layouts)
+    for (int l = 0; l < a.L; ++l) {
+      const int in = a.sizes[l], out = a.sizes[l + 1];
+      const float* W = a.W + a.w_off[l];
+      float* dst = Ws + a.ws_off[l];
+      if (in == kGenMaxW && out == kGenMaxW) {
+        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenThreads)
+          cp_async16(dst + (idx >> 5) * kLdFast + 4 * (idx & 31), W + 4 * idx);
+      } else {
+        for (int idx = tid; idx < out * in; idx += kGenThreads) cp_async4(dst + (idx / in) * (in + 1) + idx % in, W + idx);
+      }
+      cp_async_commit();
+    }
+  }
   for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
     const int r = idx / in0, i = idx % in0;
     buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
@@ -94,8 +139,15 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
     const int ld = fast ? kLdFast : in + 1;
     const float* W = a.W + a.w_off[l];
     const float* bias = a.B + a.b_off[l];
-    __syncthreads();  // previous layer done with Ws / buf
-    if (fast) {
+    if (a.preload) {
+      cp_async_wait(a.L - 1 - l);  // this thread's copies of layers 0..l have landed
+      __syncthreads();             // everyone's; and the previous layer is done with buf
+      Ws = gsm + 2 * kR * kGenMaxW + a.ws_off[l];
+    } else {
+      __syncthreads();  // previous layer done with Ws / buf
+    }
+    if (a.preload) {
+    } else if (fast) {
       float4 v[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
@@ -163,6 +215,19 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
   const int r0 = blockIdx.x * kR;
   const int last = a.L - 1;
   const int outL = a.sizes[a.L];
+  if (a.preload) {  // every layer's weights (use order: last .. 1), one cp.async group each, plain layout
+    for (int l = last; l >= 1; --l) {
+      const int in = a.sizes[l], out = a.sizes[l + 1];
+      const float* W = a.W + a.w_off[l];
+      float* dst = Ws + a.ws_off_b[l];
+      if (in == kGenMaxW && out == kGenMaxW) {
+        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenThreads) cp_async16(dst + 4 * idx, W + 4 * idx);
+      } else {
+        for (int idx = tid; idx < out * in; idx += kGenThreads) cp_async4(dst + idx, W + idx);
+      }
+      cp_async_commit();
+    }
+  }
   for (int idx = tid; idx < kR * outL; idx += kGenThreads) {
     const int r = idx / outL, o = idx % outL;
     buf[last & 1][r][o] = (r0 + r < a.k) ? a.dz[last][(int64_t)(r0 + r) * outL + o] : 0.f;
@@ -171,8 +236,15 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
     const int in = a.sizes[l], out = a.sizes[l + 1];
     const bool fast = in == kGenMaxW && out == kGenMaxW;
     const float* W = a.W + a.w_off[l];
-    __syncthreads();  // previous layer done with Ws / buf
-    if (fast) {
+    if (a.preload) {
+      cp_async_wait(l - 1);  // groups of layers last .. l have landed (l - 1 younger ones may be pending)
+      __syncthreads();
+      Ws = gsm + 2 * kR * kGenMaxW + a.ws_off_b[l];
+    } else {
+      __syncthreads();  // previous layer done with Ws / buf
+    }
+    if (a.preload) {
+    } else if (fast) {
       float4 v[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
@@ -351,10 +423,37 @@ static GenArgs gen_args(sagips_ctx* c) {
   while (splits > 1 && (int64_t)splits * (a.wtot + a.btot) > c->part_floats) splits >>= 1;
   a.split_rows = ((a.k + splits - 1) / splits + 31) / 32 * 32;
   a.part = c->part;
+  // all layers' weights in shared memory at once when they fit (the forward's
+  // padded layout; the dgrad's plain one is no larger)
+  int off = 0;
+  bool aligned = true;
+  for (int l = 0; l < G.L; ++l) {
+    const bool fast = G.sizes[l] == kGenMaxW && G.sizes[l + 1] == kGenMaxW;
+    a.ws_off[l] = off;
+    off += ((fast ? kGenMaxW * kLdFast : G.sizes[l + 1] * (G.sizes[l] + 1)) + 3) / 4 * 4;
+    if (fast && (G.w_off[l] % 4) != 0) aligned = false;
+  }
+  a.preload = (aligned && G.L <= 8 && sizeof(float) * (2 * kR * kGenMaxW + off) <= kGenSmemMax) ? 1 : 0;
+  int offb = 0;
+  for (int l = G.L - 1; l >= 1; --l) {
+    a.ws_off_b[l] = offb;
+    offb += (G.sizes[l + 1] * G.sizes[l] + 3) / 4 * 4;
+  }
   return a;
 }
 
-static size_t gen_fwd_smem() { return sizeof(float) * (2 * kR * kGenMaxW + kGenMaxW * kLdFast); }
+static size_t gen_smem(const GenArgs& a) {
+  size_t w = (size_t)kGenMaxW * kLdFast;
+  if (a.preload) {
+    w = 0;
+    for (int l = 0; l < a.L; ++l) {
+      const bool fast = a.sizes[l] == kGenMaxW && a.sizes[l + 1] == kGenMaxW;
+      w = (size_t)a.ws_off[l] + ((fast ? kGenMaxW * kLdFast : a.sizes[l + 1] * (a.sizes[l] + 1)) + 3) / 4 * 4;
+    }
+  }
+  return sizeof(float) * (2 * kR * kGenMaxW + w);
+}
+static size_t gen_fwd_smem() { return kGenSmemMax; }  // the attribute: the largest launch
 
 void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_t prefetch_bytes,
                     uint32_t* zero_hist, int zero_words) {
@@ -368,7 +467,7 @@ void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_
   a.prefetch_bytes = (prefetch_bytes / 16) * 16;
   a.zero_hist = zero_hist;
   a.zero_words = zero_words;
-  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
   count_launch();
 }
 
@@ -382,7 +481,7 @@ void launch_gen_predict(sagips_ctx* c, const float* noise, int k, float* c_out, 
   a.noise = noise;
   a.k = k;
   a.cbuf = c_out;
-  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
   count_launch();
 }
 
@@ -393,7 +492,7 @@ void launch_gen_bwd(sagips_ctx* c, cudaStream_t st) {
     configured = true;
   }
   const GenArgs a = gen_args(c);
-  k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenThreads, gen_fwd_smem(), st>>>(a);
+  k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
   count_launch();
   const int splits = (a.k + a.split_rows - 1) / a.split_rows;
   k_gen_wgrad<<<dim3(a.tile_base[a.L], splits), kGenThreads, 0, st>>>(a);
