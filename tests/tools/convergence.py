@@ -33,7 +33,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--steps", type=int, default=400)
     p.add_argument("--every", type=int, default=10)
-    p.add_argument("--mode", choices=["rma", "arar", "arar-arar", "sync", "none"], default="rma")
+    p.add_argument("--mode", choices=["rma", "rma-ag", "rma-chunked", "arar", "arar-arar", "sync", "none"], default="rma")
     p.add_argument("--group-size", type=int, default=0)
     p.add_argument("--staleness", type=int, default=1)
     p.add_argument("--outer-every", type=int, default=10)
@@ -46,8 +46,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR,
-             "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
+    modes = {"rma": L.MODE_RMA_ARAR_ARAR, "rma-ag": L.MODE_RMA_ALLGATHER, "rma-chunked": L.MODE_RMA_CHUNKED,
+             "arar": L.MODE_ARAR, "arar-arar": L.MODE_ARAR_ARAR, "sync": L.MODE_SYNC_ALLREDUCE, "none": L.MODE_NONE}
     cfg = L.config_init(L.PRESET_PAPER)
     m = a.events_per_sample
     cfg.events_per_sample = m
@@ -58,7 +58,7 @@ def main():
     cfg.mode = modes[a.mode] if world > 1 else L.MODE_NONE
     cfg.group_size = a.group_size if (a.group_size and world > 1) else world
     cfg.outer_every = a.outer_every
-    cfg.staleness = a.staleness if (world > 1 and a.mode != "sync") else 0
+    cfg.staleness = a.staleness if (world > 1 and a.mode not in ("sync", "rma-chunked")) else 0
     ctx = runtime.make_context(cfg)
     if world > 1:
         runtime.connect(ctx)
