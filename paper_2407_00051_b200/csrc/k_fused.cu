@@ -166,6 +166,15 @@ __device__ __forceinline__ void cta_stamp(unsigned long long* trace, int kern, i
   }
 }
 
+// L2 prefetch of rows [r0, r0 + n) of a float2 array: the bulk prefetch needs
+// 16-byte aligned addresses and sizes, and the fake rows (X + 2N floats) are
+// only 8-byte aligned when N is odd -- prefetch the aligned interior
+__device__ __forceinline__ void prefetch_rows(const float2* base, int64_t r0, int64_t n) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(base + r0);
+  const uintptr_t s0 = (b + 15) & ~(uintptr_t)15, e0 = (b + (uintptr_t)n * 8) & ~(uintptr_t)15;
+  if (e0 > s0) prefetch_l2(reinterpret_cast<const void*>(s0), (uint32_t)(e0 - s0));
+}
+
 // named barrier of one slot group (8 warps)
 __device__ __forceinline__ void group_sync(int s) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + s), "n"(32 * kGroupWarps) : "memory");
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_gstep(const __grid_constant__ 
     const float2 x = valid ? __ldg(a.Y + row) : make_float2(0.f, 0.f);
     if (kPrefetchY && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
       const int64_t r0 = (int64_t)(j + (int64_t)(i + 2) * n) * 128;
-      prefetch_l2(a.Y + r0, (uint32_t)((a.rows - r0 < 128 ? a.rows - r0 : 128) * 8) & ~15u);
+      prefetch_rows(a.Y, r0, a.rows - r0 < 128 ? a.rows - r0 : 128);
     }
     uint32_t m1[2], m2[2], m3[2];  // LeakyReLU' sign bits of Z_1..Z_3 (two 32-column chunks)
     // H_1 = LeakyReLU(fma(x0, w0x, fma(x1, w0y, b0)))  (the per-layer kernels' order)
@@ -613,7 +622,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) k_dfwd(const __grid_constant__ D
     const float2 x = valid ? __ldg(a.X + row) : make_float2(0.f, 0.f);
     if (kPrefetchX && w8 == 0 && lane == 0 && i + 2 < nmine) {  // this slot's next tile's rows into L2
       const int64_t r0 = (t + 2 * (int64_t)n) * 128;
-      prefetch_l2(a.X + r0, (uint32_t)((a.rows - r0 < 128 ? a.rows - r0 : 128) * 8) & ~15u);
+      prefetch_rows(a.X, r0, a.rows - r0 < 128 ? a.rows - r0 : 128);
     }
     {  // H_1
       const float2 X0 = make_float2(x.x, x.x), X1 = make_float2(x.y, x.y);
