@@ -34,8 +34,31 @@ from oracle import mlp, proxy
 
 U_BF16 = 2.0 ** -8
 VAR2 = 2.0 * U_BF16 ** 2 / 3.0   # variance of a product of two rounded operands (relative^2)
-C2U = 2.01 * U_BF16              # worst case of that product's relative error
+C2U = 2.01 * U_BF16              # worst case of that product's relative error (the wgrad's G^T h)
+U_DB = U_BF16                    # the bias gradient's operand (G)
 C_SIGMA = 6.0
+SCHEME = "bf16"
+
+
+def use_scheme(scheme):
+    """'bf16' (SAGIPS_PREC_BF16, the default) or 'split' (SAGIPS_PREC_FP32 on
+    the tensor cores, R28): every forward / dgrad operand x = hi + lo with
+    |x - hi - lo| <= 2^-18 |x| and the lo x lo product dropped -- a product's
+    relative error below 3 2^-18, modelled as u = 2^-16 per operand -- while
+    the wgrad multiplies the split G by the hi plane of H only (relative
+    error 2^-9, taken as 2^-8) and the bias gradient sums the split G."""
+    global U_BF16, VAR2, C2U, U_DB, SCHEME
+    if scheme == "bf16":
+        U_BF16 = 2.0 ** -8
+        C2U = 2.01 * U_BF16
+    elif scheme == "split":
+        U_BF16 = 2.0 ** -16
+        C2U = 1.01 * 2.0 ** -8
+    else:
+        raise ValueError(scheme)
+    VAR2 = 2.0 * U_BF16 ** 2 / 3.0
+    U_DB = U_BF16
+    SCHEME = scheme
 
 
 def _is_bf16(Ws, l):
@@ -100,7 +123,7 @@ def backward_bounds(Ws, cache, vz, vh, dout, vdout, alpha, kink_mode=0, bf16=Tru
         edWs[l] = sdz.T @ np.abs(h) + (C2U * (np.abs(dz).T @ np.abs(h)) if bf else 0.0)
         if vh is not None:
             edWs[l] = edWs[l] + np.abs(dz).T @ (C_SIGMA * np.sqrt(vh[l]))
-        edbs[l] = sdz.sum(axis=0) + (U_BF16 * np.abs(dz).sum(axis=0) if bf else 0.0)
+        edbs[l] = sdz.sum(axis=0) + (U_DB * np.abs(dz).sum(axis=0) if bf else 0.0)
         W2 = Ws[l] ** 2
         g = dz @ Ws[l]
         v = vdz @ W2 + (VAR2 * ((dz * dz) @ W2) if bf else 0.0)
