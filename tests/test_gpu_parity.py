@@ -398,6 +398,62 @@ def test_full_size_paper_step_sampled():
                       outliers=idx.size * 2 // 400)
 
 
+def test_max_size_fp32_step_sampled_rows():
+    """The largest configuration (C5's size: k = 1,024, m = 16,384, N = 2^24,
+    2N = 2^25 rows) through the fp32-class fused kernels, checked row by row
+    where the oracle can compute one row alone (the full oracle step does not
+    fit here): the generator's c; for 4,096 sampled events (incl. the first,
+    the last and sample boundaries) the bootstrap index, the real row and
+    the fake event (bit-exact / 1e-5), the D logits of both rows from the
+    GPU's own rows and the pre-step D, and the G step's logit and dy through
+    the GPU's updated D (1e-4 / 1e-3 with the R24 floor and R27 outliers)."""
+    L = lib()
+    k, m = 1024, 16384
+    N = k * m
+    cfg = L.config_init(1, seed=6, param_samples=k, events_per_sample=m, reference_rows=2 * N, shard_rows=N)
+    ctx = make_ctx(cfg)
+    ocfg = oracle_config(cfg)
+    st = gan.RankState(oracle_config(L.config_init(1, seed=6)), 0)  # same seed and model: same initial weights
+    sync_params(ctx, st)
+    d0 = ([w.copy() for w in st.dW], [b.copy() for b in st.db])
+    ctx.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    a = ocfg.leaky_slope
+    raw, _ = mlp.forward(st.gW, st.gb, gan.noise(ocfg, 0, 0), a)
+    c = proxy.constrain(raw).reshape(k, 2, 3)
+    assert_rel(ctx.get(L.T_C).reshape(k, 2, 3), c, 1e-5, 1e-6, "constrained parameters c")
+    idx = np.unique(np.concatenate([[0, 1, m - 1, m, N // 2, N - 2, N - 1], inputs.sample_indices(6, N, 4096)]))
+    seed = ocfg.seed
+    u = np.stack([px.uniform_open01(px.words(seed, px.STREAM_FAKE, 0, 0, 2 * int(e), 2)) for e in idx])
+    s_of = idx // m
+    y = np.stack([proxy.quantile(u[:, o], c[s_of, o, 0], c[s_of, o, 1], c[s_of, o, 2]) for o in range(2)], axis=1)
+    ridx = np.array([proxy.lemire_index(px.words(seed, px.STREAM_REAL, 0, 0, int(e), 1), N)[0] for e in idx])
+    sidx = np.array([proxy.lemire_index(px.words(seed, px.STREAM_SHARD, 0, 0, int(j), 1), 2 * N)[0] for j in ridx])
+    uref = np.stack([px.uniform_open01(px.words(seed, px.STREAM_REF, 0, 0, 2 * int(r), 2)) for r in sidx])
+    x32 = proxy.sample_events_f32(np.repeat(np.asarray(ocfg.true_params, dtype=np.float32).reshape(1, 6), idx.size, axis=0),
+                                  1, uref)
+    ev = ctx.get(L.T_EVENTS).reshape(-1, 2)
+    assert np.array_equal(ctx.get(L.T_REAL_IDX)[idx], ridx.astype(np.uint32)), "bootstrap indices"
+    assert np.array_equal(ev[idx], x32), "real rows"
+    assert_rel(ev[N + idx], y, 1e-5, 1e-5, "fake events")
+    # the D step's logits of the sampled real and fake rows (the GPU's rows, the pre-step D)
+    rows = np.concatenate([idx, N + idx])
+    zD, _ = mlp.forward(d0[0], d0[1], ev[rows].astype(np.float64), a)
+
+    def logits_close(gpu, ref, what):  # 1e-4; up to 0.1% of the rows within 10x (a LeakyReLU decision, R27)
+        ratio = np.abs(np.asarray(gpu, dtype=np.float64) - ref) / (1e-4 + 1e-4 * np.abs(ref))
+        bad = np.flatnonzero(ratio > 1)
+        assert bad.size <= ratio.size // 1000 and ratio.max() <= 10, f"{what}: {bad.size} rows, worst {ratio.max():.3g}"
+    logits_close(ctx.get(L.T_LOGITS_D)[rows], zD[:, 0], "D logits (sampled rows)")
+    # the G step through the GPU's updated D: logit and dy of each sampled fake row
+    gpu_d = (unflat(ctx.get(L.T_DISC_W), st.dW), unflat(ctx.get(L.T_DISC_B), st.db))
+    zG, cache = mlp.forward(gpu_d[0], gpu_d[1], ev[N + idx].astype(np.float64), a)
+    logits_close(ctx.get(L.T_LOGITS_G)[idx], zG[:, 0], "G logits (sampled rows)")
+    dzG = (mlp.sigmoid(zG[:, 0]) - 1.0) / N
+    _, _, dy = mlp.backward(gpu_d[0], cache, dzG[:, None], a)
+    assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], dy, 1e-3, "dy (sampled rows)",
+                      outliers=idx.size * 2 // 400)
+
+
 def test_step_is_deterministic():
     """Two contexts from the same state produce bit-identical losses,
     gradients, events and parameters (fixed-order reductions everywhere; the
