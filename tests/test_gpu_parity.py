@@ -36,23 +36,27 @@ def make_ctx(cfg):
 
 
 # ---------------------------------------------------------------- sampler
-@pytest.mark.parametrize("k,m", [(1, 1), (3, 5), (64, 16), (7, 1023), (1024, 1024)])
-def test_sample_events_parity(k, m):
+@pytest.mark.parametrize("k,m,bins", [(1, 1, 64), (3, 5, 64), (64, 16, 64), (7, 1023, 64), (1024, 1024, 64),
+                                       (64, 16, 1), (7, 1023, 200), (1024, 1024, 200), (1024, 1024, 0)])
+def test_sample_events_parity(k, m, bins):
+    """bins 200: the shared histograms no longer fit the lane-column layout
+    (one copy per block instead); bins 0: no histogram (hist = NULL)."""
     L = lib()
     seed, step, rank = 0xC0FFEE12345678, 123457, 3
     c32 = inputs.coefficients(k * 31 + m, k).astype(np.float32)
     c_t = torch.tensor(c32, device="cuda")
     ev = torch.empty(k * m * 2, dtype=torch.float32, device="cuda")
-    bins = 64
-    hist = torch.zeros(2 * (bins + 2), dtype=torch.int32, device="cuda")
-    L.sample_events(c_t.data_ptr(), k, m, seed, step, rank, px.STREAM_FAKE, ev.data_ptr(), hist.data_ptr(), bins,
-                    (0.0, 0.0), (4.0, 4.0), _stream())
+    hist = torch.zeros(2 * (max(bins, 1) + 2), dtype=torch.int32, device="cuda")
+    L.sample_events(c_t.data_ptr(), k, m, seed, step, rank, px.STREAM_FAKE, ev.data_ptr(),
+                    hist.data_ptr() if bins else 0, bins, (0.0, 0.0), (4.0, 4.0), _stream())
     torch.cuda.synchronize()
     y_gpu = ev.cpu().numpy().reshape(-1, 2)
     u = proxy.fake_uniforms(seed, step, rank, k * m)
     y32 = proxy.sample_events_f32(c32, m, u)
     assert np.array_equal(y_gpu, y32)                       # same fp32 operations -> bit-exact
     assert_rel(y_gpu, proxy.sample_events(c32.astype(np.float64), m, u), 1e-5, 1e-6, "events vs fp64")
+    if not bins:
+        return
     h = hist.cpu().numpy().astype(np.int64).reshape(2, bins + 2)
     for o in range(2):
         assert np.array_equal(h[o], proxy.histogram_f32(y32[:, o], 0.0, 4.0, bins))
@@ -133,6 +137,14 @@ def _check_step(cfg, t=0, disc_band=kink.BAND_FP32, fake_dev=0.0, g_outliers=0.0
     assert_grad_close(ctx.get(L.T_GEN_DW), og["packet"], 1e-3, "packet dW_G", kd["packet"], nout(og["packet"]))
     assert_grad_close(ctx.get(L.T_GEN_DB), flat(og["db_g"]), 1e-3, "db_G", kd["db_g"], nout(flat(og["db_g"])))
     return ctx, st, out
+
+
+def test_step_many_histogram_bins():
+    """hist_bins = 300: the step's four shared histograms exceed the
+    lane-column layout (one copy per block); paper widths, fused kernels."""
+    L = lib()
+    _check_step(L.config_init(1, seed=8, param_samples=64, events_per_sample=64, hist_bins=300), t=1,
+                disc_band=kink.BAND_BF16X3, g_outliers=1e-3)  # R27 mixed-pattern flips, as the k = 63 case
 
 
 def test_step_desk():
