@@ -244,7 +244,8 @@ def test_step_paper_widths_tiny(k, m):
         assert np.all(ratio <= 1.0), f"{name}: {int(np.sum(ratio > 1))} elements outside the split bound (worst {ratio.max():.3g})"
 
 
-@pytest.mark.parametrize("fused_env,k,m", [("1", 128, 1024), ("1p", 128, 1024), ("0", 128, 1024), ("1", 125, 1021)],
+@pytest.mark.parametrize("fused_env,k,m", [("1", 128, 1024), ("1p", 128, 1024), ("0", 128, 1024), ("1", 125, 1021),
+                                           ("0", 125, 1021)],
                          indirect=["fused_env"])
 def test_bf16_step_elementwise(fused_env, k, m):
     """SAGIPS_PREC_BF16 (C5's precision): discriminator GEMMs in bf16 with fp32
@@ -589,6 +590,45 @@ def test_pipelined_host_input_steps_match_the_device_steps(graph):
         assert np.array_equal(ca.get(w), cb.get(w)), w
     sa, sb = ca.get(L.T_STATS), L.StepStats.from_buffer_copy(stats[T - 1])
     assert sa.loss_d == sb.loss_d and sa.loss_g == sb.loss_g
+
+
+def _tabulated_cfg(L, preset, **kw):
+    cfg = L.config_init(preset, seed=19, sampler=L.SAMPLER_TABULATED, sampler_grid=129, **kw)
+    for j, v in enumerate((0.3, 2.0, 1.2, 0.7, 1.5, 3.0)):   # (w, b, c) per observable
+        cfg.true_params[j] = v
+    cfg.hist_lo[0] = cfg.hist_lo[1] = 0.0
+    cfg.hist_hi[0] = cfg.hist_hi[1] = 1.0
+    return cfg
+
+
+@pytest.mark.parametrize("preset", [0, 1])
+def test_tabulated_sampler_graph_and_host_inputs(preset):
+    """The tabulated-CDF sampler (R32) through the other step paths: four
+    CUDA-graph steps bit-identical to four eager ones, and a host-input step
+    (the caller's noise and real rows) bit-identical to the device-input
+    step it reproduces."""
+    import ctypes
+    L = lib()
+    kw = dict(param_samples=32, events_per_sample=45, reference_rows=4000, shard_rows=2000)
+    ca, cb = make_ctx(_tabulated_cfg(L, preset, **kw)), make_ctx(_tabulated_cfg(L, preset, **kw))
+    for t in range(4):
+        ca.train_step(t, 0, _stream())
+        cb.train_step(t, L.STEP_GRAPH, _stream())
+    torch.cuda.synchronize()
+    for w in (L.T_GEN_W, L.T_GEN_B, L.T_DISC_W, L.T_DISC_B, L.T_EVENTS, L.T_DY, L.T_HIST):
+        assert np.array_equal(ca.get(w), cb.get(w)), w
+    cc = make_ctx(_tabulated_cfg(L, preset, **kw))
+    cd = make_ctx(_tabulated_cfg(L, preset, **kw))
+    cc.train_step(0, L.STEP_LOCAL_ONLY, _stream())
+    torch.cuda.synchronize()
+    N = 32 * 45
+    noise = torch.from_numpy(cc.get(L.T_NOISE).reshape(32, -1).copy()).pin_memory()
+    real = torch.from_numpy(cc.get(L.T_EVENTS).reshape(-1, 2)[:N].copy()).pin_memory()
+    stats = (ctypes.c_uint8 * ctypes.sizeof(L.StepStats))()
+    cd.train_step_host(0, L.STEP_LOCAL_ONLY, noise.data_ptr(), real.data_ptr(), ctypes.addressof(stats), _stream())
+    torch.cuda.synchronize()
+    for w in (L.T_RAW, L.T_EVENTS, L.T_LOGITS_D, L.T_DISC_DW, L.T_DY, L.T_DRAW, L.T_GEN_DW):
+        assert np.array_equal(cc.get(w), cd.get(w)), w
 
 
 @pytest.mark.parametrize("preset", [0, 1])
