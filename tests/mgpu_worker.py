@@ -5,7 +5,7 @@ oracle's lockstep simulation of all ranks (desk preset, seconds) and checks,
 after every step, its own reduced packet and generator weights against the
 oracle (exchange).  Exit code 0 = parity held on this rank.
 
-usage: torchrun --nproc-per-node N tests/mgpu_worker.py MODE GROUP STALENESS STEPS [OUTER_EVERY]
+usage: torchrun --nproc-per-node N tests/mgpu_worker.py MODE GROUP STALENESS STEPS [OUTER_EVERY [PACKET_BIASES [GRAPH]]]
 """
 import ctypes
 import os
@@ -29,6 +29,7 @@ def main():
     mode_name, group, stale, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
     outer = int(sys.argv[5]) if len(sys.argv) > 5 else 0
     fused = int(sys.argv[6]) if len(sys.argv) > 6 else 0  # packet_biases
+    graph = int(sys.argv[7]) if len(sys.argv) > 7 else 0  # CUDA-graph steps (SAGIPS_STEP_GRAPH)
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -49,7 +50,7 @@ def main():
     history = {}
     ok = True
     for t in range(steps):
-        ctx.train_step(t, 0, sp)
+        ctx.train_step(t, L.STEP_GRAPH if graph else 0, sp)
         outs = [gan.local_step(ocfg, states[r], t) for r in range(world)]
         history[t] = [o["packet"] for o in outs]
         R = xc.reduce_step(ocfg.mode, world, group, outer, stale, ocfg.reduce_mean, t, history)

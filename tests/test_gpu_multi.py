@@ -35,6 +35,16 @@ def test_two_gpu_exchange(mode, group, stale, outer):
     _run(2, mode, group, stale, 6, outer)
 
 
+@pytest.mark.parametrize("mode,group,stale,outer", [("rma-ag", 2, 1, 0), ("sync", 2, 0, 0), ("rma-chunked", 2, 0, 0),
+                                                     ("rma", 2, 1, 0)])
+def test_two_gpu_exchange_graph_steps(mode, group, stale, outer):
+    """the same parity through CUDA-graph steps (SAGIPS_STEP_GRAPH): the push /
+    wait / fold / Adam(G) kernels captured with the step and replayed"""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run(2, mode, group, stale, 6, outer, 0, 1)
+
+
 @pytest.mark.parametrize("mode,group,stale,outer", [
     ("rma", 4, 0, 0), ("rma", 2, 0, 2), ("arar-arar", 2, 1, 3), ("rma", 4, 1, 0), ("rma-ag", 4, 0, 0),
     ("rma-ag", 4, 1, 0), ("rma-ag", 2, 1, 2), ("rma-chunked", 4, 0, 0), ("rma-chunked", 2, 0, 2)])
@@ -42,6 +52,15 @@ def test_four_gpu_grouping(mode, group, stale, outer):
     if _ngpus() < 4:
         pytest.skip("needs 4 GPUs")
     _run(4, mode, group, stale, 6, outer)
+
+
+@pytest.mark.parametrize("mode,group,stale,outer", [("rma-ag", 2, 1, 2), ("rma", 4, 1, 0), ("rma-chunked", 2, 0, 2)])
+def test_four_gpu_grouping_graph_steps(mode, group, stale, outer):
+    """grouping through CUDA-graph steps; the steps whose outer ring fires on
+    a leader run eagerly (sagips.h SAGIPS_STEP_GRAPH) between graph steps"""
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    _run(4, mode, group, stale, 6, outer, 0, 1)
 
 
 @pytest.mark.parametrize("mode,group,stale,outer", [("rma", 2, 1, 0), ("sync", 2, 0, 0), ("arar", 2, 0, 0)])
