@@ -266,10 +266,12 @@ struct FoldAdamArgs {
   const unsigned int* err;
   int64_t gather_chunk;  // RMA_CHUNKED: element i is already reduced, in pl.p[i / gather_chunk][i]; 0: fold
   int vec;               // every array 16-byte aligned: the weights go four at a time (a multiple-of-64 chunk never splits a quad)
+  uint32_t* zero_word;   // written 0 by one thread (the stats' outer-ring flag of a step without exchange), or nullptr
 };
 __device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
 __global__ void __launch_bounds__(256) k_fold_adam(const __grid_constant__ FoldAdamArgs f) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (f.zero_word && blockIdx.x == 0 && threadIdx.x == 0) *f.zero_word = 0u;
   if (f.err && *reinterpret_cast<const volatile unsigned int*>(f.err) != 0u) return;
   const GenAdam& a = f.a;
   const int64_t n = f.do_adam ? a.nw + a.nb : f.pw;
@@ -717,6 +719,7 @@ sagips_status exchange_join(sagips_ctx* c, cudaStream_t st) {
 bool exchange_fuses_adam(const sagips_ctx* c, uint64_t step) {
   (void)step;
   const auto& g = c->cfg;
+  if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) return true;  // no exchange: copy + Adam(G) in one kernel
   return g.world > 1 && one_sided(c) && c->xs && (c->xs->g > 1 || outer_one_sided(c)) && c->xs->peers_ok;
 }
 
@@ -881,6 +884,19 @@ sagips_status exchange_pull(sagips_ctx* c, uint64_t step, cudaStream_t st, const
     return SAGIPS_ERR_STATE;
   }
   if (g.world == 1 || g.mode == SAGIPS_MODE_NONE) {
+    if (adam) {  // the "reduced" packet is the own one: one launch copies it and applies Adam(G)
+      FoldAdamArgs f{};
+      f.pl.count = 1;
+      f.pl.p[0] = c->g_dW;
+      f.reduced = c->reduced;
+      f.pw = (int64_t)pw;
+      f.divisor = 1.0f;
+      f.do_adam = 1;
+      f.a = *adam;
+      f.zero_word = &c->stats->outer_fired;
+      XCK(launch_fold_adam(f, st));
+      return SAGIPS_OK;
+    }
     XCK(cudaMemsetAsync(&c->stats->outer_fired, 0, sizeof(uint32_t), st));
     XCK(cudaMemcpyAsync(c->reduced, c->g_dW, sizeof(float) * pw, cudaMemcpyDeviceToDevice, st));
     return SAGIPS_OK;
