@@ -119,4 +119,23 @@ __device__ __forceinline__ float softplus_neg(float z) {
   return fmaxf(-z, 0.0f) + log1pf(expf(-fabsf(z)));
 }
 
+// loss = scale * sum of part[0 .. nparts) in ascending order, by one block:
+// up to kLossCap partials are loaded by the whole block at once (one round
+// trip) into sp, then summed by thread 0; writes the stats' loss and the
+// non-finite flag (the SPEC's NaN guard).  k_finish_loss, and the extra
+// block of the kernels that absorb it (k_reduce_adam, k_sample_bwd).
+constexpr int kLossCap = 512;
+__device__ inline void finish_loss_block(const double* part, int nparts, double scale, float* out, uint32_t* nonfinite,
+                                         double* sp) {
+  for (int p = threadIdx.x; p < nparts && p < kLossCap; p += blockDim.x) sp[p] = part[p];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int p = 0; p < nparts; ++p) v += p < kLossCap ? sp[p] : part[p];
+    const float l = (float)(v * scale);
+    *out = l;
+    if (!isfinite(l)) *nonfinite = 1u;
+  }
+}
+
 }  // namespace sagips

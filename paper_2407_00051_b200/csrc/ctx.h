@@ -74,6 +74,8 @@ struct sagips_ctx {
   uint32_t* tile_ctrs = nullptr;          // dynamic tile-schedule counters of the layer kernels
   int tile_ctr_next = 0;
   double* loss_part = nullptr;
+  int loss_g_defer = 0;                   // fused G step: L_G's partials, finished by the sampler backward's extra block
+  double loss_g_scale = 0.0;
   sagips_step_stats* stats = nullptr;
   // step bookkeeping
   int64_t g_tau = 0, d_tau = 0;

@@ -84,8 +84,16 @@ void launch_sample_step(const float* c, int k, int m, const float* shard, int64_
 void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t step, uint32_t rank,
                           uint32_t stream_id, float* events, uint32_t* hist, int bins, const float lo[2],
                           const float hi[2], cudaStream_t st);
+// loss_part != nullptr: one extra block finishes a loss (finish_loss_block) instead of a k_finish_loss launch
+struct LossFinish {
+  const double* loss_part = nullptr;
+  int nparts = 0;
+  double scale = 0.0;
+  float* out = nullptr;
+  uint32_t* nonfinite = nullptr;
+};
 void launch_sample_bwd(const float* dy, const float* raw, int k, int m, uint64_t seed, uint32_t step,
-                       uint32_t rank, float* draw, cudaStream_t st);
+                       uint32_t rank, float* draw, cudaStream_t st, const LossFinish& loss = LossFinish{});
 
 // k_mlp_simt.cu
 void launch_gemm(bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
@@ -233,6 +241,12 @@ constexpr int kMaxRedSegs = 2 * kMaxLayers;
 struct RedAdamArgs {
   RedSeg seg[kMaxRedSegs];
   int nseg = 0;
+  // the D loss, finished by one extra block (instead of a k_finish_loss launch), or nullptr
+  const double* loss_part = nullptr;
+  int loss_nparts = 0;
+  double loss_scale = 0.0;
+  float* loss_out = nullptr;
+  uint32_t* nonfinite = nullptr;
   int adam = 1;
   float step_size = 0.f, bc2_sqrt = 1.f, b1 = 0.f, b2 = 0.f, eps = 0.f;  // (set by the launcher)
 };

@@ -53,6 +53,11 @@ void launch_adam(float* p, const float* g, float* m, float* v, int64_t n, double
 // then the element's Adam update (the same arithmetic as k_adam).
 __global__ void __launch_bounds__(256) k_reduce_adam(const __grid_constant__ RedAdamArgs a) {
   __shared__ float red[8][33];
+  if (a.loss_part && blockIdx.x == gridDim.x - 1) {  // the extra block: the step's D loss
+    __shared__ double sp[kLossCap];
+    finish_loss_block(a.loss_part, a.loss_nparts, a.loss_scale, a.loss_out, a.nonfinite, sp);
+    return;
+  }
   int si = 0;
   while (si + 1 < a.nseg && (int)blockIdx.x >= a.seg[si + 1].block0) ++si;
   const RedSeg& sg = a.seg[si];
@@ -93,6 +98,7 @@ void launch_reduce_adam(RedAdamArgs& a, double lr, int64_t tau, double b1, doubl
   a.b1 = (float)b1;
   a.b2 = (float)b2;
   a.eps = (float)eps;
+  if (a.loss_part) ++blocks;  // + the loss block
   k_reduce_adam<<<blocks, 256, 0, st>>>(a);
   count_launch();
 }

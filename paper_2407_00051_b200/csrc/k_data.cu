@@ -435,7 +435,12 @@ void launch_sample_events(const float* c, int k, int m, uint64_t seed, uint32_t 
 // block reduction has a fixed order, so the result is deterministic.
 __global__ void __launch_bounds__(256) k_sample_bwd(const float2* __restrict__ dy, const float* __restrict__ raw,
                                                     int m, PhiloxKey key, uint32_t step, uint32_t rank,
-                                                    float* __restrict__ draw) {
+                                                    float* __restrict__ draw, const __grid_constant__ LossFinish loss) {
+  if (loss.loss_part && blockIdx.x == gridDim.x - 1) {  // the extra block: the step's G loss
+    __shared__ double sp[kLossCap];
+    finish_loss_block(loss.loss_part, loss.nparts, loss.scale, loss.out, loss.nonfinite, sp);
+    return;
+  }
   const int s = blockIdx.x;
   float acc[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   auto add = [&](float2 g, float u0, float u1) {
@@ -484,11 +489,11 @@ __global__ void __launch_bounds__(256) k_sample_bwd(const float2* __restrict__ d
 }
 
 void launch_sample_bwd(const float* dy, const float* raw, int k, int m, uint64_t seed, uint32_t step,
-                       uint32_t rank, float* draw, cudaStream_t st) {
+                       uint32_t rank, float* draw, cudaStream_t st, const LossFinish& loss) {
   const int per = (m % 2 == 0) ? (m + 1) / 2 : m;  // work items per sample
   int threads = 32 * ((std::min(per, 256) + 31) / 32);
-  k_sample_bwd<<<k, threads, 0, st>>>(reinterpret_cast<const float2*>(dy), raw, m, make_key(seed),
-                                      step, rank, draw);
+  k_sample_bwd<<<k + (loss.loss_part ? 1 : 0), threads, 0, st>>>(reinterpret_cast<const float2*>(dy), raw, m,
+                                                                  make_key(seed), step, rank, draw, loss);
   count_launch();
 }
 

@@ -301,23 +301,11 @@ void launch_head(const float* H, int M, int hd, const float* w, const float* b, 
   count_launch();
 }
 
-// loss = scale * sum_{p ascending} loss_part[p]; writes stats and the
-// non-finite flag (the SPEC's NaN guard).
-// The partials are loaded by the whole block at once (one round trip), then
-// summed by thread 0 in ascending order from shared memory.
+// loss = scale * sum_{p ascending} loss_part[p] (finish_loss_block, common.cuh)
 __global__ void __launch_bounds__(256) k_finish_loss(const double* __restrict__ loss_part, int nparts, double scale,
                                                      float* out, uint32_t* nonfinite) {
-  constexpr int kCap = 512;  // >= every caller's part count (148 .. 296)
-  __shared__ double sp[kCap];
-  for (int p = threadIdx.x; p < nparts && p < kCap; p += blockDim.x) sp[p] = loss_part[p];
-  __syncthreads();
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double v = 0.0;
-    for (int p = 0; p < nparts; ++p) v += p < kCap ? sp[p] : loss_part[p];
-    const float l = (float)(v * scale);
-    *out = l;
-    if (!isfinite(l)) *nonfinite = 1u;
-  }
+  __shared__ double sp[kLossCap];
+  finish_loss_block(loss_part, nparts, scale, out, nonfinite, sp);
 }
 
 void launch_finish_loss(const double* loss_part, int nparts, double scale, float* out, uint32_t* nonfinite,

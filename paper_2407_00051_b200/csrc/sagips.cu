@@ -587,7 +587,10 @@ static void disc_forward_v2(sagips_ctx* c, const float* X, int64_t rows, int64_t
 // All discriminator gradients of a tcgen05 D step from their per-CTA partials
 // (head [hparts][129], hidden layer l: lpart/ldb [nparts[l]], layer 0
 // colpart [l0parts][384]) -> d_dW / d_dB, then Adam(D): one launch.
-static void disc_reduce_adam(sagips_ctx* c, int hparts, const int* nparts, int l0parts, cudaStream_t st) {
+// loss_scale > 0: the D loss partials (c->loss_part, hparts of them) are
+// finished by the reduction's extra block
+static void disc_reduce_adam(sagips_ctx* c, int hparts, const int* nparts, int l0parts, cudaStream_t st,
+                             double loss_scale = 0.0) {
   const auto& D = c->D;
   const auto& g = c->cfg;
   const int Lh = D.L - 1;
@@ -609,6 +612,13 @@ static void disc_reduce_adam(sagips_ctx* c, int hparts, const int* nparts, int l
   }
   seg(c->colpart, l0parts, 384, 256, true, 0);     // dW_0 [128][2]
   seg(c->colpart + 256, l0parts, 384, 128, false, 0);
+  if (loss_scale > 0.0) {
+    A.loss_part = c->loss_part;
+    A.loss_nparts = hparts;
+    A.loss_scale = loss_scale;
+    A.loss_out = &c->stats->loss_d;
+    A.nonfinite = &c->stats->nonfinite;
+  }
   c->d_tau += 1;
   launch_reduce_adam(A, g.disc_lr, c->d_tau, g.adam_beta1, g.adam_beta2, g.adam_eps, st);
   c->d_adam_done = true;
@@ -622,7 +632,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
   const int grid = tc_layers_grid(rows);
   reset_tile_ctrs(c, st);
   disc_forward_v2(c, c->X, rows, N, 0.0f, 1.0f / (float)rows, c->logits_d, true, st);
-  launch_finish_loss(c->loss_part, grid, 1.0 / rows, &c->stats->loss_d, &c->stats->nonfinite, st);
+  // (the loss partials wait in loss_part: k_reduce_adam's extra block finishes L_D)
   int cur = 0;
   int nparts[kMaxLayers] = {};
   for (int l = Lh - 1; l >= 1; --l) {
@@ -647,7 +657,7 @@ static void disc_step_v2(sagips_ctx* c, cudaStream_t st) {
     kernel_end(c, st);
     cur ^= 1;
   }
-  disc_reduce_adam(c, grid, nparts, grid, st);
+  disc_reduce_adam(c, grid, nparts, grid, st, 1.0 / rows);
 }
 
 // the fused G step (k_fused.cu): paper widths, depth 4; SAGIPS_FUSED=0 keeps the per-layer kernels
@@ -682,7 +692,12 @@ static void gen_loss_v2(sagips_ctx* c, cudaStream_t st) {
     kernel_begin(c, 12, st);
     launch_gstep(split, a, st);
     kernel_end(c, st);
-    launch_finish_loss(c->loss_part, fused_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
+    if (c->cfg.sampler == SAGIPS_SAMPLER_TABULATED) {
+      launch_finish_loss(c->loss_part, fused_grid(N), 1.0 / N, &c->stats->loss_g, &c->stats->nonfinite, st);
+    } else {  // finished by k_sample_bwd's extra block (the next launch)
+      c->loss_g_defer = fused_grid(N);
+      c->loss_g_scale = 1.0 / (double)N;
+    }
     return;
   }
   reset_tile_ctrs(c, st);
@@ -863,7 +878,18 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   mark(c, 4, st);
   // a9 sampler backward
   if (tab) launch_sample_tabulated_bwd(raw, k, m, tab_grid(g), g.seed, step, g.rank, kStreamFake, c->dy, c->draw, st);
-  else launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st);
+  else {
+    LossFinish lf;
+    if (c->loss_g_defer) {
+      lf.loss_part = c->loss_part;
+      lf.nparts = c->loss_g_defer;
+      lf.scale = c->loss_g_scale;
+      lf.out = &c->stats->loss_g;
+      lf.nonfinite = &c->stats->nonfinite;
+    }
+    launch_sample_bwd(c->dy, raw, k, m, g.seed, step, g.rank, c->draw, st, lf);
+  }
+  c->loss_g_defer = 0;
   mark(c, 5, st);
   // a10 generator backward (the output layer is linear: dZ_L = draw);
   // a11 the weight gradients land in g_dW, which *is* the packet layout
