@@ -137,8 +137,9 @@ namespace sagips {
 void adam_gen(sagips_ctx* c, cudaStream_t st);
 // k_gen.cu: fused generator passes (widths <= 128)
 bool gen_fused_ok(const sagips_ctx* c);
+// noise_step != nullptr: a1 too -- the forward draws the step's noise into c->noise itself
 void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch = nullptr, int64_t prefetch_bytes = 0,
-                    uint32_t* zero_hist = nullptr, int zero_words = 0);
+                    uint32_t* zero_hist = nullptr, int zero_words = 0, const uint32_t* noise_step = nullptr);
 // the generator forward on a caller-given noise batch (k <= param_samples rows):
 // the constrained parameters -> c_out [k][6]; reuses the step's activation buffers
 void launch_gen_predict(sagips_ctx* c, const float* noise, int k, float* c_out, cudaStream_t st);

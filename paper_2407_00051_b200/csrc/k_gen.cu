@@ -63,6 +63,13 @@ struct GenArgs {
   // every layer's weights staged up front (cp.async, one group per layer in
   // use order) when they fit in shared memory: ws_off[l] = float offset of
   // layer l's copy after the row buffers; preload = 0 stages layer by layer
+  // a1 inside the forward: the block draws its rows' noise (Philox + Box-
+  // Muller, k_normals' arithmetic, stream NOISE of this step) and also stores
+  // it to `noise`; gen_noise = 0 reads `noise`
+  int gen_noise;
+  float* noise_out;               // (gen_noise) where the drawn noise is stored: [k][sizes[0]]
+  PhiloxKey noise_key;
+  uint32_t noise_step, noise_rank;
   int preload;
   int ws_off[kMaxLayers];
   int ws_off_b[kMaxLayers];  // the dgrad's plain [out][in] copies (layers last .. 1)
@@ -129,9 +136,34 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
       cp_async_commit();
     }
   }
-  for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
-    const int r = idx / in0, i = idx % in0;
-    buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
+  if (a.gen_noise) {  // the block's kR rows = values [r0 in0, (r0 + kR) in0): whole Philox calls (kR in0 % 4 == 0)
+    for (int cl = tid; cl < kR * in0 / 4; cl += kGenThreads) {
+      const int64_t call = ((int64_t)r0 * in0) / 4 + cl;
+      const uint4 w = philox_call(a.noise_key, (uint32_t)call, a.noise_step, a.noise_rank, kStreamNoise);
+      float z[4];
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const float ua = uniform_open01(p ? w.z : w.x);
+        const float ub = uniform_open01(p ? w.w : w.y);
+        const float rr = sqrtf(-2.0f * logf(ua));
+        float sn, co;
+        sincospif(2.0f * ub, &sn, &co);
+        z[2 * p] = rr * co;
+        z[2 * p + 1] = rr * sn;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = 4 * cl + q, r = v / in0, i = v % in0;
+        const bool live = r0 + r < a.k;
+        buf[0][r][i] = live ? z[q] : 0.f;
+        if (live) a.noise_out[(int64_t)(r0 + r) * in0 + i] = z[q];
+      }
+    }
+  } else {
+    for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
+      const int r = idx / in0, i = idx % in0;
+      buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
+    }
   }
   for (int l = 0; l < a.L; ++l) {
     const int in = a.sizes[l], out = a.sizes[l + 1];
@@ -456,7 +488,7 @@ static size_t gen_smem(const GenArgs& a) {
 static size_t gen_fwd_smem() { return kGenSmemMax; }  // the attribute: the largest launch
 
 void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_t prefetch_bytes,
-                    uint32_t* zero_hist, int zero_words) {
+                    uint32_t* zero_hist, int zero_words, const uint32_t* noise_step) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_gen_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gen_fwd_smem());
@@ -467,6 +499,16 @@ void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_
   a.prefetch_bytes = (prefetch_bytes / 16) * 16;
   a.zero_hist = zero_hist;
   a.zero_words = zero_words;
+  if (noise_step && (kR * a.sizes[0]) % 4 == 0) {
+    a.gen_noise = 1;
+    a.noise_out = c->noise;
+    a.noise_key = make_key(c->cfg.seed);
+    a.noise_step = *noise_step;
+    a.noise_rank = (uint32_t)c->cfg.rank;
+  } else if (noise_step) {
+    launch_normals(c->noise, (int64_t)c->cfg.param_samples * c->cfg.noise_dim, 1.0f, c->cfg.seed, *noise_step,
+                   (uint32_t)c->cfg.rank, kStreamNoise, st);
+  }
   k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
   count_launch();
 }

@@ -824,20 +824,21 @@ static void local_step(sagips_ctx* c, uint64_t t, cudaStream_t st) {
   const float a = g.leaky_slope;
   const uint32_t step = (uint32_t)t;
   mark(c, 0, st);
-  // a1 noise ~ N(0,1) (or the caller's, sagips_train_step_host)
+  // a1 noise ~ N(0,1) (or the caller's, sagips_train_step_host); with the
+  // fused generator the forward kernel draws it itself
+  const bool fused_gen = gen_fused_ok(c);
   if (c->in_noise)
     cudaMemcpyAsync(c->noise, c->in_noise, sizeof(float) * k * g.noise_dim, cudaMemcpyDeviceToDevice, st);
-  else
+  else if (!fused_gen)
     launch_normals(c->noise, (int64_t)k * g.noise_dim, 1.0f, g.seed, step, g.rank, kStreamNoise, st);
   // a2 generator forward (hidden LeakyReLU, linear output) + a3 constrain
-  const bool fused_gen = gen_fused_ok(c);
   const bool tab = g.sampler == SAGIPS_SAMPLER_TABULATED;
   // the real rows come from the resident shard: prefetch it into L2 and zero
   // the histograms inside the generator forward (the step's sampler follows)
   const bool boot = !c->in_real;
   if (fused_gen) {
     launch_gen_fwd(c, st, boot ? c->shard : nullptr, boot ? 8 * g.shard_rows : 0, boot ? c->hist : nullptr,
-                   boot ? 4 * (g.hist_bins + 2) : 0);
+                   boot ? 4 * (g.hist_bins + 2) : 0, c->in_noise ? nullptr : &step);
   } else {
     const float* in = c->noise;
     for (int l = 0; l < G.L; ++l) {
