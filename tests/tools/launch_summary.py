@@ -13,10 +13,10 @@ def main(path):
     rows = [r for r in csv.reader(open(path)) if len(r) > 10][1:]
     names = [re.sub(r"\(.*", "", r[4]).replace("sagips::", "").replace("void ", "") for r in rows]
     ns = [float(r[14]) for r in rows]
-    starts = [i for i, n in enumerate(names) if n.startswith("k_normals")]
-    adams = [i for i, n in enumerate(names) if n.startswith("k_adam")]
-    s = starts[-1]
-    e = max(i for i in adams if i > s)
+    starts = [i for i, n in enumerate(names) if n.startswith("k_gen_fwd")]
+    ends = [i for i, n in enumerate(names) if n.startswith("k_fold_adam") or n.startswith("k_adam")]
+    s = max(i for i in starts if any(j > i for j in ends))
+    e = min(j for j in ends if j > s)
     tot = sum(ns[s:e + 1])
     print(f"one step (launches {s}-{e}, {e - s + 1} kernels): {tot / 1e3:.1f} us")
     for i in range(s, e + 1):
