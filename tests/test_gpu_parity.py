@@ -465,6 +465,18 @@ def test_max_size_fp32_step_sampled_rows():
     _, _, dy = mlp.backward(gpu_d[0], cache, dzG[:, None], a)
     assert_grad_close(ctx.get(L.T_DY).reshape(-1, 2)[idx], dy, 1e-3, "dy (sampled rows)",
                       outliers=idx.size * 2 // 400)
+    # the sampler backward of whole samples (first, middle, last) from the
+    # GPU's own dy: the oracle's sums over the sample's 16,384 events in fp64;
+    # the GPU's fp32 reduction within 1e-5 of the sum of magnitudes
+    dy_all = ctx.get(L.T_DY).reshape(-1, 2).astype(np.float64)
+    draw_gpu = ctx.get(L.T_DRAW).reshape(k, 6).astype(np.float64)
+    for smp in (0, k // 2, k - 1):
+        e0 = smp * m
+        us = px.uniform_open01(px.words(seed, px.STREAM_FAKE, 0, 0, 2 * e0, 2 * m)).reshape(m, 2)
+        dys = dy_all[e0:e0 + m]
+        _, draw_s = proxy.sampler_backward(dys, us, raw[smp][None, :], m)
+        _, mag = proxy.sampler_backward(np.abs(dys), us, raw[smp][None, :], m)
+        assert np.all(np.abs(draw_gpu[smp] - draw_s[0]) <= 1e-5 * mag[0] + 1e-30), (smp, draw_gpu[smp], draw_s[0])
 
 
 def test_step_is_deterministic():
