@@ -196,10 +196,16 @@ __device__ __forceinline__ void bins2(uint64_t y, uint64_t LO, uint64_t SC, floa
 // however concentrated the distribution; warps meet only across
 // instructions).  Used when 512 (bins+2) bytes fit (bins <= 126); otherwise
 // one [4][bins+2] copy per block.
-constexpr int kSampleThreads = 512;
+#ifndef SAGIPS_SAMPLE_THREADS
+#define SAGIPS_SAMPLE_THREADS 512
+#endif
+constexpr int kSampleThreads = SAGIPS_SAMPLE_THREADS;
 // resident blocks per SM (3 blocks at 40 registers for the variants that do
 // not spill then measured no faster at 2^24: 34.4 vs 32.8 us)
-__host__ __device__ constexpr int sample_blocks_per_sm(bool, bool, bool) { return 2; }
+#ifndef SAGIPS_SAMPLE_BPS
+#define SAGIPS_SAMPLE_BPS 1  // one 512-thread block per SM (2 blocks: 45.5 vs 43.5 us at 2^24 with histograms)
+#endif
+__host__ __device__ constexpr int sample_blocks_per_sm(bool, bool, bool) { return SAGIPS_SAMPLE_BPS; }
 __host__ __device__ constexpr bool hist_columns(int bins) { return bins + 2 <= 128; }
 
 // One thread = one group of 4 consecutive events e = 4g..4g+3:
