@@ -71,7 +71,9 @@ def test_presets_and_workspace():
 
 
 @pytest.mark.parametrize("field,value", [("group_size", 0), ("outer_rma", 2), ("staleness", 2), ("mode", 9), ("disc_hidden", 100),
-                                         ("rank", 5), ("hist_bins", 0), ("param_samples", 0)])
+                                         ("rank", 5), ("hist_bins", 0), ("param_samples", 0),
+                                         ("events_per_sample", 0), ("shard_rows", 0), ("reference_rows", 0),
+                                         ("param_samples", -1), ("world", 0), ("noise_dim", 0)])
 def test_config_validation(field, value):
     L = _lib()
     cfg = L.config_init(L.PRESET_DESK, world=4, group_size=2)
