@@ -230,3 +230,27 @@ def test_timeout_skips_the_update_and_is_reported():
     w1 = np.empty_like(w0)
     L.lib.sagips_get(ctxs[0].h, L.T_GEN_W, w1.ctypes.data, w1.nbytes)  # reports TIMEOUT too; copies first
     assert np.array_equal(w1, w0), "the generator must keep its weights when the exchange failed"
+
+
+def test_overrun_slot_is_a_protocol_error():
+    """A peer that runs more than the slot depth (4 versions) ahead
+    overwrites the packet a slow rank still needs: the slow rank's wait sees
+    a newer version in the slot (not a stale one), skips the fold and
+    Adam(G), and the next call returns PROTOCOL."""
+    L = lib()
+    ctxs, sps = make_world("rma-ag", 2, 2, 0, timeout_ms=2000)
+    for t in range(5):                          # rank 1: versions 0..4 (4 lands in version 0's slot)
+        ctxs[1].train_step(t, L.STEP_LOCAL_ONLY, sps[1])
+        ctxs[1].push_generator_grad(t, sps[1])
+    torch.cuda.synchronize()
+    ctxs[0].train_step(0, L.STEP_LOCAL_ONLY, sps[0])
+    w0 = ctxs[0].get(L.T_GEN_W)
+    ctxs[0].push_generator_grad(0, sps[0])
+    ctxs[0].pull_generator_grad(0, sps[0])      # needs rank 1's version 0: overwritten
+    torch.cuda.synchronize()
+    with pytest.raises(L.SagipsError) as e:
+        ctxs[0].train_step(1, 0, sps[0])
+    assert e.value.status == 5  # PROTOCOL
+    w1 = np.empty_like(w0)
+    L.lib.sagips_get(ctxs[0].h, L.T_GEN_W, w1.ctypes.data, w1.nbytes)
+    assert np.array_equal(w1, w0), "the generator must keep its weights when the exchange failed"
