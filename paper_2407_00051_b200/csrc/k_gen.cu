@@ -21,8 +21,13 @@ using tc::prefetch_l2;
 namespace {
 constexpr int kR = 8;         // rows per CTA (forward / dgrad)
 constexpr int kGenMaxW = 128; // widest layer these kernels handle
-constexpr int kGenThreads = 256;
-static_assert(kR == 8 && kGenThreads == 2 * kGenMaxW, "the 128 x 128 fast paths map 256 threads to 2 x 4 rows");
+constexpr int kGenThreads = 256;  // k_gen_wgrad: 16 x 16 output tiles
+// the forward and the dgrad chain: 512 threads, thread (rb, o) of the 128 x 128
+// fast path owns rows rb, rb + 4 (two rows: 16 warps per block hide the
+// shared-memory latency better than 8 warps of four rows, ncu: 12.5% occupancy)
+constexpr int kGenFT = 512;
+constexpr int kRU = kR * kGenMaxW / kGenFT;  // rows per thread in the fast path
+static_assert(kR == 8 && kRU == 2 && kGenFT == 4 * kGenMaxW, "the fast paths map 512 threads to 4 x 2 rows");
 constexpr int kGenSplits = 8;  // wgrad: row splits (one partial each, reduced in a fixed order)
 constexpr size_t kGenSmemMax = 227 * 1024;  // dynamic shared memory cap (all-layer weight staging)
 
@@ -107,7 +112,7 @@ __device__ __forceinline__ void cp_async_wait(int n) {
 // and of the (broadcast) rows.  Other shapes: thread per (row, output), W rows
 // padded to in + 1.
 constexpr int kLdFast = kGenMaxW + 4;
-__global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__ GenArgs a) {
+__global__ void __launch_bounds__(kGenFT) k_gen_fwd(const __grid_constant__ GenArgs a) {
   extern __shared__ __align__(16) float gsm[];
   float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
   float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][ld] (preload: base)
@@ -121,23 +126,23 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
       prefetch_l2(a.prefetch + o, (uint32_t)(b1 - o < 32768 ? b1 - o : 32768));
   }
   if (a.zero_hist && blockIdx.x == 0)
-    for (int i = tid; i < a.zero_words; i += kGenThreads) a.zero_hist[i] = 0u;
+    for (int i = tid; i < a.zero_words; i += kGenFT) a.zero_hist[i] = 0u;
   if (a.preload) {  // every layer's weights, layer order, one cp.async group each (same padded layouts)
     for (int l = 0; l < a.L; ++l) {
       const int in = a.sizes[l], out = a.sizes[l + 1];
       const float* W = a.W + a.w_off[l];
       float* dst = Ws + a.ws_off[l];
       if (in == kGenMaxW && out == kGenMaxW) {
-        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenThreads)
+        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenFT)
           cp_async16(dst + (idx >> 5) * kLdFast + 4 * (idx & 31), W + 4 * idx);
       } else {
-        for (int idx = tid; idx < out * in; idx += kGenThreads) cp_async4(dst + (idx / in) * (in + 1) + idx % in, W + idx);
+        for (int idx = tid; idx < out * in; idx += kGenFT) cp_async4(dst + (idx / in) * (in + 1) + idx % in, W + idx);
       }
       cp_async_commit();
     }
   }
   if (a.gen_noise) {  // the block's kR rows = values [r0 in0, (r0 + kR) in0): whole Philox calls (kR in0 % 4 == 0)
-    for (int cl = tid; cl < kR * in0 / 4; cl += kGenThreads) {
+    for (int cl = tid; cl < kR * in0 / 4; cl += kGenFT) {
       const int64_t call = ((int64_t)r0 * in0) / 4 + cl;
       const uint4 w = philox_call(a.noise_key, (uint32_t)call, a.noise_step, a.noise_rank, kStreamNoise);
       float z[4];
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
       }
     }
   } else {
-    for (int idx = tid; idx < kR * in0; idx += kGenThreads) {
+    for (int idx = tid; idx < kR * in0; idx += kGenFT) {
       const int r = idx / in0, i = idx % in0;
       buf[0][r][i] = (r0 + r < a.k) ? a.noise[(int64_t)(r0 + r) * in0 + i] : 0.f;
     }
@@ -180,16 +185,17 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
     }
     if (a.preload) {
     } else if (fast) {
-      float4 v[16];
+      constexpr int kV = kGenMaxW * kGenMaxW / 4 / kGenFT;
+      float4 v[kV];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
+      for (int u = 0; u < kV; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenFT);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int idx = tid + u * kGenThreads;  // float4 index: row idx / 32, columns 4 (idx % 32) ..
+      for (int u = 0; u < kV; ++u) {
+        const int idx = tid + u * kGenFT;  // float4 index: row idx / 32, columns 4 (idx % 32) ..
         *reinterpret_cast<float4*>(Ws + (idx >> 5) * kLdFast + 4 * (idx & 31)) = v[u];
       }
     } else {
-      for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[(idx / in) * ld + idx % in] = __ldg(W + idx);
+      for (int idx = tid; idx < out * in; idx += kGenFT) Ws[(idx / in) * ld + idx % in] = __ldg(W + idx);
     }
     __syncthreads();
     const float(*src)[kGenMaxW] = buf[l & 1];
@@ -210,20 +216,20 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
     if (fast) {
       const int o = tid & (kGenMaxW - 1), rb = tid >> 7;
       const float* w = Ws + o * kLdFast;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[kRU] = {};
 #pragma unroll 4
       for (int i = 0; i < kGenMaxW; i += 4) {
         const float4 w4 = *reinterpret_cast<const float4*>(w + i);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 2 * u][i]);
+        for (int u = 0; u < kRU; ++u) {
+          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 4 * u][i]);
           acc[u] = fmaf(x.w, w4.w, fmaf(x.z, w4.z, fmaf(x.y, w4.y, fmaf(x.x, w4.x, acc[u]))));
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) finish(rb + 2 * u, o, acc[u]);
+      for (int u = 0; u < kRU; ++u) finish(rb + 4 * u, o, acc[u]);
     } else {
-      for (int idx = tid; idx < kR * out; idx += kGenThreads) {
+      for (int idx = tid; idx < kR * out; idx += kGenFT) {
         const int r = idx / out, o = idx % out;
         const float* w = Ws + o * ld;
         float acc = 0.f;
@@ -239,7 +245,7 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_fwd(const __grid_constant__
 // conflict-free), then each input accumulates over o in order; 128 x 128
 // layers: thread (rb, i) does rows rb, rb + 2, rb + 4, rb + 6 with float4
 // (broadcast) reads of the rows.
-__global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant__ GenArgs a) {
+__global__ void __launch_bounds__(kGenFT) k_gen_dgrad(const __grid_constant__ GenArgs a) {
   extern __shared__ __align__(16) float gsm[];
   float(*buf)[kR][kGenMaxW] = reinterpret_cast<float(*)[kR][kGenMaxW]>(gsm);  // [2][kR][kGenMaxW]
   float* Ws = gsm + 2 * kR * kGenMaxW;                                         // [out][in]
@@ -253,14 +259,14 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
       const float* W = a.W + a.w_off[l];
       float* dst = Ws + a.ws_off_b[l];
       if (in == kGenMaxW && out == kGenMaxW) {
-        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenThreads) cp_async16(dst + 4 * idx, W + 4 * idx);
+        for (int idx = tid; idx < kGenMaxW * kGenMaxW / 4; idx += kGenFT) cp_async16(dst + 4 * idx, W + 4 * idx);
       } else {
-        for (int idx = tid; idx < out * in; idx += kGenThreads) cp_async4(dst + idx, W + idx);
+        for (int idx = tid; idx < out * in; idx += kGenFT) cp_async4(dst + idx, W + idx);
       }
       cp_async_commit();
     }
   }
-  for (int idx = tid; idx < kR * outL; idx += kGenThreads) {
+  for (int idx = tid; idx < kR * outL; idx += kGenFT) {
     const int r = idx / outL, o = idx % outL;
     buf[last & 1][r][o] = (r0 + r < a.k) ? a.dz[last][(int64_t)(r0 + r) * outL + o] : 0.f;
   }
@@ -277,13 +283,14 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
     }
     if (a.preload) {
     } else if (fast) {
-      float4 v[16];
+      constexpr int kV = kGenMaxW * kGenMaxW / 4 / kGenFT;
+      float4 v[kV];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenThreads);
+      for (int u = 0; u < kV; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(W) + tid + u * kGenFT);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) reinterpret_cast<float4*>(Ws)[tid + u * kGenThreads] = v[u];
+      for (int u = 0; u < kV; ++u) reinterpret_cast<float4*>(Ws)[tid + u * kGenFT] = v[u];
     } else {
-      for (int idx = tid; idx < out * in; idx += kGenThreads) Ws[idx] = __ldg(W + idx);
+      for (int idx = tid; idx < out * in; idx += kGenFT) Ws[idx] = __ldg(W + idx);
     }
     __syncthreads();
     const float(*src)[kGenMaxW] = buf[l & 1];
@@ -296,27 +303,27 @@ __global__ void __launch_bounds__(kGenThreads) k_gen_dgrad(const __grid_constant
     };
     if (fast) {
       const int i = tid & (kGenMaxW - 1), rb = tid >> 7;
-      float h[4];
+      float h[kRU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {  // in flight during the sums
-        const int r = rb + 2 * u;
+      for (int u = 0; u < kRU; ++u) {  // in flight during the sums
+        const int r = rb + 4 * u;
         h[u] = (r0 + r < a.k) ? a.act[l - 1][(int64_t)(r0 + r) * in + i] : 0.f;
       }
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[kRU] = {};
 #pragma unroll 4
       for (int o = 0; o < kGenMaxW; o += 4) {
         const float w0 = Ws[o * kGenMaxW + i], w1 = Ws[(o + 1) * kGenMaxW + i];
         const float w2 = Ws[(o + 2) * kGenMaxW + i], w3 = Ws[(o + 3) * kGenMaxW + i];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 2 * u][o]);
+        for (int u = 0; u < kRU; ++u) {
+          const float4 x = *reinterpret_cast<const float4*>(&src[rb + 4 * u][o]);
           acc[u] = fmaf(x.w, w3, fmaf(x.z, w2, fmaf(x.y, w1, fmaf(x.x, w0, acc[u]))));
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) finish(rb + 2 * u, i, acc[u], h[u]);
+      for (int u = 0; u < kRU; ++u) finish(rb + 4 * u, i, acc[u], h[u]);
     } else {
-      for (int idx = tid; idx < kR * in; idx += kGenThreads) {
+      for (int idx = tid; idx < kR * in; idx += kGenFT) {
         const int r = idx / in, i = idx % in;
         float acc = 0.f;
         for (int o = 0; o < out; ++o) acc = fmaf(src[r][o], Ws[o * in + i], acc);
@@ -509,7 +516,7 @@ void launch_gen_fwd(sagips_ctx* c, cudaStream_t st, const void* prefetch, int64_
     launch_normals(c->noise, (int64_t)c->cfg.param_samples * c->cfg.noise_dim, 1.0f, c->cfg.seed, *noise_step,
                    (uint32_t)c->cfg.rank, kStreamNoise, st);
   }
-  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenFT, gen_smem(a), st>>>(a);
   count_launch();
 }
 
@@ -523,7 +530,7 @@ void launch_gen_predict(sagips_ctx* c, const float* noise, int k, float* c_out, 
   a.noise = noise;
   a.k = k;
   a.cbuf = c_out;
-  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
+  k_gen_fwd<<<(a.k + kR - 1) / kR, kGenFT, gen_smem(a), st>>>(a);
   count_launch();
 }
 
@@ -534,7 +541,7 @@ void launch_gen_bwd(sagips_ctx* c, cudaStream_t st) {
     configured = true;
   }
   const GenArgs a = gen_args(c);
-  k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenThreads, gen_smem(a), st>>>(a);
+  k_gen_dgrad<<<(a.k + kR - 1) / kR, kGenFT, gen_smem(a), st>>>(a);
   count_launch();
   const int splits = (a.k + a.split_rows - 1) / a.split_rows;
   k_gen_wgrad<<<dim3(a.tile_base[a.L], splits), kGenThreads, 0, st>>>(a);
